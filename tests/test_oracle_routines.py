@@ -1,0 +1,191 @@
+"""Pins of the oracle's routine simulation: cost-table closed forms,
+SPEC worked examples, special cases (n = 1, rho = 1), routine
+equivalences and fp64 tolerance of the rank-order aggregation (no GPU)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import esp_oracle as O
+from synth.values import gradient
+
+PAIRS = [(k, r) for k in O.KINDS for r in O.ROUTINES
+         if O.legal(O.Cfg(k), r)]
+
+
+def _grads(n, N, dist="D1", step=0):
+    return [gradient(N, rank=r, step=step, dist=dist) for r in range(n)]
+
+
+def test_legal_pairs_table():
+    # UT routines only for uncompressed; CT routines for compressed;
+    # compressed tensors cannot use Allreduce unless allreducible
+    assert O.legal(O.Cfg("none"), "allreduce")
+    assert not O.legal(O.Cfg("none"), "allgather")
+    assert not O.legal(O.Cfg("dgc"), "allreduce")
+    assert O.legal(O.Cfg("randomk", shared_indices=True), "allreduce")
+    assert not O.legal(O.Cfg("randomk", shared_indices=False), "allreduce")
+    assert not O.legal(O.Cfg("efsignsgd"), "reducescatter_allgather")
+    assert len(PAIRS) == 3 + 4 * 3 + 4
+
+
+@pytest.mark.parametrize("kind,routine", PAIRS)
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_bytes_on_wire_closed_forms(kind, routine, n):
+    """Per-rank traffic of each phase, summed along the critical path, equals the
+    cost table's communication volume."""
+    cfg = O.Cfg(kind, 0.01)
+    N = 4133
+    res = O.sync(routine, cfg, _grads(n, N), O.new_states(n, N, routine, cfg))
+    c = res.counters
+    if kind == "none":
+        M = 4 * N
+        if routine == "allreduce":
+            assert c[0].recv == pytest.approx(2 * (n - 1) * M / n, abs=n)
+        elif routine == "reducescatter_allgather":
+            assert c[1].recv == pytest.approx(2 * (n - 1) * M / n, abs=n)  # == Allreduce
+        else:
+            assert c[0].recv + c[1].recv == n * M           # (n-1)M reduce + M broadcast
+        return
+    P = O.nparts_of(routine, n)
+    M = O.chunk_bytes(cfg, N, P) * P
+    row = O.table_row(cfg, routine)
+    if routine == "gather_broadcast":
+        # critical path: root's gather receive + a non-root's broadcast receive
+        got = c[0].phases[0][2] + c[1].phases[-1][2]
+    else:
+        got = c[1].recv
+    # ring chunking rounds M/n down when n does not divide M
+    assert got == pytest.approx(O.table_comm_bytes(row, M, n), rel=0, abs=n)
+    # op counts of the table's compression column on the critical (root) rank
+    assert (c[0].h1, c[0].h2) == O.table_ops(row, n)
+
+
+def test_spec_cost_examples():
+    # S:131-133, S:139-141 (B = 1.25e10 B/s, M = 1e8 B, n = 4)
+    B, M = 1.25e10, 1e8
+    assert O.table_comm_time("allreduce", M, 4, B) == pytest.approx(12e-3)
+    assert O.table_comm_time("allgather", M, 4, B) == pytest.approx(24e-3)
+    assert O.table_comm_time("alltoall_allgather_sparse", M, 4, B) == pytest.approx(30e-3)
+    assert O.table_comm_time("gather_broadcast_quantized", M, 4, B) == pytest.approx(32e-3)
+    assert O.table_comm_time("allreduce", 1e7, 2, 1e9) == pytest.approx(10e-3)
+    for row in ("allreduce", "allgather", "alltoall_allgather_sparse",
+                "alltoall_allgather_quantized", "gather_broadcast_sparse",
+                "gather_broadcast_quantized"):
+        assert O.table_comm_time(row, M, 1, B) == 0
+    one = lambda m: 1e-3
+    # S:147-150 constant curves h1 = h2 = 1 ms, n = 4
+    assert O.table_compression_time("allgather", M, 4, one, one) == pytest.approx(5e-3)
+    assert O.table_compression_time("alltoall_allgather_quantized", M, 4, one, one) == pytest.approx(10e-3)
+    assert O.table_compression_time("allreduce", M, 4, one, one) == pytest.approx(2e-3)
+
+
+def test_allreduce_equals_rs_ag_closed_form():
+    # Allreduce = Reduce-scatter + Allgather, both 2(n-1)M/(nB)
+    for n in (2, 4, 8):
+        M = 2 ** 20
+        rs = (n - 1) * M / n
+        ag = (n - 1) * (M / n)
+        assert rs + ag == pytest.approx(O.table_comm_bytes("allreduce", M, n))
+
+
+@pytest.mark.parametrize("kind,routine", PAIRS)
+def test_n1_is_decompress_of_compress(kind, routine):
+    cfg = O.Cfg(kind, 0.05)
+    g = gradient(1000)
+    res = O.sync(routine, cfg, [g], O.new_states(1, 1000, routine, cfg))
+    if kind == "none":
+        assert np.array_equal(res.outs[0], g)
+        return
+    ch, t = O.compress_segment(cfg, g)
+    assert np.array_equal(res.outs[0], t)
+
+
+@pytest.mark.parametrize("kind", ["dgc", "topk", "randomk"])
+@pytest.mark.parametrize("routine", ["allgather", "alltoall_allgather", "gather_broadcast"])
+def test_rho1_reduces_to_uncompressed_mean(kind, routine):
+    n, N = 4, 777
+    cfg = O.Cfg(kind, 1.0)
+    grads = _grads(n, N)
+    st = O.new_states(n, N, routine, cfg)
+    res = O.sync(routine, cfg, grads, st)
+    ref = O.sync("allreduce", O.Cfg("none"), grads, O.new_states(n, N, "allreduce", O.Cfg("none")))
+    assert np.array_equal(res.outs[0], ref.outs[0])
+    assert all(np.all(s.r == 0) for s in st)
+
+
+@pytest.mark.parametrize("kind", ["dgc", "topk", "randomk", "efsignsgd", "onebit"])
+def test_sparse_gather_broadcast_equals_allgather(kind):
+    n, N = 4, 3000
+    cfg = O.Cfg(kind, 0.02)
+    a = O.sync("allgather", cfg, _grads(n, N), O.new_states(n, N, "allgather", cfg))
+    if kind in O.SPARSE:
+        b = O.sync("gather_broadcast", cfg, _grads(n, N), O.new_states(n, N, "gather_broadcast", cfg))
+        assert np.array_equal(a.outs[0], b.outs[0])
+    for r in range(n):
+        assert np.array_equal(a.outs[r], a.outs[0])
+
+
+def test_aggregation_fp64_tolerance():
+    """rank-order fp32 mean vs exact mean: within 1e-6 * mean|x| + denormal floor."""
+    for n in (2, 4, 8):
+        xs = _grads(n, 10000, dist="D2")
+        got = O.aggregate(xs, "mean", n).astype(np.float64)
+        ref = sum(x.astype(np.float64) for x in xs) / n
+        scale = sum(np.abs(x.astype(np.float64)) for x in xs) / n
+        assert np.all(np.abs(got - ref) <= 1e-6 * scale + 1e-38)
+        s = O.aggregate(xs, "sum", n).astype(np.float64)
+        assert np.all(np.abs(s - ref * n) <= 1e-6 * scale * n + 1e-38)
+
+
+@pytest.mark.parametrize("kind", ["efsignsgd", "onebit"])
+def test_quantized_alltoall_mid_scheme(kind):
+    """Process 2: the output on partition j is the recompression of
+    (mean of decompressed chunks + r2_j); r2 obeys the EF bound."""
+    n, N = 4, 2000
+    cfg = O.Cfg(kind)
+    grads = _grads(n, N)
+    st = O.new_states(n, N, "alltoall_allgather", cfg)
+    res = O.sync("alltoall_allgather", cfg, grads, st)
+    parts = O.partitions(N, n)
+    for j, (lo, hi) in enumerate(parts):
+        seg = res.outs[0][lo:hi]
+        if kind == "efsignsgd":
+            # decoded partition is +-scale2 with a single magnitude
+            assert np.unique(np.abs(seg)).size <= 1
+        else:
+            assert np.unique(seg).size <= 2
+    for r in range(n):
+        assert np.array_equal(res.outs[r], res.outs[0])
+
+
+def test_multistep_ef_telescopes():
+    """sum_t transmitted_t + r_T == sum_t g_t (within fp32 rounding of T adds)."""
+    N, T = 5000, 5
+    for kind in ("dgc", "randomk", "efsignsgd", "onebit"):
+        cfg = O.Cfg(kind, 0.01)
+        st = O.new_states(1, N, "allgather", cfg)
+        sum_t = np.zeros(N)
+        sum_g = np.zeros(N)
+        for t in range(T):
+            g = gradient(N, step=t)
+            res = O.sync("allgather", cfg, [g], st)
+            sum_t += res.outs[0].astype(np.float64)
+            sum_g += g.astype(np.float64)
+        lhs = sum_t + st[0].r.astype(np.float64)
+        tol = T * 2 * np.spacing(np.float32(np.abs(sum_g).max() + np.abs(sum_t).max())).astype(np.float64)
+        assert np.max(np.abs(lhs - sum_g)) <= tol
+
+
+def test_golden_cost_examples():
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cost_examples.json")))
+    for e in g["comm_time_s"]:
+        assert O.table_comm_time(e["row"], e["M"], e["n"], e["B"]) == pytest.approx(e["t"]), e["cite"]
+    one = lambda m: 1e-3
+    for e in g["compression_time_const_1ms"]:
+        assert O.table_compression_time(e["row"], 1e8, e["n"], one, one) == pytest.approx(e["t"]), e["cite"]
+    for e in g["sparse_bytes"]:
+        assert O.chunk_bytes(O.Cfg("dgc", e["ratio"]), e["numel"], 1) == e["bytes"]
+    for e in g["one_bit_word_bytes"]:
+        assert O.chunk_bytes(O.Cfg("efsignsgd"), e["numel"], 1) - 16 == e["bytes"]
