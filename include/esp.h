@@ -1,0 +1,210 @@
+/*
+ * esp.h — C ABI of the B200-native Espresso (arXiv 2205.14465) compressed
+ * gradient-synchronisation hot path.
+ *
+ * What it computes (App. A): for each gradient
+ * tensor of a data-parallel job, h1 = compression fused with its
+ * error-feedback residual update (G5), then the chosen collective
+ * routine ("The collective routines for synchronization"), then
+ * h2 = fused decompression + aggregation of the n (or n^2) received pieces
+ * ("fuses the decompression operations").  The per-tensor option is the
+ * paper's compression option c_j restricted to flat
+ * communication on GPU: a (compressor, ratio, routine) triple.
+ *
+ * Conventions
+ *   - Every call returns esp_status_t; the library never aborts or throws.
+ *     Argument errors are reported synchronously; asynchronous CUDA/NCCL errors
+ *     surface on the next call or via esp_world_check().  esp_last_error()
+ *     returns a thread-local message for the last failure.
+ *   - All device work is enqueued on the caller's stream (cudaStream_t passed as
+ *     void*; NULL = legacy default stream).  The library also uses one internal
+ *     communication stream per world, joined back to the caller's stream with
+ *     events before a call returns.
+ *   - Ownership: the caller owns gradients, user payload buffers and streams;
+ *     the library owns worlds, ctx state (EF residuals) and workspaces.
+ *     Nothing is allocated on the hot path after the first call with a given
+ *     tensor set (plans are cached).
+ *   - Threading: one host thread per world at a time (an NCCL rule).
+ *   - Gradients are contiguous fp32, 16-byte aligned device pointers;
+ *     numel < 2^31 (indices are uint32, reading R18) else ESP_ERR_TOO_LARGE.
+ *   - Sim world: n virtual ranks on one GPU.  Every per-rank buffer argument is
+ *     then n rank-major slices (rank r at offset r * slice) and collectives are
+ *     device-to-device copies among the slices.
+ *
+ * Payload layouts (16-byte aligned sections; a tensor's payload is P equal-size
+ * chunks, one per partition, P = n for Alltoall/Allgather else 1; see
+ * esp_compressed_bytes):
+ *   DGC / TOPK : uint32 idx[k_pad] then float val[k_pad]; idx relative to the
+ *                partition start, ascending; padding idx = 0xFFFFFFFF, val = +0
+ *   RANDOMK    : float val[k_pad] (indices regenerate from the seed, R5)
+ *   EFSIGNSGD  : float scale, 12 pad bytes, uint32 words[w_pad] (bit l of word w
+ *                is element 32w + l, LSB first, 1 <=> p >= 0; tail bits 0)
+ *   ONEBIT     : float mean_neg, float mean_pos, 8 pad bytes, words as above
+ *   NONE       : float values[numel]
+ */
+#ifndef ESP_H_
+#define ESP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+  ESP_OK = 0,
+  ESP_ERR_INVALID_ARG = 1,  /* null pointer, bad enum, misaligned, wrong size */
+  ESP_ERR_UNSUPPORTED = 2,  /* illegal (compressor, routine) pair */
+  ESP_ERR_TOO_LARGE = 3,    /* numel >= 2^31 */
+  ESP_ERR_CUDA = 4,
+  ESP_ERR_NCCL = 5,
+  ESP_ERR_OOM = 6,
+  ESP_ERR_STATE = 7         /* object used with the wrong world / state blob */
+} esp_status_t;
+
+/* Compressors the paper evaluates (Randomk, DGC at 1%, EFSignSGD;
+ * App. D figures: Onebit).  TOPK = DGC's exact result without the sampled
+ * threshold accelerator (reading R3).  NONE = uncompressed fp32. */
+typedef enum {
+  ESP_NONE = 0, ESP_RANDOMK = 1, ESP_DGC = 2, ESP_TOPK = 3, ESP_EFSIGNSGD = 4, ESP_ONEBIT = 5
+} esp_kind_t;
+
+/* Routines of P:1057-1070 (flat communication, root = rank 0, reading R17). */
+typedef enum {
+  ESP_ALLREDUCE = 0,
+  ESP_ALLGATHER = 1,
+  ESP_ALLTOALL_ALLGATHER = 2,     /* sparse: process 1; quantized: process 2 */
+  ESP_GATHER_BROADCAST = 3,       /* sparse: process 1; quantized: process 2 */
+  ESP_REDUCESCATTER_ALLGATHER = 4,
+  ESP_REDUCE_BROADCAST = 5
+} esp_routine_t;
+
+typedef enum { ESP_MEAN = 0, ESP_SUM = 1 } esp_reduce_t;  /* reading R9 */
+
+typedef struct {
+  int32_t kind;                   /* esp_kind_t */
+  int32_t error_feedback;         /* 1: e <- (g+e) - C(g+e) (G5) */
+  double ratio;                   /* rho in (0, 1]; k = min(N, max(1, ceil(rho*N))) (R1) */
+  uint64_t seed;                  /* Randomk hash seed */
+  int32_t randomk_shared_indices; /* 1: same indices on every rank => allreducible (R5) */
+  int32_t reduce;                 /* esp_reduce_t */
+} esp_compressor_cfg_t;
+
+typedef struct esp_world_s* esp_world_t;
+typedef struct esp_ctx_s* esp_ctx_t;
+
+/* Counters of one world (reset by esp_world_reset_counters).  Byte counts are
+ * per rank (per virtual rank 0 in a sim world) and follow the cost-table
+ * conventions of P:52-117: Allgather receives (n-1)M, Alltoall (n-1)M/n, ring
+ * Allreduce 2(n-1)M/n, Gather (n-1)M at the root, Broadcast X at a non-root. */
+enum { ESP_OP_ALLREDUCE = 0, ESP_OP_ALLGATHER, ESP_OP_ALLTOALL, ESP_OP_GATHER,
+       ESP_OP_BROADCAST, ESP_OP_REDUCESCATTER, ESP_OP_REDUCE, ESP_NUM_OPS };
+typedef struct {
+  uint64_t calls[ESP_NUM_OPS];
+  uint64_t sent[ESP_NUM_OPS];
+  uint64_t recv[ESP_NUM_OPS];
+  uint64_t h1_calls;      /* compress applications on the critical rank */
+  uint64_t h2_pieces;     /* decompressed pieces on the critical rank */
+} esp_counters_t;
+
+/* Per-phase device times of the last esp_sync / esp_sync_many (ms, CUDA events;
+ * only when timing is enabled with esp_world_set_timing). */
+typedef struct {
+  float total_ms, h1_ms, comm_ms, mid_ms, h2_ms;
+} esp_timing_t;
+
+/* ---- world ---------------------------------------------------------------
+ * esp_get_nccl_unique_id: writes 128 bytes (ncclUniqueId) to out128 (host).
+ * esp_world_create_nccl: one process per GPU; id128 identical on all ranks;
+ *   creates and owns an ncclComm_t on cuda_dev.
+ * esp_world_create_sim: nranks virtual ranks on cuda_dev (config 1).
+ */
+esp_status_t esp_get_nccl_unique_id(void* out128);
+esp_status_t esp_world_create_nccl(const void* id128, int nranks, int rank, int cuda_dev,
+                                   esp_world_t* out);
+esp_status_t esp_world_create_sim(int nranks, int cuda_dev, esp_world_t* out);
+esp_status_t esp_world_destroy(esp_world_t w);
+esp_status_t esp_world_check(esp_world_t w);   /* async CUDA/NCCL errors */
+esp_status_t esp_world_info(esp_world_t w, int* nranks, int* rank, int* nlocal);
+esp_status_t esp_world_counters(esp_world_t w, esp_counters_t* out);
+/* counters of local rank lr (sim world: virtual rank lr) */
+esp_status_t esp_world_counters_local(esp_world_t w, int lr, esp_counters_t* out);
+esp_status_t esp_world_reset_counters(esp_world_t w);
+esp_status_t esp_world_set_timing(esp_world_t w, int enable);
+esp_status_t esp_last_timing(esp_world_t w, esp_timing_t* out);
+/* Max elements per bucket of esp_sync_many (0 = library default).  Smaller
+ * buckets pipeline h1 / comm / h2 across buckets (a9). */
+esp_status_t esp_world_set_bucket_elems(esp_world_t w, uint64_t elems);
+
+/* ---- ctx: one tensor's option + EF state ----------------------------------
+ * Validates the (compressor, routine) pair: NONE -> {ALLREDUCE,
+ * REDUCESCATTER_ALLGATHER, REDUCE_BROADCAST}; DGC/TOPK/EFSIGNSGD/ONEBIT ->
+ * {ALLGATHER, ALLTOALL_ALLGATHER, GATHER_BROADCAST}; RANDOMK -> those plus
+ * ALLREDUCE when randomk_shared_indices;
+ * anything else -> ESP_ERR_UNSUPPORTED.  Allocates the residual(s) (zeroed)
+ * and the workspace for every local rank of the world.
+ */
+esp_status_t esp_ctx_create(esp_world_t w, const esp_compressor_cfg_t* cfg, int routine,
+                            uint64_t tensor_id, size_t numel, esp_ctx_t* out);
+esp_status_t esp_ctx_destroy(esp_ctx_t c);
+/* Bytes of one rank's first-compression payload (P chunks). */
+esp_status_t esp_ctx_payload_bytes(esp_ctx_t c, size_t* out);
+/* EF state blob (host memory): header {uint64 magic, step, numel, r2_len,
+ * nlocal} then per local rank: float r[numel], float r2[r2_len].  r / r2 are
+ * the TRUE residuals (materialised from the lazy representation).  Pass
+ * host_buf = NULL to query the size.  set_state restores a blob (synchronous). */
+esp_status_t esp_ctx_get_state(esp_ctx_t c, void* host_buf, size_t* nbytes);
+esp_status_t esp_ctx_set_state(esp_ctx_t c, const void* host_buf, size_t nbytes);
+
+/* ---- h1 / h2 ----------------------------------------------------------------
+ * esp_compress: EF-fused compression of one rank's tensor (every local rank in a
+ * sim world).  payload: esp_ctx_payload_bytes bytes per rank, caller-owned.
+ * Advances the ctx step counter (Randomk draws).
+ * esp_decompress: out[numel] = reduce(sum over pieces in order of decompress(
+ * pieces[i])) — rank-order fp32 sum from +0.0f, then / npieces for MEAN.
+ * pieces: npieces device pointers (host array) to full payloads of this ctx.
+ */
+esp_status_t esp_compress(esp_ctx_t c, const float* grad, void* payload, void* stream);
+esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces, float* out,
+                            void* stream);
+
+/* ---- sync ---------------------------------------------------------------------
+ * h1 -> routine -> h2.  grad_inout := the aggregated gradient on every rank.
+ * esp_sync_many runs a per-tensor strategy over a tensor set with bucketing
+ * (one multi-tensor h1 launch, one collective and one h2 launch per bucket).
+ */
+esp_status_t esp_sync(esp_world_t w, esp_ctx_t c, float* grad_inout, void* stream);
+esp_status_t esp_sync_many(esp_world_t w, const esp_ctx_t* ctxs, float* const* grads,
+                           int ntensors, void* stream);
+
+/* ---- sizes / cost table ----------------------------------------------
+ * esp_compressed_bytes: bytes of one rank's payload for numel elements split
+ * into nparts partitions (R10).  esp_wire_bytes: communication volume per rank
+ * of a cost-table row (row: 0 Allreduce, 1 Allgather, 2 Alltoall/Allgather
+ * sparse, 3 Alltoall/Allgather quantized, 4 Gather/Broadcast sparse,
+ * 5 Gather/Broadcast quantized).  esp_model_time: that volume / B seconds.
+ */
+esp_status_t esp_compressed_bytes(const esp_compressor_cfg_t* cfg, size_t numel, int nparts,
+                                  size_t* out);
+esp_status_t esp_wire_bytes(int row, double M, int n, double* out);
+esp_status_t esp_model_time(int row, double M, int n, double B, double* out_seconds);
+
+/* ---- diagnostics --------------------------------------------------------------- */
+const char* esp_status_string(esp_status_t s);
+const char* esp_last_error(void);
+uint64_t esp_launch_count(void);   /* kernels this library launched (process total) */
+const char* esp_version(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESP_H_ */

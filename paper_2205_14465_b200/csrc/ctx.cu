@@ -1,0 +1,306 @@
+// Per-tensor contexts (the paper's per-tensor compression option c_j, P:1133 /
+// P:1169, restricted to flat GPU compression) and the h1 / h2 / sync entry
+// points of the C ABI.
+#include <cmath>
+
+#include "esp_internal.h"
+#include "esp_kernels.h"
+
+using namespace esp;
+
+namespace {
+
+constexpr uint64_t kStateMagic = 0x4553505354415445ull;   // "ESPSTATE"
+
+struct StateHeader {
+  uint64_t magic, step, numel, r2_len, nlocal;
+};
+
+void check_cfg(const esp_compressor_cfg_t* cfg) {
+  ESP_REQUIRE(cfg, ESP_ERR_INVALID_ARG, "cfg is NULL");
+  ESP_REQUIRE(cfg->kind >= ESP_NONE && cfg->kind <= ESP_ONEBIT, ESP_ERR_INVALID_ARG, "bad compressor kind");
+  ESP_REQUIRE(cfg->reduce == ESP_MEAN || cfg->reduce == ESP_SUM, ESP_ERR_INVALID_ARG, "bad reduce mode");
+  if (is_sparse(cfg->kind))
+    ESP_REQUIRE(cfg->ratio > 0.0 && cfg->ratio <= 1.0, ESP_ERR_INVALID_ARG, "ratio must be in (0, 1]");
+}
+
+void check_ptr16(const void* p, const char* what) {
+  ESP_REQUIRE(p, ESP_ERR_INVALID_ARG, std::string(what) + " is NULL");
+  ESP_REQUIRE(((uintptr_t)p & 15) == 0, ESP_ERR_INVALID_ARG, std::string(what) + " is not 16-byte aligned");
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+esp_status_t esp_ctx_create(esp_world_t w, const esp_compressor_cfg_t* cfg, int routine, uint64_t tensor_id,
+                            size_t numel, esp_ctx_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w && out, ESP_ERR_INVALID_ARG, "null argument");
+  check_cfg(cfg);
+  ESP_REQUIRE(routine >= ESP_ALLREDUCE && routine <= ESP_REDUCE_BROADCAST, ESP_ERR_INVALID_ARG, "bad routine");
+  ESP_REQUIRE(numel >= 1, ESP_ERR_INVALID_ARG, "numel must be >= 1");
+  ESP_REQUIRE(numel < (1ull << 31), ESP_ERR_TOO_LARGE, "numel >= 2^31 (uint32 indices, R18)");
+  ESP_REQUIRE(pair_legal(*cfg, routine), ESP_ERR_UNSUPPORTED,
+              "illegal (compressor, routine) pair (P:1064-1065, P:1073)");
+  ESP_CUDA(cudaSetDevice(w->dev));
+  auto c = std::make_unique<esp_ctx_s>();
+  c->w = w;
+  c->cfg = *cfg;
+  c->routine = routine;
+  c->tensor_id = tensor_id;
+  c->N = numel;
+  const int n = w->nranks, nl = w->nlocal;
+  c->P = cfg->kind == ESP_NONE ? 1 : nparts_of(routine, n);
+  const uint64_t L = partition_len(numel, c->P);
+  for (int p = 0; p < c->P; ++p) {
+    uint64_t lo = c->P == 1 ? 0 : std::min<uint64_t>(numel, (uint64_t)p * L);
+    uint64_t hi = c->P == 1 ? numel : std::min<uint64_t>(numel, lo + L);
+    c->plo.push_back((uint32_t)lo);
+    c->phi.push_back((uint32_t)hi);
+    c->pk.push_back(k_of(hi - lo, cfg->ratio));
+  }
+  c->chunk_bytes = chunk_bytes_of(*cfg, numel, c->P, &c->kpad);
+  c->payload_bytes = c->chunk_bytes * c->P;
+  c->hash_base = host_splitmix64(host_splitmix64(cfg->seed) ^ tensor_id);
+  if (cfg->kind != ESP_NONE) {
+    ESP_CUDA(cudaMalloc(&c->r, sizeof(float) * numel * nl));
+    ESP_CUDA(cudaMemset(c->r, 0, sizeof(float) * numel * nl));
+    ESP_CUDA(cudaMalloc(&c->lazy, sizeof(float) * 2 * c->P * nl));
+    ESP_CUDA(cudaMemset(c->lazy, 0, sizeof(float) * 2 * c->P * nl));
+  }
+  if (is_quant(cfg->kind) && (routine == ESP_ALLTOALL_ALLGATHER || routine == ESP_GATHER_BROADCAST)) {
+    c->r2_len = routine == ESP_ALLTOALL_ALLGATHER ? L : numel;
+    ESP_CUDA(cudaMalloc(&c->r2, sizeof(float) * c->r2_len * nl));
+    ESP_CUDA(cudaMemset(c->r2, 0, sizeof(float) * c->r2_len * nl));
+    ESP_CUDA(cudaMalloc(&c->lazy2, sizeof(float) * 2 * nl));
+    ESP_CUDA(cudaMemset(c->lazy2, 0, sizeof(float) * 2 * nl));
+  }
+  w->ctxs.insert(c.get());
+  *out = c.release();
+  ESP_API_END
+}
+
+esp_status_t esp_ctx_destroy(esp_ctx_t c) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(c, ESP_ERR_INVALID_ARG, "ctx is NULL");
+  cudaSetDevice(c->w->dev);
+  drop_plans_with(c->w, c);
+  cudaDeviceSynchronize();
+  cudaFree(c->r);
+  cudaFree(c->lazy);
+  cudaFree(c->r2);
+  cudaFree(c->lazy2);
+  c->w->ctxs.erase(c);
+  delete c;
+  ESP_API_END
+}
+
+esp_status_t esp_ctx_payload_bytes(esp_ctx_t c, size_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(c && out, ESP_ERR_INVALID_ARG, "null argument");
+  *out = c->payload_bytes;
+  ESP_API_END
+}
+
+// valid length of local rank lr's second residual
+static uint64_t r2_valid(esp_ctx_t c, int lr) {
+  if (!c->r2) return 0;
+  const int j = c->w->sim ? lr : c->w->rank;
+  if (c->routine == ESP_ALLTOALL_ALLGATHER) return c->phi[j] - c->plo[j];
+  return j == 0 ? c->N : 0;
+}
+
+esp_status_t esp_ctx_get_state(esp_ctx_t c, void* host_buf, size_t* nbytes) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(c && nbytes, ESP_ERR_INVALID_ARG, "null argument");
+  const int nl = c->w->nlocal;
+  const size_t need = sizeof(StateHeader) + (size_t)nl * 4 * (c->N + c->r2_len);
+  if (!host_buf) {
+    *nbytes = need;
+    return ESP_OK;
+  }
+  ESP_REQUIRE(*nbytes >= need, ESP_ERR_INVALID_ARG, "state buffer too small");
+  ESP_CUDA(cudaSetDevice(c->w->dev));
+  ESP_CUDA(cudaDeviceSynchronize());
+  StateHeader h{kStateMagic, c->step, c->N, c->r2_len, (uint64_t)nl};
+  std::memcpy(host_buf, &h, sizeof(h));
+  float* out = reinterpret_cast<float*>((unsigned char*)host_buf + sizeof(h));
+  float* tmp = nullptr;
+  ESP_CUDA(cudaMalloc(&tmp, sizeof(float) * std::max<uint64_t>(1, std::max(c->N, c->r2_len))));
+  const int kk = c->cfg.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT;
+  for (int lr = 0; lr < nl; ++lr) {
+    float* dst = out + (size_t)lr * (c->N + c->r2_len);
+    if (!c->r) {
+      std::memset(dst, 0, 4 * c->N);
+    } else if (is_quant(c->cfg.kind)) {
+      for (int p = 0; p < c->P; ++p) {
+        const uint32_t lo = c->plo[p], len = c->phi[p] - c->plo[p];
+        launch_sign_materialize(kk, c->r + (size_t)lr * c->N + lo, c->lazy + ((size_t)lr * c->P + p) * 2,
+                                tmp + lo, len, 0);
+      }
+      ESP_CUDA(cudaMemcpy(dst, tmp, 4 * c->N, cudaMemcpyDeviceToHost));
+    } else {
+      ESP_CUDA(cudaMemcpy(dst, c->r + (size_t)lr * c->N, 4 * c->N, cudaMemcpyDeviceToHost));
+    }
+    float* dst2 = dst + c->N;
+    std::memset(dst2, 0, 4 * c->r2_len);
+    const uint64_t v = r2_valid(c, lr);
+    if (v) {
+      launch_sign_materialize(kk, c->r2 + (size_t)lr * c->r2_len, c->lazy2 + (size_t)lr * 2, tmp, (uint32_t)v, 0);
+      ESP_CUDA(cudaMemcpy(dst2, tmp, 4 * v, cudaMemcpyDeviceToHost));
+    }
+  }
+  cudaFree(tmp);
+  *nbytes = need;
+  ESP_API_END
+}
+
+esp_status_t esp_ctx_set_state(esp_ctx_t c, const void* host_buf, size_t nbytes) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(c && host_buf, ESP_ERR_INVALID_ARG, "null argument");
+  StateHeader h;
+  ESP_REQUIRE(nbytes >= sizeof(h), ESP_ERR_INVALID_ARG, "state blob too small");
+  std::memcpy(&h, host_buf, sizeof(h));
+  const int nl = c->w->nlocal;
+  ESP_REQUIRE(h.magic == kStateMagic && h.numel == c->N && h.r2_len == c->r2_len && h.nlocal == (uint64_t)nl,
+              ESP_ERR_STATE, "state blob does not match this ctx");
+  ESP_REQUIRE(nbytes >= sizeof(h) + (size_t)nl * 4 * (c->N + c->r2_len), ESP_ERR_INVALID_ARG, "blob truncated");
+  ESP_CUDA(cudaSetDevice(c->w->dev));
+  ESP_CUDA(cudaDeviceSynchronize());
+  const float* in = reinterpret_cast<const float*>((const unsigned char*)host_buf + sizeof(h));
+  for (int lr = 0; lr < nl; ++lr) {
+    const float* src = in + (size_t)lr * (c->N + c->r2_len);
+    // the true residual with a zero scale pair is its own lazy representation
+    if (c->r) ESP_CUDA(cudaMemcpy(c->r + (size_t)lr * c->N, src, 4 * c->N, cudaMemcpyHostToDevice));
+    if (c->r2) ESP_CUDA(cudaMemcpy(c->r2 + (size_t)lr * c->r2_len, src + c->N, 4 * c->r2_len, cudaMemcpyHostToDevice));
+  }
+  if (c->lazy) ESP_CUDA(cudaMemset(c->lazy, 0, sizeof(float) * 2 * c->P * nl));
+  if (c->lazy2) ESP_CUDA(cudaMemset(c->lazy2, 0, sizeof(float) * 2 * nl));
+  c->step = h.step;
+  ESP_API_END
+}
+
+esp_status_t esp_compress(esp_ctx_t c, const float* grad, void* payload, void* stream) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(c, ESP_ERR_INVALID_ARG, "ctx is NULL");
+  check_ptr16(grad, "grad");
+  check_ptr16(payload, "payload");
+  ESP_REQUIRE(c->cfg.kind != ESP_NONE, ESP_ERR_UNSUPPORTED, "NONE has no compressed payload");
+  ESP_CUDA(cudaSetDevice(c->w->dev));
+  execute_compress(get_plan(c->w, {c}), grad, payload, as_stream(stream));
+  ESP_API_END
+}
+
+esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces, float* out, void* stream) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(c && pieces && npieces >= 1 && npieces <= 64, ESP_ERR_INVALID_ARG, "bad argument");
+  check_ptr16(out, "out");
+  ESP_REQUIRE(c->cfg.kind != ESP_NONE, ESP_ERR_UNSUPPORTED, "NONE has no compressed payload");
+  for (int i = 0; i < npieces; ++i) check_ptr16(pieces[i], "piece");
+  ESP_CUDA(cudaSetDevice(c->w->dev));
+  cudaStream_t st = as_stream(stream);
+  // tables for: one segment per partition, npieces pieces each
+  std::vector<SegH2> segs;
+  std::vector<uint32_t> units;
+  std::vector<const unsigned char*> pp;
+  std::vector<uint32_t> rt;
+  const bool tiles = c->cfg.kind == ESP_DGC || c->cfg.kind == ESP_TOPK;
+  const float divisor = c->cfg.reduce == ESP_MEAN ? (float)npieces : 1.0f;
+  uint32_t u0 = 0;
+  for (int p = 0; p < c->P; ++p) {
+    const uint32_t len = c->phi[p] - c->plo[p];
+    if (!len) continue;
+    SegH2 s{};
+    s.ooff = c->plo[p];
+    s.hash = c->hash_base;
+    s.part = (uint32_t)p;
+    s.n = len;
+    s.k = k_of(len, c->cfg.ratio);
+    s.kpad = c->kpad;
+    s.npieces = (uint32_t)npieces;
+    s.piece0 = (uint32_t)pp.size();
+    s.divisor = divisor;
+    for (int i = 0; i < npieces; ++i) {
+      pp.push_back((const unsigned char*)pieces[i] + (size_t)p * c->chunk_bytes);
+      rt.push_back(c->cfg.randomk_shared_indices ? 0u : (uint32_t)i + 1);
+    }
+    s.nunits = div_up(len, tiles ? kTile : kUnit);
+    s.unit0 = u0;
+    u0 += s.nunits;
+    for (uint32_t i = 0; i < s.nunits; ++i) units.push_back((uint32_t)segs.size());
+    segs.push_back(s);
+  }
+  // device scratch: dyn (out pointer, step of the last compression), tables
+  const size_t b_dyn = 16, b_seg = segs.size() * sizeof(SegH2), b_units = units.size() * 4;
+  const size_t b_pp = pp.size() * 8, b_rt = rt.size() * 4;
+  size_t off_seg = round_up(b_dyn, 256), off_units = round_up(off_seg + b_seg, 256);
+  size_t off_pp = round_up(off_units + b_units, 256), off_rt = round_up(off_pp + b_pp, 256);
+  const size_t total = round_up(off_rt + b_rt, 256);
+  unsigned char* d = nullptr;
+  ESP_CUDA(cudaMallocAsync((void**)&d, total, st));
+  for (auto& s : segs) {
+    s.optr = reinterpret_cast<const uint64_t*>(d);
+    s.step = reinterpret_cast<const uint64_t*>(d + 8);
+  }
+  std::vector<unsigned char> host(total, 0);
+  uint64_t dyn[2] = {(uint64_t)(uintptr_t)out, c->step ? c->step - 1 : 0};
+  std::memcpy(host.data(), dyn, 16);
+  std::memcpy(host.data() + off_seg, segs.data(), b_seg);
+  std::memcpy(host.data() + off_units, units.data(), b_units);
+  std::memcpy(host.data() + off_pp, pp.data(), b_pp);
+  std::memcpy(host.data() + off_rt, rt.data(), b_rt);
+  ESP_CUDA(cudaMemcpyAsync(d, host.data(), total, cudaMemcpyHostToDevice, st));
+  ESP_CUDA(cudaStreamSynchronize(st));   // host staging buffer goes out of scope
+  const SegH2* dseg = reinterpret_cast<const SegH2*>(d + off_seg);
+  const uint32_t* dunits = reinterpret_cast<const uint32_t*>(d + off_units);
+  const unsigned char* const* dpp = reinterpret_cast<const unsigned char* const*>(d + off_pp);
+  const uint32_t* drt = reinterpret_cast<const uint32_t*>(d + off_rt);
+  switch (c->cfg.kind) {
+    case ESP_DGC: case ESP_TOPK: launch_h2_sparse(dseg, dunits, (int)u0, dpp, st); break;
+    case ESP_RANDOMK: launch_h2_randomk(dseg, dunits, (int)u0, dpp, drt, st); break;
+    case ESP_EFSIGNSGD: launch_h2_sign(K_EFSIGN, dseg, dunits, (int)u0, dpp, st); break;
+    default: launch_h2_sign(K_ONEBIT, dseg, dunits, (int)u0, dpp, st); break;
+  }
+  ESP_CUDA(cudaGetLastError());
+  ESP_CUDA(cudaFreeAsync(d, st));
+  ESP_API_END
+}
+
+esp_status_t esp_sync_many(esp_world_t w, const esp_ctx_t* ctxs, float* const* grads, int ntensors,
+                           void* stream) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w && ctxs && grads && ntensors >= 1, ESP_ERR_INVALID_ARG, "bad argument");
+  std::vector<esp_ctx_s*> v(ctxs, ctxs + ntensors);
+  for (int i = 0; i < ntensors; ++i) {
+    ESP_REQUIRE(v[i], ESP_ERR_INVALID_ARG, "ctx is NULL");
+    ESP_REQUIRE(v[i]->w == w, ESP_ERR_STATE, "ctx belongs to another world");
+    check_ptr16(grads[i], "grad");
+    for (int j = 0; j < i; ++j) ESP_REQUIRE(v[j] != v[i], ESP_ERR_INVALID_ARG, "ctx listed twice");
+  }
+  ESP_CUDA(cudaSetDevice(w->dev));
+  Plan* p = get_plan(w, v);
+  execute_plan(p, grads, as_stream(stream));
+  ESP_API_END
+}
+
+esp_status_t esp_sync(esp_world_t w, esp_ctx_t c, float* grad_inout, void* stream) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w && c, ESP_ERR_INVALID_ARG, "null argument");
+  ESP_REQUIRE(c->w == w, ESP_ERR_STATE, "ctx belongs to another world");
+  check_ptr16(grad_inout, "grad");
+  ESP_CUDA(cudaSetDevice(w->dev));
+  execute_plan(get_plan(w, {c}), &grad_inout, as_stream(stream));
+  ESP_API_END
+}
+
+esp_status_t esp_last_timing(esp_world_t w, esp_timing_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w && out, ESP_ERR_INVALID_ARG, "null argument");
+  *out = w->last;
+  ESP_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+// Device helpers shared by the sm_100a kernels of this library.
+// (The CPU oracle under oracle/ shares none of this.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "esp_tables.h"
+
+namespace esp {
+
+__device__ __forceinline__ uint32_t fkey(float x) {
+  // |x| as an order-preserving unsigned key (reading R2)
+  return __float_as_uint(x) & 0x7FFFFFFFu;
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float4 ldg4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+// Streaming (read-once) 128-bit load: do not allocate in L1.
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+
+__device__ __forceinline__ void st4(float* p, float4 v) {
+  *reinterpret_cast<float4*>(p) = v;
+}
+
+__device__ __forceinline__ float f4get(const float4& v, int c) {
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ void f4set(float4& v, int c, float x) {
+  if (c == 0) v.x = x; else if (c == 1) v.y = x; else if (c == 2) v.z = x; else v.w = x;
+}
+
+// Load 4 consecutive floats at element e of an n-element array; out-of-range -> 0.
+__device__ __forceinline__ float4 load4_guard(const float* base, uint32_t e, uint32_t n) {
+  if (e + 3 < n) return ld4(base + e);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (e < n) v.x = base[e];
+  if (e + 1 < n) v.y = base[e + 1];
+  if (e + 2 < n) v.z = base[e + 2];
+  return v;
+}
+__device__ __forceinline__ float4 load4_stream_guard(const float* base, uint32_t e, uint32_t n) {
+  if (e + 3 < n) return ld_stream4(base + e);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (e < n) v.x = base[e];
+  if (e + 1 < n) v.y = base[e + 1];
+  if (e + 2 < n) v.z = base[e + 2];
+  return v;
+}
+__device__ __forceinline__ void store4_guard(float* base, uint32_t e, uint32_t n, float4 v) {
+  if (e + 3 < n) { st4(base + e, v); return; }
+  if (e < n) base[e] = v.x;
+  if (e + 1 < n) base[e + 1] = v.y;
+  if (e + 2 < n) base[e + 2] = v.z;
+}
+
+// ---- CTA-wide scans / reductions for 256 threads ---------------------------------
+// Exclusive scan of v over the CTA in thread order.  `sh` needs 9 uint32.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, uint32_t* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < (kThreads / 32) ? sh[lane] : 0u;
+    uint32_t s = w;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < 8) sh[lane] = s - w;
+    if (lane == 7) sh[8] = s;
+  }
+  __syncthreads();
+  uint32_t r = x - v + sh[warp];
+  *total = sh[8];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ uint32_t block_sum_u32(uint32_t v, uint32_t* sh) {
+  uint32_t t;
+  block_excl_scan(v, &t, sh);
+  return t;
+}
+
+// Deterministic fp64 CTA sum (fixed shuffle tree then warp order).  sh: 8 doubles.
+__device__ __forceinline__ double block_sum_f64(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < kThreads / 32; ++w) t += sh[w];
+    sh[0] = t;
+  }
+  __syncthreads();
+  t = sh[0];
+  __syncthreads();
+  return t;
+}
+
+// "Last CTA of a segment" election: every CTA calls this after its global
+// writes; returns true in exactly one CTA (the last to arrive).
+__device__ __forceinline__ bool last_cta(uint32_t* counter, uint32_t expected, int* sh_flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    uint32_t old = atomicAdd(counter, 1u);
+    *sh_flag = (old == expected - 1);
+  }
+  __syncthreads();
+  bool last = *sh_flag != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+}  // namespace esp

@@ -1,0 +1,38 @@
+// Host-callable launchers of the sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "esp_tables.h"
+
+namespace esp {
+
+void count_launches(int n);   // process-wide counter behind esp_launch_count()
+
+// DGC / TOPK h1 (k_dgc.cu)
+void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
+                   const uint32_t* group_seg, int ngroups, cudaStream_t st);
+// Randomk h1 (k_randomk.cu)
+void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
+// EFSignSGD / Onebit h1; with pieces != nullptr the input is the decode-mean of
+// npieces received chunks (mid-scheme a7, P:78-87 / P:105-115)  (k_sign.cu)
+void launch_sign_h1(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits,
+                    const unsigned char* const* pieces, cudaStream_t st);
+// NONE: pack gradients into a contiguous buffer (k_h2.cu)
+void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
+
+// h2 (k_h2.cu)
+void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles,
+                      const unsigned char* const* pieces, cudaStream_t st);
+void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
+                    const unsigned char* const* pieces, cudaStream_t st);
+void launch_h2_randomk(const SegH2* segs, const uint32_t* unit_seg, int nunits,
+                       const unsigned char* const* pieces, const uint32_t* rankterms, cudaStream_t st);
+void launch_h2_dense(const SegH2* segs, const uint32_t* unit_seg, int nunits,
+                     const unsigned char* const* pieces, cudaStream_t st);
+
+// state export of the lazy sign EF: r_true = p - delta(p)  (k_sign.cu)
+void launch_sign_materialize(int kind, const float* p, const float* lazy, float* out, uint32_t n,
+                             cudaStream_t st);
+
+}  // namespace esp

@@ -1,0 +1,99 @@
+// Device-side work tables shared by the planner (host) and the kernels.
+// Every multi-tensor kernel walks one of these tables, so one launch covers a
+// whole bucket of tensors (SURVEY.md 7 "hard part 2": many tiny tensors).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace esp {
+
+// Work granularity (elements).  A CTA of 256 threads streams one UNIT; each
+// warp owns one RUN of 1024 consecutive elements (8 x float4 per lane).
+constexpr int kThreads = 256;
+constexpr int kRun = 1024;
+constexpr int kUnit = 8192;              // 8 runs per CTA
+constexpr int kRunsPerGroup = 16;        // DGC finalize: 16 runs per CTA
+constexpr int kSample = 8192;            // DGC sampled-threshold sample size
+constexpr int kTile = 8192;              // sparse h2 output tile (32 KB smem)
+
+enum Kind : int { K_NONE = 0, K_RANDOMK = 1, K_DGC = 2, K_TOPK = 3, K_EFSIGN = 4, K_ONEBIT = 5 };
+
+// Per-segment selection state of the DGC/top-k pipeline (one per segment).
+struct SelState {
+  uint32_t thr;        // sampled threshold key (candidates: key >= thr)
+  uint32_t count;      // candidates found by the streaming pass
+  uint32_t done;       // last-CTA counter of the streaming pass
+  uint32_t fallback;   // 1: count < k, re-run compaction with thr = 0
+  uint32_t count_fb, done_fb;
+  uint32_t prefix;     // radix-select prefix of the k-th key
+  uint32_t above;      // # candidates with key above the current prefix bin
+  uint32_t need;       // k - above
+  uint32_t done_r2, done_r3, done_cnt;
+  uint32_t total_sel;  // debug: number selected (== k)
+  uint32_t pad[3];
+};
+
+// One h1 segment = (local rank, tensor, partition).
+// Per-call dynamic arguments (gradient pointers and step counters of the
+// tensors of a plan) live in a small device array `dyn` that is refreshed with
+// one async H2D copy per call, so the static tables below never change.
+struct SegH1 {
+  const uint64_t* gptr;  // &dyn[slot]: device pointer of this tensor's gradient
+  uint64_t goff;         // element offset of the segment (local rank and partition)
+  const uint64_t* step;  // &dyn[nslots + slot]: step counter (Randomk draws)
+  float* r;              // EF state: residual (sparse) / previous p (sign, lazy EF)
+  unsigned char* chunk;  // output chunk
+  const float* lazy_in;  // sign: {scale} / onebit: {mneg, mpos} of the previous step
+  float* lazy_out;       // written by the last CTA of the segment
+  uint32_t n;            // segment length (elements)
+  uint32_t k;            // selected count (sparse) / unused
+  uint32_t kpad;         // chunk capacity in entries (sparse) or words (sign)
+  uint32_t unit0;        // first unit (CTA) of this segment in the unit table
+  uint32_t nunits;
+  uint32_t group0;       // DGC: first finalize group
+  uint32_t ngroups;
+  uint32_t ef;           // error feedback on/off
+  uint64_t hash;         // Randomk: splitmix chain over (seed, tensor); DGC: sample hash
+  uint32_t part;         // partition index (Randomk hash chain)
+  uint32_t rankterm;     // 0 when indices are shared, rank + 1 otherwise (R5)
+  double ratio;
+  // DGC / sign workspace
+  uint2* cand;           // candidates, run-major: [run * kRun + i] = {idx, bits(acc)}
+  uint32_t* runcnt;      // candidates per run
+  uint32_t* hist;        // 2048 (pass) + 2048 (fallback) + 1024 + 1024
+  SelState* st;
+  uint32_t* gcnt;        // 4 * ngroups: above, tie, tie_off, sel_off
+  double* partial;       // sign: 2 doubles per unit
+  uint32_t* pcount;      // sign: 2 counts per unit (onebit) ; [0] of seg = done counter
+  // a7 (mid-scheme) input: decode-mean of npieces chunks instead of g
+  uint32_t npieces;
+  uint32_t piece0;       // index into the piece-pointer array
+  float divisor;
+  uint32_t pad_;
+};
+
+// One h2 segment: out[0..n) = reduce(sum_r decode(piece r)).
+struct SegH2 {
+  const uint64_t* optr;  // &dyn[slot]: output tensor (the gradient, in place)
+  uint64_t ooff;         // element offset of the segment
+  const uint64_t* step;  // Randomk: step counter
+  uint64_t hash;         // Randomk: splitmix chain over (seed, tensor)
+  uint32_t part;         // Randomk: partition index
+  uint32_t n;
+  uint32_t k;            // randomk: k of the segment
+  uint32_t kpad;         // entries (sparse) / words (sign) per chunk
+  uint32_t npieces;
+  uint32_t piece0;       // index into piece pointers (and randomk hash array)
+  uint32_t unit0;        // first unit/tile
+  uint32_t nunits;
+  float divisor;         // n for MEAN, 1 for SUM or already-averaged data
+};
+
+__device__ __forceinline__ const float* seg_g(const SegH1& s) {
+  return reinterpret_cast<const float*>(*s.gptr) + s.goff;
+}
+__device__ __forceinline__ float* seg_out(const SegH2& s) {
+  return reinterpret_cast<float*>(*s.optr) + s.ooff;
+}
+
+}  // namespace esp

@@ -1,0 +1,200 @@
+// h2 on sm_100a: fused decompression + aggregation of the n (Allgather) or
+// n^2 (Alltoall/Allgather) received pieces, written once into the gradient
+// ("fuses the decompression operations"; n h2(M) and n^2 h2(M/n) of the
+// cost table).
+//
+// Aggregation rule (reading R9): fp32 sum over pieces in rank order starting
+// from +0.0f, then IEEE division by the divisor (n for MEAN).  Adding an
+// implicit +0 for an absent sparse entry is the identity on a sum that started
+// at +0.0f, so the sparse kernel only touches present entries.
+#include "esp_device.cuh"
+#include "esp_kernels.h"
+
+namespace esp {
+
+constexpr int kMaxPieces = 64;
+
+// first position p in [0, len) with a[p] >= x (len if none); warp-cooperative
+// 32-ary search: ~log32(len) dependent loads instead of log2(len).
+__device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* a, uint32_t len, uint32_t x) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = len;   // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const uint32_t span = hi - lo;
+    const uint32_t p = lo + (uint32_t)(((uint64_t)(lane + 1) * span) / 33);
+    const uint32_t v = __ldg(a + p);
+    const uint32_t b = __ballot_sync(0xffffffffu, v >= x);
+    if (b) {
+      const int f = __ffs(b) - 1;
+      const uint32_t pf = __shfl_sync(0xffffffffu, p, f);
+      const uint32_t pprev = __shfl_sync(0xffffffffu, p, f > 0 ? f - 1 : 0);
+      hi = pf;
+      if (f > 0) lo = pprev + 1;
+    } else {
+      lo = __shfl_sync(0xffffffffu, p, 31) + 1;
+    }
+  }
+  const uint32_t p = lo + lane;
+  const uint32_t v = p < hi ? __ldg(a + p) : 0xFFFFFFFFu;
+  const uint32_t b = __ballot_sync(0xffffffffu, p < hi && v >= x);
+  return b ? lo + (uint32_t)(__ffs(b) - 1) : hi;
+}
+
+__global__ void __launch_bounds__(kThreads) h2_sparse_kernel(const SegH2* __restrict__ segs,
+                                                             const uint32_t* __restrict__ tile_seg,
+                                                             const unsigned char* const* __restrict__ pieces) {
+  __shared__ __align__(16) float acc[kTile];
+  __shared__ uint32_t rlo[kMaxPieces], rhi[kMaxPieces];
+  const uint32_t sid = tile_seg[blockIdx.x];
+  const SegH2 S = segs[sid];
+  const uint32_t t = blockIdx.x - S.unit0;
+  const uint32_t lo = t * kTile;
+  const uint32_t hi = min(lo + (uint32_t)kTile, S.n);
+  for (int i = threadIdx.x; i < kTile / 4; i += kThreads)
+    reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t r = warp; r < S.npieces; r += kThreads / 32) {
+    const uint32_t* idx = reinterpret_cast<const uint32_t*>(pieces[S.piece0 + r]);
+    const uint32_t a = warp_lower_bound(idx, S.kpad, lo);
+    const uint32_t b = warp_lower_bound(idx, S.kpad, hi);
+    if (lane == 0) { rlo[r] = a; rhi[r] = b; }
+  }
+  __syncthreads();
+  for (uint32_t r = 0; r < S.npieces; ++r) {
+    const unsigned char* pc = pieces[S.piece0 + r];
+    const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
+    const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
+    for (uint32_t i = rlo[r] + threadIdx.x; i < rhi[r]; i += kThreads) {
+      const uint32_t e = __ldg(idx + i) - lo;
+      acc[e] = __fadd_rn(acc[e], __ldg(val + i));   // distinct indices within a piece
+    }
+    __syncthreads();
+  }
+  const float d = S.divisor;
+  for (uint32_t i = threadIdx.x * 4; lo + i < hi; i += kThreads * 4) {
+    float4 v = *reinterpret_cast<const float4*>(acc + i);
+    if (d != 1.0f) {
+      v.x = __fdiv_rn(v.x, d);
+      v.y = __fdiv_rn(v.y, d);
+      v.z = __fdiv_rn(v.z, d);
+      v.w = __fdiv_rn(v.w, d);
+    }
+    store4_guard(seg_out(S), lo + i, S.n, v);
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restrict__ segs,
+                                                           const uint32_t* __restrict__ unit_seg,
+                                                           const unsigned char* const* __restrict__ pieces) {
+  __shared__ float sh_sp[kMaxPieces], sh_sn[kMaxPieces];
+  __shared__ const uint32_t* sh_w[kMaxPieces];
+  const uint32_t sid = unit_seg[blockIdx.x];
+  const SegH2 S = segs[sid];
+  const uint32_t u = blockIdx.x - S.unit0;
+  const uint32_t n = S.n;
+  for (uint32_t r = threadIdx.x; r < S.npieces; r += kThreads) {
+    const unsigned char* h = pieces[S.piece0 + r];
+    const float* f = reinterpret_cast<const float*>(h);
+    if (KIND == K_EFSIGN) { sh_sp[r] = f[0]; sh_sn[r] = -f[0]; }
+    else { sh_sn[r] = f[0]; sh_sp[r] = f[1]; }
+    sh_w[r] = reinterpret_cast<const uint32_t*>(h + 16);
+  }
+  __syncthreads();
+  const float d = S.divisor;
+#pragma unroll 2
+  for (int j = 0; j < kUnit / (kThreads * 4); ++j) {
+    const uint32_t e = u * kUnit + (j * kThreads + threadIdx.x) * 4;
+    if (e >= n) break;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t r = 0; r < S.npieces; ++r) {
+      const uint32_t nib = (__ldg(sh_w[r] + (e >> 5)) >> (e & 31)) & 0xFu;
+      const float sp = sh_sp[r], sn = sh_sn[r];
+      acc.x = __fadd_rn(acc.x, (nib & 1) ? sp : sn);
+      acc.y = __fadd_rn(acc.y, (nib & 2) ? sp : sn);
+      acc.z = __fadd_rn(acc.z, (nib & 4) ? sp : sn);
+      acc.w = __fadd_rn(acc.w, (nib & 8) ? sp : sn);
+    }
+    if (d != 1.0f) {
+      acc.x = __fdiv_rn(acc.x, d);
+      acc.y = __fdiv_rn(acc.y, d);
+      acc.z = __fdiv_rn(acc.z, d);
+      acc.w = __fdiv_rn(acc.w, d);
+    }
+    store4_guard(seg_out(S), e, n, acc);
+  }
+}
+
+// NONE: out = reduce(sum_r dense piece r).  Used for the sim world's
+// uncompressed routines and to unpack an NCCL-reduced bucket (1 piece).
+__global__ void __launch_bounds__(kThreads) h2_dense_kernel(const SegH2* __restrict__ segs,
+                                                            const uint32_t* __restrict__ unit_seg,
+                                                            const unsigned char* const* __restrict__ pieces) {
+  const uint32_t sid = unit_seg[blockIdx.x];
+  const SegH2 S = segs[sid];
+  const uint32_t u = blockIdx.x - S.unit0;
+  const uint32_t n = S.n;
+  const float d = S.divisor;
+  for (int j = 0; j < kUnit / (kThreads * 4); ++j) {
+    const uint32_t e = u * kUnit + (j * kThreads + threadIdx.x) * 4;
+    if (e >= n) break;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t r = 0; r < S.npieces; ++r) {
+      const float4 v = load4_guard(reinterpret_cast<const float*>(pieces[S.piece0 + r]), e, n);
+      acc.x = __fadd_rn(acc.x, v.x);
+      acc.y = __fadd_rn(acc.y, v.y);
+      acc.z = __fadd_rn(acc.z, v.z);
+      acc.w = __fadd_rn(acc.w, v.w);
+    }
+    if (d != 1.0f) {
+      acc.x = __fdiv_rn(acc.x, d);
+      acc.y = __fdiv_rn(acc.y, d);
+      acc.z = __fdiv_rn(acc.z, d);
+      acc.w = __fdiv_rn(acc.w, d);
+    }
+    store4_guard(seg_out(S), e, n, acc);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) pack_kernel(const SegH1* __restrict__ segs,
+                                                        const uint32_t* __restrict__ unit_seg) {
+  const uint32_t sid = unit_seg[blockIdx.x];
+  const SegH1 S = segs[sid];
+  const uint32_t u = blockIdx.x - S.unit0;
+  float* dst = reinterpret_cast<float*>(S.chunk);
+  for (int j = 0; j < kUnit / (kThreads * 4); ++j) {
+    const uint32_t e = u * kUnit + (j * kThreads + threadIdx.x) * 4;
+    if (e >= S.n) break;
+    store4_guard(dst, e, S.n, load4_stream_guard(seg_g(S), e, S.n));
+  }
+}
+
+void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles,
+                      const unsigned char* const* pieces, cudaStream_t st) {
+  if (ntiles == 0) return;
+  h2_sparse_kernel<<<ntiles, kThreads, 0, st>>>(segs, tile_seg, pieces);
+  count_launches(1);
+}
+
+void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
+                    const unsigned char* const* pieces, cudaStream_t st) {
+  if (nunits == 0) return;
+  if (kind == K_EFSIGN) h2_sign_kernel<K_EFSIGN><<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
+  else h2_sign_kernel<K_ONEBIT><<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
+  count_launches(1);
+}
+
+void launch_h2_dense(const SegH2* segs, const uint32_t* unit_seg, int nunits,
+                     const unsigned char* const* pieces, cudaStream_t st) {
+  if (nunits == 0) return;
+  h2_dense_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
+  count_launches(1);
+}
+
+void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st) {
+  if (nunits == 0) return;
+  pack_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg);
+  count_launches(1);
+}
+
+}  // namespace esp

@@ -1,0 +1,687 @@
+// Execution plans: bucketing of a tensor set by (compressor, routine), the
+// device work tables of every kernel, the buffers of every collective phase,
+// and the pipelined executor ("Multiple CUDA
+// streams are used to overlap the computation, communication, and
+// compression").  A plan is built once per tensor list and cached on the world;
+// a call then costs one 16-byte-per-tensor async H2D copy of the gradient
+// pointers and step counters plus the kernel/collective launches.
+#include <algorithm>
+#include <cmath>
+
+#include "esp_internal.h"
+#include "esp_kernels.h"
+
+namespace esp {
+
+struct Bucket {
+  int kind = 0, routine = 0, reduce = 0;
+  std::vector<int> tens;      // indices into Plan::ctxs
+  int P = 1;
+  size_t slot = 0;            // bytes of one slot = sum of the tensors' chunks
+  std::vector<size_t> coff;   // chunk offset of each tensor within a slot
+  size_t none_count = 0;      // NONE: floats in the packed slot (padded to n)
+  uint64_t none_bytes = 0;    // NONE: logical bytes (sum of 4 N_t) for the counters
+  LocalBufs send{}, recv1{}, recv2{}, mid{};
+  // tables (device) and sizes
+  SegH1* h1 = nullptr; int nh1 = 0;
+  uint32_t* h1_units = nullptr; int nh1_units = 0;
+  uint32_t* h1_groups = nullptr; int nh1_groups = 0;
+  SegH1* a7 = nullptr; int na7 = 0;
+  uint32_t* a7_units = nullptr; int na7_units = 0;
+  const unsigned char** a7_pieces = nullptr;
+  SegH2* h2 = nullptr; int nh2 = 0;
+  uint32_t* h2_units = nullptr; int nh2_units = 0;
+  const unsigned char** h2_pieces = nullptr;
+  uint32_t* h2_rankterms = nullptr;
+  cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr;
+  uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
+};
+
+struct Plan {
+  esp_world_s* w = nullptr;
+  std::vector<esp_ctx_s*> ctxs;
+  std::vector<Bucket> buckets;
+  Arena arena;
+  unsigned char* zero = nullptr;
+  size_t zero_bytes = 0;
+  uint64_t* dyn_dev = nullptr;
+  uint64_t* dyn_host = nullptr;
+  cudaEvent_t dyn_ev = nullptr;
+  bool dyn_pending = false;
+  ~Plan() {
+    for (auto& b : buckets) {
+      if (b.ev_h1) cudaEventDestroy(b.ev_h1);
+      if (b.ev_comm) cudaEventDestroy(b.ev_comm);
+    }
+    if (dyn_ev) cudaEventDestroy(dyn_ev);
+    if (dyn_host) cudaFreeHost(dyn_host);
+  }
+};
+
+static int grank(esp_world_s* w, int lr) { return w->sim ? lr : w->rank; }
+
+// ------------------------------------------------------------------ layout
+// Two passes over the same code: the first reserves arena offsets to size the
+// single cudaMalloc, the second fills host tables with real pointers.
+struct Layout {
+  Plan& p;
+  bool commit;
+  size_t reserve(size_t bytes) { return p.arena.reserve(bytes); }
+  template <class T>
+  T* ptr(size_t off) { return commit ? reinterpret_cast<T*>(p.arena.base + off) : nullptr; }
+};
+
+struct HostTables {
+  std::vector<SegH1> h1, a7;
+  std::vector<uint32_t> h1_units, h1_groups, a7_units, h2_units;
+  std::vector<SegH2> h2;
+  std::vector<const unsigned char*> a7_pieces, h2_pieces;
+  std::vector<uint32_t> rankterms;
+};
+
+static void fill_unit_table(std::vector<uint32_t>& units, uint32_t seg, uint32_t count) {
+  for (uint32_t i = 0; i < count; ++i) units.push_back(seg);
+}
+
+static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st, size_t& st_cursor,
+                         size_t& hist_cursor) {
+  Plan& p = L.p;
+  esp_world_s* w = p.w;
+  const int n = w->nranks, nl = w->nlocal;
+  const bool none = b.kind == ESP_NONE;
+  const bool sparse = is_sparse(b.kind);
+  const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
+  const bool quant = is_quant(b.kind);
+  const float divisor = b.reduce == ESP_MEAN ? (float)n : 1.0f;
+  const int nslots = (int)p.ctxs.size();
+
+  // ---- slot layout
+  b.coff.clear();
+  b.slot = 0;
+  if (none) {
+    for (int t : b.tens) {
+      b.coff.push_back(b.slot);
+      b.slot += round_up(4 * p.ctxs[t]->N, 16);
+    }
+    b.none_bytes = 0;
+    for (int t : b.tens) b.none_bytes += 4 * p.ctxs[t]->N;
+    b.none_count = round_up(b.slot / 4, (size_t)n * 4);
+    b.slot = b.none_count * 4;
+  } else {
+    for (int t : b.tens) {
+      b.coff.push_back(b.slot);
+      b.slot += round_up(p.ctxs[t]->chunk_bytes, 16);
+    }
+  }
+  b.P = none ? 1 : p.ctxs[b.tens[0]]->P;
+  const size_t S = b.slot;
+
+  // ---- buffers (per local rank)
+  auto bufs = [&](LocalBufs& lb, size_t per_rank) {
+    size_t stride = round_up(per_rank, 256);
+    size_t off = L.reserve(stride * nl);
+    lb = LocalBufs{L.ptr<unsigned char>(off), stride};
+  };
+  bufs(b.send, b.P * S);
+  switch (b.routine) {
+    case ESP_ALLGATHER: bufs(b.recv1, n * S); break;
+    case ESP_ALLTOALL_ALLGATHER:
+      bufs(b.recv1, n * S);
+      if (sparse) bufs(b.recv2, (size_t)n * n * S);
+      else { bufs(b.mid, S); bufs(b.recv2, n * S); }
+      break;
+    case ESP_GATHER_BROADCAST:
+      bufs(b.recv1, n * S);
+      if (quant) bufs(b.mid, S);
+      break;
+    default:   // ALLREDUCE (randomk / none), RS/AG, Reduce/Broadcast
+      if (!w->sim) bufs(b.recv1, S);
+      break;
+  }
+
+  // ---- h1 segments
+  const uint32_t h1_first = (uint32_t)T.h1.size();
+  uint32_t unit_cursor = (uint32_t)T.h1_units.size();
+  uint32_t group_cursor = (uint32_t)T.h1_groups.size();
+  for (int lr = 0; lr < nl; ++lr) {
+    for (size_t ti = 0; ti < b.tens.size(); ++ti) {
+      esp_ctx_s* c = p.ctxs[b.tens[ti]];
+      const int slot_idx = b.tens[ti];
+      for (int part = 0; part < (none ? 1 : c->P); ++part) {
+        const uint32_t lo = none ? 0 : c->plo[part], hi = none ? (uint32_t)c->N : c->phi[part];
+        const uint32_t len = hi - lo;
+        if (len == 0) continue;
+        SegH1 s{};
+        s.gptr = p.dyn_dev + slot_idx;
+        s.goff = (uint64_t)lr * c->N + lo;
+        s.step = p.dyn_dev + nslots + slot_idx;
+        s.r = c->r ? c->r + (size_t)lr * c->N + lo : nullptr;
+        s.chunk = b.send.base ? b.send.at(lr) + (size_t)part * S + b.coff[ti] : nullptr;
+        s.lazy_in = c->lazy ? c->lazy + ((size_t)lr * c->P + part) * 2 : nullptr;
+        s.lazy_out = const_cast<float*>(s.lazy_in);
+        s.n = len;
+        s.k = none ? 0 : c->pk[part];
+        s.kpad = c->kpad;
+        const uint32_t nunits = div_up(len, kUnit);
+        s.unit0 = unit_cursor;
+        s.nunits = nunits;
+        const uint32_t nruns = div_up(len, kRun);
+        s.ngroups = div_up(nruns, kRunsPerGroup);
+        s.group0 = group_cursor;
+        s.ef = c->cfg.error_feedback ? 1 : 0;
+        s.hash = b.kind == ESP_RANDOMK ? c->hash_base
+                                       : host_splitmix64(c->tensor_id * 0x100000001b3ull + part);
+        s.part = (uint32_t)part;
+        s.rankterm = (b.kind == ESP_RANDOMK && !c->cfg.randomk_shared_indices) ? grank(w, lr) + 1 : 0;
+        s.ratio = c->cfg.ratio;
+        // per-segment state (zeroed every call)
+        size_t st_off = zero_off_st + st_cursor * sizeof(SelState);
+        ++st_cursor;
+        s.st = L.ptr<SelState>(st_off);
+        if (dgc) {
+          s.cand = L.ptr<uint2>(L.reserve((size_t)nruns * kRun * sizeof(uint2)));
+          s.runcnt = L.ptr<uint32_t>(L.reserve((size_t)nruns * 4));
+          s.gcnt = L.ptr<uint32_t>(L.reserve((size_t)s.ngroups * 16));
+          s.hist = L.commit ? reinterpret_cast<uint32_t*>(p.zero + hist_cursor) : nullptr;
+          hist_cursor += 6144 * 4;
+        }
+        if (quant) {
+          s.partial = L.ptr<double>(L.reserve((size_t)nunits * 16));
+          s.pcount = L.ptr<uint32_t>(L.reserve((size_t)nunits * 8));
+        }
+        if (none) s.chunk = b.send.base ? b.send.at(lr) + b.coff[ti] : nullptr;
+        T.h1.push_back(s);
+        unit_cursor += nunits;
+        if (dgc) group_cursor += s.ngroups;
+        fill_unit_table(T.h1_units, (uint32_t)(T.h1.size() - 1 - h1_first), nunits);
+        if (dgc) fill_unit_table(T.h1_groups, (uint32_t)(T.h1.size() - 1 - h1_first), s.ngroups);
+      }
+    }
+  }
+  b.nh1 = (int)(T.h1.size() - h1_first);
+  // unit/group tables refer to segment indices local to the bucket; the
+  // unit0/group0 fields are relative to the bucket's own unit table
+  {
+    uint32_t u0 = 0, g0 = 0;
+    for (int i = 0; i < b.nh1; ++i) {
+      SegH1& s = T.h1[h1_first + i];
+      s.unit0 = u0;
+      u0 += s.nunits;
+      s.group0 = g0;
+      if (dgc) g0 += s.ngroups;
+    }
+    b.nh1_units = (int)u0;
+    b.nh1_groups = dgc ? (int)g0 : 0;
+  }
+
+  // ---- a7 segments (quantized mid-scheme)
+  const uint32_t a7_first = (uint32_t)T.a7.size();
+  if (quant && (b.routine == ESP_ALLTOALL_ALLGATHER || b.routine == ESP_GATHER_BROADCAST)) {
+    uint32_t u0 = 0;
+    for (int lr = 0; lr < nl; ++lr) {
+      const int j = grank(w, lr);
+      if (b.routine == ESP_GATHER_BROADCAST && j != 0) continue;
+      for (size_t ti = 0; ti < b.tens.size(); ++ti) {
+        esp_ctx_s* c = p.ctxs[b.tens[ti]];
+        uint32_t lo, hi;
+        if (b.routine == ESP_ALLTOALL_ALLGATHER) { lo = c->plo[j]; hi = c->phi[j]; }
+        else { lo = 0; hi = (uint32_t)c->N; }
+        const uint32_t len = hi - lo;
+        if (len == 0) continue;
+        SegH1 s{};
+        s.r = c->r2 ? c->r2 + (size_t)lr * c->r2_len : nullptr;
+        s.lazy_in = c->lazy2 ? c->lazy2 + (size_t)lr * 2 : nullptr;
+        s.lazy_out = const_cast<float*>(s.lazy_in);
+        s.chunk = b.mid.base ? b.mid.at(lr) + b.coff[ti] : nullptr;
+        s.n = len;
+        s.kpad = c->kpad;
+        s.nunits = div_up(len, kUnit);
+        s.unit0 = u0;
+        u0 += s.nunits;
+        s.ef = c->cfg.error_feedback ? 1 : 0;
+        s.npieces = (uint32_t)n;
+        s.piece0 = (uint32_t)T.a7_pieces.size();
+        s.divisor = divisor;
+        for (int r = 0; r < n; ++r)
+          T.a7_pieces.push_back(b.recv1.base ? b.recv1.at(lr) + (size_t)r * S + b.coff[ti] : nullptr);
+        s.st = L.ptr<SelState>(zero_off_st + st_cursor * sizeof(SelState));
+        ++st_cursor;
+        s.partial = L.ptr<double>(L.reserve((size_t)s.nunits * 16));
+        s.pcount = L.ptr<uint32_t>(L.reserve((size_t)s.nunits * 8));
+        T.a7.push_back(s);
+        fill_unit_table(T.a7_units, (uint32_t)(T.a7.size() - 1 - a7_first), s.nunits);
+      }
+    }
+    b.na7 = (int)(T.a7.size() - a7_first);
+    b.na7_units = (int)u0;
+  }
+
+  // ---- h2 segments
+  const uint32_t h2_first = (uint32_t)T.h2.size();
+  uint32_t u0 = 0;
+  const bool tiles = dgc;
+  for (int lr = 0; lr < nl; ++lr) {
+    for (size_t ti = 0; ti < b.tens.size(); ++ti) {
+      esp_ctx_s* c = p.ctxs[b.tens[ti]];
+      const int slot_idx = b.tens[ti];
+      const int nparts_out = (b.routine == ESP_ALLTOALL_ALLGATHER) ? c->P : 1;
+      for (int part = 0; part < nparts_out; ++part) {
+        const uint32_t lo = nparts_out > 1 ? c->plo[part] : 0;
+        const uint32_t hi = nparts_out > 1 ? c->phi[part] : (uint32_t)c->N;
+        const uint32_t len = hi - lo;
+        if (len == 0) continue;
+        SegH2 s{};
+        s.optr = p.dyn_dev + slot_idx;
+        s.ooff = (uint64_t)lr * c->N + lo;
+        s.step = p.dyn_dev + nslots + slot_idx;
+        s.hash = c->hash_base;
+        s.part = (uint32_t)part;
+        s.n = len;
+        s.k = none ? 0 : k_of(len, c->cfg.ratio);
+        s.kpad = c->kpad;
+        s.piece0 = (uint32_t)T.h2_pieces.size();
+        auto add_piece = [&](unsigned char* base, size_t off, uint32_t rankterm) {
+          T.h2_pieces.push_back(base ? base + off : nullptr);
+          T.rankterms.push_back(rankterm);
+        };
+        const uint32_t rt_shared = 0;
+        auto rt_of = [&](int r) -> uint32_t {
+          return (b.kind == ESP_RANDOMK && !c->cfg.randomk_shared_indices) ? (uint32_t)r + 1 : rt_shared;
+        };
+        switch (b.routine) {
+          case ESP_ALLGATHER:
+          case ESP_GATHER_BROADCAST:
+            if (b.routine == ESP_GATHER_BROADCAST && quant) {
+              add_piece(b.mid.base ? b.mid.at(lr) : nullptr, b.coff[ti], 0);
+              s.npieces = 1;
+              s.divisor = 1.0f;
+            } else {
+              for (int r = 0; r < n; ++r)
+                add_piece(b.recv1.base ? b.recv1.at(lr) : nullptr, (size_t)r * S + b.coff[ti], rt_of(r));
+              s.npieces = (uint32_t)n;
+              s.divisor = divisor;
+            }
+            break;
+          case ESP_ALLTOALL_ALLGATHER:
+            if (sparse) {
+              for (int r = 0; r < n; ++r)
+                add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr,
+                          (size_t)part * n * S + (size_t)r * S + b.coff[ti], rt_of(r));
+              s.npieces = (uint32_t)n;
+              s.divisor = divisor;
+            } else {
+              add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr, (size_t)part * S + b.coff[ti], 0);
+              s.npieces = 1;
+              s.divisor = 1.0f;
+            }
+            break;
+          default:   // ALLREDUCE / RS-AG / Reduce-Broadcast
+            if (w->sim) {
+              for (int r = 0; r < n; ++r)
+                add_piece(b.send.base ? b.send.at(r) : nullptr, b.coff[ti], 0);
+              s.npieces = (uint32_t)n;
+            } else {
+              add_piece(b.recv1.base ? b.recv1.at(0) : nullptr, b.coff[ti], 0);
+              s.npieces = 1;
+            }
+            s.divisor = divisor;
+            break;
+        }
+        s.nunits = div_up(len, tiles ? kTile : kUnit);
+        s.unit0 = u0;
+        u0 += s.nunits;
+        T.h2.push_back(s);
+        fill_unit_table(T.h2_units, (uint32_t)(T.h2.size() - 1 - h2_first), s.nunits);
+      }
+    }
+  }
+  b.nh2 = (int)(T.h2.size() - h2_first);
+  b.nh2_units = (int)u0;
+
+  // per critical rank op counts of the cost table
+  b.h1_calls = none ? 0 : (quant && (b.routine == ESP_ALLTOALL_ALLGATHER || b.routine == ESP_GATHER_BROADCAST) ? 2 : 1);
+  switch (b.routine) {
+    case ESP_ALLGATHER: b.h2_pieces_count = n; break;
+    case ESP_ALLTOALL_ALLGATHER: b.h2_pieces_count = sparse ? (uint64_t)n * n : 2ull * n; break;
+    case ESP_GATHER_BROADCAST: b.h2_pieces_count = quant ? n + 1 : n; break;
+    default: b.h2_pieces_count = none ? 0 : 1; break;
+  }
+}
+
+static void layout_plan(Plan& p, bool commit, HostTables& T) {
+  Layout L{p, commit};
+  p.arena.used = 0;
+  const int nslots = (int)p.ctxs.size();
+  size_t dyn_off = L.reserve(sizeof(uint64_t) * 2 * nslots);
+  p.dyn_dev = L.ptr<uint64_t>(dyn_off);
+  // count segments to size the zero region: SelState per h1/a7 segment + hist per DGC segment
+  size_t nst = 0, nhist = 0;
+  for (auto& b : p.buckets) {
+    const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
+    for (int t : b.tens) {
+      esp_ctx_s* c = p.ctxs[t];
+      int segs = 0;
+      for (int part = 0; part < (b.kind == ESP_NONE ? 1 : c->P); ++part)
+        if (b.kind == ESP_NONE ? c->N > 0 : c->phi[part] > c->plo[part]) ++segs;
+      nst += (size_t)segs * p.w->nlocal;
+      if (dgc) nhist += (size_t)segs * p.w->nlocal;
+      if (is_quant(b.kind)) nst += (size_t)p.w->nlocal;   // a7 (upper bound)
+    }
+  }
+  const size_t st_bytes = round_up(nst * sizeof(SelState), 256);
+  p.zero_bytes = st_bytes + nhist * 6144 * 4;
+  size_t zero_off = L.reserve(p.zero_bytes);
+  p.zero = commit ? p.arena.base + zero_off : nullptr;
+  size_t st_cursor = 0, hist_cursor = st_bytes;
+  T = HostTables{};
+  for (auto& b : p.buckets) {
+    HostTables TB;
+    build_bucket(L, b, TB, zero_off, st_cursor, hist_cursor);
+    // per-bucket device copies of the tables
+    auto up = [&](const auto& vec, auto*& dst) {
+      using E = typename std::decay<decltype(vec)>::type::value_type;
+      size_t off = L.reserve(std::max<size_t>(1, vec.size()) * sizeof(E));
+      dst = commit ? reinterpret_cast<typename std::decay<decltype(dst)>::type>(p.arena.base + off) : nullptr;
+      if (commit && !vec.empty())
+        ESP_CUDA(cudaMemcpy((void*)dst, vec.data(), vec.size() * sizeof(E), cudaMemcpyHostToDevice));
+    };
+    up(TB.h1, b.h1);
+    up(TB.h1_units, b.h1_units);
+    up(TB.h1_groups, b.h1_groups);
+    up(TB.a7, b.a7);
+    up(TB.a7_units, b.a7_units);
+    up(TB.a7_pieces, b.a7_pieces);
+    up(TB.h2, b.h2);
+    up(TB.h2_units, b.h2_units);
+    up(TB.h2_pieces, b.h2_pieces);
+    up(TB.rankterms, b.h2_rankterms);
+    if (commit) {
+      // pad patterns of every chunk that kernels never touch (R: payload layout)
+      for (int lr = 0; lr < p.w->nlocal; ++lr) {
+        if (b.kind == ESP_DGC || b.kind == ESP_TOPK) {
+          for (int part = 0; part < b.P; ++part)
+            for (size_t ti = 0; ti < b.tens.size(); ++ti) {
+              esp_ctx_s* c = p.ctxs[b.tens[ti]];
+              unsigned char* ch = b.send.at(lr) + (size_t)part * b.slot + b.coff[ti];
+              ESP_CUDA(cudaMemset(ch, 0xFF, 4ull * c->kpad));
+              ESP_CUDA(cudaMemset(ch + 4ull * c->kpad, 0, 4ull * c->kpad));
+            }
+        } else {
+          ESP_CUDA(cudaMemset(b.send.at(lr), 0, b.P * b.slot));
+          if (b.mid.base) ESP_CUDA(cudaMemset(b.mid.at(lr), 0, b.slot));
+        }
+      }
+    }
+  }
+}
+
+Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
+  for (Plan* up : w->plans)
+    if (up->ctxs == ctxs) return up;
+  auto p = std::make_unique<Plan>();
+  p->w = w;
+  p->ctxs = ctxs;
+  // ---- bucketing: group by (kind, routine, reduce) in order of first
+  // appearance, split each class at bucket_elems elements per rank
+  const uint64_t cap = w->bucket_elems ? w->bucket_elems : (64ull << 20);
+  std::vector<std::pair<std::tuple<int, int, int>, std::vector<int>>> classes;
+  for (int i = 0; i < (int)ctxs.size(); ++i) {
+    auto key = std::make_tuple(ctxs[i]->cfg.kind, ctxs[i]->routine, ctxs[i]->cfg.reduce);
+    auto it = std::find_if(classes.begin(), classes.end(), [&](auto& c) { return c.first == key; });
+    if (it == classes.end()) classes.push_back({key, {i}});
+    else it->second.push_back(i);
+  }
+  for (auto& cl : classes) {
+    Bucket b;
+    b.kind = std::get<0>(cl.first);
+    b.routine = std::get<1>(cl.first);
+    b.reduce = std::get<2>(cl.first);
+    uint64_t elems = 0;
+    for (int i : cl.second) {
+      if (!b.tens.empty() && elems + ctxs[i]->N > cap) {
+        p->buckets.push_back(b);
+        b.tens.clear();
+        elems = 0;
+      }
+      b.tens.push_back(i);
+      elems += ctxs[i]->N;
+    }
+    if (!b.tens.empty()) p->buckets.push_back(b);
+  }
+  HostTables T;
+  layout_plan(*p, false, T);
+  p->arena.alloc();
+  layout_plan(*p, true, T);
+  for (auto& b : p->buckets) {
+    ESP_CUDA(cudaEventCreateWithFlags(&b.ev_h1, cudaEventDisableTiming));
+    ESP_CUDA(cudaEventCreateWithFlags(&b.ev_comm, cudaEventDisableTiming));
+  }
+  ESP_CUDA(cudaMallocHost(&p->dyn_host, sizeof(uint64_t) * 2 * std::max<size_t>(1, ctxs.size())));
+  ESP_CUDA(cudaEventCreateWithFlags(&p->dyn_ev, cudaEventDisableTiming));
+  w->plans.push_back(p.release());
+  return w->plans.back();
+}
+
+void drop_plans_with(esp_world_s* w, esp_ctx_s* c) {
+  auto& v = w->plans;
+  for (auto it = v.begin(); it != v.end();) {
+    if (std::find((*it)->ctxs.begin(), (*it)->ctxs.end(), c) != (*it)->ctxs.end()) {
+      cudaStreamSynchronize(w->comm_stream);
+      cudaDeviceSynchronize();
+      delete *it;
+      it = v.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+void clear_plans(esp_world_s* w) {
+  if (!w->plans.empty()) cudaDeviceSynchronize();
+  for (Plan* p : w->plans) delete p;
+  w->plans.clear();
+}
+
+// ------------------------------------------------------------------ execution
+static void upload_dyn(Plan& p, const float* const* grads, cudaStream_t st) {
+  const size_t ns = p.ctxs.size();
+  if (p.dyn_pending) ESP_CUDA(cudaEventSynchronize(p.dyn_ev));
+  for (size_t i = 0; i < ns; ++i) {
+    p.dyn_host[i] = (uint64_t)(uintptr_t)grads[i];
+    p.dyn_host[ns + i] = p.ctxs[i]->step;
+  }
+  ESP_CUDA(cudaMemcpyAsync(p.dyn_dev, p.dyn_host, sizeof(uint64_t) * 2 * ns, cudaMemcpyHostToDevice, st));
+  ESP_CUDA(cudaEventRecord(p.dyn_ev, st));
+  p.dyn_pending = true;
+}
+
+static void run_h1(Plan& p, Bucket& b, cudaStream_t st) {
+  switch (b.kind) {
+    case ESP_DGC: case ESP_TOPK:
+      launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st);
+      break;
+    case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
+    case ESP_EFSIGNSGD: launch_sign_h1(K_EFSIGN, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
+    case ESP_ONEBIT: launch_sign_h1(K_ONEBIT, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
+    default: launch_pack(b.h1, b.h1_units, b.nh1_units, st); break;
+  }
+  ESP_CUDA(cudaGetLastError());
+  for (int lr = 0; lr < p.w->nlocal; ++lr) p.w->counters[lr].h1_calls += b.h1_calls * b.tens.size();
+}
+
+static void run_mid(Plan& p, Bucket& b, cudaStream_t cs) {
+  const int k = b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT;
+  launch_sign_h1(k, b.a7, b.a7_units, b.na7_units, b.a7_pieces, cs);
+  ESP_CUDA(cudaGetLastError());
+}
+
+static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cudaEvent_t mid1) {
+  esp_world_s* w = p.w;
+  const int n = w->nranks;
+  const size_t S = b.slot;
+  const bool quant = is_quant(b.kind);
+  switch (b.routine) {
+    case ESP_ALLGATHER:
+      coll_allgather(w, b.send, b.recv1, S, cs);
+      break;
+    case ESP_ALLTOALL_ALLGATHER:
+      coll_alltoall(w, b.send, b.recv1, S, cs);
+      if (quant) {
+        if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
+        run_mid(p, b, cs);
+        if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
+        coll_allgather(w, b.mid, b.recv2, S, cs);
+      } else {
+        coll_allgather(w, b.recv1, b.recv2, (size_t)n * S, cs);
+      }
+      break;
+    case ESP_GATHER_BROADCAST:
+      coll_gather(w, b.send, b.recv1, S, cs);
+      if (quant) {
+        if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
+        run_mid(p, b, cs);
+        if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
+        coll_broadcast(w, b.mid, S, cs);
+      } else {
+        coll_broadcast(w, b.recv1, (size_t)n * S, cs);
+      }
+      break;
+    default: {
+      // ALLREDUCE (NONE or shared-index Randomk values), RS/AG, Reduce/Broadcast
+      const size_t count = b.kind == ESP_NONE ? b.none_count : S / 4;
+      const uint64_t M = b.kind == ESP_NONE ? b.none_bytes : S;   // logical bytes
+      for (int lr = 0; lr < w->nlocal; ++lr) {
+        const bool root = (w->sim ? lr : w->rank) == 0;
+        if (b.routine == ESP_ALLREDUCE) {
+          count_coll(w, lr, ESP_OP_ALLREDUCE, 2ull * (n - 1) * M / n, 2ull * (n - 1) * M / n);
+        } else if (b.routine == ESP_REDUCESCATTER_ALLGATHER) {
+          count_coll(w, lr, ESP_OP_REDUCESCATTER, (n - 1) * M / n, (n - 1) * M / n);
+          count_coll(w, lr, ESP_OP_ALLGATHER, (n - 1) * M / n, (n - 1) * M / n);
+        } else {
+          count_coll(w, lr, ESP_OP_REDUCE, root ? 0 : M, root ? (n - 1) * M : 0);
+          count_coll(w, lr, ESP_OP_BROADCAST, root ? (n > 1 ? M : 0) : 0, root ? 0 : M);
+        }
+      }
+      if (w->sim) {
+        // executed by h2, which reads every virtual rank's packed buffer
+      } else if (b.routine == ESP_ALLREDUCE) {
+        coll_allreduce_f32(w, b.send, b.recv1, count, cs);
+      } else if (b.routine == ESP_REDUCESCATTER_ALLGATHER) {
+        LocalBufs shard{b.recv1.base + (size_t)w->rank * (count / n) * 4, b.recv1.stride};
+        coll_reducescatter_f32(w, b.send, shard, count, cs);
+        coll_allgather_inplace_f32(w, b.recv1, count / n, cs);
+      } else {
+        coll_reduce_f32(w, b.send, b.recv1, count, cs);
+        ESP_NCCL(ncclBroadcast(b.recv1.at(0), b.recv1.at(0), 4 * count, ncclUint8, 0, w->comm, cs));
+      }
+      break;
+    }
+  }
+}
+
+static void run_h2(Plan& p, Bucket& b, cudaStream_t st) {
+  switch (b.kind) {
+    case ESP_DGC: case ESP_TOPK: launch_h2_sparse(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, st); break;
+    case ESP_RANDOMK:
+      launch_h2_randomk(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, b.h2_rankterms, st);
+      break;
+    case ESP_EFSIGNSGD: launch_h2_sign(K_EFSIGN, b.h2, b.h2_units, b.nh2_units, b.h2_pieces, st); break;
+    case ESP_ONEBIT: launch_h2_sign(K_ONEBIT, b.h2, b.h2_units, b.nh2_units, b.h2_pieces, st); break;
+    default: launch_h2_dense(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, st); break;
+  }
+  ESP_CUDA(cudaGetLastError());
+  for (int lr = 0; lr < p.w->nlocal; ++lr) p.w->counters[lr].h2_pieces += b.h2_pieces_count * b.tens.size();
+}
+
+static cudaEvent_t tev(esp_world_s* w, size_t i) {
+  while (w->tev.size() <= i) {
+    cudaEvent_t e;
+    ESP_CUDA(cudaEventCreate(&e));
+    w->tev.push_back(e);
+  }
+  return w->tev[i];
+}
+
+void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
+  Plan& p = *pp;
+  esp_world_s* w = p.w;
+  const cudaStream_t cs = w->comm_stream;
+  upload_dyn(p, grads, st);
+  if (p.zero_bytes) ESP_CUDA(cudaMemsetAsync(p.zero, 0, p.zero_bytes, st));
+  const bool timing = w->timing;
+  if (timing) {
+    // serialised phases, events around each (a breakdown, not the pipelined time)
+    const size_t nb = p.buckets.size();
+    ESP_CUDA(cudaEventRecord(tev(w, 0), st));
+    for (size_t i = 0; i < nb; ++i) {
+      Bucket& b = p.buckets[i];
+      cudaEvent_t e0 = tev(w, 1 + 6 * i), e1 = tev(w, 2 + 6 * i), e2 = tev(w, 3 + 6 * i);
+      cudaEvent_t e3 = tev(w, 4 + 6 * i), m0 = tev(w, 5 + 6 * i), m1 = tev(w, 6 + 6 * i);
+      ESP_CUDA(cudaEventRecord(e0, st));
+      run_h1(p, b, st);
+      ESP_CUDA(cudaEventRecord(e1, st));
+      ESP_CUDA(cudaStreamWaitEvent(cs, e1, 0));
+      ESP_CUDA(cudaEventRecord(m0, cs));
+      ESP_CUDA(cudaEventRecord(m1, cs));
+      run_comm(p, b, cs, m0, m1);
+      ESP_CUDA(cudaEventRecord(e2, cs));
+      ESP_CUDA(cudaStreamWaitEvent(st, e2, 0));
+      run_h2(p, b, st);
+      ESP_CUDA(cudaEventRecord(e3, st));
+    }
+    ESP_CUDA(cudaEventRecord(tev(w, 1 + 6 * nb), st));
+    ESP_CUDA(cudaEventSynchronize(tev(w, 1 + 6 * nb)));
+    esp_timing_t t{};
+    ESP_CUDA(cudaEventElapsedTime(&t.total_ms, tev(w, 0), tev(w, 1 + 6 * nb)));
+    for (size_t i = 0; i < nb; ++i) {
+      float a, bb, c, m;
+      ESP_CUDA(cudaEventElapsedTime(&a, tev(w, 1 + 6 * i), tev(w, 2 + 6 * i)));
+      ESP_CUDA(cudaEventElapsedTime(&bb, tev(w, 2 + 6 * i), tev(w, 3 + 6 * i)));
+      ESP_CUDA(cudaEventElapsedTime(&c, tev(w, 3 + 6 * i), tev(w, 4 + 6 * i)));
+      ESP_CUDA(cudaEventElapsedTime(&m, tev(w, 5 + 6 * i), tev(w, 6 + 6 * i)));
+      t.h1_ms += a;
+      t.comm_ms += bb - m;
+      t.mid_ms += m;
+      t.h2_ms += c;
+    }
+    w->last = t;
+  } else {
+    // pipelined: h1(b+1) is issued before h2(b), so compression of the next
+    // bucket overlaps the collective of the previous one
+    ESP_CUDA(cudaEventRecord(w->ev_fork, st));
+    ESP_CUDA(cudaStreamWaitEvent(cs, w->ev_fork, 0));
+    const size_t nb = p.buckets.size();
+    for (size_t i = 0; i <= nb; ++i) {
+      if (i < nb) {
+        Bucket& b = p.buckets[i];
+        run_h1(p, b, st);
+        ESP_CUDA(cudaEventRecord(b.ev_h1, st));
+        ESP_CUDA(cudaStreamWaitEvent(cs, b.ev_h1, 0));
+        run_comm(p, b, cs, nullptr, nullptr);
+        ESP_CUDA(cudaEventRecord(b.ev_comm, cs));
+      }
+      if (i >= 1) {
+        Bucket& b = p.buckets[i - 1];
+        ESP_CUDA(cudaStreamWaitEvent(st, b.ev_comm, 0));
+        run_h2(p, b, st);
+      }
+    }
+  }
+  for (auto* c : p.ctxs) c->step += 1;
+}
+
+void execute_compress(Plan* pp, const float* grad, void* payload, cudaStream_t st) {
+  Plan& p = *pp;
+  esp_ctx_s* c = p.ctxs[0];
+  float* g = const_cast<float*>(grad);
+  upload_dyn(p, &g, st);
+  if (p.zero_bytes) ESP_CUDA(cudaMemsetAsync(p.zero, 0, p.zero_bytes, st));
+  Bucket& b = p.buckets[0];
+  run_h1(p, b, st);
+  for (int lr = 0; lr < p.w->nlocal; ++lr)
+    ESP_CUDA(cudaMemcpyAsync((unsigned char*)payload + (size_t)lr * c->payload_bytes, b.send.at(lr),
+                             c->payload_bytes, cudaMemcpyDeviceToDevice, st));
+  c->step += 1;
+}
+
+}  // namespace esp

@@ -1,0 +1,364 @@
+// Worlds and the collective layer (NCCL inside a
+// machine, a CCL per data format, several CUDA streams).  A world is either an
+// NCCL communicator (one process per GPU, NVLink 5 / NVSwitch) or a "sim" world
+// of n virtual ranks on one GPU whose collectives are device-to-device copies.
+#include <atomic>
+#include <cmath>
+
+#include "esp_internal.h"
+#include "esp_kernels.h"
+
+namespace esp {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+uint64_t host_splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// ---- sizes ---------------------------------------------------------------------
+uint32_t k_of(uint64_t numel, double ratio) {
+  if (numel == 0) return 0;
+  double c = std::ceil(ratio * (double)numel);   // R1: max(1, ceil(rho N)), <= N
+  uint64_t k = c < 1.0 ? 1 : (uint64_t)c;
+  return (uint32_t)(k > numel ? numel : k);
+}
+
+int nparts_of(int routine, int n) { return routine == ESP_ALLTOALL_ALLGATHER ? n : 1; }
+
+uint32_t partition_len(uint64_t numel, int nparts) {
+  if (nparts == 1) return (uint32_t)numel;
+  uint64_t L = (numel + nparts - 1) / nparts;
+  return (uint32_t)round_up(L, 32);   // R10
+}
+
+bool is_sparse(int kind) { return kind == ESP_RANDOMK || kind == ESP_DGC || kind == ESP_TOPK; }
+bool is_quant(int kind) { return kind == ESP_EFSIGNSGD || kind == ESP_ONEBIT; }
+
+bool pair_legal(const esp_compressor_cfg_t& cfg, int routine) {
+  // routines table; "cannot use Allreduce" P:1073; allreducible P:38/P:56
+  if (cfg.kind == ESP_NONE)
+    return routine == ESP_ALLREDUCE || routine == ESP_REDUCESCATTER_ALLGATHER ||
+           routine == ESP_REDUCE_BROADCAST;
+  if (routine == ESP_ALLGATHER || routine == ESP_ALLTOALL_ALLGATHER || routine == ESP_GATHER_BROADCAST)
+    return true;
+  return cfg.kind == ESP_RANDOMK && cfg.randomk_shared_indices && routine == ESP_ALLREDUCE;
+}
+
+size_t chunk_bytes_of(const esp_compressor_cfg_t& cfg, uint64_t numel, int nparts, uint32_t* kpad_out) {
+  const uint64_t L = partition_len(numel, nparts);
+  uint64_t maxlen = 0, maxk = 0;
+  for (int p = 0; p < nparts; ++p) {
+    uint64_t lo = std::min<uint64_t>(numel, (uint64_t)p * L), hi = std::min<uint64_t>(numel, lo + L);
+    if (nparts == 1) { lo = 0; hi = numel; }
+    maxlen = std::max(maxlen, hi - lo);
+    maxk = std::max<uint64_t>(maxk, k_of(hi - lo, cfg.ratio));
+  }
+  uint32_t kpad = 0;
+  size_t bytes = 0;
+  switch (cfg.kind) {
+    case ESP_DGC: case ESP_TOPK:
+      kpad = (uint32_t)round_up(maxk, 4); bytes = 8ull * kpad; break;
+    case ESP_RANDOMK:
+      kpad = (uint32_t)round_up(maxk, 4); bytes = 4ull * kpad; break;
+    case ESP_EFSIGNSGD: case ESP_ONEBIT:
+      kpad = (uint32_t)round_up((maxlen + 31) / 32, 4); bytes = 16 + 4ull * kpad; break;
+    default:
+      kpad = 0; bytes = 4ull * numel; break;
+  }
+  if (kpad_out) *kpad_out = kpad;
+  return bytes;
+}
+
+void Arena::alloc() {
+  size = round_up(used, 256);
+  if (size) ESP_CUDA(cudaMalloc(&base, size));
+}
+Arena::~Arena() {
+  if (base) cudaFree(base);
+}
+
+// ---- collectives (the *_f32 reductions are counted by the caller with logical sizes) -----------------------------------------------------------------
+void count_coll(esp_world_s* w, int lr, int op, uint64_t sent, uint64_t recv) {
+  esp_counters_t& c = w->counters[lr];
+  c.calls[op] += 1;
+  c.sent[op] += sent;
+  c.recv[op] += recv;
+}
+static int grank(esp_world_s* w, int lr) { return w->sim ? lr : w->rank; }
+
+static void d2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes && dst != src) ESP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+}
+
+void coll_allgather(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t bytes, cudaStream_t st) {
+  const int n = w->nranks;
+  for (int lr = 0; lr < w->nlocal; ++lr) count_coll(w, lr, ESP_OP_ALLGATHER, (n - 1) * bytes, (n - 1) * bytes);
+  if (w->sim) {
+    for (int q = 0; q < n; ++q)
+      for (int r = 0; r < n; ++r) d2d(recv.at(q) + r * bytes, send.at(r), bytes, st);
+  } else {
+    ESP_NCCL(ncclAllGather(send.at(0), recv.at(0), bytes, ncclUint8, w->comm, st));
+  }
+}
+
+void coll_alltoall(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t chunk, cudaStream_t st) {
+  const int n = w->nranks;
+  for (int lr = 0; lr < w->nlocal; ++lr) count_coll(w, lr, ESP_OP_ALLTOALL, (n - 1) * chunk, (n - 1) * chunk);
+  if (w->sim) {
+    for (int q = 0; q < n; ++q)
+      for (int r = 0; r < n; ++r) d2d(recv.at(q) + r * chunk, send.at(r) + q * chunk, chunk, st);
+  } else {
+    ESP_NCCL(ncclAlltoAll(send.at(0), recv.at(0), chunk, ncclUint8, w->comm, st));
+  }
+}
+
+void coll_gather(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t bytes, cudaStream_t st) {
+  const int n = w->nranks;
+  for (int lr = 0; lr < w->nlocal; ++lr) {
+    if (grank(w, lr) == 0) count_coll(w, lr, ESP_OP_GATHER, 0, (n - 1) * bytes);
+    else count_coll(w, lr, ESP_OP_GATHER, bytes, 0);
+  }
+  if (w->sim) {
+    for (int r = 0; r < n; ++r) d2d(recv.at(0) + r * bytes, send.at(r), bytes, st);
+  } else {
+    ESP_NCCL(ncclGather(send.at(0), recv.at(0), bytes, ncclUint8, 0, w->comm, st));
+  }
+}
+
+void coll_broadcast(esp_world_s* w, LocalBufs buf, size_t bytes, cudaStream_t st) {
+  const int n = w->nranks;
+  for (int lr = 0; lr < w->nlocal; ++lr) {
+    if (grank(w, lr) == 0) count_coll(w, lr, ESP_OP_BROADCAST, n > 1 ? bytes : 0, 0);
+    else count_coll(w, lr, ESP_OP_BROADCAST, 0, bytes);
+  }
+  if (w->sim) {
+    for (int q = 1; q < n; ++q) d2d(buf.at(q), buf.at(0), bytes, st);
+  } else {
+    ESP_NCCL(ncclBroadcast(buf.at(0), buf.at(0), bytes, ncclUint8, 0, w->comm, st));
+  }
+}
+
+void coll_allreduce_f32(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t count_, cudaStream_t st) {
+  ESP_REQUIRE(!w->sim, ESP_ERR_STATE, "allreduce in a sim world is executed by h2");
+  ESP_NCCL(ncclAllReduce(send.at(0), recv.at(0), count_, ncclFloat32, ncclSum, w->comm, st));
+}
+
+void coll_reducescatter_f32(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t count_, cudaStream_t st) {
+  ESP_REQUIRE(!w->sim, ESP_ERR_STATE, "reduce-scatter in a sim world is executed by h2");
+  ESP_NCCL(ncclReduceScatter(send.at(0), recv.at(0), count_ / w->nranks, ncclFloat32, ncclSum, w->comm, st));
+}
+
+void coll_allgather_inplace_f32(esp_world_s* w, LocalBufs buf, size_t count_per_rank, cudaStream_t st) {
+  ESP_REQUIRE(!w->sim, ESP_ERR_STATE, "in-place allgather in a sim world is executed by h2");
+  float* base = reinterpret_cast<float*>(buf.at(0));
+  ESP_NCCL(ncclAllGather(base + (size_t)w->rank * count_per_rank, base, count_per_rank, ncclFloat32,
+                         w->comm, st));
+}
+
+void coll_reduce_f32(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t count_, cudaStream_t st) {
+  ESP_REQUIRE(!w->sim, ESP_ERR_STATE, "reduce in a sim world is executed by h2");
+  ESP_NCCL(ncclReduce(send.at(0), recv.at(0), count_, ncclFloat32, ncclSum, 0, w->comm, st));
+}
+
+}  // namespace esp
+
+using namespace esp;
+
+extern "C" {
+
+const char* esp_status_string(esp_status_t s) {
+  switch (s) {
+    case ESP_OK: return "ESP_OK";
+    case ESP_ERR_INVALID_ARG: return "ESP_ERR_INVALID_ARG";
+    case ESP_ERR_UNSUPPORTED: return "ESP_ERR_UNSUPPORTED";
+    case ESP_ERR_TOO_LARGE: return "ESP_ERR_TOO_LARGE";
+    case ESP_ERR_CUDA: return "ESP_ERR_CUDA";
+    case ESP_ERR_NCCL: return "ESP_ERR_NCCL";
+    case ESP_ERR_OOM: return "ESP_ERR_OOM";
+    case ESP_ERR_STATE: return "ESP_ERR_STATE";
+  }
+  return "ESP_ERR_UNKNOWN";
+}
+
+const char* esp_last_error(void) { return g_last_error.c_str(); }
+uint64_t esp_launch_count(void) { return g_launches.load(); }
+const char* esp_version(void) { return "espresso-b200 0.1 (sm_100a)"; }
+
+esp_status_t esp_get_nccl_unique_id(void* out128) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(out128, ESP_ERR_INVALID_ARG, "out128 is NULL");
+  ncclUniqueId id;
+  ESP_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, 128);
+  ESP_API_END
+}
+
+static void world_common_init(esp_world_s* w) {
+  ESP_CUDA(cudaSetDevice(w->dev));
+  int lo = 0, hi = 0;
+  ESP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  // communication gets the higher priority so collectives are not starved by
+  // the next bucket's compression kernels (SURVEY.md 7 hard part 7)
+  ESP_CUDA(cudaStreamCreateWithPriority(&w->comm_stream, cudaStreamNonBlocking, hi));
+  ESP_CUDA(cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming));
+  ESP_CUDA(cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming));
+  w->counters.assign(w->nlocal, esp_counters_t{});
+}
+
+esp_status_t esp_world_create_nccl(const void* id128, int nranks, int rank, int cuda_dev, esp_world_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(id128 && out, ESP_ERR_INVALID_ARG, "null argument");
+  ESP_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks && cuda_dev >= 0, ESP_ERR_INVALID_ARG,
+              "bad nranks/rank/device");
+  auto w = std::make_unique<esp_world_s>();
+  w->sim = false;
+  w->nranks = nranks;
+  w->rank = rank;
+  w->nlocal = 1;
+  w->dev = cuda_dev;
+  world_common_init(w.get());
+  ncclUniqueId id;
+  std::memcpy(&id, id128, 128);
+  ESP_NCCL(ncclCommInitRank(&w->comm, nranks, id, rank));
+  *out = w.release();
+  ESP_API_END
+}
+
+esp_status_t esp_world_create_sim(int nranks, int cuda_dev, esp_world_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(out, ESP_ERR_INVALID_ARG, "out is NULL");
+  ESP_REQUIRE(nranks >= 1 && nranks <= 64 && cuda_dev >= 0, ESP_ERR_INVALID_ARG, "bad nranks/device");
+  auto w = std::make_unique<esp_world_s>();
+  w->sim = true;
+  w->nranks = nranks;
+  w->rank = 0;
+  w->nlocal = nranks;
+  w->dev = cuda_dev;
+  world_common_init(w.get());
+  *out = w.release();
+  ESP_API_END
+}
+
+esp_status_t esp_world_destroy(esp_world_t w) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
+  ESP_REQUIRE(w->ctxs.empty(), ESP_ERR_STATE, "destroy every ctx of the world first");
+  cudaSetDevice(w->dev);
+  cudaStreamSynchronize(w->comm_stream);
+  clear_plans(w);
+  if (w->comm) ncclCommDestroy(w->comm);
+  for (auto e : w->tev) cudaEventDestroy(e);
+  cudaEventDestroy(w->ev_join);
+  cudaEventDestroy(w->ev_fork);
+  cudaStreamDestroy(w->comm_stream);
+  delete w;
+  ESP_API_END
+}
+
+esp_status_t esp_world_check(esp_world_t w) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
+  cudaError_t e = cudaGetLastError();
+  ESP_REQUIRE(e == cudaSuccess, ESP_ERR_CUDA, std::string("async CUDA error: ") + cudaGetErrorString(e));
+  if (w->comm) {
+    ncclResult_t r = ncclSuccess;
+    ESP_NCCL(ncclCommGetAsyncError(w->comm, &r));
+    ESP_REQUIRE(r == ncclSuccess || r == ncclInProgress, ESP_ERR_NCCL,
+                std::string("async NCCL error: ") + ncclGetErrorString(r));
+  }
+  ESP_API_END
+}
+
+esp_status_t esp_world_info(esp_world_t w, int* nranks, int* rank, int* nlocal) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
+  if (nranks) *nranks = w->nranks;
+  if (rank) *rank = w->rank;
+  if (nlocal) *nlocal = w->nlocal;
+  ESP_API_END
+}
+
+esp_status_t esp_world_counters(esp_world_t w, esp_counters_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w && out, ESP_ERR_INVALID_ARG, "null argument");
+  *out = w->counters[0];
+  ESP_API_END
+}
+
+esp_status_t esp_world_counters_local(esp_world_t w, int lr, esp_counters_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w && out && lr >= 0 && lr < w->nlocal, ESP_ERR_INVALID_ARG, "bad argument");
+  *out = w->counters[lr];
+  ESP_API_END
+}
+
+esp_status_t esp_world_reset_counters(esp_world_t w) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
+  w->counters.assign(w->nlocal, esp_counters_t{});
+  ESP_API_END
+}
+
+esp_status_t esp_world_set_timing(esp_world_t w, int enable) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
+  w->timing = enable != 0;
+  ESP_API_END
+}
+
+esp_status_t esp_world_set_bucket_elems(esp_world_t w, uint64_t elems) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
+  w->bucket_elems = elems;
+  clear_plans(w);
+  ESP_API_END
+}
+
+esp_status_t esp_compressed_bytes(const esp_compressor_cfg_t* cfg, size_t numel, int nparts, size_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(cfg && out && nparts >= 1, ESP_ERR_INVALID_ARG, "bad argument");
+  ESP_REQUIRE(cfg->kind >= ESP_NONE && cfg->kind <= ESP_ONEBIT, ESP_ERR_INVALID_ARG, "bad kind");
+  ESP_REQUIRE(numel < (1ull << 31), ESP_ERR_TOO_LARGE, "numel >= 2^31");
+  *out = chunk_bytes_of(*cfg, numel, nparts, nullptr) * (size_t)nparts;
+  ESP_API_END
+}
+
+esp_status_t esp_wire_bytes(int row, double M, int n, double* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(out && n >= 1 && M >= 0 && row >= 0 && row <= 5, ESP_ERR_INVALID_ARG, "bad argument");
+  // cost table of flat communication, P:38-43 (communication volume = time * B)
+  double v = 0;
+  if (n > 1) {
+    switch (row) {
+      case 0: v = 2.0 * (n - 1) * M / n; break;            // Allreduce
+      case 1: v = (n - 1) * M; break;                      // Allgather
+      case 2: v = ((double)n * n - 1) * M / n; break;      // Alltoall/Allgather, sparse
+      case 3: v = 2.0 * (n - 1) * M / n; break;            // Alltoall/Allgather, quantized (R13)
+      case 4: v = (2.0 * n - 1) * M; break;                // Gather/Broadcast, sparse
+      case 5: v = (double)n * M; break;                    // Gather/Broadcast, quantized
+    }
+  }
+  *out = v;
+  ESP_API_END
+}
+
+esp_status_t esp_model_time(int row, double M, int n, double B, double* out_seconds) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(out_seconds && B > 0, ESP_ERR_INVALID_ARG, "bad argument");
+  double v = 0;
+  esp_status_t s = esp_wire_bytes(row, M, n, &v);
+  if (s != ESP_OK) return s;
+  *out_seconds = v / B;
+  ESP_API_END
+}
+
+}  // extern "C"

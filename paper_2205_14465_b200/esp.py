@@ -1,0 +1,285 @@
+"""Thin ctypes binding of libesp.so (include/esp.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels and NCCL calls.  torch is used for device memory, streams and
+process groups (exchange of the NCCL unique id).  There is no fallback: if
+libesp.so is missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libesp.so")
+
+KINDS = {"none": 0, "randomk": 1, "dgc": 2, "topk": 3, "efsignsgd": 4, "onebit": 5}
+ROUTINES = {"allreduce": 0, "allgather": 1, "alltoall_allgather": 2, "gather_broadcast": 3,
+            "reducescatter_allgather": 4, "reduce_broadcast": 5}
+REDUCE = {"mean": 0, "sum": 1}
+OPS = ("allreduce", "allgather", "alltoall", "gather", "broadcast", "reducescatter", "reduce")
+STATUS = {0: "ESP_OK", 1: "ESP_ERR_INVALID_ARG", 2: "ESP_ERR_UNSUPPORTED", 3: "ESP_ERR_TOO_LARGE",
+          4: "ESP_ERR_CUDA", 5: "ESP_ERR_NCCL", 6: "ESP_ERR_OOM", 7: "ESP_ERR_STATE"}
+
+# every symbol esp.h declares (tests check the library exports all of them)
+SYMBOLS = (
+    "esp_get_nccl_unique_id", "esp_world_create_nccl", "esp_world_create_sim", "esp_world_destroy",
+    "esp_world_check", "esp_world_info", "esp_world_counters", "esp_world_counters_local",
+    "esp_world_reset_counters", "esp_world_set_timing", "esp_last_timing", "esp_world_set_bucket_elems",
+    "esp_ctx_create", "esp_ctx_destroy", "esp_ctx_payload_bytes", "esp_ctx_get_state",
+    "esp_ctx_set_state", "esp_compress", "esp_decompress", "esp_sync", "esp_sync_many",
+    "esp_compressed_bytes", "esp_wire_bytes", "esp_model_time", "esp_status_string",
+    "esp_last_error", "esp_launch_count", "esp_version",
+)
+
+
+class CompressorCfg(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("error_feedback", C.c_int32), ("ratio", C.c_double),
+                ("seed", C.c_uint64), ("randomk_shared_indices", C.c_int32), ("reduce", C.c_int32)]
+
+
+class Counters(C.Structure):
+    _fields_ = [("calls", C.c_uint64 * 7), ("sent", C.c_uint64 * 7), ("recv", C.c_uint64 * 7),
+                ("h1_calls", C.c_uint64), ("h2_pieces", C.c_uint64)]
+
+
+class Timing(C.Structure):
+    _fields_ = [("total_ms", C.c_float), ("h1_ms", C.c_float), ("comm_ms", C.c_float),
+                ("mid_ms", C.c_float), ("h2_ms", C.c_float)]
+
+
+class EspError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        vp, sz, i32, u64, dbl = C.c_void_p, C.c_size_t, C.c_int, C.c_uint64, C.c_double
+        sig = {
+            "esp_get_nccl_unique_id": [vp],
+            "esp_world_create_nccl": [vp, i32, i32, i32, C.POINTER(vp)],
+            "esp_world_create_sim": [i32, i32, C.POINTER(vp)],
+            "esp_world_destroy": [vp], "esp_world_check": [vp],
+            "esp_world_info": [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)],
+            "esp_world_counters": [vp, C.POINTER(Counters)],
+            "esp_world_counters_local": [vp, i32, C.POINTER(Counters)],
+            "esp_world_reset_counters": [vp], "esp_world_set_timing": [vp, i32],
+            "esp_last_timing": [vp, C.POINTER(Timing)], "esp_world_set_bucket_elems": [vp, u64],
+            "esp_ctx_create": [vp, C.POINTER(CompressorCfg), i32, u64, sz, C.POINTER(vp)],
+            "esp_ctx_destroy": [vp], "esp_ctx_payload_bytes": [vp, C.POINTER(sz)],
+            "esp_ctx_get_state": [vp, vp, C.POINTER(sz)], "esp_ctx_set_state": [vp, vp, sz],
+            "esp_compress": [vp, vp, vp, vp], "esp_decompress": [vp, C.POINTER(vp), i32, vp, vp],
+            "esp_sync": [vp, vp, vp, vp], "esp_sync_many": [vp, C.POINTER(vp), C.POINTER(vp), i32, vp],
+            "esp_compressed_bytes": [C.POINTER(CompressorCfg), sz, i32, C.POINTER(sz)],
+            "esp_wire_bytes": [i32, dbl, i32, C.POINTER(dbl)],
+            "esp_model_time": [i32, dbl, i32, dbl, C.POINTER(dbl)],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.esp_status_string.argtypes = [C.c_int]
+        L.esp_status_string.restype = C.c_char_p
+        L.esp_last_error.argtypes = []
+        L.esp_last_error.restype = C.c_char_p
+        L.esp_launch_count.argtypes = []
+        L.esp_launch_count.restype = C.c_uint64
+        L.esp_version.argtypes = []
+        L.esp_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(status):
+    if status != 0:
+        raise EspError(status, lib().esp_last_error().decode())
+
+
+def cfg_of(kind="dgc", ratio=0.01, error_feedback=True, seed=0, shared_indices=True, reduce="mean"):
+    return CompressorCfg(KINDS[kind], int(bool(error_feedback)), float(ratio), int(seed),
+                         int(bool(shared_indices)), REDUCE[reduce])
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+# ---------------------------------------------------------------- C-named calls
+def esp_compressed_bytes(cfg: CompressorCfg, numel: int, nparts: int) -> int:
+    out = C.c_size_t()
+    _check(lib().esp_compressed_bytes(C.byref(cfg), numel, nparts, C.byref(out)))
+    return out.value
+
+
+def esp_wire_bytes(row: int, M: float, n: int) -> float:
+    out = C.c_double()
+    _check(lib().esp_wire_bytes(row, M, n, C.byref(out)))
+    return out.value
+
+
+def esp_model_time(row: int, M: float, n: int, B: float) -> float:
+    out = C.c_double()
+    _check(lib().esp_model_time(row, M, n, B, C.byref(out)))
+    return out.value
+
+
+def esp_launch_count() -> int:
+    return int(lib().esp_launch_count())
+
+
+class World:
+    """esp_world_t.  `World.sim(n)`: n virtual ranks on one GPU;
+    `World.nccl()`: one rank per process over torch.distributed's group."""
+
+    def __init__(self, handle, device):
+        self.h = handle
+        self.device = device
+        n, r, nl = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().esp_world_info(self.h, C.byref(n), C.byref(r), C.byref(nl)))
+        self.nranks, self.rank, self.nlocal = n.value, r.value, nl.value
+        self.ctxs = []
+
+    @classmethod
+    def sim(cls, nranks: int, device: int = 0):
+        h = C.c_void_p()
+        _check(lib().esp_world_create_sim(nranks, device, C.byref(h)))
+        return cls(h, device)
+
+    @classmethod
+    def nccl(cls, device: int | None = None, group=None):
+        import torch
+        import torch.distributed as dist
+        rank, n = dist.get_rank(group), dist.get_world_size(group)
+        device = torch.cuda.current_device() if device is None else device
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            _check(lib().esp_get_nccl_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (C.c_ubyte * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        _check(lib().esp_world_create_nccl(uid, n, rank, device, C.byref(h)))
+        return cls(h, device)
+
+    def counters(self, lr: int = 0) -> dict:
+        c = Counters()
+        _check(lib().esp_world_counters_local(self.h, lr, C.byref(c)))
+        d = {"h1_calls": c.h1_calls, "h2_pieces": c.h2_pieces}
+        for i, op in enumerate(OPS):
+            d[op] = {"calls": c.calls[i], "sent": c.sent[i], "recv": c.recv[i]}
+        d["sent"] = sum(c.sent)
+        d["recv"] = sum(c.recv)
+        return d
+
+    def reset_counters(self):
+        _check(lib().esp_world_reset_counters(self.h))
+
+    def set_timing(self, on: bool):
+        _check(lib().esp_world_set_timing(self.h, int(on)))
+
+    def last_timing(self) -> dict:
+        t = Timing()
+        _check(lib().esp_last_timing(self.h, C.byref(t)))
+        return {f: getattr(t, f) for f, _ in Timing._fields_}
+
+    def set_bucket_elems(self, elems: int):
+        _check(lib().esp_world_set_bucket_elems(self.h, elems))
+
+    def check(self):
+        _check(lib().esp_world_check(self.h))
+
+    def destroy(self):
+        for c in list(self.ctxs):
+            c.destroy()
+        if self.h:
+            _check(lib().esp_world_destroy(self.h))
+            self.h = None
+
+
+class Ctx:
+    """esp_ctx_t: one tensor's (compressor, ratio, routine) option and EF state."""
+
+    def __init__(self, world: World, kind="dgc", routine="allgather", numel=1, tensor_id=0, ratio=0.01,
+                 error_feedback=True, seed=0, shared_indices=True, reduce="mean"):
+        self.world = world
+        self.kind, self.routine, self.numel = kind, routine, numel
+        self.cfg = cfg_of(kind, ratio, error_feedback, seed, shared_indices, reduce)
+        self.h = C.c_void_p()
+        _check(lib().esp_ctx_create(world.h, C.byref(self.cfg), ROUTINES[routine], tensor_id, numel,
+                                    C.byref(self.h)))
+        world.ctxs.append(self)
+        pb = C.c_size_t()
+        _check(lib().esp_ctx_payload_bytes(self.h, C.byref(pb)))
+        self.payload_bytes = pb.value
+
+    def destroy(self):
+        if self.h:
+            _check(lib().esp_ctx_destroy(self.h))
+            self.h = None
+            self.world.ctxs.remove(self)
+
+    def get_state(self):
+        """-> (step, r [nlocal, numel] fp32, r2 [nlocal, r2_len] fp32) as numpy."""
+        import numpy as np
+        n = C.c_size_t()
+        _check(lib().esp_ctx_get_state(self.h, None, C.byref(n)))
+        buf = (C.c_ubyte * n.value)()
+        _check(lib().esp_ctx_get_state(self.h, buf, C.byref(n)))
+        hdr = np.frombuffer(bytes(buf[:40]), np.uint64)
+        step, numel, r2_len, nl = (int(x) for x in hdr[1:5])
+        body = np.frombuffer(bytes(buf[40:]), np.float32).reshape(nl, numel + r2_len)
+        return step, body[:, :numel].copy(), body[:, numel:].copy()
+
+    def set_state(self, step, r, r2=None):
+        import numpy as np
+        nl = self.world.nlocal
+        r = np.asarray(r, np.float32).reshape(nl, -1)
+        r2 = np.zeros((nl, 0), np.float32) if r2 is None else np.asarray(r2, np.float32).reshape(nl, -1)
+        hdr = np.array([0x4553505354415445, step, r.shape[1], r2.shape[1], nl], np.uint64)
+        blob = hdr.tobytes() + np.concatenate([r, r2], axis=1).astype(np.float32).tobytes()
+        buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+        _check(lib().esp_ctx_set_state(self.h, buf, len(blob)))
+
+
+def esp_compress(ctx: Ctx, grad, payload=None, stream=None):
+    """h1 of every local rank; returns the payload (uint8 CUDA tensor)."""
+    import torch
+    if payload is None:
+        payload = torch.empty(ctx.world.nlocal * ctx.payload_bytes, dtype=torch.uint8, device=grad.device)
+    _check(lib().esp_compress(ctx.h, _ptr(grad), _ptr(payload), _stream(stream)))
+    return payload
+
+
+def esp_decompress(ctx: Ctx, pieces, out, stream=None):
+    arr = (C.c_void_p * len(pieces))(*[p.data_ptr() for p in pieces])
+    _check(lib().esp_decompress(ctx.h, arr, len(pieces), _ptr(out), _stream(stream)))
+    return out
+
+
+def esp_sync(world: World, ctx: Ctx, grad, stream=None):
+    _check(lib().esp_sync(world.h, ctx.h, _ptr(grad), _stream(stream)))
+    return grad
+
+
+def esp_sync_many(world: World, ctxs, grads, stream=None):
+    n = len(ctxs)
+    hs = (C.c_void_p * n)(*[c.h.value for c in ctxs])
+    gs = (C.c_void_p * n)(*[g.data_ptr() for g in grads])
+    _check(lib().esp_sync_many(world.h, hs, gs, n, _stream(stream)))
+    return grads

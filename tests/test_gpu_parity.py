@@ -1,0 +1,282 @@
+"""Parity of the CUDA path (through the C ABI) against the oracle, sim world:
+n virtual ranks on one GPU (SURVEY.md 4 layers 2-3).  Bit-exact on indices,
+values, packed sign bits, residuals and aggregated outputs wherever the
+arithmetic is fixed; fp64-reduced scales within 1e-6 relative (north_star)."""
+import numpy as np
+import pytest
+
+from oracle import esp_oracle as O
+from synth.values import gradient
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def esp():
+    from paper_2205_14465_b200 import esp as E
+    return E
+
+
+def bits(x):
+    return np.ascontiguousarray(x, np.float32).view(np.uint32)
+
+
+def upload(arrs):
+    return torch.from_numpy(np.concatenate(arrs)).cuda()
+
+
+def check_out(kind, got, ref, where):
+    if kind in ("dgc", "topk", "randomk", "none"):
+        bad = np.nonzero(bits(got) != bits(ref))[0]
+        assert bad.size == 0, f"{where}: {bad.size} mismatches, first {bad[:5]} got {got[bad[:5]]} ref {ref[bad[:5]]}"
+    else:
+        np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-30, err_msg=where)
+
+
+def run_sim(kind, routine, n, N, steps=3, ratio=0.01, dist="D1", mode="mixed", ef=True,
+            reduce="mean", shared=True, lockstep=None, tensor_id=3, seed=11):
+    """Run `steps` syncs in a sim world and compare every rank's output and
+    residual with the oracle after each step."""
+    E = esp()
+    if lockstep is None:
+        lockstep = kind in O.QUANTIZED
+    w = E.World.sim(n, 0)
+    ctx = E.Ctx(w, kind, routine, N, tensor_id=tensor_id, ratio=ratio, error_feedback=ef, seed=seed,
+                shared_indices=shared, reduce=reduce)
+    cfg = O.Cfg(kind, ratio, ef, seed, shared, reduce)
+    st = O.new_states(n, N, routine, cfg)
+    try:
+        for s in range(steps):
+            if lockstep and s > 0:
+                # oracle -> GPU: re-seed the GPU state from the oracle's (never the reverse)
+                r = np.stack([x.r for x in st])
+                r2len = ctx.get_state()[2].shape[1]
+                r2 = np.zeros((n, r2len), np.float32)
+                for i, x in enumerate(st):
+                    if x.r2 is not None:
+                        r2[i, :x.r2.size] = x.r2
+                ctx.set_state(st[0].step, r, r2)
+            grads = [gradient(N, step=s, rank=r, tensor=tensor_id, dist=dist, mode=mode) for r in range(n)]
+            ref = O.sync(routine, cfg, grads, st, tensor_id=tensor_id)
+            g = upload(grads)
+            E.esp_sync(w, ctx, g)
+            torch.cuda.synchronize()
+            out = g.cpu().numpy().reshape(n, N)
+            for r in range(n):
+                check_out(kind, out[r], ref.outs[r], f"{kind}/{routine} n={n} N={N} step={s} rank={r} out")
+            if kind != "none":
+                step, rg, r2g = ctx.get_state()
+                assert step == st[0].step
+                for r in range(n):
+                    if kind in O.QUANTIZED:
+                        np.testing.assert_allclose(rg[r], st[r].r, rtol=1e-6, atol=1e-30)
+                    else:
+                        assert np.array_equal(bits(rg[r]), bits(st[r].r)), f"residual rank {r} step {s}"
+                    if st[r].r2 is not None:
+                        np.testing.assert_allclose(r2g[r, :st[r].r2.size], st[r].r2, rtol=1e-6, atol=1e-30)
+        return w
+    finally:
+        w.destroy()
+
+
+# ---------------------------------------------------------------- config 1
+@pytest.mark.parametrize("N", [1 << 20, 10 ** 6])
+def test_config1_dgc_allgather_n2(N):
+    """BASELINE config 1: 1M-element fp32 gradient, DGC top-1% with EF, Allgather,
+    n = 2 simulated ranks, 5 steps, bit-exact."""
+    run_sim("dgc", "allgather", 2, N, steps=5, ratio=0.01)
+
+
+@pytest.mark.parametrize("dist", ["D1", "D2", "D3"])
+@pytest.mark.parametrize("N", [1, 31, 33, 1000, 4097, 8193, (1 << 16) + 3, 100_003])
+def test_dgc_sizes_dists(N, dist):
+    run_sim("dgc", "allgather", 2, N, steps=2, ratio=0.01, dist=dist)
+
+
+@pytest.mark.parametrize("mode", ["equal", "zeros", "spike", "pm0", "denormal", "mixed"])
+def test_dgc_adversarial(mode):
+    # all-equal magnitudes force the fallback and the tie-break; zeros give T = 0
+    run_sim("dgc", "allgather", 2, 50_001, steps=2, ratio=0.01, dist="D4", mode=mode)
+
+
+@pytest.mark.parametrize("ratio", [0.001, 0.05, 0.5, 1.0])
+def test_dgc_ratios(ratio):
+    run_sim("dgc", "allgather", 2, 70_000, steps=2, ratio=ratio)
+
+
+# ---------------------------------------------------------------- every pair
+PAIRS = [(k, r) for k in O.KINDS for r in O.ROUTINES if O.legal(O.Cfg(k), r)]
+
+
+@pytest.mark.parametrize("kind,routine", PAIRS)
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_pairs_sim(kind, routine, n):
+    run_sim(kind, routine, n, 20_011, steps=3, ratio=0.02)
+
+
+@pytest.mark.parametrize("kind", ["efsignsgd", "onebit"])
+@pytest.mark.parametrize("N", [1, 32, 33, 1023, 8193, 300_007])
+def test_sign_sizes(kind, N):
+    run_sim(kind, "allgather", 2, N, steps=2)
+    run_sim(kind, "alltoall_allgather", 4, N, steps=2)
+
+
+def test_randomk_unshared_and_sum():
+    run_sim("randomk", "allgather", 4, 10_000, steps=3, ratio=0.03, shared=False)
+    run_sim("dgc", "allgather", 4, 10_000, steps=2, reduce="sum")
+    run_sim("efsignsgd", "gather_broadcast", 4, 10_000, steps=2, reduce="sum")
+
+
+def test_no_error_feedback():
+    for kind in ("dgc", "randomk", "efsignsgd", "onebit"):
+        run_sim(kind, "allgather", 2, 9_999, steps=2, ef=False)
+
+
+def test_n1_world():
+    for kind, routine in PAIRS:
+        run_sim(kind, routine, 1, 5_000, steps=2, ratio=0.05)
+
+
+# ---------------------------------------------------------------- h1 / h2 ABI
+@pytest.mark.parametrize("kind", ["dgc", "randomk", "efsignsgd", "onebit"])
+def test_compress_payload_bytes(kind):
+    """esp_compress payload == the oracle's serialized chunks (sparse: byte for
+    byte; sign: words byte for byte, scale header within 1e-6)."""
+    E = esp()
+    n, N = 2, 33_333
+    w = E.World.sim(n, 0)
+    try:
+        ctx = E.Ctx(w, kind, "alltoall_allgather", N, tensor_id=5, ratio=0.01)
+        cfg = O.Cfg(kind, 0.01)
+        st = O.new_states(n, N, "alltoall_allgather", cfg)
+        grads = [gradient(N, rank=r, tensor=5) for r in range(n)]
+        ref = O.sync("alltoall_allgather", cfg, grads, st, tensor_id=5)
+        pay = E.esp_compress(ctx, upload(grads))
+        torch.cuda.synchronize()
+        pay = pay.cpu().numpy().reshape(n, -1)
+        assert pay.shape[1] == len(ref.payloads[0])
+        cb = O.chunk_bytes(cfg, N, n)
+        for r in range(n):
+            got, exp = pay[r].tobytes(), ref.payloads[r]
+            for p in range(n):
+                gc, ec = got[p * cb:(p + 1) * cb], exp[p * cb:(p + 1) * cb]
+                if kind in O.SPARSE:
+                    assert gc == ec, f"rank {r} chunk {p}"
+                else:
+                    assert gc[16:] == ec[16:], f"words rank {r} chunk {p}"
+                    np.testing.assert_allclose(np.frombuffer(gc[:8], np.float32),
+                                               np.frombuffer(ec[:8], np.float32), rtol=1e-6)
+        # h2 through esp_decompress == oracle aggregation of the same pieces
+        pieces = [torch.from_numpy(pay[r].copy()).cuda() for r in range(n)]
+        out = torch.empty(N, dtype=torch.float32, device="cuda")
+        E.esp_decompress(ctx, pieces, out)
+        torch.cuda.synchronize()
+        if kind in O.SPARSE:
+            check_out(kind, out.cpu().numpy(), ref.outs[0], "decompress")
+    finally:
+        w.destroy()
+
+
+def test_sync_many_equals_single():
+    """A mixed strategy over a tensor set (bucketing, multi-tensor tables, small
+    buckets to exercise the pipeline) equals per-tensor oracle syncs."""
+    E = esp()
+    n = 4
+    specs = [("dgc", "allgather", 5000), ("none", "allreduce", 1000), ("efsignsgd", "alltoall_allgather", 7000),
+             ("dgc", "allgather", 33), ("randomk", "allreduce", 4000), ("onebit", "gather_broadcast", 3000),
+             ("dgc", "alltoall_allgather", 9000), ("none", "reduce_broadcast", 17), ("dgc", "allgather", 70000)]
+    w = E.World.sim(n, 0)
+    w.set_bucket_elems(20000)
+    try:
+        ctxs = [E.Ctx(w, k, r, N, tensor_id=t, ratio=0.01) for t, (k, r, N) in enumerate(specs)]
+        sts = [O.new_states(n, N, r, O.Cfg(k, 0.01)) for (k, r, N) in specs]
+        for s in range(3):
+            for t, (k, r, N) in enumerate(specs):
+                if k in O.QUANTIZED and s > 0:
+                    st = sts[t]
+                    r2 = np.zeros((n, ctxs[t].get_state()[2].shape[1]), np.float32)
+                    for i, x in enumerate(st):
+                        if x.r2 is not None:
+                            r2[i, :x.r2.size] = x.r2
+                    ctxs[t].set_state(st[0].step, np.stack([x.r for x in st]), r2)
+            grads = [[gradient(N, step=s, rank=r, tensor=t) for r in range(n)] for t, (_, _, N) in enumerate(specs)]
+            refs = [O.sync(r, O.Cfg(k, 0.01), grads[t], sts[t], tensor_id=t) for t, (k, r, N) in enumerate(specs)]
+            gs = [upload(grads[t]) for t in range(len(specs))]
+            E.esp_sync_many(w, ctxs, gs)
+            torch.cuda.synchronize()
+            for t, (k, r, N) in enumerate(specs):
+                out = gs[t].cpu().numpy().reshape(n, N)
+                for rr in range(n):
+                    check_out(k, out[rr], refs[t].outs[rr], f"sync_many t={t} {k}/{r} step {s} rank {rr}")
+    finally:
+        w.destroy()
+
+
+def test_counters_match_cost_table():
+    """Byte counters of the instrumented comm layer == the oracle's counters ==
+    the cost table's closed forms."""
+    E = esp()
+    n, N = 4, 12_345
+    for kind, routine in PAIRS:
+        w = E.World.sim(n, 0)
+        try:
+            ctx = E.Ctx(w, kind, routine, N, ratio=0.01)
+            cfg = O.Cfg(kind, 0.01)
+            ref = O.sync(routine, cfg, [gradient(N, rank=r) for r in range(n)], O.new_states(n, N, routine, cfg))
+            E.esp_sync(w, ctx, upload([gradient(N, rank=r) for r in range(n)]))
+            torch.cuda.synchronize()
+            for lr in range(n):
+                c = w.counters(lr)
+                assert c["recv"] == ref.counters[lr].recv, (kind, routine, lr)
+                assert c["sent"] == ref.counters[lr].sent, (kind, routine, lr)
+            c0 = w.counters(0)
+            assert (c0["h1_calls"], c0["h2_pieces"]) == (ref.counters[0].h1, ref.counters[0].h2), (kind, routine)
+        finally:
+            w.destroy()
+
+
+# ---------------------------------------------------------------- ABI negative tests
+def test_abi_errors():
+    E = esp()
+    w = E.World.sim(2, 0)
+    try:
+        with pytest.raises(E.EspError) as ei:
+            E.Ctx(w, "dgc", "allreduce", 100)
+        assert ei.value.status == 2
+        with pytest.raises(E.EspError) as ei:
+            E.Ctx(w, "randomk", "allreduce", 100, shared_indices=False)
+        assert ei.value.status == 2
+        with pytest.raises(E.EspError) as ei:
+            E.Ctx(w, "none", "allgather", 100)
+        assert ei.value.status == 2
+        with pytest.raises(E.EspError) as ei:
+            E.Ctx(w, "dgc", "allgather", 1 << 31)
+        assert ei.value.status == 3
+        with pytest.raises(E.EspError) as ei:
+            E.Ctx(w, "dgc", "allgather", 0)
+        assert ei.value.status == 1
+        with pytest.raises(E.EspError) as ei:
+            E.Ctx(w, "dgc", "allgather", 10, ratio=0.0)
+        assert ei.value.status == 1
+        ctx = E.Ctx(w, "dgc", "allgather", 100)
+        g = torch.zeros(201, device="cuda")
+        with pytest.raises(E.EspError) as ei:
+            E.esp_sync(w, ctx, g[1:])           # misaligned
+        assert ei.value.status == 1
+        w2 = E.World.sim(2, 0)
+        try:
+            with pytest.raises(E.EspError) as ei:
+                E.esp_sync(w2, ctx, g)          # ctx of another world
+            assert ei.value.status == 7
+        finally:
+            w2.destroy()
+    finally:
+        w.destroy()
