@@ -140,6 +140,15 @@ esp_status_t esp_last_timing(esp_world_t w, esp_timing_t* out);
 /* Max elements per bucket of esp_sync_many (0 = library default).  Smaller
  * buckets pipeline h1 / comm / h2 across buckets (a9). */
 esp_status_t esp_world_set_bucket_elems(esp_world_t w, uint64_t elems);
+/* Dominant-kernel probe (roofline evidence): while enabled, CUDA events are
+ * recorded on the launching stream around the streaming h1 kernel of every
+ * bucket (DGC/TOPK: the fused g + r pass; Randomk/sign: their h1 kernel; NONE:
+ * the pack copy).  esp_probe_read waits for them and returns the summed device
+ * time (ms), the number of probed launches and the algorithmic HBM bytes those
+ * launches had to move (12 B/elem with EF, +1/8 B/elem of sign bits), then
+ * clears the record. */
+esp_status_t esp_world_set_probe(esp_world_t w, int enable);
+esp_status_t esp_probe_read(esp_world_t w, double* ms, uint64_t* launches, uint64_t* bytes);
 
 /* ---- ctx: one tensor's option + EF state ----------------------------------
  * Validates the (compressor, routine) pair: NONE -> {ALLREDUCE,

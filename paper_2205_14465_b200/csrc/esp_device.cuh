@@ -47,9 +47,14 @@ __device__ __forceinline__ void f4set(float4& v, int c, float x) {
   if (c == 0) v.x = x; else if (c == 1) v.y = x; else if (c == 2) v.z = x; else v.w = x;
 }
 
+__device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 // Load 4 consecutive floats at element e of an n-element array; out-of-range -> 0.
+// Segments of a sim world may start at any float offset: the vector path is
+// taken only when the address is 16-byte aligned.
 __device__ __forceinline__ float4 load4_guard(const float* base, uint32_t e, uint32_t n) {
-  if (e + 3 < n) return ld4(base + e);
+  if (e + 3 < n && al16(base + e)) return ld4(base + e);
+  if (e + 3 < n) return make_float4(base[e], base[e + 1], base[e + 2], base[e + 3]);
   float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
   if (e < n) v.x = base[e];
   if (e + 1 < n) v.y = base[e + 1];
@@ -57,7 +62,8 @@ __device__ __forceinline__ float4 load4_guard(const float* base, uint32_t e, uin
   return v;
 }
 __device__ __forceinline__ float4 load4_stream_guard(const float* base, uint32_t e, uint32_t n) {
-  if (e + 3 < n) return ld_stream4(base + e);
+  if (e + 3 < n && al16(base + e)) return ld_stream4(base + e);
+  if (e + 3 < n) return make_float4(base[e], base[e + 1], base[e + 2], base[e + 3]);
   float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
   if (e < n) v.x = base[e];
   if (e + 1 < n) v.y = base[e + 1];
@@ -65,7 +71,8 @@ __device__ __forceinline__ float4 load4_stream_guard(const float* base, uint32_t
   return v;
 }
 __device__ __forceinline__ void store4_guard(float* base, uint32_t e, uint32_t n, float4 v) {
-  if (e + 3 < n) { st4(base + e, v); return; }
+  if (e + 3 < n && al16(base + e)) { st4(base + e, v); return; }
+  if (e + 3 < n) { base[e] = v.x; base[e + 1] = v.y; base[e + 2] = v.z; base[e + 3] = v.w; return; }
   if (e < n) base[e] = v.x;
   if (e + 1 < n) base[e + 1] = v.y;
   if (e + 2 < n) base[e + 2] = v.z;

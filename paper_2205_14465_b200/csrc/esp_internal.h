@@ -89,6 +89,12 @@ struct esp_world_s {
   esp_timing_t last{};
   std::vector<cudaEvent_t> tev;            // timing events of the last call
   uint64_t bucket_elems = 0;
+  // dominant-kernel probe (bench roofline): event pairs recorded around the
+  // streaming h1 kernel of every bucket, with the algorithmic bytes it moves
+  bool probe = false;
+  std::vector<cudaEvent_t> probe_pool;
+  size_t probe_used = 0;
+  std::vector<uint64_t> probe_bytes;
   std::vector<esp::Plan*> plans;           // owned; freed by esp::clear_plans
   std::set<esp_ctx_s*> ctxs;
 };

@@ -10,8 +10,10 @@ namespace esp {
 void count_launches(int n);   // process-wide counter behind esp_launch_count()
 
 // DGC / TOPK h1 (k_dgc.cu)
+// probe0/probe1 (optional): events recorded around the streaming pass
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
-                   const uint32_t* group_seg, int ngroups, cudaStream_t st);
+                   const uint32_t* group_seg, int ngroups, cudaStream_t st,
+                   cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr);
 // Randomk h1 (k_randomk.cu)
 void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 // EFSignSGD / Onebit h1; with pieces != nullptr the input is the decode-mean of

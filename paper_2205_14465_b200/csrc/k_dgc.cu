@@ -381,10 +381,13 @@ __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __rest
 
 // ------------------------------------------------------------------ launchers
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
-                   const uint32_t* group_seg, int ngroups, cudaStream_t st) {
+                   const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
+                   cudaEvent_t probe1) {
   if (nsegs == 0) return;
   dgc_sample_kernel<<<nsegs, 1024, 0, st>>>(segs);
+  if (probe0) cudaEventRecord(probe0, st);
   dgc_stream_kernel<false><<<nunits, kThreads, 0, st>>>(segs, unit_seg);
+  if (probe1) cudaEventRecord(probe1, st);
   dgc_stream_kernel<true><<<nunits, kThreads, 0, st>>>(segs, unit_seg);
   dgc_refine_kernel<2><<<ngroups, kThreads, 0, st>>>(segs, group_seg);
   dgc_refine_kernel<3><<<ngroups, kThreads, 0, st>>>(segs, group_seg);

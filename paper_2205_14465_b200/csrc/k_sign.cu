@@ -170,8 +170,10 @@ __global__ void __launch_bounds__(kThreads) sign_h1_kernel(const SegH1* __restri
     }
     hdr[0] = x0;
     if (KIND == K_ONEBIT) hdr[1] = x1;
-    S.lazy_out[0] = x0;
-    S.lazy_out[1] = x1;
+    if (S.ef) {   // without EF the state stays the zero residual
+      S.lazy_out[0] = x0;
+      S.lazy_out[1] = x1;
+    }
   }
 }
 

@@ -35,6 +35,7 @@ struct Bucket {
   uint32_t* h2_rankterms = nullptr;
   cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
+  uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
 };
 
 struct Plan {
@@ -199,6 +200,17 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     }
   }
   b.nh1 = (int)(T.h1.size() - h1_first);
+  {
+    // algorithmic bytes of the streaming h1 pass: read g, read r,
+    // write r = 12 B/elem with EF (4 B/elem without); sign adds 1/8 B/elem of
+    // bits; NONE's pack reads and writes 4 B/elem
+    uint64_t elems = 0;
+    for (int i = 0; i < b.nh1; ++i) elems += T.h1[h1_first + i].n;
+    const bool ef = p.ctxs[b.tens[0]]->cfg.error_feedback != 0;
+    if (none) b.h1_bytes = 8 * elems;
+    else if (quant) b.h1_bytes = (ef ? 12 : 4) * elems + elems / 8;
+    else b.h1_bytes = (ef ? 12 : 4) * elems;
+  }
   // unit/group tables refer to segment indices local to the bucket; the
   // unit0/group0 fields are relative to the bucket's own unit table
   {
@@ -495,16 +507,34 @@ static void upload_dyn(Plan& p, const float* const* grads, cudaStream_t st) {
   p.dyn_pending = true;
 }
 
+static void probe_pair(esp_world_s* w, cudaEvent_t* e0, cudaEvent_t* e1, uint64_t bytes) {
+  while (w->probe_pool.size() < 2 * (w->probe_used + 1)) {
+    cudaEvent_t e;
+    ESP_CUDA(cudaEventCreate(&e));
+    w->probe_pool.push_back(e);
+  }
+  *e0 = w->probe_pool[2 * w->probe_used];
+  *e1 = w->probe_pool[2 * w->probe_used + 1];
+  w->probe_bytes.resize(w->probe_used + 1);
+  w->probe_bytes[w->probe_used] = bytes;
+  ++w->probe_used;
+}
+
 static void run_h1(Plan& p, Bucket& b, cudaStream_t st) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (p.w->probe && b.nh1_units) probe_pair(p.w, &e0, &e1, b.h1_bytes);
+  const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
+  if (e0 && !dgc) ESP_CUDA(cudaEventRecord(e0, st));
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
-      launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st);
+      launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1);
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
     case ESP_EFSIGNSGD: launch_sign_h1(K_EFSIGN, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
     case ESP_ONEBIT: launch_sign_h1(K_ONEBIT, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
     default: launch_pack(b.h1, b.h1_units, b.nh1_units, st); break;
   }
+  if (e1 && !dgc) ESP_CUDA(cudaEventRecord(e1, st));
   ESP_CUDA(cudaGetLastError());
   for (int lr = 0; lr < p.w->nlocal; ++lr) p.w->counters[lr].h1_calls += b.h1_calls * b.tens.size();
 }

@@ -257,6 +257,7 @@ esp_status_t esp_world_destroy(esp_world_t w) {
   clear_plans(w);
   if (w->comm) ncclCommDestroy(w->comm);
   for (auto e : w->tev) cudaEventDestroy(e);
+  for (auto e : w->probe_pool) cudaEventDestroy(e);
   cudaEventDestroy(w->ev_join);
   cudaEventDestroy(w->ev_fork);
   cudaStreamDestroy(w->comm_stream);
@@ -320,6 +321,33 @@ esp_status_t esp_world_set_bucket_elems(esp_world_t w, uint64_t elems) {
   ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
   w->bucket_elems = elems;
   clear_plans(w);
+  ESP_API_END
+}
+
+esp_status_t esp_world_set_probe(esp_world_t w, int enable) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
+  w->probe = enable != 0;
+  w->probe_used = 0;
+  ESP_API_END
+}
+
+esp_status_t esp_probe_read(esp_world_t w, double* ms, uint64_t* launches, uint64_t* bytes) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w && ms && launches && bytes, ESP_ERR_INVALID_ARG, "null argument");
+  double t = 0;
+  uint64_t b = 0;
+  for (size_t i = 0; i < w->probe_used; ++i) {
+    ESP_CUDA(cudaEventSynchronize(w->probe_pool[2 * i + 1]));
+    float x = 0;
+    ESP_CUDA(cudaEventElapsedTime(&x, w->probe_pool[2 * i], w->probe_pool[2 * i + 1]));
+    t += x;
+    b += w->probe_bytes[i];
+  }
+  *ms = t;
+  *launches = w->probe_used;
+  *bytes = b;
+  w->probe_used = 0;
   ESP_API_END
 }
 

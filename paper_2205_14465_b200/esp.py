@@ -26,6 +26,7 @@ SYMBOLS = (
     "esp_get_nccl_unique_id", "esp_world_create_nccl", "esp_world_create_sim", "esp_world_destroy",
     "esp_world_check", "esp_world_info", "esp_world_counters", "esp_world_counters_local",
     "esp_world_reset_counters", "esp_world_set_timing", "esp_last_timing", "esp_world_set_bucket_elems",
+    "esp_world_set_probe", "esp_probe_read",
     "esp_ctx_create", "esp_ctx_destroy", "esp_ctx_payload_bytes", "esp_ctx_get_state",
     "esp_ctx_set_state", "esp_compress", "esp_decompress", "esp_sync", "esp_sync_many",
     "esp_compressed_bytes", "esp_wire_bytes", "esp_model_time", "esp_status_string",
@@ -74,6 +75,8 @@ def lib():
             "esp_world_counters_local": [vp, i32, C.POINTER(Counters)],
             "esp_world_reset_counters": [vp], "esp_world_set_timing": [vp, i32],
             "esp_last_timing": [vp, C.POINTER(Timing)], "esp_world_set_bucket_elems": [vp, u64],
+            "esp_world_set_probe": [vp, i32],
+            "esp_probe_read": [vp, C.POINTER(dbl), C.POINTER(u64), C.POINTER(u64)],
             "esp_ctx_create": [vp, C.POINTER(CompressorCfg), i32, u64, sz, C.POINTER(vp)],
             "esp_ctx_destroy": [vp], "esp_ctx_payload_bytes": [vp, C.POINTER(sz)],
             "esp_ctx_get_state": [vp, vp, C.POINTER(sz)], "esp_ctx_set_state": [vp, vp, sz],
@@ -177,6 +180,15 @@ class World:
         _check(lib().esp_world_create_nccl(uid, n, rank, device, C.byref(h)))
         return cls(h, device)
 
+    @classmethod
+    def nccl_single(cls, device: int = 0):
+        """A 1-rank NCCL world (no process group needed)."""
+        uid = (C.c_ubyte * 128)()
+        _check(lib().esp_get_nccl_unique_id(uid))
+        h = C.c_void_p()
+        _check(lib().esp_world_create_nccl(uid, 1, 0, device, C.byref(h)))
+        return cls(h, device)
+
     def counters(self, lr: int = 0) -> dict:
         c = Counters()
         _check(lib().esp_world_counters_local(self.h, lr, C.byref(c)))
@@ -200,6 +212,15 @@ class World:
 
     def set_bucket_elems(self, elems: int):
         _check(lib().esp_world_set_bucket_elems(self.h, elems))
+
+    def set_probe(self, on: bool):
+        _check(lib().esp_world_set_probe(self.h, int(on)))
+
+    def probe_read(self):
+        """-> (device ms, launches, algorithmic bytes) of the probed h1 kernels."""
+        ms, nl, b = C.c_double(), C.c_uint64(), C.c_uint64()
+        _check(lib().esp_probe_read(self.h, C.byref(ms), C.byref(nl), C.byref(b)))
+        return ms.value, nl.value, b.value
 
     def check(self):
         _check(lib().esp_world_check(self.h))
