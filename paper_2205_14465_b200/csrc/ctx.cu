@@ -206,7 +206,9 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
   std::vector<SegH2> segs;
   std::vector<uint32_t> units;
   std::vector<const unsigned char*> pp;
-  std::vector<uint32_t> rt;
+  std::vector<uint32_t> rt, piece_seg;
+  std::vector<size_t> toff_words;
+  size_t toff_total = 0;
   const bool tiles = c->cfg.kind == ESP_DGC || c->cfg.kind == ESP_TOPK;
   const float divisor = c->cfg.reduce == ESP_MEAN ? (float)npieces : 1.0f;
   uint32_t u0 = 0;
@@ -231,19 +233,26 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
     s.unit0 = u0;
     u0 += s.nunits;
     for (uint32_t i = 0; i < s.nunits; ++i) units.push_back((uint32_t)segs.size());
+    if (tiles) {
+      toff_words.push_back(toff_total);
+      toff_total += (size_t)npieces * (s.nunits + 1);
+      for (int i = 0; i < npieces; ++i) piece_seg.push_back((uint32_t)segs.size());
+    }
     segs.push_back(s);
   }
   // device scratch: dyn (out pointer, step of the last compression), tables
   const size_t b_dyn = 16, b_seg = segs.size() * sizeof(SegH2), b_units = units.size() * 4;
-  const size_t b_pp = pp.size() * 8, b_rt = rt.size() * 4;
+  const size_t b_pp = pp.size() * 8, b_rt = rt.size() * 4, b_ps = piece_seg.size() * 4;
   size_t off_seg = round_up(b_dyn, 256), off_units = round_up(off_seg + b_seg, 256);
   size_t off_pp = round_up(off_units + b_units, 256), off_rt = round_up(off_pp + b_pp, 256);
-  const size_t total = round_up(off_rt + b_rt, 256);
+  size_t off_ps = round_up(off_rt + b_rt, 256), off_toff = round_up(off_ps + b_ps, 256);
+  const size_t total = round_up(off_toff + toff_total * 4, 256);
   unsigned char* d = nullptr;
   ESP_CUDA(cudaMallocAsync((void**)&d, total, st));
-  for (auto& s : segs) {
-    s.optr = reinterpret_cast<const uint64_t*>(d);
-    s.step = reinterpret_cast<const uint64_t*>(d + 8);
+  for (size_t i = 0; i < segs.size(); ++i) {
+    segs[i].optr = reinterpret_cast<const uint64_t*>(d);
+    segs[i].step = reinterpret_cast<const uint64_t*>(d + 8);
+    if (tiles) segs[i].toff = reinterpret_cast<uint32_t*>(d + off_toff) + toff_words[i];
   }
   std::vector<unsigned char> host(total, 0);
   uint64_t dyn[2] = {(uint64_t)(uintptr_t)out, c->step ? c->step - 1 : 0};
@@ -252,6 +261,7 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
   std::memcpy(host.data() + off_units, units.data(), b_units);
   std::memcpy(host.data() + off_pp, pp.data(), b_pp);
   std::memcpy(host.data() + off_rt, rt.data(), b_rt);
+  std::memcpy(host.data() + off_ps, piece_seg.data(), b_ps);
   ESP_CUDA(cudaMemcpyAsync(d, host.data(), total, cudaMemcpyHostToDevice, st));
   ESP_CUDA(cudaStreamSynchronize(st));   // host staging buffer goes out of scope
   const SegH2* dseg = reinterpret_cast<const SegH2*>(d + off_seg);
@@ -259,7 +269,10 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
   const unsigned char* const* dpp = reinterpret_cast<const unsigned char* const*>(d + off_pp);
   const uint32_t* drt = reinterpret_cast<const uint32_t*>(d + off_rt);
   switch (c->cfg.kind) {
-    case ESP_DGC: case ESP_TOPK: launch_h2_sparse(dseg, dunits, (int)u0, dpp, st); break;
+    case ESP_DGC: case ESP_TOPK:
+      launch_h2_sparse(dseg, dunits, (int)u0, reinterpret_cast<const uint32_t*>(d + off_ps),
+                       (int)piece_seg.size(), dpp, st);
+      break;
     case ESP_RANDOMK: launch_h2_randomk(dseg, dunits, (int)u0, dpp, drt, st); break;
     case ESP_EFSIGNSGD: launch_h2_sign(K_EFSIGN, dseg, dunits, (int)u0, dpp, st); break;
     default: launch_h2_sign(K_ONEBIT, dseg, dunits, (int)u0, dpp, st); break;

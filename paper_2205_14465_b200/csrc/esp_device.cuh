@@ -79,7 +79,16 @@ __device__ __forceinline__ void store4_guard(float* base, uint32_t e, uint32_t n
 }
 
 // ---- CTA-wide scans / reductions for 256 threads ---------------------------------
+// BAR = 0: __syncthreads; BAR > 0: named barrier BAR over the first 256 threads
+// (the consumer warps of a warp-specialised kernel).
+template <int BAR>
+__device__ __forceinline__ void csync() {
+  if (BAR == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(kThreads) : "memory");
+}
+
 // Exclusive scan of v over the CTA in thread order.  `sh` needs 9 uint32.
+template <int BAR = 0>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, uint32_t* sh) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
@@ -89,7 +98,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total,
     if (lane >= o) x += y;
   }
   if (lane == 31) sh[warp] = x;
-  __syncthreads();
+  csync<BAR>();
   if (warp == 0) {
     uint32_t w = lane < (kThreads / 32) ? sh[lane] : 0u;
     uint32_t s = w;
@@ -101,36 +110,89 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total,
     if (lane < 8) sh[lane] = s - w;
     if (lane == 7) sh[8] = s;
   }
-  __syncthreads();
+  csync<BAR>();
   uint32_t r = x - v + sh[warp];
   *total = sh[8];
-  __syncthreads();
+  csync<BAR>();
   return r;
 }
 
+template <int BAR = 0>
 __device__ __forceinline__ uint32_t block_sum_u32(uint32_t v, uint32_t* sh) {
   uint32_t t;
-  block_excl_scan(v, &t, sh);
+  block_excl_scan<BAR>(v, &t, sh);
   return t;
 }
 
 // Deterministic fp64 CTA sum (fixed shuffle tree then warp order).  sh: 8 doubles.
+template <int BAR = 0>
 __device__ __forceinline__ double block_sum_f64(double v, double* sh) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if (lane == 0) sh[warp] = v;
-  __syncthreads();
+  csync<BAR>();
   double t = 0.0;
   if (threadIdx.x == 0) {
     for (int w = 0; w < kThreads / 32; ++w) t += sh[w];
     sh[0] = t;
   }
-  __syncthreads();
+  csync<BAR>();
   t = sh[0];
-  __syncthreads();
+  csync<BAR>();
   return t;
 }
+
+// ---- named barrier among the first `nthreads` threads (consumer warps of a
+// warp-specialised CTA; the producer warp never joins)
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---- mbarrier + 1D TMA bulk copy (cp.async.bulk, SASS UBLKCP) ------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy; completes `bytes` of transaction count on `bar`.
+// src, dst 16-byte aligned, bytes a multiple of 16.  L2 evict-first: read once.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 
 // "Last CTA of a segment" election: every CTA calls this after its global
 // writes; returns true in exactly one CTA (the last to arrive).

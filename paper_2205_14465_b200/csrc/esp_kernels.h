@@ -24,7 +24,9 @@ void launch_sign_h1(int kind, const SegH1* segs, const uint32_t* unit_seg, int n
 void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 
 // h2 (k_h2.cu)
-void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles,
+// piece_seg: segment of every piece (npieces_total entries)
+void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint32_t* piece_seg,
+                      int npieces_total,
                       const unsigned char* const* pieces, cudaStream_t st);
 void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
                     const unsigned char* const* pieces, cudaStream_t st);

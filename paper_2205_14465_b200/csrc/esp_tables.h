@@ -12,8 +12,8 @@ namespace esp {
 constexpr int kThreads = 256;
 constexpr int kRun = 1024;
 constexpr int kUnit = 8192;              // 8 runs per CTA
-constexpr int kRunsPerGroup = 16;        // DGC finalize: 16 runs per CTA
-constexpr int kSample = 8192;            // DGC sampled-threshold sample size
+constexpr int kRunsPerGroup = 64;        // DGC finalize: 64 runs (65536 elements) per CTA
+constexpr int kSample = 4096;            // DGC sampled-threshold sample size
 constexpr int kTile = 8192;              // sparse h2 output tile (32 KB smem)
 
 enum Kind : int { K_NONE = 0, K_RANDOMK = 1, K_DGC = 2, K_TOPK = 3, K_EFSIGN = 4, K_ONEBIT = 5 };
@@ -62,7 +62,8 @@ struct SegH1 {
   uint32_t* runcnt;      // candidates per run
   uint32_t* hist;        // 2048 (pass) + 2048 (fallback) + 1024 + 1024
   SelState* st;
-  uint32_t* gcnt;        // 4 * ngroups: above, tie, tie_off, sel_off
+  uint32_t* bflag;       // bucket-wide "some segment fell back" counter (zeroed every call)
+  uint32_t* gcnt;        // look-back status, one uint64 per group (zeroed every call)
   double* partial;       // sign: 2 doubles per unit
   uint32_t* pcount;      // sign: 2 counts per unit (onebit) ; [0] of seg = done counter
   // a7 (mid-scheme) input: decode-mean of npieces chunks instead of g
@@ -87,6 +88,7 @@ struct SegH2 {
   uint32_t unit0;        // first unit/tile
   uint32_t nunits;
   float divisor;         // n for MEAN, 1 for SUM or already-averaged data
+  uint32_t* toff;        // sparse: per piece, nunits + 1 tile start offsets (h2_sparse_offsets)
 };
 
 __device__ __forceinline__ const float* seg_g(const SegH1& s) {

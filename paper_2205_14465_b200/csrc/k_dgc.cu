@@ -3,21 +3,24 @@
 // P:828 and evaluated at a 1% rate; EF at P:1427).
 //
 // Pipeline per bucket (every kernel walks a multi-segment table):
-//   1. dgc_sample   one CTA per segment: thr = the j*-th largest key of a hashed
-//                   stratified sample of acc = g + r (exact k-th key when the
-//                   segment fits the sample).  Only an accelerator: the result
-//                   cannot depend on thr (reading R3).
-//   2. dgc_stream   ONE pass over g and r (12 B/elem): r := acc; candidates
-//                   key(acc) >= thr are compacted per warp-run in index order
-//                   (ballot/popc); 2048-bin histogram of candidate keys.
-//                   The last CTA of a segment picks the radix bin of the k-th key.
-//   3. dgc_stream   (fallback mode) only for segments with < k candidates:
-//                   recompact with thr = 0 from r.  Adversarial inputs only.
-//   4. dgc_refine   two more radix rounds over the candidates -> exact k-th key T,
-//                   #above, #ties to take (ties broken by ascending index).
-//   5. dgc_count    per group of runs: #above, #ties; last CTA scans offsets.
-//   6. dgc_write    ordered selection -> payload idx[]/val[] sorted by index;
-//                   EF: r[idx] := 0.
+//   1. dgc_sample   one CTA per segment: thr = lower edge of the 21-bit radix bin
+//                   holding the j*-th largest key of a hashed stratified sample of
+//                   acc = g + r (the k-th key's bin when the whole segment fits the
+//                   sample).  Only an accelerator: the result cannot depend on thr
+//                   (reading R3); too high a threshold triggers the fallback.
+//   2. dgc_stream   ONE persistent, warp-specialised pass over g and r (12 B/elem):
+//                   a producer warp streams 32 KB tiles of g and r into a 3-stage
+//                   shared-memory ring with 1D TMA bulk copies (cp.async.bulk +
+//                   mbarrier); 8 consumer warps compute acc = g + r, write r := acc,
+//                   compact candidates key(acc) >= thr per 1024-element run in index
+//                   order (ballot/popc) and histogram their top 11 key bits.  The
+//                   CTA that completes a segment picks the radix bin of the k-th key.
+//   3. dgc_fallback only segments with < k candidates: recompact with thr = 0.
+//   4. dgc_refine   two more radix rounds over the candidates -> the exact k-th key
+//                   T, #above, #ties to take (ties broken by ascending index).
+//   5. dgc_write    per group of runs: count, decoupled look-back for the group's
+//                   output offset, ordered selection -> payload idx[]/val[] sorted
+//                   by index; EF: r[idx] := 0.
 #include <cmath>
 
 #include "esp_device.cuh"
@@ -25,31 +28,34 @@
 
 namespace esp {
 
-// CTA-wide: given a histogram in global memory, find bin b (scanning from the
-// top) with above(b) < need <= above(b) + hist[b].  nbins in {1024, 2048}.
+constexpr int kStages = 3;
+
+// CTA-wide (256 threads): find bin b (scanning from the top) with
+// above(b) < need <= above(b) + hist[b].  nbins in {1024, 2048}.  GLOBAL: the
+// histogram lives in global memory and was built by other CTAs' atomics.
+template <int BAR, bool GLOBAL>
 __device__ void select_bin(const uint32_t* hist, int nbins, uint32_t need, uint32_t* out_bin,
-                           uint32_t* out_above, uint32_t* sh /* >= 256+16 */) {
+                           uint32_t* out_above, uint32_t* sh /* >= 270 */) {
   const int per = nbins / kThreads;
   const int t = threadIdx.x;
   uint32_t local[8];
   uint32_t sum = 0;
   for (int i = 0; i < per; ++i) {
-    local[i] = __ldcg(hist + t * per + i);
+    local[i] = GLOBAL ? __ldcg(hist + t * per + i) : hist[t * per + i];
     sum += local[i];
   }
-  // suffix sums: thread t gets sum over threads > t
-  uint32_t* sh_sum = sh;       // 256
-  uint32_t* sh_res = sh + 256; // bin, above
+  uint32_t* sh_sum = sh;        // 256
+  uint32_t* sh_res = sh + 256;  // bin, above
   sh_sum[t] = sum;
-  __syncthreads();
-  uint32_t v = sh_sum[kThreads - 1 - t];
-  __syncthreads();
+  csync<BAR>();
+  const uint32_t v = sh_sum[kThreads - 1 - t];
+  csync<BAR>();
   uint32_t tot;
-  uint32_t excl = block_excl_scan(v, &tot, sh + 258);
-  // excl over reversed order = sum of threads > (255 - t)
+  const uint32_t excl = block_excl_scan<BAR>(v, &tot, sh + 258);   // sum over threads > (255 - t)
   sh_sum[kThreads - 1 - t] = excl;
-  __syncthreads();
-  uint32_t above = sh_sum[t];
+  if (t == 0) { sh_res[0] = 0; sh_res[1] = 0; }
+  csync<BAR>();
+  const uint32_t above = sh_sum[t];
   if (above < need && need <= above + sum) {
     uint32_t cum = above;
     for (int i = per - 1; i >= 0; --i) {
@@ -61,168 +67,350 @@ __device__ void select_bin(const uint32_t* hist, int nbins, uint32_t need, uint3
       cum += local[i];
     }
   }
-  __syncthreads();
+  csync<BAR>();
   *out_bin = sh_res[0];
   *out_above = sh_res[1];
-  __syncthreads();
+  csync<BAR>();
 }
 
 // ------------------------------------------------------------------ 1. sample
-__global__ void __launch_bounds__(1024) dgc_sample_kernel(const SegH1* __restrict__ segs) {
+__global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __restrict__ segs) {
   __shared__ uint32_t keys[kSample];
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t sh[280];
   const SegH1 S = segs[blockIdx.x];
   const uint32_t n = S.n;
   const float* g = seg_g(S);
   const bool exact = n <= (uint32_t)kSample;
   const uint32_t s = exact ? n : (uint32_t)kSample;
-  uint32_t p2 = 1;
-  while (p2 < s) p2 <<= 1;
-  for (uint32_t j = threadIdx.x; j < p2; j += blockDim.x) {
-    uint32_t key = 0;
-    if (j < s) {
-      uint32_t pos;
-      if (exact) {
-        pos = j;
-      } else {
-        uint64_t a = (uint64_t)j * n / s, b = (uint64_t)(j + 1) * n / s;
+  {
+    // all 2 x 16 loads of a thread are issued before any is consumed (latency-bound kernel)
+    constexpr int kPer = kSample / kThreads;
+    float gv[kPer], rv[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const uint32_t j = threadIdx.x + q * kThreads;
+      uint32_t pos = j;
+      if (!exact && j < s) {
+        const uint64_t a = (uint64_t)j * n / s, b = (uint64_t)(j + 1) * n / s;
         pos = (uint32_t)(a + splitmix64(S.hash ^ j) % (b - a));
       }
-      float acc = S.ef ? __fadd_rn(g[pos], S.r[pos]) : g[pos];
-      key = fkey(acc);
+      gv[q] = j < s ? __ldg(g + pos) : 0.f;
+      rv[q] = (j < s && S.ef) ? S.r[pos] : 0.f;
     }
-    keys[j] = key;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const uint32_t j = threadIdx.x + q * kThreads;
+      if (j < s) keys[j] = fkey(S.ef ? __fadd_rn(gv[q], rv[q]) : gv[q]);
+    }
   }
+  for (int i = threadIdx.x; i < 2048; i += kThreads) hist[i] = 0;
   __syncthreads();
-  // bitonic sort, descending
-  for (uint32_t size = 2; size <= p2; size <<= 1) {
-    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-      for (uint32_t i = threadIdx.x; i < p2 / 2; i += blockDim.x) {
-        uint32_t lo = 2 * i - (i & (stride - 1));
-        uint32_t hi = lo + stride;
-        bool desc = ((lo & size) == 0);
-        uint32_t a = keys[lo], b = keys[hi];
-        if ((a < b) == desc) { keys[lo] = b; keys[hi] = a; }
+  for (uint32_t j = threadIdx.x; j < s; j += kThreads) atomicAdd(&hist[keys[j] >> 20], 1u);
+  __syncthreads();
+  uint32_t need;
+  if (exact) {
+    need = S.k;
+  } else {
+    const double rs = S.ratio * (double)s;
+    const double js = ceil(rs + 4.0 * sqrt(rs));
+    need = js >= (double)s ? s : (uint32_t)js;
+    if (need < 1) need = 1;
+  }
+  uint32_t b1, a1, b2, a2;
+  select_bin<0, false>(hist, 2048, need, &b1, &a1, sh);
+  for (int i = threadIdx.x; i < 1024; i += kThreads) hist[i] = 0;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < s; j += kThreads)
+    if ((keys[j] >> 20) == b1) atomicAdd(&hist[(keys[j] >> 10) & 1023u], 1u);
+  __syncthreads();
+  select_bin<0, false>(hist, 1024, need - a1, &b2, &a2, sh);
+  if (threadIdx.x == 0) S.st->thr = (b1 << 20) | (b2 << 10);
+}
+
+// ------------------------------------------------------------------ candidate emission
+// One warp, one 1024-element run held in registers (8 float4 per lane; element
+// base + j*128 + lane*4 + c).  Appends {idx, bits(acc)} of key >= thr in index
+// order and histograms the candidates' top 11 key bits.  Returns the count.
+__device__ __forceinline__ uint32_t emit_run(const float4 (&av)[8], uint32_t base, uint32_t n, uint32_t thr,
+                                             uint2* __restrict__ cand, uint32_t* hist) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t wcount = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t e = base + j * 128 + lane * 4;
+    uint32_t f[4], bal[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      f[c] = (e + c < n) && (fkey(f4get(av[j], c)) >= thr);
+      bal[c] = __ballot_sync(0xffffffffu, f[c]);
+    }
+    if ((bal[0] | bal[1] | bal[2] | bal[3]) == 0) continue;
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      pre += __popc(bal[c] & lt_mask);
+      tot += __popc(bal[c]);
+    }
+    uint32_t pos = wcount + pre;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (f[c]) {
+        const float x = f4get(av[j], c);
+        cand[pos] = make_uint2(e + c, __float_as_uint(x));
+        atomicAdd(&hist[fkey(x) >> 20], 1u);
+        ++pos;
       }
-      __syncthreads();
+    }
+    wcount += tot;
+  }
+  return wcount;
+}
+
+// ------------------------------------------------------------------ 2. stream (TMA)
+struct StreamSmem {
+  float g[kStages][kUnit];
+  float r[kStages][kUnit];
+  uint32_t hist[2048];
+  uint64_t full[kStages], empty[kStages];
+  uint32_t scan[280];
+  uint32_t cta_count;
+  int flag;
+};
+
+// segment bookkeeping by the 256 consumer threads of a CTA that has finished its
+// share (`units` units) of segment S: flush the private histogram, add the
+// candidate count, and if this completes the segment pick the k-th key's bin.
+__device__ void stream_segment_done(const SegH1& S, uint32_t units, StreamSmem& sm) {
+  csync<1>();
+  for (int i = threadIdx.x; i < 2048; i += kThreads) {
+    const uint32_t h = sm.hist[i];
+    if (h) {
+      atomicAdd(&S.hist[i], h);
+      sm.hist[i] = 0;
     }
   }
   if (threadIdx.x == 0) {
-    uint32_t jstar;
-    if (exact) {
-      jstar = S.k;
-    } else {
-      double rs = S.ratio * (double)s;
-      double js = ceil(rs + 4.0 * sqrt(rs));
-      jstar = js >= (double)s ? s : (uint32_t)js;
-      if (jstar < 1) jstar = 1;
-    }
-    S.st->thr = keys[jstar - 1];
+    if (sm.cta_count) atomicAdd(&S.st->count, sm.cta_count);
+    sm.cta_count = 0;
+    __threadfence();
+    const uint32_t old = atomicAdd(&S.st->done, units);
+    sm.flag = (old + units == S.nunits);
   }
-}
-
-// ------------------------------------------------------------------ 2/3. stream
-template <bool FALLBACK>
-__global__ void __launch_bounds__(kThreads) dgc_stream_kernel(const SegH1* __restrict__ segs,
-                                                              const uint32_t* __restrict__ unit_seg) {
-  __shared__ uint32_t sh_hist[2048];
-  __shared__ uint32_t sh_scan[300];
-  __shared__ uint32_t sh_total;
-  __shared__ int sh_flag;
-  const uint32_t sid = unit_seg[blockIdx.x];
-  const SegH1 S = segs[sid];
-  if (FALLBACK && *(volatile uint32_t*)&S.st->fallback == 0) return;
-  const uint32_t u = blockIdx.x - S.unit0;
-  const uint32_t n = S.n;
-  for (int i = threadIdx.x; i < 2048; i += kThreads) sh_hist[i] = 0;
-  if (threadIdx.x == 0) sh_total = 0;
-  __syncthreads();
-  const uint32_t thr = FALLBACK ? 0u : S.st->thr;
-  const float* g = seg_g(S);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t run = u * (kUnit / kRun) + warp;
-  const uint32_t base = run * kRun;
-  uint32_t wcount = 0;
-  if (base < n) {
-    float4 av[8];
-    if (FALLBACK) {
-      const float* src = S.ef ? S.r : g;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) av[j] = load4_guard(src, base + j * 128 + lane * 4, n);
-    } else {
-      float4 gv[8], rv[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) gv[j] = load4_stream_guard(g, base + j * 128 + lane * 4, n);
-      if (S.ef) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) rv[j] = load4_guard(S.r, base + j * 128 + lane * 4, n);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          av[j].x = __fadd_rn(gv[j].x, rv[j].x);
-          av[j].y = __fadd_rn(gv[j].y, rv[j].y);
-          av[j].z = __fadd_rn(gv[j].z, rv[j].z);
-          av[j].w = __fadd_rn(gv[j].w, rv[j].w);
-          store4_guard(S.r, base + j * 128 + lane * 4, n, av[j]);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) av[j] = gv[j];
-      }
+  csync<1>();
+  if (!sm.flag) return;
+  __threadfence();
+  const uint32_t total = __ldcg(&S.st->count);
+  if (total < S.k) {
+    if (threadIdx.x == 0) {
+      S.st->fallback = 1;
+      atomicAdd(S.bflag, 1u);
     }
-    uint2* cand = S.cand + (size_t)run * kRun;
-    const uint32_t lt_mask = (1u << lane) - 1u;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t e = base + j * 128 + lane * 4;
-      uint32_t f[4], bal[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float x = f4get(av[j], c);
-        f[c] = (e + c < n) && (fkey(x) >= thr);
-        bal[c] = __ballot_sync(0xffffffffu, f[c]);
-      }
-      uint32_t pre = 0, tot = 0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        pre += __popc(bal[c] & lt_mask);
-        tot += __popc(bal[c]);
-      }
-      uint32_t pos = wcount + pre;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (f[c]) {
-          float x = f4get(av[j], c);
-          cand[pos] = make_uint2(e + c, __float_as_uint(x));
-          atomicAdd(&sh_hist[fkey(x) >> 20], 1u);
-          ++pos;
-        }
-      }
-      wcount += tot;
-    }
-    if (lane == 0) {
-      S.runcnt[run] = wcount;
-      atomicAdd(&sh_total, wcount);
-    }
-  }
-  __syncthreads();
-  uint32_t* ghist = S.hist + (FALLBACK ? 2048 : 0);
-  for (int i = threadIdx.x; i < 2048; i += kThreads) {
-    uint32_t h = sh_hist[i];
-    if (h) atomicAdd(&ghist[i], h);
-  }
-  uint32_t* gcount = FALLBACK ? &S.st->count_fb : &S.st->count;
-  if (threadIdx.x == 0 && sh_total) atomicAdd(gcount, sh_total);
-  if (!last_cta(FALLBACK ? &S.st->done_fb : &S.st->done, S.nunits, &sh_flag)) return;
-  const uint32_t total = __ldcg(gcount);
-  if (!FALLBACK && total < S.k) {
-    if (threadIdx.x == 0) S.st->fallback = 1;
+    csync<1>();
     return;
   }
   uint32_t bin, above;
-  select_bin(ghist, 2048, S.k, &bin, &above, sh_scan);
+  select_bin<1, true>(S.hist, 2048, S.k, &bin, &above, sm.scan);
   if (threadIdx.x == 0) {
     S.st->prefix = bin;
     S.st->above = above;
     S.st->need = S.k - above;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads + 32, 1) dgc_stream_kernel(const SegH1* __restrict__ segs,
+                                                                      const uint32_t* __restrict__ unit_seg,
+                                                                      uint32_t nunits) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t u0 = (uint32_t)((uint64_t)blockIdx.x * nunits / gridDim.x);
+  const uint32_t u1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nunits / gridDim.x);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kThreads / 32);
+    }
+    fence_barrier_init();
+    sm.cta_count = 0;
+  }
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) sm.hist[i] = 0;
+  __syncthreads();
+
+  if (warp == kThreads / 32) {
+    // ---- producer warp: one elected lane streams tiles into the ring
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      // per-segment values are cached; the unit table is prefetched one ahead
+      uint32_t cur = 0xFFFFFFFFu, unit0 = 0, n = 0;
+      const float* gseg = nullptr;
+      const float* rseg = nullptr;
+      bool ef = false;
+      uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
+      for (uint32_t u = u0, i = 0; u < u1; ++u, ++i) {
+        const uint32_t sid = sid_next;
+        if (u + 1 < u1) sid_next = unit_seg[u + 1];
+        if (sid != cur) {
+          const SegH1& S = segs[sid];
+          cur = sid;
+          unit0 = S.unit0;
+          n = S.n;
+          gseg = seg_g(S);
+          rseg = S.r;
+          ef = S.ef != 0;
+        }
+        const int stage = i % kStages;
+        const uint32_t round = i / kStages;
+        if (round > 0) mbar_wait(&sm.empty[stage], (round - 1) & 1);
+        const uint32_t start = (u - unit0) * kUnit;
+        const uint32_t len = min((uint32_t)kUnit, n - start);
+        const float* g = gseg + start;
+        const float* r = rseg + start;
+        const uint32_t bytes = (len * 4) & ~15u;
+        if (bytes && al16(g) && (!ef || al16(r))) {
+          mbar_arrive_expect_tx(&sm.full[stage], bytes * (ef ? 2 : 1));
+          tma_load_1d(sm.g[stage], g, bytes, &sm.full[stage], pol);
+          if (ef) tma_load_1d(sm.r[stage], r, bytes, &sm.full[stage], pol);
+        } else {
+          mbar_arrive(&sm.full[stage]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- 8 consumer warps
+  uint32_t cur = 0xFFFFFFFFu, cur_units = 0, thr = 0;
+  const float* g = nullptr;
+  SegH1 S{};
+  uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
+  for (uint32_t u = u0, i = 0; u < u1; ++u, ++i) {
+    const int stage = i % kStages;
+    const uint32_t round = i / kStages;
+    const uint32_t sid = sid_next;
+    if (u + 1 < u1) sid_next = unit_seg[u + 1];
+    if (sid != cur) {
+      if (cur != 0xFFFFFFFFu) stream_segment_done(S, cur_units, sm);
+      cur = sid;
+      S = segs[sid];
+      g = seg_g(S);
+      thr = __ldcg(&S.st->thr);
+      cur_units = 0;
+    }
+    ++cur_units;
+    const uint32_t start = (u - S.unit0) * kUnit;
+    const uint32_t n = S.n;
+    const uint32_t len = min((uint32_t)kUnit, n - start);
+    const uint32_t bytes = (len * 4) & ~15u;
+    const bool tma = bytes && al16(g + start) && (!S.ef || al16(S.r + start));
+    mbar_wait(&sm.full[stage], round & 1);
+    const uint32_t lbase = warp * kRun;            // tile-relative
+    const uint32_t base = start + lbase;           // segment-relative
+    float4 av[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t l = lbase + j * 128 + lane * 4;
+      const uint32_t e = start + l;
+      float4 gv, rv;
+      if (tma && l + 4 <= bytes / 4) {
+        gv = lds4(&sm.g[stage][l]);
+        rv = S.ef ? lds4(&sm.r[stage][l]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        gv = load4_guard(g, e, n);
+        rv = S.ef ? load4_guard(S.r, e, n) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (S.ef) {
+        av[j].x = __fadd_rn(gv.x, rv.x);
+        av[j].y = __fadd_rn(gv.y, rv.y);
+        av[j].z = __fadd_rn(gv.z, rv.z);
+        av[j].w = __fadd_rn(gv.w, rv.w);
+      } else {
+        av[j] = gv;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[stage]);   // stage consumed (values in registers)
+    if (base < n) {
+      if (S.ef) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) store4_guard(S.r, base + j * 128 + lane * 4, n, av[j]);
+      }
+      const uint32_t run = base / kRun;
+      const uint32_t wc = emit_run(av, base, n, thr, S.cand + (size_t)run * kRun, sm.hist);
+      if (lane == 0) {
+        S.runcnt[run] = wc;
+        if (wc) atomicAdd(&sm.cta_count, wc);
+      }
+    }
+  }
+  if (cur != 0xFFFFFFFFu) stream_segment_done(S, cur_units, sm);
+}
+
+// ------------------------------------------------------------------ 3. fallback
+// Segments whose sampled threshold let fewer than k candidates through are
+// recompacted from acc (= r after the streaming pass) with thr = 0.  Every CTA
+// scans the segment list; only flagged segments cost work.
+__global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __restrict__ segs, int nsegs) {
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t sh[280];
+  __shared__ uint32_t cta_count;
+  __shared__ int flag;
+  __shared__ uint32_t list[256];
+  __shared__ uint32_t nlist;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (__ldcg(segs[0].bflag) == 0) return;   // no segment of this bucket fell back
+  for (int s0 = 0; s0 < nsegs; s0 += kThreads) {
+    if (threadIdx.x == 0) nlist = 0;
+    __syncthreads();
+    if (s0 + threadIdx.x < nsegs && __ldcg(&segs[s0 + threadIdx.x].st->fallback))
+      list[atomicAdd(&nlist, 1u)] = s0 + threadIdx.x;
+    __syncthreads();
+    const uint32_t cnt = nlist;
+    for (uint32_t li = 0; li < cnt; ++li) {
+    const uint32_t sid = list[li];
+    const SegH1 S = segs[sid];
+    if (blockIdx.x >= S.nunits) continue;
+    for (int i = threadIdx.x; i < 2048; i += kThreads) hist[i] = 0;
+    if (threadIdx.x == 0) cta_count = 0;
+    __syncthreads();
+    uint32_t units = 0;
+    const float* src = S.ef ? S.r : seg_g(S);
+    for (uint32_t u = blockIdx.x; u < S.nunits; u += gridDim.x, ++units) {
+      const uint32_t base = u * kUnit + warp * kRun;
+      if (base >= S.n) continue;
+      float4 av[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) av[j] = load4_guard(src, base + j * 128 + lane * 4, S.n);
+      const uint32_t run = base / kRun;
+      const uint32_t wc = emit_run(av, base, S.n, 0u, S.cand + (size_t)run * kRun, hist);
+      if (lane == 0) {
+        S.runcnt[run] = wc;
+        atomicAdd(&cta_count, wc);
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2048; i += kThreads)
+      if (hist[i]) atomicAdd(&S.hist[2048 + i], hist[i]);
+    if (threadIdx.x == 0) {
+      atomicAdd(&S.st->count_fb, cta_count);
+      __threadfence();
+      const uint32_t old = atomicAdd(&S.st->done_fb, units);
+      flag = (old + units == S.nunits);
+    }
+    __syncthreads();
+    if (flag) {
+      __threadfence();
+      uint32_t bin, above;
+      select_bin<0, true>(S.hist + 2048, 2048, S.k, &bin, &above, sh);
+      if (threadIdx.x == 0) {
+        S.st->prefix = bin;
+        S.st->above = above;
+        S.st->need = S.k - above;
+      }
+    }
+    __syncthreads();
+    }
   }
 }
 
@@ -231,7 +419,7 @@ template <int ROUND>
 __global__ void __launch_bounds__(kThreads) dgc_refine_kernel(const SegH1* __restrict__ segs,
                                                               const uint32_t* __restrict__ group_seg) {
   __shared__ uint32_t sh_hist[1024];
-  __shared__ uint32_t sh_scan[300];
+  __shared__ uint32_t sh_scan[280];
   __shared__ int sh_flag;
   constexpr int kShiftMatch = ROUND == 2 ? 20 : 10;
   constexpr int kShiftBin = ROUND == 2 ? 10 : 0;
@@ -249,20 +437,20 @@ __global__ void __launch_bounds__(kThreads) dgc_refine_kernel(const SegH1* __res
     const uint32_t cnt = __ldcg(S.runcnt + run);
     const uint2* cand = S.cand + (size_t)run * kRun;
     for (uint32_t i = lane; i < cnt; i += 32) {
-      uint32_t key = __ldcg(&cand[i].y) & 0x7FFFFFFFu;
+      const uint32_t key = __ldcg(&cand[i].y) & 0x7FFFFFFFu;
       if ((key >> kShiftMatch) == prefix) atomicAdd(&sh_hist[(key >> kShiftBin) & 1023u], 1u);
     }
   }
   __syncthreads();
   uint32_t* ghist = S.hist + (ROUND == 2 ? 4096 : 5120);
   for (int i = threadIdx.x; i < 1024; i += kThreads) {
-    uint32_t h = sh_hist[i];
+    const uint32_t h = sh_hist[i];
     if (h) atomicAdd(&ghist[i], h);
   }
   if (!last_cta(ROUND == 2 ? &S.st->done_r2 : &S.st->done_r3, S.ngroups, &sh_flag)) return;
   const uint32_t need = __ldcg(&S.st->need);
   uint32_t bin, above;
-  select_bin(ghist, 1024, need, &bin, &above, sh_scan);
+  select_bin<0, true>(ghist, 1024, need, &bin, &above, sh_scan);
   if (threadIdx.x == 0) {
     S.st->prefix = (prefix << 10) | bin;
     S.st->above = __ldcg(&S.st->above) + above;
@@ -270,66 +458,18 @@ __global__ void __launch_bounds__(kThreads) dgc_refine_kernel(const SegH1* __res
   }
 }
 
-// ------------------------------------------------------------------ 5. count
-__global__ void __launch_bounds__(kThreads) dgc_count_kernel(const SegH1* __restrict__ segs,
-                                                             const uint32_t* __restrict__ group_seg) {
-  __shared__ uint32_t sh_scan[16];
-  __shared__ int sh_flag;
-  const uint32_t sid = group_seg[blockIdx.x];
-  const SegH1 S = segs[sid];
-  const uint32_t g = blockIdx.x - S.group0;
-  const uint32_t T = __ldcg(&S.st->prefix);
-  const uint32_t nruns = (S.n + kRun - 1) / kRun;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t above = 0, tie = 0;
-  for (uint32_t rr = warp; rr < (uint32_t)kRunsPerGroup; rr += kThreads / 32) {
-    const uint32_t run = g * kRunsPerGroup + rr;
-    if (run >= nruns) break;
-    const uint32_t cnt = __ldcg(S.runcnt + run);
-    const uint2* cand = S.cand + (size_t)run * kRun;
-    for (uint32_t i = lane; i < cnt; i += 32) {
-      uint32_t key = __ldcg(&cand[i].y) & 0x7FFFFFFFu;
-      above += key > T;
-      tie += key == T;
-    }
-  }
-  above = block_sum_u32(above, sh_scan);
-  tie = block_sum_u32(tie, sh_scan);
-  if (threadIdx.x == 0) {
-    S.gcnt[4 * g + 0] = above;
-    S.gcnt[4 * g + 1] = tie;
-  }
-  if (!last_cta(&S.st->done_cnt, S.ngroups, &sh_flag)) return;
-  // scan over this segment's groups: tie offsets, then selected offsets
-  const uint32_t need = __ldcg(&S.st->need);
-  uint32_t tie_carry = 0, sel_carry = 0;
-  for (uint32_t g0 = 0; g0 < S.ngroups; g0 += kThreads) {
-    const uint32_t gi = g0 + threadIdx.x;
-    uint32_t a = 0, t = 0;
-    if (gi < S.ngroups) {
-      a = __ldcg(&S.gcnt[4 * gi + 0]);
-      t = __ldcg(&S.gcnt[4 * gi + 1]);
-    }
-    uint32_t ttot, stot;
-    uint32_t toff = tie_carry + block_excl_scan(t, &ttot, sh_scan);
-    uint32_t take = toff >= need ? 0u : min(t, need - toff);
-    uint32_t sel = a + take;
-    uint32_t soff = sel_carry + block_excl_scan(sel, &stot, sh_scan);
-    if (gi < S.ngroups) {
-      S.gcnt[4 * gi + 2] = toff;
-      S.gcnt[4 * gi + 3] = soff;
-    }
-    tie_carry += ttot;
-    sel_carry += stot;
-  }
-  if (threadIdx.x == 0) S.st->total_sel = sel_carry;
+// ------------------------------------------------------------------ 5. write
+// Look-back status word of a group: flag (2 bits: 1 aggregate, 2 inclusive
+// prefix) | #above (31 bits) | #ties (31 bits).
+__device__ __forceinline__ unsigned long long lb_pack(uint32_t flag, uint32_t above, uint32_t tie) {
+  return ((unsigned long long)flag << 62) | ((unsigned long long)above << 31) | tie;
 }
 
-// ------------------------------------------------------------------ 6. write
 __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __restrict__ segs,
                                                              const uint32_t* __restrict__ group_seg) {
   __shared__ uint32_t sh_scan[16];
   __shared__ uint32_t sh_off[kRunsPerGroup + 1];
+  __shared__ uint32_t sh_prefix[2];
   const uint32_t sid = group_seg[blockIdx.x];
   const SegH1 S = segs[sid];
   const uint32_t g = blockIdx.x - S.group0;
@@ -338,18 +478,58 @@ __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __rest
   const uint32_t nruns = (S.n + kRun - 1) / kRun;
   const uint32_t run0 = g * kRunsPerGroup;
   const uint32_t nr = min((uint32_t)kRunsPerGroup, nruns - run0);
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0;
-    for (uint32_t i = 0; i < nr; ++i) {
-      sh_off[i] = acc;
-      acc += __ldcg(S.runcnt + run0 + i);
+  {
+    const uint32_t c = threadIdx.x < nr ? __ldcg(S.runcnt + run0 + threadIdx.x) : 0u;
+    uint32_t tot;
+    const uint32_t off = block_excl_scan(c, &tot, sh_scan);
+    if (threadIdx.x < nr) sh_off[threadIdx.x] = off;
+    if (threadIdx.x == 0) sh_off[nr] = tot;
+    __syncthreads();
+  }
+  const uint32_t C = sh_off[nr];
+  auto cand_at = [&](uint32_t q) -> uint2 {
+    uint32_t lo = 0, hi = nr;   // largest i with sh_off[i] <= q
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (sh_off[mid] <= q) lo = mid; else hi = mid;
     }
-    sh_off[nr] = acc;
+    return __ldcg(S.cand + (size_t)(run0 + lo) * kRun + (q - sh_off[lo]));
+  };
+  // pass 1: the group's aggregate
+  uint32_t above = 0, tie = 0;
+  for (uint32_t q = threadIdx.x; q < C; q += kThreads) {
+    const uint32_t key = cand_at(q).y & 0x7FFFFFFFu;
+    above += key > T;
+    tie += key == T;
+  }
+  above = block_sum_u32(above, sh_scan);
+  tie = block_sum_u32(tie, sh_scan);
+  // decoupled look-back over the segment's groups (blockIdx order = group order)
+  if (threadIdx.x == 0) {
+    unsigned long long* st = reinterpret_cast<unsigned long long*>(S.gcnt);
+    uint32_t ea = 0, et = 0;
+    if (g == 0) {
+      atomicExch(&st[0], lb_pack(2, above, tie));
+    } else {
+      atomicExch(&st[g], lb_pack(1, above, tie));
+      for (int j = (int)g - 1; j >= 0; --j) {
+        unsigned long long v;
+        do {
+          v = atomicAdd(&st[j], 0ull);
+        } while ((v >> 62) == 0);
+        ea += (uint32_t)((v >> 31) & 0x7FFFFFFFu);
+        et += (uint32_t)(v & 0x7FFFFFFFu);
+        if ((v >> 62) == 2) break;
+      }
+      atomicExch(&st[g], lb_pack(2, ea + above, et + tie));
+    }
+    sh_prefix[0] = ea;
+    sh_prefix[1] = et;
   }
   __syncthreads();
-  const uint32_t C = sh_off[nr];
-  uint32_t tie_run = __ldcg(&S.gcnt[4 * g + 2]);
-  uint32_t sel_run = __ldcg(&S.gcnt[4 * g + 3]);
+  // pass 2: ordered selection; selected before this group = above_before + min(ties_before, need)
+  uint32_t tie_run = sh_prefix[1];
+  uint32_t sel_run = sh_prefix[0] + min(sh_prefix[1], need);
   uint32_t* out_idx = reinterpret_cast<uint32_t*>(S.chunk);
   float* out_val = reinterpret_cast<float*>(S.chunk + 4 * (size_t)S.kpad);
   for (uint32_t q0 = 0; q0 < C; q0 += kThreads) {
@@ -357,18 +537,16 @@ __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __rest
     uint32_t is_tie = 0, is_above = 0;
     uint2 c = make_uint2(0, 0);
     if (q < C) {
-      uint32_t i = 0;
-      while (sh_off[i + 1] <= q) ++i;
-      c = __ldcg(S.cand + (size_t)(run0 + i) * kRun + (q - sh_off[i]));
-      uint32_t key = c.y & 0x7FFFFFFFu;
+      c = cand_at(q);
+      const uint32_t key = c.y & 0x7FFFFFFFu;
       is_above = key > T;
       is_tie = key == T;
     }
     uint32_t ttot;
-    uint32_t trank = tie_run + block_excl_scan(is_tie, &ttot, sh_scan);
-    uint32_t sel = is_above || (is_tie && trank < need);
+    const uint32_t trank = tie_run + block_excl_scan(is_tie, &ttot, sh_scan);
+    const uint32_t sel = is_above || (is_tie && trank < need);
     uint32_t stot;
-    uint32_t pos = sel_run + block_excl_scan(sel, &stot, sh_scan);
+    const uint32_t pos = sel_run + block_excl_scan(sel, &stot, sh_scan);
     if (sel) {
       out_idx[pos] = c.x;
       out_val[pos] = __uint_as_float(c.y);
@@ -380,20 +558,29 @@ __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __rest
 }
 
 // ------------------------------------------------------------------ launchers
+static int g_num_sms = 0;
+
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
                    cudaEvent_t probe1) {
   if (nsegs == 0) return;
-  dgc_sample_kernel<<<nsegs, 1024, 0, st>>>(segs);
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(dgc_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(StreamSmem));
+  }
+  dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs);
+  const int grid = nunits < g_num_sms ? nunits : g_num_sms;
   if (probe0) cudaEventRecord(probe0, st);
-  dgc_stream_kernel<false><<<nunits, kThreads, 0, st>>>(segs, unit_seg);
+  dgc_stream_kernel<<<grid, kThreads + 32, sizeof(StreamSmem), st>>>(segs, unit_seg, (uint32_t)nunits);
   if (probe1) cudaEventRecord(probe1, st);
-  dgc_stream_kernel<true><<<nunits, kThreads, 0, st>>>(segs, unit_seg);
+  dgc_fallback_kernel<<<g_num_sms, kThreads, 0, st>>>(segs, nsegs);
   dgc_refine_kernel<2><<<ngroups, kThreads, 0, st>>>(segs, group_seg);
   dgc_refine_kernel<3><<<ngroups, kThreads, 0, st>>>(segs, group_seg);
-  dgc_count_kernel<<<ngroups, kThreads, 0, st>>>(segs, group_seg);
   dgc_write_kernel<<<ngroups, kThreads, 0, st>>>(segs, group_seg);
-  count_launches(7);
+  count_launches(6);
 }
 
 }  // namespace esp

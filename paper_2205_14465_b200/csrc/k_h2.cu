@@ -14,30 +14,29 @@ namespace esp {
 
 constexpr int kMaxPieces = 64;
 
-// first position p in [0, len) with a[p] >= x (len if none); warp-cooperative
-// 32-ary search: ~log32(len) dependent loads instead of log2(len).
-__device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* a, uint32_t len, uint32_t x) {
-  const int lane = threadIdx.x & 31;
-  uint32_t lo = 0, hi = len;   // answer in [lo, hi]
-  while (hi - lo > 32) {
-    const uint32_t span = hi - lo;
-    const uint32_t p = lo + (uint32_t)(((uint64_t)(lane + 1) * span) / 33);
-    const uint32_t v = __ldg(a + p);
-    const uint32_t b = __ballot_sync(0xffffffffu, v >= x);
-    if (b) {
-      const int f = __ffs(b) - 1;
-      const uint32_t pf = __shfl_sync(0xffffffffu, p, f);
-      const uint32_t pprev = __shfl_sync(0xffffffffu, p, f > 0 ? f - 1 : 0);
-      hi = pf;
-      if (f > 0) lo = pprev + 1;
-    } else {
-      lo = __shfl_sync(0xffffffffu, p, 31) + 1;
-    }
+// For every piece (sorted idx[kpad], 0xFFFFFFFF padding), the first entry of
+// each output tile: toff[t] = lower_bound(idx, t * kTile), t = 0..ntiles.  One
+// pass over the (small) pieces replaces a dependent binary search per tile.
+__global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2* __restrict__ segs,
+                                                                     const uint32_t* __restrict__ piece_seg,
+                                                                     const unsigned char* const* __restrict__ pieces) {
+  const uint32_t p = blockIdx.x;
+  const SegH2 S = segs[piece_seg[p]];
+  const uint32_t r = p - S.piece0;
+  const uint32_t ntiles = S.nunits;
+  uint32_t* toff = S.toff + (size_t)r * (ntiles + 1);
+  const uint32_t* idx = reinterpret_cast<const uint32_t*>(pieces[p]);
+  for (uint32_t i = threadIdx.x; i < S.kpad; i += kThreads) {
+    const uint32_t v = __ldg(idx + i);
+    const uint32_t t = v == 0xFFFFFFFFu ? ntiles : min(v / (uint32_t)kTile, ntiles);
+    const uint32_t prev = i == 0 ? 0u : [&] {
+      const uint32_t u = __ldg(idx + i - 1);
+      return (u == 0xFFFFFFFFu ? ntiles : min(u / (uint32_t)kTile, ntiles)) + 1;
+    }();
+    for (uint32_t q = prev; q <= t; ++q) toff[q] = i;   // tiles (tile(i-1), tile(i)] start at i
+    if (i == S.kpad - 1)
+      for (uint32_t q = t + 1; q <= ntiles; ++q) toff[q] = S.kpad;
   }
-  const uint32_t p = lo + lane;
-  const uint32_t v = p < hi ? __ldg(a + p) : 0xFFFFFFFFu;
-  const uint32_t b = __ballot_sync(0xffffffffu, p < hi && v >= x);
-  return b ? lo + (uint32_t)(__ffs(b) - 1) : hi;
 }
 
 __global__ void __launch_bounds__(kThreads) h2_sparse_kernel(const SegH2* __restrict__ segs,
@@ -50,15 +49,13 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_kernel(const SegH2* __rest
   const uint32_t t = blockIdx.x - S.unit0;
   const uint32_t lo = t * kTile;
   const uint32_t hi = min(lo + (uint32_t)kTile, S.n);
+  if (threadIdx.x < S.npieces) {
+    const uint32_t* toff = S.toff + (size_t)threadIdx.x * (S.nunits + 1);
+    rlo[threadIdx.x] = __ldg(toff + t);
+    rhi[threadIdx.x] = __ldg(toff + t + 1);
+  }
   for (int i = threadIdx.x; i < kTile / 4; i += kThreads)
     reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t r = warp; r < S.npieces; r += kThreads / 32) {
-    const uint32_t* idx = reinterpret_cast<const uint32_t*>(pieces[S.piece0 + r]);
-    const uint32_t a = warp_lower_bound(idx, S.kpad, lo);
-    const uint32_t b = warp_lower_bound(idx, S.kpad, hi);
-    if (lane == 0) { rlo[r] = a; rhi[r] = b; }
-  }
   __syncthreads();
   for (uint32_t r = 0; r < S.npieces; ++r) {
     const unsigned char* pc = pieces[S.piece0 + r];
@@ -169,11 +166,12 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const SegH1* __restrict_
   }
 }
 
-void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles,
-                      const unsigned char* const* pieces, cudaStream_t st) {
+void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint32_t* piece_seg,
+                      int npieces_total, const unsigned char* const* pieces, cudaStream_t st) {
   if (ntiles == 0) return;
+  h2_sparse_offsets_kernel<<<npieces_total, kThreads, 0, st>>>(segs, piece_seg, pieces);
   h2_sparse_kernel<<<ntiles, kThreads, 0, st>>>(segs, tile_seg, pieces);
-  count_launches(1);
+  count_launches(2);
 }
 
 void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,

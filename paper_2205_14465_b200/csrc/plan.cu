@@ -33,6 +33,7 @@ struct Bucket {
   uint32_t* h2_units = nullptr; int nh2_units = 0;
   const unsigned char** h2_pieces = nullptr;
   uint32_t* h2_rankterms = nullptr;
+  uint32_t* h2_piece_seg = nullptr; int nh2_pieces = 0;
   cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
@@ -77,7 +78,7 @@ struct HostTables {
   std::vector<uint32_t> h1_units, h1_groups, a7_units, h2_units;
   std::vector<SegH2> h2;
   std::vector<const unsigned char*> a7_pieces, h2_pieces;
-  std::vector<uint32_t> rankterms;
+  std::vector<uint32_t> rankterms, piece_seg;
 };
 
 static void fill_unit_table(std::vector<uint32_t>& units, uint32_t seg, uint32_t count) {
@@ -85,7 +86,7 @@ static void fill_unit_table(std::vector<uint32_t>& units, uint32_t seg, uint32_t
 }
 
 static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st, size_t& st_cursor,
-                         size_t& hist_cursor) {
+                         size_t& hist_cursor, uint32_t* bflag) {
   Plan& p = L.p;
   esp_world_s* w = p.w;
   const int n = w->nranks, nl = w->nlocal;
@@ -179,12 +180,13 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         size_t st_off = zero_off_st + st_cursor * sizeof(SelState);
         ++st_cursor;
         s.st = L.ptr<SelState>(st_off);
+        s.bflag = bflag;
         if (dgc) {
           s.cand = L.ptr<uint2>(L.reserve((size_t)nruns * kRun * sizeof(uint2)));
           s.runcnt = L.ptr<uint32_t>(L.reserve((size_t)nruns * 4));
-          s.gcnt = L.ptr<uint32_t>(L.reserve((size_t)s.ngroups * 16));
+          s.gcnt = L.commit ? reinterpret_cast<uint32_t*>(p.zero + hist_cursor + 6144 * 4) : nullptr;
           s.hist = L.commit ? reinterpret_cast<uint32_t*>(p.zero + hist_cursor) : nullptr;
-          hist_cursor += 6144 * 4;
+          hist_cursor += 6144 * 4 + round_up((size_t)s.ngroups * 8, 256);
         }
         if (quant) {
           s.partial = L.ptr<double>(L.reserve((size_t)nunits * 16));
@@ -342,6 +344,10 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.nunits = div_up(len, tiles ? kTile : kUnit);
         s.unit0 = u0;
         u0 += s.nunits;
+        if (tiles) {
+          s.toff = L.ptr<uint32_t>(L.reserve((size_t)s.npieces * (s.nunits + 1) * 4));
+          for (uint32_t r = 0; r < s.npieces; ++r) T.piece_seg.push_back((uint32_t)(T.h2.size() - h2_first));
+        }
         T.h2.push_back(s);
         fill_unit_table(T.h2_units, (uint32_t)(T.h2.size() - 1 - h2_first), s.nunits);
       }
@@ -373,22 +379,30 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     for (int t : b.tens) {
       esp_ctx_s* c = p.ctxs[t];
       int segs = 0;
-      for (int part = 0; part < (b.kind == ESP_NONE ? 1 : c->P); ++part)
-        if (b.kind == ESP_NONE ? c->N > 0 : c->phi[part] > c->plo[part]) ++segs;
+      for (int part = 0; part < (b.kind == ESP_NONE ? 1 : c->P); ++part) {
+        const uint64_t len = b.kind == ESP_NONE ? c->N : c->phi[part] - c->plo[part];
+        if (!len) continue;
+        ++segs;
+        // DGC: histograms (6144 u32) + look-back status (one u64 per group of runs)
+        if (dgc)
+          nhist += (6144 * 4 + round_up((size_t)div_up(div_up(len, kRun), kRunsPerGroup) * 8, 256)) *
+                   p.w->nlocal;
+      }
       nst += (size_t)segs * p.w->nlocal;
-      if (dgc) nhist += (size_t)segs * p.w->nlocal;
       if (is_quant(b.kind)) nst += (size_t)p.w->nlocal;   // a7 (upper bound)
     }
   }
   const size_t st_bytes = round_up(nst * sizeof(SelState), 256);
-  p.zero_bytes = st_bytes + nhist * 6144 * 4;
+  const size_t flags_bytes = round_up(p.buckets.size() * 4, 256);
+  p.zero_bytes = flags_bytes + st_bytes + nhist;
   size_t zero_off = L.reserve(p.zero_bytes);
   p.zero = commit ? p.arena.base + zero_off : nullptr;
-  size_t st_cursor = 0, hist_cursor = st_bytes;
+  size_t st_cursor = 0, hist_cursor = flags_bytes + st_bytes;
   T = HostTables{};
   for (auto& b : p.buckets) {
     HostTables TB;
-    build_bucket(L, b, TB, zero_off, st_cursor, hist_cursor);
+    build_bucket(L, b, TB, zero_off + flags_bytes, st_cursor, hist_cursor,
+                 commit ? reinterpret_cast<uint32_t*>(p.zero) + (&b - p.buckets.data()) : nullptr);
     // per-bucket device copies of the tables
     auto up = [&](const auto& vec, auto*& dst) {
       using E = typename std::decay<decltype(vec)>::type::value_type;
@@ -407,6 +421,8 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     up(TB.h2_units, b.h2_units);
     up(TB.h2_pieces, b.h2_pieces);
     up(TB.rankterms, b.h2_rankterms);
+    up(TB.piece_seg, b.h2_piece_seg);
+    b.nh2_pieces = (int)TB.piece_seg.size();
     if (commit) {
       // pad patterns of every chunk that kernels never touch (R: payload layout)
       for (int lr = 0; lr < p.w->nlocal; ++lr) {
@@ -435,7 +451,7 @@ Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
   p->ctxs = ctxs;
   // ---- bucketing: group by (kind, routine, reduce) in order of first
   // appearance, split each class at bucket_elems elements per rank
-  const uint64_t cap = w->bucket_elems ? w->bucket_elems : (64ull << 20);
+  const uint64_t cap = w->bucket_elems ? w->bucket_elems : (512ull << 20);
   std::vector<std::pair<std::tuple<int, int, int>, std::vector<int>>> classes;
   for (int i = 0; i < (int)ctxs.size(); ++i) {
     auto key = std::make_tuple(ctxs[i]->cfg.kind, ctxs[i]->routine, ctxs[i]->cfg.reduce);
@@ -611,7 +627,9 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
 
 static void run_h2(Plan& p, Bucket& b, cudaStream_t st) {
   switch (b.kind) {
-    case ESP_DGC: case ESP_TOPK: launch_h2_sparse(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, st); break;
+    case ESP_DGC: case ESP_TOPK:
+      launch_h2_sparse(b.h2, b.h2_units, b.nh2_units, b.h2_piece_seg, b.nh2_pieces, b.h2_pieces, st);
+      break;
     case ESP_RANDOMK:
       launch_h2_randomk(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, b.h2_rankterms, st);
       break;
