@@ -27,7 +27,6 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-
 from synth import shapes  # noqa: E402
 from synth.values import BASE_SEED, gradient  # noqa: E402
 
@@ -106,6 +105,25 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ------------------------------------------------------------------ output
+_JSON_FD = None
+
+
+def _claim_stdout():
+    """The JSON line must be the only stdout output: keep a private handle on
+    the real stdout and point fd 1 (C libraries such as NCCL print there) at
+    stderr."""
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
+def emit(line: dict):
+    fd = _JSON_FD if _JSON_FD is not None else 1
+    os.write(fd, (json.dumps(line) + "\n").encode())
+
+
 # ------------------------------------------------------------------ dist helpers
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -176,7 +194,7 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def cpu_baseline(args, model, rule, sizes, names, n):
@@ -216,6 +234,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bucket-elems", type=int, default=0)
     args = ap.parse_args()
+    _claim_stdout()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
@@ -349,7 +368,7 @@ def main():
         }
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args, model, rule, sizes, names, 1)
-        print(json.dumps(line), flush=True)
+        emit(line)
     world.destroy()
     if ws > 1:
         import torch.distributed as dist

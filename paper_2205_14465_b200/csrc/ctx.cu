@@ -206,7 +206,8 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
   std::vector<SegH2> segs;
   std::vector<uint32_t> units;
   std::vector<const unsigned char*> pp;
-  std::vector<uint32_t> rt, piece_seg;
+  std::vector<uint32_t> rt;
+  std::vector<uint4> jobs;
   std::vector<size_t> toff_words;
   size_t toff_total = 0;
   const bool tiles = c->cfg.kind == ESP_DGC || c->cfg.kind == ESP_TOPK;
@@ -236,13 +237,14 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
     if (tiles) {
       toff_words.push_back(toff_total);
       toff_total += (size_t)npieces * (s.nunits + 1);
-      for (int i = 0; i < npieces; ++i) piece_seg.push_back((uint32_t)segs.size());
+      for (int i = 0; i < npieces; ++i)
+        for (uint32_t e = 0; e < s.kpad; e += kOffJob) jobs.push_back(make_uint4((uint32_t)segs.size(), i, e, 0));
     }
     segs.push_back(s);
   }
   // device scratch: dyn (out pointer, step of the last compression), tables
   const size_t b_dyn = 16, b_seg = segs.size() * sizeof(SegH2), b_units = units.size() * 4;
-  const size_t b_pp = pp.size() * 8, b_rt = rt.size() * 4, b_ps = piece_seg.size() * 4;
+  const size_t b_pp = pp.size() * 8, b_rt = rt.size() * 4, b_ps = jobs.size() * 16;
   size_t off_seg = round_up(b_dyn, 256), off_units = round_up(off_seg + b_seg, 256);
   size_t off_pp = round_up(off_units + b_units, 256), off_rt = round_up(off_pp + b_pp, 256);
   size_t off_ps = round_up(off_rt + b_rt, 256), off_toff = round_up(off_ps + b_ps, 256);
@@ -261,7 +263,7 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
   std::memcpy(host.data() + off_units, units.data(), b_units);
   std::memcpy(host.data() + off_pp, pp.data(), b_pp);
   std::memcpy(host.data() + off_rt, rt.data(), b_rt);
-  std::memcpy(host.data() + off_ps, piece_seg.data(), b_ps);
+  std::memcpy(host.data() + off_ps, jobs.data(), b_ps);
   ESP_CUDA(cudaMemcpyAsync(d, host.data(), total, cudaMemcpyHostToDevice, st));
   ESP_CUDA(cudaStreamSynchronize(st));   // host staging buffer goes out of scope
   const SegH2* dseg = reinterpret_cast<const SegH2*>(d + off_seg);
@@ -270,8 +272,8 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
   const uint32_t* drt = reinterpret_cast<const uint32_t*>(d + off_rt);
   switch (c->cfg.kind) {
     case ESP_DGC: case ESP_TOPK:
-      launch_h2_sparse(dseg, dunits, (int)u0, reinterpret_cast<const uint32_t*>(d + off_ps),
-                       (int)piece_seg.size(), dpp, st);
+      launch_h2_sparse(dseg, dunits, (int)u0, reinterpret_cast<const uint4*>(d + off_ps),
+                       (int)jobs.size(), dpp, st);
       break;
     case ESP_RANDOMK: launch_h2_randomk(dseg, dunits, (int)u0, dpp, drt, st); break;
     case ESP_EFSIGNSGD: launch_h2_sign(K_EFSIGN, dseg, dunits, (int)u0, dpp, st); break;

@@ -24,9 +24,8 @@ void launch_sign_h1(int kind, const SegH1* segs, const uint32_t* unit_seg, int n
 void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 
 // h2 (k_h2.cu)
-// piece_seg: segment of every piece (npieces_total entries)
-void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint32_t* piece_seg,
-                      int npieces_total,
+// jobs: {segment, piece within segment, first entry, 0}, kOffJob entries each
+void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
                       const unsigned char* const* pieces, cudaStream_t st);
 void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
                     const unsigned char* const* pieces, cudaStream_t st);

@@ -10,11 +10,15 @@ namespace esp {
 // Work granularity (elements).  A CTA of 256 threads streams one UNIT; each
 // warp owns one RUN of 1024 consecutive elements (8 x float4 per lane).
 constexpr int kThreads = 256;
-constexpr int kRun = 1024;
+constexpr int kRun = 512;                // DGC: candidates are compacted per warp-run
+constexpr int kNJ = kRun / 128;          // float4 per lane per run
+constexpr int kDgcTile = 8 * kRun;       // DGC streaming tile (one run per consumer warp)
+constexpr int kSignSpan = 1024;          // sign h1: elements per warp per unit
 constexpr int kUnit = 8192;              // 8 runs per CTA
-constexpr int kRunsPerGroup = 64;        // DGC finalize: 64 runs (65536 elements) per CTA
+constexpr int kRunsPerGroup = 256;       // DGC finalize: 256 runs (262144 elements) per CTA
 constexpr int kSample = 4096;            // DGC sampled-threshold sample size
 constexpr int kTile = 8192;              // sparse h2 output tile (32 KB smem)
+constexpr int kOffJob = 4096;            // sparse h2 tile-offset pass: entries per CTA
 
 enum Kind : int { K_NONE = 0, K_RANDOMK = 1, K_DGC = 2, K_TOPK = 3, K_EFSIGN = 4, K_ONEBIT = 5 };
 

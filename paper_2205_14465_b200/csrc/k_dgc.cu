@@ -22,6 +22,8 @@
 //                   output offset, ordered selection -> payload idx[]/val[] sorted
 //                   by index; EF: r[idx] := 0.
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "esp_device.cuh"
 #include "esp_kernels.h"
@@ -35,7 +37,7 @@ constexpr int kStages = 3;
 // histogram lives in global memory and was built by other CTAs' atomics.
 template <int BAR, bool GLOBAL>
 __device__ void select_bin(const uint32_t* hist, int nbins, uint32_t need, uint32_t* out_bin,
-                           uint32_t* out_above, uint32_t* sh /* >= 270 */) {
+                           uint32_t* out_above, uint32_t* sh /* >= 270 */, uint32_t* out_total = nullptr) {
   const int per = nbins / kThreads;
   const int t = threadIdx.x;
   uint32_t local[8];
@@ -52,6 +54,7 @@ __device__ void select_bin(const uint32_t* hist, int nbins, uint32_t need, uint3
   csync<BAR>();
   uint32_t tot;
   const uint32_t excl = block_excl_scan<BAR>(v, &tot, sh + 258);   // sum over threads > (255 - t)
+  if (out_total) *out_total = tot;
   sh_sum[kThreads - 1 - t] = excl;
   if (t == 0) { sh_res[0] = 0; sh_res[1] = 0; }
   csync<BAR>();
@@ -132,13 +135,13 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
 // One warp, one 1024-element run held in registers (8 float4 per lane; element
 // base + j*128 + lane*4 + c).  Appends {idx, bits(acc)} of key >= thr in index
 // order and histograms the candidates' top 11 key bits.  Returns the count.
-__device__ __forceinline__ uint32_t emit_run(const float4 (&av)[8], uint32_t base, uint32_t n, uint32_t thr,
+__device__ __forceinline__ uint32_t emit_run(const float4 (&av)[kNJ], uint32_t base, uint32_t n, uint32_t thr,
                                              uint2* __restrict__ cand, uint32_t* hist) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t wcount = 0;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < kNJ; ++j) {
     const uint32_t e = base + j * 128 + lane * 4;
     uint32_t f[4], bal[4];
 #pragma unroll
@@ -169,15 +172,20 @@ __device__ __forceinline__ uint32_t emit_run(const float4 (&av)[8], uint32_t bas
 }
 
 // ------------------------------------------------------------------ 2. stream (TMA)
-struct StreamSmem {
-  float g[kStages][kUnit];
-  float r[kStages][kUnit];
+constexpr int kMaxStages = 6;   // 6 x 32 KB stages + header fit the 227 KB of one SM
+struct StreamSmem {   // followed (128-byte aligned) by `ns` stages of {g[kDgcTile], r[kDgcTile]}
   uint32_t hist[2048];
-  uint64_t full[kStages], empty[kStages];
+  uint64_t full[kMaxStages], empty[kMaxStages];
   uint32_t scan[280];
   uint32_t cta_count;
   int flag;
 };
+constexpr size_t kStreamHdr = (sizeof(StreamSmem) + 127) / 128 * 128;
+constexpr size_t kStageBytes = 2 * kDgcTile * sizeof(float);
+__device__ __forceinline__ float* stage_g(unsigned char* smem, int s) {
+  return reinterpret_cast<float*>(smem + kStreamHdr + (size_t)s * kStageBytes);
+}
+__device__ __forceinline__ float* stage_r(unsigned char* smem, int s) { return stage_g(smem, s) + kDgcTile; }
 
 // segment bookkeeping by the 256 consumer threads of a CTA that has finished its
 // share (`units` units) of segment S: flush the private histogram, add the
@@ -219,16 +227,16 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, StreamSmem& 
   }
 }
 
-__global__ void __launch_bounds__(kThreads + 32, 1) dgc_stream_kernel(const SegH1* __restrict__ segs,
+__global__ void __launch_bounds__(kThreads + 32, 2) dgc_stream_kernel(const SegH1* __restrict__ segs,
                                                                       const uint32_t* __restrict__ unit_seg,
-                                                                      uint32_t nunits) {
+                                                                      uint32_t nunits, int variant, int ns) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t u0 = (uint32_t)((uint64_t)blockIdx.x * nunits / gridDim.x);
   const uint32_t u1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nunits / gridDim.x);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < ns; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], kThreads / 32);
     }
@@ -241,7 +249,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) dgc_stream_kernel(const SegH
   if (warp == kThreads / 32) {
     // ---- producer warp: one elected lane streams tiles into the ring
     if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = (variant & 1) ? policy_evict_first() : policy_evict_normal();
       // per-segment values are cached; the unit table is prefetched one ahead
       uint32_t cur = 0xFFFFFFFFu, unit0 = 0, n = 0;
       const float* gseg = nullptr;
@@ -260,18 +268,18 @@ __global__ void __launch_bounds__(kThreads + 32, 1) dgc_stream_kernel(const SegH
           rseg = S.r;
           ef = S.ef != 0;
         }
-        const int stage = i % kStages;
-        const uint32_t round = i / kStages;
+        const int stage = i % ns;
+        const uint32_t round = i / ns;
         if (round > 0) mbar_wait(&sm.empty[stage], (round - 1) & 1);
-        const uint32_t start = (u - unit0) * kUnit;
-        const uint32_t len = min((uint32_t)kUnit, n - start);
+        const uint32_t start = (u - unit0) * kDgcTile;
+        const uint32_t len = min((uint32_t)kDgcTile, n - start);
         const float* g = gseg + start;
         const float* r = rseg + start;
         const uint32_t bytes = (len * 4) & ~15u;
         if (bytes && al16(g) && (!ef || al16(r))) {
           mbar_arrive_expect_tx(&sm.full[stage], bytes * (ef ? 2 : 1));
-          tma_load_1d(sm.g[stage], g, bytes, &sm.full[stage], pol);
-          if (ef) tma_load_1d(sm.r[stage], r, bytes, &sm.full[stage], pol);
+          tma_load_1d(stage_g(smem_raw, stage), g, bytes, &sm.full[stage], pol);
+          if (ef) tma_load_1d(stage_r(smem_raw, stage), r, bytes, &sm.full[stage], pol);
         } else {
           mbar_arrive(&sm.full[stage]);
         }
@@ -286,8 +294,8 @@ __global__ void __launch_bounds__(kThreads + 32, 1) dgc_stream_kernel(const SegH
   SegH1 S{};
   uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
   for (uint32_t u = u0, i = 0; u < u1; ++u, ++i) {
-    const int stage = i % kStages;
-    const uint32_t round = i / kStages;
+    const int stage = i % ns;
+    const uint32_t round = i / ns;
     const uint32_t sid = sid_next;
     if (u + 1 < u1) sid_next = unit_seg[u + 1];
     if (sid != cur) {
@@ -299,23 +307,23 @@ __global__ void __launch_bounds__(kThreads + 32, 1) dgc_stream_kernel(const SegH
       cur_units = 0;
     }
     ++cur_units;
-    const uint32_t start = (u - S.unit0) * kUnit;
+    const uint32_t start = (u - S.unit0) * kDgcTile;
     const uint32_t n = S.n;
-    const uint32_t len = min((uint32_t)kUnit, n - start);
+    const uint32_t len = min((uint32_t)kDgcTile, n - start);
     const uint32_t bytes = (len * 4) & ~15u;
     const bool tma = bytes && al16(g + start) && (!S.ef || al16(S.r + start));
     mbar_wait(&sm.full[stage], round & 1);
     const uint32_t lbase = warp * kRun;            // tile-relative
     const uint32_t base = start + lbase;           // segment-relative
-    float4 av[8];
+    float4 av[kNJ];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < kNJ; ++j) {
       const uint32_t l = lbase + j * 128 + lane * 4;
       const uint32_t e = start + l;
       float4 gv, rv;
       if (tma && l + 4 <= bytes / 4) {
-        gv = lds4(&sm.g[stage][l]);
-        rv = S.ef ? lds4(&sm.r[stage][l]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        gv = lds4(stage_g(smem_raw, stage) + l);
+        rv = S.ef ? lds4(stage_r(smem_raw, stage) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
         gv = load4_guard(g, e, n);
         rv = S.ef ? load4_guard(S.r, e, n) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -329,12 +337,29 @@ __global__ void __launch_bounds__(kThreads + 32, 1) dgc_stream_kernel(const SegH
         av[j] = gv;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[stage]);   // stage consumed (values in registers)
-    if (base < n) {
-      if (S.ef) {
+    // r := acc.  Variant bit 2: the warp writes its run back into the stage's r
+    // tile and one lane issues a 2 KB bulk store (cp.async.bulk smem -> global),
+    // releasing the stage once the TMA engine has read it.
+    const bool bulk_store = (variant & 4) && S.ef && tma && base + kRun <= n && (lbase + kRun) * 4 <= bytes;
+    if (bulk_store) {
+      float* rt = stage_r(smem_raw, stage);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) store4_guard(S.r, base + j * 128 + lane * 4, n, av[j]);
+      for (int j = 0; j < kNJ; ++j) *reinterpret_cast<float4*>(rt + lbase + j * 128 + lane * 4) = av[j];
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_1d(S.r + base, rt + lbase, kRun * 4);
+        bulk_wait_read();
+        mbar_arrive(&sm.empty[stage]);
+      }
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[stage]);   // stage consumed (values in registers)
+    }
+    if (base < n) {
+      if (S.ef && !bulk_store) {
+#pragma unroll
+        for (int j = 0; j < kNJ; ++j) store4_guard(S.r, base + j * 128 + lane * 4, n, av[j]);
       }
       const uint32_t run = base / kRun;
       const uint32_t wc = emit_run(av, base, n, thr, S.cand + (size_t)run * kRun, sm.hist);
@@ -345,6 +370,65 @@ __global__ void __launch_bounds__(kThreads + 32, 1) dgc_stream_kernel(const SegH
     }
   }
   if (cur != 0xFFFFFFFFu) stream_segment_done(S, cur_units, sm);
+}
+
+// ------------------------------------------------------------------ 2'. stream (LDG)
+// Alternative streaming pass: one 4096-element tile per CTA, 8 LDG.128 in flight
+// per lane, many resident CTAs per SM; candidate keys go straight to the
+// segment's global histogram (RED, ~0.25% of elements), the candidate count is
+// that histogram's total, and the CTA that completes a segment selects the bin.
+__global__ void __launch_bounds__(kThreads) dgc_stream_ldg_kernel(const SegH1* __restrict__ segs,
+                                                                  const uint32_t* __restrict__ unit_seg) {
+  __shared__ uint32_t sh[280];
+  __shared__ int sh_flag;
+  const uint32_t sid = unit_seg[blockIdx.x];
+  const SegH1& S = segs[sid];
+  const uint32_t u = blockIdx.x - S.unit0;
+  const uint32_t n = S.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t base = u * kDgcTile + warp * kRun;
+  uint32_t* const ghist = S.hist;
+  if (base < n) {
+    const float* g = seg_g(S);
+    float* r = S.r;
+    const bool ef = S.ef != 0;
+    float4 gv[kNJ], rv[kNJ], av[kNJ];
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) gv[j] = load4_stream_guard(g, base + j * 128 + lane * 4, n);
+    if (ef) {
+#pragma unroll
+      for (int j = 0; j < kNJ; ++j) rv[j] = load4_guard(r, base + j * 128 + lane * 4, n);
+    }
+    const uint32_t thr = __ldcg(&S.st->thr);
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) {
+      if (ef) {
+        av[j].x = __fadd_rn(gv[j].x, rv[j].x);
+        av[j].y = __fadd_rn(gv[j].y, rv[j].y);
+        av[j].z = __fadd_rn(gv[j].z, rv[j].z);
+        av[j].w = __fadd_rn(gv[j].w, rv[j].w);
+        store4_guard(r, base + j * 128 + lane * 4, n, av[j]);
+      } else {
+        av[j] = gv[j];
+      }
+    }
+    const uint32_t run = base / kRun;
+    const uint32_t wc = emit_run(av, base, n, thr, S.cand + (size_t)run * kRun, ghist);
+    if (lane == 0) S.runcnt[run] = wc;
+  }
+  if (!last_cta(&S.st->done, S.nunits, &sh_flag)) return;
+  uint32_t bin, above, total;
+  select_bin<0, true>(ghist, 2048, S.k, &bin, &above, sh, &total);
+  if (threadIdx.x == 0) {
+    if (total < S.k) {
+      S.st->fallback = 1;
+      atomicAdd(S.bflag, 1u);
+    } else {
+      S.st->prefix = bin;
+      S.st->above = above;
+      S.st->need = S.k - above;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ 3. fallback
@@ -377,11 +461,11 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
     uint32_t units = 0;
     const float* src = S.ef ? S.r : seg_g(S);
     for (uint32_t u = blockIdx.x; u < S.nunits; u += gridDim.x, ++units) {
-      const uint32_t base = u * kUnit + warp * kRun;
+      const uint32_t base = u * kDgcTile + warp * kRun;
       if (base >= S.n) continue;
-      float4 av[8];
+      float4 av[kNJ];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) av[j] = load4_guard(src, base + j * 128 + lane * 4, S.n);
+      for (int j = 0; j < kNJ; ++j) av[j] = load4_guard(src, base + j * 128 + lane * 4, S.n);
       const uint32_t run = base / kRun;
       const uint32_t wc = emit_run(av, base, S.n, 0u, S.cand + (size_t)run * kRun, hist);
       if (lane == 0) {
@@ -415,31 +499,53 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
 }
 
 // ------------------------------------------------------------------ 4. refine
+// A finalize group = kRunsPerGroup consecutive runs of one segment (one runcnt
+// per thread).  Its candidates are addressed as one flat, index-ordered list:
+// sh_off[i] = first flat position of run i; returns the group's total.
+__device__ __forceinline__ uint32_t group_offsets(const SegH1& S, uint32_t g, uint32_t* sh_off,
+                                                  uint32_t* sh_scan, uint32_t* nr_out) {
+  const uint32_t nruns = (S.n + kRun - 1) / kRun;
+  const uint32_t run0 = g * kRunsPerGroup;
+  const uint32_t nr = min((uint32_t)kRunsPerGroup, nruns - run0);
+  const uint32_t c = threadIdx.x < nr ? __ldcg(S.runcnt + run0 + threadIdx.x) : 0u;
+  uint32_t tot;
+  const uint32_t off = block_excl_scan(c, &tot, sh_scan);
+  if (threadIdx.x < nr) sh_off[threadIdx.x] = off;
+  if (threadIdx.x == 0) sh_off[nr] = tot;
+  __syncthreads();
+  *nr_out = nr;
+  return tot;
+}
+
+__device__ __forceinline__ uint2 group_cand(const SegH1& S, uint32_t g, const uint32_t* sh_off, uint32_t nr,
+                                           uint32_t q) {
+  uint32_t lo = 0, hi = nr;   // largest i with sh_off[i] <= q
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (sh_off[mid] <= q) lo = mid; else hi = mid;
+  }
+  return __ldcg(S.cand + (size_t)(g * kRunsPerGroup + lo) * kRun + (q - sh_off[lo]));
+}
+
 template <int ROUND>
 __global__ void __launch_bounds__(kThreads) dgc_refine_kernel(const SegH1* __restrict__ segs,
                                                               const uint32_t* __restrict__ group_seg) {
   __shared__ uint32_t sh_hist[1024];
   __shared__ uint32_t sh_scan[280];
+  __shared__ uint32_t sh_off[kRunsPerGroup + 1];
   __shared__ int sh_flag;
   constexpr int kShiftMatch = ROUND == 2 ? 20 : 10;
   constexpr int kShiftBin = ROUND == 2 ? 10 : 0;
   const uint32_t sid = group_seg[blockIdx.x];
   const SegH1 S = segs[sid];
   const uint32_t g = blockIdx.x - S.group0;
-  const uint32_t prefix = __ldcg(&S.st->prefix);
   for (int i = threadIdx.x; i < 1024; i += kThreads) sh_hist[i] = 0;
-  __syncthreads();
-  const uint32_t nruns = (S.n + kRun - 1) / kRun;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t rr = warp; rr < (uint32_t)kRunsPerGroup; rr += kThreads / 32) {
-    const uint32_t run = g * kRunsPerGroup + rr;
-    if (run >= nruns) break;
-    const uint32_t cnt = __ldcg(S.runcnt + run);
-    const uint2* cand = S.cand + (size_t)run * kRun;
-    for (uint32_t i = lane; i < cnt; i += 32) {
-      const uint32_t key = __ldcg(&cand[i].y) & 0x7FFFFFFFu;
-      if ((key >> kShiftMatch) == prefix) atomicAdd(&sh_hist[(key >> kShiftBin) & 1023u], 1u);
-    }
+  uint32_t nr;
+  const uint32_t C = group_offsets(S, g, sh_off, sh_scan, &nr);
+  const uint32_t prefix = __ldcg(&S.st->prefix);
+  for (uint32_t q = threadIdx.x; q < C; q += kThreads) {
+    const uint32_t key = group_cand(S, g, sh_off, nr, q).y & 0x7FFFFFFFu;
+    if ((key >> kShiftMatch) == prefix) atomicAdd(&sh_hist[(key >> kShiftBin) & 1023u], 1u);
   }
   __syncthreads();
   uint32_t* ghist = S.hist + (ROUND == 2 ? 4096 : 5120);
@@ -473,28 +579,11 @@ __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __rest
   const uint32_t sid = group_seg[blockIdx.x];
   const SegH1 S = segs[sid];
   const uint32_t g = blockIdx.x - S.group0;
+  uint32_t nr;
+  const uint32_t C = group_offsets(S, g, sh_off, sh_scan, &nr);
   const uint32_t T = __ldcg(&S.st->prefix);
   const uint32_t need = __ldcg(&S.st->need);
-  const uint32_t nruns = (S.n + kRun - 1) / kRun;
-  const uint32_t run0 = g * kRunsPerGroup;
-  const uint32_t nr = min((uint32_t)kRunsPerGroup, nruns - run0);
-  {
-    const uint32_t c = threadIdx.x < nr ? __ldcg(S.runcnt + run0 + threadIdx.x) : 0u;
-    uint32_t tot;
-    const uint32_t off = block_excl_scan(c, &tot, sh_scan);
-    if (threadIdx.x < nr) sh_off[threadIdx.x] = off;
-    if (threadIdx.x == 0) sh_off[nr] = tot;
-    __syncthreads();
-  }
-  const uint32_t C = sh_off[nr];
-  auto cand_at = [&](uint32_t q) -> uint2 {
-    uint32_t lo = 0, hi = nr;   // largest i with sh_off[i] <= q
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (sh_off[mid] <= q) lo = mid; else hi = mid;
-    }
-    return __ldcg(S.cand + (size_t)(run0 + lo) * kRun + (q - sh_off[lo]));
-  };
+  auto cand_at = [&](uint32_t q) -> uint2 { return group_cand(S, g, sh_off, nr, q); };
   // pass 1: the group's aggregate
   uint32_t above = 0, tie = 0;
   for (uint32_t q = threadIdx.x; q < C; q += kThreads) {
@@ -569,12 +658,34 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(dgc_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(StreamSmem));
+                         (int)(kStreamHdr + kMaxStages * kStageBytes));
   }
+  static const bool use_ldg = [] {
+    const char* e = getenv("ESP_DGC_STREAM");
+    return e && std::string(e) == "ldg";
+  }();
+  // tuning knobs (measured on B200): bit0 of ESP_TMA_VARIANT = L2
+  // evict-first hint on the tile loads, bit1 = 2 CTAs per SM; ESP_TMA_STAGES
+  static const int variant = [] {
+    const char* e = getenv("ESP_TMA_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  static const int stages = [] {
+    const char* e = getenv("ESP_TMA_STAGES");
+    const int s = e ? atoi(e) : 4;
+    return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
+  }();
   dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs);
-  const int grid = nunits < g_num_sms ? nunits : g_num_sms;
   if (probe0) cudaEventRecord(probe0, st);
-  dgc_stream_kernel<<<grid, kThreads + 32, sizeof(StreamSmem), st>>>(segs, unit_seg, (uint32_t)nunits);
+  if (use_ldg) {
+    dgc_stream_ldg_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg);
+  } else {
+    const int per_sm = (variant & 2) ? 2 : 1;
+    const int ns = per_sm == 2 ? (stages > 3 ? 3 : stages) : stages;
+    const int grid = nunits < per_sm * g_num_sms ? nunits : per_sm * g_num_sms;
+    dgc_stream_kernel<<<grid, kThreads + 32, kStreamHdr + ns * kStageBytes, st>>>(
+        segs, unit_seg, (uint32_t)nunits, variant, ns);
+  }
   if (probe1) cudaEventRecord(probe1, st);
   dgc_fallback_kernel<<<g_num_sms, kThreads, 0, st>>>(segs, nsegs);
   dgc_refine_kernel<2><<<ngroups, kThreads, 0, st>>>(segs, group_seg);

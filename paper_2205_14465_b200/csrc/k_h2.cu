@@ -17,16 +17,18 @@ constexpr int kMaxPieces = 64;
 // For every piece (sorted idx[kpad], 0xFFFFFFFF padding), the first entry of
 // each output tile: toff[t] = lower_bound(idx, t * kTile), t = 0..ntiles.  One
 // pass over the (small) pieces replaces a dependent binary search per tile.
+// job = {segment, piece within segment, first entry}: kOffJob entries of one piece
 __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2* __restrict__ segs,
-                                                                     const uint32_t* __restrict__ piece_seg,
+                                                                     const uint4* __restrict__ jobs,
                                                                      const unsigned char* const* __restrict__ pieces) {
-  const uint32_t p = blockIdx.x;
-  const SegH2 S = segs[piece_seg[p]];
-  const uint32_t r = p - S.piece0;
+  const uint4 job = jobs[blockIdx.x];
+  const SegH2 S = segs[job.x];
+  const uint32_t r = job.y;
   const uint32_t ntiles = S.nunits;
   uint32_t* toff = S.toff + (size_t)r * (ntiles + 1);
-  const uint32_t* idx = reinterpret_cast<const uint32_t*>(pieces[p]);
-  for (uint32_t i = threadIdx.x; i < S.kpad; i += kThreads) {
+  const uint32_t* idx = reinterpret_cast<const uint32_t*>(pieces[S.piece0 + r]);
+  const uint32_t iend = min(job.z + (uint32_t)kOffJob, S.kpad);
+  for (uint32_t i = job.z + threadIdx.x; i < iend; i += kThreads) {
     const uint32_t v = __ldg(idx + i);
     const uint32_t t = v == 0xFFFFFFFFu ? ntiles : min(v / (uint32_t)kTile, ntiles);
     const uint32_t prev = i == 0 ? 0u : [&] {
@@ -166,10 +168,10 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const SegH1* __restrict_
   }
 }
 
-void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint32_t* piece_seg,
-                      int npieces_total, const unsigned char* const* pieces, cudaStream_t st) {
+void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
+                      const unsigned char* const* pieces, cudaStream_t st) {
   if (ntiles == 0) return;
-  h2_sparse_offsets_kernel<<<npieces_total, kThreads, 0, st>>>(segs, piece_seg, pieces);
+  h2_sparse_offsets_kernel<<<njobs, kThreads, 0, st>>>(segs, jobs, pieces);
   h2_sparse_kernel<<<ntiles, kThreads, 0, st>>>(segs, tile_seg, pieces);
   count_launches(2);
 }

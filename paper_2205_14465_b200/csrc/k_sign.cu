@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kThreads) sign_h1_kernel(const SegH1* __restri
   const uint32_t u = blockIdx.x - S.unit0;
   const uint32_t n = S.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t base = u * kUnit + warp * kRun;
+  const uint32_t base = u * kUnit + warp * kSignSpan;
   float sp = 0.f, sn = 0.f;
   if (S.ef) {
     const float a = S.lazy_in[0], b = S.lazy_in[1];

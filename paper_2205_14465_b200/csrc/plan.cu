@@ -33,7 +33,7 @@ struct Bucket {
   uint32_t* h2_units = nullptr; int nh2_units = 0;
   const unsigned char** h2_pieces = nullptr;
   uint32_t* h2_rankterms = nullptr;
-  uint32_t* h2_piece_seg = nullptr; int nh2_pieces = 0;
+  uint4* h2_off_jobs = nullptr; int nh2_off_jobs = 0;
   cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
@@ -78,7 +78,8 @@ struct HostTables {
   std::vector<uint32_t> h1_units, h1_groups, a7_units, h2_units;
   std::vector<SegH2> h2;
   std::vector<const unsigned char*> a7_pieces, h2_pieces;
-  std::vector<uint32_t> rankterms, piece_seg;
+  std::vector<uint32_t> rankterms;
+  std::vector<uint4> off_jobs;
 };
 
 static void fill_unit_table(std::vector<uint32_t>& units, uint32_t seg, uint32_t count) {
@@ -164,7 +165,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.n = len;
         s.k = none ? 0 : c->pk[part];
         s.kpad = c->kpad;
-        const uint32_t nunits = div_up(len, kUnit);
+        const uint32_t nunits = div_up(len, dgc ? kDgcTile : kUnit);
         s.unit0 = unit_cursor;
         s.nunits = nunits;
         const uint32_t nruns = div_up(len, kRun);
@@ -346,7 +347,9 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         u0 += s.nunits;
         if (tiles) {
           s.toff = L.ptr<uint32_t>(L.reserve((size_t)s.npieces * (s.nunits + 1) * 4));
-          for (uint32_t r = 0; r < s.npieces; ++r) T.piece_seg.push_back((uint32_t)(T.h2.size() - h2_first));
+          for (uint32_t r = 0; r < s.npieces; ++r)
+            for (uint32_t e = 0; e < s.kpad; e += kOffJob)
+              T.off_jobs.push_back(make_uint4((uint32_t)(T.h2.size() - h2_first), r, e, 0));
         }
         T.h2.push_back(s);
         fill_unit_table(T.h2_units, (uint32_t)(T.h2.size() - 1 - h2_first), s.nunits);
@@ -421,8 +424,8 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     up(TB.h2_units, b.h2_units);
     up(TB.h2_pieces, b.h2_pieces);
     up(TB.rankterms, b.h2_rankterms);
-    up(TB.piece_seg, b.h2_piece_seg);
-    b.nh2_pieces = (int)TB.piece_seg.size();
+    up(TB.off_jobs, b.h2_off_jobs);
+    b.nh2_off_jobs = (int)TB.off_jobs.size();
     if (commit) {
       // pad patterns of every chunk that kernels never touch (R: payload layout)
       for (int lr = 0; lr < p.w->nlocal; ++lr) {
@@ -628,7 +631,7 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
 static void run_h2(Plan& p, Bucket& b, cudaStream_t st) {
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
-      launch_h2_sparse(b.h2, b.h2_units, b.nh2_units, b.h2_piece_seg, b.nh2_pieces, b.h2_pieces, st);
+      launch_h2_sparse(b.h2, b.h2_units, b.nh2_units, b.h2_off_jobs, b.nh2_off_jobs, b.h2_pieces, st);
       break;
     case ESP_RANDOMK:
       launch_h2_randomk(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, b.h2_rankterms, st);
