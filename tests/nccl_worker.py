@@ -1,0 +1,108 @@
+"""One rank of the multi-process (NCCL world) parity run, launched by
+tests/test_gpu_nccl.py through torch.distributed.run (one process per GPU).
+
+Every rank regenerates all n ranks' seeded gradients, runs the oracle's n-rank
+simulation on the host, and compares its OWN CUDA output and EF state with the
+oracle's entry for its rank — no result ever travels from the CUDA path to the
+oracle.  Byte-moving routines are bit-exact; NCCL-reduced ones (Allreduce,
+Reduce-scatter/Allgather, Reduce/Broadcast) are checked against the fp64 mean
+within 1e-6 * mean|x| (NCCL's summation order is opaque)."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import esp_oracle as O  # noqa: E402
+from paper_2205_14465_b200 import esp as E  # noqa: E402
+from synth.values import gradient  # noqa: E402
+
+REDUCED = ("allreduce", "reducescatter_allgather", "reduce_broadcast")
+
+
+def bits(x):
+    return np.ascontiguousarray(x, np.float32).view(np.uint32)
+
+
+def check(kind, routine, got, ref, grads_all, where):
+    if routine in REDUCED:
+        x = np.stack([g.astype(np.float64) for g in grads_all])
+        scale = np.abs(x).mean(0)
+        if kind == "none":
+            exact = x.mean(0)
+        else:
+            exact = ref.astype(np.float64)
+            scale = np.maximum(scale, np.abs(exact))
+        err = np.abs(got.astype(np.float64) - exact)
+        assert np.all(err <= 1e-6 * scale + 1e-30), f"{where}: max err {err.max()}"
+    elif kind in O.QUANTIZED:
+        np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-30, err_msg=where)
+    else:
+        bad = np.nonzero(bits(got) != bits(ref))[0]
+        assert bad.size == 0, f"{where}: {bad.size} mismatches at {bad[:5]}"
+
+
+def main():
+    rank, n = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = E.World.nccl(local)
+    pairs = [(k, r) for k in O.KINDS for r in O.ROUTINES if O.legal(O.Cfg(k), r)]
+    N = 30_011
+    checked = 0
+    for t, (kind, routine) in enumerate(pairs):
+        ctx = E.Ctx(w, kind, routine, N, tensor_id=t, ratio=0.02)
+        cfg = O.Cfg(kind, 0.02)
+        st = O.new_states(n, N, routine, cfg)
+        for s in range(3):
+            if kind in O.QUANTIZED and s > 0:   # lock-step: oracle state -> GPU
+                r2 = np.zeros((1, ctx.get_state()[2].shape[1]), np.float32)
+                if st[rank].r2 is not None:
+                    r2[0, :st[rank].r2.size] = st[rank].r2
+                ctx.set_state(st[rank].step, st[rank].r[None], r2)
+            grads = [gradient(N, step=s, rank=r, tensor=t) for r in range(n)]
+            ref = O.sync(routine, cfg, grads, st, tensor_id=t)
+            g = torch.from_numpy(grads[rank].copy()).cuda()
+            E.esp_sync(w, ctx, g)
+            torch.cuda.synchronize()
+            check(kind, routine, g.cpu().numpy(), ref.outs[rank], grads, f"rank {rank} {kind}/{routine} step {s}")
+            if kind != "none" and routine not in REDUCED:
+                _, rg, _ = ctx.get_state()
+                if kind in O.QUANTIZED:
+                    np.testing.assert_allclose(rg[0], st[rank].r, rtol=1e-6, atol=1e-30)
+                else:
+                    assert np.array_equal(bits(rg[0]), bits(st[rank].r)), f"residual {kind}/{routine}"
+            checked += 1
+        c = w.counters()
+        w.reset_counters()
+        exp = ref.counters[rank]
+        assert c["recv"] == 3 * exp.recv and c["sent"] == 3 * exp.sent, (kind, routine, c["recv"], exp.recv)
+        ctx.destroy()
+
+    # a mixed strategy through esp_sync_many (bucketing + pipelining with small buckets)
+    specs = [("dgc", "allgather", 70_000), ("none", "allreduce", 1000), ("efsignsgd", "alltoall_allgather", 9000),
+             ("dgc", "alltoall_allgather", 40_000), ("onebit", "gather_broadcast", 5000), ("dgc", "allgather", 33)]
+    w.set_bucket_elems(50_000)
+    ctxs = [E.Ctx(w, k, r, N_, tensor_id=100 + i, ratio=0.01) for i, (k, r, N_) in enumerate(specs)]
+    sts = [O.new_states(n, N_, r, O.Cfg(k, 0.01)) for (k, r, N_) in specs]
+    grads = [[gradient(N_, rank=q, tensor=100 + i) for q in range(n)] for i, (_, _, N_) in enumerate(specs)]
+    refs = [O.sync(r, O.Cfg(k, 0.01), grads[i], sts[i], tensor_id=100 + i) for i, (k, r, _) in enumerate(specs)]
+    gs = [torch.from_numpy(grads[i][rank].copy()).cuda() for i in range(len(specs))]
+    E.esp_sync_many(w, ctxs, gs)
+    torch.cuda.synchronize()
+    for i, (k, r, _) in enumerate(specs):
+        check(k, r, gs[i].cpu().numpy(), refs[i].outs[rank], grads[i], f"sync_many {k}/{r}")
+    w.check()
+    w.destroy()
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"rank {rank}: {checked} pair-steps + sync_many ok", flush=True)
+
+
+if __name__ == "__main__":
+    main()
