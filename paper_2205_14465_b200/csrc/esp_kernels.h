@@ -20,6 +20,8 @@ void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, 
 // npieces received chunks (mid-scheme a7, P:78-87 / P:105-115)  (k_sign.cu)
 void launch_sign_h1(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits,
                     const unsigned char* const* pieces, cudaStream_t st);
+// h1 on the persistent TMA streaming driver, tiles of kDgcTile (k_sign.cu)
+void launch_sign_h1_tma(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 // NONE: pack gradients into a contiguous buffer (k_h2.cu)
 void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 

@@ -192,6 +192,29 @@ __device__ __forceinline__ float* stage_r(unsigned char* smem, int s) { return s
 // candidate count, and if this completes the segment pick the k-th key's bin.
 __device__ void stream_segment_done(const SegH1& S, uint32_t units, StreamSmem& sm) {
   csync<1>();
+  if (units == S.nunits) {
+    // the CTA streamed the whole segment: select from its private histogram
+    const uint32_t total = sm.cta_count;
+    if (total < S.k) {
+      if (threadIdx.x == 0) {
+        S.st->fallback = 1;
+        atomicAdd(S.bflag, 1u);
+      }
+    } else {
+      uint32_t bin, above;
+      select_bin<1, false>(sm.hist, 2048, S.k, &bin, &above, sm.scan);
+      if (threadIdx.x == 0) {
+        S.st->prefix = bin;
+        S.st->above = above;
+        S.st->need = S.k - above;
+      }
+    }
+    csync<1>();
+    for (int i = threadIdx.x; i < 2048; i += kThreads) sm.hist[i] = 0;
+    if (threadIdx.x == 0) sm.cta_count = 0;
+    csync<1>();
+    return;
+  }
   for (int i = threadIdx.x; i < 2048; i += kThreads) {
     const uint32_t h = sm.hist[i];
     if (h) {
@@ -649,17 +672,37 @@ __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __rest
 // ------------------------------------------------------------------ launchers
 static int g_num_sms = 0;
 
-void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
-                   const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
-                   cudaEvent_t probe1) {
-  if (nsegs == 0) return;
+static int num_sms() {
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(dgc_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(kStreamHdr + kMaxStages * kStageBytes));
   }
+  return g_num_sms;
+}
+
+// persistent streaming kernels: one CTA per SM (measured best on B200)
+int tma_stream_grid(int nunits) { return nunits < num_sms() ? nunits : num_sms(); }
+
+int tma_stream_stages() {
+  static const int stages = [] {
+    const char* e = getenv("ESP_TMA_STAGES");
+    const int s = e ? atoi(e) : 4;
+    return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
+  }();
+  return stages;
+}
+
+void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
+                   const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
+                   cudaEvent_t probe1) {
+  if (nsegs == 0) return;
+  static const bool attr_set = [] {
+    return cudaFuncSetAttribute(dgc_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kStreamHdr + kMaxStages * kStageBytes)) == cudaSuccess;
+  }();
+  (void)attr_set;
+  num_sms();
   static const bool use_ldg = [] {
     const char* e = getenv("ESP_DGC_STREAM");
     return e && std::string(e) == "ldg";
@@ -670,11 +713,7 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
     const char* e = getenv("ESP_TMA_VARIANT");
     return e ? atoi(e) : 0;
   }();
-  static const int stages = [] {
-    const char* e = getenv("ESP_TMA_STAGES");
-    const int s = e ? atoi(e) : 4;
-    return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
-  }();
+  const int stages = tma_stream_stages();
   dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs);
   if (probe0) cudaEventRecord(probe0, st);
   if (use_ldg) {

@@ -8,6 +8,7 @@
 // one or two hashes instead of four.
 #include "esp_device.cuh"
 #include "esp_kernels.h"
+#include "stream_tma.cuh"
 
 namespace esp {
 
@@ -112,9 +113,68 @@ __global__ void __launch_bounds__(kThreads) h2_randomk_kernel(const SegH2* __res
   }
 }
 
+// The h1 on the persistent TMA streaming driver: per run of 512 elements,
+// acc = g + r, the hashed pick of each stratum touching a float4, r := sel ? 0 : acc.
+struct RandomkOp {
+  struct State {
+    uint64_t h;
+  };
+  __device__ void begin_segment(const SegH1& S, State& st) const {
+    st.h = randomk_hash(S.hash, *S.step, S.part, S.rankterm);
+  }
+  __device__ void run(const SegH1& S, const float4 (&gv)[kNJ], const float4 (&rv)[kNJ], uint32_t base,
+                      State& st) const {
+    const uint32_t n = S.n, k = S.k;
+    if (base >= n) return;
+    const int lane = threadIdx.x & 31;
+    float* val = reinterpret_cast<float*>(S.chunk);
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) {
+      const uint32_t e = base + j * 128 + lane * 4;
+      if (e >= n) continue;
+      float4 acc = gv[j];
+      if (S.ef) {
+        acc.x = __fadd_rn(acc.x, rv[j].x);
+        acc.y = __fadd_rn(acc.y, rv[j].y);
+        acc.z = __fadd_rn(acc.z, rv[j].z);
+        acc.w = __fadd_rn(acc.w, rv[j].w);
+      }
+      const uint32_t last = min(e + 3, n - 1);
+      const uint64_t j0 = stratum_of(e, k, n), j1 = stratum_of(last, k, n);
+      uint32_t sel = 0;
+      for (uint64_t jj = j0; jj <= j1; ++jj) {
+        const uint32_t idx = randomk_pick(st.h, jj, k, n);
+        if (idx >= e && idx <= last) {
+          sel |= 1u << (idx - e);
+          val[jj] = f4get(acc, idx - e);
+        }
+      }
+      if (S.ef) {
+        float4 nr = acc;
+        if (sel & 1) nr.x = 0.f;
+        if (sel & 2) nr.y = 0.f;
+        if (sel & 4) nr.z = 0.f;
+        if (sel & 8) nr.w = 0.f;
+        store4_guard(S.r, e, n, nr);
+      }
+    }
+  }
+  __device__ void end_segment(const SegH1&, uint32_t, uint32_t, State&, TmaHdr&) const {}
+};
+
+int tma_stream_grid(int nunits);
+int tma_stream_stages();
+
 void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st) {
   if (nunits == 0) return;
-  randomk_h1_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg);
+  static bool init = [] {
+    return cudaFuncSetAttribute(tma_stream_kernel<RandomkOp>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kTmaHdrBytes + kTmaMaxStages * kTmaStageBytes)) == cudaSuccess;
+  }();
+  (void)init;
+  const int ns = tma_stream_stages();
+  tma_stream_kernel<<<tma_stream_grid(nunits), kThreads + 32, kTmaHdrBytes + ns * kTmaStageBytes, st>>>(
+      segs, unit_seg, (uint32_t)nunits, ns, RandomkOp{});
   count_launches(1);
 }
 

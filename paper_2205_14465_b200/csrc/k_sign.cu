@@ -18,6 +18,7 @@
 // Alltoall/Allgather and Gather/Broadcast, fused.
 #include "esp_device.cuh"
 #include "esp_kernels.h"
+#include "stream_tma.cuh"
 
 namespace esp {
 
@@ -177,6 +178,158 @@ __global__ void __launch_bounds__(kThreads) sign_h1_kernel(const SegH1* __restri
   }
 }
 
+// ---- the same h1 on the persistent TMA streaming driver (stream_tma.cuh):
+// tiles of 4096 elements, 512 per warp (16 sign words per warp and tile).
+template <int KIND>
+struct SignOp {
+  struct State {
+    float sp, sn;
+    double s0, s1;
+    uint32_t c0, c1;
+  };
+  __device__ void begin_segment(const SegH1& S, State& st) const {
+    st.sp = st.sn = 0.f;
+    if (S.ef) {
+      const float a = __ldcg(S.lazy_in), b = __ldcg(S.lazy_in + 1);
+      if (KIND == K_EFSIGN) { st.sp = a; st.sn = -a; } else { st.sp = b; st.sn = a; }
+    }
+    st.s0 = st.s1 = 0.0;
+    st.c0 = st.c1 = 0;
+  }
+  __device__ void run(const SegH1& S, const float4 (&gv)[kNJ], const float4 (&rv)[kNJ], uint32_t base,
+                      State& st) const {
+    const uint32_t n = S.n;
+    if (base >= n) return;   // warp-uniform
+    const int lane = threadIdx.x & 31;
+    uint32_t myword = 0;
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) {
+      const uint32_t e = base + j * 128 + lane * 4;
+      float4 p = gv[j];
+      if (S.ef) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float q = f4get(rv[j], c);
+          const float rt = __fsub_rn(q, q >= 0.f ? st.sp : st.sn);   // lazy residual
+          f4set(p, c, __fadd_rn(f4get(gv[j], c), rt));
+        }
+        store4_guard(S.r, e, n, p);
+      }
+      uint32_t nib = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (e + c < n) {
+          const float v = f4get(p, c);
+          const bool b = v >= 0.f;
+          nib |= (uint32_t)b << c;
+          if (KIND == K_EFSIGN) {
+            st.s0 += fabs((double)v);
+          } else if (b) {
+            st.s1 += (double)v;
+            ++st.c1;
+          } else {
+            st.s0 += (double)v;
+            ++st.c0;
+          }
+        }
+      }
+      uint32_t word = nib << (4 * (lane & 7));
+      word |= __shfl_xor_sync(0xffffffffu, word, 1);
+      word |= __shfl_xor_sync(0xffffffffu, word, 2);
+      word |= __shfl_xor_sync(0xffffffffu, word, 4);
+      const uint32_t wv = __shfl_sync(0xffffffffu, word, (lane & 3) * 8);
+      if ((lane >> 2) == j) myword = wv;
+    }
+    uint32_t* words = reinterpret_cast<uint32_t*>(S.chunk + 16);
+    if (lane < kRun / 32 && base + lane * 32 < n) words[(base >> 5) + lane] = myword;
+  }
+  // per (CTA, segment): the CTA's partial goes to the slot of its first unit of
+  // the segment (other slots stay zero); the CTA completing the segment sums the
+  // slots in unit order (deterministic for a given grid) and writes the scale(s).
+  // the 4 sums of the CTA's consumer warps, in fixed order, on thread 0
+  __device__ static void cta_sum4(double& a, double& b, uint32_t& ca, uint32_t& cb, TmaHdr& h) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      ca += __shfl_xor_sync(0xffffffffu, ca, o);
+      cb += __shfl_xor_sync(0xffffffffu, cb, o);
+    }
+    csync<1>();   // previous users of h.red / h.scan are done
+    if (lane == 0) {
+      h.red[warp] = a;
+      h.red[8 + warp] = b;
+      h.scan[warp] = ca;
+      h.scan[8 + warp] = cb;
+    }
+    csync<1>();
+    if (threadIdx.x == 0) {
+      a = b = 0.0;
+      ca = cb = 0;
+      for (int w = 0; w < kThreads / 32; ++w) {
+        a += h.red[w];
+        b += h.red[8 + w];
+        ca += h.scan[w];
+        cb += h.scan[8 + w];
+      }
+    }
+  }
+  __device__ void end_segment(const SegH1& S, uint32_t units, uint32_t first_unit, State& st, TmaHdr& h) const {
+    double a = st.s0, b = st.s1;
+    uint32_t ca = st.c0, cb = st.c1;
+    cta_sum4(a, b, ca, cb, h);
+    if (units != S.nunits) {
+      // shared segment: publish this CTA's partial, the CTA completing it sums all
+      if (threadIdx.x == 0) {
+        S.partial[2 * first_unit] = a;
+        S.partial[2 * first_unit + 1] = b;
+        S.pcount[2 * first_unit] = ca;
+        S.pcount[2 * first_unit + 1] = cb;
+        __threadfence();
+        const uint32_t old = atomicAdd(&S.st->done, units);
+        h.flag = (old + units == S.nunits);
+      }
+      csync<1>();
+      if (!h.flag) return;
+      __threadfence();
+      a = b = 0.0;
+      ca = cb = 0;
+      for (uint32_t v = threadIdx.x; v < S.nunits; v += kThreads) {
+        a += __ldcg(S.partial + 2 * v);
+        b += __ldcg(S.partial + 2 * v + 1);
+        ca += __ldcg(S.pcount + 2 * v);
+        cb += __ldcg(S.pcount + 2 * v + 1);
+      }
+      a = block_sum_f64<1>(a, h.red);
+      b = block_sum_f64<1>(b, h.red);
+      ca = block_sum_u32<1>(ca, h.scan);
+      cb = block_sum_u32<1>(cb, h.scan);
+    }
+    // (a segment owned by one CTA is finalised directly: its sum equals the
+    // slot-wise sum, which would only add exact zeros)
+    if (threadIdx.x == 0) {
+      float* hdr = reinterpret_cast<float*>(S.chunk);
+      const uint32_t n = S.n;
+      float x0, x1;
+      if (KIND == K_EFSIGN) {
+        x0 = n ? (float)(a / (double)n) : 0.f;   // scale = ||p||_1 / N (R7)
+        x1 = 0.f;
+      } else {
+        x0 = ca ? (float)(a / (double)ca) : 0.f;  // mean of {p < 0} (R8)
+        x1 = cb ? (float)(b / (double)cb) : 0.f;  // mean of {p >= 0}
+      }
+      hdr[0] = x0;
+      if (KIND == K_ONEBIT) hdr[1] = x1;
+      if (S.ef) {
+        S.lazy_out[0] = x0;
+        S.lazy_out[1] = x1;
+      }
+    }
+    csync<1>();
+  }
+};
+
 template <int KIND>
 __global__ void sign_materialize_kernel(const float* __restrict__ p, const float* __restrict__ lazy,
                                         float* __restrict__ out, uint32_t n) {
@@ -198,6 +351,32 @@ void launch_sign_h1(int kind, const SegH1* segs, const uint32_t* unit_seg, int n
   } else {
     if (pieces) sign_h1_kernel<K_ONEBIT, true><<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
     else sign_h1_kernel<K_ONEBIT, false><<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
+  }
+  count_launches(1);
+}
+
+int tma_stream_grid(int nunits);
+int tma_stream_stages();
+
+void launch_sign_h1_tma(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st) {
+  if (nunits == 0) return;
+  const int ns = tma_stream_stages();
+  const size_t smem = kTmaHdrBytes + ns * kTmaStageBytes;
+  const int grid = tma_stream_grid(nunits);
+  if (kind == K_EFSIGN) {
+    static bool init = [] {
+      return cudaFuncSetAttribute(tma_stream_kernel<SignOp<K_EFSIGN>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kTmaHdrBytes + kTmaMaxStages * kTmaStageBytes)) == cudaSuccess;
+    }();
+    (void)init;
+    tma_stream_kernel<<<grid, kThreads + 32, smem, st>>>(segs, unit_seg, (uint32_t)nunits, ns, SignOp<K_EFSIGN>{});
+  } else {
+    static bool init = [] {
+      return cudaFuncSetAttribute(tma_stream_kernel<SignOp<K_ONEBIT>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kTmaHdrBytes + kTmaMaxStages * kTmaStageBytes)) == cudaSuccess;
+    }();
+    (void)init;
+    tma_stream_kernel<<<grid, kThreads + 32, smem, st>>>(segs, unit_seg, (uint32_t)nunits, ns, SignOp<K_ONEBIT>{});
   }
   count_launches(1);
 }

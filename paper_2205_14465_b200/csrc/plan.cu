@@ -165,7 +165,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.n = len;
         s.k = none ? 0 : c->pk[part];
         s.kpad = c->kpad;
-        const uint32_t nunits = div_up(len, dgc ? kDgcTile : kUnit);
+        // compressors stream 4096-element tiles (stream_tma.cuh); NONE's pack uses kUnit
+        const uint32_t nunits = div_up(len, none ? kUnit : kDgcTile);
         s.unit0 = unit_cursor;
         s.nunits = nunits;
         const uint32_t nruns = div_up(len, kRun);
@@ -190,8 +191,11 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           hist_cursor += 6144 * 4 + round_up((size_t)s.ngroups * 8, 256);
         }
         if (quant) {
-          s.partial = L.ptr<double>(L.reserve((size_t)nunits * 16));
-          s.pcount = L.ptr<uint32_t>(L.reserve((size_t)nunits * 8));
+          // per-(CTA, segment) partial slots: zeroed every call (SignOp::end_segment)
+          s.partial = L.commit ? reinterpret_cast<double*>(p.zero + hist_cursor) : nullptr;
+          s.pcount = L.commit ? reinterpret_cast<uint32_t*>(p.zero + hist_cursor + round_up((size_t)nunits * 16, 256))
+                              : nullptr;
+          hist_cursor += round_up((size_t)nunits * 16, 256) + round_up((size_t)nunits * 8, 256);
         }
         if (none) s.chunk = b.send.base ? b.send.at(lr) + b.coff[ti] : nullptr;
         T.h1.push_back(s);
@@ -390,6 +394,11 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
         if (dgc)
           nhist += (6144 * 4 + round_up((size_t)div_up(div_up(len, kRun), kRunsPerGroup) * 8, 256)) *
                    p.w->nlocal;
+        // sign: per-tile partial sums (16 B) and counts (8 B)
+        if (is_quant(b.kind)) {
+          const size_t nu = div_up(len, kDgcTile);
+          nhist += (round_up(nu * 16, 256) + round_up(nu * 8, 256)) * p.w->nlocal;
+        }
       }
       nst += (size_t)segs * p.w->nlocal;
       if (is_quant(b.kind)) nst += (size_t)p.w->nlocal;   // a7 (upper bound)
@@ -549,8 +558,8 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st) {
       launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1);
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
-    case ESP_EFSIGNSGD: launch_sign_h1(K_EFSIGN, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
-    case ESP_ONEBIT: launch_sign_h1(K_ONEBIT, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
+    case ESP_EFSIGNSGD: launch_sign_h1_tma(K_EFSIGN, b.h1, b.h1_units, b.nh1_units, st); break;
+    case ESP_ONEBIT: launch_sign_h1_tma(K_ONEBIT, b.h1, b.h1_units, b.nh1_units, st); break;
     default: launch_pack(b.h1, b.h1_units, b.nh1_units, st); break;
   }
   if (e1 && !dgc) ESP_CUDA(cudaEventRecord(e1, st));
