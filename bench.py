@@ -233,6 +233,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bucket-elems", type=int, default=0)
+    ap.add_argument("--phases", action="store_true", help="print a serialised h1/comm/mid/h2 breakdown to stderr")
     args = ap.parse_args()
     _claim_stdout()
     args.warmup = max(3, args.warmup)
@@ -312,6 +313,21 @@ def main():
     t_mean = max_over_ranks(sum(step_ms) / len(step_ms), ws)
     t_med = statistics.median(step_ms)
 
+    # ---- optional per-phase breakdown (serialised phases; diagnostics on stderr)
+    phases = None
+    if args.phases:
+        world.set_timing(True)
+        acc = {}
+        for _ in range(5):
+            g.copy_(g0)
+            step()
+            for k_, v_ in world.last_timing().items():
+                acc[k_] = acc.get(k_, 0.0) + v_ / 5
+        world.set_timing(False)
+        phases = {k_: max_over_ranks(v_, ws) for k_, v_ in acc.items()}
+        if rank == 0:
+            print("phases (ms, serialised, max over ranks):", json.dumps(phases), file=sys.stderr)
+
     # ---- e2e: host gradients (pinned) -> device, sync, result -> host
     out_host = torch.empty_like(host).pin_memory() if args.e2e_steps else None
     e2e_ms = None
@@ -365,6 +381,7 @@ def main():
                     "ms_per_step": e2e_ms},
             "gpu_launches": launches,
             "clocks": clk,
+            **({"phases_ms_serialised": phases} if phases else {}),
         }
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args, model, rule, sizes, names, 1)

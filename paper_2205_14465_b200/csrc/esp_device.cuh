@@ -78,6 +78,24 @@ __device__ __forceinline__ void store4_guard(float* base, uint32_t e, uint32_t n
   if (e + 2 < n) base[e + 2] = v.z;
 }
 
+// x / d for the aggregation divisor d (reading R9: IEEE division).  For a
+// power-of-two d the product with the exact reciprocal is the same correctly
+// rounded value (also for subnormal results), at a fraction of the cost; n =
+// 1, 2, 4, 8 ranks are all powers of two.
+struct Divisor {
+  float d, rcp;
+  bool pow2;
+  __device__ __forceinline__ explicit Divisor(float dd) : d(dd) {
+    const uint32_t b = __float_as_uint(dd);
+    pow2 = (b & 0x007FFFFFu) == 0 && ((b >> 23) & 0xFF) > 0 && ((b >> 23) & 0xFF) < 254;
+    rcp = pow2 ? __uint_as_float((uint32_t)(254 - ((b >> 23) & 0xFF)) << 23) : 0.f;
+  }
+  __device__ __forceinline__ float operator()(float x) const { return pow2 ? __fmul_rn(x, rcp) : __fdiv_rn(x, d); }
+  __device__ __forceinline__ float4 operator()(float4 v) const {
+    return make_float4((*this)(v.x), (*this)(v.y), (*this)(v.z), (*this)(v.w));
+  }
+};
+
 // ---- CTA-wide scans / reductions for 256 threads ---------------------------------
 // BAR = 0: __syncthreads; BAR > 0: named barrier BAR over the first 256 threads
 // (the consumer warps of a warp-specialised kernel).

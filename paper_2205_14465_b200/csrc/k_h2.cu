@@ -69,15 +69,12 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_kernel(const SegH2* __rest
     }
     __syncthreads();
   }
-  const float d = S.divisor;
+  const Divisor div(S.divisor);
+  const bool ones = S.divisor == 1.0f;
   for (uint32_t i = threadIdx.x * 4; lo + i < hi; i += kThreads * 4) {
     float4 v = *reinterpret_cast<const float4*>(acc + i);
-    if (d != 1.0f) {
-      v.x = __fdiv_rn(v.x, d);
-      v.y = __fdiv_rn(v.y, d);
-      v.z = __fdiv_rn(v.z, d);
-      v.w = __fdiv_rn(v.w, d);
-    }
+    // most of a sparse tile is +0 (+0 / d = +0): divide only touched words
+    if (!ones && (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)) v = div(v);
     store4_guard(seg_out(S), lo + i, S.n, v);
   }
 }
@@ -100,7 +97,8 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
     sh_w[r] = reinterpret_cast<const uint32_t*>(h + 16);
   }
   __syncthreads();
-  const float d = S.divisor;
+  const Divisor div(S.divisor);
+  const bool ones = S.divisor == 1.0f;
 #pragma unroll 2
   for (int j = 0; j < kUnit / (kThreads * 4); ++j) {
     const uint32_t e = u * kUnit + (j * kThreads + threadIdx.x) * 4;
@@ -114,12 +112,7 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
       acc.z = __fadd_rn(acc.z, (nib & 4) ? sp : sn);
       acc.w = __fadd_rn(acc.w, (nib & 8) ? sp : sn);
     }
-    if (d != 1.0f) {
-      acc.x = __fdiv_rn(acc.x, d);
-      acc.y = __fdiv_rn(acc.y, d);
-      acc.z = __fdiv_rn(acc.z, d);
-      acc.w = __fdiv_rn(acc.w, d);
-    }
+    if (!ones) acc = div(acc);
     store4_guard(seg_out(S), e, n, acc);
   }
 }
@@ -133,7 +126,8 @@ __global__ void __launch_bounds__(kThreads) h2_dense_kernel(const SegH2* __restr
   const SegH2 S = segs[sid];
   const uint32_t u = blockIdx.x - S.unit0;
   const uint32_t n = S.n;
-  const float d = S.divisor;
+  const Divisor div(S.divisor);
+  const bool ones = S.divisor == 1.0f;
   for (int j = 0; j < kUnit / (kThreads * 4); ++j) {
     const uint32_t e = u * kUnit + (j * kThreads + threadIdx.x) * 4;
     if (e >= n) break;
@@ -145,12 +139,7 @@ __global__ void __launch_bounds__(kThreads) h2_dense_kernel(const SegH2* __restr
       acc.z = __fadd_rn(acc.z, v.z);
       acc.w = __fadd_rn(acc.w, v.w);
     }
-    if (d != 1.0f) {
-      acc.x = __fdiv_rn(acc.x, d);
-      acc.y = __fdiv_rn(acc.y, d);
-      acc.z = __fdiv_rn(acc.z, d);
-      acc.w = __fdiv_rn(acc.w, d);
-    }
+    if (!ones) acc = div(acc);
     store4_guard(seg_out(S), e, n, acc);
   }
 }

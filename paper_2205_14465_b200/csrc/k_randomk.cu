@@ -103,12 +103,8 @@ __global__ void __launch_bounds__(kThreads) h2_randomk_kernel(const SegH2* __res
         }
       }
     }
-    if (S.divisor != 1.0f) {
-      acc.x = __fdiv_rn(acc.x, S.divisor);
-      acc.y = __fdiv_rn(acc.y, S.divisor);
-      acc.z = __fdiv_rn(acc.z, S.divisor);
-      acc.w = __fdiv_rn(acc.w, S.divisor);
-    }
+    if (S.divisor != 1.0f && (acc.x != 0.f || acc.y != 0.f || acc.z != 0.f || acc.w != 0.f))
+      acc = Divisor(S.divisor)(acc);
     store4_guard(seg_out(S), e, n, acc);
   }
 }

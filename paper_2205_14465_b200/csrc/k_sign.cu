@@ -81,10 +81,7 @@ __global__ void __launch_bounds__(kThreads) sign_h1_kernel(const SegH1* __restri
       if (S.divisor != 1.0f) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          xv[j].x = __fdiv_rn(xv[j].x, S.divisor);
-          xv[j].y = __fdiv_rn(xv[j].y, S.divisor);
-          xv[j].z = __fdiv_rn(xv[j].z, S.divisor);
-          xv[j].w = __fdiv_rn(xv[j].w, S.divisor);
+          xv[j] = Divisor(S.divisor)(xv[j]);
         }
       }
     } else {
