@@ -118,6 +118,7 @@ struct RandomkOp {
   __device__ void begin_segment(const SegH1& S, State& st) const {
     st.h = randomk_hash(S.hash, *S.step, S.part, S.rankterm);
   }
+  template <bool FULL>
   __device__ void run(const SegH1& S, const float4 (&gv)[kNJ], const float4 (&rv)[kNJ], uint32_t base,
                       State& st) const {
     const uint32_t n = S.n, k = S.k;

@@ -193,6 +193,7 @@ struct SignOp {
     st.s0 = st.s1 = 0.0;
     st.c0 = st.c1 = 0;
   }
+  template <bool FULL>
   __device__ void run(const SegH1& S, const float4 (&gv)[kNJ], const float4 (&rv)[kNJ], uint32_t base,
                       State& st) const {
     const uint32_t n = S.n;
@@ -210,12 +211,13 @@ struct SignOp {
           const float rt = __fsub_rn(q, q >= 0.f ? st.sp : st.sn);   // lazy residual
           f4set(p, c, __fadd_rn(f4get(gv[j], c), rt));
         }
-        store4_guard(S.r, e, n, p);
+        if (FULL) st4(S.r + e, p);
+        else store4_guard(S.r, e, n, p);
       }
       uint32_t nib = 0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        if (e + c < n) {
+        if (FULL || e + c < n) {
           const float v = f4get(p, c);
           const bool b = v >= 0.f;
           nib |= (uint32_t)b << c;

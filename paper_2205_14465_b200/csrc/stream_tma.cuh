@@ -55,7 +55,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1)
       const float* rseg = nullptr;
       bool ef = false;
       uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
-      for (uint32_t u = u0, i = 0; u < u1; ++u, ++i) {
+      int stage = 0;
+      uint32_t phase = 0;
+      bool wrapped = false;
+      for (uint32_t u = u0; u < u1; ++u) {
         const uint32_t sid = sid_next;
         if (u + 1 < u1) sid_next = unit_seg[u + 1];
         if (sid != cur) {
@@ -67,9 +70,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1)
           rseg = S.r;
           ef = S.ef != 0;
         }
-        const int stage = i % ns;
-        const uint32_t round = i / ns;
-        if (round > 0) mbar_wait(&hdr.empty[stage], (round - 1) & 1);
+        if (wrapped) mbar_wait(&hdr.empty[stage], phase ^ 1);
         const uint32_t start = (u - unit0) * kDgcTile;
         const uint32_t len = min((uint32_t)kDgcTile, n - start);
         const float* g = gseg + start;
@@ -82,6 +83,11 @@ __global__ void __launch_bounds__(kThreads + 32, 1)
         } else {
           mbar_arrive(&hdr.full[stage]);
         }
+        if (++stage == ns) {
+          stage = 0;
+          phase ^= 1;
+          wrapped = true;
+        }
       }
     }
     return;
@@ -92,9 +98,9 @@ __global__ void __launch_bounds__(kThreads + 32, 1)
   const float* g = nullptr;
   SegH1 S{};
   uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
-  for (uint32_t u = u0, i = 0; u < u1; ++u, ++i) {
-    const int stage = i % ns;
-    const uint32_t round = i / ns;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (uint32_t u = u0; u < u1; ++u) {
     const uint32_t sid = sid_next;
     if (u + 1 < u1) sid_next = unit_seg[u + 1];
     if (sid != cur) {
@@ -112,24 +118,40 @@ __global__ void __launch_bounds__(kThreads + 32, 1)
     const uint32_t len = min((uint32_t)kDgcTile, n - start);
     const uint32_t bytes = (len * 4) & ~15u;
     const bool tma = bytes && al16(g + start) && (!S.ef || al16(S.r + start));
-    mbar_wait(&hdr.full[stage], round & 1);
+    mbar_wait(&hdr.full[stage], phase);
     const uint32_t lbase = warp * kRun;
     const uint32_t base = start + lbase;
+    const bool full = tma && start + kDgcTile <= n;   // whole tile staged, no bounds
     float4 gv[kNJ], rv[kNJ];
+    if (full) {
+      const float* sg = tma_stage_g(smem_raw, stage) + lbase + lane * 4;
+      const float* sr = tma_stage_r(smem_raw, stage) + lbase + lane * 4;
 #pragma unroll
-    for (int j = 0; j < kNJ; ++j) {
-      const uint32_t l = lbase + j * 128 + lane * 4;
-      if (tma && l + 4 <= bytes / 4) {
-        gv[j] = lds4(tma_stage_g(smem_raw, stage) + l);
-        rv[j] = S.ef ? lds4(tma_stage_r(smem_raw, stage) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
-      } else {
-        gv[j] = load4_guard(g, start + l, n);
-        rv[j] = S.ef ? load4_guard(S.r, start + l, n) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < kNJ; ++j) {
+        gv[j] = lds4(sg + j * 128);
+        rv[j] = S.ef ? lds4(sr + j * 128) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kNJ; ++j) {
+        const uint32_t l = lbase + j * 128 + lane * 4;
+        if (tma && l + 4 <= bytes / 4) {
+          gv[j] = lds4(tma_stage_g(smem_raw, stage) + l);
+          rv[j] = S.ef ? lds4(tma_stage_r(smem_raw, stage) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          gv[j] = load4_guard(g, start + l, n);
+          rv[j] = S.ef ? load4_guard(S.r, start + l, n) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&hdr.empty[stage]);
-    op.run(S, gv, rv, base, st);
+    if (++stage == ns) {
+      stage = 0;
+      phase ^= 1;
+    }
+    if (full) op.template run<true>(S, gv, rv, base, st);
+    else op.template run<false>(S, gv, rv, base, st);
   }
   if (cur != 0xFFFFFFFFu) op.end_segment(S, cur_units, first_unit, st, hdr);
 }
