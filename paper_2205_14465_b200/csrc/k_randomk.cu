@@ -115,12 +115,13 @@ struct RandomkOp {
   struct State {
     uint64_t h;
   };
-  __device__ void begin_segment(const SegH1& S, State& st) const {
+  __device__ void begin_segment(const SegH1& S, State& st, TmaHdr&) const {
     st.h = randomk_hash(S.hash, *S.step, S.part, S.rankterm);
   }
+  const unsigned char* const* pieces = nullptr;   // not a decoding op
   template <bool FULL>
   __device__ void run(const SegH1& S, const float4 (&gv)[kNJ], const float4 (&rv)[kNJ], uint32_t base,
-                      State& st) const {
+                      State& st, TmaHdr&, const uint32_t*) const {
     const uint32_t n = S.n, k = S.k;
     if (base >= n) return;
     const int lane = threadIdx.x & 31;

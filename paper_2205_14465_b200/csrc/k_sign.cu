@@ -177,14 +177,30 @@ __global__ void __launch_bounds__(kThreads) sign_h1_kernel(const SegH1* __restri
 
 // ---- the same h1 on the persistent TMA streaming driver (stream_tma.cuh):
 // tiles of 4096 elements, 512 per warp (16 sign words per warp and tile).
-template <int KIND>
+// DECODE: the input is the decode-mean of S.npieces received chunks (a7, the
+// mid-scheme recompression); the r stream is then the second residual r2.
+template <int KIND, bool DECODE = false>
 struct SignOp {
+  const unsigned char* const* pieces = nullptr;
   struct State {
     float sp, sn;
     double s0, s1;
     uint32_t c0, c1;
   };
-  __device__ void begin_segment(const SegH1& S, State& st) const {
+  __device__ void begin_segment(const SegH1& S, State& st, TmaHdr& h) const {
+    if (DECODE) {
+      // stage the segment's piece table (scales, word pointers) in shared memory
+      csync<1>();
+      for (uint32_t q = threadIdx.x; q < S.npieces; q += kThreads) {
+        const unsigned char* p = pieces[S.piece0 + q];
+        float a, b;
+        piece_scales<KIND>(p, &a, &b);
+        h.psp[q] = a;
+        h.psn[q] = b;
+        h.pw[q] = reinterpret_cast<const uint32_t*>(p + 16);
+      }
+      csync<1>();
+    }
     st.sp = st.sn = 0.f;
     if (S.ef) {
       const float a = __ldcg(S.lazy_in), b = __ldcg(S.lazy_in + 1);
@@ -195,21 +211,69 @@ struct SignOp {
   }
   template <bool FULL>
   __device__ void run(const SegH1& S, const float4 (&gv)[kNJ], const float4 (&rv)[kNJ], uint32_t base,
-                      State& st) const {
+                      State& st, TmaHdr& h, const uint32_t* sw) const {
     const uint32_t n = S.n;
     if (base >= n) return;   // warp-uniform
     const int lane = threadIdx.x & 31;
+    float4 xv[kNJ];
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) xv[j] = gv[j];
+    if (DECODE) {
+      // rank-order fp32 sum of the decoded chunks from +0, then / divisor (R9);
+      // the words of up to 8 pieces are loaded in one batch before any is used
+#pragma unroll
+      for (int j = 0; j < kNJ; ++j) xv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t q0 = 0; q0 < S.npieces; q0 += 8) {
+        const uint32_t qn = min(8u, S.npieces - q0);
+        uint32_t wb[8][kNJ];
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q) {
+          if (q < qn) {
+#pragma unroll
+            for (int j = 0; j < kNJ; ++j) {
+              const uint32_t e = base + j * 128 + lane * 4;
+              const uint32_t l = (base & (kDgcTile - 1)) + j * 128 + lane * 4;   // tile-relative
+              wb[q][j] = !(FULL || e < n) ? 0u
+                         : sw             ? sw[(q0 + q) * (kDgcTile / 32) + (l >> 5)]
+                                          : __ldg(h.pw[q0 + q] + (e >> 5));
+            }
+          }
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q) {
+          if (q < qn) {
+            const float psp = h.psp[q0 + q], psn = h.psn[q0 + q];
+#pragma unroll
+            for (int j = 0; j < kNJ; ++j) {
+              const uint32_t e = base + j * 128 + lane * 4;
+              if (FULL || e < n) {
+                const uint32_t nib = (wb[q][j] >> (e & 31)) & 0xFu;
+                xv[j].x = __fadd_rn(xv[j].x, (nib & 1) ? psp : psn);
+                xv[j].y = __fadd_rn(xv[j].y, (nib & 2) ? psp : psn);
+                xv[j].z = __fadd_rn(xv[j].z, (nib & 4) ? psp : psn);
+                xv[j].w = __fadd_rn(xv[j].w, (nib & 8) ? psp : psn);
+              }
+            }
+          }
+        }
+      }
+      if (S.divisor != 1.0f) {
+        const Divisor div(S.divisor);
+#pragma unroll
+        for (int j = 0; j < kNJ; ++j) xv[j] = div(xv[j]);
+      }
+    }
     uint32_t myword = 0;
 #pragma unroll
     for (int j = 0; j < kNJ; ++j) {
       const uint32_t e = base + j * 128 + lane * 4;
-      float4 p = gv[j];
+      float4 p = xv[j];
       if (S.ef) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const float q = f4get(rv[j], c);
           const float rt = __fsub_rn(q, q >= 0.f ? st.sp : st.sn);   // lazy residual
-          f4set(p, c, __fadd_rn(f4get(gv[j], c), rt));
+          f4set(p, c, __fadd_rn(f4get(xv[j], c), rt));
         }
         if (FULL) st4(S.r + e, p);
         else store4_guard(S.r, e, n, p);
@@ -357,27 +421,29 @@ void launch_sign_h1(int kind, const SegH1* segs, const uint32_t* unit_seg, int n
 int tma_stream_grid(int nunits);
 int tma_stream_stages();
 
-void launch_sign_h1_tma(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st) {
-  if (nunits == 0) return;
+template <class Op>
+static void launch_tma_op(const SegH1* segs, const uint32_t* unit_seg, int nunits, Op op, cudaStream_t st) {
+  static bool init = [] {
+    return cudaFuncSetAttribute(tma_stream_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kTmaHdrBytes + kTmaMaxStages * kTmaStageBytes)) == cudaSuccess;
+  }();
+  (void)init;
   const int ns = tma_stream_stages();
-  const size_t smem = kTmaHdrBytes + ns * kTmaStageBytes;
-  const int grid = tma_stream_grid(nunits);
-  if (kind == K_EFSIGN) {
-    static bool init = [] {
-      return cudaFuncSetAttribute(tma_stream_kernel<SignOp<K_EFSIGN>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(kTmaHdrBytes + kTmaMaxStages * kTmaStageBytes)) == cudaSuccess;
-    }();
-    (void)init;
-    tma_stream_kernel<<<grid, kThreads + 32, smem, st>>>(segs, unit_seg, (uint32_t)nunits, ns, SignOp<K_EFSIGN>{});
-  } else {
-    static bool init = [] {
-      return cudaFuncSetAttribute(tma_stream_kernel<SignOp<K_ONEBIT>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(kTmaHdrBytes + kTmaMaxStages * kTmaStageBytes)) == cudaSuccess;
-    }();
-    (void)init;
-    tma_stream_kernel<<<grid, kThreads + 32, smem, st>>>(segs, unit_seg, (uint32_t)nunits, ns, SignOp<K_ONEBIT>{});
-  }
+  tma_stream_kernel<<<tma_stream_grid(nunits), kThreads + 32, kTmaHdrBytes + ns * kTmaStageBytes, st>>>(
+      segs, unit_seg, (uint32_t)nunits, ns, op);
   count_launches(1);
+}
+
+void launch_sign_h1_tma(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits,
+                        const unsigned char* const* pieces, cudaStream_t st) {
+  if (nunits == 0) return;
+  if (kind == K_EFSIGN) {
+    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, true>{pieces}, st);
+    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, false>{}, st);
+  } else {
+    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, true>{pieces}, st);
+    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, false>{}, st);
+  }
 }
 
 void launch_sign_materialize(int kind, const float* p, const float* lazy, float* out, uint32_t n,

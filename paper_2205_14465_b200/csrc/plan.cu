@@ -254,10 +254,11 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.chunk = b.mid.base ? b.mid.at(lr) + b.coff[ti] : nullptr;
         s.n = len;
         s.kpad = c->kpad;
-        s.nunits = div_up(len, kUnit);
+        s.nunits = div_up(len, kDgcTile);
         s.unit0 = u0;
         u0 += s.nunits;
         s.ef = c->cfg.error_feedback ? 1 : 0;
+        s.bflag = bflag;
         s.npieces = (uint32_t)n;
         s.piece0 = (uint32_t)T.a7_pieces.size();
         s.divisor = divisor;
@@ -265,8 +266,11 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           T.a7_pieces.push_back(b.recv1.base ? b.recv1.at(lr) + (size_t)r * S + b.coff[ti] : nullptr);
         s.st = L.ptr<SelState>(zero_off_st + st_cursor * sizeof(SelState));
         ++st_cursor;
-        s.partial = L.ptr<double>(L.reserve((size_t)s.nunits * 16));
-        s.pcount = L.ptr<uint32_t>(L.reserve((size_t)s.nunits * 8));
+        // per-(CTA, segment) partial slots, zeroed every call (SignOp::end_segment)
+        s.partial = L.commit ? reinterpret_cast<double*>(p.zero + hist_cursor) : nullptr;
+        s.pcount = L.commit ? reinterpret_cast<uint32_t*>(p.zero + hist_cursor + round_up((size_t)s.nunits * 16, 256))
+                            : nullptr;
+        hist_cursor += round_up((size_t)s.nunits * 16, 256) + round_up((size_t)s.nunits * 8, 256);
         T.a7.push_back(s);
         fill_unit_table(T.a7_units, (uint32_t)(T.a7.size() - 1 - a7_first), s.nunits);
       }
@@ -401,7 +405,11 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
         }
       }
       nst += (size_t)segs * p.w->nlocal;
-      if (is_quant(b.kind)) nst += (size_t)p.w->nlocal;   // a7 (upper bound)
+      if (is_quant(b.kind)) {
+        nst += (size_t)p.w->nlocal;   // a7 (upper bound)
+        const size_t nu = div_up(c->N, kDgcTile);   // a7 partial slots (upper bound: whole tensor)
+        nhist += (round_up(nu * 16, 256) + round_up(nu * 8, 256)) * p.w->nlocal;
+      }
     }
   }
   const size_t st_bytes = round_up(nst * sizeof(SelState), 256);
@@ -558,8 +566,8 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st) {
       launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1);
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
-    case ESP_EFSIGNSGD: launch_sign_h1_tma(K_EFSIGN, b.h1, b.h1_units, b.nh1_units, st); break;
-    case ESP_ONEBIT: launch_sign_h1_tma(K_ONEBIT, b.h1, b.h1_units, b.nh1_units, st); break;
+    case ESP_EFSIGNSGD: launch_sign_h1_tma(K_EFSIGN, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
+    case ESP_ONEBIT: launch_sign_h1_tma(K_ONEBIT, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
     default: launch_pack(b.h1, b.h1_units, b.nh1_units, st); break;
   }
   if (e1 && !dgc) ESP_CUDA(cudaEventRecord(e1, st));
@@ -569,7 +577,7 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st) {
 
 static void run_mid(Plan& p, Bucket& b, cudaStream_t cs) {
   const int k = b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT;
-  launch_sign_h1(k, b.a7, b.a7_units, b.na7_units, b.a7_pieces, cs);
+  launch_sign_h1_tma(k, b.a7, b.a7_units, b.na7_units, b.a7_pieces, cs);
   ESP_CUDA(cudaGetLastError());
 }
 

@@ -15,12 +15,16 @@
 namespace esp {
 
 constexpr int kTmaMaxStages = 6;
+constexpr int kMaxPiecesTma = 64;
 struct TmaHdr {
   uint64_t full[kTmaMaxStages], empty[kTmaMaxStages];
   double red[16];
   uint32_t scan[280];
   uint32_t misc[8];
   int flag;
+  // per-segment piece table of decoding ops (a7): scales and word pointers
+  float psp[kMaxPiecesTma], psn[kMaxPiecesTma];
+  const uint32_t* pw[kMaxPiecesTma];
 };
 constexpr size_t kTmaHdrBytes = (sizeof(TmaHdr) + 127) / 128 * 128;
 constexpr size_t kTmaStageBytes = 2 * kDgcTile * sizeof(float);
@@ -54,6 +58,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1)
       const float* gseg = nullptr;
       const float* rseg = nullptr;
       bool ef = false;
+      uint32_t npieces = 0, piece0 = 0;
       uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
       int stage = 0;
       uint32_t phase = 0;
@@ -66,9 +71,13 @@ __global__ void __launch_bounds__(kThreads + 32, 1)
           cur = sid;
           unit0 = S.unit0;
           n = S.n;
-          gseg = seg_g(S);
+          gseg = S.gptr ? seg_g(S) : nullptr;   // a7 segments have no g stream
           rseg = S.r;
           ef = S.ef != 0;
+          // decoding segments (a7): the tile's sign words of every piece are
+          // staged in the (unused) g slot, kDgcTile/32 words per piece
+          npieces = (!gseg && op.pieces) ? S.npieces : 0u;
+          piece0 = S.piece0;
         }
         if (wrapped) mbar_wait(&hdr.empty[stage], phase ^ 1);
         const uint32_t start = (u - unit0) * kDgcTile;
@@ -76,10 +85,15 @@ __global__ void __launch_bounds__(kThreads + 32, 1)
         const float* g = gseg + start;
         const float* r = rseg + start;
         const uint32_t bytes = (len * 4) & ~15u;
-        if (bytes && al16(g) && (!ef || al16(r))) {
-          mbar_arrive_expect_tx(&hdr.full[stage], bytes * (ef ? 2 : 1));
-          tma_load_1d(tma_stage_g(smem_raw, stage), g, bytes, &hdr.full[stage], pol);
+        const uint32_t wbytes = (((len + 31) / 32) * 4 + 15) & ~15u;
+        const uint32_t nstreams = (gseg ? 1u : 0u) + (ef ? 1u : 0u);
+        if (bytes && (nstreams || npieces) && (!gseg || al16(g)) && (!ef || al16(r))) {
+          mbar_arrive_expect_tx(&hdr.full[stage], bytes * nstreams + wbytes * npieces);
+          if (gseg) tma_load_1d(tma_stage_g(smem_raw, stage), g, bytes, &hdr.full[stage], pol);
           if (ef) tma_load_1d(tma_stage_r(smem_raw, stage), r, bytes, &hdr.full[stage], pol);
+          for (uint32_t q = 0; q < npieces; ++q)
+            tma_load_1d(tma_stage_g(smem_raw, stage) + q * (kDgcTile / 32),
+                        op.pieces[piece0 + q] + 16 + start / 8, wbytes, &hdr.full[stage], pol);
         } else {
           mbar_arrive(&hdr.full[stage]);
         }
@@ -107,51 +121,63 @@ __global__ void __launch_bounds__(kThreads + 32, 1)
       if (cur != 0xFFFFFFFFu) op.end_segment(S, cur_units, first_unit, st, hdr);
       cur = sid;
       S = segs[sid];
-      g = seg_g(S);
+      g = S.gptr ? seg_g(S) : nullptr;
       cur_units = 0;
       first_unit = u - S.unit0;
-      op.begin_segment(S, st);
+      op.begin_segment(S, st, hdr);
     }
     ++cur_units;
     const uint32_t start = (u - S.unit0) * kDgcTile;
     const uint32_t n = S.n;
     const uint32_t len = min((uint32_t)kDgcTile, n - start);
     const uint32_t bytes = (len * 4) & ~15u;
-    const bool tma = bytes && al16(g + start) && (!S.ef || al16(S.r + start));
+    const bool has_g = g != nullptr;
+    const bool dec = !has_g && op.pieces && S.npieces > 0;
+    const bool tma = bytes && (has_g || S.ef || dec) && (!has_g || al16(g + start)) && (!S.ef || al16(S.r + start));
     mbar_wait(&hdr.full[stage], phase);
     const uint32_t lbase = warp * kRun;
     const uint32_t base = start + lbase;
     const bool full = tma && start + kDgcTile <= n;   // whole tile staged, no bounds
+    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 gv[kNJ], rv[kNJ];
     if (full) {
       const float* sg = tma_stage_g(smem_raw, stage) + lbase + lane * 4;
       const float* sr = tma_stage_r(smem_raw, stage) + lbase + lane * 4;
 #pragma unroll
       for (int j = 0; j < kNJ; ++j) {
-        gv[j] = lds4(sg + j * 128);
-        rv[j] = S.ef ? lds4(sr + j * 128) : make_float4(0.f, 0.f, 0.f, 0.f);
+        gv[j] = has_g ? lds4(sg + j * 128) : zero4;
+        rv[j] = S.ef ? lds4(sr + j * 128) : zero4;
       }
     } else {
 #pragma unroll
       for (int j = 0; j < kNJ; ++j) {
         const uint32_t l = lbase + j * 128 + lane * 4;
         if (tma && l + 4 <= bytes / 4) {
-          gv[j] = lds4(tma_stage_g(smem_raw, stage) + l);
-          rv[j] = S.ef ? lds4(tma_stage_r(smem_raw, stage) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
+          gv[j] = has_g ? lds4(tma_stage_g(smem_raw, stage) + l) : zero4;
+          rv[j] = S.ef ? lds4(tma_stage_r(smem_raw, stage) + l) : zero4;
         } else {
-          gv[j] = load4_guard(g, start + l, n);
-          rv[j] = S.ef ? load4_guard(S.r, start + l, n) : make_float4(0.f, 0.f, 0.f, 0.f);
+          gv[j] = has_g ? load4_guard(g, start + l, n) : zero4;
+          rv[j] = S.ef ? load4_guard(S.r, start + l, n) : zero4;
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&hdr.empty[stage]);
+    // staged sign words of a decoding op are read inside run: release after it
+    const uint32_t* sw = (tma && dec) ? reinterpret_cast<const uint32_t*>(tma_stage_g(smem_raw, stage)) : nullptr;
+    const int used = stage;
+    if (!sw) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hdr.empty[used]);
+    }
     if (++stage == ns) {
       stage = 0;
       phase ^= 1;
     }
-    if (full) op.template run<true>(S, gv, rv, base, st);
-    else op.template run<false>(S, gv, rv, base, st);
+    if (full) op.template run<true>(S, gv, rv, base, st, hdr, sw);
+    else op.template run<false>(S, gv, rv, base, st, hdr, sw);
+    if (sw) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&hdr.empty[used]);
+    }
   }
   if (cur != 0xFFFFFFFFu) op.end_segment(S, cur_units, first_unit, st, hdr);
 }
