@@ -1,11 +1,17 @@
-// Randomk h1 on sm_100a (Randomk evaluated at a 1% rate,
-// P:1426; EF at P:1427).  One fused pass (12 B/elem): acc = g + r; the element
-// is selected iff it is the hashed pick of its stratum (reading R5); selected
-// values go to val[j], and r := selected ? 0 : acc.
+// Randomk on sm_100a (Randomk evaluated at a 1% rate,
+// P:1426; EF at P:1427).
 //
-// Stratum j covers [floor(jN/k), floor((j+1)N/k)); element i lies in stratum
-// ceil((i+1)k/N) - 1, so each float4 touches at most a few strata and needs
-// one or two hashes instead of four.
+// h1: one fused pass (12 B/elem) on the persistent TMA streaming driver: acc =
+// g + r; each stratum j = [floor(jN/k), floor((j+1)N/k)) picks one element
+// (reading R5); val[j] = acc[pick]; r := picked ? 0 : acc.  The work is
+// organised per stratum, not per element: a warp's 512-element run meets only
+// ~ρ·512 strata, whose picks (one 64-bit hash and division each) are computed
+// one per lane and applied through a per-warp shared-memory copy of the run's
+// acc values and a 512-bit pick mask.
+//
+// h2: per 8192-element tile, the picks of the tile's strata are accumulated
+// in shared memory piece by piece in rank order (every piece touches distinct
+// positions), then the tile is written once (÷ n).
 #include "esp_device.cuh"
 #include "esp_kernels.h"
 #include "stream_tma.cuh"
@@ -28,137 +34,107 @@ __device__ __forceinline__ uint32_t randomk_pick(uint64_t h, uint64_t j, uint64_
   return (uint32_t)(a + splitmix64(h ^ j) % (b - a));
 }
 
-__global__ void __launch_bounds__(kThreads) randomk_h1_kernel(const SegH1* __restrict__ segs,
-                                                              const uint32_t* __restrict__ unit_seg) {
-  const uint32_t sid = unit_seg[blockIdx.x];
-  const SegH1 S = segs[sid];
-  const uint32_t u = blockIdx.x - S.unit0;
-  const uint32_t n = S.n, k = S.k;
-  float* val = reinterpret_cast<float*>(S.chunk);
-  const float* g = seg_g(S);
-  const uint64_t h = randomk_hash(S.hash, *S.step, S.part, S.rankterm);
-#pragma unroll 2
-  for (int j = 0; j < kUnit / (kThreads * 4); ++j) {
-    const uint32_t e = u * kUnit + (j * kThreads + threadIdx.x) * 4;
-    if (e >= n) break;
-    float4 acc = load4_stream_guard(g, e, n);
-    if (S.ef) {
-      const float4 r = load4_guard(S.r, e, n);
-      acc.x = __fadd_rn(acc.x, r.x);
-      acc.y = __fadd_rn(acc.y, r.y);
-      acc.z = __fadd_rn(acc.z, r.z);
-      acc.w = __fadd_rn(acc.w, r.w);
-    }
-    const uint32_t last = min(e + 3, n - 1);
-    const uint64_t j0 = stratum_of(e, k, n), j1 = stratum_of(last, k, n);
-    uint32_t sel = 0;
-    for (uint64_t jj = j0; jj <= j1; ++jj) {
-      const uint32_t idx = randomk_pick(h, jj, k, n);
-      if (idx >= e && idx <= last) {
-        sel |= 1u << (idx - e);
-        val[jj] = f4get(acc, idx - e);
-      }
-    }
-    if (S.ef) {
-      float4 nr = acc;
-      if (sel & 1) nr.x = 0.f;
-      if (sel & 2) nr.y = 0.f;
-      if (sel & 4) nr.z = 0.f;
-      if (sel & 8) nr.w = 0.f;
-      store4_guard(S.r, e, n, nr);
-    }
-  }
-}
-
-// h2 for Randomk: out = reduce(sum over pieces of the scattered values).  Each
-// piece r carries its own hash base (identical for all r when indices are
-// shared); contributions are added in rank order.
-__global__ void __launch_bounds__(kThreads) h2_randomk_kernel(const SegH2* __restrict__ segs,
-                                                              const uint32_t* __restrict__ unit_seg,
-                                                              const unsigned char* const* __restrict__ pieces,
-                                                              const uint32_t* __restrict__ rankterms) {
-  const uint32_t sid = unit_seg[blockIdx.x];
-  const SegH2 S = segs[sid];
-  const uint32_t u = blockIdx.x - S.unit0;
-  const uint32_t n = S.n, k = S.k;
-  __shared__ uint64_t sh_h[64];
-  const uint64_t step = *S.step;
-  for (uint32_t r = threadIdx.x; r < S.npieces; r += kThreads)
-    sh_h[r] = randomk_hash(S.hash, step, S.part, rankterms[S.piece0 + r]);
-  __syncthreads();
-  for (int j = 0; j < kUnit / (kThreads * 4); ++j) {
-    const uint32_t e = u * kUnit + (j * kThreads + threadIdx.x) * 4;
-    if (e >= n) break;
-    const uint32_t last = min(e + 3, n - 1);
-    const uint64_t j0 = stratum_of(e, k, n), j1 = stratum_of(last, k, n);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t r = 0; r < S.npieces; ++r) {
-      const float* val = reinterpret_cast<const float*>(pieces[S.piece0 + r]);
-      const uint64_t h = sh_h[r];
-      for (uint64_t jj = j0; jj <= j1; ++jj) {
-        const uint32_t idx = randomk_pick(h, jj, k, n);
-        if (idx >= e && idx <= last) {
-          const int c = idx - e;
-          f4set(acc, c, __fadd_rn(f4get(acc, c), __ldg(val + jj)));
-        }
-      }
-    }
-    if (S.divisor != 1.0f && (acc.x != 0.f || acc.y != 0.f || acc.z != 0.f || acc.w != 0.f))
-      acc = Divisor(S.divisor)(acc);
-    store4_guard(seg_out(S), e, n, acc);
-  }
-}
-
-// The h1 on the persistent TMA streaming driver: per run of 512 elements,
-// acc = g + r, the hashed pick of each stratum touching a float4, r := sel ? 0 : acc.
+// ------------------------------------------------------------------ h1
 struct RandomkOp {
   struct State {
     uint64_t h;
   };
+  const unsigned char* const* pieces = nullptr;   // not a decoding op
   __device__ void begin_segment(const SegH1& S, State& st, TmaHdr&) const {
     st.h = randomk_hash(S.hash, *S.step, S.part, S.rankterm);
   }
-  const unsigned char* const* pieces = nullptr;   // not a decoding op
   template <bool FULL>
   __device__ void run(const SegH1& S, const float4 (&gv)[kNJ], const float4 (&rv)[kNJ], uint32_t base,
-                      State& st, TmaHdr&, const uint32_t*) const {
+                      State& st, TmaHdr& hd, const uint32_t*) const {
     const uint32_t n = S.n, k = S.k;
-    if (base >= n) return;
-    const int lane = threadIdx.x & 31;
-    float* val = reinterpret_cast<float*>(S.chunk);
+    if (base >= n) return;   // warp-uniform
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float* scr = hd.wscr[warp];
+    uint32_t* msk = hd.wsel[warp];
+    float4 av[kNJ];
 #pragma unroll
     for (int j = 0; j < kNJ; ++j) {
-      const uint32_t e = base + j * 128 + lane * 4;
-      if (e >= n) continue;
-      float4 acc = gv[j];
+      av[j] = gv[j];
       if (S.ef) {
-        acc.x = __fadd_rn(acc.x, rv[j].x);
-        acc.y = __fadd_rn(acc.y, rv[j].y);
-        acc.z = __fadd_rn(acc.z, rv[j].z);
-        acc.w = __fadd_rn(acc.w, rv[j].w);
+        av[j].x = __fadd_rn(gv[j].x, rv[j].x);
+        av[j].y = __fadd_rn(gv[j].y, rv[j].y);
+        av[j].z = __fadd_rn(gv[j].z, rv[j].z);
+        av[j].w = __fadd_rn(gv[j].w, rv[j].w);
       }
-      const uint32_t last = min(e + 3, n - 1);
-      const uint64_t j0 = stratum_of(e, k, n), j1 = stratum_of(last, k, n);
-      uint32_t sel = 0;
-      for (uint64_t jj = j0; jj <= j1; ++jj) {
-        const uint32_t idx = randomk_pick(st.h, jj, k, n);
-        if (idx >= e && idx <= last) {
-          sel |= 1u << (idx - e);
-          val[jj] = f4get(acc, idx - e);
+      *reinterpret_cast<float4*>(scr + j * 128 + lane * 4) = av[j];
+    }
+    if (lane < kRun / 32) msk[lane] = 0u;
+    __syncwarp();
+    const uint32_t hi = min(base + (uint32_t)kRun, n) - 1;   // last element of the run
+    const uint64_t j0 = stratum_of(base, k, n), j1 = stratum_of(hi, k, n);
+    float* val = reinterpret_cast<float*>(S.chunk);
+    for (uint64_t jb = j0; jb <= j1; jb += 32) {
+      const uint64_t jj = jb + lane;
+      if (jj <= j1) {
+        const uint32_t p = randomk_pick(st.h, jj, k, n);
+        if (p >= base && p <= hi) {   // the boundary strata may pick outside the run
+          const uint32_t off = p - base;
+          val[jj] = scr[off];
+          atomicOr(&msk[off >> 5], 1u << (off & 31));
         }
       }
-      if (S.ef) {
-        float4 nr = acc;
-        if (sel & 1) nr.x = 0.f;
-        if (sel & 2) nr.y = 0.f;
-        if (sel & 4) nr.z = 0.f;
-        if (sel & 8) nr.w = 0.f;
-        store4_guard(S.r, e, n, nr);
-      }
+    }
+    __syncwarp();
+    if (!S.ef) return;
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) {
+      const uint32_t off = j * 128 + lane * 4;
+      const uint32_t sel = (msk[off >> 5] >> (off & 31)) & 0xFu;
+      float4 nr = av[j];
+      if (sel & 1) nr.x = 0.f;
+      if (sel & 2) nr.y = 0.f;
+      if (sel & 4) nr.z = 0.f;
+      if (sel & 8) nr.w = 0.f;
+      if (FULL) st4(S.r + base + off, nr);
+      else store4_guard(S.r, base + off, n, nr);
     }
   }
   __device__ void end_segment(const SegH1&, uint32_t, uint32_t, State&, TmaHdr&) const {}
 };
+
+// ------------------------------------------------------------------ h2
+// out = reduce(sum over pieces of the scattered values); each piece carries
+// its own hash (identical for all pieces when indices are shared).
+__global__ void __launch_bounds__(kThreads) h2_randomk_kernel(const SegH2* __restrict__ segs,
+                                                              const uint32_t* __restrict__ unit_seg,
+                                                              const unsigned char* const* __restrict__ pieces,
+                                                              const uint32_t* __restrict__ rankterms) {
+  __shared__ __align__(16) float acc[kUnit];
+  __shared__ uint64_t sh_h[64];
+  const uint32_t sid = unit_seg[blockIdx.x];
+  const SegH2 S = segs[sid];
+  const uint32_t u = blockIdx.x - S.unit0;
+  const uint32_t n = S.n, k = S.k;
+  const uint32_t lo = u * kUnit, hi = min(lo + (uint32_t)kUnit, n) - 1;
+  const uint64_t step = *S.step;
+  for (uint32_t r = threadIdx.x; r < S.npieces; r += kThreads)
+    sh_h[r] = randomk_hash(S.hash, step, S.part, rankterms[S.piece0 + r]);
+  for (int i = threadIdx.x; i < kUnit / 4; i += kThreads)
+    reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  const uint64_t j0 = stratum_of(lo, k, n), j1 = stratum_of(hi, k, n);
+  for (uint32_t r = 0; r < S.npieces; ++r) {
+    const float* val = reinterpret_cast<const float*>(pieces[S.piece0 + r]);
+    const uint64_t h = sh_h[r];
+    for (uint64_t jj = j0 + threadIdx.x; jj <= j1; jj += kThreads) {
+      const uint32_t p = randomk_pick(h, jj, k, n);
+      if (p >= lo && p <= hi) acc[p - lo] = __fadd_rn(acc[p - lo], __ldg(val + jj));
+    }
+    __syncthreads();
+  }
+  const Divisor div(S.divisor);
+  const bool ones = S.divisor == 1.0f;
+  for (uint32_t i = threadIdx.x * 4; lo + i <= hi; i += kThreads * 4) {
+    float4 v = *reinterpret_cast<const float4*>(acc + i);
+    if (!ones && (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)) v = div(v);
+    store4_guard(seg_out(S), lo + i, n, v);
+  }
+}
 
 int tma_stream_grid(int nunits);
 int tma_stream_stages();

@@ -25,6 +25,9 @@ struct TmaHdr {
   // per-segment piece table of decoding ops (a7): scales and word pointers
   float psp[kMaxPiecesTma], psn[kMaxPiecesTma];
   const uint32_t* pw[kMaxPiecesTma];
+  // per-warp scratch of ops that address a run's elements by position (Randomk)
+  alignas(16) float wscr[kThreads / 32][kRun];
+  uint32_t wsel[kThreads / 32][kRun / 32];
 };
 constexpr size_t kTmaHdrBytes = (sizeof(TmaHdr) + 127) / 128 * 128;
 constexpr size_t kTmaStageBytes = 2 * kDgcTile * sizeof(float);
