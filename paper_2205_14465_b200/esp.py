@@ -146,6 +146,18 @@ def esp_launch_count() -> int:
     return int(lib().esp_launch_count())
 
 
+def exchange_unique_id(group=None) -> bytes:
+    """Rank 0 of the torch.distributed group creates the 128-byte ncclUniqueId
+    (esp_get_nccl_unique_id), every rank receives it (works over gloo or nccl)."""
+    import torch.distributed as dist
+    uid = (C.c_ubyte * 128)()
+    if dist.get_rank(group) == 0:
+        _check(lib().esp_get_nccl_unique_id(uid))
+    obj = [bytes(uid)]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
 class World:
     """esp_world_t.  `World.sim(n)`: n virtual ranks on one GPU;
     `World.nccl()`: one rank per process over torch.distributed's group."""
@@ -170,12 +182,7 @@ class World:
         import torch.distributed as dist
         rank, n = dist.get_rank(group), dist.get_world_size(group)
         device = torch.cuda.current_device() if device is None else device
-        uid = (C.c_ubyte * 128)()
-        if rank == 0:
-            _check(lib().esp_get_nccl_unique_id(uid))
-        obj = [bytes(uid)]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        uid = (C.c_ubyte * 128).from_buffer_copy(obj[0])
+        uid = (C.c_ubyte * 128).from_buffer_copy(exchange_unique_id(group))
         h = C.c_void_p()
         _check(lib().esp_world_create_nccl(uid, n, rank, device, C.byref(h)))
         return cls(h, device)
