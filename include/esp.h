@@ -69,7 +69,9 @@ typedef enum {
 
 /* Compressors the paper evaluates (Randomk, DGC at 1%, EFSignSGD;
  * App. D figures: Onebit).  TOPK = DGC's exact result without the sampled
- * threshold accelerator (reading R3).  NONE = uncompressed fp32. */
+ * threshold accelerator (reading R3): every element enters the exact radix
+ * select, the unsampled baseline DGC's threshold speeds up.  NONE =
+ * uncompressed fp32. */
 typedef enum {
   ESP_NONE = 0, ESP_RANDOMK = 1, ESP_DGC = 2, ESP_TOPK = 3, ESP_EFSIGNSGD = 4, ESP_ONEBIT = 5
 } esp_kind_t;

@@ -16,10 +16,6 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
                    cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr);
 // Randomk h1 (k_randomk.cu)
 void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
-// EFSignSGD / Onebit h1; with pieces != nullptr the input is the decode-mean of
-// npieces received chunks (mid-scheme a7, P:78-87 / P:105-115)  (k_sign.cu)
-void launch_sign_h1(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits,
-                    const unsigned char* const* pieces, cudaStream_t st);
 // h1 on the persistent TMA streaming driver, tiles of kDgcTile (k_sign.cu)
 // pieces != nullptr: a7 (input = decode-mean of the segment's pieces, r = r2)
 void launch_sign_h1_tma(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits,

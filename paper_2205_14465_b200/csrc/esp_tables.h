@@ -56,7 +56,8 @@ struct SegH1 {
   uint32_t nunits;
   uint32_t group0;       // DGC: first finalize group
   uint32_t ngroups;
-  uint32_t ef;           // error feedback on/off
+  uint16_t ef;           // error feedback on/off
+  uint16_t unsampled;    // TOPK: no sampled threshold, every element is a candidate
   uint64_t hash;         // Randomk: splitmix chain over (seed, tensor); DGC: sample hash
   uint32_t part;         // partition index (Randomk hash chain)
   uint32_t rankterm;     // 0 when indices are shared, rank + 1 otherwise (R5)

@@ -9,12 +9,13 @@
 //                   sample).  Only an accelerator: the result cannot depend on thr
 //                   (reading R3); too high a threshold triggers the fallback.
 //   2. dgc_stream   ONE persistent, warp-specialised pass over g and r (12 B/elem):
-//                   a producer warp streams 32 KB tiles of g and r into a 3-stage
+//                   a producer warp streams 16 KB tiles of g and of r into a 4-stage
 //                   shared-memory ring with 1D TMA bulk copies (cp.async.bulk +
 //                   mbarrier); 8 consumer warps compute acc = g + r, write r := acc,
-//                   compact candidates key(acc) >= thr per 1024-element run in index
-//                   order (ballot/popc) and histogram their top 11 key bits.  The
+//                   compact candidates key(acc) >= thr per 512-element run in index
+//                   order (vote/ballot/popc) and histogram their top 11 key bits.  The
 //                   CTA that completes a segment picks the radix bin of the k-th key.
+//                   (TOPK: thr = 0, every element is a candidate.)
 //   3. dgc_fallback only segments with < k candidates: recompact with thr = 0.
 //   4. dgc_refine   two more radix rounds over the candidates -> the exact k-th key
 //                   T, #above, #ties to take (ties broken by ascending index).
@@ -81,6 +82,10 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t sh[280];
   const SegH1 S = segs[blockIdx.x];
+  if (S.unsampled) {   // TOPK: the exact radix select runs over every element
+    if (threadIdx.x == 0) S.st->thr = 0;
+    return;
+  }
   const uint32_t n = S.n;
   const float* g = seg_g(S);
   const bool exact = n <= (uint32_t)kSample;
@@ -94,8 +99,11 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
       const uint32_t j = threadIdx.x + q * kThreads;
       uint32_t pos = j;
       if (!exact && j < s) {
-        const uint64_t a = (uint64_t)j * n / s, b = (uint64_t)(j + 1) * n / s;
-        pos = (uint32_t)(a + splitmix64(S.hash ^ j) % (b - a));
+        // stratum [jN/s, (j+1)N/s) with s = kSample = 2^12: shifts, no division;
+        // position within it by a multiply-high of the hash (a sampler only)
+        static_assert(kSample == 4096, "shift assumes kSample == 2^12");
+        const uint32_t a = (uint32_t)(((uint64_t)j * n) >> 12), b = (uint32_t)(((uint64_t)(j + 1) * n) >> 12);
+        pos = a + (uint32_t)(((uint64_t)(uint32_t)splitmix64(S.hash ^ j) * (b - a)) >> 32);
       }
       gv[q] = j < s ? __ldg(g + pos) : 0.f;
       rv[q] = (j < s && S.ef) ? S.r[pos] : 0.f;
@@ -443,65 +451,6 @@ __global__ void __launch_bounds__(kThreads + 32, 2) dgc_stream_kernel(const SegH
   if (cur != 0xFFFFFFFFu) stream_segment_done(S, cur_units, sm);
 }
 
-// ------------------------------------------------------------------ 2'. stream (LDG)
-// Alternative streaming pass: one 4096-element tile per CTA, 8 LDG.128 in flight
-// per lane, many resident CTAs per SM; candidate keys go straight to the
-// segment's global histogram (RED, ~0.25% of elements), the candidate count is
-// that histogram's total, and the CTA that completes a segment selects the bin.
-__global__ void __launch_bounds__(kThreads) dgc_stream_ldg_kernel(const SegH1* __restrict__ segs,
-                                                                  const uint32_t* __restrict__ unit_seg) {
-  __shared__ uint32_t sh[280];
-  __shared__ int sh_flag;
-  const uint32_t sid = unit_seg[blockIdx.x];
-  const SegH1& S = segs[sid];
-  const uint32_t u = blockIdx.x - S.unit0;
-  const uint32_t n = S.n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t base = u * kDgcTile + warp * kRun;
-  uint32_t* const ghist = S.hist;
-  if (base < n) {
-    const float* g = seg_g(S);
-    float* r = S.r;
-    const bool ef = S.ef != 0;
-    float4 gv[kNJ], rv[kNJ], av[kNJ];
-#pragma unroll
-    for (int j = 0; j < kNJ; ++j) gv[j] = load4_stream_guard(g, base + j * 128 + lane * 4, n);
-    if (ef) {
-#pragma unroll
-      for (int j = 0; j < kNJ; ++j) rv[j] = load4_guard(r, base + j * 128 + lane * 4, n);
-    }
-    const uint32_t thr = __ldcg(&S.st->thr);
-#pragma unroll
-    for (int j = 0; j < kNJ; ++j) {
-      if (ef) {
-        av[j].x = __fadd_rn(gv[j].x, rv[j].x);
-        av[j].y = __fadd_rn(gv[j].y, rv[j].y);
-        av[j].z = __fadd_rn(gv[j].z, rv[j].z);
-        av[j].w = __fadd_rn(gv[j].w, rv[j].w);
-        store4_guard(r, base + j * 128 + lane * 4, n, av[j]);
-      } else {
-        av[j] = gv[j];
-      }
-    }
-    const uint32_t run = base / kRun;
-    const uint32_t wc = emit_run(av, base, n, thr, S.cand + (size_t)run * kRun, ghist);
-    if (lane == 0) S.runcnt[run] = wc;
-  }
-  if (!last_cta(&S.st->done, S.nunits, &sh_flag)) return;
-  uint32_t bin, above, total;
-  select_bin<0, true>(ghist, 2048, S.k, &bin, &above, sh, &total);
-  if (threadIdx.x == 0) {
-    if (total < S.k) {
-      S.st->fallback = 1;
-      atomicAdd(S.bflag, 1u);
-    } else {
-      S.st->prefix = bin;
-      S.st->above = above;
-      S.st->need = S.k - above;
-    }
-  }
-}
-
 // ------------------------------------------------------------------ 3. fallback
 // Segments whose sampled threshold let fewer than k candidates through are
 // recompacted from acc (= r after the streaming pass) with thr = 0.  Every CTA
@@ -702,6 +651,9 @@ __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __rest
       is_above = key > T;
       is_tie = key == T;
     }
+    // chunks without any key >= T (most of them when the candidate set is loose,
+    // e.g. TOPK's unsampled set) add nothing: skip their two scans
+    if (!__syncthreads_or(is_above | is_tie)) continue;
     uint32_t ttot;
     const uint32_t trank = tie_run + block_excl_scan(is_tie, &ttot, sh_scan);
     const uint32_t sel = is_above || (is_tie && trank < need);
@@ -751,10 +703,6 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
   }();
   (void)attr_set;
   num_sms();
-  static const bool use_ldg = [] {
-    const char* e = getenv("ESP_DGC_STREAM");
-    return e && std::string(e) == "ldg";
-  }();
   // tuning knobs (measured on B200): bit0 of ESP_TMA_VARIANT = L2
   // evict-first hint on the tile loads, bit1 = 2 CTAs per SM; ESP_TMA_STAGES
   static const int variant = [] {
@@ -764,9 +712,7 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
   const int stages = tma_stream_stages();
   dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs);
   if (probe0) cudaEventRecord(probe0, st);
-  if (use_ldg) {
-    dgc_stream_ldg_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg);
-  } else {
+  {
     const int per_sm = (variant & 2) ? 2 : 1;
     const int ns = per_sm == 2 ? (stages > 3 ? 3 : stages) : stages;
     const int grid = nunits < per_sm * g_num_sms ? nunits : per_sm * g_num_sms;

@@ -16,6 +16,7 @@
 // With DECODE the input is not a gradient but the mean of npieces received
 // chunks: the mid-scheme "decompress, aggregate, recompress" of quantized
 // Alltoall/Allgather and Gather/Broadcast, fused.
+// Both run on the persistent TMA streaming driver (stream_tma.cuh).
 #include "esp_device.cuh"
 #include "esp_kernels.h"
 #include "stream_tma.cuh"
@@ -32,146 +33,6 @@ __device__ __forceinline__ void piece_scales(const unsigned char* h, float* sp, 
   } else {
     *sn = __ldg(f);
     *sp = __ldg(f + 1);
-  }
-}
-
-template <int KIND, bool DECODE>
-__global__ void __launch_bounds__(kThreads) sign_h1_kernel(const SegH1* __restrict__ segs,
-                                                           const uint32_t* __restrict__ unit_seg,
-                                                           const unsigned char* const* __restrict__ pieces) {
-  __shared__ double sh_d[8];
-  __shared__ uint32_t sh_u[16];
-  __shared__ int sh_flag;
-  const uint32_t sid = unit_seg[blockIdx.x];
-  const SegH1 S = segs[sid];
-  const uint32_t u = blockIdx.x - S.unit0;
-  const uint32_t n = S.n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t base = u * kUnit + warp * kSignSpan;
-  float sp = 0.f, sn = 0.f;
-  if (S.ef) {
-    const float a = S.lazy_in[0], b = S.lazy_in[1];
-    if (KIND == K_EFSIGN) { sp = a; sn = -a; } else { sp = b; sn = a; }
-  }
-  double s0 = 0.0, s1 = 0.0;
-  uint32_t c0 = 0, c1 = 0;
-  uint32_t myword = 0;
-  if (base < n) {
-    float4 xv[8], pv[8];
-    if (DECODE) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) xv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (uint32_t r = 0; r < S.npieces; ++r) {
-        const unsigned char* h = pieces[S.piece0 + r];
-        float psp, psn;
-        piece_scales<KIND>(h, &psp, &psn);
-        const uint32_t* words = reinterpret_cast<const uint32_t*>(h + 16);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t e = base + j * 128 + lane * 4;
-          if (e < n) {
-            const uint32_t nib = (__ldg(words + (e >> 5)) >> (e & 31)) & 0xFu;
-            xv[j].x = __fadd_rn(xv[j].x, (nib & 1) ? psp : psn);
-            xv[j].y = __fadd_rn(xv[j].y, (nib & 2) ? psp : psn);
-            xv[j].z = __fadd_rn(xv[j].z, (nib & 4) ? psp : psn);
-            xv[j].w = __fadd_rn(xv[j].w, (nib & 8) ? psp : psn);
-          }
-        }
-      }
-      if (S.divisor != 1.0f) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          xv[j] = Divisor(S.divisor)(xv[j]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) xv[j] = load4_stream_guard(seg_g(S), base + j * 128 + lane * 4, n);
-    }
-    if (S.ef) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) pv[j] = load4_guard(S.r, base + j * 128 + lane * 4, n);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t e = base + j * 128 + lane * 4;
-      float4 p = xv[j];
-      if (S.ef) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float q = f4get(pv[j], c);
-          const float rt = __fsub_rn(q, q >= 0.f ? sp : sn);   // lazy residual
-          f4set(p, c, __fadd_rn(f4get(xv[j], c), rt));
-        }
-        store4_guard(S.r, e, n, p);
-      }
-      uint32_t nib = 0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (e + c < n) {
-          const float v = f4get(p, c);
-          const bool b = v >= 0.f;
-          nib |= (uint32_t)b << c;
-          if (KIND == K_EFSIGN) {
-            s0 += fabs((double)v);
-          } else if (b) {
-            s1 += (double)v;
-            ++c1;
-          } else {
-            s0 += (double)v;
-            ++c0;
-          }
-        }
-      }
-      uint32_t word = nib << (4 * (lane & 7));
-      word |= __shfl_xor_sync(0xffffffffu, word, 1);
-      word |= __shfl_xor_sync(0xffffffffu, word, 2);
-      word |= __shfl_xor_sync(0xffffffffu, word, 4);
-      const uint32_t wv = __shfl_sync(0xffffffffu, word, (lane & 3) * 8);
-      if ((lane >> 2) == j) myword = wv;
-    }
-    uint32_t* words = reinterpret_cast<uint32_t*>(S.chunk + 16);
-    if (base + lane * 32 < n) words[(base >> 5) + lane] = myword;
-  }
-  s0 = block_sum_f64(s0, sh_d);
-  s1 = block_sum_f64(s1, sh_d);
-  c0 = block_sum_u32(c0, sh_u);
-  c1 = block_sum_u32(c1, sh_u);
-  if (threadIdx.x == 0) {
-    S.partial[2 * u] = s0;
-    S.partial[2 * u + 1] = s1;
-    S.pcount[2 * u] = c0;
-    S.pcount[2 * u + 1] = c1;
-  }
-  if (!last_cta(&S.st->done, S.nunits, &sh_flag)) return;
-  double a = 0.0, b = 0.0;
-  uint32_t ca = 0, cb = 0;
-  for (uint32_t v = threadIdx.x; v < S.nunits; v += kThreads) {
-    a += __ldcg(S.partial + 2 * v);
-    b += __ldcg(S.partial + 2 * v + 1);
-    ca += __ldcg(S.pcount + 2 * v);
-    cb += __ldcg(S.pcount + 2 * v + 1);
-  }
-  a = block_sum_f64(a, sh_d);
-  b = block_sum_f64(b, sh_d);
-  ca = block_sum_u32(ca, sh_u);
-  cb = block_sum_u32(cb, sh_u);
-  if (threadIdx.x == 0) {
-    float* hdr = reinterpret_cast<float*>(S.chunk);
-    float x0, x1;
-    if (KIND == K_EFSIGN) {
-      x0 = n ? (float)(a / (double)n) : 0.f;   // scale = ||p||_1 / N (R7)
-      x1 = 0.f;
-    } else {
-      x0 = ca ? (float)(a / (double)ca) : 0.f;  // mean of {p < 0} (R8)
-      x1 = cb ? (float)(b / (double)cb) : 0.f;  // mean of {p >= 0}
-    }
-    hdr[0] = x0;
-    if (KIND == K_ONEBIT) hdr[1] = x1;
-    if (S.ef) {   // without EF the state stays the zero residual
-      S.lazy_out[0] = x0;
-      S.lazy_out[1] = x1;
-    }
   }
 }
 
@@ -403,19 +264,6 @@ __global__ void sign_materialize_kernel(const float* __restrict__ p, const float
     const float q = p[i];
     out[i] = __fsub_rn(q, q >= 0.f ? sp : sn);
   }
-}
-
-void launch_sign_h1(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits,
-                    const unsigned char* const* pieces, cudaStream_t st) {
-  if (nunits == 0) return;
-  if (kind == K_EFSIGN) {
-    if (pieces) sign_h1_kernel<K_EFSIGN, true><<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
-    else sign_h1_kernel<K_EFSIGN, false><<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
-  } else {
-    if (pieces) sign_h1_kernel<K_ONEBIT, true><<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
-    else sign_h1_kernel<K_ONEBIT, false><<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
-  }
-  count_launches(1);
 }
 
 int tma_stream_grid(int nunits);

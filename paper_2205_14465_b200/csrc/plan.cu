@@ -173,6 +173,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.ngroups = div_up(nruns, kRunsPerGroup);
         s.group0 = group_cursor;
         s.ef = c->cfg.error_feedback ? 1 : 0;
+        s.unsampled = b.kind == ESP_TOPK ? 1 : 0;
         s.hash = b.kind == ESP_RANDOMK ? c->hash_base
                                        : host_splitmix64(c->tensor_id * 0x100000001b3ull + part);
         s.part = (uint32_t)part;

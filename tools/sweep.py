@@ -24,7 +24,7 @@ sys.path.insert(0, ROOT)
 
 from paper_2205_14465_b200 import esp as E  # noqa: E402
 
-COMPRESSORS = [("dgc", 0.01), ("dgc", 0.001), ("randomk", 0.01), ("efsignsgd", 1.0), ("onebit", 1.0)]
+COMPRESSORS = [("dgc", 0.01), ("dgc", 0.001), ("topk", 0.001), ("randomk", 0.01), ("efsignsgd", 1.0), ("onebit", 1.0)]
 L2_BYTES = 126 << 20
 
 
