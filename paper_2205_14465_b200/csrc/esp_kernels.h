@@ -10,10 +10,18 @@ namespace esp {
 void count_launches(int n);   // process-wide counter behind esp_launch_count()
 
 // DGC / TOPK h1 (k_dgc.cu)
-// probe0/probe1 (optional): events recorded around the streaming pass
+// probe0/probe1 (optional): events recorded around the streaming pass.
+// dsts != nullptr (fused Allgather over NVLink): the payload entries are stored
+// at dsts[q] + chunk_off for q < ndst (every rank's receive slot of this rank)
+// and each write CTA then increments every cnts[q] (system-scope release).
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st,
-                   cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr);
+                   cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr,
+                   unsigned char* const* dsts = nullptr, unsigned long long* const* cnts = nullptr,
+                   int ndst = 0);
+// block the stream until *cnt >= target (arrivals of a fused Allgather); traps
+// after ~10 s so that a missing peer becomes an error, not a hang
+void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, cudaStream_t st);
 // Randomk h1 (k_randomk.cu)
 void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 // h1 on the persistent TMA streaming driver, tiles of kDgcTile (k_sign.cu)

@@ -17,7 +17,8 @@ constexpr int kSignSpan = 1024;          // sign h1: elements per warp per unit
 constexpr int kUnit = 8192;              // 8 runs per CTA
 constexpr int kRunsPerGroup = 256;       // DGC finalize: 256 runs (262144 elements) per CTA
 constexpr int kSample = 4096;            // DGC sampled-threshold sample size
-constexpr int kTile = 8192;              // sparse h2 output tile (32 KB smem)
+constexpr int kTile = 4096;              // sparse h2 output tile (16 KB smem)
+constexpr int kTileThreads = 128;        // sparse h2 CTA size (up to 13 tiles in flight per SM)
 constexpr int kOffJob = 4096;            // sparse h2 tile-offset pass: entries per CTA
 
 enum Kind : int { K_NONE = 0, K_RANDOMK = 1, K_DGC = 2, K_TOPK = 3, K_EFSIGN = 4, K_ONEBIT = 5 };
@@ -47,6 +48,8 @@ struct SegH1 {
   const uint64_t* step;  // &dyn[nslots + slot]: step counter (Randomk draws)
   float* r;              // EF state: residual (sparse) / previous p (sign, lazy EF)
   unsigned char* chunk;  // output chunk
+  uint32_t chunk_off;    // the chunk's offset within a slot (fused Allgather destinations)
+  uint32_t pad0_;
   const float* lazy_in;  // sign: {scale} / onebit: {mneg, mpos} of the previous step
   float* lazy_out;       // written by the last CTA of the segment
   uint32_t n;            // segment length (elements)

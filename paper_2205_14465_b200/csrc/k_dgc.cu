@@ -592,7 +592,10 @@ __device__ __forceinline__ unsigned long long lb_pack(uint32_t flag, uint32_t ab
 }
 
 __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __restrict__ segs,
-                                                             const uint32_t* __restrict__ group_seg) {
+                                                             const uint32_t* __restrict__ group_seg,
+                                                             unsigned char* const* __restrict__ dsts,
+                                                             unsigned long long* const* __restrict__ cnts,
+                                                             int ndst) {
   __shared__ uint32_t sh_scan[16];
   __shared__ uint32_t sh_off[kRunsPerGroup + 1];
   __shared__ uint32_t sh_prefix[2];
@@ -660,13 +663,50 @@ __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __rest
     uint32_t stot;
     const uint32_t pos = sel_run + block_excl_scan(sel, &stot, sh_scan);
     if (sel) {
-      out_idx[pos] = c.x;
-      out_val[pos] = __uint_as_float(c.y);
+      if (dsts) {
+        // fused Allgather: the entry goes straight into this rank's slot of
+        // every rank's receive buffer over NVLink (consecutive threads write
+        // consecutive positions: coalesced peer stores)
+        for (int q = 0; q < ndst; ++q) {
+          unsigned char* ch = dsts[q] + S.chunk_off;
+          reinterpret_cast<uint32_t*>(ch)[pos] = c.x;
+          reinterpret_cast<float*>(ch + 4 * (size_t)S.kpad)[pos] = __uint_as_float(c.y);
+        }
+      } else {
+        out_idx[pos] = c.x;
+        out_val[pos] = __uint_as_float(c.y);
+      }
       if (S.ef) S.r[c.x] = 0.0f;
     }
     tie_run += ttot;
     sel_run += stot;
   }
+  if (dsts) {
+    // publish: the barrier orders the CTA's peer stores before thread 0's
+    // system-scope fence (cumulative), which precedes the arrival increments
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int q = 0; q < ndst; ++q) atomicAdd_system(cnts[q], 1ull);
+    }
+  }
+}
+
+__global__ void wait_arrivals_kernel(const unsigned long long* cnt, unsigned long long target) {
+  if (threadIdx.x != 0) return;
+  const long long t0 = clock64();
+  while (true) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+    if (v >= target) break;
+    __nanosleep(200);
+    if (clock64() - t0 > 20000000000ll) __trap();   // ~10 s: a peer never arrived
+  }
+}
+
+void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, cudaStream_t st) {
+  wait_arrivals_kernel<<<1, 32, 0, st>>>(cnt, target);
+  count_launches(1);
 }
 
 // ------------------------------------------------------------------ launchers
@@ -695,7 +735,8 @@ int tma_stream_stages() {
 
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
-                   cudaEvent_t probe1) {
+                   cudaEvent_t probe1, unsigned char* const* dsts, unsigned long long* const* cnts,
+                   int ndst) {
   if (nsegs == 0) return;
   static const bool attr_set = [] {
     return cudaFuncSetAttribute(dgc_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -723,7 +764,7 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
   dgc_fallback_kernel<<<g_num_sms, kThreads, 0, st>>>(segs, nsegs);
   dgc_refine_kernel<2><<<ngroups, kThreads, 0, st>>>(segs, group_seg);
   dgc_refine_kernel<3><<<ngroups, kThreads, 0, st>>>(segs, group_seg);
-  dgc_write_kernel<<<ngroups, kThreads, 0, st>>>(segs, group_seg);
+  dgc_write_kernel<<<ngroups, kThreads, 0, st>>>(segs, group_seg, dsts, cnts, ndst);
   count_launches(6);
 }
 

@@ -41,9 +41,10 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2
   }
 }
 
-__global__ void __launch_bounds__(kThreads) h2_sparse_kernel(const SegH2* __restrict__ segs,
-                                                             const uint32_t* __restrict__ tile_seg,
-                                                             const unsigned char* const* __restrict__ pieces) {
+__global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __restrict__ segs,
+                                                                 const uint32_t* __restrict__ tile_seg,
+                                                                 const unsigned char* const* __restrict__ pieces) {
+  constexpr int kThreads = kTileThreads;   // small CTAs: many independent tiles per SM
   __shared__ __align__(16) float acc[kTile];
   __shared__ uint32_t rlo[kMaxPieces], rhi[kMaxPieces];
   const uint32_t sid = tile_seg[blockIdx.x];
@@ -161,7 +162,7 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
                       const unsigned char* const* pieces, cudaStream_t st) {
   if (ntiles == 0) return;
   h2_sparse_offsets_kernel<<<njobs, kThreads, 0, st>>>(segs, jobs, pieces);
-  h2_sparse_kernel<<<ntiles, kThreads, 0, st>>>(segs, tile_seg, pieces);
+  h2_sparse_kernel<<<ntiles, kTileThreads, 0, st>>>(segs, tile_seg, pieces);
   count_launches(2);
 }
 

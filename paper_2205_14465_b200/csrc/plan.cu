@@ -37,6 +37,17 @@ struct Bucket {
   cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
+  // ---- fused Allgather over NVLink peer memory: the DGC
+  // write kernel stores every selected entry straight into all ranks' recv
+  // buffers (double-buffered by call parity) and bumps their arrival counters;
+  // h2 starts after a wait kernel has seen n x ngroups arrivals for this call.
+  bool fused = false;
+  size_t recv1_off = 0, cnt_off = 0;            // arena offsets (identical on every rank)
+  const unsigned char** h2_pieces_odd = nullptr;   // h2 pieces of the parity-1 buffer
+  unsigned char** dsts = nullptr;               // device [2][n]: my slot in every rank's buffer
+  unsigned long long** cnts = nullptr;          // device [n]: every rank's arrival counter
+  unsigned long long* my_cnt = nullptr;
+  uint64_t epoch = 0;
 };
 
 struct Plan {
@@ -50,10 +61,16 @@ struct Plan {
   uint64_t* dyn_host = nullptr;
   cudaEvent_t dyn_ev = nullptr;
   bool dyn_pending = false;
+  bool peers_ready = false;             // fused buckets: peer arenas opened (first collective call)
+  std::vector<void*> peer_bases;        // IPC-opened arenas of the other ranks
   ~Plan() {
+    for (void* pb : peer_bases)
+      if (pb) cudaIpcCloseMemHandle(pb);
     for (auto& b : buckets) {
       if (b.ev_h1) cudaEventDestroy(b.ev_h1);
       if (b.ev_comm) cudaEventDestroy(b.ev_comm);
+      if (b.dsts) cudaFree(b.dsts);
+      if (b.cnts) cudaFree(b.cnts);
     }
     if (dyn_ev) cudaEventDestroy(dyn_ev);
     if (dyn_host) cudaFreeHost(dyn_host);
@@ -77,10 +94,18 @@ struct HostTables {
   std::vector<SegH1> h1, a7;
   std::vector<uint32_t> h1_units, h1_groups, a7_units, h2_units;
   std::vector<SegH2> h2;
-  std::vector<const unsigned char*> a7_pieces, h2_pieces;
+  std::vector<const unsigned char*> a7_pieces, h2_pieces, h2_pieces_odd;
   std::vector<uint32_t> rankterms;
   std::vector<uint4> off_jobs;
 };
+
+static bool fused_allgather_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ESP_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 static void fill_unit_table(std::vector<uint32_t>& units, uint32_t seg, uint32_t count) {
   for (uint32_t i = 0; i < count; ++i) units.push_back(seg);
@@ -124,10 +149,19 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     size_t stride = round_up(per_rank, 256);
     size_t off = L.reserve(stride * nl);
     lb = LocalBufs{L.ptr<unsigned char>(off), stride};
+    return off;
   };
   bufs(b.send, b.P * S);
+  b.fused = fused_allgather_enabled() && !w->sim && n > 1 && dgc && b.routine == ESP_ALLGATHER;
   switch (b.routine) {
-    case ESP_ALLGATHER: bufs(b.recv1, n * S); break;
+    case ESP_ALLGATHER:
+      if (b.fused) {
+        b.recv1_off = bufs(b.recv1, 2 * n * S);   // two call-parity copies of the n slots
+        b.cnt_off = L.reserve(256);
+      } else {
+        bufs(b.recv1, n * S);
+      }
+      break;
     case ESP_ALLTOALL_ALLGATHER:
       bufs(b.recv1, n * S);
       if (sparse) bufs(b.recv2, (size_t)n * n * S);
@@ -160,6 +194,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.step = p.dyn_dev + nslots + slot_idx;
         s.r = c->r ? c->r + (size_t)lr * c->N + lo : nullptr;
         s.chunk = b.send.base ? b.send.at(lr) + (size_t)part * S + b.coff[ti] : nullptr;
+        s.chunk_off = (uint32_t)((size_t)part * S + b.coff[ti]);
         s.lazy_in = c->lazy ? c->lazy + ((size_t)lr * c->P + part) * 2 : nullptr;
         s.lazy_out = const_cast<float*>(s.lazy_in);
         s.n = len;
@@ -306,6 +341,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.piece0 = (uint32_t)T.h2_pieces.size();
         auto add_piece = [&](unsigned char* base, size_t off, uint32_t rankterm) {
           T.h2_pieces.push_back(base ? base + off : nullptr);
+          // fused Allgather: the parity-1 copy of the n slots follows the parity-0 copy
+          T.h2_pieces_odd.push_back(base && b.fused ? base + off + (size_t)n * S : nullptr);
           T.rankterms.push_back(rankterm);
         };
         const uint32_t rt_shared = 0;
@@ -441,6 +478,7 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     up(TB.h2, b.h2);
     up(TB.h2_units, b.h2_units);
     up(TB.h2_pieces, b.h2_pieces);
+    if (b.fused) up(TB.h2_pieces_odd, b.h2_pieces_odd);
     up(TB.rankterms, b.h2_rankterms);
     up(TB.off_jobs, b.h2_off_jobs);
     b.nh2_off_jobs = (int)TB.off_jobs.size();
@@ -459,9 +497,69 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
           ESP_CUDA(cudaMemset(b.send.at(lr), 0, b.P * b.slot));
           if (b.mid.base) ESP_CUDA(cudaMemset(b.mid.at(lr), 0, b.slot));
         }
+        if (b.fused) {
+          // every slot of both parity copies carries the pad pattern; writers
+          // (every rank's DGC write kernel) only ever store entries [0, k)
+          const int n = p.w->nranks;
+          for (int copy = 0; copy < 2 * n; ++copy)
+            for (size_t ti = 0; ti < b.tens.size(); ++ti) {
+              esp_ctx_s* c = p.ctxs[b.tens[ti]];
+              unsigned char* ch = b.recv1.at(lr) + (size_t)copy * b.slot + b.coff[ti];
+              ESP_CUDA(cudaMemset(ch, 0xFF, 4ull * c->kpad));
+              ESP_CUDA(cudaMemset(ch + 4ull * c->kpad, 0, 4ull * c->kpad));
+            }
+          ESP_CUDA(cudaMemset(p.arena.base + b.cnt_off, 0, 256));
+        }
       }
     }
   }
+}
+
+// Fused buckets need every rank's arena mapped: exchange CUDA IPC handles of
+// the arena through the NCCL communicator (a collective: done on the first
+// esp_sync / esp_sync_many of the plan, which every rank calls) and build the
+// destination / counter tables.
+static void open_peers(Plan& p, cudaStream_t st) {
+  esp_world_s* w = p.w;
+  const int n = w->nranks;
+  cudaIpcMemHandle_t mine;
+  ESP_CUDA(cudaIpcGetMemHandle(&mine, p.arena.base));
+  unsigned char* dbuf = nullptr;
+  ESP_CUDA(cudaMalloc(&dbuf, sizeof(mine) * (n + 1)));
+  ESP_CUDA(cudaMemcpy(dbuf + sizeof(mine) * n, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+  ESP_NCCL(ncclAllGather(dbuf + sizeof(mine) * n, dbuf, sizeof(mine), ncclUint8, w->comm, st));
+  std::vector<cudaIpcMemHandle_t> all(n);
+  ESP_CUDA(cudaStreamSynchronize(st));
+  ESP_CUDA(cudaMemcpy(all.data(), dbuf, sizeof(mine) * n, cudaMemcpyDeviceToHost));
+  cudaFree(dbuf);
+  std::vector<unsigned char*> base(n);
+  p.peer_bases.assign(n, nullptr);
+  for (int q = 0; q < n; ++q) {
+    if (q == w->rank) {
+      base[q] = p.arena.base;
+    } else {
+      void* ptr = nullptr;
+      ESP_CUDA(cudaIpcOpenMemHandle(&ptr, all[q], cudaIpcMemLazyEnablePeerAccess));
+      p.peer_bases[q] = ptr;
+      base[q] = static_cast<unsigned char*>(ptr);
+    }
+  }
+  for (auto& b : p.buckets) {
+    if (!b.fused) continue;
+    const size_t S = b.slot;
+    std::vector<unsigned char*> dsts(2 * n);
+    std::vector<unsigned long long*> cnts(n);
+    for (int par = 0; par < 2; ++par)
+      for (int q = 0; q < n; ++q)
+        dsts[par * n + q] = base[q] + b.recv1_off + ((size_t)par * n + w->rank) * S;
+    for (int q = 0; q < n; ++q) cnts[q] = reinterpret_cast<unsigned long long*>(base[q] + b.cnt_off);
+    b.my_cnt = reinterpret_cast<unsigned long long*>(p.arena.base + b.cnt_off);
+    ESP_CUDA(cudaMalloc(&b.dsts, sizeof(void*) * 2 * n));
+    ESP_CUDA(cudaMalloc(&b.cnts, sizeof(void*) * n));
+    ESP_CUDA(cudaMemcpy(b.dsts, dsts.data(), sizeof(void*) * 2 * n, cudaMemcpyHostToDevice));
+    ESP_CUDA(cudaMemcpy(b.cnts, cnts.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+  }
+  p.peers_ready = true;
 }
 
 Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
@@ -557,14 +655,22 @@ static void probe_pair(esp_world_s* w, cudaEvent_t* e0, cudaEvent_t* e1, uint64_
   ++w->probe_used;
 }
 
-static void run_h1(Plan& p, Bucket& b, cudaStream_t st) {
+// `fused`: this call's h1 stores its payload straight into every rank's
+// receive buffer (only from the collective esp_sync / esp_sync_many path)
+static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p.w->probe && b.nh1_units) probe_pair(p.w, &e0, &e1, b.h1_bytes);
   const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
   if (e0 && !dgc) ESP_CUDA(cudaEventRecord(e0, st));
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
-      launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1);
+      if (fused) {
+        const int n = p.w->nranks;
+        launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1,
+                      b.dsts + (b.epoch & 1) * n, b.cnts, n);
+      } else {
+        launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1);
+      }
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
     case ESP_EFSIGNSGD: launch_sign_h1_tma(K_EFSIGN, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
@@ -589,7 +695,15 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
   const bool quant = is_quant(b.kind);
   switch (b.routine) {
     case ESP_ALLGATHER:
-      coll_allgather(w, b.send, b.recv1, S, cs);
+      if (b.fused) {
+        // the payloads were pushed by every rank's h1; wait for all n x ngroups
+        // arrivals of this call (the counter is monotonic across calls)
+        count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
+        launch_wait_arrivals(b.my_cnt, (b.epoch + 1) * (unsigned long long)n * b.nh1_groups, cs);
+        ESP_CUDA(cudaGetLastError());
+      } else {
+        coll_allgather(w, b.send, b.recv1, S, cs);
+      }
       break;
     case ESP_ALLTOALL_ALLGATHER:
       coll_alltoall(w, b.send, b.recv1, S, cs);
@@ -649,7 +763,8 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
 static void run_h2(Plan& p, Bucket& b, cudaStream_t st) {
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
-      launch_h2_sparse(b.h2, b.h2_units, b.nh2_units, b.h2_off_jobs, b.nh2_off_jobs, b.h2_pieces, st);
+      launch_h2_sparse(b.h2, b.h2_units, b.nh2_units, b.h2_off_jobs, b.nh2_off_jobs,
+                       (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, st);
       break;
     case ESP_RANDOMK:
       launch_h2_randomk(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, b.h2_rankterms, st);
@@ -675,6 +790,8 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
   Plan& p = *pp;
   esp_world_s* w = p.w;
   const cudaStream_t cs = w->comm_stream;
+  if (!p.peers_ready && std::any_of(p.buckets.begin(), p.buckets.end(), [](const Bucket& b) { return b.fused; }))
+    open_peers(p, cs);
   upload_dyn(p, grads, st);
   if (p.zero_bytes) ESP_CUDA(cudaMemsetAsync(p.zero, 0, p.zero_bytes, st));
   const bool timing = w->timing;
@@ -687,7 +804,7 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
       cudaEvent_t e0 = tev(w, 1 + 6 * i), e1 = tev(w, 2 + 6 * i), e2 = tev(w, 3 + 6 * i);
       cudaEvent_t e3 = tev(w, 4 + 6 * i), m0 = tev(w, 5 + 6 * i), m1 = tev(w, 6 + 6 * i);
       ESP_CUDA(cudaEventRecord(e0, st));
-      run_h1(p, b, st);
+      run_h1(p, b, st, b.fused);
       ESP_CUDA(cudaEventRecord(e1, st));
       ESP_CUDA(cudaStreamWaitEvent(cs, e1, 0));
       ESP_CUDA(cudaEventRecord(m0, cs));
@@ -696,6 +813,7 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
       ESP_CUDA(cudaEventRecord(e2, cs));
       ESP_CUDA(cudaStreamWaitEvent(st, e2, 0));
       run_h2(p, b, st);
+      if (b.fused) ++b.epoch;
       ESP_CUDA(cudaEventRecord(e3, st));
     }
     ESP_CUDA(cudaEventRecord(tev(w, 1 + 6 * nb), st));
@@ -723,7 +841,7 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
     for (size_t i = 0; i <= nb; ++i) {
       if (i < nb) {
         Bucket& b = p.buckets[i];
-        run_h1(p, b, st);
+        run_h1(p, b, st, b.fused);
         ESP_CUDA(cudaEventRecord(b.ev_h1, st));
         ESP_CUDA(cudaStreamWaitEvent(cs, b.ev_h1, 0));
         run_comm(p, b, cs, nullptr, nullptr);
@@ -733,6 +851,7 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
         Bucket& b = p.buckets[i - 1];
         ESP_CUDA(cudaStreamWaitEvent(st, b.ev_comm, 0));
         run_h2(p, b, st);
+        if (b.fused) ++b.epoch;
       }
     }
   }
