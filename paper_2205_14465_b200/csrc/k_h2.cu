@@ -41,42 +41,79 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2
   }
 }
 
+// Persistent over tiles (stride gridDim.x): consecutive tiles of a CTA mostly
+// belong to the same segment, so its descriptor is reloaded only on a change,
+// and the next tile's offsets are fetched before this tile's work.
 __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __restrict__ segs,
                                                                  const uint32_t* __restrict__ tile_seg,
+                                                                 uint32_t ntiles,
                                                                  const unsigned char* const* __restrict__ pieces) {
   constexpr int kThreads = kTileThreads;   // small CTAs: many independent tiles per SM
   __shared__ __align__(16) float acc[kTile];
   __shared__ uint32_t rlo[kMaxPieces], rhi[kMaxPieces];
-  const uint32_t sid = tile_seg[blockIdx.x];
-  const SegH2 S = segs[sid];
-  const uint32_t t = blockIdx.x - S.unit0;
-  const uint32_t lo = t * kTile;
-  const uint32_t hi = min(lo + (uint32_t)kTile, S.n);
+  uint32_t tg = blockIdx.x;
+  if (tg >= ntiles) return;
+  uint32_t sid = tile_seg[tg];
+  SegH2 S = segs[sid];
+  float* out = seg_out(S);
+  uint32_t my_lo = 0, my_hi = 0;   // thread r < npieces: offsets of piece r for the current tile
   if (threadIdx.x < S.npieces) {
-    const uint32_t* toff = S.toff + (size_t)threadIdx.x * (S.nunits + 1);
-    rlo[threadIdx.x] = __ldg(toff + t);
-    rhi[threadIdx.x] = __ldg(toff + t + 1);
+    const uint32_t* toff = S.toff + (size_t)threadIdx.x * (S.nunits + 1) + (tg - S.unit0);
+    my_lo = __ldg(toff);
+    my_hi = __ldg(toff + 1);
   }
-  for (int i = threadIdx.x; i < kTile / 4; i += kThreads)
-    reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncthreads();
-  for (uint32_t r = 0; r < S.npieces; ++r) {
-    const unsigned char* pc = pieces[S.piece0 + r];
-    const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
-    const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
-    for (uint32_t i = rlo[r] + threadIdx.x; i < rhi[r]; i += kThreads) {
-      const uint32_t e = __ldg(idx + i) - lo;
-      acc[e] = __fadd_rn(acc[e], __ldg(val + i));   // distinct indices within a piece
+  while (true) {
+    const uint32_t t = tg - S.unit0;
+    const uint32_t lo = t * kTile;
+    const uint32_t hi = min(lo + (uint32_t)kTile, S.n);
+    if (threadIdx.x < S.npieces) {
+      rlo[threadIdx.x] = my_lo;
+      rhi[threadIdx.x] = my_hi;
     }
+    for (int i = threadIdx.x; i < kTile / 4; i += kThreads)
+      reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // prefetch the next tile's segment id
+    const uint32_t tn = tg + gridDim.x;
+    const uint32_t sid_n = tn < ntiles ? tile_seg[tn] : sid;
     __syncthreads();
-  }
-  const Divisor div(S.divisor);
-  const bool ones = S.divisor == 1.0f;
-  for (uint32_t i = threadIdx.x * 4; lo + i < hi; i += kThreads * 4) {
-    float4 v = *reinterpret_cast<const float4*>(acc + i);
-    // most of a sparse tile is +0 (+0 / d = +0): divide only touched words
-    if (!ones && (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)) v = div(v);
-    store4_guard(seg_out(S), lo + i, S.n, v);
+    for (uint32_t r = 0; r < S.npieces; ++r) {
+      const unsigned char* pc = pieces[S.piece0 + r];
+      const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
+      const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
+      for (uint32_t i = rlo[r] + threadIdx.x; i < rhi[r]; i += kThreads) {
+        const uint32_t e = __ldg(idx + i) - lo;
+        acc[e] = __fadd_rn(acc[e], __ldg(val + i));   // distinct indices within a piece
+      }
+      __syncthreads();
+    }
+    const Divisor div(S.divisor);
+    const bool ones = S.divisor == 1.0f;
+    // next tile's offsets (same segment in the common case) before the writes
+    SegH2 Sn = S;
+    float* out_n = out;
+    if (tn < ntiles) {
+      if (sid_n != sid) {
+        Sn = segs[sid_n];
+        out_n = seg_out(Sn);
+      }
+      if (threadIdx.x < Sn.npieces) {
+        const uint32_t* toff = Sn.toff + (size_t)threadIdx.x * (Sn.nunits + 1) + (tn - Sn.unit0);
+        my_lo = __ldg(toff);
+        my_hi = __ldg(toff + 1);
+      }
+    }
+    for (uint32_t i = threadIdx.x * 4; lo + i < hi; i += kThreads * 4) {
+      float4 v = *reinterpret_cast<const float4*>(acc + i);
+      // most of a sparse tile is +0 (+0 / d = +0): divide only touched words
+      if (!ones && (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)) v = div(v);
+      store4_guard(out, lo + i, S.n, v);
+    }
+    if (tn >= ntiles) break;
+    tg = tn;
+    sid = sid_n;
+    S = Sn;
+    out = out_n;
+    __syncthreads();   // acc / rlo / rhi are reused
   }
 }
 
@@ -162,7 +199,15 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
                       const unsigned char* const* pieces, cudaStream_t st) {
   if (ntiles == 0) return;
   h2_sparse_offsets_kernel<<<njobs, kThreads, 0, st>>>(segs, jobs, pieces);
-  h2_sparse_kernel<<<ntiles, kTileThreads, 0, st>>>(segs, tile_seg, pieces);
+  static int grid_cap = [] {
+    int dev = 0, sms = 148, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sparse_kernel, kTileThreads, 0);
+    return sms * (per_sm > 0 ? per_sm : 8);
+  }();
+  const int grid = ntiles < grid_cap ? ntiles : grid_cap;
+  h2_sparse_kernel<<<grid, kTileThreads, 0, st>>>(segs, tile_seg, (uint32_t)ntiles, pieces);
   count_launches(2);
 }
 
