@@ -15,7 +15,7 @@ constexpr int kNJ = kRun / 128;          // float4 per lane per run
 constexpr int kDgcTile = 8 * kRun;       // DGC streaming tile (one run per consumer warp)
 constexpr int kSignSpan = 1024;          // sign h1: elements per warp per unit
 constexpr int kUnit = 8192;              // 8 runs per CTA
-constexpr int kRunsPerGroup = 256;       // DGC finalize: 256 runs (262144 elements) per CTA
+constexpr int kRunsPerGroup = 256;       // DGC finalize: 256 runs (131072 elements) per CTA
 constexpr int kSample = 4096;            // DGC sampled-threshold sample size
 constexpr int kTile = 4096;              // sparse h2 output tile (16 KB smem)
 constexpr int kTileThreads = 128;        // sparse h2 CTA size (up to 13 tiles in flight per SM)
@@ -28,14 +28,15 @@ struct SelState {
   uint32_t thr;        // sampled threshold key (candidates: key >= thr)
   uint32_t count;      // candidates found by the streaming pass
   uint32_t done;       // last-CTA counter of the streaming pass
-  uint32_t fallback;   // 1: count < k, re-run compaction with thr = 0
+  uint32_t fallback;   // 1: count < k, re-run compaction with thr_lo (then 0)
   uint32_t count_fb, done_fb;
   uint32_t prefix;     // radix-select prefix of the k-th key
   uint32_t above;      // # candidates with key above the current prefix bin
   uint32_t need;       // k - above
   uint32_t done_r2, done_r3, done_cnt;
   uint32_t total_sel;  // debug: number selected (== k)
-  uint32_t pad[3];
+  uint32_t thr_lo;     // safe lower threshold of the fallback (sample bin far below thr)
+  uint32_t pad[2];
 };
 
 // One h1 segment = (local rank, tensor, partition).

@@ -16,7 +16,8 @@
 //                   order (vote/ballot/popc) and histogram their top 11 key bits.  The
 //                   CTA that completes a segment picks the radix bin of the k-th key.
 //                   (TOPK: thr = 0, every element is a candidate.)
-//   3. dgc_fallback only segments with < k candidates: recompact with thr = 0.
+//   3. dgc_fallback only segments with < k candidates: recompact with the
+//                   sample's far lower threshold thr_lo (then, if that misses too, 0).
 //   4. dgc_refine   two more radix rounds over the candidates -> the exact k-th key
 //                   T, #above, #ties to take (ties broken by ascending index).
 //   5. dgc_write    per group of runs: count, decoupled look-back for the group's
@@ -77,7 +78,9 @@ __device__ void select_bin(const uint32_t* hist, int nbins, uint32_t need, uint3
 }
 
 // ------------------------------------------------------------------ 1. sample
-__global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __restrict__ segs) {
+// force (test hook, ESP_DGC_FORCE_FALLBACK): bit 0 sets thr above every key so
+// that every segment with k > 0 takes the fallback; bit 1 does the same to thr_lo
+__global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __restrict__ segs, int force) {
   __shared__ uint32_t keys[kSample];
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t sh[280];
@@ -99,11 +102,14 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
       const uint32_t j = threadIdx.x + q * kThreads;
       uint32_t pos = j;
       if (!exact && j < s) {
-        // stratum [jN/s, (j+1)N/s) with s = kSample = 2^12: shifts, no division;
-        // position within it by a multiply-high of the hash (a sampler only)
-        static_assert(kSample == 4096, "shift assumes kSample == 2^12");
-        const uint32_t a = (uint32_t)(((uint64_t)j * n) >> 12), b = (uint32_t)(((uint64_t)(j + 1) * n) >> 12);
-        pos = a + (uint32_t)(((uint64_t)(uint32_t)splitmix64(S.hash ^ j) * (b - a)) >> 32);
+        // 512 strata [GN/512, (G+1)N/512) (shifts, no division), 8 consecutive
+        // samples from each at a hashed offset: a random 4-byte gather costs a
+        // whole DRAM sector, a run of 8 costs one or two (a sampler only; the
+        // selection stays exact whatever threshold it yields)
+        static_assert(kSample == 4096, "512 strata x 8 assumes kSample == 2^12");
+        const uint32_t G = j >> 3;
+        const uint32_t a = (uint32_t)(((uint64_t)G * n) >> 9), b = (uint32_t)(((uint64_t)(G + 1) * n) >> 9);
+        pos = a + (uint32_t)(((uint64_t)(uint32_t)splitmix64(S.hash ^ G) * (b - a - 7)) >> 32) + (j & 7u);
       }
       gv[q] = j < s ? __ldg(g + pos) : 0.f;
       rv[q] = (j < s && S.ef) ? S.r[pos] : 0.f;
@@ -129,13 +135,21 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
   }
   uint32_t b1, a1, b2, a2;
   select_bin<0, false>(hist, 2048, need, &b1, &a1, sh);
+  // the fallback's threshold: the 11-bit bin of a sample rank about twice as
+  // deep (a miss at thr is a ~1e-4 event per segment, one at thr_lo needs
+  // both tails at once)
+  uint32_t b_lo = 0, a_lo;
+  if (!exact) select_bin<0, false>(hist, 2048, min(s, 2 * need + 16), &b_lo, &a_lo, sh);
   for (int i = threadIdx.x; i < 1024; i += kThreads) hist[i] = 0;
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < s; j += kThreads)
     if ((keys[j] >> 20) == b1) atomicAdd(&hist[(keys[j] >> 10) & 1023u], 1u);
   __syncthreads();
   select_bin<0, false>(hist, 1024, need - a1, &b2, &a2, sh);
-  if (threadIdx.x == 0) S.st->thr = (b1 << 20) | (b2 << 10);
+  if (threadIdx.x == 0) {
+    S.st->thr = (force & 1) ? 0xFFFFFFFFu : (b1 << 20) | (b2 << 10);
+    S.st->thr_lo = (force & 2) ? 0xFFFFFFFFu : exact ? 0u : b_lo << 20;
+  }
 }
 
 // ------------------------------------------------------------------ candidate emission
@@ -453,7 +467,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) dgc_stream_kernel(const SegH
 
 // ------------------------------------------------------------------ 3. fallback
 // Segments whose sampled threshold let fewer than k candidates through are
-// recompacted from acc (= r after the streaming pass) with thr = 0.  Every CTA
+// recompacted from acc (= r after the streaming pass) with thr_lo.  Every CTA
 // scans the segment list; only flagged segments cost work.
 __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __restrict__ segs, int nsegs) {
   __shared__ uint32_t hist[2048];
@@ -480,19 +494,23 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
     __syncthreads();
     uint32_t units = 0;
     const float* src = S.ef ? S.r : seg_g(S);
-    for (uint32_t u = blockIdx.x; u < S.nunits; u += gridDim.x, ++units) {
-      const uint32_t base = u * kDgcTile + warp * kRun;
-      if (base >= S.n) continue;
-      float4 av[kNJ];
+    const uint32_t thr_fb = __ldcg(&S.st->thr_lo);
+    auto recompact = [&](uint32_t u0, uint32_t ustep, uint32_t thr) {
+      for (uint32_t u = u0; u < S.nunits; u += ustep, ++units) {
+        const uint32_t base = u * kDgcTile + warp * kRun;
+        if (base >= S.n) continue;
+        float4 av[kNJ];
 #pragma unroll
-      for (int j = 0; j < kNJ; ++j) av[j] = load4_guard(src, base + j * 128 + lane * 4, S.n);
-      const uint32_t run = base / kRun;
-      const uint32_t wc = emit_run(av, base, S.n, 0u, S.cand + (size_t)run * kRun, hist);
-      if (lane == 0) {
-        S.runcnt[run] = wc;
-        atomicAdd(&cta_count, wc);
+        for (int j = 0; j < kNJ; ++j) av[j] = load4_guard(src, base + j * 128 + lane * 4, S.n);
+        const uint32_t run = base / kRun;
+        const uint32_t wc = emit_run(av, base, S.n, thr, S.cand + (size_t)run * kRun, hist);
+        if (lane == 0) {
+          S.runcnt[run] = wc;
+          atomicAdd(&cta_count, wc);
+        }
       }
-    }
+    };
+    recompact(blockIdx.x, gridDim.x, thr_fb);
     __syncthreads();
     for (int i = threadIdx.x; i < 2048; i += kThreads)
       if (hist[i]) atomicAdd(&S.hist[2048 + i], hist[i]);
@@ -505,6 +523,21 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
     __syncthreads();
     if (flag) {
       __threadfence();
+      if (__ldcg(&S.st->count_fb) < S.k) {
+        // thr_lo missed as well (both sample tails at once): this CTA alone
+        // recompacts the whole segment with thr = 0 -- slow, and never expected
+        __syncthreads();
+        for (int i = threadIdx.x; i < 2048; i += kThreads) {
+          hist[i] = 0;
+          S.hist[2048 + i] = 0;
+        }
+        __syncthreads();
+        recompact(0, 1, 0u);
+        __syncthreads();
+        for (int i = threadIdx.x; i < 2048; i += kThreads) S.hist[2048 + i] = hist[i];
+        __threadfence();
+        __syncthreads();
+      }
       uint32_t bin, above;
       select_bin<0, true>(S.hist + 2048, 2048, S.k, &bin, &above, sh);
       if (threadIdx.x == 0) {
@@ -519,6 +552,7 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
 }
 
 // ------------------------------------------------------------------ 4. refine
+constexpr int kBatch = 4;   // candidate loads in flight per thread (refine, write pass 1)
 // A finalize group = kRunsPerGroup consecutive runs of one segment (one runcnt
 // per thread).  Its candidates are addressed as one flat, index-ordered list:
 // sh_off[i] = first flat position of run i; returns the group's total.
@@ -563,9 +597,18 @@ __global__ void __launch_bounds__(kThreads) dgc_refine_kernel(const SegH1* __res
   uint32_t nr;
   const uint32_t C = group_offsets(S, g, sh_off, sh_scan, &nr);
   const uint32_t prefix = __ldcg(&S.st->prefix);
-  for (uint32_t q = threadIdx.x; q < C; q += kThreads) {
-    const uint32_t key = group_cand(S, g, sh_off, nr, q).y & 0x7FFFFFFFu;
-    if ((key >> kShiftMatch) == prefix) atomicAdd(&sh_hist[(key >> kShiftBin) & 1023u], 1u);
+  // latency-bound: kBatch independent candidate loads in flight per thread
+  for (uint32_t q0 = threadIdx.x; q0 < C; q0 += kBatch * kThreads) {
+    uint32_t key[kBatch];
+#pragma unroll
+    for (int m = 0; m < kBatch; ++m) {
+      const uint32_t q = q0 + m * kThreads;
+      key[m] = q < C ? group_cand(S, g, sh_off, nr, q).y & 0x7FFFFFFFu : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int m = 0; m < kBatch; ++m)
+      if (key[m] != 0xFFFFFFFFu && (key[m] >> kShiftMatch) == prefix)
+        atomicAdd(&sh_hist[(key[m] >> kShiftBin) & 1023u], 1u);
   }
   __syncthreads();
   uint32_t* ghist = S.hist + (ROUND == 2 ? 4096 : 5120);
@@ -609,10 +652,19 @@ __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __rest
   auto cand_at = [&](uint32_t q) -> uint2 { return group_cand(S, g, sh_off, nr, q); };
   // pass 1: the group's aggregate
   uint32_t above = 0, tie = 0;
-  for (uint32_t q = threadIdx.x; q < C; q += kThreads) {
-    const uint32_t key = cand_at(q).y & 0x7FFFFFFFu;
-    above += key > T;
-    tie += key == T;
+  for (uint32_t q0 = threadIdx.x; q0 < C; q0 += kBatch * kThreads) {
+    uint32_t key[kBatch];
+#pragma unroll
+    for (int m = 0; m < kBatch; ++m) {
+      const uint32_t q = q0 + m * kThreads;
+      key[m] = q < C ? cand_at(q).y & 0x7FFFFFFFu : 0u;   // 0 < T unless T = 0
+    }
+#pragma unroll
+    for (int m = 0; m < kBatch; ++m) {
+      const bool in = q0 + m * kThreads < C;
+      above += in && key[m] > T;
+      tie += in && key[m] == T;
+    }
   }
   above = block_sum_u32(above, sh_scan);
   tie = block_sum_u32(tie, sh_scan);
@@ -644,12 +696,14 @@ __global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __rest
   uint32_t sel_run = sh_prefix[0] + min(sh_prefix[1], need);
   uint32_t* out_idx = reinterpret_cast<uint32_t*>(S.chunk);
   float* out_val = reinterpret_cast<float*>(S.chunk + 4 * (size_t)S.kpad);
+  // software-pipelined: the next chunk's candidate is loaded before this one is used
+  uint2 c_next = threadIdx.x < C ? cand_at(threadIdx.x) : make_uint2(0, 0);
   for (uint32_t q0 = 0; q0 < C; q0 += kThreads) {
     const uint32_t q = q0 + threadIdx.x;
     uint32_t is_tie = 0, is_above = 0;
-    uint2 c = make_uint2(0, 0);
+    const uint2 c = c_next;
+    if (q + kThreads < C) c_next = cand_at(q + kThreads);
     if (q < C) {
-      c = cand_at(q);
       const uint32_t key = c.y & 0x7FFFFFFFu;
       is_above = key > T;
       is_tie = key == T;
@@ -751,7 +805,8 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
     return e ? atoi(e) : 0;
   }();
   const int stages = tma_stream_stages();
-  dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs);
+  const char* ff = getenv("ESP_DGC_FORCE_FALLBACK");   // read per launch: a test hook
+  dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs, ff ? atoi(ff) : 0);
   if (probe0) cudaEventRecord(probe0, st);
   {
     const int per_sm = (variant & 2) ? 2 : 1;

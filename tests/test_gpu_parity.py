@@ -107,6 +107,17 @@ def test_dgc_adversarial(mode):
     run_sim("dgc", "allgather", 2, 50_001, steps=2, ratio=0.01, dist="D4", mode=mode)
 
 
+@pytest.mark.parametrize("force", ["1", "3"])
+@pytest.mark.parametrize("N", [3000, 50_001, 600_001])
+def test_dgc_forced_fallback(force, N, monkeypatch):
+    """The sampled threshold only accelerates: forcing every segment through the
+    fallback (1: recompaction at thr_lo; 3: thr_lo misses too -> thr = 0) must
+    leave the selection bit-identical (reading R3)."""
+    monkeypatch.setenv("ESP_DGC_FORCE_FALLBACK", force)
+    run_sim("dgc", "allgather", 2, N, steps=2, ratio=0.01)
+    run_sim("dgc", "alltoall_allgather", 4, N, steps=2, ratio=0.01)
+
+
 @pytest.mark.parametrize("ratio", [0.001, 0.05, 0.5, 1.0])
 def test_dgc_ratios(ratio):
     run_sim("dgc", "allgather", 2, 70_000, steps=2, ratio=ratio)
