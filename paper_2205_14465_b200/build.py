@@ -40,7 +40,8 @@ def _nvcc():
 def _flags(nd):
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
                    "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(nd, "include"),
-                   "-I", os.path.join(ROOT, "include"), "-diag-suppress", "186"]
+                   "-I", os.path.join(ROOT, "include"), "-diag-suppress", "186",
+                   *os.environ.get("ESP_NVCC_EXTRA", "").split()]   # tuning experiments only
 
 
 def _deps_mtime():

@@ -17,8 +17,11 @@ constexpr int kSignSpan = 1024;          // sign h1: elements per warp per unit
 constexpr int kUnit = 8192;              // 8 runs per CTA
 constexpr int kRunsPerGroup = 256;       // DGC finalize: 256 runs (131072 elements) per CTA
 constexpr int kSample = 4096;            // DGC sampled-threshold sample size
-constexpr int kTile = 4096;              // sparse h2 output tile (16 KB smem)
-constexpr int kTileThreads = 128;        // sparse h2 CTA size (up to 13 tiles in flight per SM)
+#ifndef ESP_H2_TILE
+#define ESP_H2_TILE 1024
+#endif
+constexpr int kTile = ESP_H2_TILE;       // sparse h2 output tile (one warp each)
+constexpr int kTileThreads = 128;        // sparse h2 CTA size (4 warps = 4 tiles in flight)
 constexpr int kOffJob = 4096;            // sparse h2 tile-offset pass: entries per CTA
 
 enum Kind : int { K_NONE = 0, K_RANDOMK = 1, K_DGC = 2, K_TOPK = 3, K_EFSIGN = 4, K_ONEBIT = 5 };

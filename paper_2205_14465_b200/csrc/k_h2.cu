@@ -41,79 +41,113 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2
   }
 }
 
-// Persistent over tiles (stride gridDim.x): consecutive tiles of a CTA mostly
-// belong to the same segment, so its descriptor is reloaded only on a change,
-// and the next tile's offsets are fetched before this tile's work.
+// One WARP per output tile, persistent over tiles (stride = all warps of the
+// grid): no CTA barrier anywhere, so 64 independent tiles per SM hide the load
+// latencies of the entry lists (a CTA-wide tile loop was latency-bound).
+// Per tile: the dense zero fill straight from registers (the 4 B/elem write
+// that bounds the kernel), then only the touched words are rewritten:
+//   one piece:     out[e] = (+0 + v) / d
+//   several:       out[e] = out[e] + v_r for r in rank order (the zero fill is
+//                  the sum's +0; __syncwarp orders the pieces), then each
+//                  distinct touched word is divided once (a per-warp bitmap
+//                  in shared memory elects the owner).
 __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __restrict__ segs,
                                                                  const uint32_t* __restrict__ tile_seg,
                                                                  uint32_t ntiles,
                                                                  const unsigned char* const* __restrict__ pieces) {
-  constexpr int kThreads = kTileThreads;   // small CTAs: many independent tiles per SM
-  __shared__ __align__(16) float acc[kTile];
-  __shared__ uint32_t rlo[kMaxPieces], rhi[kMaxPieces];
-  uint32_t tg = blockIdx.x;
+  constexpr int kWarps = kTileThreads / 32;
+  constexpr unsigned kFull = 0xffffffffu;
+  __shared__ uint32_t seen_all[kWarps][kTile / 32];
+  const int lane = threadIdx.x & 31;
+  uint32_t* seen = seen_all[threadIdx.x >> 5];
+  const uint32_t GW = gridDim.x * kWarps;
+  uint32_t tg = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (tg >= ntiles) return;
-  uint32_t sid = tile_seg[tg];
-  SegH2 S = segs[sid];
+  SegH2 S = segs[tile_seg[tg]];
   float* out = seg_out(S);
-  uint32_t my_lo = 0, my_hi = 0;   // thread r < npieces: offsets of piece r for the current tile
-  if (threadIdx.x < S.npieces) {
-    const uint32_t* toff = S.toff + (size_t)threadIdx.x * (S.nunits + 1) + (tg - S.unit0);
-    my_lo = __ldg(toff);
-    my_hi = __ldg(toff + 1);
-  }
+  // lane holds the entry range of pieces lane and lane + 32 for the current tile
+  uint32_t plo0 = 0, phi0 = 0, plo1 = 0, phi1 = 0;
+  auto load_toff = [&](const SegH2& s, uint32_t t) {
+    if ((uint32_t)lane < s.npieces) {
+      const uint32_t* toff = s.toff + (size_t)lane * (s.nunits + 1) + t;
+      plo0 = __ldg(toff);
+      phi0 = __ldg(toff + 1);
+    }
+    if ((uint32_t)lane + 32 < s.npieces) {
+      const uint32_t* toff = s.toff + (size_t)(lane + 32) * (s.nunits + 1) + t;
+      plo1 = __ldg(toff);
+      phi1 = __ldg(toff + 1);
+    }
+  };
+  load_toff(S, tg - S.unit0);
   while (true) {
     const uint32_t t = tg - S.unit0;
     const uint32_t lo = t * kTile;
     const uint32_t hi = min(lo + (uint32_t)kTile, S.n);
-    if (threadIdx.x < S.npieces) {
-      rlo[threadIdx.x] = my_lo;
-      rhi[threadIdx.x] = my_hi;
+    for (uint32_t i = lane * 4; lo + i < hi; i += 128) store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
+    const uint32_t np = S.npieces;
+    const bool ones = S.divisor == 1.0f;
+    const Divisor div(S.divisor);
+    if (np > 1 && !ones)
+      for (int i = lane; i < kTile / 32; i += 32) seen[i] = 0;
+    const uint32_t clo0 = plo0, chi0 = phi0, clo1 = plo1, chi1 = phi1;
+    auto range = [&](uint32_t r, uint32_t* a, uint32_t* b) {
+      *a = __shfl_sync(kFull, r < 32 ? clo0 : clo1, r & 31);
+      *b = __shfl_sync(kFull, r < 32 ? chi0 : chi1, r & 31);
+    };
+    // the next tile (same segment unless past its last tile): offsets in flight
+    // while this tile's entries are processed
+    const uint32_t tn = tg + GW;
+    const SegH2* Sn_p = nullptr;
+    if (tn < ntiles) {
+      if (tn >= S.unit0 + S.nunits) Sn_p = segs + tile_seg[tn];
+      load_toff(Sn_p ? *Sn_p : S, tn - (Sn_p ? Sn_p->unit0 : S.unit0));
     }
-    for (int i = threadIdx.x; i < kTile / 4; i += kThreads)
-      reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    // prefetch the next tile's segment id
-    const uint32_t tn = tg + gridDim.x;
-    const uint32_t sid_n = tn < ntiles ? tile_seg[tn] : sid;
-    __syncthreads();
-    for (uint32_t r = 0; r < S.npieces; ++r) {
-      const unsigned char* pc = pieces[S.piece0 + r];
+    __syncwarp();   // zero stores (and the bitmap reset) before the touched-word stores
+    if (np == 1) {
+      const unsigned char* pc = pieces[S.piece0];
       const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
       const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
-      for (uint32_t i = rlo[r] + threadIdx.x; i < rhi[r]; i += kThreads) {
-        const uint32_t e = __ldg(idx + i) - lo;
-        acc[e] = __fadd_rn(acc[e], __ldg(val + i));   // distinct indices within a piece
+      uint32_t a, b;
+      range(0, &a, &b);
+      for (uint32_t i = a + lane; i < b; i += 32) {
+        const float v = __fadd_rn(0.f, __ldg(val + i));   // +0 + v: the oracle's sum from +0
+        out[__ldg(idx + i)] = ones ? v : div(v);
       }
-      __syncthreads();
-    }
-    const Divisor div(S.divisor);
-    const bool ones = S.divisor == 1.0f;
-    // next tile's offsets (same segment in the common case) before the writes
-    SegH2 Sn = S;
-    float* out_n = out;
-    if (tn < ntiles) {
-      if (sid_n != sid) {
-        Sn = segs[sid_n];
-        out_n = seg_out(Sn);
+    } else {
+      for (uint32_t r = 0; r < np; ++r) {
+        const unsigned char* pc = pieces[S.piece0 + r];
+        const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
+        const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
+        uint32_t a, b;
+        range(r, &a, &b);
+        for (uint32_t i = a + lane; i < b; i += 32) {
+          const uint32_t e = __ldg(idx + i);
+          const float v = __ldg(val + i);
+          out[e] = __fadd_rn(__ldcg(out + e), v);   // distinct indices within a piece
+        }
+        __syncwarp();
       }
-      if (threadIdx.x < Sn.npieces) {
-        const uint32_t* toff = Sn.toff + (size_t)threadIdx.x * (Sn.nunits + 1) + (tn - Sn.unit0);
-        my_lo = __ldg(toff);
-        my_hi = __ldg(toff + 1);
+      if (!ones) {
+        for (uint32_t r = 0; r < np; ++r) {
+          const uint32_t* idx = reinterpret_cast<const uint32_t*>(pieces[S.piece0 + r]);
+          uint32_t a, b;
+          range(r, &a, &b);
+          for (uint32_t i = a + lane; i < b; i += 32) {
+            const uint32_t e = __ldg(idx + i);
+            const uint32_t w = e - lo, m = 1u << (w & 31);
+            if (!(atomicOr(&seen[w >> 5], m) & m)) out[e] = div(__ldcg(out + e));
+          }
+        }
       }
-    }
-    for (uint32_t i = threadIdx.x * 4; lo + i < hi; i += kThreads * 4) {
-      float4 v = *reinterpret_cast<const float4*>(acc + i);
-      // most of a sparse tile is +0 (+0 / d = +0): divide only touched words
-      if (!ones && (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)) v = div(v);
-      store4_guard(out, lo + i, S.n, v);
     }
     if (tn >= ntiles) break;
     tg = tn;
-    sid = sid_n;
-    S = Sn;
-    out = out_n;
-    __syncthreads();   // acc / rlo / rhi are reused
+    if (Sn_p) {
+      S = *Sn_p;
+      out = seg_out(S);
+    }
+    __syncwarp();   // bitmap reuse
   }
 }
 
@@ -206,7 +240,8 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sparse_kernel, kTileThreads, 0);
     return sms * (per_sm > 0 ? per_sm : 8);
   }();
-  const int grid = ntiles < grid_cap ? ntiles : grid_cap;
+  const int need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);   // one warp per tile
+  const int grid = need < grid_cap ? need : grid_cap;
   h2_sparse_kernel<<<grid, kTileThreads, 0, st>>>(segs, tile_seg, (uint32_t)ntiles, pieces);
   count_launches(2);
 }
