@@ -99,16 +99,23 @@ struct Divisor {
 // ---- CTA-wide scans / reductions for 256 threads ---------------------------------
 // BAR = 0: __syncthreads; BAR > 0: named barrier BAR over the first 256 threads
 // (the consumer warps of a warp-specialised kernel).
+// BAR = b > 0 also serves the b-th group of 256 consumer threads (threads
+// 256(b-1) .. 256b-1) of a kernel with several consumer groups.
 template <int BAR>
 __device__ __forceinline__ void csync() {
   if (BAR == 0) __syncthreads();
   else asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(kThreads) : "memory");
 }
+// thread index within the 256 threads that take part in barrier BAR
+template <int BAR>
+__device__ __forceinline__ int ctid() {
+  return BAR == 0 ? (int)threadIdx.x : (int)(threadIdx.x & (kThreads - 1));
+}
 
 // Exclusive scan of v over the CTA in thread order.  `sh` needs 9 uint32.
 template <int BAR = 0>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total, uint32_t* sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = ctid<BAR>() >> 5;
   uint32_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -145,13 +152,13 @@ __device__ __forceinline__ uint32_t block_sum_u32(uint32_t v, uint32_t* sh) {
 // Deterministic fp64 CTA sum (fixed shuffle tree then warp order).  sh: 8 doubles.
 template <int BAR = 0>
 __device__ __forceinline__ double block_sum_f64(double v, double* sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = ctid<BAR>() >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if (lane == 0) sh[warp] = v;
   csync<BAR>();
   double t = 0.0;
-  if (threadIdx.x == 0) {
+  if (ctid<BAR>() == 0) {
     for (int w = 0; w < kThreads / 32; ++w) t += sh[w];
     sh[0] = t;
   }

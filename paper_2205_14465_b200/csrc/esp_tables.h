@@ -15,7 +15,7 @@ constexpr int kNJ = kRun / 128;          // float4 per lane per run
 constexpr int kDgcTile = 8 * kRun;       // DGC streaming tile (one run per consumer warp)
 constexpr int kSignSpan = 1024;          // sign h1: elements per warp per unit
 constexpr int kUnit = 8192;              // 8 runs per CTA
-constexpr int kRunsPerGroup = 256;       // DGC finalize: 256 runs (131072 elements) per CTA
+constexpr int kRunsPerGroup = 64;        // DGC finalize: runs per warp-group (32768 elements)
 constexpr int kSample = 4096;            // DGC sampled-threshold sample size
 #ifndef ESP_H2_TILE
 #define ESP_H2_TILE 1024
@@ -74,7 +74,8 @@ struct SegH1 {
   uint32_t* runcnt;      // candidates per run
   uint32_t* hist;        // 2048 (pass) + 2048 (fallback) + 1024 + 1024
   SelState* st;
-  uint32_t* bflag;       // bucket-wide "some segment fell back" counter (zeroed every call)
+  uint32_t* bflag;       // bucket-wide "some segment fell back" counter; bflag[1]: the
+                         // finalize's grid-barrier counter (both zeroed every call)
   uint32_t* gcnt;        // look-back status, one uint64 per group (zeroed every call)
   double* partial;       // sign: 2 doubles per unit
   uint32_t* pcount;      // sign: 2 counts per unit (onebit) ; [0] of seg = done counter

@@ -28,6 +28,7 @@
 #include <string>
 
 #include "esp_device.cuh"
+#include "esp_internal.h"
 #include "esp_kernels.h"
 
 namespace esp {
@@ -40,7 +41,7 @@ template <int BAR, bool GLOBAL>
 __device__ void select_bin(const uint32_t* hist, int nbins, uint32_t need, uint32_t* out_bin,
                            uint32_t* out_above, uint32_t* sh /* >= 270 */, uint32_t* out_total = nullptr) {
   const int per = nbins / kThreads;
-  const int t = threadIdx.x;
+  const int t = ctid<BAR>();
   uint32_t local[8];
   uint32_t sum = 0;
   for (int i = 0; i < per; ++i) {
@@ -230,12 +231,16 @@ __device__ __forceinline__ uint32_t emit_run_full(const float4 (&av)[kNJ], uint3
 
 // ------------------------------------------------------------------ 2. stream (TMA)
 constexpr int kMaxStages = 6;   // 6 x 32 KB stages + header fit the 227 KB of one SM
-struct StreamSmem {   // followed (128-byte aligned) by `ns` stages of {g[kDgcTile], r[kDgcTile]}
+constexpr int kMaxGroups = 2;   // consumer groups of 8 warps (tiles in flight being computed)
+struct GroupSmem {   // per consumer group
   uint32_t hist[2048];
-  uint64_t full[kMaxStages], empty[kMaxStages];
   uint32_t scan[280];
   uint32_t cta_count;
   int flag;
+};
+struct StreamSmem {   // followed (128-byte aligned) by `ns` stages of {g[kDgcTile], r[kDgcTile]}
+  uint64_t full[kMaxStages], empty[kMaxStages];
+  GroupSmem grp[kMaxGroups];
 };
 constexpr size_t kStreamHdr = (sizeof(StreamSmem) + 127) / 128 * 128;
 constexpr size_t kStageBytes = 2 * kDgcTile * sizeof(float);
@@ -247,69 +252,75 @@ __device__ __forceinline__ float* stage_r(unsigned char* smem, int s) { return s
 // segment bookkeeping by the 256 consumer threads of a CTA that has finished its
 // share (`units` units) of segment S: flush the private histogram, add the
 // candidate count, and if this completes the segment pick the k-th key's bin.
-__device__ void stream_segment_done(const SegH1& S, uint32_t units, StreamSmem& sm) {
-  csync<1>();
+template <int BAR>
+__device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& sm) {
+  const int tid = ctid<BAR>();
+  csync<BAR>();
   if (units == S.nunits) {
     // the CTA streamed the whole segment: select from its private histogram
     const uint32_t total = sm.cta_count;
     if (total < S.k) {
-      if (threadIdx.x == 0) {
+      if (tid == 0) {
         S.st->fallback = 1;
         atomicAdd(S.bflag, 1u);
       }
     } else {
       uint32_t bin, above;
-      select_bin<1, false>(sm.hist, 2048, S.k, &bin, &above, sm.scan);
-      if (threadIdx.x == 0) {
+      select_bin<BAR, false>(sm.hist, 2048, S.k, &bin, &above, sm.scan);
+      if (tid == 0) {
         S.st->prefix = bin;
         S.st->above = above;
         S.st->need = S.k - above;
       }
     }
-    csync<1>();
-    for (int i = threadIdx.x; i < 2048; i += kThreads) sm.hist[i] = 0;
-    if (threadIdx.x == 0) sm.cta_count = 0;
-    csync<1>();
+    csync<BAR>();
+    for (int i = tid; i < 2048; i += kThreads) sm.hist[i] = 0;
+    if (tid == 0) sm.cta_count = 0;
+    csync<BAR>();
     return;
   }
-  for (int i = threadIdx.x; i < 2048; i += kThreads) {
+  for (int i = tid; i < 2048; i += kThreads) {
     const uint32_t h = sm.hist[i];
     if (h) {
       atomicAdd(&S.hist[i], h);
       sm.hist[i] = 0;
     }
   }
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     if (sm.cta_count) atomicAdd(&S.st->count, sm.cta_count);
     sm.cta_count = 0;
     __threadfence();
     const uint32_t old = atomicAdd(&S.st->done, units);
     sm.flag = (old + units == S.nunits);
   }
-  csync<1>();
+  csync<BAR>();
   if (!sm.flag) return;
   __threadfence();
   const uint32_t total = __ldcg(&S.st->count);
   if (total < S.k) {
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       S.st->fallback = 1;
       atomicAdd(S.bflag, 1u);
     }
-    csync<1>();
+    csync<BAR>();
     return;
   }
   uint32_t bin, above;
-  select_bin<1, true>(S.hist, 2048, S.k, &bin, &above, sm.scan);
-  if (threadIdx.x == 0) {
+  select_bin<BAR, true>(S.hist, 2048, S.k, &bin, &above, sm.scan);
+  if (tid == 0) {
     S.st->prefix = bin;
     S.st->above = above;
     S.st->need = S.k - above;
   }
 }
 
-__global__ void __launch_bounds__(kThreads + 32, 2) dgc_stream_kernel(const SegH1* __restrict__ segs,
-                                                                      const uint32_t* __restrict__ unit_seg,
-                                                                      uint32_t nunits, int variant, int ns) {
+// NCG consumer groups of 8 warps: group c takes the CTA's tiles i = c, c + NCG,
+// ... (stage i mod ns), so NCG tiles are computed at once while the producer
+// keeps the ring full.
+template <int NCG>
+__global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(const SegH1* __restrict__ segs,
+                                                                            const uint32_t* __restrict__ unit_seg,
+                                                                            uint32_t nunits, int variant, int ns) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -321,12 +332,12 @@ __global__ void __launch_bounds__(kThreads + 32, 2) dgc_stream_kernel(const SegH
       mbar_init(&sm.empty[s], kThreads / 32);
     }
     fence_barrier_init();
-    sm.cta_count = 0;
+    for (int c = 0; c < NCG; ++c) sm.grp[c].cta_count = 0;
   }
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) sm.hist[i] = 0;
+  for (int i = threadIdx.x; i < NCG * 2048; i += blockDim.x) sm.grp[i / 2048].hist[i % 2048] = 0;
   __syncthreads();
 
-  if (warp == kThreads / 32) {
+  if (warp == NCG * kThreads / 32) {
     // ---- producer warp: one elected lane streams tiles into the ring
     if (lane == 0) {
       const uint64_t pol = (variant & 1) ? policy_evict_first() : policy_evict_normal();
@@ -374,18 +385,24 @@ __global__ void __launch_bounds__(kThreads + 32, 2) dgc_stream_kernel(const SegH
     return;
   }
 
-  // ---- 8 consumer warps
+  // ---- NCG groups of 8 consumer warps
+  const int cg = NCG == 1 ? 0 : warp / (kThreads / 32);
+  GroupSmem& gs = sm.grp[cg];
+  auto seg_done = [&](const SegH1& S, uint32_t units) {
+    if (NCG == 1 || cg == 0) stream_segment_done<1>(S, units, gs);
+    else stream_segment_done<2>(S, units, gs);
+  };
   uint32_t cur = 0xFFFFFFFFu, cur_units = 0, thr = 0;
   const float* g = nullptr;
   SegH1 S{};
-  uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
-  int stage = 0;
+  uint32_t sid_next = u0 + cg < u1 ? unit_seg[u0 + cg] : 0u;
+  int stage = cg;
   uint32_t phase = 0;
-  for (uint32_t u = u0; u < u1; ++u) {
+  for (uint32_t u = u0 + cg; u < u1; u += NCG) {
     const uint32_t sid = sid_next;
-    if (u + 1 < u1) sid_next = unit_seg[u + 1];
+    if (u + NCG < u1) sid_next = unit_seg[u + NCG];
     if (sid != cur) {
-      if (cur != 0xFFFFFFFFu) stream_segment_done(S, cur_units, sm);
+      if (cur != 0xFFFFFFFFu) seg_done(S, cur_units);
       cur = sid;
       S = segs[sid];
       g = seg_g(S);
@@ -395,7 +412,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) dgc_stream_kernel(const SegH
     ++cur_units;
     const uint32_t start = (u - S.unit0) * kDgcTile;
     const uint32_t n = S.n;
-    const uint32_t lbase = warp * kRun;            // tile-relative
+    const uint32_t lbase = (warp & 7) * kRun;      // tile-relative
     const uint32_t base = start + lbase;           // segment-relative
     // fast path: a whole tile in shared memory (aligned, EF on, inside the segment)
     const bool full = S.ef && start + kDgcTile <= n && al16(g + start) && al16(S.r + start);
@@ -440,8 +457,9 @@ __global__ void __launch_bounds__(kThreads + 32, 2) dgc_stream_kernel(const SegH
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[stage]);   // stage consumed (values in registers)
-    if (++stage == ns) {
-      stage = 0;
+    stage += NCG;
+    if (stage >= ns) {
+      stage -= ns;
       phase ^= 1;
     }
     if (base < n) {
@@ -454,22 +472,22 @@ __global__ void __launch_bounds__(kThreads + 32, 2) dgc_stream_kernel(const SegH
         for (int j = 0; j < kNJ; ++j) store4_guard(S.r, base + j * 128 + lane * 4, n, av[j]);
       }
       const uint32_t run = base / kRun;
-      const uint32_t wc = full ? emit_run_full(av, base, thr, S.cand + (size_t)run * kRun, sm.hist)
-                               : emit_run(av, base, n, thr, S.cand + (size_t)run * kRun, sm.hist);
+      const uint32_t wc = full ? emit_run_full(av, base, thr, S.cand + (size_t)run * kRun, gs.hist)
+                               : emit_run(av, base, n, thr, S.cand + (size_t)run * kRun, gs.hist);
       if (lane == 0) {
         S.runcnt[run] = wc;
-        if (wc) atomicAdd(&sm.cta_count, wc);
+        if (wc) atomicAdd(&gs.cta_count, wc);
       }
     }
   }
-  if (cur != 0xFFFFFFFFu) stream_segment_done(S, cur_units, sm);
+  if (cur != 0xFFFFFFFFu) seg_done(S, cur_units);
 }
 
 // ------------------------------------------------------------------ 3. fallback
 // Segments whose sampled threshold let fewer than k candidates through are
 // recompacted from acc (= r after the streaming pass) with thr_lo.  Every CTA
 // scans the segment list; only flagged segments cost work.
-__global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __restrict__ segs, int nsegs) {
+__device__ void fallback_pass(const SegH1* __restrict__ segs, int nsegs, uint32_t cta, uint32_t ncta) {
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t sh[280];
   __shared__ uint32_t cta_count;
@@ -488,7 +506,7 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
     for (uint32_t li = 0; li < cnt; ++li) {
     const uint32_t sid = list[li];
     const SegH1 S = segs[sid];
-    if (blockIdx.x >= S.nunits) continue;
+    if (cta >= S.nunits) continue;
     for (int i = threadIdx.x; i < 2048; i += kThreads) hist[i] = 0;
     if (threadIdx.x == 0) cta_count = 0;
     __syncthreads();
@@ -510,7 +528,7 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
         }
       }
     };
-    recompact(blockIdx.x, gridDim.x, thr_fb);
+    recompact(cta, ncta, thr_fb);
     __syncthreads();
     for (int i = threadIdx.x; i < 2048; i += kThreads)
       if (hist[i]) atomicAdd(&S.hist[2048 + i], hist[i]);
@@ -551,76 +569,205 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
   }
 }
 
-// ------------------------------------------------------------------ 4. refine
-constexpr int kBatch = 4;   // candidate loads in flight per thread (refine, write pass 1)
-// A finalize group = kRunsPerGroup consecutive runs of one segment (one runcnt
-// per thread).  Its candidates are addressed as one flat, index-ordered list:
-// sh_off[i] = first flat position of run i; returns the group's total.
-__device__ __forceinline__ uint32_t group_offsets(const SegH1& S, uint32_t g, uint32_t* sh_off,
-                                                  uint32_t* sh_scan, uint32_t* nr_out) {
-  const uint32_t nruns = (S.n + kRun - 1) / kRun;
-  const uint32_t run0 = g * kRunsPerGroup;
-  const uint32_t nr = min((uint32_t)kRunsPerGroup, nruns - run0);
-  const uint32_t c = threadIdx.x < nr ? __ldcg(S.runcnt + run0 + threadIdx.x) : 0u;
-  uint32_t tot;
-  const uint32_t off = block_excl_scan(c, &tot, sh_scan);
-  if (threadIdx.x < nr) sh_off[threadIdx.x] = off;
-  if (threadIdx.x == 0) sh_off[nr] = tot;
-  __syncthreads();
-  *nr_out = nr;
-  return tot;
+// Thin kernel over the fallback pass (every CTA scans the segment list).
+__global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __restrict__ segs, int nsegs) {
+  fallback_pass(segs, nsegs, blockIdx.x, gridDim.x);
 }
 
-__device__ __forceinline__ uint2 group_cand(const SegH1& S, uint32_t g, const uint32_t* sh_off, uint32_t nr,
-                                           uint32_t q) {
-  uint32_t lo = 0, hi = nr;   // largest i with sh_off[i] <= q
+// ------------------------------------------------------------------ 4. refine
+// A finalize group = kRunsPerGroup (64) consecutive runs of one segment, owned
+// by ONE WARP: the finalize is a chain of dependent small loads (descriptor,
+// run counts, candidates, counters), so it is throughput-bound on the number of
+// independent chains in flight -- 64 warps per SM, no CTA barriers.  The
+// group's candidates are addressed as one flat, index-ordered list:
+// off[i] = first flat position of run i (lane l holds runs 2l and 2l+1).
+static_assert(kRunsPerGroup == 64, "two run counts per lane");
+constexpr int kBatch = 4;            // candidate loads in flight per lane
+constexpr uint32_t kDirect = 2048;   // refine: up to this many candidates, global atomics directly
+constexpr int kWarpsPerCta = kThreads / 32;
+
+struct WarpGroup {
+  const SegH1* S;
+  uint32_t g;      // group index within the segment
+  uint32_t C;      // candidates in the group
+  uint32_t nr;     // runs in the group
+};
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// off: this warp's 65-entry offset table in shared memory
+__device__ __forceinline__ WarpGroup warp_group_offsets(const SegH1* segs, const uint32_t* group_seg, uint32_t gi,
+                                                        uint32_t* off) {
+  const int lane = threadIdx.x & 31;
+  WarpGroup G;
+  G.S = segs + group_seg[gi];
+  const SegH1& S = *G.S;
+  G.g = gi - S.group0;
+  const uint32_t nruns = (S.n + kRun - 1) / kRun;
+  const uint32_t run0 = G.g * kRunsPerGroup;
+  G.nr = min((uint32_t)kRunsPerGroup, nruns - run0);
+  const uint32_t i0 = 2 * lane, i1 = 2 * lane + 1;
+  const uint32_t c0 = i0 < G.nr ? __ldcg(S.runcnt + run0 + i0) : 0u;
+  const uint32_t c1 = i1 < G.nr ? __ldcg(S.runcnt + run0 + i1) : 0u;
+  const uint32_t incl = warp_incl_scan(c0 + c1);
+  const uint32_t ex = incl - c0 - c1;
+  off[i0] = ex;
+  off[i1] = ex + c0;
+  G.C = __shfl_sync(0xffffffffu, incl, 31);
+  if (lane == 31) off[64] = incl;
+  __syncwarp();
+  return G;
+}
+
+__device__ __forceinline__ uint2 warp_group_cand(const WarpGroup& G, const uint32_t* off, uint32_t q) {
+  uint32_t lo = 0, hi = G.nr;   // largest i with off[i] <= q
   while (hi - lo > 1) {
     const uint32_t mid = (lo + hi) >> 1;
-    if (sh_off[mid] <= q) lo = mid; else hi = mid;
+    if (off[mid] <= q) lo = mid; else hi = mid;
   }
-  return __ldcg(S.cand + (size_t)(g * kRunsPerGroup + lo) * kRun + (q - sh_off[lo]));
+  return __ldcg(G.S->cand + (size_t)(G.g * kRunsPerGroup + lo) * kRun + (q - off[lo]));
+}
+
+// After round 2 a group's candidates are DENSE: compacted in place to the
+// front of the group's slot range, the count in runcnt[first run].
+__device__ __forceinline__ WarpGroup warp_group_dense(const SegH1* segs, const uint32_t* group_seg, uint32_t gi) {
+  WarpGroup G;
+  G.S = segs + group_seg[gi];
+  G.g = gi - G.S->group0;
+  G.nr = 0;
+  G.C = __ldcg(G.S->runcnt + (size_t)G.g * kRunsPerGroup);
+  return G;
+}
+__device__ __forceinline__ uint2* group_slots(const WarpGroup& G) {
+  return G.S->cand + (size_t)G.g * kRunsPerGroup * kRun;
+}
+
+// Warp-wide: bin b of a 1024-bin global histogram (scanning from the top) with
+// above(b) < need <= above(b) + hist[b]; (0, 0) if there is none (as select_bin).
+__device__ __forceinline__ void warp_select_bin(const uint32_t* hist, uint32_t need, uint32_t* out_bin,
+                                                uint32_t* out_above) {
+  const int lane = threadIdx.x & 31;
+  uint32_t h[32];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(hist) + lane * 8 + i);
+    h[4 * i] = v.x; h[4 * i + 1] = v.y; h[4 * i + 2] = v.z; h[4 * i + 3] = v.w;
+    sum += v.x + v.y + v.z + v.w;
+  }
+  // above this lane's bins = sum over lanes > lane (suffix scan)
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_down_sync(0xffffffffu, x, o);
+    if (lane + o < 32) x += y;
+  }
+  const uint32_t above = x - sum;
+  uint32_t bin = 0, ab = 0;
+  const bool mine = above < need && need <= above + sum;
+  if (mine) {
+    uint32_t cum = above;
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+      if (cum + h[i] >= need) { bin = lane * 32 + i; ab = cum; break; }
+      cum += h[i];
+    }
+  }
+  const uint32_t m = __ballot_sync(0xffffffffu, mine);
+  if (m) {
+    const int src = __ffs(m) - 1;
+    bin = __shfl_sync(0xffffffffu, bin, src);
+    ab = __shfl_sync(0xffffffffu, ab, src);
+  }
+  *out_bin = m ? bin : 0u;
+  *out_above = m ? ab : 0u;
 }
 
 template <int ROUND>
-__global__ void __launch_bounds__(kThreads) dgc_refine_kernel(const SegH1* __restrict__ segs,
-                                                              const uint32_t* __restrict__ group_seg) {
-  __shared__ uint32_t sh_hist[1024];
-  __shared__ uint32_t sh_scan[280];
-  __shared__ uint32_t sh_off[kRunsPerGroup + 1];
-  __shared__ int sh_flag;
+__global__ void __launch_bounds__(kThreads, 8) dgc_refine_kernel(const SegH1* __restrict__ segs,
+                                                              const uint32_t* __restrict__ group_seg,
+                                                              uint32_t ngroups) {
+  __shared__ uint32_t sh_off[kWarpsPerCta][kRunsPerGroup + 1];
+  // 1024 16-bit bins per warp, two per word (a group has <= 64 x 512 candidates < 2^16)
+  __shared__ uint32_t sh_hist[kWarpsPerCta][512];
   constexpr int kShiftMatch = ROUND == 2 ? 20 : 10;
   constexpr int kShiftBin = ROUND == 2 ? 10 : 0;
-  const uint32_t sid = group_seg[blockIdx.x];
-  const SegH1 S = segs[sid];
-  const uint32_t g = blockIdx.x - S.group0;
-  for (int i = threadIdx.x; i < 1024; i += kThreads) sh_hist[i] = 0;
-  uint32_t nr;
-  const uint32_t C = group_offsets(S, g, sh_off, sh_scan, &nr);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t gi = blockIdx.x * kWarpsPerCta + w;
+  if (gi >= ngroups) return;   // warp-uniform; this kernel has no CTA barrier
+  uint32_t* off = sh_off[w];
+  // round 2 reads the run-major candidates and compacts them in place (every
+  // later pass reads them densely); round 3 reads the dense list
+  const WarpGroup G = ROUND == 2 ? warp_group_offsets(segs, group_seg, gi, off) : warp_group_dense(segs, group_seg, gi);
+  const SegH1& S = *G.S;
+  uint2* dense = group_slots(G);
   const uint32_t prefix = __ldcg(&S.st->prefix);
-  // latency-bound: kBatch independent candidate loads in flight per thread
-  for (uint32_t q0 = threadIdx.x; q0 < C; q0 += kBatch * kThreads) {
-    uint32_t key[kBatch];
+  uint32_t* ghist = S.hist + (ROUND == 2 ? 4096 : 5120);
+  // few candidates (the sampled DGC case): global atomics per match; many
+  // (TOPK, fallbacks): a warp-private shared histogram, flushed once
+  const bool direct = G.C <= kDirect;
+  uint32_t* wh = sh_hist[w];
+  if (!direct) {
+    for (int i = lane; i < 512; i += 32) wh[i] = 0;
+    __syncwarp();
+  }
+  for (uint32_t base = 0; base < G.C; base += kBatch * 32) {   // warp-uniform trip count
+    uint2 cv[kBatch];
 #pragma unroll
     for (int m = 0; m < kBatch; ++m) {
-      const uint32_t q = q0 + m * kThreads;
-      key[m] = q < C ? group_cand(S, g, sh_off, nr, q).y & 0x7FFFFFFFu : 0xFFFFFFFFu;
+      const uint32_t q = base + m * 32 + lane;
+      cv[m] = q < G.C ? (ROUND == 2 ? warp_group_cand(G, off, q) : __ldcg(dense + q)) : make_uint2(0u, 0u);
+    }
+    if (ROUND == 2) {
+      // slot q <= the source slot of every candidate >= q, so once the whole
+      // batch is in registers its stores clobber nothing unread
+      __syncwarp();
+#pragma unroll
+      for (int m = 0; m < kBatch; ++m) {
+        const uint32_t q = base + m * 32 + lane;
+        if (q < G.C) dense[q] = cv[m];
+      }
     }
 #pragma unroll
-    for (int m = 0; m < kBatch; ++m)
-      if (key[m] != 0xFFFFFFFFu && (key[m] >> kShiftMatch) == prefix)
-        atomicAdd(&sh_hist[(key[m] >> kShiftBin) & 1023u], 1u);
+    for (int m = 0; m < kBatch; ++m) {
+      const uint32_t key = cv[m].y & 0x7FFFFFFFu;
+      if (base + m * 32 + lane < G.C && (key >> kShiftMatch) == prefix) {
+        const uint32_t bin = (key >> kShiftBin) & 1023u;
+        if (direct) atomicAdd(&ghist[bin], 1u);
+        else atomicAdd(&wh[bin >> 1], 1u << (16 * (bin & 1)));
+      }
+    }
   }
-  __syncthreads();
-  uint32_t* ghist = S.hist + (ROUND == 2 ? 4096 : 5120);
-  for (int i = threadIdx.x; i < 1024; i += kThreads) {
-    const uint32_t h = sh_hist[i];
-    if (h) atomicAdd(&ghist[i], h);
+  if (ROUND == 2 && lane == 0) S.runcnt[(size_t)G.g * kRunsPerGroup] = G.C;   // the dense count
+  if (!direct) {
+    __syncwarp();
+    for (int i = lane; i < 512; i += 32) {
+      const uint32_t h = wh[i];
+      if (h & 0xFFFFu) atomicAdd(&ghist[2 * i], h & 0xFFFFu);
+      if (h >> 16) atomicAdd(&ghist[2 * i + 1], h >> 16);
+    }
   }
-  if (!last_cta(ROUND == 2 ? &S.st->done_r2 : &S.st->done_r3, S.ngroups, &sh_flag)) return;
+  // the warp that completes the segment's round selects the next 10 bits
+  uint32_t last = 0;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(ROUND == 2 ? &S.st->done_r2 : &S.st->done_r3, 1u) == S.ngroups - 1;
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  __threadfence();
   const uint32_t need = __ldcg(&S.st->need);
   uint32_t bin, above;
-  select_bin<0, true>(ghist, 1024, need, &bin, &above, sh_scan);
-  if (threadIdx.x == 0) {
+  warp_select_bin(ghist, need, &bin, &above);
+  if (lane == 0) {
     S.st->prefix = (prefix << 10) | bin;
     S.st->above = __ldcg(&S.st->above) + above;
     S.st->need = need - above;
@@ -634,114 +781,124 @@ __device__ __forceinline__ unsigned long long lb_pack(uint32_t flag, uint32_t ab
   return ((unsigned long long)flag << 62) | ((unsigned long long)above << 31) | tie;
 }
 
-__global__ void __launch_bounds__(kThreads) dgc_write_kernel(const SegH1* __restrict__ segs,
+__global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __restrict__ segs,
                                                              const uint32_t* __restrict__ group_seg,
+                                                             uint32_t ngroups,
                                                              unsigned char* const* __restrict__ dsts,
                                                              unsigned long long* const* __restrict__ cnts,
                                                              int ndst) {
-  __shared__ uint32_t sh_scan[16];
-  __shared__ uint32_t sh_off[kRunsPerGroup + 1];
-  __shared__ uint32_t sh_prefix[2];
-  const uint32_t sid = group_seg[blockIdx.x];
-  const SegH1 S = segs[sid];
-  const uint32_t g = blockIdx.x - S.group0;
-  uint32_t nr;
-  const uint32_t C = group_offsets(S, g, sh_off, sh_scan, &nr);
-  const uint32_t T = __ldcg(&S.st->prefix);
-  const uint32_t need = __ldcg(&S.st->need);
-  auto cand_at = [&](uint32_t q) -> uint2 { return group_cand(S, g, sh_off, nr, q); };
-  // pass 1: the group's aggregate
-  uint32_t above = 0, tie = 0;
-  for (uint32_t q0 = threadIdx.x; q0 < C; q0 += kBatch * kThreads) {
-    uint32_t key[kBatch];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint32_t gi = blockIdx.x * kWarpsPerCta + w;
+  if (gi < ngroups) {
+    const WarpGroup G = warp_group_dense(segs, group_seg, gi);
+    const SegH1& S = *G.S;
+    const uint32_t C = G.C, g = G.g;
+    const uint2* dense = group_slots(G);
+    const uint32_t T = __ldcg(&S.st->prefix);
+    const uint32_t need = __ldcg(&S.st->need);
+    // pass 1: the group's aggregate
+    uint32_t above = 0, tie = 0;
+    for (uint32_t q0 = lane; q0 < C; q0 += kBatch * 32) {
+      uint32_t key[kBatch];
 #pragma unroll
-    for (int m = 0; m < kBatch; ++m) {
-      const uint32_t q = q0 + m * kThreads;
-      key[m] = q < C ? cand_at(q).y & 0x7FFFFFFFu : 0u;   // 0 < T unless T = 0
+      for (int m = 0; m < kBatch; ++m) {
+        const uint32_t q = q0 + m * 32;
+        key[m] = q < C ? __ldcg(&dense[q].y) & 0x7FFFFFFFu : 0u;
+      }
+#pragma unroll
+      for (int m = 0; m < kBatch; ++m) {
+        const bool in = q0 + m * 32 < C;
+        above += in && key[m] > T;
+        tie += in && key[m] == T;
+      }
     }
 #pragma unroll
-    for (int m = 0; m < kBatch; ++m) {
-      const bool in = q0 + m * kThreads < C;
-      above += in && key[m] > T;
-      tie += in && key[m] == T;
+    for (int o = 16; o > 0; o >>= 1) {
+      above += __shfl_xor_sync(0xffffffffu, above, o);
+      tie += __shfl_xor_sync(0xffffffffu, tie, o);
     }
-  }
-  above = block_sum_u32(above, sh_scan);
-  tie = block_sum_u32(tie, sh_scan);
-  // decoupled look-back over the segment's groups (blockIdx order = group order)
-  if (threadIdx.x == 0) {
-    unsigned long long* st = reinterpret_cast<unsigned long long*>(S.gcnt);
+    // decoupled look-back over the segment's groups, 32 predecessors per step
+    // (lane i reads group g-1-i of the window)
+    unsigned long long* lb = reinterpret_cast<unsigned long long*>(S.gcnt);
     uint32_t ea = 0, et = 0;
-    if (g == 0) {
-      atomicExch(&st[0], lb_pack(2, above, tie));
-    } else {
-      atomicExch(&st[g], lb_pack(1, above, tie));
-      for (int j = (int)g - 1; j >= 0; --j) {
+    if (lane == 0) atomicExch(&lb[g], lb_pack(g == 0 ? 2 : 1, above, tie));
+    if (g > 0) {
+      int top = (int)g - 1;
+      while (true) {
+        const int j = top - lane;
         unsigned long long v;
-        do {
-          v = atomicAdd(&st[j], 0ull);
-        } while ((v >> 62) == 0);
-        ea += (uint32_t)((v >> 31) & 0x7FFFFFFFu);
-        et += (uint32_t)(v & 0x7FFFFFFFu);
-        if ((v >> 62) == 2) break;
-      }
-      atomicExch(&st[g], lb_pack(2, ea + above, et + tie));
-    }
-    sh_prefix[0] = ea;
-    sh_prefix[1] = et;
-  }
-  __syncthreads();
-  // pass 2: ordered selection; selected before this group = above_before + min(ties_before, need)
-  uint32_t tie_run = sh_prefix[1];
-  uint32_t sel_run = sh_prefix[0] + min(sh_prefix[1], need);
-  uint32_t* out_idx = reinterpret_cast<uint32_t*>(S.chunk);
-  float* out_val = reinterpret_cast<float*>(S.chunk + 4 * (size_t)S.kpad);
-  // software-pipelined: the next chunk's candidate is loaded before this one is used
-  uint2 c_next = threadIdx.x < C ? cand_at(threadIdx.x) : make_uint2(0, 0);
-  for (uint32_t q0 = 0; q0 < C; q0 += kThreads) {
-    const uint32_t q = q0 + threadIdx.x;
-    uint32_t is_tie = 0, is_above = 0;
-    const uint2 c = c_next;
-    if (q + kThreads < C) c_next = cand_at(q + kThreads);
-    if (q < C) {
-      const uint32_t key = c.y & 0x7FFFFFFFu;
-      is_above = key > T;
-      is_tie = key == T;
-    }
-    // chunks without any key >= T (most of them when the candidate set is loose,
-    // e.g. TOPK's unsampled set) add nothing: skip their two scans
-    if (!__syncthreads_or(is_above | is_tie)) continue;
-    uint32_t ttot;
-    const uint32_t trank = tie_run + block_excl_scan(is_tie, &ttot, sh_scan);
-    const uint32_t sel = is_above || (is_tie && trank < need);
-    uint32_t stot;
-    const uint32_t pos = sel_run + block_excl_scan(sel, &stot, sh_scan);
-    if (sel) {
-      if (dsts) {
-        // fused Allgather: the entry goes straight into this rank's slot of
-        // every rank's receive buffer over NVLink (consecutive threads write
-        // consecutive positions: coalesced peer stores)
-        for (int q = 0; q < ndst; ++q) {
-          unsigned char* ch = dsts[q] + S.chunk_off;
-          reinterpret_cast<uint32_t*>(ch)[pos] = c.x;
-          reinterpret_cast<float*>(ch + 4 * (size_t)S.kpad)[pos] = __uint_as_float(c.y);
+        if (j >= 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(lb + j) : "memory");
+        else v = lb_pack(2, 0, 0);   // before the first group: an inclusive zero
+        const uint32_t flag = (uint32_t)(v >> 62);
+        if (__any_sync(0xffffffffu, flag == 0)) {
+          __nanosleep(20);
+          continue;   // a predecessor in the window has not published yet
         }
-      } else {
-        out_idx[pos] = c.x;
-        out_val[pos] = __uint_as_float(c.y);
+        const uint32_t inc = __ballot_sync(0xffffffffu, flag == 2);
+        const int lim = inc ? __ffs(inc) - 1 : 31;   // nearest inclusive predecessor
+        uint32_t a = lane <= lim ? (uint32_t)((v >> 31) & 0x7FFFFFFFu) : 0u;
+        uint32_t t = lane <= lim ? (uint32_t)(v & 0x7FFFFFFFu) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          t += __shfl_xor_sync(0xffffffffu, t, o);
+        }
+        ea += a;
+        et += t;
+        if (inc) break;
+        top -= 32;
       }
-      if (S.ef) S.r[c.x] = 0.0f;
+      if (lane == 0) atomicExch(&lb[g], lb_pack(2, ea + above, et + tie));
     }
-    tie_run += ttot;
-    sel_run += stot;
+    // pass 2: ordered selection; selected before this group = above_before + min(ties_before, need)
+    uint32_t tie_run = et;
+    uint32_t sel_run = ea + min(et, need);
+    uint32_t* out_idx = reinterpret_cast<uint32_t*>(S.chunk);
+    float* out_val = reinterpret_cast<float*>(S.chunk + 4 * (size_t)S.kpad);
+    uint2 c_next = lane < C ? __ldcg(dense + lane) : make_uint2(0, 0);
+    for (uint32_t q0 = 0; q0 < C; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      const uint2 c = c_next;
+      if (q + 32 < C) c_next = __ldcg(dense + q + 32);
+      const uint32_t key = c.y & 0x7FFFFFFFu;
+      const bool in = q < C;
+      const bool is_above = in && key > T, is_tie = in && key == T;
+      const uint32_t tb = __ballot_sync(0xffffffffu, is_tie);
+      const uint32_t trank = tie_run + __popc(tb & lt_mask);
+      const bool sel = is_above || (is_tie && trank < need);
+      const uint32_t sb = __ballot_sync(0xffffffffu, sel);
+      const uint32_t pos = sel_run + __popc(sb & lt_mask);
+      if (sel) {
+        if (dsts) {
+          // fused Allgather: the entry goes straight into this rank's slot of
+          // every rank's receive buffer over NVLink (consecutive lanes write
+          // consecutive positions: coalesced peer stores)
+          for (int d = 0; d < ndst; ++d) {
+            unsigned char* ch = dsts[d] + S.chunk_off;
+            reinterpret_cast<uint32_t*>(ch)[pos] = c.x;
+            reinterpret_cast<float*>(ch + 4 * (size_t)S.kpad)[pos] = __uint_as_float(c.y);
+          }
+        } else {
+          out_idx[pos] = c.x;
+          out_val[pos] = __uint_as_float(c.y);
+        }
+        if (S.ef) S.r[c.x] = 0.0f;
+      }
+      tie_run += __popc(tb);
+      sel_run += __popc(sb);
+    }
   }
   if (dsts) {
     // publish: the barrier orders the CTA's peer stores before thread 0's
     // system-scope fence (cumulative), which precedes the arrival increments
+    // (one per group of the CTA, as the waiting side counts groups)
     __syncthreads();
     if (threadIdx.x == 0) {
+      const uint32_t first = blockIdx.x * kWarpsPerCta;
+      const unsigned long long mine = first < ngroups ? min((uint32_t)kWarpsPerCta, ngroups - first) : 0u;
       __threadfence_system();
-      for (int q = 0; q < ndst; ++q) atomicAdd_system(cnts[q], 1ull);
+      for (int d = 0; d < ndst; ++d) atomicAdd_system(cnts[d], mine);
     }
   }
 }
@@ -793,13 +950,16 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
                    int ndst) {
   if (nsegs == 0) return;
   static const bool attr_set = [] {
-    return cudaFuncSetAttribute(dgc_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(kStreamHdr + kMaxStages * kStageBytes)) == cudaSuccess;
+    const int bytes = (int)(kStreamHdr + kMaxStages * kStageBytes);
+    return cudaFuncSetAttribute(dgc_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(dgc_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+               cudaSuccess;
   }();
   (void)attr_set;
   num_sms();
   // tuning knobs (measured on B200): bit0 of ESP_TMA_VARIANT = L2
-  // evict-first hint on the tile loads, bit1 = 2 CTAs per SM; ESP_TMA_STAGES
+  // evict-first hint on the tile loads, bit2 = one consumer group; ESP_TMA_STAGES
   static const int variant = [] {
     const char* e = getenv("ESP_TMA_VARIANT");
     return e ? atoi(e) : 0;
@@ -809,17 +969,22 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
   dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs, ff ? atoi(ff) : 0);
   if (probe0) cudaEventRecord(probe0, st);
   {
-    const int per_sm = (variant & 2) ? 2 : 1;
-    const int ns = per_sm == 2 ? (stages > 3 ? 3 : stages) : stages;
-    const int grid = nunits < per_sm * g_num_sms ? nunits : per_sm * g_num_sms;
-    dgc_stream_kernel<<<grid, kThreads + 32, kStreamHdr + ns * kStageBytes, st>>>(
-        segs, unit_seg, (uint32_t)nunits, variant, ns);
+    const int grid = nunits < g_num_sms ? nunits : g_num_sms;
+    if (variant & 4)   // one consumer group (A/B experiments)
+      dgc_stream_kernel<1><<<grid, kThreads + 32, kStreamHdr + stages * kStageBytes, st>>>(
+          segs, unit_seg, (uint32_t)nunits, variant, stages);
+    else
+      dgc_stream_kernel<2><<<grid, 2 * kThreads + 32, kStreamHdr + stages * kStageBytes, st>>>(
+          segs, unit_seg, (uint32_t)nunits, variant, stages);
   }
   if (probe1) cudaEventRecord(probe1, st);
   dgc_fallback_kernel<<<g_num_sms, kThreads, 0, st>>>(segs, nsegs);
-  dgc_refine_kernel<2><<<ngroups, kThreads, 0, st>>>(segs, group_seg);
-  dgc_refine_kernel<3><<<ngroups, kThreads, 0, st>>>(segs, group_seg);
-  dgc_write_kernel<<<ngroups, kThreads, 0, st>>>(segs, group_seg, dsts, cnts, ndst);
+  const int wgrid = (ngroups + kWarpsPerCta - 1) / kWarpsPerCta;   // one warp per finalize group
+  if (wgrid > 0) {
+    dgc_refine_kernel<2><<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
+    dgc_refine_kernel<3><<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
+    dgc_write_kernel<<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups, dsts, cnts, ndst);
+  }
   count_launches(6);
 }
 

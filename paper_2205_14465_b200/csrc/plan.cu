@@ -451,7 +451,7 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     }
   }
   const size_t st_bytes = round_up(nst * sizeof(SelState), 256);
-  const size_t flags_bytes = round_up(p.buckets.size() * 4, 256);
+  const size_t flags_bytes = round_up(p.buckets.size() * 8, 256);   // per bucket: fallback flag, grid barrier
   p.zero_bytes = flags_bytes + st_bytes + nhist;
   size_t zero_off = L.reserve(p.zero_bytes);
   p.zero = commit ? p.arena.base + zero_off : nullptr;
@@ -460,7 +460,7 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
   for (auto& b : p.buckets) {
     HostTables TB;
     build_bucket(L, b, TB, zero_off + flags_bytes, st_cursor, hist_cursor,
-                 commit ? reinterpret_cast<uint32_t*>(p.zero) + (&b - p.buckets.data()) : nullptr);
+                 commit ? reinterpret_cast<uint32_t*>(p.zero) + 2 * (&b - p.buckets.data()) : nullptr);
     // per-bucket device copies of the tables
     auto up = [&](const auto& vec, auto*& dst) {
       using E = typename std::decay<decltype(vec)>::type::value_type;
