@@ -24,6 +24,7 @@
 //                   output offset, ordered selection -> payload idx[]/val[] sorted
 //                   by index; EF: r[idx] := 0.
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -231,7 +232,7 @@ __device__ __forceinline__ uint32_t emit_run_full(const float4 (&av)[kNJ], uint3
 
 // ------------------------------------------------------------------ 2. stream (TMA)
 constexpr int kMaxStages = 6;   // 6 x 32 KB stages + header fit the 227 KB of one SM
-constexpr int kMaxGroups = 2;   // consumer groups of 8 warps (tiles in flight being computed)
+constexpr int kMaxGroups = 3;   // consumer groups of 8 warps (tiles in flight being computed)
 struct GroupSmem {   // per consumer group
   uint32_t hist[2048];
   uint32_t scan[280];
@@ -316,7 +317,10 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& s
 
 // NCG consumer groups of 8 warps: group c takes the CTA's tiles i = c, c + NCG,
 // ... (stage i mod ns), so NCG tiles are computed at once while the producer
-// keeps the ring full.
+// keeps the ring full.  ns must be a multiple of NCG: then every use of a stage
+// by a group follows that group's own previous use of it, which is what makes
+// the one-bit phase parity of the full barrier unambiguous (with ns % NCG != 0
+// a warp could pass a parity test one fill early).
 template <int NCG>
 __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(const SegH1* __restrict__ segs,
                                                                             const uint32_t* __restrict__ unit_seg,
@@ -390,7 +394,8 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
   GroupSmem& gs = sm.grp[cg];
   auto seg_done = [&](const SegH1& S, uint32_t units) {
     if (NCG == 1 || cg == 0) stream_segment_done<1>(S, units, gs);
-    else stream_segment_done<2>(S, units, gs);
+    else if (cg == 1) stream_segment_done<2>(S, units, gs);
+    else stream_segment_done<3>(S, units, gs);
   };
   uint32_t cur = 0xFFFFFFFFu, cur_units = 0, thr = 0;
   const float* g = nullptr;
@@ -944,6 +949,21 @@ int tma_stream_stages() {
   return stages;
 }
 
+// ESP_DEBUG_SYNC=1: synchronize after every kernel of the DGC pipeline and name
+// the one that failed (debugging aid; off by default)
+static void debug_sync(const char* what, cudaStream_t st) {
+  static const bool on = [] {
+    const char* e = getenv("ESP_DEBUG_SYNC");
+    return e && atoi(e) != 0;
+  }();
+  if (!on) return;
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[esp] %s failed: %s\n", what, cudaGetErrorString(e));
+    fflush(stderr);
+  }
+}
+
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
                    cudaEvent_t probe1, unsigned char* const* dsts, unsigned long long* const* cnts,
@@ -954,12 +974,14 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
     return cudaFuncSetAttribute(dgc_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
                cudaSuccess &&
            cudaFuncSetAttribute(dgc_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(dgc_stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
                cudaSuccess;
   }();
   (void)attr_set;
   num_sms();
   // tuning knobs (measured on B200): bit0 of ESP_TMA_VARIANT = L2
-  // evict-first hint on the tile loads, bit2 = one consumer group; ESP_TMA_STAGES
+  // evict-first hint on the tile loads, bit2 = one consumer group, bit3 = two; ESP_TMA_STAGES
   static const int variant = [] {
     const char* e = getenv("ESP_TMA_VARIANT");
     return e ? atoi(e) : 0;
@@ -967,23 +989,35 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
   const int stages = tma_stream_stages();
   const char* ff = getenv("ESP_DGC_FORCE_FALLBACK");   // read per launch: a test hook
   dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs, ff ? atoi(ff) : 0);
+  debug_sync("dgc_sample", st);
   if (probe0) cudaEventRecord(probe0, st);
   {
     const int grid = nunits < g_num_sms ? nunits : g_num_sms;
     if (variant & 4)   // one consumer group (A/B experiments)
       dgc_stream_kernel<1><<<grid, kThreads + 32, kStreamHdr + stages * kStageBytes, st>>>(
           segs, unit_seg, (uint32_t)nunits, variant, stages);
-    else
-      dgc_stream_kernel<2><<<grid, 2 * kThreads + 32, kStreamHdr + stages * kStageBytes, st>>>(
-          segs, unit_seg, (uint32_t)nunits, variant, stages);
+    else if (variant & 8) {   // two groups
+      const int ns = stages < 2 ? 2 : stages & ~1;
+      dgc_stream_kernel<2><<<grid, 2 * kThreads + 32, kStreamHdr + ns * kStageBytes, st>>>(
+          segs, unit_seg, (uint32_t)nunits, variant, ns);
+    } else {                  // three groups (default)
+      const int ns = stages < 3 ? 3 : stages - stages % 3;
+      dgc_stream_kernel<3><<<grid, 3 * kThreads + 32, kStreamHdr + ns * kStageBytes, st>>>(
+          segs, unit_seg, (uint32_t)nunits, variant, ns);
+    }
   }
+  debug_sync("dgc_stream", st);
   if (probe1) cudaEventRecord(probe1, st);
   dgc_fallback_kernel<<<g_num_sms, kThreads, 0, st>>>(segs, nsegs);
+  debug_sync("dgc_fallback", st);
   const int wgrid = (ngroups + kWarpsPerCta - 1) / kWarpsPerCta;   // one warp per finalize group
   if (wgrid > 0) {
     dgc_refine_kernel<2><<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
+    debug_sync("dgc_refine<2>", st);
     dgc_refine_kernel<3><<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
+    debug_sync("dgc_refine<3>", st);
     dgc_write_kernel<<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups, dsts, cnts, ndst);
+    debug_sync("dgc_write", st);
   }
   count_launches(6);
 }
