@@ -47,7 +47,11 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2
 // Per tile: the dense zero fill straight from registers (the 4 B/elem write
 // that bounds the kernel), then only the touched words are rewritten:
 //   one piece:     out[e] = (+0 + v) / d
-//   several:       out[e] = out[e] + v_r for r in rank order (the zero fill is
+//   several, <= 32 entries in the tile (the sparse common case): one entry per
+//                  lane, equal indices grouped by __match_any_sync, each group
+//                  summed from +0 in lane (= rank) order by its lowest lane and
+//                  stored once;
+//   several, more: out[e] = out[e] + v_r for r in rank order (the zero fill is
 //                  the sum's +0; __syncwarp orders the pieces), then each
 //                  distinct touched word is divided once (a per-warp bitmap
 //                  in shared memory elects the owner).
@@ -80,6 +84,14 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
     }
   };
   load_toff(S, tg - S.unit0);
+  // lane r holds the pointers of pieces r and r + 32 of the current segment
+  const unsigned char* pp0 = nullptr;
+  const unsigned char* pp1 = nullptr;
+  auto load_pp = [&](const SegH2& s) {
+    if ((uint32_t)lane < s.npieces) pp0 = pieces[s.piece0 + lane];
+    if ((uint32_t)lane + 32 < s.npieces) pp1 = pieces[s.piece0 + lane + 32];
+  };
+  load_pp(S);
   while (true) {
     const uint32_t t = tg - S.unit0;
     const uint32_t lo = t * kTile;
@@ -115,28 +127,68 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
         out[__ldg(idx + i)] = ones ? v : div(v);
       }
     } else {
+      // the tile's entries of all pieces, in rank order: lane l takes the l-th
+      uint32_t tot = 0, my_r = 0xFFFFFFFFu, my_i = 0;
       for (uint32_t r = 0; r < np; ++r) {
-        const unsigned char* pc = pieces[S.piece0 + r];
-        const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
-        const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
         uint32_t a, b;
         range(r, &a, &b);
-        for (uint32_t i = a + lane; i < b; i += 32) {
-          const uint32_t e = __ldg(idx + i);
-          const float v = __ldg(val + i);
-          out[e] = __fadd_rn(__ldcg(out + e), v);   // distinct indices within a piece
+        if ((uint32_t)lane >= tot && (uint32_t)lane < tot + (b - a)) {
+          my_r = r;
+          my_i = a + (lane - tot);
         }
-        __syncwarp();
+        tot += b - a;
       }
-      if (!ones) {
+      if (tot <= 32) {
+        // one entry per lane: lanes holding the same index form a group
+        // (__match_any_sync), whose lowest lane sums it in lane = rank order
+        // from +0 and stores it once -- no read-modify-write round trips
+        const int src = (int)(my_r & 31u);
+        const unsigned char* q0 = reinterpret_cast<const unsigned char*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(pp0), src));
+        const unsigned char* q1 = reinterpret_cast<const unsigned char*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(pp1), src));
+        uint32_t e = 0x80000000u | (uint32_t)lane;   // no entry: a key no index has
+        float v = 0.f;
+        if (my_r != 0xFFFFFFFFu) {
+          const unsigned char* pc = my_r < 32 ? q0 : q1;
+          e = __ldg(reinterpret_cast<const uint32_t*>(pc) + my_i);
+          v = __ldg(reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad) + my_i);
+        }
+        const uint32_t grp = __match_any_sync(0xffffffffu, e);
+        float sum = 0.f;
+        uint32_t rest = grp;
+        for (uint32_t m = 0; m < np; ++m) {   // at most one member per piece
+          const float x = __shfl_sync(0xffffffffu, v, rest ? __ffs(rest) - 1 : lane);
+          if (rest) {
+            sum = __fadd_rn(sum, x);
+            rest &= rest - 1;
+          }
+        }
+        if (my_r != 0xFFFFFFFFu && __ffs(grp) - 1 == lane) out[e] = ones ? sum : div(sum);
+      } else {
         for (uint32_t r = 0; r < np; ++r) {
-          const uint32_t* idx = reinterpret_cast<const uint32_t*>(pieces[S.piece0 + r]);
+          const unsigned char* pc = pieces[S.piece0 + r];
+          const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
+          const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
           uint32_t a, b;
           range(r, &a, &b);
           for (uint32_t i = a + lane; i < b; i += 32) {
             const uint32_t e = __ldg(idx + i);
-            const uint32_t w = e - lo, m = 1u << (w & 31);
-            if (!(atomicOr(&seen[w >> 5], m) & m)) out[e] = div(__ldcg(out + e));
+            const float v = __ldg(val + i);
+            out[e] = __fadd_rn(__ldcg(out + e), v);   // distinct indices within a piece
+          }
+          __syncwarp();
+        }
+        if (!ones) {
+          for (uint32_t r = 0; r < np; ++r) {
+            const uint32_t* idx = reinterpret_cast<const uint32_t*>(pieces[S.piece0 + r]);
+            uint32_t a, b;
+            range(r, &a, &b);
+            for (uint32_t i = a + lane; i < b; i += 32) {
+              const uint32_t e = __ldg(idx + i);
+              const uint32_t w = e - lo, m = 1u << (w & 31);
+              if (!(atomicOr(&seen[w >> 5], m) & m)) out[e] = div(__ldcg(out + e));
+            }
           }
         }
       }
@@ -146,6 +198,7 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
     if (Sn_p) {
       S = *Sn_p;
       out = seg_out(S);
+      load_pp(S);
     }
     __syncwarp();   // bitmap reuse
   }
