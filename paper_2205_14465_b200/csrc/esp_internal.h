@@ -117,6 +117,23 @@ struct esp_ctx_s {
   uint64_t r2_len = 0;
   uint64_t step = 0;
   uint64_t hash_base = 0;            // mix(mix(seed) ^ tensor_id)
+  // esp_decompress: device tables of the last (pieces, out) seen, reused while
+  // the caller passes the same buffers; staged through pinned memory
+  struct DecCache {
+    std::vector<const void*> pieces;
+    float* out = nullptr;
+    bool valid = false;
+    unsigned char* d = nullptr;      // device tables
+    size_t dcap = 0;
+    unsigned char* h = nullptr;      // pinned staging (guarded by ev)
+    size_t hcap = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+    size_t off_seg = 0, off_units = 0, off_pp = 0, off_rt = 0, off_ps = 0;
+    uint32_t nunits = 0;
+    int njobs = 0;
+    uint64_t step_uploaded = ~0ull;  // Randomk: step of the dyn word on the device
+  } dec;
 };
 
 namespace esp {

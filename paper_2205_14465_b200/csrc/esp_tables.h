@@ -72,7 +72,7 @@ struct SegH1 {
   // DGC / sign workspace
   uint2* cand;           // candidates, run-major: [run * kRun + i] = {idx, bits(acc)}
   uint32_t* runcnt;      // candidates per run
-  uint32_t* hist;        // 2048 (pass) + 2048 (fallback) + 1024 + 1024
+  uint32_t* hist;        // dgc_hist_words(hrep): stream, fallback, round 2, round 3
   SelState* st;
   uint32_t* bflag;       // bucket-wide "some segment fell back" counter; bflag[1]: the
                          // finalize's grid-barrier counter (both zeroed every call)
@@ -83,8 +83,20 @@ struct SegH1 {
   uint32_t npieces;
   uint32_t piece0;       // index into the piece-pointer array
   float divisor;
-  uint32_t pad_;
+  uint32_t hrep;         // DGC: replicas of the round-2/3 histograms (spread same-bin atomics)
 };
+
+// DGC histogram words of a segment: 2048 (stream) + 2048 (fallback) + 1024 x hrep
+// (round 2) + 1024 x hrep (round 3).  A round's matches number about k, all
+// landing in 1024 bins (32 cache lines): a segment with k in the millions
+// spreads them over hrep replicas, one per warp-group residue.
+constexpr uint32_t kMaxHrep = 16;
+__host__ __device__ inline uint32_t dgc_hrep(uint32_t k, uint32_t ngroups) {
+  uint32_t r = k / 65536u;
+  r = r < 1 ? 1 : (r > kMaxHrep ? kMaxHrep : r);
+  return r < ngroups ? r : (ngroups ? ngroups : 1);
+}
+__host__ __device__ inline uint32_t dgc_hist_words(uint32_t hrep) { return 4096 + 2048 * hrep; }
 
 // One h2 segment: out[0..n) = reduce(sum_r decode(piece r)).
 struct SegH2 {

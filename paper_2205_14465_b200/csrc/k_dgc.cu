@@ -15,7 +15,8 @@
 //                   compact candidates key(acc) >= thr per 512-element run in index
 //                   order (vote/ballot/popc) and histogram their top 11 key bits.  The
 //                   CTA that completes a segment picks the radix bin of the k-th key.
-//                   (TOPK: thr = 0, every element is a candidate.)
+//                   (TOPK: no threshold; every key is histogrammed, nothing emitted,
+//                   and step 3 recompacts from the k-th key's bin up.)
 //   3. dgc_fallback only segments with < k candidates: recompact with the
 //                   sample's far lower threshold thr_lo (then, if that misses too, 0).
 //   4. dgc_refine   two more radix rounds over the candidates -> the exact k-th key
@@ -87,8 +88,8 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t sh[280];
   const SegH1 S = segs[blockIdx.x];
-  if (S.unsampled) {   // TOPK: the exact radix select runs over every element
-    if (threadIdx.x == 0) S.st->thr = 0;
+  if (S.unsampled) {   // TOPK: no candidates in the streaming pass, which
+    if (threadIdx.x == 0) S.st->thr = 0xFFFFFFFFu;   // histograms every key instead
     return;
   }
   const uint32_t n = S.n;
@@ -260,7 +261,17 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& s
   if (units == S.nunits) {
     // the CTA streamed the whole segment: select from its private histogram
     const uint32_t total = sm.cta_count;
-    if (total < S.k) {
+    if (S.unsampled) {
+      // TOPK: the histogram holds every key and nothing was emitted; the
+      // recompaction pass takes the keys from the k-th key's 11-bit bin up
+      uint32_t bin, above;
+      select_bin<BAR, false>(sm.hist, 2048, S.k, &bin, &above, sm.scan);
+      if (tid == 0) {
+        S.st->thr_lo = bin << 20;
+        S.st->fallback = 1;
+        atomicAdd(S.bflag, 1u);
+      }
+    } else if (total < S.k) {
       if (tid == 0) {
         S.st->fallback = 1;
         atomicAdd(S.bflag, 1u);
@@ -298,6 +309,16 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& s
   if (!sm.flag) return;
   __threadfence();
   const uint32_t total = __ldcg(&S.st->count);
+  if (S.unsampled) {   // TOPK (see above)
+    uint32_t bin, above;
+    select_bin<BAR, true>(S.hist, 2048, S.k, &bin, &above, sm.scan);
+    if (tid == 0) {
+      S.st->thr_lo = bin << 20;
+      S.st->fallback = 1;
+      atomicAdd(S.bflag, 1u);
+    }
+    return;
+  }
   if (total < S.k) {
     if (tid == 0) {
       S.st->fallback = 1;
@@ -477,6 +498,16 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
         for (int j = 0; j < kNJ; ++j) store4_guard(S.r, base + j * 128 + lane * 4, n, av[j]);
       }
       const uint32_t run = base / kRun;
+      if (S.unsampled) {
+        // TOPK: the top 11 bits of every key (the radix select's first digit)
+#pragma unroll
+        for (int j = 0; j < kNJ; ++j) {
+          const uint32_t e = base + j * 128 + lane * 4;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (e + c < n) atomicAdd(&gs.hist[fkey(f4get(av[j], c)) >> 20], 1u);
+        }
+      }
       const uint32_t wc = full ? emit_run_full(av, base, thr, S.cand + (size_t)run * kRun, gs.hist)
                                : emit_run(av, base, n, thr, S.cand + (size_t)run * kRun, gs.hist);
       if (lane == 0) {
@@ -655,19 +686,25 @@ __device__ __forceinline__ uint2* group_slots(const WarpGroup& G) {
   return G.S->cand + (size_t)G.g * kRunsPerGroup * kRun;
 }
 
-// Warp-wide: bin b of a 1024-bin global histogram (scanning from the top) with
-// above(b) < need <= above(b) + hist[b]; (0, 0) if there is none (as select_bin).
-__device__ __forceinline__ void warp_select_bin(const uint32_t* hist, uint32_t need, uint32_t* out_bin,
-                                                uint32_t* out_above) {
+// Warp-wide: bin b of a 1024-bin global histogram, the sum of `rep` replicas
+// (scanning from the top) with above(b) < need <= above(b) + hist[b]; (0, 0)
+// if there is none (as select_bin).
+__device__ __forceinline__ void warp_select_bin(const uint32_t* hist, uint32_t rep, uint32_t need,
+                                                uint32_t* out_bin, uint32_t* out_above) {
   const int lane = threadIdx.x & 31;
   uint32_t h[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) h[i] = 0;
+  for (uint32_t r = 0; r < rep; ++r) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(hist + 1024u * r) + lane * 8 + i);
+      h[4 * i] += v.x; h[4 * i + 1] += v.y; h[4 * i + 2] += v.z; h[4 * i + 3] += v.w;
+    }
+  }
   uint32_t sum = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(hist) + lane * 8 + i);
-    h[4 * i] = v.x; h[4 * i + 1] = v.y; h[4 * i + 2] = v.z; h[4 * i + 3] = v.w;
-    sum += v.x + v.y + v.z + v.w;
-  }
+  for (int i = 0; i < 32; ++i) sum += h[i];
   // above this lane's bins = sum over lanes > lane (suffix scan)
   uint32_t x = sum;
 #pragma unroll
@@ -715,7 +752,9 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_refine_kernel(const SegH1* __
   const SegH1& S = *G.S;
   uint2* dense = group_slots(G);
   const uint32_t prefix = __ldcg(&S.st->prefix);
-  uint32_t* ghist = S.hist + (ROUND == 2 ? 4096 : 5120);
+  // this warp's replica of the round histogram
+  uint32_t* const ghist_all = S.hist + 4096 + (ROUND == 2 ? 0u : 1024u * S.hrep);
+  uint32_t* ghist = ghist_all + 1024u * (G.g % S.hrep);
   // few candidates (the sampled DGC case): global atomics per match; many
   // (TOPK, fallbacks): a warp-private shared histogram, flushed once
   const bool direct = G.C <= kDirect;
@@ -771,7 +810,7 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_refine_kernel(const SegH1* __
   __threadfence();
   const uint32_t need = __ldcg(&S.st->need);
   uint32_t bin, above;
-  warp_select_bin(ghist, need, &bin, &above);
+  warp_select_bin(ghist_all, S.hrep, need, &bin, &above);
   if (lane == 0) {
     S.st->prefix = (prefix << 10) | bin;
     S.st->above = __ldcg(&S.st->above) + above;
