@@ -26,7 +26,8 @@ void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long targ
 void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 // h1 on the persistent TMA streaming driver, tiles of kDgcTile (k_sign.cu)
 // pieces != nullptr: a7 (input = decode-mean of the segment's pieces, r = r2)
-void launch_sign_h1_tma(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits,
+// (+ one finalize kernel over the nsegs segments: the scales from the per-run partials)
+void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                         const unsigned char* const* pieces, cudaStream_t st);
 // NONE: pack gradients into a contiguous buffer (k_h2.cu)
 void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);

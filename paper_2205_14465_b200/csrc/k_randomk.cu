@@ -36,19 +36,22 @@ __device__ __forceinline__ uint32_t randomk_pick(uint64_t h, uint64_t j, uint64_
 
 // ------------------------------------------------------------------ h1
 struct RandomkOp {
+  static constexpr int kGroups = 3;   // consumer groups
   struct State {
     uint64_t h;
   };
   const unsigned char* const* pieces = nullptr;   // not a decoding op
-  __device__ void begin_segment(const SegH1& S, State& st, TmaHdr&) const {
+  bool stage_words = false;
+  template <int BAR>
+  __device__ void begin_segment(const SegH1& S, State& st, TmaGroup&) const {
     st.h = randomk_hash(S.hash, *S.step, S.part, S.rankterm);
   }
   template <bool FULL>
   __device__ void run(const SegH1& S, const float4 (&gv)[kNJ], const float4 (&rv)[kNJ], uint32_t base,
-                      State& st, TmaHdr& hd, const uint32_t*) const {
+                      State& st, TmaGroup& hd, const uint32_t*) const {
     const uint32_t n = S.n, k = S.k;
     if (base >= n) return;   // warp-uniform
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) & 7;   // warp within the group
     float* scr = hd.wscr[warp];
     uint32_t* msk = hd.wsel[warp];
     float4 av[kNJ];
@@ -94,7 +97,8 @@ struct RandomkOp {
       else store4_guard(S.r, base + off, n, nr);
     }
   }
-  __device__ void end_segment(const SegH1&, uint32_t, uint32_t, State&, TmaHdr&) const {}
+  template <int BAR>
+  __device__ void end_segment(const SegH1&, uint32_t, uint32_t, State&, TmaGroup&) const {}
 };
 
 // ------------------------------------------------------------------ h2
@@ -136,20 +140,9 @@ __global__ void __launch_bounds__(kThreads) h2_randomk_kernel(const SegH2* __res
   }
 }
 
-int tma_stream_grid(int nunits);
-int tma_stream_stages();
-
 void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st) {
   if (nunits == 0) return;
-  static bool init = [] {
-    return cudaFuncSetAttribute(tma_stream_kernel<RandomkOp>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(kTmaHdrBytes + kTmaMaxStages * kTmaStageBytes)) == cudaSuccess;
-  }();
-  (void)init;
-  const int ns = tma_stream_stages();
-  tma_stream_kernel<<<tma_stream_grid(nunits), kThreads + 32, kTmaHdrBytes + ns * kTmaStageBytes, st>>>(
-      segs, unit_seg, (uint32_t)nunits, ns, RandomkOp{});
-  count_launches(1);
+  launch_tma_op(segs, unit_seg, nunits, RandomkOp{}, st);
 }
 
 void launch_h2_randomk(const SegH2* segs, const uint32_t* unit_seg, int nunits,

@@ -11,7 +11,7 @@
 // nibbles of a 32-element word, one more shuffle transposes so that each lane
 // stores one word (one coalesced 128 B store per warp per 1024 elements).
 // sum|p| (EFSignSGD) or the class sums/counts (Onebit) are accumulated in fp64
-// and combined deterministically by the last CTA of the segment.
+// per warp run and combined in run order by sign_finalize_kernel.
 //
 // With DECODE the input is not a gradient but the mean of npieces received
 // chunks: the mid-scheme "decompress, aggregate, recompress" of quantized
@@ -36,43 +36,54 @@ __device__ __forceinline__ void piece_scales(const unsigned char* h, float* sp, 
   }
 }
 
-// ---- the same h1 on the persistent TMA streaming driver (stream_tma.cuh):
-// tiles of 4096 elements, 512 per warp (16 sign words per warp and tile).
+// ---- h1 on the persistent TMA streaming driver (stream_tma.cuh): tiles of
+// 4096 elements, 512 per warp (16 sign words per warp and tile).
 // DECODE: the input is the decode-mean of S.npieces received chunks (a7, the
 // mid-scheme recompression); the r stream is then the second residual r2.
+// No CTA barrier anywhere: every warp run writes its own partial sums (slot =
+// run index, all slots rewritten each call) and sign_finalize_kernel reduces
+// them per segment in run order, so segment boundaries cost nothing here.
 template <int KIND, bool DECODE = false>
 struct SignOp {
+  // consumer groups of 8 warps (the decoding variant needs ~100 registers)
+  static constexpr int kGroups = DECODE ? 2 : 3;
   const unsigned char* const* pieces = nullptr;
+  // DECODE: stage the pieces' sign words in the tile's g slot by TMA (the stage
+  // is then held until they are used) instead of loading them with LDG
+  bool stage_words = false;
   struct State {
-    float sp, sn;
-    double s0, s1;
-    uint32_t c0, c1;
+    float sp, sn;                            // lazy EF: last step's scale pair
+    float qsp0, qsn0, qsp1, qsn1;            // DECODE: scales of pieces lane, lane + 32
+    const uint32_t* qw0;                     // DECODE: words of pieces lane, lane + 32
+    const uint32_t* qw1;
   };
-  __device__ void begin_segment(const SegH1& S, State& st, TmaHdr& h) const {
-    if (DECODE) {
-      // stage the segment's piece table (scales, word pointers) in shared memory
-      csync<1>();
-      for (uint32_t q = threadIdx.x; q < S.npieces; q += kThreads) {
-        const unsigned char* p = pieces[S.piece0 + q];
-        float a, b;
-        piece_scales<KIND>(p, &a, &b);
-        h.psp[q] = a;
-        h.psn[q] = b;
-        h.pw[q] = reinterpret_cast<const uint32_t*>(p + 16);
-      }
-      csync<1>();
-    }
+  template <int BAR>
+  __device__ void begin_segment(const SegH1& S, State& st, TmaGroup&) const {
     st.sp = st.sn = 0.f;
     if (S.ef) {
       const float a = __ldcg(S.lazy_in), b = __ldcg(S.lazy_in + 1);
       if (KIND == K_EFSIGN) { st.sp = a; st.sn = -a; } else { st.sp = b; st.sn = a; }
     }
-    st.s0 = st.s1 = 0.0;
-    st.c0 = st.c1 = 0;
+    if (DECODE) {
+      // the segment's piece table, one piece per lane (two for n > 32)
+      const uint32_t lane = threadIdx.x & 31;
+      st.qsp0 = st.qsn0 = st.qsp1 = st.qsn1 = 0.f;
+      st.qw0 = st.qw1 = nullptr;
+      if (lane < S.npieces) {
+        const unsigned char* p = pieces[S.piece0 + lane];
+        piece_scales<KIND>(p, &st.qsp0, &st.qsn0);
+        st.qw0 = reinterpret_cast<const uint32_t*>(p + 16);
+      }
+      if (lane + 32 < S.npieces) {
+        const unsigned char* p = pieces[S.piece0 + lane + 32];
+        piece_scales<KIND>(p, &st.qsp1, &st.qsn1);
+        st.qw1 = reinterpret_cast<const uint32_t*>(p + 16);
+      }
+    }
   }
   template <bool FULL>
   __device__ void run(const SegH1& S, const float4 (&gv)[kNJ], const float4 (&rv)[kNJ], uint32_t base,
-                      State& st, TmaHdr& h, const uint32_t* sw) const {
+                      State& st, TmaGroup&, const uint32_t* sw) const {
     const uint32_t n = S.n;
     if (base >= n) return;   // warp-uniform
     const int lane = threadIdx.x & 31;
@@ -81,40 +92,35 @@ struct SignOp {
     for (int j = 0; j < kNJ; ++j) xv[j] = gv[j];
     if (DECODE) {
       // rank-order fp32 sum of the decoded chunks from +0, then / divisor (R9);
-      // the words of up to 8 pieces are loaded in one batch before any is used
+      // the pieces' words come from the stage (TMA) or, unstaged, by LDG
 #pragma unroll
       for (int j = 0; j < kNJ; ++j) xv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (uint32_t q0 = 0; q0 < S.npieces; q0 += 8) {
-        const uint32_t qn = min(8u, S.npieces - q0);
-        uint32_t wb[8][kNJ];
+      const uint32_t lt = (base & (kDgcTile - 1)) + lane * 4;   // tile-relative element of j = 0
+      for (uint32_t q = 0; q < S.npieces; ++q) {
+        const float psp = __shfl_sync(0xffffffffu, q < 32 ? st.qsp0 : st.qsp1, q & 31);
+        const float psn = __shfl_sync(0xffffffffu, q < 32 ? st.qsn0 : st.qsn1, q & 31);
+        uint32_t wb[kNJ];
+        if (sw) {
 #pragma unroll
-        for (uint32_t q = 0; q < 8; ++q) {
-          if (q < qn) {
+          for (int j = 0; j < kNJ; ++j) wb[j] = sw[q * (kDgcTile / 32) + ((lt + j * 128) >> 5)];
+        } else {
+          const uint32_t* pw = reinterpret_cast<const uint32_t*>(__shfl_sync(
+              0xffffffffu, reinterpret_cast<unsigned long long>(q < 32 ? st.qw0 : st.qw1), q & 31));
 #pragma unroll
-            for (int j = 0; j < kNJ; ++j) {
-              const uint32_t e = base + j * 128 + lane * 4;
-              const uint32_t l = (base & (kDgcTile - 1)) + j * 128 + lane * 4;   // tile-relative
-              wb[q][j] = !(FULL || e < n) ? 0u
-                         : sw             ? sw[(q0 + q) * (kDgcTile / 32) + (l >> 5)]
-                                          : __ldg(h.pw[q0 + q] + (e >> 5));
-            }
+          for (int j = 0; j < kNJ; ++j) {
+            const uint32_t e = base + j * 128 + lane * 4;
+            wb[j] = (FULL || e < n) ? __ldg(pw + (e >> 5)) : 0u;
           }
         }
 #pragma unroll
-        for (uint32_t q = 0; q < 8; ++q) {
-          if (q < qn) {
-            const float psp = h.psp[q0 + q], psn = h.psn[q0 + q];
-#pragma unroll
-            for (int j = 0; j < kNJ; ++j) {
-              const uint32_t e = base + j * 128 + lane * 4;
-              if (FULL || e < n) {
-                const uint32_t nib = (wb[q][j] >> (e & 31)) & 0xFu;
-                xv[j].x = __fadd_rn(xv[j].x, (nib & 1) ? psp : psn);
-                xv[j].y = __fadd_rn(xv[j].y, (nib & 2) ? psp : psn);
-                xv[j].z = __fadd_rn(xv[j].z, (nib & 4) ? psp : psn);
-                xv[j].w = __fadd_rn(xv[j].w, (nib & 8) ? psp : psn);
-              }
-            }
+        for (int j = 0; j < kNJ; ++j) {
+          const uint32_t e = base + j * 128 + lane * 4;
+          if (FULL || e < n) {
+            const uint32_t nib = (wb[j] >> (e & 31)) & 0xFu;
+            xv[j].x = __fadd_rn(xv[j].x, (nib & 1) ? psp : psn);
+            xv[j].y = __fadd_rn(xv[j].y, (nib & 2) ? psp : psn);
+            xv[j].z = __fadd_rn(xv[j].z, (nib & 4) ? psp : psn);
+            xv[j].w = __fadd_rn(xv[j].w, (nib & 8) ? psp : psn);
           }
         }
       }
@@ -124,6 +130,8 @@ struct SignOp {
         for (int j = 0; j < kNJ; ++j) xv[j] = div(xv[j]);
       }
     }
+    double s0 = 0.0, s1 = 0.0;   // this run's sums (EFSignSGD: sum|p|; Onebit: class sums)
+    uint32_t c0 = 0, c1 = 0;
     uint32_t myword = 0;
 #pragma unroll
     for (int j = 0; j < kNJ; ++j) {
@@ -147,13 +155,13 @@ struct SignOp {
           const bool b = v >= 0.f;
           nib |= (uint32_t)b << c;
           if (KIND == K_EFSIGN) {
-            st.s0 += fabs((double)v);
+            s0 += fabs((double)v);
           } else if (b) {
-            st.s1 += (double)v;
-            ++st.c1;
+            s1 += (double)v;
+            ++c1;
           } else {
-            st.s0 += (double)v;
-            ++st.c0;
+            s0 += (double)v;
+            ++c0;
           }
         }
       }
@@ -166,93 +174,74 @@ struct SignOp {
     }
     uint32_t* words = reinterpret_cast<uint32_t*>(S.chunk + 16);
     if (lane < kRun / 32 && base + lane * 32 < n) words[(base >> 5) + lane] = myword;
-  }
-  // per (CTA, segment): the CTA's partial goes to the slot of its first unit of
-  // the segment (other slots stay zero); the CTA completing the segment sums the
-  // slots in unit order (deterministic for a given grid) and writes the scale(s).
-  // the 4 sums of the CTA's consumer warps, in fixed order, on thread 0
-  __device__ static void cta_sum4(double& a, double& b, uint32_t& ca, uint32_t& cb, TmaHdr& h) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // the run's partial (fixed xor tree), slot = run index
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b += __shfl_xor_sync(0xffffffffu, b, o);
-      ca += __shfl_xor_sync(0xffffffffu, ca, o);
-      cb += __shfl_xor_sync(0xffffffffu, cb, o);
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      if (KIND != K_EFSIGN) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+      }
     }
-    csync<1>();   // previous users of h.red / h.scan are done
     if (lane == 0) {
-      h.red[warp] = a;
-      h.red[8 + warp] = b;
-      h.scan[warp] = ca;
-      h.scan[8 + warp] = cb;
-    }
-    csync<1>();
-    if (threadIdx.x == 0) {
-      a = b = 0.0;
-      ca = cb = 0;
-      for (int w = 0; w < kThreads / 32; ++w) {
-        a += h.red[w];
-        b += h.red[8 + w];
-        ca += h.scan[w];
-        cb += h.scan[8 + w];
+      const uint32_t run = base / kRun;
+      S.partial[2 * run] = s0;
+      if (KIND != K_EFSIGN) {
+        S.partial[2 * run + 1] = s1;
+        S.pcount[2 * run] = c0;
+        S.pcount[2 * run + 1] = c1;
       }
     }
   }
-  __device__ void end_segment(const SegH1& S, uint32_t units, uint32_t first_unit, State& st, TmaHdr& h) const {
-    double a = st.s0, b = st.s1;
-    uint32_t ca = st.c0, cb = st.c1;
-    cta_sum4(a, b, ca, cb, h);
-    if (units != S.nunits) {
-      // shared segment: publish this CTA's partial, the CTA completing it sums all
-      if (threadIdx.x == 0) {
-        S.partial[2 * first_unit] = a;
-        S.partial[2 * first_unit + 1] = b;
-        S.pcount[2 * first_unit] = ca;
-        S.pcount[2 * first_unit + 1] = cb;
-        __threadfence();
-        const uint32_t old = atomicAdd(&S.st->done, units);
-        h.flag = (old + units == S.nunits);
-      }
-      csync<1>();
-      if (!h.flag) return;
-      __threadfence();
-      a = b = 0.0;
-      ca = cb = 0;
-      for (uint32_t v = threadIdx.x; v < S.nunits; v += kThreads) {
-        a += __ldcg(S.partial + 2 * v);
-        b += __ldcg(S.partial + 2 * v + 1);
-        ca += __ldcg(S.pcount + 2 * v);
-        cb += __ldcg(S.pcount + 2 * v + 1);
-      }
-      a = block_sum_f64<1>(a, h.red);
-      b = block_sum_f64<1>(b, h.red);
-      ca = block_sum_u32<1>(ca, h.scan);
-      cb = block_sum_u32<1>(cb, h.scan);
-    }
-    // (a segment owned by one CTA is finalised directly: its sum equals the
-    // slot-wise sum, which would only add exact zeros)
-    if (threadIdx.x == 0) {
-      float* hdr = reinterpret_cast<float*>(S.chunk);
-      const uint32_t n = S.n;
-      float x0, x1;
-      if (KIND == K_EFSIGN) {
-        x0 = n ? (float)(a / (double)n) : 0.f;   // scale = ||p||_1 / N (R7)
-        x1 = 0.f;
-      } else {
-        x0 = ca ? (float)(a / (double)ca) : 0.f;  // mean of {p < 0} (R8)
-        x1 = cb ? (float)(b / (double)cb) : 0.f;  // mean of {p >= 0}
-      }
-      hdr[0] = x0;
-      if (KIND == K_ONEBIT) hdr[1] = x1;
-      if (S.ef) {
-        S.lazy_out[0] = x0;
-        S.lazy_out[1] = x1;
-      }
-    }
-    csync<1>();
-  }
+  template <int BAR>
+  __device__ void end_segment(const SegH1&, uint32_t, uint32_t, State&, TmaGroup&) const {}
 };
+
+// One CTA per segment: the scale(s) from the per-run partials, reduced in run
+// order (each thread a strided slice, then the fixed block tree): the result
+// does not depend on the grid of the streaming pass.
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __restrict__ segs) {
+  __shared__ double shd[8];
+  __shared__ uint32_t shu[16];
+  const SegH1 S = segs[blockIdx.x];
+  const uint32_t nruns = (S.n + kRun - 1) / kRun;
+  double a = 0.0, b = 0.0;
+  uint32_t ca = 0, cb = 0;
+  for (uint32_t v = threadIdx.x; v < nruns; v += kThreads) {
+    a += __ldcg(S.partial + 2 * v);
+    if (KIND != K_EFSIGN) {
+      b += __ldcg(S.partial + 2 * v + 1);
+      ca += __ldcg(S.pcount + 2 * v);
+      cb += __ldcg(S.pcount + 2 * v + 1);
+    }
+  }
+  a = block_sum_f64(a, shd);
+  if (KIND != K_EFSIGN) {
+    b = block_sum_f64(b, shd);
+    ca = block_sum_u32(ca, shu);
+    cb = block_sum_u32(cb, shu);
+  }
+  if (threadIdx.x == 0) {
+    float* hdr = reinterpret_cast<float*>(S.chunk);
+    const uint32_t n = S.n;
+    float x0, x1;
+    if (KIND == K_EFSIGN) {
+      x0 = n ? (float)(a / (double)n) : 0.f;   // scale = ||p||_1 / N (R7)
+      x1 = 0.f;
+    } else {
+      x0 = ca ? (float)(a / (double)ca) : 0.f;  // mean of {p < 0} (R8)
+      x1 = cb ? (float)(b / (double)cb) : 0.f;  // mean of {p >= 0}
+    }
+    hdr[0] = x0;
+    if (KIND == K_ONEBIT) hdr[1] = x1;
+    if (S.ef) {
+      S.lazy_out[0] = x0;
+      S.lazy_out[1] = x1;
+    }
+  }
+}
 
 template <int KIND>
 __global__ void sign_materialize_kernel(const float* __restrict__ p, const float* __restrict__ lazy,
@@ -266,32 +255,23 @@ __global__ void sign_materialize_kernel(const float* __restrict__ p, const float
   }
 }
 
-int tma_stream_grid(int nunits);
-int tma_stream_stages();
-
-template <class Op>
-static void launch_tma_op(const SegH1* segs, const uint32_t* unit_seg, int nunits, Op op, cudaStream_t st) {
-  static bool init = [] {
-    return cudaFuncSetAttribute(tma_stream_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(kTmaHdrBytes + kTmaMaxStages * kTmaStageBytes)) == cudaSuccess;
-  }();
-  (void)init;
-  const int ns = tma_stream_stages();
-  tma_stream_kernel<<<tma_stream_grid(nunits), kThreads + 32, kTmaHdrBytes + ns * kTmaStageBytes, st>>>(
-      segs, unit_seg, (uint32_t)nunits, ns, op);
-  count_launches(1);
-}
-
-void launch_sign_h1_tma(int kind, const SegH1* segs, const uint32_t* unit_seg, int nunits,
+void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                         const unsigned char* const* pieces, cudaStream_t st) {
   if (nunits == 0) return;
+  static const bool stage = [] {   // ESP_A7_STAGE=0: load the pieces' words by LDG
+    const char* e = getenv("ESP_A7_STAGE");
+    return !e || atoi(e) != 0;
+  }();
   if (kind == K_EFSIGN) {
-    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, true>{pieces}, st);
+    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, true>{pieces, stage}, st);
     else launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, false>{}, st);
   } else {
-    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, true>{pieces}, st);
+    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, true>{pieces, stage}, st);
     else launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, false>{}, st);
   }
+  if (kind == K_EFSIGN) sign_finalize_kernel<K_EFSIGN><<<nsegs, kThreads, 0, st>>>(segs);
+  else sign_finalize_kernel<K_ONEBIT><<<nsegs, kThreads, 0, st>>>(segs);
+  count_launches(1);
 }
 
 void launch_sign_materialize(int kind, const float* p, const float* lazy, float* out, uint32_t n,

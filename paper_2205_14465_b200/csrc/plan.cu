@@ -236,11 +236,9 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           hist_cursor += hbytes + round_up((size_t)s.ngroups * 8, 256);
         }
         if (quant) {
-          // per-(CTA, segment) partial slots: zeroed every call (SignOp::end_segment)
-          s.partial = L.commit ? reinterpret_cast<double*>(p.zero + hist_cursor) : nullptr;
-          s.pcount = L.commit ? reinterpret_cast<uint32_t*>(p.zero + hist_cursor + round_up((size_t)nunits * 16, 256))
-                              : nullptr;
-          hist_cursor += round_up((size_t)nunits * 16, 256) + round_up((size_t)nunits * 8, 256);
+          // per-run partial sums, every slot rewritten each call (SignOp::run)
+          s.partial = L.ptr<double>(L.reserve((size_t)nruns * 16));
+          s.pcount = L.ptr<uint32_t>(L.reserve((size_t)nruns * 8));
         }
         if (none) s.chunk = b.send.base ? b.send.at(lr) + b.coff[ti] : nullptr;
         T.h1.push_back(s);
@@ -311,11 +309,9 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           T.a7_pieces.push_back(b.recv1.base ? b.recv1.at(lr) + (size_t)r * S + b.coff[ti] : nullptr);
         s.st = L.ptr<SelState>(zero_off_st + st_cursor * sizeof(SelState));
         ++st_cursor;
-        // per-(CTA, segment) partial slots, zeroed every call (SignOp::end_segment)
-        s.partial = L.commit ? reinterpret_cast<double*>(p.zero + hist_cursor) : nullptr;
-        s.pcount = L.commit ? reinterpret_cast<uint32_t*>(p.zero + hist_cursor + round_up((size_t)s.nunits * 16, 256))
-                            : nullptr;
-        hist_cursor += round_up((size_t)s.nunits * 16, 256) + round_up((size_t)s.nunits * 8, 256);
+        // per-run partial sums, every slot rewritten each call (SignOp::run)
+        s.partial = L.ptr<double>(L.reserve((size_t)div_up(s.n, kRun) * 16));
+        s.pcount = L.ptr<uint32_t>(L.reserve((size_t)div_up(s.n, kRun) * 8));
         T.a7.push_back(s);
         fill_unit_table(T.a7_units, (uint32_t)(T.a7.size() - 1 - a7_first), s.nunits);
       }
@@ -447,17 +443,10 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
           nhist += (round_up((size_t)dgc_hist_words(dgc_hrep(c->pk[part], ng)) * 4, 256) +
                     round_up((size_t)ng * 8, 256)) * p.w->nlocal;
         }
-        // sign: per-tile partial sums (16 B) and counts (8 B)
-        if (is_quant(b.kind)) {
-          const size_t nu = div_up(len, kDgcTile);
-          nhist += (round_up(nu * 16, 256) + round_up(nu * 8, 256)) * p.w->nlocal;
-        }
       }
       nst += (size_t)segs * p.w->nlocal;
       if (is_quant(b.kind)) {
         nst += (size_t)p.w->nlocal;   // a7 (upper bound)
-        const size_t nu = div_up(c->N, kDgcTile);   // a7 partial slots (upper bound: whole tensor)
-        nhist += (round_up(nu * 16, 256) + round_up(nu * 8, 256)) * p.w->nlocal;
       }
     }
   }
@@ -695,8 +684,8 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
       }
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
-    case ESP_EFSIGNSGD: launch_sign_h1_tma(K_EFSIGN, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
-    case ESP_ONEBIT: launch_sign_h1_tma(K_ONEBIT, b.h1, b.h1_units, b.nh1_units, nullptr, st); break;
+    case ESP_EFSIGNSGD: launch_sign_h1_tma(K_EFSIGN, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st); break;
+    case ESP_ONEBIT: launch_sign_h1_tma(K_ONEBIT, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st); break;
     default: launch_pack(b.h1, b.h1_units, b.nh1_units, st); break;
   }
   if (e1 && !dgc) ESP_CUDA(cudaEventRecord(e1, st));
@@ -706,7 +695,7 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
 
 static void run_mid(Plan& p, Bucket& b, cudaStream_t cs) {
   const int k = b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT;
-  launch_sign_h1_tma(k, b.a7, b.a7_units, b.na7_units, b.a7_pieces, cs);
+  launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, b.a7_pieces, cs);
   ESP_CUDA(cudaGetLastError());
 }
 
