@@ -22,13 +22,22 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
 // block the stream until *cnt >= target (arrivals of a fused Allgather); traps
 // after ~10 s so that a missing peer becomes an error, not a hang
 void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, cudaStream_t st);
+// fused collectives: copy each job's bytes into peer memory, then one
+// system-scope release + arrival per job on the destination's counter (k_push.cu)
+void launch_push(const PushJob* jobs, int njobs, const unsigned char* src, unsigned char* const* dsts,
+                 unsigned long long* const* cnts, cudaStream_t st);
 // Randomk h1 (k_randomk.cu)
 void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 // h1 on the persistent TMA streaming driver, tiles of kDgcTile (k_sign.cu)
 // pieces != nullptr: a7 (input = decode-mean of the segment's pieces, r = r2)
 // (+ one finalize kernel over the nsegs segments: the scales from the per-run partials)
+// dsts != nullptr (fused collective): the chunk of a segment is stored at
+// dsts[S.part] + chunk_off (dmode 1, the partition owner / root) or at every
+// dsts[d] + chunk_off, d < ndst (dmode 2); the finalize kernel then bumps the
+// matching cnts[] once per segment (system-scope release)
 void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
-                        const unsigned char* const* pieces, cudaStream_t st);
+                        const unsigned char* const* pieces, cudaStream_t st, unsigned char* const* dsts = nullptr,
+                        unsigned long long* const* cnts = nullptr, int dmode = 0, int ndst = 0);
 // NONE: pack gradients into a contiguous buffer (k_h2.cu)
 void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 

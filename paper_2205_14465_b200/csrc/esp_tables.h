@@ -98,6 +98,16 @@ __host__ __device__ inline uint32_t dgc_hrep(uint32_t k, uint32_t ngroups) {
 }
 __host__ __device__ inline uint32_t dgc_hist_words(uint32_t hrep) { return 4096 + 2048 * hrep; }
 
+// One job of the push kernel (fused collectives): bytes (a multiple of 16,
+// <= kPushChunk) from src + src_off to dsts[d] + dst_off; one arrival on cnts[d].
+constexpr int kPushChunk = 32768;
+struct PushJob {
+  uint64_t src_off;
+  uint64_t dst_off;
+  uint32_t bytes;
+  uint32_t d;
+};
+
 // One h2 segment: out[0..n) = reduce(sum_r decode(piece r)).
 struct SegH2 {
   const uint64_t* optr;  // &dyn[slot]: output tensor (the gradient, in place)

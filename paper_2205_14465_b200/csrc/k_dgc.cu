@@ -960,6 +960,7 @@ __global__ void wait_arrivals_kernel(const unsigned long long* cnt, unsigned lon
 }
 
 void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, cudaStream_t st) {
+  if (target == 0) return;   // nothing to wait for (e.g. the root's own broadcast)
   wait_arrivals_kernel<<<1, 32, 0, st>>>(cnt, target);
   count_launches(1);
 }

@@ -42,6 +42,7 @@ struct RandomkOp {
   };
   const unsigned char* const* pieces = nullptr;   // not a decoding op
   bool stage_words = false;
+  __device__ bool sys_fence() const { return false; }
   template <int BAR>
   __device__ void begin_segment(const SegH1& S, State& st, TmaGroup&) const {
     st.h = randomk_hash(S.hash, *S.step, S.part, S.rankterm);

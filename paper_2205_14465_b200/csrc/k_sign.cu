@@ -51,6 +51,13 @@ struct SignOp {
   // DECODE: stage the pieces' sign words in the tile's g slot by TMA (the stage
   // is then held until they are used) instead of loading them with LDG
   bool stage_words = false;
+  // fused collective (NVLink peer stores): dmode 0 = the local chunk S.chunk,
+  // 1 = dsts[S.part] + S.chunk_off (the partition owner), 2 = dsts[d] +
+  // S.chunk_off for every d < ndst
+  unsigned char* const* dsts = nullptr;
+  int dmode = 0, ndst = 0;
+  bool fence = false;
+  __device__ bool sys_fence() const { return fence; }
   struct State {
     float sp, sn;                            // lazy EF: last step's scale pair
     float qsp0, qsn0, qsp1, qsn1;            // DECODE: scales of pieces lane, lane + 32
@@ -172,8 +179,16 @@ struct SignOp {
       const uint32_t wv = __shfl_sync(0xffffffffu, word, (lane & 3) * 8);
       if ((lane >> 2) == j) myword = wv;
     }
-    uint32_t* words = reinterpret_cast<uint32_t*>(S.chunk + 16);
-    if (lane < kRun / 32 && base + lane * 32 < n) words[(base >> 5) + lane] = myword;
+    if (lane < kRun / 32 && base + lane * 32 < n) {
+      const uint32_t wi = (base >> 5) + lane;
+      if (dmode == 0) {
+        reinterpret_cast<uint32_t*>(S.chunk + 16)[wi] = myword;
+      } else if (dmode == 1) {
+        reinterpret_cast<uint32_t*>(dsts[S.part] + S.chunk_off + 16)[wi] = myword;
+      } else {
+        for (int d = 0; d < ndst; ++d) reinterpret_cast<uint32_t*>(dsts[d] + S.chunk_off + 16)[wi] = myword;
+      }
+    }
     // the run's partial (fixed xor tree), slot = run index
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -201,8 +216,15 @@ struct SignOp {
 // One CTA per segment: the scale(s) from the per-run partials, reduced in run
 // order (each thread a strided slice, then the fixed block tree): the result
 // does not depend on the grid of the streaming pass.
+// Fused collective (dmode != 0): the header goes to the destination chunk(s),
+// then one system-scope fence and one arrival per destination (the words were
+// stored, and fenced per thread, by the streaming pass that precedes this
+// kernel in stream order).
 template <int KIND>
-__global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __restrict__ segs) {
+__global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __restrict__ segs,
+                                                                 unsigned char* const* __restrict__ dsts,
+                                                                 unsigned long long* const* __restrict__ cnts,
+                                                                 int dmode, int ndst) {
   __shared__ double shd[8];
   __shared__ uint32_t shu[16];
   const SegH1 S = segs[blockIdx.x];
@@ -234,8 +256,18 @@ __global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __
       x0 = ca ? (float)(a / (double)ca) : 0.f;  // mean of {p < 0} (R8)
       x1 = cb ? (float)(b / (double)cb) : 0.f;  // mean of {p >= 0}
     }
-    hdr[0] = x0;
-    if (KIND == K_ONEBIT) hdr[1] = x1;
+    auto put = [&](float* h) {
+      h[0] = x0;
+      if (KIND == K_ONEBIT) h[1] = x1;
+    };
+    if (dmode == 0) {
+      put(hdr);
+    } else {
+      const int d0 = dmode == 1 ? (int)S.part : 0, d1 = dmode == 1 ? (int)S.part + 1 : ndst;
+      for (int d = d0; d < d1; ++d) put(reinterpret_cast<float*>(dsts[d] + S.chunk_off));
+      __threadfence_system();
+      for (int d = d0; d < d1; ++d) atomicAdd_system(cnts[d], 1ull);
+    }
     if (S.ef) {
       S.lazy_out[0] = x0;
       S.lazy_out[1] = x1;
@@ -256,21 +288,27 @@ __global__ void sign_materialize_kernel(const float* __restrict__ p, const float
 }
 
 void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
-                        const unsigned char* const* pieces, cudaStream_t st) {
+                        const unsigned char* const* pieces, cudaStream_t st, unsigned char* const* dsts,
+                        unsigned long long* const* cnts, int dmode, int ndst) {
   if (nunits == 0) return;
   static const bool stage = [] {   // ESP_A7_STAGE=0: load the pieces' words by LDG
     const char* e = getenv("ESP_A7_STAGE");
     return !e || atoi(e) != 0;
   }();
+  if (!dsts) dmode = 0;
+  static const bool fence = [] {
+    const char* e = getenv("ESP_SYS_FENCE");
+    return e && atoi(e) != 0;
+  }();
   if (kind == K_EFSIGN) {
-    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, true>{pieces, stage}, st);
-    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, false>{}, st);
+    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, true>{pieces, stage, dsts, dmode, ndst, fence && dmode}, st);
+    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, false>{nullptr, false, dsts, dmode, ndst, fence && dmode}, st);
   } else {
-    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, true>{pieces, stage}, st);
-    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, false>{}, st);
+    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, true>{pieces, stage, dsts, dmode, ndst, fence && dmode}, st);
+    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, false>{nullptr, false, dsts, dmode, ndst, fence && dmode}, st);
   }
-  if (kind == K_EFSIGN) sign_finalize_kernel<K_EFSIGN><<<nsegs, kThreads, 0, st>>>(segs);
-  else sign_finalize_kernel<K_ONEBIT><<<nsegs, kThreads, 0, st>>>(segs);
+  if (kind == K_EFSIGN) sign_finalize_kernel<K_EFSIGN><<<nsegs, kThreads, 0, st>>>(segs, dsts, cnts, dmode, ndst);
+  else sign_finalize_kernel<K_ONEBIT><<<nsegs, kThreads, 0, st>>>(segs, dsts, cnts, dmode, ndst);
   count_launches(1);
 }
 

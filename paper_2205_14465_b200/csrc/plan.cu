@@ -37,15 +37,34 @@ struct Bucket {
   cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
-  // ---- fused Allgather over NVLink peer memory: the DGC
-  // write kernel stores every selected entry straight into all ranks' recv
-  // buffers (double-buffered by call parity) and bumps their arrival counters;
-  // h2 starts after a wait kernel has seen n x ngroups arrivals for this call.
+  // ---- compression fused with the collective over NVLink peer memory
+  // (DESIGN.md 9): the producing kernel (DGC write, sign
+  // h1 / a7) stores its payload straight into the receiving ranks' buffers
+  // (double-buffered by call parity) and bumps their arrival counters; the
+  // consumer starts after a wait kernel has seen this call's arrivals.
+  //   phase 1 = h1 -> recv1 (Allgather, Alltoall, Gather) or recv2 (sparse
+  //             Alltoall/Allgather: chunk (part, src) goes straight to its
+  //             final place on every rank, the forwarding hop disappears)
+  //   phase 2 = a7 -> recv2 (quantized Alltoall/Allgather) or mid (quantized
+  //             Gather/Broadcast, from the root)
   bool fused = false;
-  size_t recv1_off = 0, cnt_off = 0;            // arena offsets (identical on every rank)
-  const unsigned char** h2_pieces_odd = nullptr;   // h2 pieces of the parity-1 buffer
-  unsigned char** dsts = nullptr;               // device [2][n]: my slot in every rank's buffer
-  unsigned long long** cnts = nullptr;          // device [n]: every rank's arrival counter
+  int h1_dmode = 0;                             // sign h1: 1 = to the partition owner, 2 = to all
+  size_t dst1_off = 0, dst1_par = 0, dst1_slot = 0;   // phase-1 destination: off + par * par_stride + src * slot
+  size_t dst2_off = 0, dst2_par = 0, dst2_slot = 0;   // phase-2 destination
+  size_t cnt_off = 0;                           // [0] phase-1, [1] phase-2 arrival counters
+  uint64_t target1 = 0, target2 = 0;            // arrivals per call
+  // push mode (default): producers write locally, then push_kernel copies the
+  // slots into the peers' buffers (phase-1 source = send, phase-2 = stage)
+  bool push = false;
+  LocalBufs stage{};
+  PushJob* push1 = nullptr; int npush1 = 0;
+  PushJob* push2 = nullptr; int npush2 = 0;
+  const unsigned char** h2_pieces_odd = nullptr;   // h2 pieces of the parity-1 buffers
+  const unsigned char** a7_pieces_odd = nullptr;
+  unsigned char** dsts = nullptr;               // device [2][n]: my phase-1 slot in every rank's buffer
+  unsigned char** dsts2 = nullptr;              // device [2][n]: my phase-2 slot
+  unsigned long long** cnts = nullptr;          // device [n]: every rank's phase-1 counter
+  unsigned long long** cnts2 = nullptr;         // device [n]: every rank's phase-2 counter
   unsigned long long* my_cnt = nullptr;
   uint64_t epoch = 0;
 };
@@ -76,7 +95,9 @@ struct Plan {
       if (b.ev_h1) cudaEventDestroy(b.ev_h1);
       if (b.ev_comm) cudaEventDestroy(b.ev_comm);
       if (b.dsts) cudaFree(b.dsts);
+      if (b.dsts2) cudaFree(b.dsts2);
       if (b.cnts) cudaFree(b.cnts);
+      if (b.cnts2) cudaFree(b.cnts2);
     }
     for (auto& e : dyn_ev)
       if (e) cudaEventDestroy(e);
@@ -101,9 +122,10 @@ struct HostTables {
   std::vector<SegH1> h1, a7;
   std::vector<uint32_t> h1_units, h1_groups, a7_units, h2_units;
   std::vector<SegH2> h2;
-  std::vector<const unsigned char*> a7_pieces, h2_pieces, h2_pieces_odd;
+  std::vector<const unsigned char*> a7_pieces, a7_pieces_odd, h2_pieces, h2_pieces_odd;
   std::vector<uint32_t> rankterms;
   std::vector<uint4> off_jobs;
+  std::vector<PushJob> push1, push2;
 };
 
 static bool fused_allgather_enabled() {
@@ -112,6 +134,21 @@ static bool fused_allgather_enabled() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+// ESP_PUSH=0: the producing kernels store into peer memory themselves instead of
+// a push kernel after them (A/B knob)
+static bool push_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ESP_PUSH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// push jobs: [src_off, src_off + bytes) -> destination d at dst_off, in kPushChunk pieces
+static void add_push(std::vector<PushJob>& v, size_t src_off, size_t dst_off, size_t bytes, int d) {
+  for (size_t c = 0; c < bytes; c += kPushChunk)
+    v.push_back(PushJob{src_off + c, dst_off + c, (uint32_t)std::min<size_t>(kPushChunk, bytes - c), (uint32_t)d});
 }
 
 static void fill_unit_table(std::vector<uint32_t>& units, uint32_t seg, uint32_t count) {
@@ -158,16 +195,95 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     lb = LocalBufs{L.ptr<unsigned char>(off), stride};
     return off;
   };
+  b.fused = fused_allgather_enabled() && !w->sim && n > 1 &&
+            ((dgc && (b.routine == ESP_ALLGATHER || b.routine == ESP_ALLTOALL_ALLGATHER)) ||
+             (quant && (b.routine == ESP_ALLGATHER || b.routine == ESP_ALLTOALL_ALLGATHER ||
+                        b.routine == ESP_GATHER_BROADCAST)));
+  // (the fused producers write peers directly; the send buffer still serves esp_compress)
   bufs(b.send, b.P * S);
-  b.fused = fused_allgather_enabled() && !w->sim && n > 1 && dgc && b.routine == ESP_ALLGATHER;
+  // one real rank: every collective is the identity, so the receive buffers
+  // alias the send/mid buffers and the collectives move nothing
+  const bool solo = !w->sim && n == 1;
+  if (solo) {
+    b.recv1 = b.send;
+    if (quant && (b.routine == ESP_ALLTOALL_ALLGATHER || b.routine == ESP_GATHER_BROADCAST)) {
+      bufs(b.mid, S);
+      b.recv2 = b.mid;
+    } else {
+      b.recv2 = b.send;
+    }
+  } else if (b.fused) {
+    // two call-parity copies of every receive buffer; identical arena layouts on
+    // every rank, so a peer's buffer is its arena base + the same offset
+    b.cnt_off = L.reserve(256);
+    if (b.routine == ESP_ALLGATHER) {
+      b.dst1_off = bufs(b.recv1, 2 * n * S);
+      b.dst1_par = (size_t)n * S;
+      b.dst1_slot = S;
+      b.h1_dmode = 2;
+    } else if (b.routine == ESP_ALLTOALL_ALLGATHER && sparse) {
+      b.dst1_off = bufs(b.recv2, 2 * (size_t)n * n * S);
+      b.dst1_par = (size_t)n * n * S;
+      b.dst1_slot = S;
+    } else if (b.routine == ESP_ALLTOALL_ALLGATHER) {   // quantized, process 2
+      b.dst1_off = bufs(b.recv1, 2 * n * S);
+      b.dst1_par = (size_t)n * S;
+      b.dst1_slot = S;
+      b.h1_dmode = 1;
+      b.dst2_off = bufs(b.recv2, 2 * n * S);
+      b.dst2_par = (size_t)n * S;
+      b.dst2_slot = S;
+    } else {                                            // quantized Gather/Broadcast
+      b.dst1_off = bufs(b.recv1, 2 * n * S);
+      b.dst1_par = (size_t)n * S;
+      b.dst1_slot = S;
+      b.h1_dmode = 1;                                   // part 0 = the root
+      b.dst2_off = bufs(b.mid, 2 * S);
+      b.dst2_par = S;
+      b.dst2_slot = 0;
+    }
+    b.push = push_enabled();
+    if (b.push) {
+      // jobs and arrivals per call (J jobs per slot)
+      const uint64_t J = div_up(S, kPushChunk);
+      const bool root = w->rank == 0;
+      if (quant) bufs(b.stage, S);   // a7's local output
+      // (no self copies: a rank reads its own chunks from the local source)
+      const int me = w->rank;
+      switch (b.routine) {
+        case ESP_ALLGATHER:
+          for (int d = 0; d < n; ++d)
+            if (d != me) add_push(T.push1, 0, 0, S, d);
+          b.target1 = (n - 1) * J;
+          break;
+        case ESP_ALLTOALL_ALLGATHER:
+          if (sparse) {
+            for (int d = 0; d < n; ++d)
+              for (int part = 0; part < b.P && d != me; ++part)
+                add_push(T.push1, (size_t)part * S, (size_t)part * n * S, S, d);
+            b.target1 = (uint64_t)(n - 1) * b.P * J;
+          } else {
+            for (int d = 0; d < n; ++d)
+              if (d != me) add_push(T.push1, (size_t)d * S, 0, S, d);
+            for (int d = 0; d < n; ++d)
+              if (d != me) add_push(T.push2, 0, 0, S, d);
+            b.target1 = (n - 1) * J;
+            b.target2 = (n - 1) * J;
+          }
+          break;
+        default:   // quantized Gather/Broadcast: to the root, then the root's a7 to all
+          if (!root) add_push(T.push1, 0, 0, S, 0);
+          if (root)
+            for (int d = 1; d < n; ++d) add_push(T.push2, 0, 0, S, d);
+          b.target1 = (n - 1) * J;
+          b.target2 = root ? 0 : J;
+          break;
+      }
+    }
+  } else
   switch (b.routine) {
     case ESP_ALLGATHER:
-      if (b.fused) {
-        b.recv1_off = bufs(b.recv1, 2 * n * S);   // two call-parity copies of the n slots
-        b.cnt_off = L.reserve(256);
-      } else {
-        bufs(b.recv1, n * S);
-      }
+      bufs(b.recv1, n * S);
       break;
     case ESP_ALLTOALL_ALLGATHER:
       bufs(b.recv1, n * S);
@@ -201,7 +317,12 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.step = p.dyn_dev + nslots + slot_idx;
         s.r = c->r ? c->r + (size_t)lr * c->N + lo : nullptr;
         s.chunk = b.send.base ? b.send.at(lr) + (size_t)part * S + b.coff[ti] : nullptr;
-        s.chunk_off = (uint32_t)((size_t)part * S + b.coff[ti]);
+        // fused destinations: dsts[q] + chunk_off (DGC: every rank q; sign: the
+        // partition owner q = part, or every q).  Sparse Alltoall/Allgather lands
+        // in recv2's [part][src] layout
+        const size_t part_off = !dgc ? 0 : (b.fused && b.routine == ESP_ALLTOALL_ALLGATHER) ? (size_t)part * n * S
+                                                                                            : (size_t)part * S;
+        s.chunk_off = (uint32_t)(part_off + b.coff[ti]);
         s.lazy_in = c->lazy ? c->lazy + ((size_t)lr * c->P + part) * 2 : nullptr;
         s.lazy_out = const_cast<float*>(s.lazy_in);
         s.n = len;
@@ -294,7 +415,9 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.r = c->r2 ? c->r2 + (size_t)lr * c->r2_len : nullptr;
         s.lazy_in = c->lazy2 ? c->lazy2 + (size_t)lr * 2 : nullptr;
         s.lazy_out = const_cast<float*>(s.lazy_in);
-        s.chunk = b.mid.base ? b.mid.at(lr) + b.coff[ti] : nullptr;
+        s.chunk = b.fused ? (b.stage.base ? b.stage.at(lr) + b.coff[ti] : nullptr)
+                          : (b.mid.base ? b.mid.at(lr) + b.coff[ti] : nullptr);
+        s.chunk_off = (uint32_t)b.coff[ti];
         s.n = len;
         s.kpad = c->kpad;
         s.nunits = div_up(len, kDgcTile);
@@ -305,8 +428,19 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.npieces = (uint32_t)n;
         s.piece0 = (uint32_t)T.a7_pieces.size();
         s.divisor = divisor;
-        for (int r = 0; r < n; ++r)
+        for (int r = 0; r < n; ++r) {
+          if (b.push && r == w->rank) {
+            // push mode: my own chunk is read where h1 wrote it (rewritten only by
+            // the next call's h1, after this call's consumers in stream order)
+            unsigned char* mine = b.send.at(lr) + (size_t)(b.routine == ESP_ALLTOALL_ALLGATHER ? r : 0) * S + b.coff[ti];
+            T.a7_pieces.push_back(mine);
+            T.a7_pieces_odd.push_back(mine);
+            continue;
+          }
           T.a7_pieces.push_back(b.recv1.base ? b.recv1.at(lr) + (size_t)r * S + b.coff[ti] : nullptr);
+          T.a7_pieces_odd.push_back(b.recv1.base && b.fused ? b.recv1.at(lr) + b.dst1_par + (size_t)r * S + b.coff[ti]
+                                                            : nullptr);
+        }
         s.st = L.ptr<SelState>(zero_off_st + st_cursor * sizeof(SelState));
         ++st_cursor;
         // per-run partial sums, every slot rewritten each call (SignOp::run)
@@ -344,12 +478,23 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.k = none ? 0 : k_of(len, c->cfg.ratio);
         s.kpad = c->kpad;
         s.piece0 = (uint32_t)T.h2_pieces.size();
+        // fused: the parity-1 copy of the buffer h2 reads follows the parity-0 copy
+        const size_t par_stride = b.routine == ESP_ALLGATHER ? b.dst1_par
+                                  : (b.routine == ESP_ALLTOALL_ALLGATHER && sparse) ? b.dst1_par
+                                                                                     : b.dst2_par;
         auto add_piece = [&](unsigned char* base, size_t off, uint32_t rankterm) {
           T.h2_pieces.push_back(base ? base + off : nullptr);
-          // fused Allgather: the parity-1 copy of the n slots follows the parity-0 copy
-          T.h2_pieces_odd.push_back(base && b.fused ? base + off + (size_t)n * S : nullptr);
+          T.h2_pieces_odd.push_back(base && b.fused ? base + off + par_stride : nullptr);
           T.rankterms.push_back(rankterm);
         };
+        // push mode: a piece this rank produced itself is read from its local
+        // source (no self copy); same pointer for both parities
+        auto local_piece = [&](unsigned char* ptr) {
+          T.h2_pieces.push_back(ptr);
+          T.h2_pieces_odd.push_back(ptr);
+          T.rankterms.push_back(0);
+        };
+        const int me = w->rank;
         const uint32_t rt_shared = 0;
         auto rt_of = [&](int r) -> uint32_t {
           return (b.kind == ESP_RANDOMK && !c->cfg.randomk_shared_indices) ? (uint32_t)r + 1 : rt_shared;
@@ -358,12 +503,15 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           case ESP_ALLGATHER:
           case ESP_GATHER_BROADCAST:
             if (b.routine == ESP_GATHER_BROADCAST && quant) {
-              add_piece(b.mid.base ? b.mid.at(lr) : nullptr, b.coff[ti], 0);
+              if (b.push && me == 0) local_piece(b.stage.at(lr) + b.coff[ti]);
+              else add_piece(b.mid.base ? b.mid.at(lr) : nullptr, b.coff[ti], 0);
               s.npieces = 1;
               s.divisor = 1.0f;
             } else {
-              for (int r = 0; r < n; ++r)
-                add_piece(b.recv1.base ? b.recv1.at(lr) : nullptr, (size_t)r * S + b.coff[ti], rt_of(r));
+              for (int r = 0; r < n; ++r) {
+                if (b.push && r == me) local_piece(b.send.at(lr) + b.coff[ti]);
+                else add_piece(b.recv1.base ? b.recv1.at(lr) : nullptr, (size_t)r * S + b.coff[ti], rt_of(r));
+              }
               s.npieces = (uint32_t)n;
               s.divisor = divisor;
             }
@@ -371,12 +519,14 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           case ESP_ALLTOALL_ALLGATHER:
             if (sparse) {
               for (int r = 0; r < n; ++r)
-                add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr,
+                if (b.push && r == me) local_piece(b.send.at(lr) + (size_t)part * S + b.coff[ti]);
+                else add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr,
                           (size_t)part * n * S + (size_t)r * S + b.coff[ti], rt_of(r));
               s.npieces = (uint32_t)n;
               s.divisor = divisor;
             } else {
-              add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr, (size_t)part * S + b.coff[ti], 0);
+              if (b.push && part == me) local_piece(b.stage.at(lr) + b.coff[ti]);
+              else add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr, (size_t)part * S + b.coff[ti], 0);
               s.npieces = 1;
               s.divisor = 1.0f;
             }
@@ -411,6 +561,18 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
   b.nh2_units = (int)u0;
 
   // per critical rank op counts of the cost table
+  // fused: arrivals per call (each DGC write group / sign finalize CTA signals
+  // each of its destinations once; every rank has the same segment list)
+  if (b.fused && !b.push) {
+    if (dgc) {
+      b.target1 = (uint64_t)n * b.nh1_groups;
+    } else {
+      uint64_t mine = 0;
+      for (int i = 0; i < b.nh1; ++i) mine += T.h1[h1_first + i].part == (uint32_t)w->rank;
+      b.target1 = (uint64_t)n * (b.h1_dmode == 2 || b.routine == ESP_GATHER_BROADCAST ? (uint64_t)b.nh1 : mine);
+      b.target2 = (uint64_t)b.nh1;   // sum over owners q of their a7 segments
+    }
+  }
   b.h1_calls = none ? 0 : (quant && (b.routine == ESP_ALLTOALL_ALLGATHER || b.routine == ESP_GATHER_BROADCAST) ? 2 : 1);
   switch (b.routine) {
     case ESP_ALLGATHER: b.h2_pieces_count = n; break;
@@ -475,12 +637,17 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     up(TB.a7, b.a7);
     up(TB.a7_units, b.a7_units);
     up(TB.a7_pieces, b.a7_pieces);
+    if (b.fused) up(TB.a7_pieces_odd, b.a7_pieces_odd);
     up(TB.h2, b.h2);
     up(TB.h2_units, b.h2_units);
     up(TB.h2_pieces, b.h2_pieces);
     if (b.fused) up(TB.h2_pieces_odd, b.h2_pieces_odd);
     up(TB.rankterms, b.h2_rankterms);
     up(TB.off_jobs, b.h2_off_jobs);
+    up(TB.push1, b.push1);
+    up(TB.push2, b.push2);
+    b.npush1 = (int)TB.push1.size();
+    b.npush2 = (int)TB.push2.size();
     b.nh2_off_jobs = (int)TB.off_jobs.size();
     if (commit) {
       // pad patterns of every chunk that kernels never touch (R: payload layout)
@@ -498,16 +665,26 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
           if (b.mid.base) ESP_CUDA(cudaMemset(b.mid.at(lr), 0, b.slot));
         }
         if (b.fused) {
-          // every slot of both parity copies carries the pad pattern; writers
-          // (every rank's DGC write kernel) only ever store entries [0, k)
           const int n = p.w->nranks;
-          for (int copy = 0; copy < 2 * n; ++copy)
-            for (size_t ti = 0; ti < b.tens.size(); ++ti) {
-              esp_ctx_s* c = p.ctxs[b.tens[ti]];
-              unsigned char* ch = b.recv1.at(lr) + (size_t)copy * b.slot + b.coff[ti];
-              ESP_CUDA(cudaMemset(ch, 0xFF, 4ull * c->kpad));
-              ESP_CUDA(cudaMemset(ch + 4ull * c->kpad, 0, 4ull * c->kpad));
-            }
+          if (b.kind == ESP_DGC || b.kind == ESP_TOPK) {
+            // every slot of both parity copies carries the pad pattern; writers
+            // (every rank's DGC write kernel) only ever store entries [0, k)
+            const bool a2a = b.routine == ESP_ALLTOALL_ALLGATHER;
+            unsigned char* buf = a2a ? b.recv2.at(lr) : b.recv1.at(lr);
+            const int copies = 2 * n * (a2a ? n : 1);
+            for (int copy = 0; copy < copies; ++copy)
+              for (size_t ti = 0; ti < b.tens.size(); ++ti) {
+                esp_ctx_s* c = p.ctxs[b.tens[ti]];
+                unsigned char* ch = buf + (size_t)copy * b.slot + b.coff[ti];
+                ESP_CUDA(cudaMemset(ch, 0xFF, 4ull * c->kpad));
+                ESP_CUDA(cudaMemset(ch + 4ull * c->kpad, 0, 4ull * c->kpad));
+              }
+          } else {
+            if (b.recv1.base) ESP_CUDA(cudaMemset(b.recv1.at(lr), 0, 2ull * n * b.slot));
+            if (b.recv2.base) ESP_CUDA(cudaMemset(b.recv2.at(lr), 0, 2ull * n * b.slot));
+            if (b.mid.base) ESP_CUDA(cudaMemset(b.mid.at(lr), 0, 2ull * b.slot));
+            if (b.stage.base) ESP_CUDA(cudaMemset(b.stage.at(lr), 0, b.slot));
+          }
           ESP_CUDA(cudaMemset(p.arena.base + b.cnt_off, 0, 256));
         }
       }
@@ -544,20 +721,29 @@ static void open_peers(Plan& p, cudaStream_t st) {
       base[q] = static_cast<unsigned char*>(ptr);
     }
   }
+  auto upload = [](auto& dev, const auto& host) {
+    ESP_CUDA(cudaMalloc(&dev, sizeof(host[0]) * host.size()));
+    ESP_CUDA(cudaMemcpy(dev, host.data(), sizeof(host[0]) * host.size(), cudaMemcpyHostToDevice));
+  };
   for (auto& b : p.buckets) {
     if (!b.fused) continue;
-    const size_t S = b.slot;
-    std::vector<unsigned char*> dsts(2 * n);
-    std::vector<unsigned long long*> cnts(n);
+    // my slot in every rank q's phase-1/2 buffer, per call parity; counters
+    std::vector<unsigned char*> dsts(2 * n), dsts2(2 * n);
+    std::vector<unsigned long long*> cnts(n), cnts2(n);
     for (int par = 0; par < 2; ++par)
-      for (int q = 0; q < n; ++q)
-        dsts[par * n + q] = base[q] + b.recv1_off + ((size_t)par * n + w->rank) * S;
-    for (int q = 0; q < n; ++q) cnts[q] = reinterpret_cast<unsigned long long*>(base[q] + b.cnt_off);
+      for (int q = 0; q < n; ++q) {
+        dsts[par * n + q] = base[q] + b.dst1_off + par * b.dst1_par + (size_t)w->rank * b.dst1_slot;
+        dsts2[par * n + q] = base[q] + b.dst2_off + par * b.dst2_par + (size_t)w->rank * b.dst2_slot;
+      }
+    for (int q = 0; q < n; ++q) {
+      cnts[q] = reinterpret_cast<unsigned long long*>(base[q] + b.cnt_off);
+      cnts2[q] = cnts[q] + 1;
+    }
     b.my_cnt = reinterpret_cast<unsigned long long*>(p.arena.base + b.cnt_off);
-    ESP_CUDA(cudaMalloc(&b.dsts, sizeof(void*) * 2 * n));
-    ESP_CUDA(cudaMalloc(&b.cnts, sizeof(void*) * n));
-    ESP_CUDA(cudaMemcpy(b.dsts, dsts.data(), sizeof(void*) * 2 * n, cudaMemcpyHostToDevice));
-    ESP_CUDA(cudaMemcpy(b.cnts, cnts.data(), sizeof(void*) * n, cudaMemcpyHostToDevice));
+    upload(b.dsts, dsts);
+    upload(b.dsts2, dsts2);
+    upload(b.cnts, cnts);
+    upload(b.cnts2, cnts2);
   }
   p.peers_ready = true;
 }
@@ -673,6 +859,7 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
   if (p.w->probe && b.nh1_units) probe_pair(p.w, &e0, &e1, b.h1_bytes);
   const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
   if (e0 && !dgc) ESP_CUDA(cudaEventRecord(e0, st));
+  if (b.push) fused = false;   // local payload; push_kernel moves it (run_comm)
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
       if (fused) {
@@ -684,8 +871,15 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
       }
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
-    case ESP_EFSIGNSGD: launch_sign_h1_tma(K_EFSIGN, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st); break;
-    case ESP_ONEBIT: launch_sign_h1_tma(K_ONEBIT, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st); break;
+    case ESP_EFSIGNSGD:
+    case ESP_ONEBIT: {
+      const int k = b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT;
+      const int n = p.w->nranks;
+      if (fused) launch_sign_h1_tma(k, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st,
+                                    b.dsts + (b.epoch & 1) * n, b.cnts, b.h1_dmode, n);
+      else launch_sign_h1_tma(k, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st);
+      break;
+    }
     default: launch_pack(b.h1, b.h1_units, b.nh1_units, st); break;
   }
   if (e1 && !dgc) ESP_CUDA(cudaEventRecord(e1, st));
@@ -695,7 +889,16 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
 
 static void run_mid(Plan& p, Bucket& b, cudaStream_t cs) {
   const int k = b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT;
-  launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, b.a7_pieces, cs);
+  if (b.fused && b.push) {
+    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, (b.epoch & 1) ? b.a7_pieces_odd : b.a7_pieces, cs);
+  } else if (b.fused) {
+    // recompressed chunks go straight into every rank's phase-2 buffer
+    const int n = p.w->nranks;
+    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, (b.epoch & 1) ? b.a7_pieces_odd : b.a7_pieces, cs,
+                       b.dsts2 + (b.epoch & 1) * n, b.cnts2, 2, n);
+  } else {
+    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, b.a7_pieces, cs);
+  }
   ESP_CUDA(cudaGetLastError());
 }
 
@@ -704,17 +907,59 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
   const int n = w->nranks;
   const size_t S = b.slot;
   const bool quant = is_quant(b.kind);
+  if (b.fused) {
+    // the payloads were pushed by the producers (every rank's h1, then a7);
+    // wait for this call's arrivals (the counters are monotonic across calls).
+    // The counters record the routine's logical traffic (the cost table)
+    const unsigned long long e1 = b.epoch + 1;
+    const int par = (int)(b.epoch & 1);
+    auto push1 = [&] {
+      if (b.push) launch_push(b.push1, b.npush1, b.send.at(0), b.dsts + par * n, b.cnts, cs);
+    };
+    auto push2 = [&] {
+      if (b.push) launch_push(b.push2, b.npush2, b.stage.at(0), b.dsts2 + par * n, b.cnts2, cs);
+    };
+    push1();
+    switch (b.routine) {
+      case ESP_ALLGATHER:
+        count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
+        launch_wait_arrivals(b.my_cnt, e1 * b.target1, cs);
+        break;
+      case ESP_ALLTOALL_ALLGATHER:
+        count_coll(w, 0, ESP_OP_ALLTOALL, (n - 1) * S, (n - 1) * S);
+        launch_wait_arrivals(b.my_cnt, e1 * b.target1, cs);
+        if (quant) {
+          if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
+          run_mid(p, b, cs);
+          if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
+          push2();
+          count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
+          launch_wait_arrivals(b.my_cnt + 1, e1 * b.target2, cs);
+        } else {
+          count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * n * S, (n - 1) * n * S);
+        }
+        break;
+      default: {   // quantized Gather/Broadcast
+        const bool root = w->rank == 0;
+        count_coll(w, 0, ESP_OP_GATHER, root ? 0 : S, root ? (n - 1) * S : 0);
+        if (root) {
+          launch_wait_arrivals(b.my_cnt, e1 * b.target1, cs);
+          if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
+          run_mid(p, b, cs);
+          if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
+          push2();
+        }
+        count_coll(w, 0, ESP_OP_BROADCAST, root ? S : 0, root ? 0 : S);
+        launch_wait_arrivals(b.my_cnt + 1, e1 * b.target2, cs);
+        break;
+      }
+    }
+    ESP_CUDA(cudaGetLastError());
+    return;
+  }
   switch (b.routine) {
     case ESP_ALLGATHER:
-      if (b.fused) {
-        // the payloads were pushed by every rank's h1; wait for all n x ngroups
-        // arrivals of this call (the counter is monotonic across calls)
-        count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
-        launch_wait_arrivals(b.my_cnt, (b.epoch + 1) * (unsigned long long)n * b.nh1_groups, cs);
-        ESP_CUDA(cudaGetLastError());
-      } else {
-        coll_allgather(w, b.send, b.recv1, S, cs);
-      }
+      coll_allgather(w, b.send, b.recv1, S, cs);
       break;
     case ESP_ALLTOALL_ALLGATHER:
       coll_alltoall(w, b.send, b.recv1, S, cs);
@@ -764,7 +1009,7 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
         coll_allgather_inplace_f32(w, b.recv1, count / n, cs);
       } else {
         coll_reduce_f32(w, b.send, b.recv1, count, cs);
-        ESP_NCCL(ncclBroadcast(b.recv1.at(0), b.recv1.at(0), 4 * count, ncclUint8, 0, w->comm, cs));
+        if (n > 1) ESP_NCCL(ncclBroadcast(b.recv1.at(0), b.recv1.at(0), 4 * count, ncclUint8, 0, w->comm, cs));
       }
       break;
     }
@@ -780,8 +1025,11 @@ static void run_h2(Plan& p, Bucket& b, cudaStream_t st) {
     case ESP_RANDOMK:
       launch_h2_randomk(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, b.h2_rankterms, st);
       break;
-    case ESP_EFSIGNSGD: launch_h2_sign(K_EFSIGN, b.h2, b.h2_units, b.nh2_units, b.h2_pieces, st); break;
-    case ESP_ONEBIT: launch_h2_sign(K_ONEBIT, b.h2, b.h2_units, b.nh2_units, b.h2_pieces, st); break;
+    case ESP_EFSIGNSGD:
+    case ESP_ONEBIT:
+      launch_h2_sign(b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT, b.h2, b.h2_units, b.nh2_units,
+                     (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, st);
+      break;
     default: launch_h2_dense(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, st); break;
   }
   ESP_CUDA(cudaGetLastError());

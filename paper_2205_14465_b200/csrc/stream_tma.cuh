@@ -206,6 +206,11 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1)
     }
   }
   if (cur != 0xFFFFFFFFu) end_seg(S, cur_units, first_unit, st);
+  // ops that store into peer GPUs' memory: the arrival signal is sent by the
+  // next kernel in stream order, after this grid has completed (kernel
+  // completion performs all of its stores, peer stores included); the optional
+  // per-thread system fence is an A/B knob (ESP_SYS_FENCE=1)
+  if (op.sys_fence()) __threadfence_system();
 }
 
 int tma_stream_grid(int nunits);

@@ -97,10 +97,16 @@ static int grank(esp_world_s* w, int lr) { return w->sim ? lr : w->rank; }
 static void d2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (bytes && dst != src) ESP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
 }
+// one real rank: the plan aliases receive and send buffers, nothing moves
+static bool solo(esp_world_s* w) { return !w->sim && w->nranks == 1; }
 
 void coll_allgather(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t bytes, cudaStream_t st) {
   const int n = w->nranks;
   for (int lr = 0; lr < w->nlocal; ++lr) count_coll(w, lr, ESP_OP_ALLGATHER, (n - 1) * bytes, (n - 1) * bytes);
+  if (solo(w)) {
+    d2d(recv.at(0), send.at(0), bytes, st);
+    return;
+  }
   if (w->sim) {
     for (int q = 0; q < n; ++q)
       for (int r = 0; r < n; ++r) d2d(recv.at(q) + r * bytes, send.at(r), bytes, st);
@@ -112,6 +118,10 @@ void coll_allgather(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t bytes
 void coll_alltoall(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t chunk, cudaStream_t st) {
   const int n = w->nranks;
   for (int lr = 0; lr < w->nlocal; ++lr) count_coll(w, lr, ESP_OP_ALLTOALL, (n - 1) * chunk, (n - 1) * chunk);
+  if (solo(w)) {
+    d2d(recv.at(0), send.at(0), chunk, st);
+    return;
+  }
   if (w->sim) {
     for (int q = 0; q < n; ++q)
       for (int r = 0; r < n; ++r) d2d(recv.at(q) + r * chunk, send.at(r) + q * chunk, chunk, st);
@@ -126,6 +136,10 @@ void coll_gather(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t bytes, c
     if (grank(w, lr) == 0) count_coll(w, lr, ESP_OP_GATHER, 0, (n - 1) * bytes);
     else count_coll(w, lr, ESP_OP_GATHER, bytes, 0);
   }
+  if (solo(w)) {
+    d2d(recv.at(0), send.at(0), bytes, st);
+    return;
+  }
   if (w->sim) {
     for (int r = 0; r < n; ++r) d2d(recv.at(0) + r * bytes, send.at(r), bytes, st);
   } else {
@@ -139,6 +153,9 @@ void coll_broadcast(esp_world_s* w, LocalBufs buf, size_t bytes, cudaStream_t st
     if (grank(w, lr) == 0) count_coll(w, lr, ESP_OP_BROADCAST, n > 1 ? bytes : 0, 0);
     else count_coll(w, lr, ESP_OP_BROADCAST, 0, bytes);
   }
+  if (solo(w)) {
+    return;
+  }
   if (w->sim) {
     for (int q = 1; q < n; ++q) d2d(buf.at(q), buf.at(0), bytes, st);
   } else {
@@ -147,16 +164,27 @@ void coll_broadcast(esp_world_s* w, LocalBufs buf, size_t bytes, cudaStream_t st
 }
 
 void coll_allreduce_f32(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t count_, cudaStream_t st) {
+  if (solo(w)) {
+    d2d(recv.at(0), send.at(0), 4 * count_, st);
+    return;
+  }
   ESP_REQUIRE(!w->sim, ESP_ERR_STATE, "allreduce in a sim world is executed by h2");
   ESP_NCCL(ncclAllReduce(send.at(0), recv.at(0), count_, ncclFloat32, ncclSum, w->comm, st));
 }
 
 void coll_reducescatter_f32(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t count_, cudaStream_t st) {
+  if (solo(w)) {
+    d2d(recv.at(0), send.at(0), 4 * count_, st);
+    return;
+  }
   ESP_REQUIRE(!w->sim, ESP_ERR_STATE, "reduce-scatter in a sim world is executed by h2");
   ESP_NCCL(ncclReduceScatter(send.at(0), recv.at(0), count_ / w->nranks, ncclFloat32, ncclSum, w->comm, st));
 }
 
 void coll_allgather_inplace_f32(esp_world_s* w, LocalBufs buf, size_t count_per_rank, cudaStream_t st) {
+  if (solo(w)) {
+    return;
+  }
   ESP_REQUIRE(!w->sim, ESP_ERR_STATE, "in-place allgather in a sim world is executed by h2");
   float* base = reinterpret_cast<float*>(buf.at(0));
   ESP_NCCL(ncclAllGather(base + (size_t)w->rank * count_per_rank, base, count_per_rank, ncclFloat32,
@@ -164,6 +192,10 @@ void coll_allgather_inplace_f32(esp_world_s* w, LocalBufs buf, size_t count_per_
 }
 
 void coll_reduce_f32(esp_world_s* w, LocalBufs send, LocalBufs recv, size_t count_, cudaStream_t st) {
+  if (solo(w)) {
+    d2d(recv.at(0), send.at(0), 4 * count_, st);
+    return;
+  }
   ESP_REQUIRE(!w->sim, ESP_ERR_STATE, "reduce in a sim world is executed by h2");
   ESP_NCCL(ncclReduce(send.at(0), recv.at(0), count_, ncclFloat32, ncclSum, 0, w->comm, st));
 }

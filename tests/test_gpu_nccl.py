@@ -12,7 +12,7 @@ torch = pytest.importorskip("torch")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("nproc", [2, 4, 8])
+@pytest.mark.parametrize("nproc", [1, 2, 4, 8])
 def test_nccl_world_parity(nproc):
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs, found {torch.cuda.device_count()}")
