@@ -44,26 +44,28 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2
 // One WARP per output tile, persistent over tiles (stride = all warps of the
 // grid): no CTA barrier anywhere, so 64 independent tiles per SM hide the load
 // latencies of the entry lists (a CTA-wide tile loop was latency-bound).
-// Per tile: the dense zero fill straight from registers (the 4 B/elem write
-// that bounds the kernel), then only the touched words are rewritten:
-//   one piece:     out[e] = (+0 + v) / d
-//   several, <= 32 entries in the tile (the sparse common case): one entry per
-//                  lane, equal indices grouped by __match_any_sync, each group
-//                  summed from +0 in lane (= rank) order by its lowest lane and
-//                  stored once;
-//   several, more: out[e] = out[e] + v_r for r in rank order (the zero fill is
-//                  the sum's +0; __syncwarp orders the pieces), then each
-//                  distinct touched word is divided once (a per-warp bitmap
-//                  in shared memory elects the owner).
+// Per tile, by the number of entries the pieces have in it:
+//   one piece:     dense zero fill straight from registers (the 4 B/elem write
+//                  that bounds the kernel), then out[e] = (+0 + v) / d for the
+//                  touched words;
+//   several, <= 32 entries in the tile (the sparse common case): zero fill, then
+//                  one entry per lane, equal indices grouped by
+//                  __match_any_sync, each group summed from +0 in lane (= rank)
+//                  order by its lowest lane and stored once;
+//   several, more: the warp's 1024-float shared-memory tile starts at +0, the
+//                  pieces are added in rank order (indices are distinct within a
+//                  piece; __syncwarp orders the pieces), then the tile is
+//                  divided and written once with coalesced float4 stores -- no
+//                  global read-modify-write.
 __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __restrict__ segs,
                                                                  const uint32_t* __restrict__ tile_seg,
                                                                  uint32_t ntiles,
                                                                  const unsigned char* const* __restrict__ pieces) {
   constexpr int kWarps = kTileThreads / 32;
   constexpr unsigned kFull = 0xffffffffu;
-  __shared__ uint32_t seen_all[kWarps][kTile / 32];
+  __shared__ __align__(16) float acc_all[kWarps][kTile];
   const int lane = threadIdx.x & 31;
-  uint32_t* seen = seen_all[threadIdx.x >> 5];
+  float* acc = acc_all[threadIdx.x >> 5];
   const uint32_t GW = gridDim.x * kWarps;
   uint32_t tg = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (tg >= ntiles) return;
@@ -96,12 +98,9 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
     const uint32_t t = tg - S.unit0;
     const uint32_t lo = t * kTile;
     const uint32_t hi = min(lo + (uint32_t)kTile, S.n);
-    for (uint32_t i = lane * 4; lo + i < hi; i += 128) store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
     const uint32_t np = S.npieces;
     const bool ones = S.divisor == 1.0f;
     const Divisor div(S.divisor);
-    if (np > 1 && !ones)
-      for (int i = lane; i < kTile / 32; i += 32) seen[i] = 0;
     const uint32_t clo0 = plo0, chi0 = phi0, clo1 = plo1, chi1 = phi1;
     auto range = [&](uint32_t r, uint32_t* a, uint32_t* b) {
       *a = __shfl_sync(kFull, r < 32 ? clo0 : clo1, r & 31);
@@ -115,20 +114,9 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
       if (tn >= S.unit0 + S.nunits) Sn_p = segs + tile_seg[tn];
       load_toff(Sn_p ? *Sn_p : S, tn - (Sn_p ? Sn_p->unit0 : S.unit0));
     }
-    __syncwarp();   // zero stores (and the bitmap reset) before the touched-word stores
-    if (np == 1) {
-      const unsigned char* pc = pieces[S.piece0];
-      const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
-      const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
-      uint32_t a, b;
-      range(0, &a, &b);
-      for (uint32_t i = a + lane; i < b; i += 32) {
-        const float v = __fadd_rn(0.f, __ldg(val + i));   // +0 + v: the oracle's sum from +0
-        out[__ldg(idx + i)] = ones ? v : div(v);
-      }
-    } else {
-      // the tile's entries of all pieces, in rank order: lane l takes the l-th
-      uint32_t tot = 0, my_r = 0xFFFFFFFFu, my_i = 0;
+    // the tile's entries of all pieces, in rank order: lane l takes the l-th
+    uint32_t tot = 0, my_r = 0xFFFFFFFFu, my_i = 0;
+    if (np > 1) {
       for (uint32_t r = 0; r < np; ++r) {
         uint32_t a, b;
         range(r, &a, &b);
@@ -138,15 +126,53 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
         }
         tot += b - a;
       }
-      if (tot <= 32) {
+    }
+    if (np > 1 && tot > 32) {
+      // shared-memory accumulation in rank order, one coalesced write
+#pragma unroll
+      for (int i = lane * 4; i < kTile; i += 128)
+        *reinterpret_cast<float4*>(acc + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+      __syncwarp();
+      for (uint32_t r = 0; r < np; ++r) {
+        const unsigned char* pc = reinterpret_cast<const unsigned char*>(__shfl_sync(
+            kFull, reinterpret_cast<unsigned long long>(r < 32 ? pp0 : pp1), r & 31));
+        const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
+        const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
+        uint32_t a, b;
+        range(r, &a, &b);
+        for (uint32_t i = a + lane; i < b; i += 32) {
+          const uint32_t w = __ldg(idx + i) - lo;
+          acc[w] = __fadd_rn(acc[w], __ldg(val + i));   // distinct indices within a piece
+        }
+        __syncwarp();
+      }
+      for (uint32_t i = lane * 4; lo + i < hi; i += 128) {
+        float4 v = *reinterpret_cast<const float4*>(acc + i);
+        if (!ones) v = div(v);
+        store4_guard(out, lo + i, S.n, v);
+      }
+    } else {
+      for (uint32_t i = lane * 4; lo + i < hi; i += 128) store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
+      __syncwarp();   // zero stores before the touched-word stores
+      if (np == 1) {
+        const unsigned char* pc = pieces[S.piece0];
+        const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
+        const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
+        uint32_t a, b;
+        range(0, &a, &b);
+        for (uint32_t i = a + lane; i < b; i += 32) {
+          const float v = __fadd_rn(0.f, __ldg(val + i));   // +0 + v: the oracle's sum from +0
+          out[__ldg(idx + i)] = ones ? v : div(v);
+        }
+      } else {
         // one entry per lane: lanes holding the same index form a group
         // (__match_any_sync), whose lowest lane sums it in lane = rank order
         // from +0 and stores it once -- no read-modify-write round trips
         const int src = (int)(my_r & 31u);
         const unsigned char* q0 = reinterpret_cast<const unsigned char*>(
-            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(pp0), src));
+            __shfl_sync(kFull, reinterpret_cast<unsigned long long>(pp0), src));
         const unsigned char* q1 = reinterpret_cast<const unsigned char*>(
-            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(pp1), src));
+            __shfl_sync(kFull, reinterpret_cast<unsigned long long>(pp1), src));
         uint32_t e = 0x80000000u | (uint32_t)lane;   // no entry: a key no index has
         float v = 0.f;
         if (my_r != 0xFFFFFFFFu) {
@@ -154,43 +180,17 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
           e = __ldg(reinterpret_cast<const uint32_t*>(pc) + my_i);
           v = __ldg(reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad) + my_i);
         }
-        const uint32_t grp = __match_any_sync(0xffffffffu, e);
+        const uint32_t grp = __match_any_sync(kFull, e);
         float sum = 0.f;
         uint32_t rest = grp;
         for (uint32_t m = 0; m < np; ++m) {   // at most one member per piece
-          const float x = __shfl_sync(0xffffffffu, v, rest ? __ffs(rest) - 1 : lane);
+          const float x = __shfl_sync(kFull, v, rest ? __ffs(rest) - 1 : lane);
           if (rest) {
             sum = __fadd_rn(sum, x);
             rest &= rest - 1;
           }
         }
         if (my_r != 0xFFFFFFFFu && __ffs(grp) - 1 == lane) out[e] = ones ? sum : div(sum);
-      } else {
-        for (uint32_t r = 0; r < np; ++r) {
-          const unsigned char* pc = pieces[S.piece0 + r];
-          const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
-          const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
-          uint32_t a, b;
-          range(r, &a, &b);
-          for (uint32_t i = a + lane; i < b; i += 32) {
-            const uint32_t e = __ldg(idx + i);
-            const float v = __ldg(val + i);
-            out[e] = __fadd_rn(__ldcg(out + e), v);   // distinct indices within a piece
-          }
-          __syncwarp();
-        }
-        if (!ones) {
-          for (uint32_t r = 0; r < np; ++r) {
-            const uint32_t* idx = reinterpret_cast<const uint32_t*>(pieces[S.piece0 + r]);
-            uint32_t a, b;
-            range(r, &a, &b);
-            for (uint32_t i = a + lane; i < b; i += 32) {
-              const uint32_t e = __ldg(idx + i);
-              const uint32_t w = e - lo, m = 1u << (w & 31);
-              if (!(atomicOr(&seen[w >> 5], m) & m)) out[e] = div(__ldcg(out + e));
-            }
-          }
-        }
       }
     }
     if (tn >= ntiles) break;
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
       out = seg_out(S);
       load_pp(S);
     }
-    __syncwarp();   // bitmap reuse
+    __syncwarp();   // shared tile reuse
   }
 }
 
