@@ -43,8 +43,10 @@ void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaSt
 
 // h2 (k_h2.cu)
 // jobs: {segment, piece within segment, first entry, 0}, kOffJob entries each
+// max_pieces: the largest npieces of the launch's segments (> 1 enables the
+// shared-memory accumulation path and its dynamic shared memory)
 void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
-                      const unsigned char* const* pieces, cudaStream_t st);
+                      const unsigned char* const* pieces, int max_pieces, cudaStream_t st);
 void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
                     const unsigned char* const* pieces, cudaStream_t st);
 void launch_h2_randomk(const SegH2* segs, const uint32_t* unit_seg, int nunits,

@@ -63,9 +63,11 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
                                                                  const unsigned char* const* __restrict__ pieces) {
   constexpr int kWarps = kTileThreads / 32;
   constexpr unsigned kFull = 0xffffffffu;
-  __shared__ __align__(16) float acc_all[kWarps][kTile];
+  // the per-warp accumulation tiles (dynamic: absent when every segment of the
+  // launch has a single piece, so that case keeps its full occupancy)
+  extern __shared__ __align__(16) float acc_all[];
   const int lane = threadIdx.x & 31;
-  float* acc = acc_all[threadIdx.x >> 5];
+  float* acc = acc_all + (threadIdx.x >> 5) * kTile;
   const uint32_t GW = gridDim.x * kWarps;
   uint32_t tg = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (tg >= ntiles) return;
@@ -283,19 +285,23 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const SegH1* __restrict_
 }
 
 void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
-                      const unsigned char* const* pieces, cudaStream_t st) {
+                      const unsigned char* const* pieces, int max_pieces, cudaStream_t st) {
   if (ntiles == 0) return;
   h2_sparse_offsets_kernel<<<njobs, kThreads, 0, st>>>(segs, jobs, pieces);
-  static int grid_cap = [] {
+  constexpr int kSmem = kTileThreads / 32 * kTile * (int)sizeof(float);
+  auto cap = [](int smem) {
     int dev = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sparse_kernel, kTileThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sparse_kernel, kTileThreads, smem);
     return sms * (per_sm > 0 ? per_sm : 8);
-  }();
+  };
+  static const int cap1 = cap(0), capn = cap(kSmem);
+  const int smem = max_pieces > 1 ? kSmem : 0;
+  const int grid_cap = max_pieces > 1 ? capn : cap1;
   const int need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);   // one warp per tile
   const int grid = need < grid_cap ? need : grid_cap;
-  h2_sparse_kernel<<<grid, kTileThreads, 0, st>>>(segs, tile_seg, (uint32_t)ntiles, pieces);
+  h2_sparse_kernel<<<grid, kTileThreads, smem, st>>>(segs, tile_seg, (uint32_t)ntiles, pieces);
   count_launches(2);
 }
 

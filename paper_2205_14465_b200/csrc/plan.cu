@@ -34,6 +34,7 @@ struct Bucket {
   const unsigned char** h2_pieces = nullptr;
   uint32_t* h2_rankterms = nullptr;
   uint4* h2_off_jobs = nullptr; int nh2_off_jobs = 0;
+  int h2_max_pieces = 0;
   cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
@@ -558,6 +559,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     }
   }
   b.nh2 = (int)(T.h2.size() - h2_first);
+  b.h2_max_pieces = 0;
+  for (int i = 0; i < b.nh2; ++i) b.h2_max_pieces = std::max(b.h2_max_pieces, (int)T.h2[h2_first + i].npieces);
   b.nh2_units = (int)u0;
 
   // per critical rank op counts of the cost table
@@ -1020,7 +1023,7 @@ static void run_h2(Plan& p, Bucket& b, cudaStream_t st) {
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
       launch_h2_sparse(b.h2, b.h2_units, b.nh2_units, b.h2_off_jobs, b.nh2_off_jobs,
-                       (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, st);
+                       (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, b.h2_max_pieces, st);
       break;
     case ESP_RANDOMK:
       launch_h2_randomk(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, b.h2_rankterms, st);

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libesp.so")
+LIB_PATH = os.environ.get("ESP_LIB") or os.path.join(HERE, "libesp.so")   # ESP_LIB: another build, for A/B runs
 
 KINDS = {"none": 0, "randomk": 1, "dgc": 2, "topk": 3, "efsignsgd": 4, "onebit": 5}
 ROUTINES = {"allreduce": 0, "allgather": 1, "alltoall_allgather": 2, "gather_broadcast": 3,
