@@ -256,7 +256,7 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
         pp.push_back((const unsigned char*)pieces[i] + (size_t)p * c->chunk_bytes);
         rt.push_back(c->cfg.randomk_shared_indices ? 0u : (uint32_t)i + 1);
       }
-      s.nunits = div_up(len, tiles ? kTile : kUnit);
+      s.nunits = div_up(len, tiles ? kTile : is_quant(c->cfg.kind) ? kSignUnit : kUnit);
       s.unit0 = u0;
       u0 += s.nunits;
       for (uint32_t i = 0; i < s.nunits; ++i) units.push_back((uint32_t)segs.size());

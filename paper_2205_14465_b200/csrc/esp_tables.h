@@ -15,6 +15,10 @@ constexpr int kNJ = kRun / 128;          // float4 per lane per run
 constexpr int kDgcTile = 8 * kRun;       // DGC streaming tile (one run per consumer warp)
 constexpr int kSignSpan = 1024;          // sign h1: elements per warp per unit
 constexpr int kUnit = 8192;              // 8 runs per CTA
+#ifndef ESP_SIGN_UNIT
+#define ESP_SIGN_UNIT 8192
+#endif
+constexpr int kSignUnit = ESP_SIGN_UNIT;  // sign h2: elements per CTA (one prologue per 128 KB of output)
 constexpr int kRunsPerGroup = 64;        // DGC finalize: runs per warp-group (32768 elements)
 constexpr int kSample = 4096;            // DGC sampled-threshold sample size
 #ifndef ESP_H2_TILE

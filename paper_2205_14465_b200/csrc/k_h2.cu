@@ -206,41 +206,71 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
   }
 }
 
+// Sign h2: a grid of a few CTAs per SM, each over a contiguous range of the
+// bucket's units (mostly inside one segment), so the dependent prologue of a
+// segment (its table entry, the piece pointers and scales) is paid once per
+// (CTA, segment) instead of once per unit.  Per unit: pieces outer, the
+// thread's kJ float4 inner, so all kJ word loads of a piece are in flight
+// together; rank-order fp32 sum from +0, then / divisor (R9).
 template <int KIND>
 __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restrict__ segs,
                                                            const uint32_t* __restrict__ unit_seg,
+                                                           uint32_t nunits,
                                                            const unsigned char* const* __restrict__ pieces) {
   __shared__ float sh_sp[kMaxPieces], sh_sn[kMaxPieces];
   __shared__ const uint32_t* sh_w[kMaxPieces];
-  const uint32_t sid = unit_seg[blockIdx.x];
-  const SegH2 S = segs[sid];
-  const uint32_t u = blockIdx.x - S.unit0;
-  const uint32_t n = S.n;
-  for (uint32_t r = threadIdx.x; r < S.npieces; r += kThreads) {
-    const unsigned char* h = pieces[S.piece0 + r];
-    const float* f = reinterpret_cast<const float*>(h);
-    if (KIND == K_EFSIGN) { sh_sp[r] = f[0]; sh_sn[r] = -f[0]; }
-    else { sh_sn[r] = f[0]; sh_sp[r] = f[1]; }
-    sh_w[r] = reinterpret_cast<const uint32_t*>(h + 16);
-  }
-  __syncthreads();
-  const Divisor div(S.divisor);
-  const bool ones = S.divisor == 1.0f;
-#pragma unroll 2
-  for (int j = 0; j < kUnit / (kThreads * 4); ++j) {
-    const uint32_t e = u * kUnit + (j * kThreads + threadIdx.x) * 4;
-    if (e >= n) break;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t r = 0; r < S.npieces; ++r) {
-      const uint32_t nib = (__ldg(sh_w[r] + (e >> 5)) >> (e & 31)) & 0xFu;
-      const float sp = sh_sp[r], sn = sh_sn[r];
-      acc.x = __fadd_rn(acc.x, (nib & 1) ? sp : sn);
-      acc.y = __fadd_rn(acc.y, (nib & 2) ? sp : sn);
-      acc.z = __fadd_rn(acc.z, (nib & 4) ? sp : sn);
-      acc.w = __fadd_rn(acc.w, (nib & 8) ? sp : sn);
+  constexpr int kJ = kSignUnit / (kThreads * 4);
+  const uint32_t u0 = (uint32_t)((uint64_t)blockIdx.x * nunits / gridDim.x);
+  const uint32_t u1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nunits / gridDim.x);
+  uint32_t cur = 0xFFFFFFFFu;
+  SegH2 S{};
+  for (uint32_t gu = u0; gu < u1; ++gu) {
+    const uint32_t sid = unit_seg[gu];
+    if (sid != cur) {
+      __syncthreads();   // the previous segment's table is no longer read
+      cur = sid;
+      S = segs[sid];
+      for (uint32_t r = threadIdx.x; r < S.npieces; r += kThreads) {
+        const unsigned char* h = pieces[S.piece0 + r];
+        const float* f = reinterpret_cast<const float*>(h);
+        if (KIND == K_EFSIGN) { sh_sp[r] = f[0]; sh_sn[r] = -f[0]; }
+        else { sh_sn[r] = f[0]; sh_sp[r] = f[1]; }
+        sh_w[r] = reinterpret_cast<const uint32_t*>(h + 16);
+      }
+      __syncthreads();
     }
-    if (!ones) acc = div(acc);
-    store4_guard(seg_out(S), e, n, acc);
+    const uint32_t n = S.n;
+    const Divisor div(S.divisor);
+    const bool ones = S.divisor == 1.0f;
+    const uint32_t e0 = (gu - S.unit0) * kSignUnit + threadIdx.x * 4;
+    float4 acc[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t r = 0; r < S.npieces; ++r) {
+      const uint32_t* w = sh_w[r];
+      const float sp = sh_sp[r], sn = sh_sn[r];
+      uint32_t wd[kJ];
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const uint32_t e = e0 + j * kThreads * 4;
+        wd[j] = e < n ? __ldg(w + (e >> 5)) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const uint32_t e = e0 + j * kThreads * 4;
+        const uint32_t nib = (wd[j] >> (e & 31)) & 0xFu;
+        acc[j].x = __fadd_rn(acc[j].x, (nib & 1) ? sp : sn);
+        acc[j].y = __fadd_rn(acc[j].y, (nib & 2) ? sp : sn);
+        acc[j].z = __fadd_rn(acc[j].z, (nib & 4) ? sp : sn);
+        acc[j].w = __fadd_rn(acc[j].w, (nib & 8) ? sp : sn);
+      }
+    }
+    float* out = seg_out(S);
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const uint32_t e = e0 + j * kThreads * 4;
+      if (e < n) store4_guard(out, e, n, ones ? acc[j] : div(acc[j]));
+    }
   }
 }
 
@@ -308,8 +338,16 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
 void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
                     const unsigned char* const* pieces, cudaStream_t st) {
   if (nunits == 0) return;
-  if (kind == K_EFSIGN) h2_sign_kernel<K_EFSIGN><<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
-  else h2_sign_kernel<K_ONEBIT><<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
+  static const int cap = [] {
+    int dev = 0, sms = 148, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sign_kernel<K_EFSIGN>, kThreads, 0);
+    return sms * (per_sm > 0 ? per_sm : 4);
+  }();
+  const int grid = nunits < cap ? nunits : cap;
+  if (kind == K_EFSIGN) h2_sign_kernel<K_EFSIGN><<<grid, kThreads, 0, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
+  else h2_sign_kernel<K_ONEBIT><<<grid, kThreads, 0, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
   count_launches(1);
 }
 

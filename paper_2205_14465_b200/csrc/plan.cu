@@ -544,7 +544,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
             s.divisor = divisor;
             break;
         }
-        s.nunits = div_up(len, tiles ? kTile : kUnit);
+        s.nunits = div_up(len, tiles ? kTile : quant ? kSignUnit : kUnit);
         s.unit0 = u0;
         u0 += s.nunits;
         if (tiles) {
