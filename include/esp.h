@@ -95,6 +95,13 @@ typedef struct {
   uint64_t seed;                  /* Randomk hash seed */
   int32_t randomk_shared_indices; /* 1: same indices on every rank => allreducible (R5) */
   int32_t reduce;                 /* esp_reduce_t */
+  /* Alltoall/Allgather and Gather/Broadcast (App. A, reading R19):
+   * 1 = forward the first compression's chunks (decompress n^2 resp. n pieces),
+   * 2 = decompress + aggregate + recompress mid-scheme with a second residual
+   * (alpha = 1/n resp. 1); 0 = the cost table's choice ("the first process for
+   * sparse tensors and the second process for quantized tensors").
+   * Ignored by the other routines; other values -> ESP_ERR_INVALID_ARG. */
+  int32_t process;
 } esp_compressor_cfg_t;
 
 typedef struct esp_world_s* esp_world_t;

@@ -56,6 +56,19 @@ class Cfg:
     seed: int = 0
     shared_indices: bool = True   # Randomk (R5)
     reduce: str = "mean"          # R9
+    process: int = 0              # Alltoall/Allgather, Gather/Broadcast: 1 or 2 (0: the table's choice, R19)
+
+
+def process_of(cfg: Cfg) -> int:
+    """The two processes of the divisible routines (App. A, P:66-87 and
+    P:93-115): process 1 forwards the first compression's chunks (decompress n^2
+    resp. n pieces); process 2 decompresses, aggregates and recompresses
+    mid-scheme.  "We take the first process for sparse tensors and the second
+    process for quantized tensors in Table ..., but the decision tree
+    abstraction covers all of them": 0 selects that default."""
+    if cfg.process in (1, 2):
+        return cfg.process
+    return 1 if cfg.kind in SPARSE else 2
 
 
 def legal(cfg: Cfg, routine: str) -> bool:
@@ -341,10 +354,11 @@ def new_states(n: int, numel: int, routine: str, cfg: Cfg):
     st = []
     for rank in range(n):
         r2 = None
-        if cfg.kind in QUANTIZED and routine == "alltoall_allgather":
+        p2 = cfg.kind != "none" and process_of(cfg) == 2
+        if p2 and routine == "alltoall_allgather":
             lo, hi = partitions(numel, n)[rank]
             r2 = np.zeros(hi - lo, np.float32)
-        elif cfg.kind in QUANTIZED and routine == "gather_broadcast" and rank == 0:
+        elif p2 and routine == "gather_broadcast" and rank == 0:
             r2 = np.zeros(numel, np.float32)
         st.append(RankState(np.zeros(numel, np.float32), r2))
     return st
@@ -433,7 +447,7 @@ def sync(routine: str, cfg: Cfg, grads, states, tensor_id: int = 0) -> SyncResul
             cnt[r].h2 += n
         outs = [out.copy() for _ in range(n)]
 
-    elif routine == "alltoall_allgather" and cfg.kind in SPARSE:
+    elif routine == "alltoall_allgather" and process_of(cfg) == 1:
         # process 1: Alltoall chunks (r -> j), Allgather the n received
         # chunks, decompress all n^2 pieces.
         for r in range(n):
@@ -447,9 +461,10 @@ def sync(routine: str, cfg: Cfg, grads, states, tensor_id: int = 0) -> SyncResul
         outs = [out.copy() for _ in range(n)]
 
     elif routine == "alltoall_allgather":
-        # quantized process 2: rank j decompresses the n chunks of
-        # partition j, aggregates, adds its second residual, recompresses
-        # (alpha = 1/n), Allgather; everyone decompresses the n partitions.
+        # process 2: rank j decompresses the n chunks of partition j,
+        # aggregates, adds its second residual, recompresses (alpha = 1/n: the
+        # same compressor on the partition, k_j = k_of(len_j) for sparse ones),
+        # Allgather; everyone decompresses the n partitions.
         c2 = []
         for j in range(n):
             lo, hi = parts[j]
@@ -473,7 +488,7 @@ def sync(routine: str, cfg: Cfg, grads, states, tensor_id: int = 0) -> SyncResul
             cnt[r].h2 += n
         outs = [out.copy() for _ in range(n)]
 
-    elif routine == "gather_broadcast" and cfg.kind in SPARSE:
+    elif routine == "gather_broadcast" and process_of(cfg) == 1:
         # process 1: Gather to root 0 (R17), Broadcast all n payloads.
         cnt[0].comm("gather", 0, (n - 1) * M)
         for r in range(1, n):
@@ -486,7 +501,7 @@ def sync(routine: str, cfg: Cfg, grads, states, tensor_id: int = 0) -> SyncResul
         outs = [out.copy() for _ in range(n)]
 
     elif routine == "gather_broadcast":
-        # quantized process 2 (R12, R14): root decompresses n payloads,
+        # process 2 (R12, R14): root decompresses n payloads,
         # aggregates, adds r2, recompresses (alpha = 1), broadcasts one payload.
         cnt[0].comm("gather", 0, (n - 1) * M)
         for r in range(1, n):
@@ -577,7 +592,8 @@ def table_row(cfg: Cfg, routine: str) -> str:
         return "allreduce"
     if routine == "allgather":
         return "allgather"
-    t = "sparse" if cfg.kind in SPARSE else "quantized"
+    # the table's "sparse" / "quantized" rows are processes 1 / 2
+    t = "sparse" if process_of(cfg) == 1 else "quantized"
     return f"{routine}_{t}"
 
 

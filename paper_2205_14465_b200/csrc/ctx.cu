@@ -21,6 +21,7 @@ void check_cfg(const esp_compressor_cfg_t* cfg) {
   ESP_REQUIRE(cfg, ESP_ERR_INVALID_ARG, "cfg is NULL");
   ESP_REQUIRE(cfg->kind >= ESP_NONE && cfg->kind <= ESP_ONEBIT, ESP_ERR_INVALID_ARG, "bad compressor kind");
   ESP_REQUIRE(cfg->reduce == ESP_MEAN || cfg->reduce == ESP_SUM, ESP_ERR_INVALID_ARG, "bad reduce mode");
+  ESP_REQUIRE(cfg->process >= 0 && cfg->process <= 2, ESP_ERR_INVALID_ARG, "process must be 0, 1 or 2");
   if (is_sparse(cfg->kind))
     ESP_REQUIRE(cfg->ratio > 0.0 && cfg->ratio <= 1.0, ESP_ERR_INVALID_ARG, "ratio must be in (0, 1]");
 }
@@ -72,12 +73,14 @@ esp_status_t esp_ctx_create(esp_world_t w, const esp_compressor_cfg_t* cfg, int 
     ESP_CUDA(cudaMalloc(&c->lazy, sizeof(float) * 2 * c->P * nl));
     ESP_CUDA(cudaMemset(c->lazy, 0, sizeof(float) * 2 * c->P * nl));
   }
-  if (is_quant(cfg->kind) && (routine == ESP_ALLTOALL_ALLGATHER || routine == ESP_GATHER_BROADCAST)) {
+  if (mid_scheme(*cfg, routine)) {
     c->r2_len = routine == ESP_ALLTOALL_ALLGATHER ? L : numel;
     ESP_CUDA(cudaMalloc(&c->r2, sizeof(float) * c->r2_len * nl));
     ESP_CUDA(cudaMemset(c->r2, 0, sizeof(float) * c->r2_len * nl));
-    ESP_CUDA(cudaMalloc(&c->lazy2, sizeof(float) * 2 * nl));
-    ESP_CUDA(cudaMemset(c->lazy2, 0, sizeof(float) * 2 * nl));
+    if (is_quant(cfg->kind)) {
+      ESP_CUDA(cudaMalloc(&c->lazy2, sizeof(float) * 2 * nl));
+      ESP_CUDA(cudaMemset(c->lazy2, 0, sizeof(float) * 2 * nl));
+    }
   }
   w->ctxs.insert(c.get());
   *out = c.release();
@@ -152,9 +155,11 @@ esp_status_t esp_ctx_get_state(esp_ctx_t c, void* host_buf, size_t* nbytes) {
     float* dst2 = dst + c->N;
     std::memset(dst2, 0, 4 * c->r2_len);
     const uint64_t v = r2_valid(c, lr);
-    if (v) {
+    if (v && c->lazy2) {
       launch_sign_materialize(kk, c->r2 + (size_t)lr * c->r2_len, c->lazy2 + (size_t)lr * 2, tmp, (uint32_t)v, 0);
       ESP_CUDA(cudaMemcpy(dst2, tmp, 4 * v, cudaMemcpyDeviceToHost));
+    } else if (v) {
+      ESP_CUDA(cudaMemcpy(dst2, c->r2 + (size_t)lr * c->r2_len, 4 * v, cudaMemcpyDeviceToHost));
     }
   }
   cudaFree(tmp);

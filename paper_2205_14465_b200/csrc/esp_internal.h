@@ -57,6 +57,10 @@ uint32_t partition_len(uint64_t numel, int nparts);   // L (multiple of 32) or n
 int nparts_of(int routine, int n);
 bool is_sparse(int kind);
 bool is_quant(int kind);
+// process 1 / 2 of the divisible routines (R19; 0 -> sparse 1, quantized 2)
+int process_of(const esp_compressor_cfg_t& cfg);
+// a divisible routine in process 2: decompress-aggregate-recompress mid-scheme (a7)
+bool mid_scheme(const esp_compressor_cfg_t& cfg, int routine);
 bool pair_legal(const esp_compressor_cfg_t& cfg, int routine);
 size_t chunk_bytes_of(const esp_compressor_cfg_t& cfg, uint64_t numel, int nparts,
                       uint32_t* kpad_out);

@@ -7,6 +7,8 @@
 // pointers and step counters plus the kernel/collective launches.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "esp_internal.h"
 #include "esp_kernels.h"
@@ -15,6 +17,8 @@ namespace esp {
 
 struct Bucket {
   int kind = 0, routine = 0, reduce = 0;
+  int proc = 1;                // process of a divisible routine (R19)
+  bool p2 = false;             // mid-scheme decompress-aggregate-recompress (a7)
   std::vector<int> tens;      // indices into Plan::ctxs
   int P = 1;
   size_t slot = 0;            // bytes of one slot = sum of the tensors' chunks
@@ -29,6 +33,15 @@ struct Bucket {
   SegH1* a7 = nullptr; int na7 = 0;
   uint32_t* a7_units = nullptr; int na7_units = 0;
   const unsigned char** a7_pieces = nullptr;
+  // a7 of a sparse compressor (process 2): h2 of the n chunks into a dense
+  // temporary (a7h2), then the compressor's h1 on it with r = r2 (a7)
+  uint32_t* a7_groups = nullptr; int na7_groups = 0;
+  SegH2* a7h2 = nullptr; int na7h2 = 0;
+  uint32_t* a7h2_units = nullptr; int na7h2_units = 0;
+  uint32_t* a7h2_rankterms = nullptr;
+  uint4* a7h2_off_jobs = nullptr; int na7h2_off_jobs = 0;
+  uint64_t* a7ptr = nullptr;   // device [nlocal]: base of each local rank's temporary
+  LocalBufs a7tmp{};
   SegH2* h2 = nullptr; int nh2 = 0;
   uint32_t* h2_units = nullptr; int nh2_units = 0;
   const unsigned char** h2_pieces = nullptr;
@@ -121,7 +134,9 @@ struct Layout {
 
 struct HostTables {
   std::vector<SegH1> h1, a7;
-  std::vector<uint32_t> h1_units, h1_groups, a7_units, h2_units;
+  std::vector<uint32_t> h1_units, h1_groups, a7_units, a7_groups, h2_units, a7h2_units, a7h2_rankterms;
+  std::vector<SegH2> a7h2;
+  std::vector<uint4> a7h2_off_jobs;
   std::vector<SegH2> h2;
   std::vector<const unsigned char*> a7_pieces, a7_pieces_odd, h2_pieces, h2_pieces_odd;
   std::vector<uint32_t> rankterms;
@@ -156,18 +171,21 @@ static void fill_unit_table(std::vector<uint32_t>& units, uint32_t seg, uint32_t
   for (uint32_t i = 0; i < count; ++i) units.push_back(seg);
 }
 
-static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st, size_t& st_cursor,
-                         size_t& hist_cursor, uint32_t* bflag) {
+// Slot layout and every buffer a peer may address (send, receive, mid, stage,
+// arrival counters): reserved for all buckets FIRST, before anything whose
+// size depends on the rank (a7 workspaces exist on owners only), so that the
+// offsets inside the arena are identical on every rank (fused collectives
+// address a peer's buffer as its arena base + the same offset).
+static void layout_buffers(Layout& L, Bucket& b, HostTables& T) {
   Plan& p = L.p;
   esp_world_s* w = p.w;
   const int n = w->nranks, nl = w->nlocal;
   const bool none = b.kind == ESP_NONE;
-  const bool sparse = is_sparse(b.kind);
   const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
   const bool quant = is_quant(b.kind);
-  const float divisor = b.reduce == ESP_MEAN ? (float)n : 1.0f;
-  const int nslots = (int)p.ctxs.size();
-
+  const bool divis = b.routine == ESP_ALLTOALL_ALLGATHER || b.routine == ESP_GATHER_BROADCAST;
+  const bool p2 = !none && divis && b.proc == 2;   // mid-scheme recompression (a7)
+  b.p2 = p2;
   // ---- slot layout
   b.coff.clear();
   b.slot = 0;
@@ -196,10 +214,9 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     lb = LocalBufs{L.ptr<unsigned char>(off), stride};
     return off;
   };
-  b.fused = fused_allgather_enabled() && !w->sim && n > 1 &&
-            ((dgc && (b.routine == ESP_ALLGATHER || b.routine == ESP_ALLTOALL_ALLGATHER)) ||
-             (quant && (b.routine == ESP_ALLGATHER || b.routine == ESP_ALLTOALL_ALLGATHER ||
-                        b.routine == ESP_GATHER_BROADCAST)));
+  b.fused = fused_allgather_enabled() && !w->sim && n > 1 && (dgc || quant) &&
+            (b.routine == ESP_ALLGATHER || b.routine == ESP_ALLTOALL_ALLGATHER ||
+             (b.routine == ESP_GATHER_BROADCAST && p2));
   // (the fused producers write peers directly; the send buffer still serves esp_compress)
   bufs(b.send, b.P * S);
   // one real rank: every collective is the identity, so the receive buffers
@@ -207,7 +224,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
   const bool solo = !w->sim && n == 1;
   if (solo) {
     b.recv1 = b.send;
-    if (quant && (b.routine == ESP_ALLTOALL_ALLGATHER || b.routine == ESP_GATHER_BROADCAST)) {
+    if (p2) {
       bufs(b.mid, S);
       b.recv2 = b.mid;
     } else {
@@ -222,11 +239,12 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
       b.dst1_par = (size_t)n * S;
       b.dst1_slot = S;
       b.h1_dmode = 2;
-    } else if (b.routine == ESP_ALLTOALL_ALLGATHER && sparse) {
+    } else if (b.routine == ESP_ALLTOALL_ALLGATHER && !p2) {   // process 1
       b.dst1_off = bufs(b.recv2, 2 * (size_t)n * n * S);
       b.dst1_par = (size_t)n * n * S;
       b.dst1_slot = S;
-    } else if (b.routine == ESP_ALLTOALL_ALLGATHER) {   // quantized, process 2
+      b.h1_dmode = 2;
+    } else if (b.routine == ESP_ALLTOALL_ALLGATHER) {   // process 2
       b.dst1_off = bufs(b.recv1, 2 * n * S);
       b.dst1_par = (size_t)n * S;
       b.dst1_slot = S;
@@ -234,7 +252,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
       b.dst2_off = bufs(b.recv2, 2 * n * S);
       b.dst2_par = (size_t)n * S;
       b.dst2_slot = S;
-    } else {                                            // quantized Gather/Broadcast
+    } else {                                            // Gather/Broadcast, process 2
       b.dst1_off = bufs(b.recv1, 2 * n * S);
       b.dst1_par = (size_t)n * S;
       b.dst1_slot = S;
@@ -243,12 +261,12 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
       b.dst2_par = S;
       b.dst2_slot = 0;
     }
-    b.push = push_enabled();
+    b.push = push_enabled() || (p2 && !quant);   // sparse a7 has no peer-store variant
     if (b.push) {
       // jobs and arrivals per call (J jobs per slot)
       const uint64_t J = div_up(S, kPushChunk);
       const bool root = w->rank == 0;
-      if (quant) bufs(b.stage, S);   // a7's local output
+      if (p2) bufs(b.stage, S);   // a7's local output
       // (no self copies: a rank reads its own chunks from the local source)
       const int me = w->rank;
       switch (b.routine) {
@@ -258,7 +276,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           b.target1 = (n - 1) * J;
           break;
         case ESP_ALLTOALL_ALLGATHER:
-          if (sparse) {
+          if (!p2) {
             for (int d = 0; d < n; ++d)
               for (int part = 0; part < b.P && d != me; ++part)
                 add_push(T.push1, (size_t)part * S, (size_t)part * n * S, S, d);
@@ -272,7 +290,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
             b.target2 = (n - 1) * J;
           }
           break;
-        default:   // quantized Gather/Broadcast: to the root, then the root's a7 to all
+        default:   // Gather/Broadcast process 2: to the root, then the root's a7 to all
           if (!root) add_push(T.push1, 0, 0, S, 0);
           if (root)
             for (int d = 1; d < n; ++d) add_push(T.push2, 0, 0, S, d);
@@ -288,17 +306,42 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
       break;
     case ESP_ALLTOALL_ALLGATHER:
       bufs(b.recv1, n * S);
-      if (sparse) bufs(b.recv2, (size_t)n * n * S);
+      if (!p2) bufs(b.recv2, (size_t)n * n * S);
       else { bufs(b.mid, S); bufs(b.recv2, n * S); }
       break;
     case ESP_GATHER_BROADCAST:
       bufs(b.recv1, n * S);
-      if (quant) bufs(b.mid, S);
+      if (p2) bufs(b.mid, S);
       break;
     default:   // ALLREDUCE (randomk / none), RS/AG, Reduce/Broadcast
       if (!w->sim) bufs(b.recv1, S);
       break;
   }
+
+}
+
+static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st, size_t& st_cursor,
+                         size_t& hist_cursor, uint32_t* bflag) {
+  Plan& p = L.p;
+  esp_world_s* w = p.w;
+  const int n = w->nranks, nl = w->nlocal;
+  const bool none = b.kind == ESP_NONE;
+  const bool sparse = is_sparse(b.kind);
+  const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
+  const bool quant = is_quant(b.kind);
+  const float divisor = b.reduce == ESP_MEAN ? (float)n : 1.0f;
+  const int nslots = (int)p.ctxs.size();
+  const bool divis = b.routine == ESP_ALLTOALL_ALLGATHER || b.routine == ESP_GATHER_BROADCAST;
+  const bool p2 = !none && divis && b.proc == 2;   // mid-scheme recompression (a7)
+  b.p2 = p2;
+
+  const size_t S = b.slot;
+  auto bufs = [&](LocalBufs& lb, size_t per_rank) {
+    size_t stride = round_up(per_rank, 256);
+    size_t off = L.reserve(stride * nl);
+    lb = LocalBufs{L.ptr<unsigned char>(off), stride};
+    return off;
+  };
 
   // ---- h1 segments
   const uint32_t h1_first = (uint32_t)T.h1.size();
@@ -321,8 +364,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         // fused destinations: dsts[q] + chunk_off (DGC: every rank q; sign: the
         // partition owner q = part, or every q).  Sparse Alltoall/Allgather lands
         // in recv2's [part][src] layout
-        const size_t part_off = !dgc ? 0 : (b.fused && b.routine == ESP_ALLTOALL_ALLGATHER) ? (size_t)part * n * S
-                                                                                            : (size_t)part * S;
+        const size_t part_off = (b.fused && b.routine == ESP_ALLTOALL_ALLGATHER && !p2) ? (size_t)part * n * S
+                                : dgc ? (size_t)part * S : 0;
         s.chunk_off = (uint32_t)(part_off + b.coff[ti]);
         s.lazy_in = c->lazy ? c->lazy + ((size_t)lr * c->P + part) * 2 : nullptr;
         s.lazy_out = const_cast<float*>(s.lazy_in);
@@ -398,37 +441,37 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     b.nh1_groups = dgc ? (int)g0 : 0;
   }
 
-  // ---- a7 segments (quantized mid-scheme)
+  // ---- a7 segments (process 2, the owner's mid-scheme recompression)
   const uint32_t a7_first = (uint32_t)T.a7.size();
-  if (quant && (b.routine == ESP_ALLTOALL_ALLGATHER || b.routine == ESP_GATHER_BROADCAST)) {
-    uint32_t u0 = 0;
+  const uint32_t a7h2_first = (uint32_t)T.a7h2.size();
+  if (p2) {
+    // sparse: a dense temporary per local rank holds the decode-mean of each
+    // tensor's n chunks (16-byte aligned per tensor); its base is read through
+    // a static device word, like a gradient through the dyn array
+    size_t tmp_elems = 0;
+    for (int t : b.tens) tmp_elems += round_up(b.routine == ESP_ALLTOALL_ALLGATHER ? partition_len(p.ctxs[t]->N, n)
+                                                                                   : p.ctxs[t]->N, 4);
+    if (!quant) {
+      bufs(b.a7tmp, 4 * tmp_elems);
+      b.a7ptr = L.ptr<uint64_t>(L.reserve(8 * (size_t)nl));
+    }
+    uint32_t u0 = 0, g0 = 0, hu0 = 0;
     for (int lr = 0; lr < nl; ++lr) {
       const int j = grank(w, lr);
       if (b.routine == ESP_GATHER_BROADCAST && j != 0) continue;
+      size_t toff_elems = 0;
       for (size_t ti = 0; ti < b.tens.size(); ++ti) {
         esp_ctx_s* c = p.ctxs[b.tens[ti]];
+        const int slot_idx = b.tens[ti];
         uint32_t lo, hi;
         if (b.routine == ESP_ALLTOALL_ALLGATHER) { lo = c->plo[j]; hi = c->phi[j]; }
         else { lo = 0; hi = (uint32_t)c->N; }
         const uint32_t len = hi - lo;
+        const size_t my_off = toff_elems;
+        toff_elems += round_up(b.routine == ESP_ALLTOALL_ALLGATHER ? partition_len(c->N, n) : c->N, 4);
         if (len == 0) continue;
-        SegH1 s{};
-        s.r = c->r2 ? c->r2 + (size_t)lr * c->r2_len : nullptr;
-        s.lazy_in = c->lazy2 ? c->lazy2 + (size_t)lr * 2 : nullptr;
-        s.lazy_out = const_cast<float*>(s.lazy_in);
-        s.chunk = b.fused ? (b.stage.base ? b.stage.at(lr) + b.coff[ti] : nullptr)
-                          : (b.mid.base ? b.mid.at(lr) + b.coff[ti] : nullptr);
-        s.chunk_off = (uint32_t)b.coff[ti];
-        s.n = len;
-        s.kpad = c->kpad;
-        s.nunits = div_up(len, kDgcTile);
-        s.unit0 = u0;
-        u0 += s.nunits;
-        s.ef = c->cfg.error_feedback ? 1 : 0;
-        s.bflag = bflag;
-        s.npieces = (uint32_t)n;
-        s.piece0 = (uint32_t)T.a7_pieces.size();
-        s.divisor = divisor;
+        // the n received chunks of this partition (rank order)
+        const uint32_t piece0 = (uint32_t)T.a7_pieces.size();
         for (int r = 0; r < n; ++r) {
           if (b.push && r == w->rank) {
             // push mode: my own chunk is read where h1 wrote it (rewritten only by
@@ -442,17 +485,91 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           T.a7_pieces_odd.push_back(b.recv1.base && b.fused ? b.recv1.at(lr) + b.dst1_par + (size_t)r * S + b.coff[ti]
                                                             : nullptr);
         }
+        SegH1 s{};
+        s.r = c->r2 ? c->r2 + (size_t)lr * c->r2_len : nullptr;
+        s.lazy_in = c->lazy2 ? c->lazy2 + (size_t)lr * 2 : nullptr;
+        s.lazy_out = const_cast<float*>(s.lazy_in);
+        s.chunk = b.fused ? (b.stage.base ? b.stage.at(lr) + b.coff[ti] : nullptr)
+                          : (b.mid.base ? b.mid.at(lr) + b.coff[ti] : nullptr);
+        s.chunk_off = (uint32_t)b.coff[ti];
+        s.n = len;
+        s.kpad = c->kpad;
+        s.nunits = div_up(len, kDgcTile);
+        s.unit0 = u0;
+        u0 += s.nunits;
+        s.ef = c->cfg.error_feedback ? 1 : 0;
+        s.bflag = bflag ? bflag + 2 : nullptr;   // the a7 launch's own fallback / barrier words
         s.st = L.ptr<SelState>(zero_off_st + st_cursor * sizeof(SelState));
         ++st_cursor;
-        // per-run partial sums, every slot rewritten each call (SignOp::run)
-        s.partial = L.ptr<double>(L.reserve((size_t)div_up(s.n, kRun) * 16));
-        s.pcount = L.ptr<uint32_t>(L.reserve((size_t)div_up(s.n, kRun) * 8));
+        if (quant) {
+          s.npieces = (uint32_t)n;
+          s.piece0 = piece0;
+          s.divisor = divisor;
+          // per-run partial sums, every slot rewritten each call (SignOp::run)
+          s.partial = L.ptr<double>(L.reserve((size_t)div_up(s.n, kRun) * 16));
+          s.pcount = L.ptr<uint32_t>(L.reserve((size_t)div_up(s.n, kRun) * 8));
+        } else {
+          // (i) decode-mean of the n chunks into the temporary (an h2 segment)
+          SegH2 d{};
+          d.optr = b.a7ptr ? b.a7ptr + lr : nullptr;
+          d.ooff = my_off;
+          d.step = p.dyn_dev + nslots + slot_idx;
+          d.hash = c->hash_base;
+          d.part = (uint32_t)(b.routine == ESP_ALLTOALL_ALLGATHER ? j : 0);
+          d.n = len;
+          d.k = k_of(len, c->cfg.ratio);
+          d.kpad = c->kpad;
+          d.npieces = (uint32_t)n;
+          d.piece0 = piece0;
+          d.divisor = divisor;
+          d.nunits = div_up(len, dgc ? kTile : kUnit);
+          d.unit0 = hu0;
+          hu0 += d.nunits;
+          for (int r = 0; r < n; ++r)
+            T.a7h2_rankterms.push_back((b.kind == ESP_RANDOMK && !c->cfg.randomk_shared_indices) ? r + 1 : 0);
+          if (dgc) {
+            d.toff = L.ptr<uint32_t>(L.reserve((size_t)d.npieces * (d.nunits + 1) * 4));
+            for (uint32_t r = 0; r < d.npieces; ++r)
+              for (uint32_t e = 0; e < d.kpad; e += kOffJob)
+                T.a7h2_off_jobs.push_back(make_uint4((uint32_t)(T.a7h2.size() - a7h2_first), r, e, 0));
+          }
+          T.a7h2.push_back(d);
+          fill_unit_table(T.a7h2_units, (uint32_t)(T.a7h2.size() - 1 - a7h2_first), d.nunits);
+          // (ii) the compressor's h1 on the temporary with r = r2 (alpha = 1/n resp. 1)
+          s.gptr = b.a7ptr ? b.a7ptr + lr : nullptr;
+          s.goff = my_off;
+          s.step = p.dyn_dev + nslots + slot_idx;
+          s.k = k_of(len, c->cfg.ratio);
+          const uint32_t nruns = div_up(len, kRun);
+          s.ngroups = div_up(nruns, kRunsPerGroup);
+          s.group0 = g0;
+          s.unsampled = b.kind == ESP_TOPK ? 1 : 0;
+          s.part = d.part;
+          s.hash = b.kind == ESP_RANDOMK ? c->hash_base
+                                         : host_splitmix64(c->tensor_id * 0x100000001b3ull + 0x9e37u + d.part);
+          s.rankterm = (b.kind == ESP_RANDOMK && !c->cfg.randomk_shared_indices) ? (uint32_t)j + 1 : 0;
+          s.ratio = c->cfg.ratio;
+          if (dgc) {
+            s.cand = L.ptr<uint2>(L.reserve((size_t)nruns * kRun * sizeof(uint2)));
+            s.runcnt = L.ptr<uint32_t>(L.reserve((size_t)nruns * 4));
+            s.hrep = dgc_hrep(s.k, s.ngroups);
+            const size_t hbytes = round_up((size_t)dgc_hist_words(s.hrep) * 4, 256);
+            s.gcnt = L.commit ? reinterpret_cast<uint32_t*>(p.zero + hist_cursor + hbytes) : nullptr;
+            s.hist = L.commit ? reinterpret_cast<uint32_t*>(p.zero + hist_cursor) : nullptr;
+            hist_cursor += hbytes + round_up((size_t)s.ngroups * 8, 256);
+            g0 += s.ngroups;
+            fill_unit_table(T.a7_groups, (uint32_t)(T.a7.size() - a7_first), s.ngroups);
+          }
+        }
         T.a7.push_back(s);
         fill_unit_table(T.a7_units, (uint32_t)(T.a7.size() - 1 - a7_first), s.nunits);
       }
     }
     b.na7 = (int)(T.a7.size() - a7_first);
     b.na7_units = (int)u0;
+    b.na7_groups = (int)g0;
+    b.na7h2 = (int)(T.a7h2.size() - a7h2_first);
+    b.na7h2_units = (int)hu0;
   }
 
   // ---- h2 segments
@@ -481,8 +598,12 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.piece0 = (uint32_t)T.h2_pieces.size();
         // fused: the parity-1 copy of the buffer h2 reads follows the parity-0 copy
         const size_t par_stride = b.routine == ESP_ALLGATHER ? b.dst1_par
-                                  : (b.routine == ESP_ALLTOALL_ALLGATHER && sparse) ? b.dst1_par
-                                                                                     : b.dst2_par;
+                                  : (b.routine == ESP_ALLTOALL_ALLGATHER && !p2) ? b.dst1_par
+                                                                                 : b.dst2_par;
+        // process 2: the piece of partition part is the owner's recompression
+        // (Randomk: drawn with rank = owner when indices are not shared)
+        const uint32_t rt2 = (b.kind == ESP_RANDOMK && !c->cfg.randomk_shared_indices)
+                                 ? (uint32_t)(b.routine == ESP_ALLTOALL_ALLGATHER ? part : 0) + 1 : 0;
         auto add_piece = [&](unsigned char* base, size_t off, uint32_t rankterm) {
           T.h2_pieces.push_back(base ? base + off : nullptr);
           T.h2_pieces_odd.push_back(base && b.fused ? base + off + par_stride : nullptr);
@@ -503,9 +624,9 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         switch (b.routine) {
           case ESP_ALLGATHER:
           case ESP_GATHER_BROADCAST:
-            if (b.routine == ESP_GATHER_BROADCAST && quant) {
+            if (b.routine == ESP_GATHER_BROADCAST && p2) {
               if (b.push && me == 0) local_piece(b.stage.at(lr) + b.coff[ti]);
-              else add_piece(b.mid.base ? b.mid.at(lr) : nullptr, b.coff[ti], 0);
+              else add_piece(b.mid.base ? b.mid.at(lr) : nullptr, b.coff[ti], rt2);
               s.npieces = 1;
               s.divisor = 1.0f;
             } else {
@@ -518,7 +639,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
             }
             break;
           case ESP_ALLTOALL_ALLGATHER:
-            if (sparse) {
+            if (!p2) {
               for (int r = 0; r < n; ++r)
                 if (b.push && r == me) local_piece(b.send.at(lr) + (size_t)part * S + b.coff[ti]);
                 else add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr,
@@ -527,7 +648,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
               s.divisor = divisor;
             } else {
               if (b.push && part == me) local_piece(b.stage.at(lr) + b.coff[ti]);
-              else add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr, (size_t)part * S + b.coff[ti], 0);
+              else add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr, (size_t)part * S + b.coff[ti], rt2);
               s.npieces = 1;
               s.divisor = 1.0f;
             }
@@ -576,11 +697,11 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
       b.target2 = (uint64_t)b.nh1;   // sum over owners q of their a7 segments
     }
   }
-  b.h1_calls = none ? 0 : (quant && (b.routine == ESP_ALLTOALL_ALLGATHER || b.routine == ESP_GATHER_BROADCAST) ? 2 : 1);
+  b.h1_calls = none ? 0 : (p2 ? 2 : 1);
   switch (b.routine) {
     case ESP_ALLGATHER: b.h2_pieces_count = n; break;
-    case ESP_ALLTOALL_ALLGATHER: b.h2_pieces_count = sparse ? (uint64_t)n * n : 2ull * n; break;
-    case ESP_GATHER_BROADCAST: b.h2_pieces_count = quant ? n + 1 : n; break;
+    case ESP_ALLTOALL_ALLGATHER: b.h2_pieces_count = !p2 ? (uint64_t)n * n : 2ull * n; break;
+    case ESP_GATHER_BROADCAST: b.h2_pieces_count = p2 ? n + 1 : n; break;
     default: b.h2_pieces_count = none ? 0 : 1; break;
   }
 }
@@ -591,6 +712,8 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
   const int nslots = (int)p.ctxs.size();
   size_t dyn_off = L.reserve(sizeof(uint64_t) * 2 * nslots);
   p.dyn_dev = L.ptr<uint64_t>(dyn_off);
+  std::vector<HostTables> TBs(p.buckets.size());
+  for (size_t i = 0; i < p.buckets.size(); ++i) layout_buffers(L, p.buckets[i], TBs[i]);
   // count segments to size the zero region: SelState per h1/a7 segment + hist per DGC segment
   size_t nst = 0, nhist = 0;
   for (auto& b : p.buckets) {
@@ -610,22 +733,33 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
         }
       }
       nst += (size_t)segs * p.w->nlocal;
-      if (is_quant(b.kind)) {
+      if (mid_scheme(c->cfg, c->routine)) {
         nst += (size_t)p.w->nlocal;   // a7 (upper bound)
+        if (dgc)
+          for (int lr = 0; lr < p.w->nlocal; ++lr) {
+            // the owner's recompression of its partition (A2A) / the whole tensor (root)
+            const int j = grank(p.w, lr);
+            const uint64_t len = c->routine == ESP_ALLTOALL_ALLGATHER ? c->phi[j] - c->plo[j] : (j == 0 ? c->N : 0);
+            if (!len) continue;
+            const uint32_t ng = (uint32_t)div_up(div_up(len, kRun), kRunsPerGroup);
+            nhist += round_up((size_t)dgc_hist_words(dgc_hrep(k_of(len, c->cfg.ratio), ng)) * 4, 256) +
+                     round_up((size_t)ng * 8, 256);
+          }
       }
     }
   }
   const size_t st_bytes = round_up(nst * sizeof(SelState), 256);
-  const size_t flags_bytes = round_up(p.buckets.size() * 8, 256);   // per bucket: fallback flag, grid barrier
+  // per bucket: fallback flag + grid barrier of h1, the same two of a7
+  const size_t flags_bytes = round_up(p.buckets.size() * 16, 256);
   p.zero_bytes = flags_bytes + st_bytes + nhist;
   size_t zero_off = L.reserve(p.zero_bytes);
   p.zero = commit ? p.arena.base + zero_off : nullptr;
   size_t st_cursor = 0, hist_cursor = flags_bytes + st_bytes;
   T = HostTables{};
   for (auto& b : p.buckets) {
-    HostTables TB;
+    HostTables& TB = TBs[&b - p.buckets.data()];
     build_bucket(L, b, TB, zero_off + flags_bytes, st_cursor, hist_cursor,
-                 commit ? reinterpret_cast<uint32_t*>(p.zero) + 2 * (&b - p.buckets.data()) : nullptr);
+                 commit ? reinterpret_cast<uint32_t*>(p.zero) + 4 * (&b - p.buckets.data()) : nullptr);
     // per-bucket device copies of the tables
     auto up = [&](const auto& vec, auto*& dst) {
       using E = typename std::decay<decltype(vec)>::type::value_type;
@@ -639,6 +773,17 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     up(TB.h1_groups, b.h1_groups);
     up(TB.a7, b.a7);
     up(TB.a7_units, b.a7_units);
+    up(TB.a7_groups, b.a7_groups);
+    up(TB.a7h2, b.a7h2);
+    up(TB.a7h2_units, b.a7h2_units);
+    up(TB.a7h2_rankterms, b.a7h2_rankterms);
+    up(TB.a7h2_off_jobs, b.a7h2_off_jobs);
+    b.na7h2_off_jobs = (int)TB.a7h2_off_jobs.size();
+    if (commit && b.a7ptr) {
+      std::vector<uint64_t> bases(p.w->nlocal);
+      for (int lr = 0; lr < p.w->nlocal; ++lr) bases[lr] = (uint64_t)(uintptr_t)b.a7tmp.at(lr);
+      ESP_CUDA(cudaMemcpy(b.a7ptr, bases.data(), 8 * bases.size(), cudaMemcpyHostToDevice));
+    }
     up(TB.a7_pieces, b.a7_pieces);
     if (b.fused) up(TB.a7_pieces_odd, b.a7_pieces_odd);
     up(TB.h2, b.h2);
@@ -654,34 +799,37 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     b.nh2_off_jobs = (int)TB.off_jobs.size();
     if (commit) {
       // pad patterns of every chunk that kernels never touch (R: payload layout)
+      // DGC / TOPK chunks carry the pad pattern (idx 0xFFFFFFFF, val +0) past
+      // entry k: writers only store [0, k)
+      auto pad_slots = [&](const LocalBufs& lb, int lr, size_t nslots_) {
+        if (!lb.base) return;
+        for (size_t q = 0; q < nslots_; ++q)
+          for (size_t ti = 0; ti < b.tens.size(); ++ti) {
+            esp_ctx_s* c = p.ctxs[b.tens[ti]];
+            unsigned char* ch = lb.at(lr) + q * b.slot + b.coff[ti];
+            ESP_CUDA(cudaMemset(ch, 0xFF, 4ull * c->kpad));
+            ESP_CUDA(cudaMemset(ch + 4ull * c->kpad, 0, 4ull * c->kpad));
+          }
+      };
+      const bool dgc_kind = b.kind == ESP_DGC || b.kind == ESP_TOPK;
       for (int lr = 0; lr < p.w->nlocal; ++lr) {
-        if (b.kind == ESP_DGC || b.kind == ESP_TOPK) {
-          for (int part = 0; part < b.P; ++part)
-            for (size_t ti = 0; ti < b.tens.size(); ++ti) {
-              esp_ctx_s* c = p.ctxs[b.tens[ti]];
-              unsigned char* ch = b.send.at(lr) + (size_t)part * b.slot + b.coff[ti];
-              ESP_CUDA(cudaMemset(ch, 0xFF, 4ull * c->kpad));
-              ESP_CUDA(cudaMemset(ch + 4ull * c->kpad, 0, 4ull * c->kpad));
-            }
+        if (dgc_kind) {
+          pad_slots(b.send, lr, b.P);
+          if (b.p2) {
+            pad_slots(b.mid, lr, b.fused ? 2 : 1);   // fused: the G/B broadcast target (two parities)
+            pad_slots(b.stage, lr, 1);
+          }
         } else {
           ESP_CUDA(cudaMemset(b.send.at(lr), 0, b.P * b.slot));
           if (b.mid.base) ESP_CUDA(cudaMemset(b.mid.at(lr), 0, b.slot));
         }
         if (b.fused) {
           const int n = p.w->nranks;
-          if (b.kind == ESP_DGC || b.kind == ESP_TOPK) {
-            // every slot of both parity copies carries the pad pattern; writers
-            // (every rank's DGC write kernel) only ever store entries [0, k)
-            const bool a2a = b.routine == ESP_ALLTOALL_ALLGATHER;
-            unsigned char* buf = a2a ? b.recv2.at(lr) : b.recv1.at(lr);
-            const int copies = 2 * n * (a2a ? n : 1);
-            for (int copy = 0; copy < copies; ++copy)
-              for (size_t ti = 0; ti < b.tens.size(); ++ti) {
-                esp_ctx_s* c = p.ctxs[b.tens[ti]];
-                unsigned char* ch = buf + (size_t)copy * b.slot + b.coff[ti];
-                ESP_CUDA(cudaMemset(ch, 0xFF, 4ull * c->kpad));
-                ESP_CUDA(cudaMemset(ch + 4ull * c->kpad, 0, 4ull * c->kpad));
-              }
+          if (dgc_kind) {
+            // every slot of both parity copies of every receive buffer
+            const bool a2a1 = b.routine == ESP_ALLTOALL_ALLGATHER && !b.p2;
+            pad_slots(b.recv1, lr, 2 * (size_t)n);
+            pad_slots(b.recv2, lr, 2 * (size_t)n * (a2a1 ? n : 1));
           } else {
             if (b.recv1.base) ESP_CUDA(cudaMemset(b.recv1.at(lr), 0, 2ull * n * b.slot));
             if (b.recv2.base) ESP_CUDA(cudaMemset(b.recv2.at(lr), 0, 2ull * n * b.slot));
@@ -757,12 +905,12 @@ Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
   auto p = std::make_unique<Plan>();
   p->w = w;
   p->ctxs = ctxs;
-  // ---- bucketing: group by (kind, routine, reduce) in order of first
+  // ---- bucketing: group by (kind, routine, reduce, process) in order of first
   // appearance, split each class at bucket_elems elements per rank
   const uint64_t cap = w->bucket_elems ? w->bucket_elems : (512ull << 20);
-  std::vector<std::pair<std::tuple<int, int, int>, std::vector<int>>> classes;
+  std::vector<std::pair<std::tuple<int, int, int, int>, std::vector<int>>> classes;
   for (int i = 0; i < (int)ctxs.size(); ++i) {
-    auto key = std::make_tuple(ctxs[i]->cfg.kind, ctxs[i]->routine, ctxs[i]->cfg.reduce);
+    auto key = std::make_tuple(ctxs[i]->cfg.kind, ctxs[i]->routine, ctxs[i]->cfg.reduce, process_of(ctxs[i]->cfg));
     auto it = std::find_if(classes.begin(), classes.end(), [&](auto& c) { return c.first == key; });
     if (it == classes.end()) classes.push_back({key, {i}});
     else it->second.push_back(i);
@@ -772,6 +920,7 @@ Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
     b.kind = std::get<0>(cl.first);
     b.routine = std::get<1>(cl.first);
     b.reduce = std::get<2>(cl.first);
+    b.proc = std::get<3>(cl.first);
     uint64_t elems = 0;
     for (int i : cl.second) {
       if (!b.tens.empty() && elems + ctxs[i]->N > cap) {
@@ -890,9 +1039,37 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
   for (int lr = 0; lr < p.w->nlocal; ++lr) p.w->counters[lr].h1_calls += b.h1_calls * b.tens.size();
 }
 
+// ESP_DEBUG_SYNC=1: synchronize after each phase of the collective layer and
+// name the one that failed (debugging aid; off by default)
+static void dbg(const char* what, cudaStream_t st) {
+  static const bool on = [] {
+    const char* e = getenv("ESP_DEBUG_SYNC");
+    return e && atoi(e) != 0;
+  }();
+  if (!on) return;
+  const cudaError_t e = cudaStreamSynchronize(st);
+  fprintf(stderr, "[esp] %s: %s\n", what, e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+  fflush(stderr);
+}
+
 static void run_mid(Plan& p, Bucket& b, cudaStream_t cs) {
   const int k = b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT;
-  if (b.fused && b.push) {
+  const unsigned char* const* pieces = (b.fused && (b.epoch & 1)) ? b.a7_pieces_odd : b.a7_pieces;
+  if (!is_quant(b.kind)) {
+    // sparse process 2: decode-mean of the n chunks into the temporary, then the
+    // compressor's h1 on it (r = r2), output to stage (push) or mid
+    if (b.kind == ESP_RANDOMK) {
+      launch_h2_randomk(b.a7h2, b.a7h2_units, b.na7h2_units, pieces, b.a7h2_rankterms, cs);
+      dbg("a7 decode (randomk)", cs);
+      launch_randomk_h1(b.a7, b.a7_units, b.na7_units, cs);
+    } else {
+      launch_h2_sparse(b.a7h2, b.a7h2_units, b.na7h2_units, b.a7h2_off_jobs, b.na7h2_off_jobs, pieces,
+                       p.w->nranks, cs);
+      dbg("a7 decode (sparse)", cs);
+      launch_dgc_h1(b.a7, b.na7, b.a7_units, b.na7_units, b.a7_groups, b.na7_groups, cs);
+    }
+    dbg("a7 recompress", cs);
+  } else if (b.fused && b.push) {
     launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, (b.epoch & 1) ? b.a7_pieces_odd : b.a7_pieces, cs);
   } else if (b.fused) {
     // recompressed chunks go straight into every rank's phase-2 buffer
@@ -909,7 +1086,7 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
   esp_world_s* w = p.w;
   const int n = w->nranks;
   const size_t S = b.slot;
-  const bool quant = is_quant(b.kind);
+  const bool quant = b.p2;   // a mid-scheme recompression between the two phases
   if (b.fused) {
     // the payloads were pushed by the producers (every rank's h1, then a7);
     // wait for this call's arrivals (the counters are monotonic across calls).
@@ -918,19 +1095,23 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
     const int par = (int)(b.epoch & 1);
     auto push1 = [&] {
       if (b.push) launch_push(b.push1, b.npush1, b.send.at(0), b.dsts + par * n, b.cnts, cs);
+      dbg("push phase 1", cs);
     };
     auto push2 = [&] {
       if (b.push) launch_push(b.push2, b.npush2, b.stage.at(0), b.dsts2 + par * n, b.cnts2, cs);
+      dbg("push phase 2", cs);
     };
     push1();
     switch (b.routine) {
       case ESP_ALLGATHER:
         count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
         launch_wait_arrivals(b.my_cnt, e1 * b.target1, cs);
+        dbg("wait phase 1", cs);
         break;
       case ESP_ALLTOALL_ALLGATHER:
         count_coll(w, 0, ESP_OP_ALLTOALL, (n - 1) * S, (n - 1) * S);
         launch_wait_arrivals(b.my_cnt, e1 * b.target1, cs);
+        dbg("wait phase 1", cs);
         if (quant) {
           if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
           run_mid(p, b, cs);
@@ -938,15 +1119,17 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
           push2();
           count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
           launch_wait_arrivals(b.my_cnt + 1, e1 * b.target2, cs);
+        dbg("wait phase 2", cs);
         } else {
           count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * n * S, (n - 1) * n * S);
         }
         break;
-      default: {   // quantized Gather/Broadcast
+      default: {   // Gather/Broadcast, process 2
         const bool root = w->rank == 0;
         count_coll(w, 0, ESP_OP_GATHER, root ? 0 : S, root ? (n - 1) * S : 0);
         if (root) {
           launch_wait_arrivals(b.my_cnt, e1 * b.target1, cs);
+        dbg("wait phase 1", cs);
           if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
           run_mid(p, b, cs);
           if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
@@ -954,6 +1137,7 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
         }
         count_coll(w, 0, ESP_OP_BROADCAST, root ? S : 0, root ? 0 : S);
         launch_wait_arrivals(b.my_cnt + 1, e1 * b.target2, cs);
+        dbg("wait phase 2", cs);
         break;
       }
     }

@@ -41,6 +41,14 @@ uint32_t partition_len(uint64_t numel, int nparts) {
 
 bool is_sparse(int kind) { return kind == ESP_RANDOMK || kind == ESP_DGC || kind == ESP_TOPK; }
 bool is_quant(int kind) { return kind == ESP_EFSIGNSGD || kind == ESP_ONEBIT; }
+int process_of(const esp_compressor_cfg_t& cfg) {
+  if (cfg.process == 1 || cfg.process == 2) return cfg.process;
+  return is_sparse(cfg.kind) ? 1 : 2;   // the cost table's choice
+}
+bool mid_scheme(const esp_compressor_cfg_t& cfg, int routine) {
+  return cfg.kind != ESP_NONE && process_of(cfg) == 2 &&
+         (routine == ESP_ALLTOALL_ALLGATHER || routine == ESP_GATHER_BROADCAST);
+}
 
 bool pair_legal(const esp_compressor_cfg_t& cfg, int routine) {
   // routines table; "cannot use Allreduce" P:1073; allreducible P:38/P:56

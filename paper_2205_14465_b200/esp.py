@@ -36,7 +36,8 @@ SYMBOLS = (
 
 class CompressorCfg(C.Structure):
     _fields_ = [("kind", C.c_int32), ("error_feedback", C.c_int32), ("ratio", C.c_double),
-                ("seed", C.c_uint64), ("randomk_shared_indices", C.c_int32), ("reduce", C.c_int32)]
+                ("seed", C.c_uint64), ("randomk_shared_indices", C.c_int32), ("reduce", C.c_int32),
+                ("process", C.c_int32)]
 
 
 class Counters(C.Structure):
@@ -107,9 +108,9 @@ def _check(status):
         raise EspError(status, lib().esp_last_error().decode())
 
 
-def cfg_of(kind="dgc", ratio=0.01, error_feedback=True, seed=0, shared_indices=True, reduce="mean"):
+def cfg_of(kind="dgc", ratio=0.01, error_feedback=True, seed=0, shared_indices=True, reduce="mean", process=0):
     return CompressorCfg(KINDS[kind], int(bool(error_feedback)), float(ratio), int(seed),
-                         int(bool(shared_indices)), REDUCE[reduce])
+                         int(bool(shared_indices)), REDUCE[reduce], int(process))
 
 
 def _ptr(t):
@@ -244,10 +245,10 @@ class Ctx:
     """esp_ctx_t: one tensor's (compressor, ratio, routine) option and EF state."""
 
     def __init__(self, world: World, kind="dgc", routine="allgather", numel=1, tensor_id=0, ratio=0.01,
-                 error_feedback=True, seed=0, shared_indices=True, reduce="mean"):
+                 error_feedback=True, seed=0, shared_indices=True, reduce="mean", process=0):
         self.world = world
         self.kind, self.routine, self.numel = kind, routine, numel
-        self.cfg = cfg_of(kind, ratio, error_feedback, seed, shared_indices, reduce)
+        self.cfg = cfg_of(kind, ratio, error_feedback, seed, shared_indices, reduce, process)
         self.h = C.c_void_p()
         _check(lib().esp_ctx_create(world.h, C.byref(self.cfg), ROUTINES[routine], tensor_id, numel,
                                     C.byref(self.h)))

@@ -52,12 +52,17 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = E.World.nccl(local)
-    pairs = [(k, r) for k in O.KINDS for r in O.ROUTINES if O.legal(O.Cfg(k), r)]
+    pairs = [(k, r, 0) for k in O.KINDS for r in O.ROUTINES if O.legal(O.Cfg(k), r)]
+    # the other process of each divisible routine (R19)
+    pairs += [(k, r, 2 if k in O.SPARSE else 1) for k in ("dgc", "randomk", "efsignsgd")
+              for r in ("alltoall_allgather", "gather_broadcast")]
     N = 30_011
     checked = 0
-    for t, (kind, routine) in enumerate(pairs):
-        ctx = E.Ctx(w, kind, routine, N, tensor_id=t, ratio=0.02)
-        cfg = O.Cfg(kind, 0.02)
+    for t, (kind, routine, proc) in enumerate(pairs):
+        if os.environ.get("ESP_TEST_VERBOSE"):
+            print(f"rank {rank}: {kind}/{routine}/process {proc}", flush=True)
+        ctx = E.Ctx(w, kind, routine, N, tensor_id=t, ratio=0.02, process=proc)
+        cfg = O.Cfg(kind, 0.02, process=proc)
         st = O.new_states(n, N, routine, cfg)
         for s in range(3):
             if kind in O.QUANTIZED and s > 0:   # lock-step: oracle state -> GPU
@@ -77,6 +82,9 @@ def main():
                     np.testing.assert_allclose(rg[0], st[rank].r, rtol=1e-6, atol=1e-30)
                 else:
                     assert np.array_equal(bits(rg[0]), bits(st[rank].r)), f"residual {kind}/{routine}"
+                    if st[rank].r2 is not None:
+                        _, _, r2g = ctx.get_state()
+                        assert np.array_equal(bits(r2g[0, :st[rank].r2.size]), bits(st[rank].r2)), "r2"
             checked += 1
         c = w.counters()
         w.reset_counters()

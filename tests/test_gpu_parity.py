@@ -42,7 +42,7 @@ def check_out(kind, got, ref, where):
 
 
 def run_sim(kind, routine, n, N, steps=3, ratio=0.01, dist="D1", mode="mixed", ef=True,
-            reduce="mean", shared=True, lockstep=None, tensor_id=3, seed=11):
+            reduce="mean", shared=True, lockstep=None, tensor_id=3, seed=11, process=0):
     """Run `steps` syncs in a sim world and compare every rank's output and
     residual with the oracle after each step."""
     E = esp()
@@ -50,8 +50,8 @@ def run_sim(kind, routine, n, N, steps=3, ratio=0.01, dist="D1", mode="mixed", e
         lockstep = kind in O.QUANTIZED
     w = E.World.sim(n, 0)
     ctx = E.Ctx(w, kind, routine, N, tensor_id=tensor_id, ratio=ratio, error_feedback=ef, seed=seed,
-                shared_indices=shared, reduce=reduce)
-    cfg = O.Cfg(kind, ratio, ef, seed, shared, reduce)
+                shared_indices=shared, reduce=reduce, process=process)
+    cfg = O.Cfg(kind, ratio, ef, seed, shared, reduce, process)
     st = O.new_states(n, N, routine, cfg)
     try:
         for s in range(steps):
@@ -80,8 +80,10 @@ def run_sim(kind, routine, n, N, steps=3, ratio=0.01, dist="D1", mode="mixed", e
                         np.testing.assert_allclose(rg[r], st[r].r, rtol=1e-6, atol=1e-30)
                     else:
                         assert np.array_equal(bits(rg[r]), bits(st[r].r)), f"residual rank {r} step {s}"
-                    if st[r].r2 is not None:
+                    if st[r].r2 is not None and kind in O.QUANTIZED:
                         np.testing.assert_allclose(r2g[r, :st[r].r2.size], st[r].r2, rtol=1e-6, atol=1e-30)
+                    elif st[r].r2 is not None:   # sparse second residual: exact
+                        assert np.array_equal(bits(r2g[r, :st[r].r2.size]), bits(st[r].r2)), f"r2 rank {r} step {s}"
         return w
     finally:
         w.destroy()
@@ -291,3 +293,24 @@ def test_abi_errors():
             w2.destroy()
     finally:
         w.destroy()
+
+
+# ---------------------------------------------- both processes of both divisible routines
+XPROC = [(k, r, p) for k in ("dgc", "topk", "randomk", "efsignsgd", "onebit")
+         for r in ("alltoall_allgather", "gather_broadcast") for p in (1, 2)]
+
+
+@pytest.mark.parametrize("kind,routine,process", XPROC)
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_processes(kind, routine, process, n):
+    """Process 1 (forward the chunks) and process 2 (decompress, aggregate and
+    recompress mid-scheme with r2) of Alltoall/Allgather and Gather/Broadcast
+    for every compressor ("the decision tree abstraction covers
+    all of them"; R19) against the oracle, 3 steps."""
+    run_sim(kind, routine, n, 70_001, steps=3, ratio=0.02, process=process, dist="D3" if kind == "dgc" else "D1")
+
+
+@pytest.mark.parametrize("process", [1, 2])
+def test_processes_unshared_randomk(process):
+    run_sim("randomk", "alltoall_allgather", 4, 33_333, steps=2, ratio=0.05, shared=False, process=process)
+    run_sim("randomk", "gather_broadcast", 4, 33_333, steps=2, ratio=0.05, shared=False, process=process)

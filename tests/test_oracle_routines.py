@@ -189,3 +189,85 @@ def test_golden_cost_examples():
         assert O.chunk_bytes(O.Cfg("dgc", e["ratio"]), e["numel"], 1) == e["bytes"]
     for e in g["one_bit_word_bytes"]:
         assert O.chunk_bytes(O.Cfg("efsignsgd"), e["numel"], 1) - 16 == e["bytes"]
+
+
+# ---- the other process of each divisible routine ("the decision
+# tree abstraction covers all of them"; reading R19) -------------------------
+XPROC = [(k, r, p) for k in ("dgc", "topk", "randomk", "efsignsgd", "onebit")
+         for r in ("alltoall_allgather", "gather_broadcast") for p in (1, 2)]
+
+
+@pytest.mark.parametrize("kind,routine,process", XPROC)
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_process_bytes_and_ops_closed_forms(kind, routine, process, n):
+    """Both processes of both divisible routines, for every compressor, move
+    the bytes and apply the h1/h2 counts of the cost table's row for that
+    process (rows "sparse" = process 1, "quantized" = process 2)."""
+    cfg = O.Cfg(kind, 0.01, process=process)
+    N = 4133
+    res = O.sync(routine, cfg, _grads(n, N), O.new_states(n, N, routine, cfg))
+    c = res.counters
+    P = O.nparts_of(routine, n)
+    M = O.chunk_bytes(cfg, N, P) * P
+    row = O.table_row(cfg, routine)
+    assert row.endswith("_sparse" if process == 1 else "_quantized")
+    got = c[0].phases[0][2] + c[1].phases[-1][2] if routine == "gather_broadcast" else c[1].recv
+    assert got == pytest.approx(O.table_comm_bytes(row, M, n), rel=0, abs=n)
+    assert (c[0].h1, c[0].h2) == O.table_ops(row, n)
+    for r in range(n):
+        assert np.array_equal(res.outs[r], res.outs[0])
+
+
+@pytest.mark.parametrize("kind", ["efsignsgd", "onebit", "dgc", "randomk"])
+def test_process1_alltoall_equals_per_partition_allgather(kind):
+    """Process 1 only forwards the first compression's chunks: its output is the
+    rank-order mean of every rank's per-partition decompression -- which is
+    exactly the process-1 Gather/Broadcast of per-partition payloads, and for a
+    single partition (n = 1) decompress(compress(g))."""
+    n, N = 4, 3001
+    cfg = O.Cfg(kind, 0.02, process=1)
+    grads = _grads(n, N)
+    res = O.sync("alltoall_allgather", cfg, grads, O.new_states(n, N, "alltoall_allgather", cfg))
+    parts = O.partitions(N, n)
+    ref = np.zeros(N, np.float32)
+    for p, (lo, hi) in enumerate(parts):
+        dec = []
+        for r in range(n):
+            acc = grads[r][lo:hi].astype(np.float32)   # fresh state: acc = g
+            _, t = O.compress_segment(cfg, acc, part=p, rank=r)
+            dec.append(t)
+        ref[lo:hi] = O.aggregate(dec, "mean", n)
+    assert np.array_equal(res.outs[0], ref)
+
+
+@pytest.mark.parametrize("kind", ["dgc", "topk"])
+@pytest.mark.parametrize("routine", ["alltoall_allgather", "gather_broadcast"])
+def test_sparse_process2_recompression(kind, routine):
+    """Sparse process 2: partition j of the output is the
+    exact top-k_j of q = (rank-order mean of the decoded chunks) + r2 (brute-force
+    stable sort), and the second residual obeys the exact sparse EF identity
+    transmitted + r2_new == q."""
+    n, N = 4, 2500
+    cfg = O.Cfg(kind, 0.03, process=2)
+    grads = _grads(n, N, dist="D3")   # bf16-rounded: heavy ties
+    st = O.new_states(n, N, routine, cfg)
+    res = O.sync(routine, cfg, grads, st)
+    P = O.nparts_of(routine, n)
+    parts = O.partitions(N, P)
+    owners = range(n) if routine == "alltoall_allgather" else [0]
+    for j, (lo, hi) in zip(owners, parts):
+        dec = []
+        for r in range(n):
+            _, t = O.compress_segment(cfg, grads[r][lo:hi].astype(np.float32), part=j, rank=r)
+            dec.append(t)
+        q = O.aggregate(dec, "mean", n)               # r2 was 0 before the step
+        k = O.k_of(hi - lo, cfg.ratio)
+        keys = O.key(q).astype(np.int64)
+        order = sorted(range(hi - lo), key=lambda i: (-keys[i], i))[:k]
+        sel = np.zeros(hi - lo, bool)
+        sel[order] = True
+        out = res.outs[0][lo:hi]
+        assert np.array_equal(out[sel].view(np.uint32), q[sel].view(np.uint32))
+        assert np.all(out[~sel] == 0)
+        r2 = st[j].r2
+        assert np.array_equal((out + r2).view(np.uint32), q.view(np.uint32))
