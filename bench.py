@@ -31,7 +31,7 @@ from synth import shapes  # noqa: E402
 from synth.values import BASE_SEED, gradient  # noqa: E402
 
 WORKLOADS = {
-    # name: (model, per-tensor rule numel -> (kind, ratio, routine))
+    # name: (model, per-tensor rule numel -> (kind, ratio, routine[, extra ctx options]))
     "bert_large_dgc_allgather": ("bert_large", lambda N: ("dgc", 0.001, "allgather")),
     "bert_large_dgc_alltoall": ("bert_large", lambda N: ("dgc", 0.001, "alltoall_allgather")),
     "resnet50_efsignsgd_alltoall": ("resnet50", lambda N: ("efsignsgd", 1.0, "alltoall_allgather")),
@@ -39,7 +39,20 @@ WORKLOADS = {
         "dgc": ("dgc", 0.01, "allgather"),
         "efsignsgd": ("efsignsgd", 1.0, "alltoall_allgather"),
         "none": ("none", 1.0, "allreduce")}[shapes.gpt2_medium_mixed_rule(N)]),
+    # DGC with momentum correction (R20, NEXT-2): 20 B/elem streaming pass
+    "bert_large_dgc_momentum_allgather": ("bert_large", lambda N: ("dgc", 0.001, "allgather", {"momentum": 0.9})),
 }
+
+
+def opt(rule, N):
+    """-> (kind, ratio, routine, extra) of a workload rule."""
+    r = rule(N)
+    return (*r, {}) if len(r) == 3 else r
+
+
+def strategy_str(rule, N):
+    k, ra, ro, ex = opt(rule, N)
+    return "/".join([k, str(ra), ro] + [f"{a}={b}" for a, b in sorted(ex.items())])
 DEFAULT = "bert_large_dgc_allgather"
 E2E_CHUNKS = 4   # tensor groups of the pipelined e2e loop
 
@@ -172,13 +185,13 @@ def run_reference(args):
     grads = {i: [gradient(sizes[i], rank=r, tensor=i) for r in range(n)] for i in idx}
     states = {}
     for i in idx:
-        kind, ratio, routine = rule(sizes[i])
-        states[i] = O.new_states(n, sizes[i], routine, O.Cfg(kind, ratio))
+        kind, ratio, routine, ex = opt(rule, sizes[i])
+        states[i] = O.new_states(n, sizes[i], routine, O.Cfg(kind, ratio, **ex))
 
     def step():
         for i in idx:
-            kind, ratio, routine = rule(sizes[i])
-            O.sync(routine, O.Cfg(kind, ratio), grads[i], states[i], tensor_id=i)
+            kind, ratio, routine, ex = opt(rule, sizes[i])
+            O.sync(routine, O.Cfg(kind, ratio, **ex), grads[i], states[i], tensor_id=i)
 
     for _ in range(args.warmup):
         step()
@@ -212,8 +225,8 @@ def cpu_baseline(args, model, rule, sizes, names, n):
         tot = sum(sizes[i] for i in idx)
     t = 0.0
     for i in idx:
-        kind, ratio, routine = rule(sizes[i])
-        cfg = O.Cfg(kind, ratio)
+        kind, ratio, routine, ex = opt(rule, sizes[i])
+        cfg = O.Cfg(kind, ratio, **ex)
         grads = [gradient(sizes[i], rank=r, tensor=i) for r in range(n)]
         st = O.new_states(n, sizes[i], routine, cfg)
         t0 = time.perf_counter()
@@ -260,8 +273,8 @@ def main():
         world.set_bucket_elems(args.bucket_elems)
     ctxs = []
     for t, N in enumerate(sizes):
-        kind, ratio, routine = rule(N)
-        ctxs.append(E.Ctx(world, kind, routine, N, tensor_id=t, ratio=ratio))
+        kind, ratio, routine, ex = opt(rule, N)
+        ctxs.append(E.Ctx(world, kind, routine, N, tensor_id=t, ratio=ratio, **ex))
 
     # gradients: one flat buffer, tensors at 16-byte aligned offsets
     offs, o = [], 0
@@ -407,7 +420,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": args.workload, "model_shapes": model, "tensors": len(sizes),
                        "params_per_rank": total, "parallelism": f"dp{ws}",
-                       "strategy": sorted({"/".join(map(str, rule(N))) for N in sizes}),
+                       "strategy": sorted({strategy_str(rule, N) for N in sizes}),
                        "median_ms_per_step": t_med, "wall_ms_per_step_incl_input_restore": wall * 1e3 / args.steps,
                        "l2": "inputs 4x params bytes per rank >> 126 MB L2; a D2D input restore (outside the "
                              "per-step events) also evicts L2 between steps"},

@@ -102,6 +102,12 @@ typedef struct {
    * sparse tensors and the second process for quantized tensors").
    * Ignored by the other routines; other values -> ESP_ERR_INVALID_ARG. */
   int32_t process;
+  /* DGC / TOPK momentum correction with momentum factor masking (the DGC
+   * algorithm cited at P:828, reading R20), m in [0, 1):
+   * u <- fl(fl(m*u) + g), v <- fl(v + u), select top-k of v, transmit v[sel],
+   * v[sel] <- 0, u[sel] <- 0.  0 = off (plain error feedback, R4).  Requires
+   * error_feedback = 1 and kind DGC or TOPK, else ESP_ERR_INVALID_ARG. */
+  double momentum;
 } esp_compressor_cfg_t;
 
 typedef struct esp_world_s* esp_world_t;
@@ -178,6 +184,11 @@ esp_status_t esp_ctx_payload_bytes(esp_ctx_t c, size_t* out);
  * host_buf = NULL to query the size.  set_state restores a blob (synchronous). */
 esp_status_t esp_ctx_get_state(esp_ctx_t c, void* host_buf, size_t* nbytes);
 esp_status_t esp_ctx_set_state(esp_ctx_t c, const void* host_buf, size_t nbytes);
+/* The momentum buffer u of a ctx with cfg.momentum != 0: `count` must be
+ * nlocal * numel floats (host memory, rank-major in a sim world).
+ * ESP_ERR_STATE if the ctx has no momentum buffer. */
+esp_status_t esp_ctx_get_momentum(esp_ctx_t c, float* host, size_t count);
+esp_status_t esp_ctx_set_momentum(esp_ctx_t c, const float* host, size_t count);
 
 /* ---- h1 / h2 ----------------------------------------------------------------
  * esp_compress: EF-fused compression of one rank's tensor (every local rank in a

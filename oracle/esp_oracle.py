@@ -57,6 +57,7 @@ class Cfg:
     shared_indices: bool = True   # Randomk (R5)
     reduce: str = "mean"          # R9
     process: int = 0              # Alltoall/Allgather, Gather/Broadcast: 1 or 2 (0: the table's choice, R19)
+    momentum: float = 0.0         # DGC momentum correction factor m (R20); 0 = plain error feedback
 
 
 def process_of(cfg: Cfg) -> int:
@@ -345,9 +346,10 @@ def aggregate(dense_list, reduce: str, n: int) -> np.ndarray:
 # --------------------------------------------------------------------------
 @dataclass
 class RankState:
-    r: np.ndarray                      # EF residual (N)
+    r: np.ndarray                      # EF residual (N); with momentum correction: v (R20)
     r2: np.ndarray | None = None       # second residual of a mid-scheme recompression (R11)
     step: int = 0
+    u: np.ndarray | None = None        # DGC momentum buffer (R20)
 
 
 def new_states(n: int, numel: int, routine: str, cfg: Cfg):
@@ -360,7 +362,8 @@ def new_states(n: int, numel: int, routine: str, cfg: Cfg):
             r2 = np.zeros(hi - lo, np.float32)
         elif p2 and routine == "gather_broadcast" and rank == 0:
             r2 = np.zeros(numel, np.float32)
-        st.append(RankState(np.zeros(numel, np.float32), r2))
+        u = np.zeros(numel, np.float32) if cfg.momentum else None
+        st.append(RankState(np.zeros(numel, np.float32), r2, u=u))
     return st
 
 
@@ -390,7 +393,18 @@ class SyncResult:
 
 
 def _compress_rank(cfg, routine, g, st, tensor_id, rank, n):
-    """h1 with EF on one rank: acc = g + r; per-partition compression; r update."""
+    """h1 with EF on one rank: acc = g + r; per-partition compression; r update.
+
+    Momentum correction (DGC, R20): u = fl(fl(m u) + g) replaces g, the
+    residual r plays DGC's accumulator v (acc = fl(u + v)), and after the
+    selection both v and u are zeroed at the selected indices ("momentum factor
+    masking")."""
+    if cfg.momentum:
+        if cfg.kind not in ("dgc", "topk") or not cfg.error_feedback:
+            raise ValueError("momentum correction needs DGC/TOPK with error feedback")
+        mu = (np.float32(cfg.momentum) * st.u).astype(np.float32)
+        st.u = (mu + g.astype(np.float32)).astype(np.float32)
+        g = st.u
     acc = (g + st.r).astype(np.float32) if cfg.error_feedback else g.astype(np.float32)
     P = nparts_of(routine, n)
     chunks, trans = [], np.zeros_like(acc)
@@ -398,6 +412,8 @@ def _compress_rank(cfg, routine, g, st, tensor_id, rank, n):
         ch, t = compress_segment(cfg, acc[lo:hi], tensor_id=tensor_id, step=st.step, part=p, rank=rank)
         chunks.append(ch)
         trans[lo:hi] = t
+        if cfg.momentum:
+            st.u[lo + ch.idx.astype(np.int64)] = 0.0
     if cfg.error_feedback:
         st.r = residual_update(acc, trans)
     return chunks

@@ -22,6 +22,10 @@ void check_cfg(const esp_compressor_cfg_t* cfg) {
   ESP_REQUIRE(cfg->kind >= ESP_NONE && cfg->kind <= ESP_ONEBIT, ESP_ERR_INVALID_ARG, "bad compressor kind");
   ESP_REQUIRE(cfg->reduce == ESP_MEAN || cfg->reduce == ESP_SUM, ESP_ERR_INVALID_ARG, "bad reduce mode");
   ESP_REQUIRE(cfg->process >= 0 && cfg->process <= 2, ESP_ERR_INVALID_ARG, "process must be 0, 1 or 2");
+  ESP_REQUIRE(cfg->momentum >= 0.0 && cfg->momentum < 1.0, ESP_ERR_INVALID_ARG, "momentum must be in [0, 1)");
+  if (cfg->momentum != 0.0)
+    ESP_REQUIRE((cfg->kind == ESP_DGC || cfg->kind == ESP_TOPK) && cfg->error_feedback, ESP_ERR_INVALID_ARG,
+                "momentum correction needs DGC/TOPK with error feedback (R20)");
   if (is_sparse(cfg->kind))
     ESP_REQUIRE(cfg->ratio > 0.0 && cfg->ratio <= 1.0, ESP_ERR_INVALID_ARG, "ratio must be in (0, 1]");
 }
@@ -73,6 +77,10 @@ esp_status_t esp_ctx_create(esp_world_t w, const esp_compressor_cfg_t* cfg, int 
     ESP_CUDA(cudaMalloc(&c->lazy, sizeof(float) * 2 * c->P * nl));
     ESP_CUDA(cudaMemset(c->lazy, 0, sizeof(float) * 2 * c->P * nl));
   }
+  if (cfg->momentum != 0.0) {
+    ESP_CUDA(cudaMalloc(&c->u, sizeof(float) * numel * nl));
+    ESP_CUDA(cudaMemset(c->u, 0, sizeof(float) * numel * nl));
+  }
   if (mid_scheme(*cfg, routine)) {
     c->r2_len = routine == ESP_ALLTOALL_ALLGATHER ? L : numel;
     ESP_CUDA(cudaMalloc(&c->r2, sizeof(float) * c->r2_len * nl));
@@ -97,6 +105,7 @@ esp_status_t esp_ctx_destroy(esp_ctx_t c) {
   cudaFree(c->lazy);
   cudaFree(c->r2);
   cudaFree(c->lazy2);
+  cudaFree(c->u);
   if (c->dec.d) cudaFree(c->dec.d);
   if (c->dec.h) cudaFreeHost(c->dec.h);
   if (c->dec.ev) cudaEventDestroy(c->dec.ev);
@@ -189,6 +198,28 @@ esp_status_t esp_ctx_set_state(esp_ctx_t c, const void* host_buf, size_t nbytes)
   if (c->lazy) ESP_CUDA(cudaMemset(c->lazy, 0, sizeof(float) * 2 * c->P * nl));
   if (c->lazy2) ESP_CUDA(cudaMemset(c->lazy2, 0, sizeof(float) * 2 * nl));
   c->step = h.step;
+  ESP_API_END
+}
+
+esp_status_t esp_ctx_get_momentum(esp_ctx_t c, float* host, size_t count) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(c && host, ESP_ERR_INVALID_ARG, "null argument");
+  ESP_REQUIRE(c->u, ESP_ERR_STATE, "ctx has no momentum buffer (cfg.momentum == 0)");
+  ESP_REQUIRE(count == c->N * (size_t)c->w->nlocal, ESP_ERR_INVALID_ARG, "count must be nlocal * numel");
+  ESP_CUDA(cudaSetDevice(c->w->dev));
+  ESP_CUDA(cudaDeviceSynchronize());
+  ESP_CUDA(cudaMemcpy(host, c->u, 4 * count, cudaMemcpyDeviceToHost));
+  ESP_API_END
+}
+
+esp_status_t esp_ctx_set_momentum(esp_ctx_t c, const float* host, size_t count) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(c && host, ESP_ERR_INVALID_ARG, "null argument");
+  ESP_REQUIRE(c->u, ESP_ERR_STATE, "ctx has no momentum buffer (cfg.momentum == 0)");
+  ESP_REQUIRE(count == c->N * (size_t)c->w->nlocal, ESP_ERR_INVALID_ARG, "count must be nlocal * numel");
+  ESP_CUDA(cudaSetDevice(c->w->dev));
+  ESP_CUDA(cudaDeviceSynchronize());
+  ESP_CUDA(cudaMemcpy(c->u, host, 4 * count, cudaMemcpyHostToDevice));
   ESP_API_END
 }
 

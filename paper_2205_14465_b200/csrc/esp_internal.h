@@ -118,6 +118,7 @@ struct esp_ctx_s {
   float* lazy = nullptr;             // nlocal * P * 2
   float* r2 = nullptr;               // nlocal * r2_len   (second residual, R11)
   float* lazy2 = nullptr;            // nlocal * 2
+  float* u = nullptr;                // nlocal * N: DGC momentum buffer (cfg.momentum != 0)
   uint64_t r2_len = 0;
   uint64_t step = 0;
   uint64_t hash_base = 0;            // mix(mix(seed) ^ tensor_id)

@@ -18,7 +18,7 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
                    const uint32_t* group_seg, int ngroups, cudaStream_t st,
                    cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr,
                    unsigned char* const* dsts = nullptr, unsigned long long* const* cnts = nullptr,
-                   int ndst = 0);
+                   int ndst = 0, bool mom = false);
 // block the stream until *cnt >= target (arrivals of a fused Allgather); traps
 // after ~10 s so that a missing peer becomes an error, not a hang
 void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, cudaStream_t st);

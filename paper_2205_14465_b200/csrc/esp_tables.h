@@ -88,6 +88,10 @@ struct SegH1 {
   uint32_t piece0;       // index into the piece-pointer array
   float divisor;
   uint32_t hrep;         // DGC: replicas of the round-2/3 histograms (spread same-bin atomics)
+  // DGC momentum correction (R20): u buffer of the segment (nullptr = off), factor m
+  float* mom;
+  float mcoef;
+  uint32_t pad1_;
 };
 
 // DGC histogram words of a segment: 2048 (stream) + 2048 (fallback) + 1024 x hrep

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
   {
     // all 2 x 16 loads of a thread are issued before any is consumed (latency-bound kernel)
     constexpr int kPer = kSample / kThreads;
-    float gv[kPer], rv[kPer];
+    float gv[kPer], rv[kPer], uv[kPer];
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       const uint32_t j = threadIdx.x + q * kThreads;
@@ -116,6 +116,11 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
       }
       gv[q] = j < s ? __ldg(g + pos) : 0.f;
       rv[q] = (j < s && S.ef) ? S.r[pos] : 0.f;
+      uv[q] = (j < s && S.mom) ? S.mom[pos] : 0.f;
+    }
+    if (S.mom) {   // momentum correction (R20): the candidate is fl(fl(m u) + g) + v
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) gv[q] = __fadd_rn(__fmul_rn(S.mcoef, uv[q]), gv[q]);
     }
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
@@ -246,10 +251,17 @@ struct StreamSmem {   // followed (128-byte aligned) by `ns` stages of {g[kDgcTi
 };
 constexpr size_t kStreamHdr = (sizeof(StreamSmem) + 127) / 128 * 128;
 constexpr size_t kStageBytes = 2 * kDgcTile * sizeof(float);
+// momentum correction (R20): a third tile per stage holds u
+constexpr size_t kStageBytesMom = 3 * kDgcTile * sizeof(float);
+constexpr int kMaxStagesMom = 4;   // 4 x 48 KB + header
+template <bool MOM = false>
 __device__ __forceinline__ float* stage_g(unsigned char* smem, int s) {
-  return reinterpret_cast<float*>(smem + kStreamHdr + (size_t)s * kStageBytes);
+  return reinterpret_cast<float*>(smem + kStreamHdr + (size_t)s * (MOM ? kStageBytesMom : kStageBytes));
 }
-__device__ __forceinline__ float* stage_r(unsigned char* smem, int s) { return stage_g(smem, s) + kDgcTile; }
+template <bool MOM = false>
+__device__ __forceinline__ float* stage_r(unsigned char* smem, int s) { return stage_g<MOM>(smem, s) + kDgcTile; }
+template <bool MOM = false>
+__device__ __forceinline__ float* stage_u(unsigned char* smem, int s) { return stage_g<MOM>(smem, s) + 2 * kDgcTile; }
 
 // segment bookkeeping by the 256 consumer threads of a CTA that has finished its
 // share (`units` units) of segment S: flush the private histogram, add the
@@ -342,7 +354,7 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& s
 // by a group follows that group's own previous use of it, which is what makes
 // the one-bit phase parity of the full barrier unambiguous (with ns % NCG != 0
 // a warp could pass a parity test one fill early).
-template <int NCG>
+template <int NCG, bool MOM = false>
 __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(const SegH1* __restrict__ segs,
                                                                             const uint32_t* __restrict__ unit_seg,
                                                                             uint32_t nunits, int variant, int ns) {
@@ -370,6 +382,7 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
       uint32_t cur = 0xFFFFFFFFu, unit0 = 0, n = 0;
       const float* gseg = nullptr;
       const float* rseg = nullptr;
+      const float* useg = nullptr;
       bool ef = false;
       uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
       int stage = 0;
@@ -385,6 +398,7 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
           n = S.n;
           gseg = seg_g(S);
           rseg = S.r;
+          useg = S.mom;
           ef = S.ef != 0;
         }
         if (wrapped) mbar_wait(&sm.empty[stage], phase ^ 1);
@@ -392,11 +406,13 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
         const uint32_t len = min((uint32_t)kDgcTile, n - start);
         const float* g = gseg + start;
         const float* r = rseg + start;
+        const float* um = useg + start;
         const uint32_t bytes = (len * 4) & ~15u;
-        if (bytes && al16(g) && (!ef || al16(r))) {
-          mbar_arrive_expect_tx(&sm.full[stage], bytes * (ef ? 2 : 1));
-          tma_load_1d(stage_g(smem_raw, stage), g, bytes, &sm.full[stage], pol);
-          if (ef) tma_load_1d(stage_r(smem_raw, stage), r, bytes, &sm.full[stage], pol);
+        if (bytes && al16(g) && (!ef || al16(r)) && (!MOM || al16(um))) {
+          mbar_arrive_expect_tx(&sm.full[stage], bytes * ((ef ? 2 : 1) + (MOM ? 1 : 0)));
+          tma_load_1d(stage_g<MOM>(smem_raw, stage), g, bytes, &sm.full[stage], pol);
+          if (ef) tma_load_1d(stage_r<MOM>(smem_raw, stage), r, bytes, &sm.full[stage], pol);
+          if (MOM) tma_load_1d(stage_u<MOM>(smem_raw, stage), um, bytes, &sm.full[stage], pol);
         } else {
           mbar_arrive(&sm.full[stage]);
         }
@@ -441,15 +457,26 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
     const uint32_t lbase = (warp & 7) * kRun;      // tile-relative
     const uint32_t base = start + lbase;           // segment-relative
     // fast path: a whole tile in shared memory (aligned, EF on, inside the segment)
-    const bool full = S.ef && start + kDgcTile <= n && al16(g + start) && al16(S.r + start);
+    const bool full = S.ef && start + kDgcTile <= n && al16(g + start) && al16(S.r + start) &&
+                      (!MOM || al16(S.mom + start));
     float4 av[kNJ];
+    float4 um[MOM ? kNJ : 1];   // MOM: u' = fl(fl(m u) + g), stored after the stage is released
     mbar_wait(&sm.full[stage], phase);
     if (full) {
-      const float* sg = stage_g(smem_raw, stage) + lbase + lane * 4;
-      const float* sr = stage_r(smem_raw, stage) + lbase + lane * 4;
+      const float* sg = stage_g<MOM>(smem_raw, stage) + lbase + lane * 4;
+      const float* sr = stage_r<MOM>(smem_raw, stage) + lbase + lane * 4;
 #pragma unroll
       for (int j = 0; j < kNJ; ++j) {
-        const float4 gv = lds4(sg + j * 128), rv = lds4(sr + j * 128);
+        float4 gv = lds4(sg + j * 128);
+        const float4 rv = lds4(sr + j * 128);
+        if (MOM) {
+          const float4 uv = lds4(stage_u<MOM>(smem_raw, stage) + lbase + lane * 4 + j * 128);
+          gv.x = __fadd_rn(__fmul_rn(S.mcoef, uv.x), gv.x);
+          gv.y = __fadd_rn(__fmul_rn(S.mcoef, uv.y), gv.y);
+          gv.z = __fadd_rn(__fmul_rn(S.mcoef, uv.z), gv.z);
+          gv.w = __fadd_rn(__fmul_rn(S.mcoef, uv.w), gv.w);
+          um[MOM ? j : 0] = gv;
+        }
         av[j].x = __fadd_rn(gv.x, rv.x);
         av[j].y = __fadd_rn(gv.y, rv.y);
         av[j].z = __fadd_rn(gv.z, rv.z);
@@ -458,19 +485,34 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
     } else {
       const uint32_t len = min((uint32_t)kDgcTile, n - start);
       const uint32_t bytes = (len * 4) & ~15u;
-      const bool tma = bytes && al16(g + start) && (!S.ef || al16(S.r + start));
+      const bool tma = bytes && al16(g + start) && (!S.ef || al16(S.r + start)) && (!MOM || al16(S.mom + start));
 #pragma unroll
       for (int j = 0; j < kNJ; ++j) {
         const uint32_t l = lbase + j * 128 + lane * 4;
         const uint32_t e = start + l;
         float4 gv, rv;
         if (tma && l + 4 <= bytes / 4) {
-          gv = lds4(stage_g(smem_raw, stage) + l);
-          rv = S.ef ? lds4(stage_r(smem_raw, stage) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
+          gv = lds4(stage_g<MOM>(smem_raw, stage) + l);
+          rv = S.ef ? lds4(stage_r<MOM>(smem_raw, stage) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (MOM) {
+            const float4 uv = lds4(stage_u<MOM>(smem_raw, stage) + l);
+            gv.x = __fadd_rn(__fmul_rn(S.mcoef, uv.x), gv.x);
+            gv.y = __fadd_rn(__fmul_rn(S.mcoef, uv.y), gv.y);
+            gv.z = __fadd_rn(__fmul_rn(S.mcoef, uv.z), gv.z);
+            gv.w = __fadd_rn(__fmul_rn(S.mcoef, uv.w), gv.w);
+          }
         } else {
           gv = load4_guard(g, e, n);
           rv = S.ef ? load4_guard(S.r, e, n) : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (MOM) {
+            const float4 uv = load4_guard(S.mom, e, n);
+            gv.x = __fadd_rn(__fmul_rn(S.mcoef, uv.x), gv.x);
+            gv.y = __fadd_rn(__fmul_rn(S.mcoef, uv.y), gv.y);
+            gv.z = __fadd_rn(__fmul_rn(S.mcoef, uv.z), gv.z);
+            gv.w = __fadd_rn(__fmul_rn(S.mcoef, uv.w), gv.w);
+          }
         }
+        if (MOM) um[MOM ? j : 0] = gv;
         if (S.ef) {
           av[j].x = __fadd_rn(gv.x, rv.x);
           av[j].y = __fadd_rn(gv.y, rv.y);
@@ -493,9 +535,18 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
         float* rp = S.r + base + lane * 4;
 #pragma unroll
         for (int j = 0; j < kNJ; ++j) st4(rp + j * 128, av[j]);
+        if (MOM) {
+          float* up = S.mom + base + lane * 4;
+#pragma unroll
+          for (int j = 0; j < kNJ; ++j) st4(up + j * 128, um[MOM ? j : 0]);
+        }
       } else if (S.ef) {
 #pragma unroll
         for (int j = 0; j < kNJ; ++j) store4_guard(S.r, base + j * 128 + lane * 4, n, av[j]);
+        if (MOM) {
+#pragma unroll
+          for (int j = 0; j < kNJ; ++j) store4_guard(S.mom, base + j * 128 + lane * 4, n, um[MOM ? j : 0]);
+        }
       }
       const uint32_t run = base / kRun;
       if (S.unsampled) {
@@ -928,6 +979,7 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __r
           out_val[pos] = __uint_as_float(c.y);
         }
         if (S.ef) S.r[c.x] = 0.0f;
+        if (S.mom) S.mom[c.x] = 0.0f;   // momentum factor masking (R20)
       }
       tie_run += __popc(tb);
       sel_run += __popc(sb);
@@ -1007,7 +1059,7 @@ static void debug_sync(const char* what, cudaStream_t st) {
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
                    cudaEvent_t probe1, unsigned char* const* dsts, unsigned long long* const* cnts,
-                   int ndst) {
+                   int ndst, bool mom) {
   if (nsegs == 0) return;
   static const bool attr_set = [] {
     const int bytes = (int)(kStreamHdr + kMaxStages * kStageBytes);
@@ -1016,7 +1068,13 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
            cudaFuncSetAttribute(dgc_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
                cudaSuccess &&
            cudaFuncSetAttribute(dgc_stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
-               cudaSuccess;
+               cudaSuccess &&
+           cudaFuncSetAttribute(dgc_stream_kernel<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kStreamHdr + kMaxStagesMom * kStageBytesMom)) == cudaSuccess &&
+           cudaFuncSetAttribute(dgc_stream_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kStreamHdr + kMaxStagesMom * kStageBytesMom)) == cudaSuccess &&
+           cudaFuncSetAttribute(dgc_stream_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kStreamHdr + kMaxStagesMom * kStageBytesMom)) == cudaSuccess;
   }();
   (void)attr_set;
   num_sms();
@@ -1033,7 +1091,24 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
   if (probe0) cudaEventRecord(probe0, st);
   {
     const int grid = nunits < g_num_sms ? nunits : g_num_sms;
-    if (variant & 4)   // one consumer group (A/B experiments)
+    // momentum correction: three tiles per stage (R20); ESP_MOM_GROUPS = consumer
+    // groups (stages: 3 for three groups, else 4)
+    static const int mom_groups = [] {
+      const char* e = getenv("ESP_MOM_GROUPS");
+      const int g = e ? atoi(e) : 2;
+      return g < 1 ? 1 : (g > 3 ? 3 : g);
+    }();
+    const size_t mom_smem = kStreamHdr + kMaxStagesMom * kStageBytesMom;
+    if (mom && mom_groups == 3)
+      dgc_stream_kernel<3, true><<<grid, 3 * kThreads + 32, mom_smem, st>>>(segs, unit_seg, (uint32_t)nunits,
+                                                                            variant, 3);
+    else if (mom && mom_groups == 2)
+      dgc_stream_kernel<2, true><<<grid, 2 * kThreads + 32, mom_smem, st>>>(segs, unit_seg, (uint32_t)nunits,
+                                                                            variant, 4);
+    else if (mom)
+      dgc_stream_kernel<1, true><<<grid, kThreads + 32, mom_smem, st>>>(segs, unit_seg, (uint32_t)nunits,
+                                                                        variant, 4);
+    else if (variant & 4)   // one consumer group (A/B experiments)
       dgc_stream_kernel<1><<<grid, kThreads + 32, kStreamHdr + stages * kStageBytes, st>>>(
           segs, unit_seg, (uint32_t)nunits, variant, stages);
     else if (variant & 8) {   // two groups

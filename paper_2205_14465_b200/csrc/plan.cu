@@ -18,6 +18,7 @@ namespace esp {
 struct Bucket {
   int kind = 0, routine = 0, reduce = 0;
   int proc = 1;                // process of a divisible routine (R19)
+  double momentum = 0.0;       // DGC momentum correction factor (R20)
   bool p2 = false;             // mid-scheme decompress-aggregate-recompress (a7)
   std::vector<int> tens;      // indices into Plan::ctxs
   int P = 1;
@@ -386,6 +387,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.part = (uint32_t)part;
         s.rankterm = (b.kind == ESP_RANDOMK && !c->cfg.randomk_shared_indices) ? grank(w, lr) + 1 : 0;
         s.ratio = c->cfg.ratio;
+        s.mom = c->u ? c->u + (size_t)lr * c->N + lo : nullptr;
+        s.mcoef = (float)c->cfg.momentum;
         // per-segment state (zeroed every call)
         size_t st_off = zero_off_st + st_cursor * sizeof(SelState);
         ++st_cursor;
@@ -424,6 +427,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     const bool ef = p.ctxs[b.tens[0]]->cfg.error_feedback != 0;
     if (none) b.h1_bytes = 8 * elems;
     else if (quant) b.h1_bytes = (ef ? 12 : 4) * elems + elems / 8;
+    else if (b.momentum != 0.0) b.h1_bytes = 20 * elems;   // + read u, write u (R20)
     else b.h1_bytes = (ef ? 12 : 4) * elems;
   }
   // unit/group tables refer to segment indices local to the bucket; the
@@ -908,9 +912,10 @@ Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
   // ---- bucketing: group by (kind, routine, reduce, process) in order of first
   // appearance, split each class at bucket_elems elements per rank
   const uint64_t cap = w->bucket_elems ? w->bucket_elems : (512ull << 20);
-  std::vector<std::pair<std::tuple<int, int, int, int>, std::vector<int>>> classes;
+  std::vector<std::pair<std::tuple<int, int, int, int, double>, std::vector<int>>> classes;
   for (int i = 0; i < (int)ctxs.size(); ++i) {
-    auto key = std::make_tuple(ctxs[i]->cfg.kind, ctxs[i]->routine, ctxs[i]->cfg.reduce, process_of(ctxs[i]->cfg));
+    auto key = std::make_tuple(ctxs[i]->cfg.kind, ctxs[i]->routine, ctxs[i]->cfg.reduce, process_of(ctxs[i]->cfg),
+                               ctxs[i]->cfg.momentum);
     auto it = std::find_if(classes.begin(), classes.end(), [&](auto& c) { return c.first == key; });
     if (it == classes.end()) classes.push_back({key, {i}});
     else it->second.push_back(i);
@@ -921,6 +926,7 @@ Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
     b.routine = std::get<1>(cl.first);
     b.reduce = std::get<2>(cl.first);
     b.proc = std::get<3>(cl.first);
+    b.momentum = std::get<4>(cl.first);
     uint64_t elems = 0;
     for (int i : cl.second) {
       if (!b.tens.empty() && elems + ctxs[i]->N > cap) {
@@ -1017,9 +1023,10 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
       if (fused) {
         const int n = p.w->nranks;
         launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1,
-                      b.dsts + (b.epoch & 1) * n, b.cnts, n);
+                      b.dsts + (b.epoch & 1) * n, b.cnts, n, b.momentum != 0.0);
       } else {
-        launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1);
+        launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1, nullptr, nullptr,
+                      0, b.momentum != 0.0);
       }
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;

@@ -28,7 +28,7 @@ SYMBOLS = (
     "esp_world_reset_counters", "esp_world_set_timing", "esp_last_timing", "esp_world_set_bucket_elems",
     "esp_world_set_probe", "esp_probe_read",
     "esp_ctx_create", "esp_ctx_destroy", "esp_ctx_payload_bytes", "esp_ctx_get_state",
-    "esp_ctx_set_state", "esp_compress", "esp_decompress", "esp_sync", "esp_sync_many",
+    "esp_ctx_set_state", "esp_ctx_get_momentum", "esp_ctx_set_momentum", "esp_compress", "esp_decompress", "esp_sync", "esp_sync_many",
     "esp_compressed_bytes", "esp_wire_bytes", "esp_model_time", "esp_status_string",
     "esp_last_error", "esp_launch_count", "esp_version",
 )
@@ -37,7 +37,7 @@ SYMBOLS = (
 class CompressorCfg(C.Structure):
     _fields_ = [("kind", C.c_int32), ("error_feedback", C.c_int32), ("ratio", C.c_double),
                 ("seed", C.c_uint64), ("randomk_shared_indices", C.c_int32), ("reduce", C.c_int32),
-                ("process", C.c_int32)]
+                ("process", C.c_int32), ("momentum", C.c_double)]
 
 
 class Counters(C.Structure):
@@ -81,6 +81,7 @@ def lib():
             "esp_ctx_create": [vp, C.POINTER(CompressorCfg), i32, u64, sz, C.POINTER(vp)],
             "esp_ctx_destroy": [vp], "esp_ctx_payload_bytes": [vp, C.POINTER(sz)],
             "esp_ctx_get_state": [vp, vp, C.POINTER(sz)], "esp_ctx_set_state": [vp, vp, sz],
+            "esp_ctx_get_momentum": [vp, vp, sz], "esp_ctx_set_momentum": [vp, vp, sz],
             "esp_compress": [vp, vp, vp, vp], "esp_decompress": [vp, C.POINTER(vp), i32, vp, vp],
             "esp_sync": [vp, vp, vp, vp], "esp_sync_many": [vp, C.POINTER(vp), C.POINTER(vp), i32, vp],
             "esp_compressed_bytes": [C.POINTER(CompressorCfg), sz, i32, C.POINTER(sz)],
@@ -108,9 +109,10 @@ def _check(status):
         raise EspError(status, lib().esp_last_error().decode())
 
 
-def cfg_of(kind="dgc", ratio=0.01, error_feedback=True, seed=0, shared_indices=True, reduce="mean", process=0):
+def cfg_of(kind="dgc", ratio=0.01, error_feedback=True, seed=0, shared_indices=True, reduce="mean", process=0,
+           momentum=0.0):
     return CompressorCfg(KINDS[kind], int(bool(error_feedback)), float(ratio), int(seed),
-                         int(bool(shared_indices)), REDUCE[reduce], int(process))
+                         int(bool(shared_indices)), REDUCE[reduce], int(process), float(momentum))
 
 
 def _ptr(t):
@@ -245,10 +247,10 @@ class Ctx:
     """esp_ctx_t: one tensor's (compressor, ratio, routine) option and EF state."""
 
     def __init__(self, world: World, kind="dgc", routine="allgather", numel=1, tensor_id=0, ratio=0.01,
-                 error_feedback=True, seed=0, shared_indices=True, reduce="mean", process=0):
+                 error_feedback=True, seed=0, shared_indices=True, reduce="mean", process=0, momentum=0.0):
         self.world = world
         self.kind, self.routine, self.numel = kind, routine, numel
-        self.cfg = cfg_of(kind, ratio, error_feedback, seed, shared_indices, reduce, process)
+        self.cfg = cfg_of(kind, ratio, error_feedback, seed, shared_indices, reduce, process, momentum)
         self.h = C.c_void_p()
         _check(lib().esp_ctx_create(world.h, C.byref(self.cfg), ROUTINES[routine], tensor_id, numel,
                                     C.byref(self.h)))
@@ -274,6 +276,19 @@ class Ctx:
         step, numel, r2_len, nl = (int(x) for x in hdr[1:5])
         body = np.frombuffer(bytes(buf[40:]), np.float32).reshape(nl, numel + r2_len)
         return step, body[:, :numel].copy(), body[:, numel:].copy()
+
+    def get_momentum(self):
+        """-> the DGC momentum buffer u [nlocal, numel] fp32 (momentum != 0 only)."""
+        import numpy as np
+        nl = self.world.nlocal
+        out = np.zeros((nl, self.numel), np.float32)
+        _check(lib().esp_ctx_get_momentum(self.h, out.ctypes.data_as(C.c_void_p), out.size))
+        return out
+
+    def set_momentum(self, u):
+        import numpy as np
+        u = np.ascontiguousarray(np.asarray(u, np.float32).reshape(self.world.nlocal, self.numel))
+        _check(lib().esp_ctx_set_momentum(self.h, u.ctypes.data_as(C.c_void_p), u.size))
 
     def set_state(self, step, r, r2=None):
         import numpy as np

@@ -314,3 +314,50 @@ def test_processes(kind, routine, process, n):
 def test_processes_unshared_randomk(process):
     run_sim("randomk", "alltoall_allgather", 4, 33_333, steps=2, ratio=0.05, shared=False, process=process)
     run_sim("randomk", "gather_broadcast", 4, 33_333, steps=2, ratio=0.05, shared=False, process=process)
+
+
+# ---------------------------------------------- DGC momentum correction (R20)
+@pytest.mark.parametrize("kind", ["dgc", "topk"])
+@pytest.mark.parametrize("routine,n", [("allgather", 2), ("allgather", 4), ("alltoall_allgather", 4),
+                                       ("gather_broadcast", 2)])
+def test_momentum_correction(kind, routine, n):
+    """u = fl(fl(m u) + g), v = fl(v + u), top-k of v, v[sel] = u[sel] = 0:
+    outputs, v (the residual) and u bit-exact against the oracle over 4 steps."""
+    E = esp()
+    N, m = 70_001, 0.9
+    w = E.World.sim(n, 0)
+    try:
+        ctx = E.Ctx(w, kind, routine, N, tensor_id=9, ratio=0.01, momentum=m)
+        cfg = O.Cfg(kind, 0.01, momentum=m)
+        st = O.new_states(n, N, routine, cfg)
+        for s in range(4):
+            grads = [gradient(N, step=s, rank=r, tensor=9, dist="D3") for r in range(n)]
+            ref = O.sync(routine, cfg, grads, st, tensor_id=9)
+            g = upload(grads)
+            E.esp_sync(w, ctx, g)
+            torch.cuda.synchronize()
+            out = g.cpu().numpy().reshape(n, N)
+            _, rg, _ = ctx.get_state()
+            ug = ctx.get_momentum()
+            for r in range(n):
+                check_out(kind, out[r], ref.outs[r], f"momentum {kind}/{routine} step {s} rank {r}")
+                assert np.array_equal(bits(rg[r]), bits(st[r].r)), f"v rank {r} step {s}"
+                assert np.array_equal(bits(ug[r]), bits(st[r].u)), f"u rank {r} step {s}"
+    finally:
+        w.destroy()
+
+
+def test_momentum_abi_errors():
+    E = esp()
+    w = E.World.sim(2, 0)
+    try:
+        for kw in (dict(kind="randomk"), dict(kind="efsignsgd"), dict(kind="dgc", error_feedback=False)):
+            with pytest.raises(E.EspError):
+                E.Ctx(w, routine="allgather", numel=100, momentum=0.9, **kw)
+        with pytest.raises(E.EspError):
+            E.Ctx(w, "dgc", "allgather", 100, momentum=1.0)
+        c = E.Ctx(w, "dgc", "allgather", 100)
+        with pytest.raises(E.EspError):
+            c.get_momentum()
+    finally:
+        w.destroy()

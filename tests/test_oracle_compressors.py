@@ -217,3 +217,68 @@ def test_partitions():
             parts = O.partitions(N, n)
             assert parts[0][0] == 0 and parts[-1][1] == N
             assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+
+
+# ---- DGC momentum correction (R20) -----------------------------------------
+def test_momentum_zero_is_plain_dgc():
+    N, n = 20_000, 2
+    a, b = O.Cfg("dgc", 0.01), O.Cfg("dgc", 0.01, momentum=0.0)
+    sa, sb = O.new_states(n, N, "allgather", a), O.new_states(n, N, "allgather", b)
+    for s in range(3):
+        grads = [gradient(N, step=s, rank=r) for r in range(n)]
+        ra = O.sync("allgather", a, grads, sa)
+        rb = O.sync("allgather", b, grads, sb)
+        assert np.array_equal(ra.outs[0], rb.outs[0])
+
+
+def test_momentum_geometric_series_closed_form():
+    """A coordinate that is never selected, under a constant gradient c, obeys
+    u_t = c (1 - m^(t+1)) / (1 - m) and v_t = sum_{s<=t} u_s.  With m = 1/2 and
+    c = 2^-20 every term is exact in fp32, so the oracle must match exactly;
+    a dominant spike keeps the coordinate unselected (k = 1)."""
+    N, m, c, T = 64, 0.5, 2.0 ** -20, 12
+    cfg = O.Cfg("dgc", 1 / 64, momentum=m)   # k = 1
+    st = O.new_states(1, N, "allgather", cfg)
+    v = 0.0
+    for t in range(T):
+        g = np.full(N, c, np.float32)
+        g[0] = 1.0                      # selected every step (largest by far)
+        O.sync("allgather", cfg, [g], st)
+        u = c * (1 - m ** (t + 1)) / (1 - m)
+        v += u
+        assert st[0].u[5] == np.float32(u)
+        assert st[0].r[5] == np.float32(v)
+        assert st[0].u[0] == 0 and st[0].r[0] == 0   # momentum factor masking
+
+
+def test_momentum_rho1_is_uncompressed_mean():
+    """rho = 1: every coordinate is sent and both u and v are reset each step,
+    so the output is the plain mean of the gradients whatever m is."""
+    n, N = 3, 1000
+    cfg = O.Cfg("dgc", 1.0, momentum=0.9)
+    st = O.new_states(n, N, "allgather", cfg)
+    for s in range(3):
+        grads = [gradient(N, step=s, rank=r) for r in range(n)]
+        res = O.sync("allgather", cfg, grads, st)
+        assert np.array_equal(res.outs[0], O.aggregate(grads, "mean", n))
+        assert all(np.all(x.u == 0) and np.all(x.r == 0) for x in st)
+
+
+def test_momentum_ef_identity_and_masking():
+    """transmitted + v_new == fl(u_new_unmasked + v_old) bit for bit, and
+    u_new is zero exactly on the selected support."""
+    N = 30_000
+    cfg = O.Cfg("dgc", 0.01, momentum=0.9)
+    st = O.new_states(1, N, "allgather", cfg)
+    for s in range(4):
+        g = gradient(N, step=s, dist="D3")
+        u_pred = (np.float32(0.9) * st[0].u).astype(np.float32)
+        u_pred = (u_pred + g).astype(np.float32)
+        acc = (u_pred + st[0].r).astype(np.float32)
+        res = O.sync("allgather", cfg, [g], st)
+        out, v = res.outs[0], st[0].r
+        assert np.array_equal((out + v).view(np.uint32), acc.view(np.uint32))
+        sel = np.zeros(N, bool)
+        sel[O.topk_select(acc, O.k_of(N, 0.01)).astype(np.int64)] = True
+        assert np.all(st[0].u[sel] == 0)
+        assert np.array_equal(st[0].u[~sel].view(np.uint32), u_pred[~sel].view(np.uint32))
