@@ -215,7 +215,7 @@ static void layout_buffers(Layout& L, Bucket& b, HostTables& T) {
     lb = LocalBufs{L.ptr<unsigned char>(off), stride};
     return off;
   };
-  b.fused = fused_allgather_enabled() && !w->sim && n > 1 && (dgc || quant) &&
+  b.fused = fused_allgather_enabled() && !w->sim && n > 1 && !none &&
             (b.routine == ESP_ALLGATHER || b.routine == ESP_ALLTOALL_ALLGATHER ||
              (b.routine == ESP_GATHER_BROADCAST && p2));
   // (the fused producers write peers directly; the send buffer still serves esp_compress)
@@ -262,7 +262,8 @@ static void layout_buffers(Layout& L, Bucket& b, HostTables& T) {
       b.dst2_par = S;
       b.dst2_slot = 0;
     }
-    b.push = push_enabled() || (p2 && !quant);   // sparse a7 has no peer-store variant
+    // sparse a7 and Randomk have no producer-store variant
+    b.push = push_enabled() || (p2 && !quant) || b.kind == ESP_RANDOMK;
     if (b.push) {
       // jobs and arrivals per call (J jobs per slot)
       const uint64_t J = div_up(S, kPushChunk);
@@ -615,10 +616,10 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         };
         // push mode: a piece this rank produced itself is read from its local
         // source (no self copy); same pointer for both parities
-        auto local_piece = [&](unsigned char* ptr) {
+        auto local_piece = [&](unsigned char* ptr, uint32_t rankterm) {
           T.h2_pieces.push_back(ptr);
           T.h2_pieces_odd.push_back(ptr);
-          T.rankterms.push_back(0);
+          T.rankterms.push_back(rankterm);
         };
         const int me = w->rank;
         const uint32_t rt_shared = 0;
@@ -629,13 +630,13 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           case ESP_ALLGATHER:
           case ESP_GATHER_BROADCAST:
             if (b.routine == ESP_GATHER_BROADCAST && p2) {
-              if (b.push && me == 0) local_piece(b.stage.at(lr) + b.coff[ti]);
+              if (b.push && me == 0) local_piece(b.stage.at(lr) + b.coff[ti], rt2);
               else add_piece(b.mid.base ? b.mid.at(lr) : nullptr, b.coff[ti], rt2);
               s.npieces = 1;
               s.divisor = 1.0f;
             } else {
               for (int r = 0; r < n; ++r) {
-                if (b.push && r == me) local_piece(b.send.at(lr) + b.coff[ti]);
+                if (b.push && r == me) local_piece(b.send.at(lr) + b.coff[ti], rt_of(r));
                 else add_piece(b.recv1.base ? b.recv1.at(lr) : nullptr, (size_t)r * S + b.coff[ti], rt_of(r));
               }
               s.npieces = (uint32_t)n;
@@ -645,13 +646,13 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           case ESP_ALLTOALL_ALLGATHER:
             if (!p2) {
               for (int r = 0; r < n; ++r)
-                if (b.push && r == me) local_piece(b.send.at(lr) + (size_t)part * S + b.coff[ti]);
+                if (b.push && r == me) local_piece(b.send.at(lr) + (size_t)part * S + b.coff[ti], rt_of(r));
                 else add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr,
                           (size_t)part * n * S + (size_t)r * S + b.coff[ti], rt_of(r));
               s.npieces = (uint32_t)n;
               s.divisor = divisor;
             } else {
-              if (b.push && part == me) local_piece(b.stage.at(lr) + b.coff[ti]);
+              if (b.push && part == me) local_piece(b.stage.at(lr) + b.coff[ti], rt2);
               else add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr, (size_t)part * S + b.coff[ti], rt2);
               s.npieces = 1;
               s.divisor = 1.0f;
@@ -1217,7 +1218,8 @@ static void run_h2(Plan& p, Bucket& b, cudaStream_t st) {
                        (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, b.h2_max_pieces, st);
       break;
     case ESP_RANDOMK:
-      launch_h2_randomk(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, b.h2_rankterms, st);
+      launch_h2_randomk(b.h2, b.h2_units, b.nh2_units, (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces,
+                        b.h2_rankterms, st);
       break;
     case ESP_EFSIGNSGD:
     case ESP_ONEBIT:

@@ -52,17 +52,20 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = E.World.nccl(local)
-    pairs = [(k, r, 0) for k in O.KINDS for r in O.ROUTINES if O.legal(O.Cfg(k), r)]
+    pairs = [(k, r, 0, True) for k in O.KINDS for r in O.ROUTINES if O.legal(O.Cfg(k), r)]
     # the other process of each divisible routine (R19)
-    pairs += [(k, r, 2 if k in O.SPARSE else 1) for k in ("dgc", "randomk", "efsignsgd")
+    pairs += [(k, r, 2 if k in O.SPARSE else 1, True) for k in ("dgc", "randomk", "efsignsgd")
               for r in ("alltoall_allgather", "gather_broadcast")]
+    # Randomk with per-rank indices (R5) through the fused routines
+    pairs += [("randomk", r, p, False) for r, p in (("allgather", 0), ("alltoall_allgather", 1),
+                                                   ("alltoall_allgather", 2), ("gather_broadcast", 2))]
     N = 30_011
     checked = 0
-    for t, (kind, routine, proc) in enumerate(pairs):
+    for t, (kind, routine, proc, shared) in enumerate(pairs):
         if os.environ.get("ESP_TEST_VERBOSE"):
             print(f"rank {rank}: {kind}/{routine}/process {proc}", flush=True)
-        ctx = E.Ctx(w, kind, routine, N, tensor_id=t, ratio=0.02, process=proc)
-        cfg = O.Cfg(kind, 0.02, process=proc)
+        ctx = E.Ctx(w, kind, routine, N, tensor_id=t, ratio=0.02, process=proc, shared_indices=shared)
+        cfg = O.Cfg(kind, 0.02, shared_indices=shared, process=proc)
         st = O.new_states(n, N, routine, cfg)
         for s in range(3):
             if kind in O.QUANTIZED and s > 0:   # lock-step: oracle state -> GPU
