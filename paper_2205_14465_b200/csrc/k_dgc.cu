@@ -83,7 +83,8 @@ __device__ void select_bin(const uint32_t* hist, int nbins, uint32_t need, uint3
 // ------------------------------------------------------------------ 1. sample
 // force (test hook, ESP_DGC_FORCE_FALLBACK): bit 0 sets thr above every key so
 // that every segment with k > 0 takes the fallback; bit 1 does the same to thr_lo
-__global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __restrict__ segs, int force) {
+__global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __restrict__ segs, int force,
+                                                             float margin) {
   __shared__ uint32_t keys[kSample];
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t sh[280];
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
     need = S.k;
   } else {
     const double rs = S.ratio * (double)s;
-    const double js = ceil(rs + 4.0 * sqrt(rs));
+    const double js = ceil(rs + (double)margin * sqrt(rs));
     need = js >= (double)s ? s : (uint32_t)js;
     if (need < 1) need = 1;
   }
@@ -1086,7 +1087,13 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
   }();
   const int stages = tma_stream_stages();
   const char* ff = getenv("ESP_DGC_FORCE_FALLBACK");   // read per launch: a test hook
-  dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs, ff ? atoi(ff) : 0);
+  // sample-rank margin in standard deviations of the sample count (a sampler
+  // knob: a miss only sends that segment through the fallback recompaction)
+  static const float margin = [] {
+    const char* e = getenv("ESP_DGC_MARGIN");
+    return e ? (float)atof(e) : 4.0f;
+  }();
+  dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs, ff ? atoi(ff) : 0, margin);
   debug_sync("dgc_sample", st);
   if (probe0) cudaEventRecord(probe0, st);
   {
