@@ -213,13 +213,18 @@ struct SignOp {
   __device__ void end_segment(const SegH1&, uint32_t, uint32_t, State&, TmaGroup&) const {}
 };
 
-// One CTA per segment: the scale(s) from the per-run partials, reduced in run
-// order (each thread a strided slice, then the fixed block tree): the result
-// does not depend on the grid of the streaming pass.
+// The scale(s) of a segment from its per-run partials, reduced in run order
+// by a fixed two-level tree: CTA (seg = blockIdx.x, chunk = blockIdx.y) reduces
+// kFinRuns consecutive runs (each thread a strided slice, then the fixed block
+// tree) and parks the chunk's result in its first run's slots; the segment's
+// last CTA (counter in its zeroed SelState) reduces the chunk results in chunk
+// order.  The result does not depend on the grid of the streaming pass, and a
+// single large tensor is reduced by many CTAs (one CTA per segment serialised
+// the 2^28-element sweep sizes).
 // Fused collective (dmode != 0): the header goes to the destination chunk(s),
 // then one system-scope fence and one arrival per destination (the words were
-// stored, and fenced per thread, by the streaming pass that precedes this
-// kernel in stream order).
+// stored by the streaming pass that precedes this kernel in stream order).
+constexpr uint32_t kFinRuns = 4096;
 template <int KIND>
 __global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __restrict__ segs,
                                                                  unsigned char* const* __restrict__ dsts,
@@ -227,11 +232,16 @@ __global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __
                                                                  int dmode, int ndst) {
   __shared__ double shd[8];
   __shared__ uint32_t shu[16];
+  __shared__ int last;
   const SegH1 S = segs[blockIdx.x];
   const uint32_t nruns = (S.n + kRun - 1) / kRun;
+  const uint32_t nch = (nruns + kFinRuns - 1) / kFinRuns;
+  const uint32_t ch = blockIdx.y;
+  if (ch >= (nch ? nch : 1u)) return;   // block-uniform
+  const uint32_t r0 = ch * kFinRuns, r1 = min(nruns, r0 + kFinRuns);
   double a = 0.0, b = 0.0;
   uint32_t ca = 0, cb = 0;
-  for (uint32_t v = threadIdx.x; v < nruns; v += kThreads) {
+  for (uint32_t v = r0 + threadIdx.x; v < r1; v += kThreads) {
     a += __ldcg(S.partial + 2 * v);
     if (KIND != K_EFSIGN) {
       b += __ldcg(S.partial + 2 * v + 1);
@@ -244,6 +254,38 @@ __global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __
     b = block_sum_f64(b, shd);
     ca = block_sum_u32(ca, shu);
     cb = block_sum_u32(cb, shu);
+  }
+  if (nch > 1) {
+    // park this chunk's sums, the last CTA of the segment reduces the chunks
+    if (threadIdx.x == 0) {
+      S.partial[2 * r0] = a;
+      if (KIND != K_EFSIGN) {
+        S.partial[2 * r0 + 1] = b;
+        S.pcount[2 * r0] = ca;
+        S.pcount[2 * r0 + 1] = cb;
+      }
+      __threadfence();
+      last = atomicAdd(&S.st->done, 1u) == nch - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    a = b = 0.0;
+    ca = cb = 0;
+    for (uint32_t c = threadIdx.x; c < nch; c += kThreads) {
+      a += __ldcg(S.partial + 2 * (c * kFinRuns));
+      if (KIND != K_EFSIGN) {
+        b += __ldcg(S.partial + 2 * (c * kFinRuns) + 1);
+        ca += __ldcg(S.pcount + 2 * (c * kFinRuns));
+        cb += __ldcg(S.pcount + 2 * (c * kFinRuns) + 1);
+      }
+    }
+    a = block_sum_f64(a, shd);
+    if (KIND != K_EFSIGN) {
+      b = block_sum_f64(b, shd);
+      ca = block_sum_u32(ca, shu);
+      cb = block_sum_u32(cb, shu);
+    }
   }
   if (threadIdx.x == 0) {
     float* hdr = reinterpret_cast<float*>(S.chunk);
@@ -289,7 +331,7 @@ __global__ void sign_materialize_kernel(const float* __restrict__ p, const float
 
 void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                         const unsigned char* const* pieces, cudaStream_t st, unsigned char* const* dsts,
-                        unsigned long long* const* cnts, int dmode, int ndst) {
+                        unsigned long long* const* cnts, int dmode, int ndst, uint32_t max_len) {
   if (nunits == 0) return;
   static const bool stage = [] {   // ESP_A7_STAGE=0: load the pieces' words by LDG
     const char* e = getenv("ESP_A7_STAGE");
@@ -307,8 +349,10 @@ void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* 
     if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, true>{pieces, stage, dsts, dmode, ndst, fence && dmode}, st);
     else launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, false>{nullptr, false, dsts, dmode, ndst, fence && dmode}, st);
   }
-  if (kind == K_EFSIGN) sign_finalize_kernel<K_EFSIGN><<<nsegs, kThreads, 0, st>>>(segs, dsts, cnts, dmode, ndst);
-  else sign_finalize_kernel<K_ONEBIT><<<nsegs, kThreads, 0, st>>>(segs, dsts, cnts, dmode, ndst);
+  const uint32_t max_runs = (max_len + kRun - 1) / kRun;
+  const dim3 fgrid((unsigned)nsegs, max_runs > kFinRuns ? (max_runs + kFinRuns - 1) / kFinRuns : 1u);
+  if (kind == K_EFSIGN) sign_finalize_kernel<K_EFSIGN><<<fgrid, kThreads, 0, st>>>(segs, dsts, cnts, dmode, ndst);
+  else sign_finalize_kernel<K_ONEBIT><<<fgrid, kThreads, 0, st>>>(segs, dsts, cnts, dmode, ndst);
   count_launches(1);
 }
 

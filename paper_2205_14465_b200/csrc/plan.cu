@@ -49,6 +49,7 @@ struct Bucket {
   uint32_t* h2_rankterms = nullptr;
   uint4* h2_off_jobs = nullptr; int nh2_off_jobs = 0;
   int h2_max_pieces = 0;
+  uint32_t h1_max_len = 0, a7_max_len = 0;   // longest h1 / a7 segment
   cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
@@ -419,6 +420,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     }
   }
   b.nh1 = (int)(T.h1.size() - h1_first);
+  b.h1_max_len = 0;
+  for (int i = 0; i < b.nh1; ++i) b.h1_max_len = std::max(b.h1_max_len, T.h1[h1_first + i].n);
   {
     // algorithmic bytes of the streaming h1 pass: read g, read r,
     // write r = 12 B/elem with EF (4 B/elem without); sign adds 1/8 B/elem of
@@ -571,6 +574,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
       }
     }
     b.na7 = (int)(T.a7.size() - a7_first);
+    b.a7_max_len = 0;
+    for (int i = 0; i < b.na7; ++i) b.a7_max_len = std::max(b.a7_max_len, T.a7[a7_first + i].n);
     b.na7_units = (int)u0;
     b.na7_groups = (int)g0;
     b.na7h2 = (int)(T.a7h2.size() - a7h2_first);
@@ -1036,8 +1041,9 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
       const int k = b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT;
       const int n = p.w->nranks;
       if (fused) launch_sign_h1_tma(k, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st,
-                                    b.dsts + (b.epoch & 1) * n, b.cnts, b.h1_dmode, n);
-      else launch_sign_h1_tma(k, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st);
+                                    b.dsts + (b.epoch & 1) * n, b.cnts, b.h1_dmode, n, b.h1_max_len);
+      else launch_sign_h1_tma(k, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st, nullptr, nullptr, 0, 0,
+                              b.h1_max_len);
       break;
     }
     default: launch_pack(b.h1, b.h1_units, b.nh1_units, st); break;
@@ -1078,14 +1084,16 @@ static void run_mid(Plan& p, Bucket& b, cudaStream_t cs) {
     }
     dbg("a7 recompress", cs);
   } else if (b.fused && b.push) {
-    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, (b.epoch & 1) ? b.a7_pieces_odd : b.a7_pieces, cs);
+    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, (b.epoch & 1) ? b.a7_pieces_odd : b.a7_pieces, cs,
+                       nullptr, nullptr, 0, 0, b.a7_max_len);
   } else if (b.fused) {
     // recompressed chunks go straight into every rank's phase-2 buffer
     const int n = p.w->nranks;
     launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, (b.epoch & 1) ? b.a7_pieces_odd : b.a7_pieces, cs,
-                       b.dsts2 + (b.epoch & 1) * n, b.cnts2, 2, n);
+                       b.dsts2 + (b.epoch & 1) * n, b.cnts2, 2, n, b.a7_max_len);
   } else {
-    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, b.a7_pieces, cs);
+    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, b.a7_pieces, cs, nullptr, nullptr, 0, 0,
+                       b.a7_max_len);
   }
   ESP_CUDA(cudaGetLastError());
 }
