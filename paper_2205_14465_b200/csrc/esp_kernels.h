@@ -8,6 +8,14 @@
 namespace esp {
 
 void count_launches(int n);   // process-wide counter behind esp_launch_count()
+// ESP_CARVEOUT=1: every kernel prefers the maximum shared-memory carveout (an
+// A/B knob; measured 5% slower on BERT-large, so off by default)
+bool set_max_smem_carveout(const void* fn);
+#define ESP_CARVE(...)                                                                                \
+  do {                                                                                              \
+    static const bool esp_carve_ = ::esp::set_max_smem_carveout(reinterpret_cast<const void*>(__VA_ARGS__)); \
+    (void)esp_carve_;                                                                               \
+  } while (0)
 
 // DGC / TOPK h1 (k_dgc.cu)
 // probe0/probe1 (optional): events recorded around the streaming pass.

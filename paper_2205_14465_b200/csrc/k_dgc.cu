@@ -1014,6 +1014,7 @@ __global__ void wait_arrivals_kernel(const unsigned long long* cnt, unsigned lon
 
 void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, cudaStream_t st) {
   if (target == 0) return;   // nothing to wait for (e.g. the root's own broadcast)
+  ESP_CARVE(wait_arrivals_kernel);
   wait_arrivals_kernel<<<1, 32, 0, st>>>(cnt, target);
   count_launches(1);
 }
@@ -1093,6 +1094,7 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
     const char* e = getenv("ESP_DGC_MARGIN");
     return e ? (float)atof(e) : 4.0f;
   }();
+  ESP_CARVE(dgc_sample_kernel);
   dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs, ff ? atoi(ff) : 0, margin);
   debug_sync("dgc_sample", st);
   if (probe0) cudaEventRecord(probe0, st);
@@ -1106,6 +1108,12 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
       return g < 1 ? 1 : (g > 3 ? 3 : g);
     }();
     const size_t mom_smem = kStreamHdr + kMaxStagesMom * kStageBytesMom;
+    ESP_CARVE(dgc_stream_kernel<3, true>);
+    ESP_CARVE(dgc_stream_kernel<2, true>);
+    ESP_CARVE(dgc_stream_kernel<1, true>);
+    ESP_CARVE(dgc_stream_kernel<1>);
+    ESP_CARVE(dgc_stream_kernel<2>);
+    ESP_CARVE(dgc_stream_kernel<3>);
     if (mom && mom_groups == 3)
       dgc_stream_kernel<3, true><<<grid, 3 * kThreads + 32, mom_smem, st>>>(segs, unit_seg, (uint32_t)nunits,
                                                                             variant, 3);
@@ -1130,14 +1138,18 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
   }
   debug_sync("dgc_stream", st);
   if (probe1) cudaEventRecord(probe1, st);
+  ESP_CARVE(dgc_fallback_kernel);
   dgc_fallback_kernel<<<g_num_sms, kThreads, 0, st>>>(segs, nsegs);
   debug_sync("dgc_fallback", st);
   const int wgrid = (ngroups + kWarpsPerCta - 1) / kWarpsPerCta;   // one warp per finalize group
   if (wgrid > 0) {
+    ESP_CARVE(dgc_refine_kernel<2>);
     dgc_refine_kernel<2><<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_refine<2>", st);
+    ESP_CARVE(dgc_refine_kernel<3>);
     dgc_refine_kernel<3><<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_refine<3>", st);
+    ESP_CARVE(dgc_write_kernel);
     dgc_write_kernel<<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups, dsts, cnts, ndst);
     debug_sync("dgc_write", st);
   }

@@ -17,10 +17,13 @@ constexpr int kMaxPieces = 64;
 // For every piece (sorted idx[kpad], 0xFFFFFFFF padding), the first entry of
 // each output tile: toff[t] = lower_bound(idx, t * kTile), t = 0..ntiles.  One
 // pass over the (small) pieces replaces a dependent binary search per tile.
-// job = {segment, piece within segment, first entry}: kOffJob entries of one piece
+// job = {segment, piece within segment, first entry}: kOffJob entries of one
+// piece; every thread issues all of its loads (its entries and their
+// predecessors) before using any (the loop was a chain of dependent loads).
 __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2* __restrict__ segs,
                                                                      const uint4* __restrict__ jobs,
                                                                      const unsigned char* const* __restrict__ pieces) {
+  constexpr int kPer = kOffJob / kThreads;
   const uint4 job = jobs[blockIdx.x];
   const SegH2 S = segs[job.x];
   const uint32_t r = job.y;
@@ -28,16 +31,23 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2
   uint32_t* toff = S.toff + (size_t)r * (ntiles + 1);
   const uint32_t* idx = reinterpret_cast<const uint32_t*>(pieces[S.piece0 + r]);
   const uint32_t iend = min(job.z + (uint32_t)kOffJob, S.kpad);
-  for (uint32_t i = job.z + threadIdx.x; i < iend; i += kThreads) {
-    const uint32_t v = __ldg(idx + i);
-    const uint32_t t = v == 0xFFFFFFFFu ? ntiles : min(v / (uint32_t)kTile, ntiles);
-    const uint32_t prev = i == 0 ? 0u : [&] {
-      const uint32_t u = __ldg(idx + i - 1);
-      return (u == 0xFFFFFFFFu ? ntiles : min(u / (uint32_t)kTile, ntiles)) + 1;
-    }();
-    for (uint32_t q = prev; q <= t; ++q) toff[q] = i;   // tiles (tile(i-1), tile(i)] start at i
+  auto tile_of = [&](uint32_t v) { return v == 0xFFFFFFFFu ? ntiles : min(v / (uint32_t)kTile, ntiles); };
+  uint32_t v[kPer], u[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const uint32_t i = job.z + threadIdx.x + q * kThreads;
+    v[q] = i < iend ? __ldg(idx + i) : 0u;
+    u[q] = (i < iend && i > 0) ? __ldg(idx + i - 1) : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const uint32_t i = job.z + threadIdx.x + q * kThreads;
+    if (i >= iend) break;
+    const uint32_t t = tile_of(v[q]);
+    const uint32_t prev = i == 0 ? 0u : tile_of(u[q]) + 1;
+    for (uint32_t qq = prev; qq <= t; ++qq) toff[qq] = i;   // tiles (tile(i-1), tile(i)] start at i
     if (i == S.kpad - 1)
-      for (uint32_t q = t + 1; q <= ntiles; ++q) toff[q] = S.kpad;
+      for (uint32_t qq = t + 1; qq <= ntiles; ++qq) toff[qq] = S.kpad;
   }
 }
 
@@ -317,6 +327,7 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const SegH1* __restrict_
 void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
                       const unsigned char* const* pieces, int max_pieces, cudaStream_t st) {
   if (ntiles == 0) return;
+  ESP_CARVE(h2_sparse_offsets_kernel);
   h2_sparse_offsets_kernel<<<njobs, kThreads, 0, st>>>(segs, jobs, pieces);
   constexpr int kSmem = kTileThreads / 32 * kTile * (int)sizeof(float);
   auto cap = [](int smem) {
@@ -331,6 +342,7 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
   const int grid_cap = max_pieces > 1 ? capn : cap1;
   const int need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);   // one warp per tile
   const int grid = need < grid_cap ? need : grid_cap;
+  ESP_CARVE(h2_sparse_kernel);
   h2_sparse_kernel<<<grid, kTileThreads, smem, st>>>(segs, tile_seg, (uint32_t)ntiles, pieces);
   count_launches(2);
 }
@@ -346,6 +358,8 @@ void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int n
     return sms * (per_sm > 0 ? per_sm : 4);
   }();
   const int grid = nunits < cap ? nunits : cap;
+  ESP_CARVE(h2_sign_kernel<K_EFSIGN>);
+  ESP_CARVE(h2_sign_kernel<K_ONEBIT>);
   if (kind == K_EFSIGN) h2_sign_kernel<K_EFSIGN><<<grid, kThreads, 0, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
   else h2_sign_kernel<K_ONEBIT><<<grid, kThreads, 0, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
   count_launches(1);
@@ -354,12 +368,14 @@ void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int n
 void launch_h2_dense(const SegH2* segs, const uint32_t* unit_seg, int nunits,
                      const unsigned char* const* pieces, cudaStream_t st) {
   if (nunits == 0) return;
+  ESP_CARVE(h2_dense_kernel);
   h2_dense_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
   count_launches(1);
 }
 
 void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st) {
   if (nunits == 0) return;
+  ESP_CARVE(pack_kernel);
   pack_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg);
   count_launches(1);
 }

@@ -149,6 +149,7 @@ void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, 
 void launch_h2_randomk(const SegH2* segs, const uint32_t* unit_seg, int nunits,
                        const unsigned char* const* pieces, const uint32_t* rankterms, cudaStream_t st) {
   if (nunits == 0) return;
+  ESP_CARVE(h2_randomk_kernel);
   h2_randomk_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces, rankterms);
   count_launches(1);
 }

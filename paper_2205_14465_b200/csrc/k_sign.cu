@@ -351,6 +351,8 @@ void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* 
   }
   const uint32_t max_runs = (max_len + kRun - 1) / kRun;
   const dim3 fgrid((unsigned)nsegs, max_runs > kFinRuns ? (max_runs + kFinRuns - 1) / kFinRuns : 1u);
+  ESP_CARVE(sign_finalize_kernel<K_EFSIGN>);
+  ESP_CARVE(sign_finalize_kernel<K_ONEBIT>);
   if (kind == K_EFSIGN) sign_finalize_kernel<K_EFSIGN><<<fgrid, kThreads, 0, st>>>(segs, dsts, cnts, dmode, ndst);
   else sign_finalize_kernel<K_ONEBIT><<<fgrid, kThreads, 0, st>>>(segs, dsts, cnts, dmode, ndst);
   count_launches(1);

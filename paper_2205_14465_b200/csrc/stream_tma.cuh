@@ -231,6 +231,7 @@ static void launch_tma_op_n(const SegH1* segs, const uint32_t* unit_seg, int nun
   (void)init;
   int ns = tma_stream_stages();
   ns = ns < NCG ? NCG : (ns > kMaxNs ? kMaxNs : ns - ns % NCG);
+  ESP_CARVE(tma_stream_kernel<Op, NCG>);
   tma_stream_kernel<Op, NCG><<<tma_stream_grid(nunits), NCG * kThreads + 32, kTmaHdrBytes + ns * kTmaStageBytes,
                                st>>>(segs, unit_seg, (uint32_t)nunits, ns, op);
   count_launches(1);

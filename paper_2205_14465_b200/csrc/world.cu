@@ -2,6 +2,7 @@
 // machine, a CCL per data format, several CUDA streams).  A world is either an
 // NCCL communicator (one process per GPU, NVLink 5 / NVSwitch) or a "sim" world
 // of n virtual ranks on one GPU whose collectives are device-to-device copies.
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 
@@ -15,6 +16,14 @@ static std::atomic<uint64_t> g_launches{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+bool set_max_smem_carveout(const void* fn) {
+  static const bool on = [] {
+    const char* e = getenv("ESP_CARVEOUT");   // measured slower on BERT-large: off by default
+    return e && e[0] == '1';
+  }();
+  return on && cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    (int)cudaSharedmemCarveoutMaxShared) == cudaSuccess;
+}
 
 uint64_t host_splitmix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
