@@ -25,7 +25,9 @@
  *     Nothing is allocated on the hot path after the first call with a given
  *     tensor set (plans are cached).
  *   - Threading: one host thread per world at a time (an NCCL rule).
- *   - Gradients are contiguous fp32, 16-byte aligned device pointers;
+ *   - Gradients are contiguous fp32 device pointers, 4-byte aligned for
+ *     esp_sync / esp_sync_many (16-byte aligned ones take the TMA fast path),
+ *     16-byte aligned for esp_compress / esp_decompress buffers;
  *     numel < 2^31 (indices are uint32, reading R18) else ESP_ERR_TOO_LARGE.
  *   - Sim world: n virtual ranks on one GPU.  Every per-rank buffer argument is
  *     then n rank-major slices (rank r at offset r * slice) and collectives are

@@ -35,6 +35,14 @@ void check_ptr16(const void* p, const char* what) {
   ESP_REQUIRE(((uintptr_t)p & 15) == 0, ESP_ERR_INVALID_ARG, std::string(what) + " is not 16-byte aligned");
 }
 
+// gradients of esp_sync / esp_sync_many: 4-byte alignment suffices (tensors that
+// are not 16-byte aligned take the guarded-load paths of the kernels; e.g. the
+// per-parameter views of a DDP gradient bucket)
+void check_ptr4(const void* p, const char* what) {
+  ESP_REQUIRE(p, ESP_ERR_INVALID_ARG, std::string(what) + " is NULL");
+  ESP_REQUIRE(((uintptr_t)p & 3) == 0, ESP_ERR_INVALID_ARG, std::string(what) + " is not 4-byte aligned");
+}
+
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 }  // namespace
@@ -382,7 +390,7 @@ esp_status_t esp_sync_many(esp_world_t w, const esp_ctx_t* ctxs, float* const* g
   for (int i = 0; i < ntensors; ++i) {
     ESP_REQUIRE(v[i], ESP_ERR_INVALID_ARG, "ctx is NULL");
     ESP_REQUIRE(v[i]->w == w, ESP_ERR_STATE, "ctx belongs to another world");
-    check_ptr16(grads[i], "grad");
+    check_ptr4(grads[i], "grad");
     for (int j = 0; j < i; ++j) ESP_REQUIRE(v[j] != v[i], ESP_ERR_INVALID_ARG, "ctx listed twice");
   }
   ESP_CUDA(cudaSetDevice(w->dev));
@@ -395,7 +403,7 @@ esp_status_t esp_sync(esp_world_t w, esp_ctx_t c, float* grad_inout, void* strea
   ESP_API_BEGIN
   ESP_REQUIRE(w && c, ESP_ERR_INVALID_ARG, "null argument");
   ESP_REQUIRE(c->w == w, ESP_ERR_STATE, "ctx belongs to another world");
-  check_ptr16(grad_inout, "grad");
+  check_ptr4(grad_inout, "grad");
   ESP_CUDA(cudaSetDevice(w->dev));
   execute_plan(get_plan(w, {c}), &grad_inout, as_stream(stream));
   ESP_API_END

@@ -24,3 +24,18 @@ def test_nccl_world_parity(nproc):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
     assert r.stdout.count("sync_many ok") == nproc
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_ddp_comm_hook(nproc):
+    """NEXT-4: the libesp DDP communication hook (paper_2205_14465_b200/ddp.py)."""
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs, found {torch.cuda.device_count()}")
+    import __graft_entry__
+    __graft_entry__.build()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={29600 + nproc}",
+           os.path.join(ROOT, "tests", "ddp_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    assert r.stdout.count("ddp hook ok") == nproc
