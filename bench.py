@@ -41,7 +41,19 @@ WORKLOADS = {
         "none": ("none", 1.0, "allreduce")}[shapes.gpt2_medium_mixed_rule(N)]),
     # DGC with momentum correction (R20, NEXT-2): 20 B/elem streaming pass
     "bert_large_dgc_momentum_allgather": ("bert_large", lambda N: ("dgc", 0.001, "allgather", {"momentum": 0.9})),
+    # NEXT-3: per-size options chosen by the cost model over the measured curves
+    # (paper_2205_14465_b200/strategy.py) for the run's rank count
+    "gpt2_medium_selected": ("gpt2_medium", "selected"),
 }
+
+
+def workload(name, n):
+    """-> (model, rule) with the selected strategy resolved for n ranks."""
+    model, rule = WORKLOADS[name]
+    if rule == "selected":
+        from paper_2205_14465_b200 import strategy
+        rule = strategy.Selector(max(1, n)).rule
+    return model, rule
 
 
 def opt(rule, N):
@@ -169,7 +181,7 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import esp_oracle as O
-    model, rule = WORKLOADS[args.workload]
+    model, rule = workload(args.workload, ws)
     names = [nm for nm, _ in shapes.MODELS[model]()]
     sizes = shapes.numels(model)
     # sample: the first ~4M elements of encoder/transformer weights after the embeddings
@@ -264,7 +276,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2205_14465_b200 import esp as E
 
-    model, rule = WORKLOADS[args.workload]
+    model, rule = workload(args.workload, ws)
     names = [nm for nm, _ in shapes.MODELS[model]()]
     sizes = shapes.numels(model)
     total = sum(sizes)

@@ -225,6 +225,42 @@ esp_status_t esp_compressed_bytes(const esp_compressor_cfg_t* cfg, size_t numel,
 esp_status_t esp_wire_bytes(int row, double M, int n, double* out);
 esp_status_t esp_model_time(int row, double M, int n, double B, double* out_seconds);
 
+/* ---- strategy selection (App. A; Algorithm 1
+ * P:1299-1361; readings R15, R21) -----------------------------------------------
+ * esp_curve_t: a measured cost curve, n samples (input bytes, seconds) with
+ *   strictly increasing bytes ("profiled ... 2^10, 2^11, ..., 2^30", P:27-29;
+ *   tools/sweep.py).  esp_curve_eval: log-log piecewise-linear interpolation,
+ *   clamped to the first sample below it, the last segment's slope above the
+ *   last sample ("curve fitting").  ESP_ERR_INVALID_ARG on an empty or
+ *   non-increasing curve or a non-positive sample.
+ * esp_option_t: one candidate compression option of a tensor (the paper's c_j
+ *   restricted to GPU + flat communication): compressor cfg, routine, and the
+ *   h1 / h2 curves of that compressor (ignored for NONE).
+ * esp_option_time: predicted synchronisation time of one tensor of numel fp32
+ *   over n ranks at B bytes/s: the cost table's communication column for the
+ *   option's row with M = its payload bytes, plus the table's compression
+ *   column with h1(.) / h2(.) evaluated at the input bytes of each application
+ *   (h1(M) = h1 at 4 numel bytes, h1(M/n) and h2(M/n) at 4 numel / n); NONE has
+ *   no compression time.  ESP_ERR_UNSUPPORTED for an illegal pair.
+ * esp_select_option: Algorithm 1's GetBestOption for one tensor with no
+ *   computation to overlap (R21): the argmin of esp_option_time over the
+ *   candidates (ties: lowest index); *best = its index.
+ */
+typedef struct {
+  const double* bytes;
+  const double* seconds;
+  int32_t n;
+} esp_curve_t;
+typedef struct {
+  esp_compressor_cfg_t cfg;
+  int32_t routine;
+  esp_curve_t h1, h2;
+} esp_option_t;
+esp_status_t esp_curve_eval(const esp_curve_t* c, double bytes, double* out_seconds);
+esp_status_t esp_option_time(const esp_option_t* opt, size_t numel, int n, double B, double* out_seconds);
+esp_status_t esp_select_option(const esp_option_t* opts, int nopt, size_t numel, int n, double B, int* best,
+                               double* out_seconds);
+
 /* ---- diagnostics --------------------------------------------------------------- */
 const char* esp_status_string(esp_status_t s);
 const char* esp_last_error(void);

@@ -623,3 +623,47 @@ def table_ops(row: str, n: int):
         "gather_broadcast_sparse": (1, n),
         "gather_broadcast_quantized": (2, n + 1),
     }[row]
+
+
+# --------------------------------------------------------------------------
+# strategy selection (App. A; Algorithm 1
+# P:1299-1361; readings R15, R21) -- test infrastructure like the rest
+# --------------------------------------------------------------------------
+def curve_eval(samples, nbytes: float) -> float:
+    """Measured cost curve (input bytes, seconds), fitted log-log piecewise
+    linearly ("curve fitting"); clamped below the first sample, the last
+    segment extended above the last."""
+    xs = [math.log(b) for b, _ in samples]
+    ys = [math.log(t) for _, t in samples]
+    if len(samples) == 1 or nbytes <= samples[0][0]:
+        return samples[0][1]
+    x = math.log(nbytes)
+    i = 1
+    while i < len(xs) - 1 and nbytes > samples[i][0]:
+        i += 1
+    return math.exp(ys[i - 1] + (ys[i] - ys[i - 1]) * (x - xs[i - 1]) / (xs[i] - xs[i - 1]))
+
+
+def option_time(cfg: Cfg, routine: str, numel: int, n: int, B: float, h1, h2) -> float:
+    """Predicted sync time of one tensor: the cost table's row for the option
+     with M = its payload, h(.) keyed by input bytes (R15)."""
+    if cfg.kind == "none":
+        return table_comm_bytes("allreduce", 4 * numel, n) / B
+    P = nparts_of(routine, n)
+    M = chunk_bytes(cfg, numel, P) * P
+    row = table_row(cfg, routine)
+    inb = 4.0 * numel
+    f1 = lambda m: curve_eval(h1, inb if m == M else inb / n)   # h1(M) / h1(M/n)
+    f2 = lambda m: curve_eval(h2, inb if m == M else inb / n)
+    return table_comm_bytes(row, M, n) / B + table_compression_time(row, M, n, f1, f2)
+
+
+def select_option(options, numel: int, n: int, B: float):
+    """GetBestOption (Algorithm 1) for one tensor with no
+    computation to overlap (R21): the fastest candidate, ties to the first."""
+    best, bt = -1, 0.0
+    for i, (cfg, routine, h1, h2) in enumerate(options):
+        t = option_time(cfg, routine, numel, n, B, h1, h2)
+        if best < 0 or t < bt:
+            best, bt = i, t
+    return best, bt

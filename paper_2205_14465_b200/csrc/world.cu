@@ -428,6 +428,93 @@ esp_status_t esp_wire_bytes(int row, double M, int n, double* out) {
   ESP_API_END
 }
 
+esp_status_t esp_curve_eval(const esp_curve_t* c, double bytes, double* out_seconds) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(c && out_seconds && c->n >= 1 && c->bytes && c->seconds && bytes > 0, ESP_ERR_INVALID_ARG,
+              "bad curve");
+  for (int i = 0; i < c->n; ++i) {
+    ESP_REQUIRE(c->bytes[i] > 0 && c->seconds[i] > 0, ESP_ERR_INVALID_ARG, "curve samples must be positive");
+    if (i) ESP_REQUIRE(c->bytes[i] > c->bytes[i - 1], ESP_ERR_INVALID_ARG, "curve sizes must increase");
+  }
+  // log-log piecewise-linear; clamp below the first sample (launch floor),
+  // extend the last segment above the last sample
+  if (c->n == 1 || bytes <= c->bytes[0]) {   // one sample: a constant
+    *out_seconds = c->seconds[0];
+    return ESP_OK;
+  }
+  int i = 1;
+  while (i < c->n - 1 && bytes > c->bytes[i]) ++i;
+  const double x0 = std::log(c->bytes[i - 1]), x1 = std::log(c->bytes[i]);
+  const double y0 = std::log(c->seconds[i - 1]), y1 = std::log(c->seconds[i]);
+  const double x = std::log(bytes);
+  *out_seconds = std::exp(y0 + (y1 - y0) * (x - x0) / (x1 - x0));
+  ESP_API_END
+}
+
+esp_status_t esp_option_time(const esp_option_t* o, size_t numel, int n, double B, double* out_seconds) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(o && out_seconds && n >= 1 && B > 0 && numel >= 1, ESP_ERR_INVALID_ARG, "bad argument");
+  ESP_REQUIRE(numel < (1ull << 31), ESP_ERR_TOO_LARGE, "numel >= 2^31");
+  ESP_REQUIRE(pair_legal(o->cfg, o->routine), ESP_ERR_UNSUPPORTED, "illegal (compressor, routine) pair");
+  const double in_bytes = 4.0 * (double)numel;
+  if (o->cfg.kind == ESP_NONE) {
+    // uncompressed: communication only; all UT routines move 2(n-1)M/n
+    *out_seconds = (n > 1 ? 2.0 * (n - 1) * in_bytes / n : 0.0) / B;
+    return ESP_OK;
+  }
+  const int P = nparts_of(o->routine, n);
+  const double M = (double)chunk_bytes_of(o->cfg, numel, P, nullptr) * P;
+  const bool p2 = mid_scheme(o->cfg, o->routine);
+  int row = 0;
+  switch (o->routine) {
+    case ESP_ALLREDUCE: row = 0; break;
+    case ESP_ALLGATHER: row = 1; break;
+    case ESP_ALLTOALL_ALLGATHER: row = p2 ? 3 : 2; break;
+    default: row = p2 ? 5 : 4; break;   // Gather/Broadcast
+  }
+  double comm = 0;
+  esp_status_t s = esp_model_time(row, M, n, B, &comm);
+  if (s != ESP_OK) return s;
+  auto ev = [&](const esp_curve_t& c, double b) {
+    double t = 0;
+    const esp_status_t e = esp_curve_eval(&c, b, &t);
+    ESP_REQUIRE(e == ESP_OK, e, "bad cost curve");
+    return t;
+  };
+  const double part = in_bytes / n;
+  double comp = 0;
+  switch (row) {   // compression column of P:38-43 (R12: Gather/Broadcast quantized decodes h2(M))
+    case 0: comp = ev(o->h1, in_bytes) + ev(o->h2, in_bytes); break;
+    case 1: comp = ev(o->h1, in_bytes) + n * ev(o->h2, in_bytes); break;
+    case 2: comp = ev(o->h1, in_bytes) + (double)n * n * ev(o->h2, part); break;
+    case 3: comp = ev(o->h1, in_bytes) + ev(o->h1, part) + 2.0 * n * ev(o->h2, part); break;
+    case 4: comp = ev(o->h1, in_bytes) + n * ev(o->h2, in_bytes); break;
+    default: comp = 2.0 * ev(o->h1, in_bytes) + (n + 1.0) * ev(o->h2, in_bytes); break;
+  }
+  *out_seconds = comm + comp;
+  ESP_API_END
+}
+
+esp_status_t esp_select_option(const esp_option_t* opts, int nopt, size_t numel, int n, double B, int* best,
+                               double* out_seconds) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(opts && nopt >= 1 && best && out_seconds, ESP_ERR_INVALID_ARG, "bad argument");
+  int bi = -1;
+  double bt = 0;
+  for (int i = 0; i < nopt; ++i) {
+    double t = 0;
+    const esp_status_t s = esp_option_time(opts + i, numel, n, B, &t);
+    if (s != ESP_OK) return s;
+    if (bi < 0 || t < bt) {
+      bi = i;
+      bt = t;
+    }
+  }
+  *best = bi;
+  *out_seconds = bt;
+  ESP_API_END
+}
+
 esp_status_t esp_model_time(int row, double M, int n, double B, double* out_seconds) {
   ESP_API_BEGIN
   ESP_REQUIRE(out_seconds && B > 0, ESP_ERR_INVALID_ARG, "bad argument");

@@ -30,7 +30,8 @@ SYMBOLS = (
     "esp_ctx_create", "esp_ctx_destroy", "esp_ctx_payload_bytes", "esp_ctx_get_state",
     "esp_ctx_set_state", "esp_ctx_get_momentum", "esp_ctx_set_momentum", "esp_compress", "esp_decompress", "esp_sync", "esp_sync_many",
     "esp_compressed_bytes", "esp_wire_bytes", "esp_model_time", "esp_status_string",
-    "esp_last_error", "esp_launch_count", "esp_version",
+    "esp_last_error", "esp_launch_count", "esp_version", "esp_curve_eval", "esp_option_time",
+    "esp_select_option",
 )
 
 
@@ -38,6 +39,14 @@ class CompressorCfg(C.Structure):
     _fields_ = [("kind", C.c_int32), ("error_feedback", C.c_int32), ("ratio", C.c_double),
                 ("seed", C.c_uint64), ("randomk_shared_indices", C.c_int32), ("reduce", C.c_int32),
                 ("process", C.c_int32), ("momentum", C.c_double)]
+
+
+class Curve(C.Structure):
+    _fields_ = [("bytes", C.POINTER(C.c_double)), ("seconds", C.POINTER(C.c_double)), ("n", C.c_int32)]
+
+
+class Option(C.Structure):
+    _fields_ = [("cfg", CompressorCfg), ("routine", C.c_int32), ("h1", Curve), ("h2", Curve)]
 
 
 class Counters(C.Structure):
@@ -87,6 +96,9 @@ def lib():
             "esp_compressed_bytes": [C.POINTER(CompressorCfg), sz, i32, C.POINTER(sz)],
             "esp_wire_bytes": [i32, dbl, i32, C.POINTER(dbl)],
             "esp_model_time": [i32, dbl, i32, dbl, C.POINTER(dbl)],
+            "esp_curve_eval": [C.POINTER(Curve), dbl, C.POINTER(dbl)],
+            "esp_option_time": [C.POINTER(Option), sz, i32, dbl, C.POINTER(dbl)],
+            "esp_select_option": [C.POINTER(Option), i32, sz, i32, dbl, C.POINTER(i32), C.POINTER(dbl)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -327,3 +339,39 @@ def esp_sync_many(world: World, ctxs, grads, stream=None):
     gs = (C.c_void_p * n)(*[g.data_ptr() for g in grads])
     _check(lib().esp_sync_many(world.h, hs, gs, n, _stream(stream)))
     return grads
+
+
+# ---- strategy selection (esp_curve_eval / esp_option_time / esp_select_option)
+def make_curve(samples):
+    """samples: [(input bytes, seconds), ...] -> Curve (keeps its arrays alive)."""
+    b = (C.c_double * len(samples))(*[float(x) for x, _ in samples])
+    t = (C.c_double * len(samples))(*[float(y) for _, y in samples])
+    c = Curve(C.cast(b, C.POINTER(C.c_double)), C.cast(t, C.POINTER(C.c_double)), len(samples))
+    c._keep = (b, t)
+    return c
+
+
+def curve_eval(samples, nbytes):
+    out = C.c_double()
+    _check(lib().esp_curve_eval(C.byref(make_curve(samples)), float(nbytes), C.byref(out)))
+    return out.value
+
+
+def make_option(kind, ratio, routine, h1=((1.0, 1e-9),), h2=((1.0, 1e-9),), process=0, **kw):
+    o = Option(cfg_of(kind, ratio, process=process, **kw), ROUTINES[routine], make_curve(h1), make_curve(h2))
+    o._keep = (o.h1, o.h2)
+    return o
+
+
+def option_time(opt, numel, n, B):
+    out = C.c_double()
+    _check(lib().esp_option_time(C.byref(opt), numel, n, float(B), C.byref(out)))
+    return out.value
+
+
+def select_option(opts, numel, n, B):
+    """-> (index of the fastest option, its predicted seconds)."""
+    arr = (Option * len(opts))(*opts)
+    best, t = C.c_int(), C.c_double()
+    _check(lib().esp_select_option(arr, len(opts), numel, n, float(B), C.byref(best), C.byref(t)))
+    return best.value, t.value
