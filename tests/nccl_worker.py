@@ -96,18 +96,34 @@ def main():
         ctx.destroy()
 
     # a mixed strategy through esp_sync_many (bucketing + pipelining with small buckets)
-    specs = [("dgc", "allgather", 70_000), ("none", "allreduce", 1000), ("efsignsgd", "alltoall_allgather", 9000),
-             ("dgc", "alltoall_allgather", 40_000), ("onebit", "gather_broadcast", 5000), ("dgc", "allgather", 33)]
+    # a mixed strategy through esp_sync_many (bucketing + pipelining with small
+    # buckets), including tensors smaller than n x 32 (empty partitions), both
+    # processes and momentum, for 3 steps (EF carried across calls and both
+    # call parities of the fused buffers)
+    specs = [("dgc", "allgather", 70_000, {}), ("none", "allreduce", 1000, {}),
+             ("efsignsgd", "alltoall_allgather", 9000, {}), ("dgc", "alltoall_allgather", 40_000, {}),
+             ("onebit", "gather_broadcast", 5000, {}), ("dgc", "allgather", 33, {}),
+             ("efsignsgd", "alltoall_allgather", 40, {}), ("dgc", "alltoall_allgather", 50, {"process": 2}),
+             ("randomk", "alltoall_allgather", 3000, {"process": 2}), ("topk", "gather_broadcast", 77, {"process": 2}),
+             ("dgc", "allgather", 12_345, {"momentum": 0.9}), ("efsignsgd", "alltoall_allgather", 6000, {"process": 1})]
     w.set_bucket_elems(50_000)
-    ctxs = [E.Ctx(w, k, r, N_, tensor_id=100 + i, ratio=0.01) for i, (k, r, N_) in enumerate(specs)]
-    sts = [O.new_states(n, N_, r, O.Cfg(k, 0.01)) for (k, r, N_) in specs]
-    grads = [[gradient(N_, rank=q, tensor=100 + i) for q in range(n)] for i, (_, _, N_) in enumerate(specs)]
-    refs = [O.sync(r, O.Cfg(k, 0.01), grads[i], sts[i], tensor_id=100 + i) for i, (k, r, _) in enumerate(specs)]
-    gs = [torch.from_numpy(grads[i][rank].copy()).cuda() for i in range(len(specs))]
-    E.esp_sync_many(w, ctxs, gs)
-    torch.cuda.synchronize()
-    for i, (k, r, _) in enumerate(specs):
-        check(k, r, gs[i].cpu().numpy(), refs[i].outs[rank], grads[i], f"sync_many {k}/{r}")
+    ctxs = [E.Ctx(w, k, r, N_, tensor_id=100 + i, ratio=0.01, **ex) for i, (k, r, N_, ex) in enumerate(specs)]
+    cfgs = [O.Cfg(k, 0.01, **ex) for (k, r, N_, ex) in specs]
+    sts = [O.new_states(n, N_, r, cfgs[i]) for i, (k, r, N_, _) in enumerate(specs)]
+    for s in range(3):
+        for i, (k, r, N_, _) in enumerate(specs):
+            if k in O.QUANTIZED and s > 0:   # lock-step: oracle state -> GPU
+                r2 = np.zeros((1, ctxs[i].get_state()[2].shape[1]), np.float32)
+                if sts[i][rank].r2 is not None:
+                    r2[0, :sts[i][rank].r2.size] = sts[i][rank].r2
+                ctxs[i].set_state(sts[i][rank].step, sts[i][rank].r[None], r2)
+        grads = [[gradient(N_, step=s, rank=q, tensor=100 + i) for q in range(n)] for i, (_, _, N_, _) in enumerate(specs)]
+        refs = [O.sync(r, cfgs[i], grads[i], sts[i], tensor_id=100 + i) for i, (k, r, _, _) in enumerate(specs)]
+        gs = [torch.from_numpy(grads[i][rank].copy()).cuda() for i in range(len(specs))]
+        E.esp_sync_many(w, ctxs, gs)
+        torch.cuda.synchronize()
+        for i, (k, r, _, _) in enumerate(specs):
+            check(k, r, gs[i].cpu().numpy(), refs[i].outs[rank], grads[i], f"sync_many {k}/{r} step {s}")
     w.check()
     w.destroy()
     dist.barrier()
