@@ -234,8 +234,15 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
   const uint32_t u1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nunits / gridDim.x);
   uint32_t cur = 0xFFFFFFFFu;
   SegH2 S{};
+  // single-piece segments (the owner's recompressed partition, one broadcast
+  // payload): the next unit's words are loaded while this unit is computed and
+  // stored (the loop was bound by one word-load latency per unit)
+  uint32_t wnext[kJ];
+  bool have_next = false;
+  uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
   for (uint32_t gu = u0; gu < u1; ++gu) {
-    const uint32_t sid = unit_seg[gu];
+    const uint32_t sid = sid_next;
+    if (gu + 1 < u1) sid_next = unit_seg[gu + 1];
     if (sid != cur) {
       __syncthreads();   // the previous segment's table is no longer read
       cur = sid;
@@ -248,6 +255,7 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
         sh_w[r] = reinterpret_cast<const uint32_t*>(h + 16);
       }
       __syncthreads();
+      have_next = false;
     }
     const uint32_t n = S.n;
     const Divisor div(S.divisor);
@@ -256,23 +264,52 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
     float4 acc[kJ];
 #pragma unroll
     for (int j = 0; j < kJ; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t r = 0; r < S.npieces; ++r) {
-      const uint32_t* w = sh_w[r];
-      const float sp = sh_sp[r], sn = sh_sn[r];
+    if (S.npieces == 1) {
+      const uint32_t* w = sh_w[0];
       uint32_t wd[kJ];
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
         const uint32_t e = e0 + j * kThreads * 4;
-        wd[j] = e < n ? __ldg(w + (e >> 5)) : 0u;
+        wd[j] = have_next ? wnext[j] : (e < n ? __ldg(w + (e >> 5)) : 0u);
       }
+      // prefetch the next unit of the same segment
+      have_next = gu + 1 < u1 && sid_next == cur;
+      if (have_next) {
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+          const uint32_t e = e0 + kSignUnit + j * kThreads * 4;
+          wnext[j] = e < n ? __ldg(w + (e >> 5)) : 0u;
+        }
+      }
+      const float sp = sh_sp[0], sn = sh_sn[0];
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
         const uint32_t e = e0 + j * kThreads * 4;
         const uint32_t nib = (wd[j] >> (e & 31)) & 0xFu;
-        acc[j].x = __fadd_rn(acc[j].x, (nib & 1) ? sp : sn);
-        acc[j].y = __fadd_rn(acc[j].y, (nib & 2) ? sp : sn);
-        acc[j].z = __fadd_rn(acc[j].z, (nib & 4) ? sp : sn);
-        acc[j].w = __fadd_rn(acc[j].w, (nib & 8) ? sp : sn);
+        acc[j].x = __fadd_rn(0.f, (nib & 1) ? sp : sn);
+        acc[j].y = __fadd_rn(0.f, (nib & 2) ? sp : sn);
+        acc[j].z = __fadd_rn(0.f, (nib & 4) ? sp : sn);
+        acc[j].w = __fadd_rn(0.f, (nib & 8) ? sp : sn);
+      }
+    } else {
+      for (uint32_t r = 0; r < S.npieces; ++r) {
+        const uint32_t* w = sh_w[r];
+        const float sp = sh_sp[r], sn = sh_sn[r];
+        uint32_t wd[kJ];
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+          const uint32_t e = e0 + j * kThreads * 4;
+          wd[j] = e < n ? __ldg(w + (e >> 5)) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+          const uint32_t e = e0 + j * kThreads * 4;
+          const uint32_t nib = (wd[j] >> (e & 31)) & 0xFu;
+          acc[j].x = __fadd_rn(acc[j].x, (nib & 1) ? sp : sn);
+          acc[j].y = __fadd_rn(acc[j].y, (nib & 2) ? sp : sn);
+          acc[j].z = __fadd_rn(acc[j].z, (nib & 4) ? sp : sn);
+          acc[j].w = __fadd_rn(acc[j].w, (nib & 8) ? sp : sn);
+        }
       }
     }
     float* out = seg_out(S);

@@ -224,7 +224,7 @@ struct SignOp {
 // Fused collective (dmode != 0): the header goes to the destination chunk(s),
 // then one system-scope fence and one arrival per destination (the words were
 // stored by the streaming pass that precedes this kernel in stream order).
-constexpr uint32_t kFinRuns = 4096;
+constexpr uint32_t kFinRuns = 16384;
 template <int KIND>
 __global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __restrict__ segs,
                                                                  unsigned char* const* __restrict__ dsts,
@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __
   const uint32_t r0 = ch * kFinRuns, r1 = min(nruns, r0 + kFinRuns);
   double a = 0.0, b = 0.0;
   uint32_t ca = 0, cb = 0;
-  for (uint32_t v = r0 + threadIdx.x; v < r1; v += kThreads) {
+#pragma unroll 8
+  for (uint32_t v = r0 + threadIdx.x; v < r1; v += kThreads) {   // unrolled: 8 loads in flight
     a += __ldcg(S.partial + 2 * v);
     if (KIND != K_EFSIGN) {
       b += __ldcg(S.partial + 2 * v + 1);
