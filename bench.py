@@ -43,16 +43,18 @@ WORKLOADS = {
     "bert_large_dgc_momentum_allgather": ("bert_large", lambda N: ("dgc", 0.001, "allgather", {"momentum": 0.9})),
     # NEXT-3: per-size options chosen by the cost model over the measured curves
     # (paper_2205_14465_b200/strategy.py) for the run's rank count
-    "gpt2_medium_selected": ("gpt2_medium", "selected"),
+    "gpt2_medium_selected": ("gpt2_medium", ("selected", "paper", "dgc")),
+    "gpt2_medium_selected_bucketed": ("gpt2_medium", ("selected", "bucketed", "dgc")),
+    "gpt2_medium_selected_bucketed_all": ("gpt2_medium", ("selected", "bucketed", None)),
 }
 
 
 def workload(name, n):
     """-> (model, rule) with the selected strategy resolved for n ranks."""
     model, rule = WORKLOADS[name]
-    if rule == "selected":
+    if isinstance(rule, tuple) and rule[0] == "selected":
         from paper_2205_14465_b200 import strategy
-        rule = strategy.Selector(max(1, n)).rule
+        rule = strategy.Selector(max(1, n), model=rule[1], algorithm=rule[2]).rule
     return model, rule
 
 

@@ -16,8 +16,10 @@ from paper_2205_14465_b200 import strategy as S  # noqa: E402
 from synth import shapes  # noqa: E402
 
 
-def fixed_index(N):
-    return {"dgc": 1, "efsignsgd": 8, "none": 0}[shapes.gpt2_medium_mixed_rule(N)]
+def fixed_option(N):
+    k = shapes.gpt2_medium_mixed_rule(N)
+    return {"dgc": ("dgc", 0.01, "allgather", 0), "efsignsgd": ("efsignsgd", 1.0, "alltoall_allgather", 2),
+            "none": ("none", 1.0, "allreduce", 0)}[k]
 
 
 def main():
@@ -25,23 +27,31 @@ def main():
     ap.add_argument("--model", default="gpt2_medium")
     ap.add_argument("--n", type=int, default=8)
     ap.add_argument("--B", type=float, default=7.7e11, help="bytes/s per direction (measured NVLink 5)")
+    ap.add_argument("--cost-model", dest="cost_model", default="paper", choices=["paper", "bucketed"])
+    ap.add_argument("--algorithm", default="dgc", help="the GC algorithm (P:1217); 'all' = every algorithm")
     args = ap.parse_args()
-    sel = S.Selector(args.n, args.B)
+    alg = None if args.algorithm == "all" else args.algorithm
+    sel = S.Selector(args.n, args.B, model=args.cost_model, algorithm=alg)
+    full = S.Selector(args.n, args.B, model=args.cost_model, algorithm=None)   # prices the fixed rule
     sizes = shapes.numels(args.model)
     per_size, total, total_fixed = {}, 0.0, 0.0
     for N in sorted(set(sizes), reverse=True):   # Property #2: larger tensors first
         best, t = sel.choose(N)
-        fi = fixed_index(N) if args.model == "gpt2_medium" else 0
-        tf = sel.predicted(fi, N)
+        fo = fixed_option(N) if args.model == "gpt2_medium" else ("none", 1.0, "allreduce", 0)
+        fi = [c[:4] for c in full.candidates].index(fo)
+        tf = full.predicted(fi, N)
         cnt = sizes.count(N)
-        per_size[str(N)] = {"count": cnt, "selected": S.CANDIDATES[best][:4], "predicted_s": t,
-                            "fixed_rule": S.CANDIDATES[fi][:4], "fixed_rule_predicted_s": tf}
+        per_size[str(N)] = {"count": cnt, "selected": sel.candidates[best][:4], "predicted_s": t,
+                            "fixed_rule": fo, "fixed_rule_predicted_s": tf}
         total += cnt * t
         total_fixed += cnt * tf
     out = {"model": args.model, "n": args.n, "B": args.B, "sweep": "profiles/r01_sweep.json",
            "objective": "sum of per-tensor sync times (cost table P:38-43 + fitted h1/h2, reading R21)",
            "predicted_total_s": total, "fixed_rule_predicted_total_s": total_fixed, "per_size": per_size}
-    path = os.path.join(ROOT, "profiles", f"r01_strategy_{args.model}_n{args.n}.json")
+    suffix = ("" if args.cost_model == "paper" else "_bucketed") + ("" if args.algorithm == "dgc" else "_" + args.algorithm)
+    out["cost_model"] = args.cost_model
+    out["algorithm"] = args.algorithm
+    path = os.path.join(ROOT, "profiles", f"r01_strategy_{args.model}_n{args.n}{suffix}.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     for N, v in per_size.items():
