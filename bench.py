@@ -440,7 +440,7 @@ def main():
                              "per-step events) also evicts L2 between steps"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"] if achieved else None, "traffic": traffic,
-                         "kernel": "h1 streaming pass (dgc_stream_kernel / sign_h1 / randomk_h1)",
+                         "kernel": "h1 streaming pass (dgc_stream_kernel / tma_stream_kernel<SignOp|RandomkOp> / pack_kernel)",
                          "algorithmic_bytes_per_step": probe_bytes / max(1, args.steps),
                          "launches_per_step": probe_n / max(1, args.steps),
                          "kernel_ms_per_step": probe_ms / max(1, args.steps),

@@ -46,7 +46,8 @@ void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, 
 void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                         const unsigned char* const* pieces, cudaStream_t st, unsigned char* const* dsts = nullptr,
                         unsigned long long* const* cnts = nullptr, int dmode = 0, int ndst = 0,
-                        uint32_t max_len = 0);   // the longest segment (sizes the finalize grid)
+                        uint32_t max_len = 0,    // the longest segment (sizes the finalize grid)
+                        cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr);
 // NONE: pack gradients into a contiguous buffer (k_h2.cu)
 void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 

@@ -332,7 +332,8 @@ __global__ void sign_materialize_kernel(const float* __restrict__ p, const float
 
 void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                         const unsigned char* const* pieces, cudaStream_t st, unsigned char* const* dsts,
-                        unsigned long long* const* cnts, int dmode, int ndst, uint32_t max_len) {
+                        unsigned long long* const* cnts, int dmode, int ndst, uint32_t max_len,
+                        cudaEvent_t probe0, cudaEvent_t probe1) {
   if (nunits == 0) return;
   static const bool stage = [] {   // ESP_A7_STAGE=0: load the pieces' words by LDG
     const char* e = getenv("ESP_A7_STAGE");
@@ -343,6 +344,7 @@ void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* 
     const char* e = getenv("ESP_SYS_FENCE");
     return e && atoi(e) != 0;
   }();
+  if (probe0) cudaEventRecord(probe0, st);   // the roofline probe brackets the streaming pass only
   if (kind == K_EFSIGN) {
     if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, true>{pieces, stage, dsts, dmode, ndst, fence && dmode}, st);
     else launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, false>{nullptr, false, dsts, dmode, ndst, fence && dmode}, st);
@@ -350,6 +352,7 @@ void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* 
     if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, true>{pieces, stage, dsts, dmode, ndst, fence && dmode}, st);
     else launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, false>{nullptr, false, dsts, dmode, ndst, fence && dmode}, st);
   }
+  if (probe1) cudaEventRecord(probe1, st);
   const uint32_t max_runs = (max_len + kRun - 1) / kRun;
   const dim3 fgrid((unsigned)nsegs, max_runs > kFinRuns ? (max_runs + kFinRuns - 1) / kFinRuns : 1u);
   ESP_CARVE(sign_finalize_kernel<K_EFSIGN>);

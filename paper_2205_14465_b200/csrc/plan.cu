@@ -1022,7 +1022,8 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p.w->probe && b.nh1_units) probe_pair(p.w, &e0, &e1, b.h1_bytes);
   const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
-  if (e0 && !dgc) ESP_CUDA(cudaEventRecord(e0, st));
+  const bool sign = b.kind == ESP_EFSIGNSGD || b.kind == ESP_ONEBIT;
+  if (e0 && !dgc && !sign) ESP_CUDA(cudaEventRecord(e0, st));
   if (b.push) fused = false;   // local payload; push_kernel moves it (run_comm)
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
@@ -1041,14 +1042,14 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
       const int k = b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT;
       const int n = p.w->nranks;
       if (fused) launch_sign_h1_tma(k, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st,
-                                    b.dsts + (b.epoch & 1) * n, b.cnts, b.h1_dmode, n, b.h1_max_len);
+                                    b.dsts + (b.epoch & 1) * n, b.cnts, b.h1_dmode, n, b.h1_max_len, e0, e1);
       else launch_sign_h1_tma(k, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st, nullptr, nullptr, 0, 0,
-                              b.h1_max_len);
+                              b.h1_max_len, e0, e1);
       break;
     }
     default: launch_pack(b.h1, b.h1_units, b.nh1_units, st); break;
   }
-  if (e1 && !dgc) ESP_CUDA(cudaEventRecord(e1, st));
+  if (e1 && !dgc && !sign) ESP_CUDA(cudaEventRecord(e1, st));
   ESP_CUDA(cudaGetLastError());
   for (int lr = 0; lr < p.w->nlocal; ++lr) p.w->counters[lr].h1_calls += b.h1_calls * b.tens.size();
 }
