@@ -670,7 +670,10 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
 // group's candidates are addressed as one flat, index-ordered list:
 // off[i] = first flat position of run i (lane l holds runs 2l and 2l+1).
 static_assert(kRunsPerGroup == 64, "two run counts per lane");
-constexpr int kBatch = 4;            // candidate loads in flight per lane
+#ifndef ESP_KBATCH
+#define ESP_KBATCH 4
+#endif
+constexpr int kBatch = ESP_KBATCH;   // candidate loads in flight per lane
 constexpr uint32_t kDirect = 2048;   // refine: up to this many candidates, global atomics directly
 constexpr int kWarpsPerCta = kThreads / 32;
 

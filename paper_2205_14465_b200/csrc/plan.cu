@@ -75,6 +75,12 @@ struct Bucket {
   LocalBufs stage{};
   PushJob* push1 = nullptr; int npush1 = 0;
   PushJob* push2 = nullptr; int npush2 = 0;
+  // process-1 Gather/Broadcast: the root forwards all n payloads; its jobs read
+  // from anywhere in its arena (own payload: send, the others: recv1 of the
+  // call's parity), so there is one table per parity and src = arena base
+  PushJob* push2_odd = nullptr;
+  bool push2_arena = false;
+  size_t send_off = 0;
   const unsigned char** h2_pieces_odd = nullptr;   // h2 pieces of the parity-1 buffers
   const unsigned char** a7_pieces_odd = nullptr;
   unsigned char** dsts = nullptr;               // device [2][n]: my phase-1 slot in every rank's buffer
@@ -143,7 +149,7 @@ struct HostTables {
   std::vector<const unsigned char*> a7_pieces, a7_pieces_odd, h2_pieces, h2_pieces_odd;
   std::vector<uint32_t> rankterms;
   std::vector<uint4> off_jobs;
-  std::vector<PushJob> push1, push2;
+  std::vector<PushJob> push1, push2, push2_odd;
 };
 
 static bool fused_allgather_enabled() {
@@ -218,9 +224,9 @@ static void layout_buffers(Layout& L, Bucket& b, HostTables& T) {
   };
   b.fused = fused_allgather_enabled() && !w->sim && n > 1 && !none &&
             (b.routine == ESP_ALLGATHER || b.routine == ESP_ALLTOALL_ALLGATHER ||
-             (b.routine == ESP_GATHER_BROADCAST && p2));
+             b.routine == ESP_GATHER_BROADCAST);
   // (the fused producers write peers directly; the send buffer still serves esp_compress)
-  bufs(b.send, b.P * S);
+  b.send_off = bufs(b.send, b.P * S);
   // one real rank: every collective is the identity, so the receive buffers
   // alias the send/mid buffers and the collectives move nothing
   const bool solo = !w->sim && n == 1;
@@ -254,6 +260,13 @@ static void layout_buffers(Layout& L, Bucket& b, HostTables& T) {
       b.dst2_off = bufs(b.recv2, 2 * n * S);
       b.dst2_par = (size_t)n * S;
       b.dst2_slot = S;
+    } else if (!p2) {                                   // Gather/Broadcast, process 1
+      b.dst1_off = bufs(b.recv1, 2 * n * S);            // phase 1: every payload into the root's slot [src]
+      b.dst1_par = (size_t)n * S;
+      b.dst1_slot = S;
+      b.dst2_off = b.dst1_off;                          // phase 2: the root's n payloads into every
+      b.dst2_par = (size_t)n * S;                       // rank's recv1 (slot offsets in the jobs)
+      b.dst2_slot = 0;
     } else {                                            // Gather/Broadcast, process 2
       b.dst1_off = bufs(b.recv1, 2 * n * S);
       b.dst1_par = (size_t)n * S;
@@ -264,7 +277,8 @@ static void layout_buffers(Layout& L, Bucket& b, HostTables& T) {
       b.dst2_slot = 0;
     }
     // sparse a7 and Randomk have no producer-store variant
-    b.push = push_enabled() || (p2 && !quant) || b.kind == ESP_RANDOMK;
+    b.push = push_enabled() || (p2 && !quant) || b.kind == ESP_RANDOMK ||
+             (b.routine == ESP_GATHER_BROADCAST && !p2);
     if (b.push) {
       // jobs and arrivals per call (J jobs per slot)
       const uint64_t J = div_up(S, kPushChunk);
@@ -293,7 +307,25 @@ static void layout_buffers(Layout& L, Bucket& b, HostTables& T) {
             b.target2 = (n - 1) * J;
           }
           break;
-        default:   // Gather/Broadcast process 2: to the root, then the root's a7 to all
+        default:   // Gather/Broadcast
+          if (!p2) {
+            // process 1: to the root, then the root forwards all n payloads to
+            // everyone (a rank's own payload is read locally, never sent back)
+            if (!root) add_push(T.push1, 0, 0, S, 0);
+            if (root)
+              for (int d = 1; d < n; ++d)
+                for (int r = 0; r < n; ++r) {
+                  if (r == d) continue;
+                  const size_t src0 = r == 0 ? b.send_off : b.dst1_off + (size_t)r * S;
+                  add_push(T.push2, src0, (size_t)r * S, S, d);
+                  add_push(T.push2_odd, r == 0 ? src0 : src0 + b.dst1_par, (size_t)r * S, S, d);
+                }
+            b.push2_arena = true;
+            b.target1 = (n - 1) * J;
+            b.target2 = root ? 0 : (n - 1) * J;
+            break;
+          }
+          // process 2: to the root, then the root's a7 to all
           if (!root) add_push(T.push1, 0, 0, S, 0);
           if (root)
             for (int d = 1; d < n; ++d) add_push(T.push2, 0, 0, S, d);
@@ -804,6 +836,7 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     up(TB.off_jobs, b.h2_off_jobs);
     up(TB.push1, b.push1);
     up(TB.push2, b.push2);
+    up(TB.push2_odd, b.push2_odd);
     b.npush1 = (int)TB.push1.size();
     b.npush2 = (int)TB.push2.size();
     b.nh2_off_jobs = (int)TB.off_jobs.size();
@@ -1115,7 +1148,10 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
       dbg("push phase 1", cs);
     };
     auto push2 = [&] {
-      if (b.push) launch_push(b.push2, b.npush2, b.stage.at(0), b.dsts2 + par * n, b.cnts2, cs);
+      if (b.push && b.push2_arena)
+        launch_push(par ? b.push2_odd : b.push2, b.npush2, p.arena.base, b.dsts2 + par * n, b.cnts2, cs);
+      else if (b.push)
+        launch_push(b.push2, b.npush2, b.stage.at(0), b.dsts2 + par * n, b.cnts2, cs);
       dbg("push phase 2", cs);
     };
     push1();
@@ -1141,18 +1177,22 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
           count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * n * S, (n - 1) * n * S);
         }
         break;
-      default: {   // Gather/Broadcast, process 2
+      default: {   // Gather/Broadcast
         const bool root = w->rank == 0;
         count_coll(w, 0, ESP_OP_GATHER, root ? 0 : S, root ? (n - 1) * S : 0);
         if (root) {
           launch_wait_arrivals(b.my_cnt, e1 * b.target1, cs);
-        dbg("wait phase 1", cs);
-          if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
-          run_mid(p, b, cs);
-          if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
+          dbg("wait phase 1", cs);
+          if (quant) {   // process 2: the root's mid-scheme recompression
+            if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
+            run_mid(p, b, cs);
+            if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
+          }
           push2();
         }
-        count_coll(w, 0, ESP_OP_BROADCAST, root ? S : 0, root ? 0 : S);
+        // process 1 broadcasts the n payloads, process 2 one
+        const size_t bc = quant ? S : (size_t)n * S;
+        count_coll(w, 0, ESP_OP_BROADCAST, root ? bc : 0, root ? 0 : bc);
         launch_wait_arrivals(b.my_cnt + 1, e1 * b.target2, cs);
         dbg("wait phase 2", cs);
         break;
