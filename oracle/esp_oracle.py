@@ -27,6 +27,10 @@ Pins (tests/test_oracle_*.py, marker "not gpu"):
                         "parity unpinned" for the exact index choice.
   * aggregation         rank-order fp32 sum vs fp64 mean within 1e-6 relative
   * routines            routine equivalences, n = 1, rho = 1 reductions
+  * second residual r2  multi-step two-level EF telescoping for process 2 of both
+                        divisible routines (sum out + r2_T + mean r_T == mean sum g);
+                        exact closed-form a7 (scale2 = mean|A + r2|, class means)
+                        with a non-zero r2 on an input where every step is exact
   * bytes on wire       closed forms of the cost table, S:131-150 numbers
 """
 from __future__ import annotations
@@ -648,7 +652,19 @@ def option_time(cfg: Cfg, routine: str, numel: int, n: int, B: float, h1, h2) ->
     """Predicted sync time of one tensor: the cost table's row for the option
      with M = its payload, h(.) keyed by input bytes (R15)."""
     if cfg.kind == "none":
-        return table_comm_bytes("allreduce", 4 * numel, n) / B
+        # the uncompressed routines' volumes (P:55; S:126): Allreduce 2(n-1)M/n;
+        # Reduce-scatter (n-1)M/n + Allgather of the M/n shards (n-1)M/n;
+        # Reduce (n-1)M + Broadcast of the M-byte result M
+        M = 4.0 * numel
+        if n == 1:
+            return 0.0
+        if routine == "allreduce":
+            v = 2 * (n - 1) * M / n
+        elif routine == "reducescatter_allgather":
+            v = (n - 1) * M / n + (n - 1) * (M / n)
+        else:
+            v = (n - 1) * M + M
+        return v / B
     P = nparts_of(routine, n)
     M = chunk_bytes(cfg, numel, P) * P
     row = table_row(cfg, routine)

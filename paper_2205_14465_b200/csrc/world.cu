@@ -458,8 +458,12 @@ esp_status_t esp_option_time(const esp_option_t* o, size_t numel, int n, double 
   ESP_REQUIRE(pair_legal(o->cfg, o->routine), ESP_ERR_UNSUPPORTED, "illegal (compressor, routine) pair");
   const double in_bytes = 4.0 * (double)numel;
   if (o->cfg.kind == ESP_NONE) {
-    // uncompressed: communication only; all UT routines move 2(n-1)M/n
-    *out_seconds = (n > 1 ? 2.0 * (n - 1) * in_bytes / n : 0.0) / B;
+    // uncompressed: communication only.  Allreduce and Reduce-scatter +
+    // Allgather move 2(n-1)M/n; Reduce (n-1)M then Broadcast of
+    // the M-byte result M: nM
+    double v = 0.0;
+    if (n > 1) v = o->routine == ESP_REDUCE_BROADCAST ? (double)n * in_bytes : 2.0 * (n - 1) * in_bytes / n;
+    *out_seconds = v / B;
     return ESP_OK;
   }
   const int P = nparts_of(o->routine, n);

@@ -271,3 +271,99 @@ def test_sparse_process2_recompression(kind, routine):
         assert np.all(out[~sel] == 0)
         r2 = st[j].r2
         assert np.array_equal((out + r2).view(np.uint32), q.view(np.uint32))
+
+
+# ---- the second residual r2 of process 2 (reading R11; P:78-87 Alltoall/
+# Allgather, P:105-115 Gather/Broadcast) --------------------------------------
+P2_CASES = [(k, r) for k in ("efsignsgd", "onebit", "dgc", "randomk")
+            for r in ("alltoall_allgather", "gather_broadcast")]
+
+
+def _placed_r2(states, routine, N, n):
+    """The owners' second residuals placed at their tensor positions (A2A:
+    owner j holds partition j; G/B: the root holds the whole tensor)."""
+    out = np.zeros(N, np.float64)
+    if routine == "alltoall_allgather":
+        for j, (lo, hi) in enumerate(O.partitions(N, n)):
+            out[lo:hi] = states[j].r2
+    else:
+        out[:] = states[0].r2
+    return out
+
+
+@pytest.mark.parametrize("kind,routine", P2_CASES)
+def test_process2_two_level_ef_telescopes(kind, routine):
+    """Two-level error feedback conserves the gradient over T steps.  Per step,
+    rank r transmits t1_r = acc_r - r_r,new (first EF); the owner aggregates
+    A = mean_r t1_r, adds r2 and transmits t2 = q - r2_new (second EF); every
+    rank outputs t2.  Summing over steps telescopes:
+        sum_t out_t + r2_T + mean_r r_{r,T} == mean_r sum_t g_{r,t}
+    (exact in real arithmetic; here within the fp32 rounding of the adds).
+    Dropping r2 from q (q = A) leaves sum_t r2_t instead of r2_T: caught."""
+    n, N, T = 4, 1536, 6
+    # Randomk: unshared draws, else the second draw repeats the first's support
+    # and r2 stays 0 (nothing to pin)
+    cfg = O.Cfg(kind, 0.05, process=2, shared_indices=kind != "randomk")
+    st = O.new_states(n, N, routine, cfg)
+    s_out = np.zeros(N)
+    s_g = np.zeros(N)
+    mag = 0.0
+    for t in range(T):
+        grads = [gradient(N, rank=r, step=t, tensor=3) for r in range(n)]
+        res = O.sync(routine, cfg, grads, st, tensor_id=3)
+        s_out += res.outs[0].astype(np.float64)
+        s_g += sum(g.astype(np.float64) for g in grads) / n
+        mag = max(mag, max(float(np.abs(g).max()) for g in grads), float(np.abs(res.outs[0]).max()))
+    lhs = s_out + _placed_r2(st, routine, N, n) + sum(s.r.astype(np.float64) for s in st) / n
+    # each step adds a few fp32 roundings of values <= a few x mag per element
+    tol = 8 * T * float(np.spacing(np.float32(4 * mag)))
+    assert np.max(np.abs(lhs - s_g)) <= tol
+    # r2 must actually be carrying something for the pin to bite
+    assert np.abs(_placed_r2(st, routine, N, n)).max() > 100 * tol
+
+
+def _dyadic(rng, n, lo=-8, hi=8, den=8):
+    return (rng.integers(lo, hi + 1, n) / den).astype(np.float32)
+
+
+@pytest.mark.parametrize("kind", ["efsignsgd", "onebit"])
+@pytest.mark.parametrize("routine", ["alltoall_allgather", "gather_broadcast"])
+def test_quantized_a7_closed_form_with_nonzero_r2(kind, routine):
+    """a7 on an input where every step is exact (P:78-87 / P:105-115 with EF):
+    ranks send all-equal magnitudes c_r with random signs, so the first
+    compression is lossless (scale = c_r, or class means c_r / -c_r) and the
+    owner's aggregate is A = (g_0 + g_1) / 2 exactly.  With a non-zero second
+    residual d (dyadic), q = A + d is exact, and the recompression must be the
+    closed form scale2 = sum|q| / len (class means for Onebit), bits q >= 0,
+    r2_new = q - decode -- computed here in exact rational arithmetic."""
+    from fractions import Fraction as F
+    n, N = 2, 64
+    cfg = O.Cfg(kind, process=2)
+    rng = np.random.default_rng(7)
+    signs = [np.where(rng.random(N) < 0.5, -1.0, 1.0).astype(np.float32) for _ in range(n)]
+    grads = [signs[0] * np.float32(1.0), signs[1] * np.float32(0.5)]
+    st = O.new_states(n, N, routine, cfg)
+    parts = O.partitions(N, n) if routine == "alltoall_allgather" else [(0, N)]
+    owners = list(range(n)) if routine == "alltoall_allgather" else [0]
+    d_full = _dyadic(rng, N)
+    for j, (lo, hi) in zip(owners, parts):
+        st[j].r2 = d_full[lo:hi].copy()
+    res = O.sync(routine, cfg, grads, st)
+    for j, (lo, hi) in zip(owners, parts):
+        A = [(F(float(grads[0][i])) + F(float(grads[1][i]))) / 2 for i in range(lo, hi)]
+        q = [a + F(float(d_full[i])) for a, i in zip(A, range(lo, hi))]
+        if kind == "efsignsgd":
+            s = sum(abs(x) for x in q) / len(q)
+            dec = [s if x >= 0 else -s for x in q]
+        else:
+            pos = [x for x in q if x >= 0]
+            neg = [x for x in q if x < 0]
+            mp = sum(pos) / len(pos) if pos else F(0)
+            mn = sum(neg) / len(neg) if neg else F(0)
+            dec = [mp if x >= 0 else mn for x in q]
+        # decoded values are exactly representable here (dyadic / 32 or / class size
+        # rounded once to fp32): compare in fp32
+        want = np.array([float(x) for x in dec], np.float32)
+        assert np.array_equal(res.outs[0][lo:hi], want), (j, kind, routine)
+        want_r2 = np.array([float(x) for x in q], np.float32) - want
+        assert np.array_equal(st[j].r2, want_r2.astype(np.float32))

@@ -52,6 +52,18 @@ def test_option_time_closed_form():
         2 * 3 * 4 * N / 4 / B, rel=1e-12)
 
 
+@pytest.mark.parametrize("routine,ms", [("allreduce", 12.0), ("reducescatter_allgather", 12.0),
+                                        ("reduce_broadcast", 32.0)])
+def test_uncompressed_routine_times_spec_examples(routine, ms):
+    """Per-step volumes of S:126 at n = 4, M = 1e8 B, B = 1.25e10 B/s:
+    Allreduce 2(n-1)M/(nB) = 12 ms; Reduce-scatter (n-1)M/(nB) = 6 ms + Allgather
+    of the shards 6 ms; Reduce (n-1)M/B = 24 ms + Broadcast of the M-byte result
+    M/B = 8 ms."""
+    N, n, B = 25_000_000, 4, 1.25e10
+    assert O.option_time(O.Cfg("none", 1.0), routine, N, n, B, None, None) == pytest.approx(ms * 1e-3, rel=1e-12)
+    assert E.option_time(E.make_option("none", 1.0, routine), N, n, B) == pytest.approx(ms * 1e-3, rel=1e-12)
+
+
 def _random_curve(rng):
     xs = sorted({2 ** rng.randint(8, 30) for _ in range(6)})
     t, out = rng.uniform(5e-6, 5e-5), []
@@ -61,7 +73,7 @@ def _random_curve(rng):
     return out
 
 
-OPTS = [("none", "allreduce", 0), ("randomk", "allreduce", 0), ("dgc", "allgather", 0),
+OPTS = [("none", "allreduce", 0), ("none", "reduce_broadcast", 0), ("none", "reducescatter_allgather", 0), ("randomk", "allreduce", 0), ("dgc", "allgather", 0),
         ("dgc", "alltoall_allgather", 1), ("dgc", "alltoall_allgather", 2), ("dgc", "gather_broadcast", 1),
         ("dgc", "gather_broadcast", 2), ("efsignsgd", "allgather", 0), ("efsignsgd", "alltoall_allgather", 2),
         ("onebit", "gather_broadcast", 2), ("randomk", "alltoall_allgather", 1)]
