@@ -165,6 +165,17 @@ esp_status_t esp_world_set_bucket_elems(esp_world_t w, uint64_t elems);
  * launches had to move (12 B/elem with EF, +1/8 B/elem of sign bits), then
  * clears the record. */
 esp_status_t esp_world_set_probe(esp_world_t w, int enable);
+/* Fused collectives (n > 1): a rank waits for its peers' payloads on the GPU.
+ * If a payload has not arrived after `seconds` of wall time (default 300), the
+ * wait gives up, the call's output is invalid, and esp_world_check plus every
+ * later esp_sync / esp_sync_many return ESP_ERR_NCCL (the world is unusable). */
+esp_status_t esp_world_set_timeout(esp_world_t w, double seconds);
+/* Execution plans (bucketing, device tables, buffers) are cached per tensor
+ * list.  set_plan_cache bounds the cache (least recently used plans are freed;
+ * default 16); drop_plans frees all of them (e.g. when a training framework
+ * rebuilds its gradient buckets).  Every rank must make the same calls. */
+esp_status_t esp_world_set_plan_cache(esp_world_t w, int max_plans);
+esp_status_t esp_world_drop_plans(esp_world_t w);
 esp_status_t esp_probe_read(esp_world_t w, double* ms, uint64_t* launches, uint64_t* bytes);
 
 /* ---- ctx: one tensor's option + EF state ----------------------------------

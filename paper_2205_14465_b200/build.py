@@ -40,22 +40,37 @@ def _nvcc():
 def _flags(nd):
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
                    "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(nd, "include"),
-                   "-I", os.path.join(ROOT, "include"), "-diag-suppress", "186",
-                   *os.environ.get("ESP_NVCC_EXTRA", "").split()]   # tuning experiments only
+                   "-I", os.path.join(ROOT, "include"), "-diag-suppress", "186"]
 
 
-def _deps_mtime():
-    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "esp.h")]
-    return max(os.path.getmtime(f) for f in files)
+def _fingerprint(flags) -> str:
+    """sha256 over every source and header byte and the compiler flags: the
+    library is rebuilt whenever any of them differs from what built it
+    (file timestamps do not survive copies, so they are not trusted)."""
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)) + [os.path.join(ROOT, "include", "esp.h")]
+    for f in files:
+        h.update(os.path.basename(f).encode() + b"\0")
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    h.update(" ".join(flags).encode())
+    return h.hexdigest()
+
+
+STAMP = LIB + ".sha256"
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     nd = nccl_dir()
     os.makedirs(OBJ, exist_ok=True)
-    newest = _deps_mtime()
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
     flags = _flags(nd)
+    fp = _fingerprint(flags)
+    if not force and os.path.exists(LIB) and os.path.exists(STAMP):
+        with open(STAMP) as fh:
+            if fh.read().strip() == fp:
+                return LIB
+    print(f"[libesp] compiling {len(SOURCES)} sources for sm_100a -> {LIB}", file=sys.stderr)
 
     def compile_one(src):
         obj = os.path.join(OBJ, src.replace(".cu", ".o"))
@@ -76,6 +91,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(LIB + ".tmp", LIB)
+    with open(STAMP, "w") as fh:
+        fh.write(fp + "\n")
     return LIB
 
 

@@ -99,7 +99,13 @@ struct esp_world_s {
   std::vector<cudaEvent_t> probe_pool;
   size_t probe_used = 0;
   std::vector<uint64_t> probe_bytes;
-  std::vector<esp::Plan*> plans;           // owned; freed by esp::clear_plans
+  std::vector<esp::Plan*> plans;           // owned; freed by esp::clear_plans (LRU order, most recent last)
+  size_t plan_cap = 16;                    // cached plans kept per world (least recently used evicted)
+  // fused collectives: a wait kernel that saw no arrival within wait_timeout_ns
+  // sets the mapped word *wait_err_host (device alias wait_err)
+  unsigned int* wait_err_host = nullptr;
+  unsigned int* wait_err = nullptr;
+  unsigned long long wait_timeout_ns = 300ull * 1000000000ull;
   std::set<esp_ctx_s*> ctxs;
 };
 
@@ -168,6 +174,7 @@ void execute_plan(Plan* p, float* const* grads, cudaStream_t st);
 // h1 only, copying each rank's payload to `payload` (esp_compress)
 void execute_compress(Plan* p, const float* grad, void* payload, cudaStream_t st);
 void clear_plans(esp_world_s* w);
+void trim_plans(esp_world_s* w);   // evict least recently used plans down to w->plan_cap
 
 }  // namespace esp
 

@@ -15,16 +15,10 @@ constexpr int kNJ = kRun / 128;          // float4 per lane per run
 constexpr int kDgcTile = 8 * kRun;       // DGC streaming tile (one run per consumer warp)
 constexpr int kSignSpan = 1024;          // sign h1: elements per warp per unit
 constexpr int kUnit = 8192;              // 8 runs per CTA
-#ifndef ESP_SIGN_UNIT
-#define ESP_SIGN_UNIT 8192
-#endif
-constexpr int kSignUnit = ESP_SIGN_UNIT;  // sign h2: elements per CTA (one prologue per 128 KB of output)
+constexpr int kSignUnit = 8192;  // sign h2: elements per CTA (one prologue per 128 KB of output)
 constexpr int kRunsPerGroup = 64;        // DGC finalize: runs per warp-group (32768 elements)
 constexpr int kSample = 4096;            // DGC sampled-threshold sample size
-#ifndef ESP_H2_TILE
-#define ESP_H2_TILE 1024
-#endif
-constexpr int kTile = ESP_H2_TILE;       // sparse h2 output tile (one warp each)
+constexpr int kTile = 1024;      // sparse h2 output tile (one warp each)
 constexpr int kTileThreads = 128;        // sparse h2 CTA size (4 warps = 4 tiles in flight)
 constexpr int kOffJob = 4096;            // sparse h2 tile-offset pass: entries per CTA
 
@@ -56,8 +50,6 @@ struct SegH1 {
   const uint64_t* step;  // &dyn[nslots + slot]: step counter (Randomk draws)
   float* r;              // EF state: residual (sparse) / previous p (sign, lazy EF)
   unsigned char* chunk;  // output chunk
-  uint32_t chunk_off;    // the chunk's offset within a slot (fused Allgather destinations)
-  uint32_t pad0_;
   const float* lazy_in;  // sign: {scale} / onebit: {mneg, mpos} of the previous step
   float* lazy_out;       // written by the last CTA of the segment
   uint32_t n;            // segment length (elements)

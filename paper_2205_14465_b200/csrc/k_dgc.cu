@@ -358,7 +358,7 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& s
 template <int NCG, bool MOM = false>
 __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(const SegH1* __restrict__ segs,
                                                                             const uint32_t* __restrict__ unit_seg,
-                                                                            uint32_t nunits, int variant, int ns) {
+                                                                            uint32_t nunits, int ns) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
   if (warp == NCG * kThreads / 32) {
     // ---- producer warp: one elected lane streams tiles into the ring
     if (lane == 0) {
-      const uint64_t pol = (variant & 1) ? policy_evict_first() : policy_evict_normal();
+      const uint64_t pol = policy_evict_normal();
       // per-segment values are cached; the unit table is prefetched one ahead
       uint32_t cur = 0xFFFFFFFFu, unit0 = 0, n = 0;
       const float* gseg = nullptr;
@@ -670,10 +670,7 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
 // group's candidates are addressed as one flat, index-ordered list:
 // off[i] = first flat position of run i (lane l holds runs 2l and 2l+1).
 static_assert(kRunsPerGroup == 64, "two run counts per lane");
-#ifndef ESP_KBATCH
-#define ESP_KBATCH 4
-#endif
-constexpr int kBatch = ESP_KBATCH;   // candidate loads in flight per lane
+constexpr int kBatch = 4;   // candidate loads in flight per lane
 constexpr uint32_t kDirect = 2048;   // refine: up to this many candidates, global atomics directly
 constexpr int kWarpsPerCta = kThreads / 32;
 
@@ -882,10 +879,7 @@ __device__ __forceinline__ unsigned long long lb_pack(uint32_t flag, uint32_t ab
 
 __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __restrict__ segs,
                                                              const uint32_t* __restrict__ group_seg,
-                                                             uint32_t ngroups,
-                                                             unsigned char* const* __restrict__ dsts,
-                                                             unsigned long long* const* __restrict__ cnts,
-                                                             int ndst) {
+                                                             uint32_t ngroups) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t gi = blockIdx.x * kWarpsPerCta + w;
@@ -969,19 +963,8 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __r
       const uint32_t sb = __ballot_sync(0xffffffffu, sel);
       const uint32_t pos = sel_run + __popc(sb & lt_mask);
       if (sel) {
-        if (dsts) {
-          // fused Allgather: the entry goes straight into this rank's slot of
-          // every rank's receive buffer over NVLink (consecutive lanes write
-          // consecutive positions: coalesced peer stores)
-          for (int d = 0; d < ndst; ++d) {
-            unsigned char* ch = dsts[d] + S.chunk_off;
-            reinterpret_cast<uint32_t*>(ch)[pos] = c.x;
-            reinterpret_cast<float*>(ch + 4 * (size_t)S.kpad)[pos] = __uint_as_float(c.y);
-          }
-        } else {
-          out_idx[pos] = c.x;
-          out_val[pos] = __uint_as_float(c.y);
-        }
+        out_idx[pos] = c.x;
+        out_val[pos] = __uint_as_float(c.y);
         if (S.ef) S.r[c.x] = 0.0f;
         if (S.mom) S.mom[c.x] = 0.0f;   // momentum factor masking (R20)
       }
@@ -989,36 +972,40 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __r
       sel_run += __popc(sb);
     }
   }
-  if (dsts) {
-    // publish: the barrier orders the CTA's peer stores before thread 0's
-    // system-scope fence (cumulative), which precedes the arrival increments
-    // (one per group of the CTA, as the waiting side counts groups)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint32_t first = blockIdx.x * kWarpsPerCta;
-      const unsigned long long mine = first < ngroups ? min((uint32_t)kWarpsPerCta, ngroups - first) : 0u;
-      __threadfence_system();
-      for (int d = 0; d < ndst; ++d) atomicAdd_system(cnts[d], mine);
-    }
-  }
 }
 
-__global__ void wait_arrivals_kernel(const unsigned long long* cnt, unsigned long long target) {
+// Blocks the stream until *cnt >= target.  A peer that has not arrived after
+// timeout_ns of wall time (%globaltimer, independent of the SM clock) is an
+// error, not a hang: the kernel records it in the world's mapped error word
+// and returns; esp_world_check and the next esp_sync* call report it (the
+// consumers of this call then read an incomplete payload).  No __trap: a trap
+// would destroy the CUDA context of the whole process.
+__global__ void wait_arrivals_kernel(const unsigned long long* cnt, unsigned long long target,
+                                     unsigned int* err, unsigned long long timeout_ns) {
   if (threadIdx.x != 0) return;
-  const long long t0 = clock64();
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  uint32_t sleep = 32;
   while (true) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
     if (v >= target) break;
-    __nanosleep(200);
-    if (clock64() - t0 > 20000000000ll) __trap();   // ~10 s: a peer never arrived
+    __nanosleep(sleep);
+    if (sleep < 1024) sleep <<= 1;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      atomicExch_system(err, 1u);
+      __threadfence_system();
+      break;
+    }
   }
 }
 
-void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, cudaStream_t st) {
+void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, unsigned int* err,
+                          unsigned long long timeout_ns, cudaStream_t st) {
   if (target == 0) return;   // nothing to wait for (e.g. the root's own broadcast)
-  ESP_CARVE(wait_arrivals_kernel);
-  wait_arrivals_kernel<<<1, 32, 0, st>>>(cnt, target);
+  wait_arrivals_kernel<<<1, 32, 0, st>>>(cnt, target, err, timeout_ns);
   count_launches(1);
 }
 
@@ -1037,14 +1024,8 @@ static int num_sms() {
 // persistent streaming kernels: one CTA per SM (measured best on B200)
 int tma_stream_grid(int nunits) { return nunits < num_sms() ? nunits : num_sms(); }
 
-int tma_stream_stages() {
-  static const int stages = [] {
-    const char* e = getenv("ESP_TMA_STAGES");
-    const int s = e ? atoi(e) : 4;
-    return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
-  }();
-  return stages;
-}
+// ring depth of the streaming kernels (measured flat from 3 to 6 on B200)
+int tma_stream_stages() { return 4; }
 
 // ESP_DEBUG_SYNC=1: synchronize after every kernel of the DGC pipeline and name
 // the one that failed (debugging aid; off by default)
@@ -1063,97 +1044,45 @@ static void debug_sync(const char* what, cudaStream_t st) {
 
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
-                   cudaEvent_t probe1, unsigned char* const* dsts, unsigned long long* const* cnts,
-                   int ndst, bool mom) {
+                   cudaEvent_t probe1, bool mom) {
   if (nsegs == 0) return;
-  static const bool attr_set = [] {
-    const int bytes = (int)(kStreamHdr + kMaxStages * kStageBytes);
-    return cudaFuncSetAttribute(dgc_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+  // three consumer groups of 8 warps over a 3-stage ring of 32 KB (plain EF);
+  // two groups over 4 stages of 48 KB with the momentum stream (R20) -- the
+  // configurations measured fastest on B200 (DESIGN.md tuning log)
+  constexpr int kNs = 3, kNsMom = 4;
+  const size_t smem = kStreamHdr + kNs * kStageBytes;
+  const size_t mom_smem = kStreamHdr + kNsMom * kStageBytesMom;
+  static const bool attr_set = [&] {
+    return cudaFuncSetAttribute(dgc_stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
                cudaSuccess &&
-           cudaFuncSetAttribute(dgc_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
-               cudaSuccess &&
-           cudaFuncSetAttribute(dgc_stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
-               cudaSuccess &&
-           cudaFuncSetAttribute(dgc_stream_kernel<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(kStreamHdr + kMaxStagesMom * kStageBytesMom)) == cudaSuccess &&
            cudaFuncSetAttribute(dgc_stream_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(kStreamHdr + kMaxStagesMom * kStageBytesMom)) == cudaSuccess &&
-           cudaFuncSetAttribute(dgc_stream_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(kStreamHdr + kMaxStagesMom * kStageBytesMom)) == cudaSuccess;
+                                (int)mom_smem) == cudaSuccess;
   }();
   (void)attr_set;
   num_sms();
-  // tuning knobs (measured on B200): bit0 of ESP_TMA_VARIANT = L2
-  // evict-first hint on the tile loads, bit2 = one consumer group, bit3 = two; ESP_TMA_STAGES
-  static const int variant = [] {
-    const char* e = getenv("ESP_TMA_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  const int stages = tma_stream_stages();
   const char* ff = getenv("ESP_DGC_FORCE_FALLBACK");   // read per launch: a test hook
-  // sample-rank margin in standard deviations of the sample count (a sampler
-  // knob: a miss only sends that segment through the fallback recompaction)
-  static const float margin = [] {
-    const char* e = getenv("ESP_DGC_MARGIN");
-    return e ? (float)atof(e) : 4.0f;
-  }();
-  ESP_CARVE(dgc_sample_kernel);
-  dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs, ff ? atoi(ff) : 0, margin);
+  // sample-rank margin in standard deviations of the sample count (4: 2 and 1
+  // measured to send segments through the fallback recompaction)
+  constexpr float kMargin = 4.0f;
+  dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs, ff ? atoi(ff) : 0, kMargin);
   debug_sync("dgc_sample", st);
   if (probe0) cudaEventRecord(probe0, st);
-  {
-    const int grid = nunits < g_num_sms ? nunits : g_num_sms;
-    // momentum correction: three tiles per stage (R20); ESP_MOM_GROUPS = consumer
-    // groups (stages: 3 for three groups, else 4)
-    static const int mom_groups = [] {
-      const char* e = getenv("ESP_MOM_GROUPS");
-      const int g = e ? atoi(e) : 2;
-      return g < 1 ? 1 : (g > 3 ? 3 : g);
-    }();
-    const size_t mom_smem = kStreamHdr + kMaxStagesMom * kStageBytesMom;
-    ESP_CARVE(dgc_stream_kernel<3, true>);
-    ESP_CARVE(dgc_stream_kernel<2, true>);
-    ESP_CARVE(dgc_stream_kernel<1, true>);
-    ESP_CARVE(dgc_stream_kernel<1>);
-    ESP_CARVE(dgc_stream_kernel<2>);
-    ESP_CARVE(dgc_stream_kernel<3>);
-    if (mom && mom_groups == 3)
-      dgc_stream_kernel<3, true><<<grid, 3 * kThreads + 32, mom_smem, st>>>(segs, unit_seg, (uint32_t)nunits,
-                                                                            variant, 3);
-    else if (mom && mom_groups == 2)
-      dgc_stream_kernel<2, true><<<grid, 2 * kThreads + 32, mom_smem, st>>>(segs, unit_seg, (uint32_t)nunits,
-                                                                            variant, 4);
-    else if (mom)
-      dgc_stream_kernel<1, true><<<grid, kThreads + 32, mom_smem, st>>>(segs, unit_seg, (uint32_t)nunits,
-                                                                        variant, 4);
-    else if (variant & 4)   // one consumer group (A/B experiments)
-      dgc_stream_kernel<1><<<grid, kThreads + 32, kStreamHdr + stages * kStageBytes, st>>>(
-          segs, unit_seg, (uint32_t)nunits, variant, stages);
-    else if (variant & 8) {   // two groups
-      const int ns = stages < 2 ? 2 : stages & ~1;
-      dgc_stream_kernel<2><<<grid, 2 * kThreads + 32, kStreamHdr + ns * kStageBytes, st>>>(
-          segs, unit_seg, (uint32_t)nunits, variant, ns);
-    } else {                  // three groups (default)
-      const int ns = stages < 3 ? 3 : stages - stages % 3;
-      dgc_stream_kernel<3><<<grid, 3 * kThreads + 32, kStreamHdr + ns * kStageBytes, st>>>(
-          segs, unit_seg, (uint32_t)nunits, variant, ns);
-    }
-  }
+  const int grid = nunits < g_num_sms ? nunits : g_num_sms;
+  if (mom)
+    dgc_stream_kernel<2, true><<<grid, 2 * kThreads + 32, mom_smem, st>>>(segs, unit_seg, (uint32_t)nunits, kNsMom);
+  else
+    dgc_stream_kernel<3><<<grid, 3 * kThreads + 32, smem, st>>>(segs, unit_seg, (uint32_t)nunits, kNs);
   debug_sync("dgc_stream", st);
   if (probe1) cudaEventRecord(probe1, st);
-  ESP_CARVE(dgc_fallback_kernel);
   dgc_fallback_kernel<<<g_num_sms, kThreads, 0, st>>>(segs, nsegs);
   debug_sync("dgc_fallback", st);
   const int wgrid = (ngroups + kWarpsPerCta - 1) / kWarpsPerCta;   // one warp per finalize group
   if (wgrid > 0) {
-    ESP_CARVE(dgc_refine_kernel<2>);
     dgc_refine_kernel<2><<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_refine<2>", st);
-    ESP_CARVE(dgc_refine_kernel<3>);
     dgc_refine_kernel<3><<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_refine<3>", st);
-    ESP_CARVE(dgc_write_kernel);
-    dgc_write_kernel<<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups, dsts, cnts, ndst);
+    dgc_write_kernel<<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_write", st);
   }
   count_launches(6);

@@ -364,7 +364,6 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const SegH1* __restrict_
 void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
                       const unsigned char* const* pieces, int max_pieces, cudaStream_t st) {
   if (ntiles == 0) return;
-  ESP_CARVE(h2_sparse_offsets_kernel);
   h2_sparse_offsets_kernel<<<njobs, kThreads, 0, st>>>(segs, jobs, pieces);
   constexpr int kSmem = kTileThreads / 32 * kTile * (int)sizeof(float);
   auto cap = [](int smem) {
@@ -379,7 +378,6 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
   const int grid_cap = max_pieces > 1 ? capn : cap1;
   const int need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);   // one warp per tile
   const int grid = need < grid_cap ? need : grid_cap;
-  ESP_CARVE(h2_sparse_kernel);
   h2_sparse_kernel<<<grid, kTileThreads, smem, st>>>(segs, tile_seg, (uint32_t)ntiles, pieces);
   count_launches(2);
 }
@@ -395,8 +393,6 @@ void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int n
     return sms * (per_sm > 0 ? per_sm : 4);
   }();
   const int grid = nunits < cap ? nunits : cap;
-  ESP_CARVE(h2_sign_kernel<K_EFSIGN>);
-  ESP_CARVE(h2_sign_kernel<K_ONEBIT>);
   if (kind == K_EFSIGN) h2_sign_kernel<K_EFSIGN><<<grid, kThreads, 0, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
   else h2_sign_kernel<K_ONEBIT><<<grid, kThreads, 0, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
   count_launches(1);
@@ -405,14 +401,12 @@ void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int n
 void launch_h2_dense(const SegH2* segs, const uint32_t* unit_seg, int nunits,
                      const unsigned char* const* pieces, cudaStream_t st) {
   if (nunits == 0) return;
-  ESP_CARVE(h2_dense_kernel);
   h2_dense_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
   count_launches(1);
 }
 
 void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st) {
   if (nunits == 0) return;
-  ESP_CARVE(pack_kernel);
   pack_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg);
   count_launches(1);
 }

@@ -51,7 +51,6 @@ __global__ void __launch_bounds__(kPushThreads) push_kernel(const PushJob* __res
 void launch_push(const PushJob* jobs, int njobs, const unsigned char* src, unsigned char* const* dsts,
                  unsigned long long* const* cnts, cudaStream_t st) {
   if (njobs == 0) return;
-  ESP_CARVE(push_kernel);
   push_kernel<<<njobs, kPushThreads, 0, st>>>(jobs, src, dsts, cnts);
   count_launches(1);
 }

@@ -42,7 +42,6 @@ struct RandomkOp {
   };
   const unsigned char* const* pieces = nullptr;   // not a decoding op
   bool stage_words = false;
-  __device__ bool sys_fence() const { return false; }
   template <int BAR>
   __device__ void begin_segment(const SegH1& S, State& st, TmaGroup&) const {
     st.h = randomk_hash(S.hash, *S.step, S.part, S.rankterm);
@@ -149,7 +148,6 @@ void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, 
 void launch_h2_randomk(const SegH2* segs, const uint32_t* unit_seg, int nunits,
                        const unsigned char* const* pieces, const uint32_t* rankterms, cudaStream_t st) {
   if (nunits == 0) return;
-  ESP_CARVE(h2_randomk_kernel);
   h2_randomk_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces, rankterms);
   count_launches(1);
 }

@@ -51,13 +51,6 @@ struct SignOp {
   // DECODE: stage the pieces' sign words in the tile's g slot by TMA (the stage
   // is then held until they are used) instead of loading them with LDG
   bool stage_words = false;
-  // fused collective (NVLink peer stores): dmode 0 = the local chunk S.chunk,
-  // 1 = dsts[S.part] + S.chunk_off (the partition owner), 2 = dsts[d] +
-  // S.chunk_off for every d < ndst
-  unsigned char* const* dsts = nullptr;
-  int dmode = 0, ndst = 0;
-  bool fence = false;
-  __device__ bool sys_fence() const { return fence; }
   struct State {
     float sp, sn;                            // lazy EF: last step's scale pair
     float qsp0, qsn0, qsp1, qsn1;            // DECODE: scales of pieces lane, lane + 32
@@ -181,13 +174,7 @@ struct SignOp {
     }
     if (lane < kRun / 32 && base + lane * 32 < n) {
       const uint32_t wi = (base >> 5) + lane;
-      if (dmode == 0) {
-        reinterpret_cast<uint32_t*>(S.chunk + 16)[wi] = myword;
-      } else if (dmode == 1) {
-        reinterpret_cast<uint32_t*>(dsts[S.part] + S.chunk_off + 16)[wi] = myword;
-      } else {
-        for (int d = 0; d < ndst; ++d) reinterpret_cast<uint32_t*>(dsts[d] + S.chunk_off + 16)[wi] = myword;
-      }
+      reinterpret_cast<uint32_t*>(S.chunk + 16)[wi] = myword;
     }
     // the run's partial (fixed xor tree), slot = run index
 #pragma unroll
@@ -221,15 +208,9 @@ struct SignOp {
 // order.  The result does not depend on the grid of the streaming pass, and a
 // single large tensor is reduced by many CTAs (one CTA per segment serialised
 // the 2^28-element sweep sizes).
-// Fused collective (dmode != 0): the header goes to the destination chunk(s),
-// then one system-scope fence and one arrival per destination (the words were
-// stored by the streaming pass that precedes this kernel in stream order).
 constexpr uint32_t kFinRuns = 16384;
 template <int KIND>
-__global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __restrict__ segs,
-                                                                 unsigned char* const* __restrict__ dsts,
-                                                                 unsigned long long* const* __restrict__ cnts,
-                                                                 int dmode, int ndst) {
+__global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __restrict__ segs) {
   __shared__ double shd[8];
   __shared__ uint32_t shu[16];
   __shared__ int last;
@@ -299,18 +280,8 @@ __global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __
       x0 = ca ? (float)(a / (double)ca) : 0.f;  // mean of {p < 0} (R8)
       x1 = cb ? (float)(b / (double)cb) : 0.f;  // mean of {p >= 0}
     }
-    auto put = [&](float* h) {
-      h[0] = x0;
-      if (KIND == K_ONEBIT) h[1] = x1;
-    };
-    if (dmode == 0) {
-      put(hdr);
-    } else {
-      const int d0 = dmode == 1 ? (int)S.part : 0, d1 = dmode == 1 ? (int)S.part + 1 : ndst;
-      for (int d = d0; d < d1; ++d) put(reinterpret_cast<float*>(dsts[d] + S.chunk_off));
-      __threadfence_system();
-      for (int d = d0; d < d1; ++d) atomicAdd_system(cnts[d], 1ull);
-    }
+    hdr[0] = x0;
+    if (KIND == K_ONEBIT) hdr[1] = x1;
     if (S.ef) {
       S.lazy_out[0] = x0;
       S.lazy_out[1] = x1;
@@ -331,34 +302,23 @@ __global__ void sign_materialize_kernel(const float* __restrict__ p, const float
 }
 
 void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
-                        const unsigned char* const* pieces, cudaStream_t st, unsigned char* const* dsts,
-                        unsigned long long* const* cnts, int dmode, int ndst, uint32_t max_len,
+                        const unsigned char* const* pieces, cudaStream_t st, uint32_t max_len,
                         cudaEvent_t probe0, cudaEvent_t probe1) {
   if (nunits == 0) return;
-  static const bool stage = [] {   // ESP_A7_STAGE=0: load the pieces' words by LDG
-    const char* e = getenv("ESP_A7_STAGE");
-    return !e || atoi(e) != 0;
-  }();
-  if (!dsts) dmode = 0;
-  static const bool fence = [] {
-    const char* e = getenv("ESP_SYS_FENCE");
-    return e && atoi(e) != 0;
-  }();
+  // a7 stages the pieces' sign words by TMA (measured faster than LDG)
   if (probe0) cudaEventRecord(probe0, st);   // the roofline probe brackets the streaming pass only
   if (kind == K_EFSIGN) {
-    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, true>{pieces, stage, dsts, dmode, ndst, fence && dmode}, st);
-    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, false>{nullptr, false, dsts, dmode, ndst, fence && dmode}, st);
+    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, true>{pieces, true}, st);
+    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, false>{nullptr, false}, st);
   } else {
-    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, true>{pieces, stage, dsts, dmode, ndst, fence && dmode}, st);
-    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, false>{nullptr, false, dsts, dmode, ndst, fence && dmode}, st);
+    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, true>{pieces, true}, st);
+    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, false>{nullptr, false}, st);
   }
   if (probe1) cudaEventRecord(probe1, st);
   const uint32_t max_runs = (max_len + kRun - 1) / kRun;
   const dim3 fgrid((unsigned)nsegs, max_runs > kFinRuns ? (max_runs + kFinRuns - 1) / kFinRuns : 1u);
-  ESP_CARVE(sign_finalize_kernel<K_EFSIGN>);
-  ESP_CARVE(sign_finalize_kernel<K_ONEBIT>);
-  if (kind == K_EFSIGN) sign_finalize_kernel<K_EFSIGN><<<fgrid, kThreads, 0, st>>>(segs, dsts, cnts, dmode, ndst);
-  else sign_finalize_kernel<K_ONEBIT><<<fgrid, kThreads, 0, st>>>(segs, dsts, cnts, dmode, ndst);
+  if (kind == K_EFSIGN) sign_finalize_kernel<K_EFSIGN><<<fgrid, kThreads, 0, st>>>(segs);
+  else sign_finalize_kernel<K_ONEBIT><<<fgrid, kThreads, 0, st>>>(segs);
   count_launches(1);
 }
 

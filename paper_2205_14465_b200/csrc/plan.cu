@@ -54,24 +54,25 @@ struct Bucket {
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
   // ---- compression fused with the collective over NVLink peer memory
-  // (DESIGN.md 9): the producing kernel (DGC write, sign
-  // h1 / a7) stores its payload straight into the receiving ranks' buffers
+  // (DESIGN.md 9): the producers (DGC write, sign h1 /
+  // a7) write their payload locally, then push_kernel copies each slot
+  // straight to its final place in the receiving ranks' buffers
   // (double-buffered by call parity) and bumps their arrival counters; the
   // consumer starts after a wait kernel has seen this call's arrivals.
-  //   phase 1 = h1 -> recv1 (Allgather, Alltoall, Gather) or recv2 (sparse
+  //   phase 1 = send -> recv1 (Allgather, Alltoall, Gather) or recv2 (sparse
   //             Alltoall/Allgather: chunk (part, src) goes straight to its
   //             final place on every rank, the forwarding hop disappears)
-  //   phase 2 = a7 -> recv2 (quantized Alltoall/Allgather) or mid (quantized
-  //             Gather/Broadcast, from the root)
+  //   phase 2 = stage (a7's output) -> recv2 (quantized Alltoall/Allgather)
+  //             or mid (quantized Gather/Broadcast, from the root)
   bool fused = false;
-  int h1_dmode = 0;                             // sign h1: 1 = to the partition owner, 2 = to all
   size_t dst1_off = 0, dst1_par = 0, dst1_slot = 0;   // phase-1 destination: off + par * par_stride + src * slot
   size_t dst2_off = 0, dst2_par = 0, dst2_slot = 0;   // phase-2 destination
-  size_t cnt_off = 0;                           // [0] phase-1, [1] phase-2 arrival counters
+  // arrival counters, one per (phase, call parity): [2 * phase + parity].  A
+  // peer's call-(t+2) arrivals can only follow its call-(t+1) consumers,
+  // which follow every call-t push of that peer in stream order, so a
+  // parity's counter never runs ahead of a call it has not completed
+  size_t cnt_off = 0;
   uint64_t target1 = 0, target2 = 0;            // arrivals per call
-  // push mode (default): producers write locally, then push_kernel copies the
-  // slots into the peers' buffers (phase-1 source = send, phase-2 = stage)
-  bool push = false;
   LocalBufs stage{};
   PushJob* push1 = nullptr; int npush1 = 0;
   PushJob* push2 = nullptr; int npush2 = 0;
@@ -85,9 +86,9 @@ struct Bucket {
   const unsigned char** a7_pieces_odd = nullptr;
   unsigned char** dsts = nullptr;               // device [2][n]: my phase-1 slot in every rank's buffer
   unsigned char** dsts2 = nullptr;              // device [2][n]: my phase-2 slot
-  unsigned long long** cnts = nullptr;          // device [n]: every rank's phase-1 counter
-  unsigned long long** cnts2 = nullptr;         // device [n]: every rank's phase-2 counter
-  unsigned long long* my_cnt = nullptr;
+  unsigned long long** cnts = nullptr;          // device [2][n]: every rank's phase-1 counter per parity
+  unsigned long long** cnts2 = nullptr;         // device [2][n]: every rank's phase-2 counter per parity
+  unsigned long long* my_cnt = nullptr;         // my 4 counters [2 * phase + parity]
   uint64_t epoch = 0;
 };
 
@@ -155,15 +156,6 @@ struct HostTables {
 static bool fused_allgather_enabled() {
   static const bool on = [] {
     const char* e = getenv("ESP_FUSED");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-// ESP_PUSH=0: the producing kernels store into peer memory themselves instead of
-// a push kernel after them (A/B knob)
-static bool push_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("ESP_PUSH");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -246,17 +238,14 @@ static void layout_buffers(Layout& L, Bucket& b, HostTables& T) {
       b.dst1_off = bufs(b.recv1, 2 * n * S);
       b.dst1_par = (size_t)n * S;
       b.dst1_slot = S;
-      b.h1_dmode = 2;
     } else if (b.routine == ESP_ALLTOALL_ALLGATHER && !p2) {   // process 1
       b.dst1_off = bufs(b.recv2, 2 * (size_t)n * n * S);
       b.dst1_par = (size_t)n * n * S;
       b.dst1_slot = S;
-      b.h1_dmode = 2;
     } else if (b.routine == ESP_ALLTOALL_ALLGATHER) {   // process 2
       b.dst1_off = bufs(b.recv1, 2 * n * S);
       b.dst1_par = (size_t)n * S;
       b.dst1_slot = S;
-      b.h1_dmode = 1;
       b.dst2_off = bufs(b.recv2, 2 * n * S);
       b.dst2_par = (size_t)n * S;
       b.dst2_slot = S;
@@ -271,15 +260,11 @@ static void layout_buffers(Layout& L, Bucket& b, HostTables& T) {
       b.dst1_off = bufs(b.recv1, 2 * n * S);
       b.dst1_par = (size_t)n * S;
       b.dst1_slot = S;
-      b.h1_dmode = 1;                                   // part 0 = the root
       b.dst2_off = bufs(b.mid, 2 * S);
       b.dst2_par = S;
       b.dst2_slot = 0;
     }
-    // sparse a7 and Randomk have no producer-store variant
-    b.push = push_enabled() || (p2 && !quant) || b.kind == ESP_RANDOMK ||
-             (b.routine == ESP_GATHER_BROADCAST && !p2);
-    if (b.push) {
+    {
       // jobs and arrivals per call (J jobs per slot)
       const uint64_t J = div_up(S, kPushChunk);
       const bool root = w->rank == 0;
@@ -396,12 +381,6 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.step = p.dyn_dev + nslots + slot_idx;
         s.r = c->r ? c->r + (size_t)lr * c->N + lo : nullptr;
         s.chunk = b.send.base ? b.send.at(lr) + (size_t)part * S + b.coff[ti] : nullptr;
-        // fused destinations: dsts[q] + chunk_off (DGC: every rank q; sign: the
-        // partition owner q = part, or every q).  Sparse Alltoall/Allgather lands
-        // in recv2's [part][src] layout
-        const size_t part_off = (b.fused && b.routine == ESP_ALLTOALL_ALLGATHER && !p2) ? (size_t)part * n * S
-                                : dgc ? (size_t)part * S : 0;
-        s.chunk_off = (uint32_t)(part_off + b.coff[ti]);
         s.lazy_in = c->lazy ? c->lazy + ((size_t)lr * c->P + part) * 2 : nullptr;
         s.lazy_out = const_cast<float*>(s.lazy_in);
         s.n = len;
@@ -513,7 +492,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         // the n received chunks of this partition (rank order)
         const uint32_t piece0 = (uint32_t)T.a7_pieces.size();
         for (int r = 0; r < n; ++r) {
-          if (b.push && r == w->rank) {
+          if (b.fused && r == w->rank) {
             // push mode: my own chunk is read where h1 wrote it (rewritten only by
             // the next call's h1, after this call's consumers in stream order)
             unsigned char* mine = b.send.at(lr) + (size_t)(b.routine == ESP_ALLTOALL_ALLGATHER ? r : 0) * S + b.coff[ti];
@@ -531,7 +510,6 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.lazy_out = const_cast<float*>(s.lazy_in);
         s.chunk = b.fused ? (b.stage.base ? b.stage.at(lr) + b.coff[ti] : nullptr)
                           : (b.mid.base ? b.mid.at(lr) + b.coff[ti] : nullptr);
-        s.chunk_off = (uint32_t)b.coff[ti];
         s.n = len;
         s.kpad = c->kpad;
         s.nunits = div_up(len, kDgcTile);
@@ -667,13 +645,13 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           case ESP_ALLGATHER:
           case ESP_GATHER_BROADCAST:
             if (b.routine == ESP_GATHER_BROADCAST && p2) {
-              if (b.push && me == 0) local_piece(b.stage.at(lr) + b.coff[ti], rt2);
+              if (b.fused && me == 0) local_piece(b.stage.at(lr) + b.coff[ti], rt2);
               else add_piece(b.mid.base ? b.mid.at(lr) : nullptr, b.coff[ti], rt2);
               s.npieces = 1;
               s.divisor = 1.0f;
             } else {
               for (int r = 0; r < n; ++r) {
-                if (b.push && r == me) local_piece(b.send.at(lr) + b.coff[ti], rt_of(r));
+                if (b.fused && r == me) local_piece(b.send.at(lr) + b.coff[ti], rt_of(r));
                 else add_piece(b.recv1.base ? b.recv1.at(lr) : nullptr, (size_t)r * S + b.coff[ti], rt_of(r));
               }
               s.npieces = (uint32_t)n;
@@ -683,13 +661,13 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           case ESP_ALLTOALL_ALLGATHER:
             if (!p2) {
               for (int r = 0; r < n; ++r)
-                if (b.push && r == me) local_piece(b.send.at(lr) + (size_t)part * S + b.coff[ti], rt_of(r));
+                if (b.fused && r == me) local_piece(b.send.at(lr) + (size_t)part * S + b.coff[ti], rt_of(r));
                 else add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr,
                           (size_t)part * n * S + (size_t)r * S + b.coff[ti], rt_of(r));
               s.npieces = (uint32_t)n;
               s.divisor = divisor;
             } else {
-              if (b.push && part == me) local_piece(b.stage.at(lr) + b.coff[ti], rt2);
+              if (b.fused && part == me) local_piece(b.stage.at(lr) + b.coff[ti], rt2);
               else add_piece(b.recv2.base ? b.recv2.at(lr) : nullptr, (size_t)part * S + b.coff[ti], rt2);
               s.npieces = 1;
               s.divisor = 1.0f;
@@ -727,18 +705,6 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
   b.nh2_units = (int)u0;
 
   // per critical rank op counts of the cost table
-  // fused: arrivals per call (each DGC write group / sign finalize CTA signals
-  // each of its destinations once; every rank has the same segment list)
-  if (b.fused && !b.push) {
-    if (dgc) {
-      b.target1 = (uint64_t)n * b.nh1_groups;
-    } else {
-      uint64_t mine = 0;
-      for (int i = 0; i < b.nh1; ++i) mine += T.h1[h1_first + i].part == (uint32_t)w->rank;
-      b.target1 = (uint64_t)n * (b.h1_dmode == 2 || b.routine == ESP_GATHER_BROADCAST ? (uint64_t)b.nh1 : mine);
-      b.target2 = (uint64_t)b.nh1;   // sum over owners q of their a7 segments
-    }
-  }
   b.h1_calls = none ? 0 : (p2 ? 2 : 1);
   switch (b.routine) {
     case ESP_ALLGATHER: b.h2_pieces_count = n; break;
@@ -921,18 +887,18 @@ static void open_peers(Plan& p, cudaStream_t st) {
   };
   for (auto& b : p.buckets) {
     if (!b.fused) continue;
-    // my slot in every rank q's phase-1/2 buffer, per call parity; counters
+    // my slot in every rank q's phase-1/2 buffer and q's arrival counters,
+    // per call parity ([parity][q])
     std::vector<unsigned char*> dsts(2 * n), dsts2(2 * n);
-    std::vector<unsigned long long*> cnts(n), cnts2(n);
+    std::vector<unsigned long long*> cnts(2 * n), cnts2(2 * n);
     for (int par = 0; par < 2; ++par)
       for (int q = 0; q < n; ++q) {
         dsts[par * n + q] = base[q] + b.dst1_off + par * b.dst1_par + (size_t)w->rank * b.dst1_slot;
         dsts2[par * n + q] = base[q] + b.dst2_off + par * b.dst2_par + (size_t)w->rank * b.dst2_slot;
+        unsigned long long* c = reinterpret_cast<unsigned long long*>(base[q] + b.cnt_off);
+        cnts[par * n + q] = c + par;
+        cnts2[par * n + q] = c + 2 + par;
       }
-    for (int q = 0; q < n; ++q) {
-      cnts[q] = reinterpret_cast<unsigned long long*>(base[q] + b.cnt_off);
-      cnts2[q] = cnts[q] + 1;
-    }
     b.my_cnt = reinterpret_cast<unsigned long long*>(p.arena.base + b.cnt_off);
     upload(b.dsts, dsts);
     upload(b.dsts2, dsts2);
@@ -942,9 +908,28 @@ static void open_peers(Plan& p, cudaStream_t st) {
   p.peers_ready = true;
 }
 
+// Plans are cached per world in LRU order (most recent last) and bounded by
+// w->plan_cap.  Evicting a fused plan is safe without a cross-rank barrier:
+// its last call has completed here (the eviction synchronizes), so every
+// peer's pushes into this arena have landed (they precede our wait kernel's
+// arrivals), and ranks run the same call sequence, so no peer calls it again.
+void trim_plans(esp_world_s* w) {
+  if (w->plans.size() <= w->plan_cap) return;
+  cudaDeviceSynchronize();
+  while (w->plans.size() > w->plan_cap) {
+    delete w->plans.front();
+    w->plans.erase(w->plans.begin());
+  }
+}
+
 Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
-  for (Plan* up : w->plans)
-    if (up->ctxs == ctxs) return up;
+  for (size_t i = 0; i < w->plans.size(); ++i)
+    if (w->plans[i]->ctxs == ctxs) {
+      Plan* up = w->plans[i];
+      w->plans.erase(w->plans.begin() + i);
+      w->plans.push_back(up);
+      return up;
+    }
   auto p = std::make_unique<Plan>();
   p->w = w;
   p->ctxs = ctxs;
@@ -992,7 +977,9 @@ Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
   for (auto& b : p->buckets)
     if (b.kind == ESP_RANDOMK) p->needs_step = true;
   w->plans.push_back(p.release());
-  return w->plans.back();
+  Plan* mine = w->plans.back();
+  trim_plans(w);
+  return mine;
 }
 
 void drop_plans_with(esp_world_s* w, esp_ctx_s* c) {
@@ -1049,35 +1036,24 @@ static void probe_pair(esp_world_s* w, cudaEvent_t* e0, cudaEvent_t* e1, uint64_
   ++w->probe_used;
 }
 
-// `fused`: this call's h1 stores its payload straight into every rank's
-// receive buffer (only from the collective esp_sync / esp_sync_many path)
-static void run_h1(Plan& p, Bucket& b, cudaStream_t st, bool fused = false) {
+// h1 of a bucket: the payload is written locally (send); in a fused bucket
+// push_kernel then moves it to the peers (run_comm)
+static void run_h1(Plan& p, Bucket& b, cudaStream_t st) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p.w->probe && b.nh1_units) probe_pair(p.w, &e0, &e1, b.h1_bytes);
   const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
   const bool sign = b.kind == ESP_EFSIGNSGD || b.kind == ESP_ONEBIT;
   if (e0 && !dgc && !sign) ESP_CUDA(cudaEventRecord(e0, st));
-  if (b.push) fused = false;   // local payload; push_kernel moves it (run_comm)
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
-      if (fused) {
-        const int n = p.w->nranks;
-        launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1,
-                      b.dsts + (b.epoch & 1) * n, b.cnts, n, b.momentum != 0.0);
-      } else {
-        launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1, nullptr, nullptr,
-                      0, b.momentum != 0.0);
-      }
+      launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1,
+                    b.momentum != 0.0);
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
     case ESP_EFSIGNSGD:
     case ESP_ONEBIT: {
       const int k = b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT;
-      const int n = p.w->nranks;
-      if (fused) launch_sign_h1_tma(k, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st,
-                                    b.dsts + (b.epoch & 1) * n, b.cnts, b.h1_dmode, n, b.h1_max_len, e0, e1);
-      else launch_sign_h1_tma(k, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st, nullptr, nullptr, 0, 0,
-                              b.h1_max_len, e0, e1);
+      launch_sign_h1_tma(k, b.h1, b.nh1, b.h1_units, b.nh1_units, nullptr, st, b.h1_max_len, e0, e1);
       break;
     }
     default: launch_pack(b.h1, b.h1_units, b.nh1_units, st); break;
@@ -1117,17 +1093,8 @@ static void run_mid(Plan& p, Bucket& b, cudaStream_t cs) {
       launch_dgc_h1(b.a7, b.na7, b.a7_units, b.na7_units, b.a7_groups, b.na7_groups, cs);
     }
     dbg("a7 recompress", cs);
-  } else if (b.fused && b.push) {
-    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, (b.epoch & 1) ? b.a7_pieces_odd : b.a7_pieces, cs,
-                       nullptr, nullptr, 0, 0, b.a7_max_len);
-  } else if (b.fused) {
-    // recompressed chunks go straight into every rank's phase-2 buffer
-    const int n = p.w->nranks;
-    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, (b.epoch & 1) ? b.a7_pieces_odd : b.a7_pieces, cs,
-                       b.dsts2 + (b.epoch & 1) * n, b.cnts2, 2, n, b.a7_max_len);
   } else {
-    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, b.a7_pieces, cs, nullptr, nullptr, 0, 0,
-                       b.a7_max_len);
+    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, pieces, cs, b.a7_max_len);
   }
   ESP_CUDA(cudaGetLastError());
 }
@@ -1138,32 +1105,35 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
   const size_t S = b.slot;
   const bool quant = b.p2;   // a mid-scheme recompression between the two phases
   if (b.fused) {
-    // the payloads were pushed by the producers (every rank's h1, then a7);
-    // wait for this call's arrivals (the counters are monotonic across calls).
-    // The counters record the routine's logical traffic (the cost table)
-    const unsigned long long e1 = b.epoch + 1;
+    // push_kernel moves the local payloads (h1's send, then a7's stage) to
+    // the peers; wait for this call's arrivals on the counter of this call's
+    // parity (monotonic across that parity's calls).  The byte counters record
+    // the routine's logical traffic (the cost table)
     const int par = (int)(b.epoch & 1);
+    const unsigned long long e1 = (b.epoch >> 1) + 1;   // calls of this parity so far, this one included
+    unsigned long long* cnt1 = b.my_cnt + par;          // [2 * phase + parity]
+    unsigned long long* cnt2 = b.my_cnt + 2 + par;
     auto push1 = [&] {
-      if (b.push) launch_push(b.push1, b.npush1, b.send.at(0), b.dsts + par * n, b.cnts, cs);
+      launch_push(b.push1, b.npush1, b.send.at(0), b.dsts + par * n, b.cnts + par * n, cs);
       dbg("push phase 1", cs);
     };
     auto push2 = [&] {
-      if (b.push && b.push2_arena)
-        launch_push(par ? b.push2_odd : b.push2, b.npush2, p.arena.base, b.dsts2 + par * n, b.cnts2, cs);
-      else if (b.push)
-        launch_push(b.push2, b.npush2, b.stage.at(0), b.dsts2 + par * n, b.cnts2, cs);
+      if (b.push2_arena)
+        launch_push(par ? b.push2_odd : b.push2, b.npush2, p.arena.base, b.dsts2 + par * n, b.cnts2 + par * n, cs);
+      else
+        launch_push(b.push2, b.npush2, b.stage.at(0), b.dsts2 + par * n, b.cnts2 + par * n, cs);
       dbg("push phase 2", cs);
     };
     push1();
     switch (b.routine) {
       case ESP_ALLGATHER:
         count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
-        launch_wait_arrivals(b.my_cnt, e1 * b.target1, cs);
+        launch_wait_arrivals(cnt1, e1 * b.target1, w->wait_err, w->wait_timeout_ns, cs);
         dbg("wait phase 1", cs);
         break;
       case ESP_ALLTOALL_ALLGATHER:
         count_coll(w, 0, ESP_OP_ALLTOALL, (n - 1) * S, (n - 1) * S);
-        launch_wait_arrivals(b.my_cnt, e1 * b.target1, cs);
+        launch_wait_arrivals(cnt1, e1 * b.target1, w->wait_err, w->wait_timeout_ns, cs);
         dbg("wait phase 1", cs);
         if (quant) {
           if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
@@ -1171,7 +1141,7 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
           if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
           push2();
           count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
-          launch_wait_arrivals(b.my_cnt + 1, e1 * b.target2, cs);
+          launch_wait_arrivals(cnt2, e1 * b.target2, w->wait_err, w->wait_timeout_ns, cs);
         dbg("wait phase 2", cs);
         } else {
           count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * n * S, (n - 1) * n * S);
@@ -1181,7 +1151,7 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
         const bool root = w->rank == 0;
         count_coll(w, 0, ESP_OP_GATHER, root ? 0 : S, root ? (n - 1) * S : 0);
         if (root) {
-          launch_wait_arrivals(b.my_cnt, e1 * b.target1, cs);
+          launch_wait_arrivals(cnt1, e1 * b.target1, w->wait_err, w->wait_timeout_ns, cs);
           dbg("wait phase 1", cs);
           if (quant) {   // process 2: the root's mid-scheme recompression
             if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
@@ -1193,7 +1163,7 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
         // process 1 broadcasts the n payloads, process 2 one
         const size_t bc = quant ? S : (size_t)n * S;
         count_coll(w, 0, ESP_OP_BROADCAST, root ? bc : 0, root ? 0 : bc);
-        launch_wait_arrivals(b.my_cnt + 1, e1 * b.target2, cs);
+        launch_wait_arrivals(cnt2, e1 * b.target2, w->wait_err, w->wait_timeout_ns, cs);
         dbg("wait phase 2", cs);
         break;
       }
@@ -1294,6 +1264,8 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
   Plan& p = *pp;
   esp_world_s* w = p.w;
   const cudaStream_t cs = w->comm_stream;
+  ESP_REQUIRE(!*const_cast<volatile unsigned int*>(w->wait_err_host), ESP_ERR_NCCL,
+              "a peer's payload did not arrive within the wait timeout of an earlier call");
   if (!p.peers_ready && std::any_of(p.buckets.begin(), p.buckets.end(), [](const Bucket& b) { return b.fused; }))
     open_peers(p, cs);
   upload_dyn(p, grads, st);
@@ -1308,7 +1280,7 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
       cudaEvent_t e0 = tev(w, 1 + 6 * i), e1 = tev(w, 2 + 6 * i), e2 = tev(w, 3 + 6 * i);
       cudaEvent_t e3 = tev(w, 4 + 6 * i), m0 = tev(w, 5 + 6 * i), m1 = tev(w, 6 + 6 * i);
       ESP_CUDA(cudaEventRecord(e0, st));
-      run_h1(p, b, st, b.fused);
+      run_h1(p, b, st);
       ESP_CUDA(cudaEventRecord(e1, st));
       ESP_CUDA(cudaStreamWaitEvent(cs, e1, 0));
       ESP_CUDA(cudaEventRecord(m0, cs));
@@ -1345,7 +1317,7 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
     for (size_t i = 0; i <= nb; ++i) {
       if (i < nb) {
         Bucket& b = p.buckets[i];
-        run_h1(p, b, st, b.fused);
+        run_h1(p, b, st);
         ESP_CUDA(cudaEventRecord(b.ev_h1, st));
         ESP_CUDA(cudaStreamWaitEvent(cs, b.ev_h1, 0));
         run_comm(p, b, cs, nullptr, nullptr);

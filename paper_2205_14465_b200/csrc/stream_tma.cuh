@@ -206,11 +206,6 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1)
     }
   }
   if (cur != 0xFFFFFFFFu) end_seg(S, cur_units, first_unit, st);
-  // ops that store into peer GPUs' memory: the arrival signal is sent by the
-  // next kernel in stream order, after this grid has completed (kernel
-  // completion performs all of its stores, peer stores included); the optional
-  // per-thread system fence is an A/B knob (ESP_SYS_FENCE=1)
-  if (op.sys_fence()) __threadfence_system();
 }
 
 int tma_stream_grid(int nunits);
@@ -231,23 +226,15 @@ static void launch_tma_op_n(const SegH1* segs, const uint32_t* unit_seg, int nun
   (void)init;
   int ns = tma_stream_stages();
   ns = ns < NCG ? NCG : (ns > kMaxNs ? kMaxNs : ns - ns % NCG);
-  ESP_CARVE(tma_stream_kernel<Op, NCG>);
   tma_stream_kernel<Op, NCG><<<tma_stream_grid(nunits), NCG * kThreads + 32, kTmaHdrBytes + ns * kTmaStageBytes,
                                st>>>(segs, unit_seg, (uint32_t)nunits, ns, op);
   count_launches(1);
 }
 
-// Op::kGroups consumer groups (ESP_TMA_GROUPS=1..3 overrides it, for A/B runs)
+// Op::kGroups consumer groups of 8 warps
 template <class Op>
 static void launch_tma_op(const SegH1* segs, const uint32_t* unit_seg, int nunits, Op op, cudaStream_t st) {
-  static const int groups = [] {
-    const char* e = getenv("ESP_TMA_GROUPS");
-    const int g = e ? atoi(e) : Op::kGroups;
-    return g < 1 ? 1 : (g > kTmaGroups ? kTmaGroups : g);
-  }();
-  if (groups == 1) launch_tma_op_n<Op, 1>(segs, unit_seg, nunits, op, st);
-  else if (groups == 2) launch_tma_op_n<Op, 2>(segs, unit_seg, nunits, op, st);
-  else launch_tma_op_n<Op, 3>(segs, unit_seg, nunits, op, st);
+  launch_tma_op_n<Op, Op::kGroups>(segs, unit_seg, nunits, op, st);
 }
 
 }  // namespace esp

@@ -16,14 +16,6 @@ static std::atomic<uint64_t> g_launches{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
-bool set_max_smem_carveout(const void* fn) {
-  static const bool on = [] {
-    const char* e = getenv("ESP_CARVEOUT");   // measured slower on BERT-large: off by default
-    return e && e[0] == '1';
-  }();
-  return on && cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    (int)cudaSharedmemCarveoutMaxShared) == cudaSuccess;
-}
 
 uint64_t host_splitmix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
@@ -261,6 +253,9 @@ static void world_common_init(esp_world_s* w) {
   ESP_CUDA(cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming));
   ESP_CUDA(cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming));
   w->counters.assign(w->nlocal, esp_counters_t{});
+  ESP_CUDA(cudaHostAlloc(&w->wait_err_host, sizeof(unsigned int), cudaHostAllocMapped));
+  *w->wait_err_host = 0;
+  ESP_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&w->wait_err), w->wait_err_host, 0));
 }
 
 esp_status_t esp_world_create_nccl(const void* id128, int nranks, int rank, int cuda_dev, esp_world_t* out) {
@@ -309,6 +304,7 @@ esp_status_t esp_world_destroy(esp_world_t w) {
   for (auto e : w->probe_pool) cudaEventDestroy(e);
   cudaEventDestroy(w->ev_join);
   cudaEventDestroy(w->ev_fork);
+  if (w->wait_err_host) cudaFreeHost(w->wait_err_host);
   cudaStreamDestroy(w->comm_stream);
   delete w;
   ESP_API_END
@@ -319,6 +315,8 @@ esp_status_t esp_world_check(esp_world_t w) {
   ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
   cudaError_t e = cudaGetLastError();
   ESP_REQUIRE(e == cudaSuccess, ESP_ERR_CUDA, std::string("async CUDA error: ") + cudaGetErrorString(e));
+  ESP_REQUIRE(!*const_cast<volatile unsigned int*>(w->wait_err_host), ESP_ERR_NCCL,
+              "a peer's payload did not arrive within the wait timeout (esp_world_set_timeout)");
   if (w->comm) {
     ncclResult_t r = ncclSuccess;
     ESP_NCCL(ncclCommGetAsyncError(w->comm, &r));
@@ -369,6 +367,29 @@ esp_status_t esp_world_set_bucket_elems(esp_world_t w, uint64_t elems) {
   ESP_API_BEGIN
   ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
   w->bucket_elems = elems;
+  clear_plans(w);
+  ESP_API_END
+}
+
+esp_status_t esp_world_set_timeout(esp_world_t w, double seconds) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w && seconds > 0 && seconds < 1e9, ESP_ERR_INVALID_ARG, "bad argument");
+  w->wait_timeout_ns = (unsigned long long)(seconds * 1e9);
+  ESP_API_END
+}
+
+esp_status_t esp_world_set_plan_cache(esp_world_t w, int max_plans) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w && max_plans >= 1, ESP_ERR_INVALID_ARG, "bad argument");
+  w->plan_cap = (size_t)max_plans;
+  trim_plans(w);
+  ESP_API_END
+}
+
+esp_status_t esp_world_drop_plans(esp_world_t w) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
+  cudaSetDevice(w->dev);
   clear_plans(w);
   ESP_API_END
 }

@@ -29,6 +29,18 @@ class EspressoState:
         self.rule = rule
         self.pid = {id(p): i for i, p in enumerate(model.parameters())}
         self.ctxs: dict[int, E.Ctx] = {}
+        self.layout: dict[int, tuple] = {}   # bucket index -> its parameters' ids
+
+    def note_bucket(self, index: int, ids: tuple):
+        """DDP rebuilds its buckets after the first iteration (and may again, e.g.
+        with find_unused_parameters): when a bucket's parameter list changes,
+        the cached libesp plans of the old lists are freed on every rank (every
+        rank sees the same rebuild at the same step)."""
+        old = self.layout.get(index)
+        if old is not None and old != ids:
+            self.world.drop_plans()
+            self.layout.clear()
+        self.layout[index] = ids
 
     def ctx(self, p: torch.Tensor, numel: int) -> E.Ctx:
         i = self.pid[id(p)]
@@ -49,6 +61,10 @@ class EspressoState:
 def espresso_hook(state: EspressoState, bucket: torch.distributed.GradBucket) -> torch.futures.Future[torch.Tensor]:
     grads = bucket.gradients()
     params = bucket.parameters()
+    if bucket.buffer().dtype != torch.float32:
+        raise TypeError(f"espresso_hook synchronises fp32 gradients; got a {bucket.buffer().dtype} bucket "
+                        "(keep fp32 master gradients or cast before the hook)")
+    state.note_bucket(bucket.index(), tuple(state.pid[id(p)] for p in params))
     ctxs = [state.ctx(p, g.numel()) for p, g in zip(params, grads)]
     E.esp_sync_many(state.world, ctxs, grads, torch.cuda.current_stream())
     fut = torch.futures.Future()

@@ -26,7 +26,8 @@ SYMBOLS = (
     "esp_get_nccl_unique_id", "esp_world_create_nccl", "esp_world_create_sim", "esp_world_destroy",
     "esp_world_check", "esp_world_info", "esp_world_counters", "esp_world_counters_local",
     "esp_world_reset_counters", "esp_world_set_timing", "esp_last_timing", "esp_world_set_bucket_elems",
-    "esp_world_set_probe", "esp_probe_read",
+    "esp_world_set_probe", "esp_probe_read", "esp_world_set_timeout", "esp_world_set_plan_cache",
+    "esp_world_drop_plans",
     "esp_ctx_create", "esp_ctx_destroy", "esp_ctx_payload_bytes", "esp_ctx_get_state",
     "esp_ctx_set_state", "esp_ctx_get_momentum", "esp_ctx_set_momentum", "esp_compress", "esp_decompress", "esp_sync", "esp_sync_many",
     "esp_compressed_bytes", "esp_wire_bytes", "esp_model_time", "esp_status_string",
@@ -86,6 +87,8 @@ def lib():
             "esp_world_reset_counters": [vp], "esp_world_set_timing": [vp, i32],
             "esp_last_timing": [vp, C.POINTER(Timing)], "esp_world_set_bucket_elems": [vp, u64],
             "esp_world_set_probe": [vp, i32],
+            "esp_world_set_timeout": [vp, dbl], "esp_world_set_plan_cache": [vp, i32],
+            "esp_world_drop_plans": [vp],
             "esp_probe_read": [vp, C.POINTER(dbl), C.POINTER(u64), C.POINTER(u64)],
             "esp_ctx_create": [vp, C.POINTER(CompressorCfg), i32, u64, sz, C.POINTER(vp)],
             "esp_ctx_destroy": [vp], "esp_ctx_payload_bytes": [vp, C.POINTER(sz)],
@@ -129,6 +132,24 @@ def cfg_of(kind="dgc", ratio=0.01, error_feedback=True, seed=0, shared_indices=T
 
 def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _require(t, what, dtype, device, numel=None, min_numel=None):
+    """The C ABI takes raw device pointers: a tensor of the wrong dtype, device,
+    layout or size would be read / written out of bounds.  Reject it here."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{what}: expected a torch.Tensor, got {type(t).__name__}")
+    if not t.is_cuda or t.device.index != device:
+        raise ValueError(f"{what}: must live on cuda:{device}, got {t.device}")
+    if t.dtype != dtype:
+        raise TypeError(f"{what}: dtype must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: must be contiguous")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{what}: expected {numel} elements, got {t.numel()}")
+    if min_numel is not None and t.numel() < min_numel:
+        raise ValueError(f"{what}: expected at least {min_numel} elements, got {t.numel()}")
 
 
 def _stream(stream):
@@ -247,6 +268,15 @@ class World:
     def check(self):
         _check(lib().esp_world_check(self.h))
 
+    def set_timeout(self, seconds: float):
+        _check(lib().esp_world_set_timeout(self.h, float(seconds)))
+
+    def set_plan_cache(self, max_plans: int):
+        _check(lib().esp_world_set_plan_cache(self.h, int(max_plans)))
+
+    def drop_plans(self):
+        _check(lib().esp_world_drop_plans(self.h))
+
     def destroy(self):
         for c in list(self.ctxs):
             c.destroy()
@@ -316,25 +346,39 @@ class Ctx:
 def esp_compress(ctx: Ctx, grad, payload=None, stream=None):
     """h1 of every local rank; returns the payload (uint8 CUDA tensor)."""
     import torch
+    w = ctx.world
+    _require(grad, "grad", torch.float32, w.device, numel=w.nlocal * ctx.numel)
     if payload is None:
-        payload = torch.empty(ctx.world.nlocal * ctx.payload_bytes, dtype=torch.uint8, device=grad.device)
+        payload = torch.empty(w.nlocal * ctx.payload_bytes, dtype=torch.uint8, device=grad.device)
+    _require(payload, "payload", torch.uint8, w.device, min_numel=w.nlocal * ctx.payload_bytes)
     _check(lib().esp_compress(ctx.h, _ptr(grad), _ptr(payload), _stream(stream)))
     return payload
 
 
 def esp_decompress(ctx: Ctx, pieces, out, stream=None):
+    import torch
+    for i, p in enumerate(pieces):
+        _require(p, f"pieces[{i}]", torch.uint8, ctx.world.device, min_numel=ctx.payload_bytes)
+    _require(out, "out", torch.float32, ctx.world.device, numel=ctx.numel)
     arr = (C.c_void_p * len(pieces))(*[p.data_ptr() for p in pieces])
     _check(lib().esp_decompress(ctx.h, arr, len(pieces), _ptr(out), _stream(stream)))
     return out
 
 
 def esp_sync(world: World, ctx: Ctx, grad, stream=None):
+    import torch
+    _require(grad, "grad", torch.float32, world.device, numel=world.nlocal * ctx.numel)
     _check(lib().esp_sync(world.h, ctx.h, _ptr(grad), _stream(stream)))
     return grad
 
 
 def esp_sync_many(world: World, ctxs, grads, stream=None):
+    import torch
     n = len(ctxs)
+    if len(grads) != n:
+        raise ValueError(f"{n} ctxs but {len(grads)} gradients")
+    for i, (c, g) in enumerate(zip(ctxs, grads)):
+        _require(g, f"grads[{i}]", torch.float32, world.device, numel=world.nlocal * c.numel)
     hs = (C.c_void_p * n)(*[c.h.value for c in ctxs])
     gs = (C.c_void_p * n)(*[g.data_ptr() for g in grads])
     _check(lib().esp_sync_many(world.h, hs, gs, n, _stream(stream)))

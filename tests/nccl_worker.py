@@ -124,8 +124,59 @@ def main():
         torch.cuda.synchronize()
         for i, (k, r, _, _) in enumerate(specs):
             check(k, r, gs[i].cpu().numpy(), refs[i].outs[rank], grads[i], f"sync_many {k}/{r} step {s}")
+    # back to back: T calls with no host synchronisation between them and a
+    # rank-dependent GPU delay before some, so fast ranks run ahead into the
+    # next call (both parities of the fused buffers and arrival counters
+    # reused while a slow peer is still pushing the previous call)
+    w.set_bucket_elems(0)
+    bspecs = [("dgc", "allgather", 20_000, {}), ("dgc", "alltoall_allgather", 30_000, {}),
+              ("dgc", "alltoall_allgather", 9000, {"process": 2}), ("randomk", "gather_broadcast", 7000, {}),
+              ("topk", "gather_broadcast", 5000, {}), ("none", "allreduce", 3000, {}),
+              ("randomk", "allgather", 4000, {"shared_indices": False})]
+    T = 6
+    bctx = [E.Ctx(w, k, r, N_, tensor_id=300 + i, ratio=0.01, **ex) for i, (k, r, N_, ex) in enumerate(bspecs)]
+    bcfg = [O.Cfg(k, 0.01, **ex) for (k, r, N_, ex) in bspecs]
+    bst = [O.new_states(n, N_, r, bcfg[i]) for i, (k, r, N_, _) in enumerate(bspecs)]
+    ball = [[[gradient(N_, step=s, rank=q, tensor=300 + i) for q in range(n)] for i, (_, _, N_, _) in enumerate(bspecs)]
+            for s in range(T)]
+    bg = [[torch.from_numpy(ball[s][i][rank].copy()).cuda() for i in range(len(bspecs))] for s in range(T)]
+    torch.cuda.synchronize()
+    dist.barrier()
+    for s in range(T):
+        if (s + rank) % 2 == 1:
+            torch.cuda._sleep(2_000_000 * (1 + rank))   # ~1-4 ms of skew on this rank
+        E.esp_sync_many(w, bctx, bg[s])
+    torch.cuda.synchronize()
+    for s in range(T):
+        for i, (k, r, _, _) in enumerate(bspecs):
+            ref = O.sync(r, bcfg[i], ball[s][i], bst[i], tensor_id=300 + i)
+            check(k, r, bg[s][i].cpu().numpy(), ref.outs[rank], ball[s][i], f"back-to-back {k}/{r} step {s}")
     w.check()
     w.destroy()
+
+    # a peer that never arrives: rank 0 calls once more than the others; its
+    # wait gives up after the timeout instead of hanging or trapping, and the
+    # world reports the failure (the CUDA context stays usable)
+    w2 = E.World.nccl(local)
+    w2.set_timeout(2.0)
+    c2 = E.Ctx(w2, "dgc", "allgather", 5000, tensor_id=400, ratio=0.01)
+    g2 = torch.from_numpy(gradient(5000, rank=rank, tensor=400)).cuda()
+    E.esp_sync(w2, c2, g2)
+    torch.cuda.synchronize()
+    w2.check()
+    dist.barrier()
+    if rank == 0:
+        E.esp_sync(w2, c2, g2)
+        torch.cuda.synchronize()
+        try:
+            w2.check()
+            raise AssertionError("a missing peer was not reported")
+        except E.EspError as e:
+            assert "did not arrive" in str(e), str(e)
+        torch.ones(1, device="cuda").sum().item()   # the context still works
+    dist.barrier()
+    c2.destroy()
+    w2.destroy()
     dist.barrier()
     dist.destroy_process_group()
     print(f"rank {rank}: {checked} pair-steps + sync_many ok", flush=True)
