@@ -2,12 +2,17 @@
 """Benchmark of the compressed gradient-synchronisation hot path on B200.
 
 Metric (BASELINE.json): compressed gradient-sync GB/s (device-timed, max over
-ranks) = (sum over tensors of 4 * numel) * n_ranks / t_step, t_step = max over
-ranks of the CUDA-event time of one esp_sync_many over the whole gradient set
-(h1 -> collective -> h2), inputs resident in HBM.
+ranks).  Per rank, one step synchronises that rank's whole gradient set,
+sum over tensors of 4 * numel bytes, with one esp_sync_many (h1 -> collective
+-> h2); t_step = max over ranks of its CUDA-event time, inputs resident in HBM.
+`value` is the whole job's throughput, the gradient bytes all n ranks
+synchronised per step / t_step (weak scaling: each rank syncs its own full
+gradient set); `value_per_rank` = 4 * sum numel / t_step is BASELINE.md's
+per-rank figure (value / n).
 
     python bench.py [--gpus N --steps K --warmup W --workload NAME]
-    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
+        (--gpus N > 1 without a torchrun environment re-launches itself under
+         torch.distributed.run with N ranks, one per GPU, NCCL)
     python bench.py --impl reference ...                  (the CPU oracle, host cores)
 
 Default workload = BASELINE config 4: BERT-large (BertForPreTraining shapes,
@@ -18,7 +23,9 @@ from __future__ import annotations
 
 import argparse
 import json
+import multiprocessing
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -133,6 +140,64 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ------------------------------------------------------------------ NVLink counters
+def nvlink_bytes(gpu_index: int):
+    """(tx, rx) bytes over all NVLinks of the GPU so far, from NVML's NVLink
+    throughput counters (data payload, KiB) or, where those are missing, the
+    per-link byte counters; None if NVML offers neither."""
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(gpu_index)
+        vals = nv.nvmlDeviceGetFieldValues(h, [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                               nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
+        if all(v.nvmlReturn == 0 for v in vals):
+            return {"tx": int(vals[0].value.ullVal) * 1024, "rx": int(vals[1].value.ullVal) * 1024,
+                    "source": "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX (KiB)"}
+        tx = rx = 0
+        for link in range(18):
+            v = nv.nvmlDeviceGetFieldValues(h, [(nv.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, link),
+                                                (nv.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, link)])
+            if v[0].nvmlReturn == 0:
+                tx += int(v[0].value.ullVal)
+            if v[1].nvmlReturn == 0:
+                rx += int(v[1].value.ullVal)
+        return {"tx": tx, "rx": rx, "source": "NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES per link"}
+    except Exception as e:   # noqa: BLE001 (diagnostic only)
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
+# ------------------------------------------------------------------ config-1 latency
+def latency_config1(E, device: int, reps: int = 200):
+    """BASELINE config 1 as a latency probe: one 2^20-element fp32 gradient, DGC
+    top-1% with error feedback, Allgather, n = 2 simulated ranks on this GPU
+    (sim world: both ranks' h1 / h2 kernels, the collective is two D2D copies).
+    Mean device time per esp_sync over `reps` back-to-back calls (inputs L2-
+    resident: this probes the per-call launch chain)."""
+    import torch
+    N, n = 1 << 20, 2
+    w = E.World.sim(n, device)
+    c = E.Ctx(w, "dgc", "allgather", N, tensor_id=0, ratio=0.01)
+    g = torch.from_numpy(__import__("numpy").concatenate([gradient(N, rank=r) for r in range(n)])).cuda()
+    for _ in range(10):
+        E.esp_sync(w, c, g)
+    l0 = E.esp_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        E.esp_sync(w, c, g)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    launches = (E.esp_launch_count() - l0) / reps
+    w.destroy()
+    hbm = 2 * (12 * N + 4 * N)   # per rank: h1 12 B/elem + h2 4 B/elem (SURVEY.md 8d)
+    return {"workload": "config 1: 2^20 fp32, DGC 1%, EF, Allgather, sim n=2", "us_per_sync": us,
+            "gbs": n * 4 * N / (us * 1e-6) / 1e9, "kernel_launches_per_sync": launches,
+            "roofline_us": hbm / (peaks()[0]["hbm_gbs"] * 1e3), "reps": reps}
+
+
 # ------------------------------------------------------------------ output
 _JSON_FD = None
 
@@ -169,6 +234,16 @@ def max_over_ranks(x: float, ws: int) -> float:
     return float(t.item())
 
 
+def max_over_ranks_vec(xs, ws):
+    if ws == 1:
+        return list(xs)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(xs, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
 def barrier(ws):
     if ws > 1:
         import torch.distributed as dist
@@ -196,39 +271,73 @@ def run_reference(args):
         if tot >= 4_000_000:
             break
     n = max(1, args.gpus)
-    grads = {i: [gradient(sizes[i], rank=r, tensor=i) for r in range(n)] for i in idx}
-    states = {}
-    for i in idx:
-        kind, ratio, routine, ex = opt(rule, sizes[i])
-        states[i] = O.new_states(n, sizes[i], routine, O.Cfg(kind, ratio, **ex))
-
-    def step():
-        for i in idx:
-            kind, ratio, routine, ex = opt(rule, sizes[i])
-            O.sync(routine, O.Cfg(kind, ratio, **ex), grads[i], states[i], tensor_id=i)
-
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = (time.perf_counter() - t0) / args.steps
+    cores = os.cpu_count() or 1
+    jobs = [(args.workload, n, i, sizes[i]) for i in idx]
+    # one worker process per host core, each owning a share of the tensors (the
+    # oracle is single-threaded numpy); every step syncs every sampled tensor once
+    with multiprocessing.get_context("fork").Pool(min(cores, len(jobs)), initializer=_oracle_worker_init) as pool:
+        pool.map(_oracle_job, jobs)                      # builds each worker's states
+        for _ in range(args.warmup):
+            pool.map(_oracle_job, jobs)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_oracle_job, jobs)
+        dt = (time.perf_counter() - t0) / args.steps
     value = n * 4 * tot / dt / 1e9
-    sample = f"{len(idx)} tensors of {args.workload} ({tot} elements per rank, first non-embedding tensors), n={n} ranks simulated"
+    sample = (f"{len(idx)} tensors of {args.workload} ({tot} elements per rank, first non-embedding tensors), "
+              f"n={n} ranks simulated, {min(cores, len(jobs))} worker processes on {cores} host cores ({_cpu_model()})")
     line = {
         "impl": "reference", "metric": "compressed gradient-sync GB/s", "value": value, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": args.workload, "parallelism": f"dp{n}"},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": min(cores, len(jobs)), "kind": "oracle",
+                         "sample": sample, "host": {"nproc": cores, "cpu_model": _cpu_model()}},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
 
 
-def cpu_baseline(args, model, rule, sizes, names, n):
-    """Oracle timed on this host on a bounded sample (~10-30 s of CPU work)."""
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+# oracle worker processes (fork): each keeps the EF states of the tensors it was
+# handed, so repeated steps carry error feedback like the real path
+_W = {}
+
+
+def _oracle_worker_init():
+    os.environ["OMP_NUM_THREADS"] = "1"
+
+
+def _oracle_job(job):
     from oracle import esp_oracle as O
+    name, n, i, N = job
+    if ("rule", name, n) not in _W:
+        _W[("rule", name, n)] = workload(name, n)[1]
+    rule = _W[("rule", name, n)]
+    kind, ratio, routine, ex = opt(rule, N)
+    cfg = O.Cfg(kind, ratio, **ex)
+    if (name, i) not in _W:
+        _W[(name, i)] = ([gradient(N, rank=r, tensor=i) for r in range(n)], O.new_states(n, N, routine, cfg))
+    grads, st = _W[(name, i)]
+    t0 = time.perf_counter()
+    O.sync(routine, cfg, grads, st, tensor_id=i)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(args, model, rule, sizes, names, n):
+    """The oracle timed on this host on a bounded sample (~10-30 s of CPU work):
+    single-threaded, then one worker process per host core over the same
+    tensors (the oracle itself is single-threaded numpy)."""
     idx, tot = [], 0
     for i, nm in enumerate(names):
         if any(s in nm for s in ("layer.0.", "layer.1.", "layer.2.", "layer1.", "h.0.", "h.1.")):
@@ -237,18 +346,21 @@ def cpu_baseline(args, model, rule, sizes, names, n):
     if not idx:
         idx = list(range(min(20, len(sizes))))
         tot = sum(sizes[i] for i in idx)
-    t = 0.0
-    for i in idx:
-        kind, ratio, routine, ex = opt(rule, sizes[i])
-        cfg = O.Cfg(kind, ratio, **ex)
-        grads = [gradient(sizes[i], rank=r, tensor=i) for r in range(n)]
-        st = O.new_states(n, sizes[i], routine, cfg)
+    jobs = [(args.workload, n, i, sizes[i]) for i in idx]
+    t1 = sum(_oracle_job(j) for j in jobs)          # one core (states built on the first call, untimed)
+    t1 = sum(_oracle_job(j) for j in jobs)
+    cores = os.cpu_count() or 1
+    nw = min(cores, len(jobs))
+    with multiprocessing.get_context("fork").Pool(nw, initializer=_oracle_worker_init) as pool:
+        pool.map(_oracle_job, jobs)
         t0 = time.perf_counter()
-        O.sync(routine, cfg, grads, st, tensor_id=i)
-        t += time.perf_counter() - t0
-    return {"value": n * 4 * tot / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"{len(idx)} tensors ({tot} elements per rank) of the first layers, n={n} ranks simulated, "
-                      f"single-threaded numpy, {t:.1f} s"}
+        pool.map(_oracle_job, jobs)
+        tall = time.perf_counter() - t0
+    return {"value": n * 4 * tot / tall / 1e9, "unit": "GB/s", "cores": nw, "kind": "oracle",
+            "single_thread_value": n * 4 * tot / t1 / 1e9,
+            "host": {"nproc": cores, "cpu_model": _cpu_model()},
+            "sample": f"{len(idx)} tensors ({tot} elements per rank) of the first layers, n={n} ranks simulated; "
+                      f"value: {nw} worker processes over the tensors ({tall:.1f} s); single thread {t1:.1f} s"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -263,7 +375,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bucket-elems", type=int, default=0)
     ap.add_argument("--phases", action="store_true", help="print a serialised h1/comm/mid/h2 breakdown to stderr")
+    ap.add_argument("--no-latency", action="store_true", help="skip the config-1 latency probe")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        # one process per GPU: re-launch under torch.distributed.run; rank 0 prints the line
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.run(cmd).returncode)
     _claim_stdout()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -307,15 +429,26 @@ def main():
     def step():
         E.esp_sync_many(world, ctxs, views, stream)
 
-    for _ in range(args.warmup):
+    # L2 hygiene: before every timed step, after restoring the gradients, write
+    # a buffer of twice the 126 MB L2 so that no input of the step starts in L2
+    # (the restore itself leaves the last ~126 MB of g resident otherwise)
+    flush = torch.empty(2 * 126 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+
+    def restore():
         g.copy_(g0)
+        flush.fill_(1.0)
+
+    for _ in range(args.warmup):
+        restore()
         step()
     torch.cuda.synchronize()
     barrier(ws)
 
-    # ---- timed region: K steps, per-step CUDA events on the launching stream;
-    # the input restore (the "backward pass" that produces fresh gradients) is
-    # outside the events
+    # ---- timed region: K steps, per-step CUDA events on the launching stream.
+    # Before every step: the input restore (the "backward pass" that produces
+    # fresh gradients) and the L2 flush, a device synchronize and a barrier
+    # across ranks, so that every rank starts the step together; the step's
+    # time is then the max over ranks of its event time
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local) if rank == 0 else None
     if clocks:
@@ -326,35 +459,43 @@ def main():
     barrier(ws)
     torch.cuda.synchronize()
     w0 = time.perf_counter()
+    nvl0 = nvlink_bytes(local) if ws > 1 else None
     for i in range(args.steps):
-        g.copy_(g0)
+        restore()
+        if ws > 1:
+            torch.cuda.synchronize()
+            barrier(ws)
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     barrier(ws)
     wall = time.perf_counter() - w0
+    nvl1 = nvlink_bytes(local) if ws > 1 else None
     launches = E.esp_launch_count() - launches0
     probe_ms, probe_n, probe_bytes = world.probe_read()
     world.set_probe(False)
     clk = clocks.stop() if clocks else None
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    t_mean = max_over_ranks(sum(step_ms) / len(step_ms), ws)
+    step_ms = max_over_ranks_vec([a.elapsed_time(b) for a, b in ev], ws)   # per step, max over ranks
+    t_mean = sum(step_ms) / len(step_ms)
     t_med = statistics.median(step_ms)
 
     # ---- optional per-phase breakdown (serialised phases; diagnostics on stderr)
     phases = None
-    if args.phases:
+    counters = None
+    if args.phases or ws > 1:
         world.set_timing(True)
+        world.reset_counters()
         acc = {}
         for _ in range(5):
-            g.copy_(g0)
+            restore()
             step()
             for k_, v_ in world.last_timing().items():
                 acc[k_] = acc.get(k_, 0.0) + v_ / 5
         world.set_timing(False)
         phases = {k_: max_over_ranks(v_, ws) for k_, v_ in acc.items()}
-        if rank == 0:
+        counters = world.counters()
+        if rank == 0 and args.phases:
             print("phases (ms, serialised, max over ranks):", json.dumps(phases), file=sys.stderr)
 
     # ---- e2e: host gradients (pinned) -> device, sync, result -> host, through
@@ -427,8 +568,27 @@ def main():
             pass
         bytes_per_rank = 4 * total
         value = ws * bytes_per_rank / (t_mean / 1e3) / 1e9
+        link = None
+        if ws > 1:
+            # NVLink: bytes this rank pushed per step (fused collectives) and the
+            # cost-table volume, against the serialised comm phase and the link
+            push_b = counters["pushed"] / 5
+            logical = counters["sent"] / 5
+            comm_ms = phases.get("comm_ms") if phases else None
+            link = {"bytes_pushed_per_rank_per_step": push_b, "cost_table_bytes_per_rank_per_step": logical,
+                    "comm_ms_serialised": comm_ms,
+                    "achieved_GBps": push_b / (comm_ms * 1e-3) / 1e9 if comm_ms else None,
+                    "peak_GBps": 770.0, "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
+                    "frac": (push_b / (comm_ms * 1e-3) / 1e9) / 770.0 if comm_ms else None}
+            if nvl0 and nvl1 and "tx" in nvl0 and "tx" in nvl1:
+                link["nvml_tx_bytes_per_step"] = (nvl1["tx"] - nvl0["tx"]) / args.steps
+                link["nvml_rx_bytes_per_step"] = (nvl1["rx"] - nvl0["rx"]) / args.steps
+                link["nvml_source"] = nvl1["source"]
+            else:
+                link["nvml"] = nvl1
         line = {
             "metric": "compressed gradient-sync GB/s", "value": value, "unit": "GB/s",
+            "value_per_rank": bytes_per_rank / (t_mean / 1e3) / 1e9,
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_mean,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
@@ -436,8 +596,8 @@ def main():
                        "params_per_rank": total, "parallelism": f"dp{ws}",
                        "strategy": sorted({strategy_str(rule, N) for N in sizes}),
                        "median_ms_per_step": t_med, "wall_ms_per_step_incl_input_restore": wall * 1e3 / args.steps,
-                       "l2": "inputs 4x params bytes per rank >> 126 MB L2; a D2D input restore (outside the "
-                             "per-step events) also evicts L2 between steps"},
+                       "l2": "flushed: after the (untimed) gradient restore, a 252 MB buffer (2x L2) is "
+                             "written before every timed step"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"] if achieved else None, "traffic": traffic,
                          "kernel": "h1 streaming pass (dgc_stream_kernel / tma_stream_kernel<SignOp|RandomkOp> / pack_kernel)",
@@ -452,7 +612,10 @@ def main():
             "gpu_launches": launches,
             "clocks": clk,
             **({"phases_ms_serialised": phases} if phases else {}),
+            **({"link": link} if link else {}),
         }
+        if not args.no_latency:
+            line["latency_config1"] = latency_config1(E, local)
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args, model, rule, sizes, names, 1)
         emit(line)

@@ -127,6 +127,9 @@ typedef struct {
   uint64_t recv[ESP_NUM_OPS];
   uint64_t h1_calls;      /* compress applications on the critical rank */
   uint64_t h2_pieces;     /* decompressed pieces on the critical rank */
+  uint64_t pushed;        /* bytes this rank actually stored into peers' memory over
+                             NVLink (fused collectives; the cost-table figures above
+                             are logical volumes) */
 } esp_counters_t;
 
 /* Per-phase device times of the last esp_sync / esp_sync_many (ms, CUDA events;
@@ -145,6 +148,15 @@ esp_status_t esp_get_nccl_unique_id(void* out128);
 esp_status_t esp_world_create_nccl(const void* id128, int nranks, int rank, int cuda_dev,
                                    esp_world_t* out);
 esp_status_t esp_world_create_sim(int nranks, int cuda_dev, esp_world_t* out);
+/* Loopback group (tests): nranks worlds in this process on one GPU, out[r]
+ * acting as rank r of an nranks-rank job with the fused (byte-moving)
+ * collectives of a real multi-GPU run -- the same job tables, slot layouts,
+ * arrival counters and call parities -- over plain device pointers instead of
+ * CUDA IPC.  Synchronised only through esp_sync_many_loopback, which runs
+ * every rank's kernels on one stream in dependency order (no kernel waits for
+ * a later one).  NCCL-reduced buckets (NONE, Randomk Allreduce) are
+ * ESP_ERR_UNSUPPORTED here.  Each world is destroyed with esp_world_destroy. */
+esp_status_t esp_world_create_loopback(int nranks, int cuda_dev, esp_world_t* out /* [nranks] */);
 esp_status_t esp_world_destroy(esp_world_t w);
 esp_status_t esp_world_check(esp_world_t w);   /* async CUDA/NCCL errors */
 esp_status_t esp_world_info(esp_world_t w, int* nranks, int* rank, int* nlocal);
@@ -223,6 +235,10 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
 esp_status_t esp_sync(esp_world_t w, esp_ctx_t c, float* grad_inout, void* stream);
 esp_status_t esp_sync_many(esp_world_t w, const esp_ctx_t* ctxs, float* const* grads,
                            int ntensors, void* stream);
+/* esp_sync_many for every rank of a loopback group: ctxs and grads are
+ * [nranks][ntensors] (rank-major), ctxs[r][.] created on worlds[r]. */
+esp_status_t esp_sync_many_loopback(const esp_world_t* worlds, int nranks, const esp_ctx_t* ctxs,
+                                    float* const* grads, int ntensors, void* stream);
 
 /* ---- sizes / cost table ----------------------------------------------
  * esp_compressed_bytes: bytes of one rank's payload for numel elements split

@@ -393,14 +393,40 @@ esp_status_t esp_sync_many(esp_world_t w, const esp_ctx_t* ctxs, float* const* g
     check_ptr4(grads[i], "grad");
     for (int j = 0; j < i; ++j) ESP_REQUIRE(v[j] != v[i], ESP_ERR_INVALID_ARG, "ctx listed twice");
   }
+  ESP_REQUIRE(!w->loopback, ESP_ERR_STATE, "a loopback world syncs through esp_sync_many_loopback");
   ESP_CUDA(cudaSetDevice(w->dev));
   Plan* p = get_plan(w, v);
   execute_plan(p, grads, as_stream(stream));
   ESP_API_END
 }
 
+esp_status_t esp_sync_many_loopback(const esp_world_t* worlds, int nranks, const esp_ctx_t* ctxs,
+                                    float* const* grads, int ntensors, void* stream) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(worlds && ctxs && grads && nranks >= 2 && ntensors >= 1, ESP_ERR_INVALID_ARG, "bad argument");
+  std::vector<Plan*> plans(nranks);
+  std::vector<float* const*> gr(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    esp_world_s* w = worlds[r];
+    ESP_REQUIRE(w && w->loopback && w->nranks == nranks && w->rank == r, ESP_ERR_STATE,
+                "worlds[r] must be rank r of one loopback group");
+    ESP_REQUIRE(w->dev == worlds[0]->dev, ESP_ERR_STATE, "a loopback group lives on one device");
+    std::vector<esp_ctx_s*> v(ctxs + (size_t)r * ntensors, ctxs + (size_t)(r + 1) * ntensors);
+    for (int i = 0; i < ntensors; ++i) {
+      ESP_REQUIRE(v[i] && v[i]->w == w, ESP_ERR_STATE, "ctxs[r][i] must belong to worlds[r]");
+      check_ptr4(grads[(size_t)r * ntensors + i], "grad");
+    }
+    ESP_CUDA(cudaSetDevice(w->dev));
+    plans[r] = get_plan(w, v);
+    gr[r] = grads + (size_t)r * ntensors;
+  }
+  execute_loopback(plans, gr, as_stream(stream));
+  ESP_API_END
+}
+
 esp_status_t esp_sync(esp_world_t w, esp_ctx_t c, float* grad_inout, void* stream) {
   ESP_API_BEGIN
+  ESP_REQUIRE(!w || !w->loopback, ESP_ERR_STATE, "a loopback world syncs through esp_sync_many_loopback");
   ESP_REQUIRE(w && c, ESP_ERR_INVALID_ARG, "null argument");
   ESP_REQUIRE(c->w == w, ESP_ERR_STATE, "ctx belongs to another world");
   check_ptr4(grad_inout, "grad");

@@ -84,6 +84,7 @@ struct Plan;
 
 struct esp_world_s {
   bool sim = false;
+  bool loopback = false;                   // one of n worlds of one process acting as ranks (tests)
   int nranks = 1, rank = 0, nlocal = 1, dev = 0;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
@@ -171,6 +172,8 @@ void coll_allgather_inplace_f32(esp_world_s* w, LocalBufs buf, size_t count_per_
 Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs);
 void drop_plans_with(esp_world_s* w, esp_ctx_s* c);
 void execute_plan(Plan* p, float* const* grads, cudaStream_t st);
+// the n worlds of a loopback group as ranks 0..n-1 on one GPU (plans[r] of world r)
+void execute_loopback(const std::vector<Plan*>& plans, const std::vector<float* const*>& grads, cudaStream_t st);
 // h1 only, copying each rank's payload to `payload` (esp_compress)
 void execute_compress(Plan* p, const float* grad, void* payload, cudaStream_t st);
 void clear_plans(esp_world_s* w);

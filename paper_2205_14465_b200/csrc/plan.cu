@@ -76,6 +76,7 @@ struct Bucket {
   LocalBufs stage{};
   PushJob* push1 = nullptr; int npush1 = 0;
   PushJob* push2 = nullptr; int npush2 = 0;
+  uint64_t push1_bytes = 0, push2_bytes = 0, push2_odd_bytes = 0;   // bytes moved per call
   // process-1 Gather/Broadcast: the root forwards all n payloads; its jobs read
   // from anywhere in its arena (own payload: send, the others: recv1 of the
   // call's parity), so there is one table per parity and src = arena base
@@ -805,6 +806,10 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     up(TB.push2_odd, b.push2_odd);
     b.npush1 = (int)TB.push1.size();
     b.npush2 = (int)TB.push2.size();
+    b.push1_bytes = b.push2_bytes = b.push2_odd_bytes = 0;
+    for (const PushJob& j : TB.push1) b.push1_bytes += j.bytes;
+    for (const PushJob& j : TB.push2) b.push2_bytes += j.bytes;
+    for (const PushJob& j : TB.push2_odd) b.push2_odd_bytes += j.bytes;
     b.nh2_off_jobs = (int)TB.off_jobs.size();
     if (commit) {
       // pad patterns of every chunk that kernels never touch (R: payload layout)
@@ -856,6 +861,8 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
 // the arena through the NCCL communicator (a collective: done on the first
 // esp_sync / esp_sync_many of the plan, which every rank calls) and build the
 // destination / counter tables.
+static void build_peer_tables(Plan& p, const std::vector<unsigned char*>& base);
+
 static void open_peers(Plan& p, cudaStream_t st) {
   esp_world_s* w = p.w;
   const int n = w->nranks;
@@ -881,6 +888,13 @@ static void open_peers(Plan& p, cudaStream_t st) {
       base[q] = static_cast<unsigned char*>(ptr);
     }
   }
+  build_peer_tables(p, base);
+}
+
+// destination / counter tables of every fused bucket from the n arena bases
+static void build_peer_tables(Plan& p, const std::vector<unsigned char*>& base) {
+  esp_world_s* w = p.w;
+  const int n = w->nranks;
   auto upload = [](auto& dev, const auto& host) {
     ESP_CUDA(cudaMalloc(&dev, sizeof(host[0]) * host.size()));
     ESP_CUDA(cudaMemcpy(dev, host.data(), sizeof(host[0]) * host.size(), cudaMemcpyHostToDevice));
@@ -1099,76 +1113,96 @@ static void run_mid(Plan& p, Bucket& b, cudaStream_t cs) {
   ESP_CUDA(cudaGetLastError());
 }
 
+// Fused collective of a bucket in three stages.  Every rank runs them in
+// order; across ranks, stage s of any rank may depend only on stages < s of
+// the others (stage 1 pushes the first payloads, stage 2 waits for them and
+// runs the owner's / root's a7 and second push, stage 3 waits for those), so
+// the loopback executor can run all ranks' stage 1, then all stage 2, then all
+// stage 3, on one stream with every wait already satisfied when it starts.
+// push_kernel moves the local payloads (h1's send, then a7's stage) to the
+// peers; a wait kernel blocks on the counter of this call's parity (monotonic
+// across that parity's calls).  The byte counters record the routine's
+// logical traffic (the cost table).
+static void fused_stage(Plan& p, Bucket& b, int stage, cudaStream_t cs, cudaEvent_t mid0, cudaEvent_t mid1) {
+  esp_world_s* w = p.w;
+  const int n = w->nranks;
+  const size_t S = b.slot;
+  const bool quant = b.p2;   // a mid-scheme recompression between the two phases
+  const int par = (int)(b.epoch & 1);
+  const unsigned long long e1 = (b.epoch >> 1) + 1;   // calls of this parity so far, this one included
+  unsigned long long* cnt1 = b.my_cnt + par;          // [2 * phase + parity]
+  unsigned long long* cnt2 = b.my_cnt + 2 + par;
+  const bool root = w->rank == 0;
+  auto push2 = [&] {
+    if (b.push2_arena)
+      launch_push(par ? b.push2_odd : b.push2, b.npush2, p.arena.base, b.dsts2 + par * n, b.cnts2 + par * n, cs);
+    else
+      launch_push(b.push2, b.npush2, b.stage.at(0), b.dsts2 + par * n, b.cnts2 + par * n, cs);
+    w->counters[0].pushed += par && b.push2_arena ? b.push2_odd_bytes : b.push2_bytes;
+    dbg("push phase 2", cs);
+  };
+  auto mid = [&] {
+    if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
+    run_mid(p, b, cs);
+    if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
+  };
+  auto wait = [&](unsigned long long* c, uint64_t target) {
+    launch_wait_arrivals(c, e1 * target, w->wait_err, w->wait_timeout_ns, cs);
+    dbg("wait", cs);
+  };
+  if (stage == 1) {
+    launch_push(b.push1, b.npush1, b.send.at(0), b.dsts + par * n, b.cnts + par * n, cs);
+    w->counters[0].pushed += b.push1_bytes;
+    dbg("push phase 1", cs);
+    return;
+  }
+  switch (b.routine) {
+    case ESP_ALLGATHER:
+      if (stage == 2) {
+        count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
+        wait(cnt1, b.target1);
+      }
+      break;
+    case ESP_ALLTOALL_ALLGATHER:
+      if (stage == 2) {
+        count_coll(w, 0, ESP_OP_ALLTOALL, (n - 1) * S, (n - 1) * S);
+        wait(cnt1, b.target1);
+        if (quant) {
+          mid();
+          push2();
+          count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
+        } else {
+          count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * n * S, (n - 1) * n * S);
+        }
+      } else if (quant) {
+        wait(cnt2, b.target2);
+      }
+      break;
+    default:   // Gather/Broadcast
+      if (stage == 2) {
+        count_coll(w, 0, ESP_OP_GATHER, root ? 0 : S, root ? (n - 1) * S : 0);
+        if (root) {
+          wait(cnt1, b.target1);
+          if (quant) mid();   // process 2: the root's mid-scheme recompression
+          push2();            // process 1: the root forwards the n payloads
+        }
+        const size_t bc = quant ? S : (size_t)n * S;
+        count_coll(w, 0, ESP_OP_BROADCAST, root ? bc : 0, root ? 0 : bc);
+      } else {
+        wait(cnt2, b.target2);
+      }
+      break;
+  }
+  ESP_CUDA(cudaGetLastError());
+}
+
 static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cudaEvent_t mid1) {
   esp_world_s* w = p.w;
   const int n = w->nranks;
   const size_t S = b.slot;
   const bool quant = b.p2;   // a mid-scheme recompression between the two phases
   if (b.fused) {
-    // push_kernel moves the local payloads (h1's send, then a7's stage) to
-    // the peers; wait for this call's arrivals on the counter of this call's
-    // parity (monotonic across that parity's calls).  The byte counters record
-    // the routine's logical traffic (the cost table)
-    const int par = (int)(b.epoch & 1);
-    const unsigned long long e1 = (b.epoch >> 1) + 1;   // calls of this parity so far, this one included
-    unsigned long long* cnt1 = b.my_cnt + par;          // [2 * phase + parity]
-    unsigned long long* cnt2 = b.my_cnt + 2 + par;
-    auto push1 = [&] {
-      launch_push(b.push1, b.npush1, b.send.at(0), b.dsts + par * n, b.cnts + par * n, cs);
-      dbg("push phase 1", cs);
-    };
-    auto push2 = [&] {
-      if (b.push2_arena)
-        launch_push(par ? b.push2_odd : b.push2, b.npush2, p.arena.base, b.dsts2 + par * n, b.cnts2 + par * n, cs);
-      else
-        launch_push(b.push2, b.npush2, b.stage.at(0), b.dsts2 + par * n, b.cnts2 + par * n, cs);
-      dbg("push phase 2", cs);
-    };
-    push1();
-    switch (b.routine) {
-      case ESP_ALLGATHER:
-        count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
-        launch_wait_arrivals(cnt1, e1 * b.target1, w->wait_err, w->wait_timeout_ns, cs);
-        dbg("wait phase 1", cs);
-        break;
-      case ESP_ALLTOALL_ALLGATHER:
-        count_coll(w, 0, ESP_OP_ALLTOALL, (n - 1) * S, (n - 1) * S);
-        launch_wait_arrivals(cnt1, e1 * b.target1, w->wait_err, w->wait_timeout_ns, cs);
-        dbg("wait phase 1", cs);
-        if (quant) {
-          if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
-          run_mid(p, b, cs);
-          if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
-          push2();
-          count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * S, (n - 1) * S);
-          launch_wait_arrivals(cnt2, e1 * b.target2, w->wait_err, w->wait_timeout_ns, cs);
-        dbg("wait phase 2", cs);
-        } else {
-          count_coll(w, 0, ESP_OP_ALLGATHER, (n - 1) * n * S, (n - 1) * n * S);
-        }
-        break;
-      default: {   // Gather/Broadcast
-        const bool root = w->rank == 0;
-        count_coll(w, 0, ESP_OP_GATHER, root ? 0 : S, root ? (n - 1) * S : 0);
-        if (root) {
-          launch_wait_arrivals(cnt1, e1 * b.target1, w->wait_err, w->wait_timeout_ns, cs);
-          dbg("wait phase 1", cs);
-          if (quant) {   // process 2: the root's mid-scheme recompression
-            if (mid0) ESP_CUDA(cudaEventRecord(mid0, cs));
-            run_mid(p, b, cs);
-            if (mid1) ESP_CUDA(cudaEventRecord(mid1, cs));
-          }
-          push2();
-        }
-        // process 1 broadcasts the n payloads, process 2 one
-        const size_t bc = quant ? S : (size_t)n * S;
-        count_coll(w, 0, ESP_OP_BROADCAST, root ? bc : 0, root ? 0 : bc);
-        launch_wait_arrivals(cnt2, e1 * b.target2, w->wait_err, w->wait_timeout_ns, cs);
-        dbg("wait phase 2", cs);
-        break;
-      }
-    }
-    ESP_CUDA(cudaGetLastError());
+    for (int stage = 1; stage <= 3; ++stage) fused_stage(p, b, stage, cs, mid0, mid1);
     return;
   }
   switch (b.routine) {
@@ -1332,6 +1366,49 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
     }
   }
   for (auto* c : p.ctxs) c->step += 1;
+}
+
+// Loopback: the n worlds of one process on one GPU act as ranks 0..n-1 of a
+// fused-collective job.  Their plans address each other's arenas directly (no
+// IPC), and every kernel runs on one stream in an order that satisfies every
+// dependency before it is launched: all ranks' h1, then stage 1 (pushes) of
+// all ranks, stage 2, stage 3 (fused_stage), then all ranks' h2.  No kernel
+// ever waits for a kernel launched after it, so nothing relies on concurrent
+// residency on one GPU; a wrong job table leaves a counter short and its wait
+// kernel reports a timeout.  This runs the real ranks' job tables, slot
+// layouts, parities and counters for any n on a single GPU (tests).
+void execute_loopback(const std::vector<Plan*>& plans, const std::vector<float* const*>& grads, cudaStream_t st) {
+  const int n = (int)plans.size();
+  for (Plan* p : plans)
+    for (const Bucket& b : p->buckets)
+      ESP_REQUIRE(b.fused, ESP_ERR_UNSUPPORTED,
+                  "loopback worlds run the fused (byte-moving) routines only; NCCL-reduced buckets need a real world");
+  for (Plan* p : plans) {
+    ESP_REQUIRE(p->buckets.size() == plans[0]->buckets.size(), ESP_ERR_STATE, "ranks disagree on the bucketing");
+    if (!p->peers_ready) {
+      std::vector<unsigned char*> base(n);
+      for (int q = 0; q < n; ++q) base[q] = plans[q]->arena.base;
+      build_peer_tables(*p, base);
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    Plan& p = *plans[r];
+    ESP_REQUIRE(!*const_cast<volatile unsigned int*>(p.w->wait_err_host), ESP_ERR_NCCL,
+                "a payload did not arrive within the wait timeout of an earlier call");
+    upload_dyn(p, grads[r], st);
+    if (p.zero_bytes) ESP_CUDA(cudaMemsetAsync(p.zero, 0, p.zero_bytes, st));
+  }
+  for (size_t i = 0; i < plans[0]->buckets.size(); ++i) {
+    for (int r = 0; r < n; ++r) run_h1(*plans[r], plans[r]->buckets[i], st);
+    for (int stage = 1; stage <= 3; ++stage)
+      for (int r = 0; r < n; ++r) fused_stage(*plans[r], plans[r]->buckets[i], stage, st, nullptr, nullptr);
+    for (int r = 0; r < n; ++r) {
+      run_h2(*plans[r], plans[r]->buckets[i], st);
+      ++plans[r]->buckets[i].epoch;
+    }
+  }
+  for (Plan* p : plans)
+    for (auto* c : p->ctxs) c->step += 1;
 }
 
 void execute_compress(Plan* pp, const float* grad, void* payload, cudaStream_t st) {

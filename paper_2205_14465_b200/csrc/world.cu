@@ -292,6 +292,26 @@ esp_status_t esp_world_create_sim(int nranks, int cuda_dev, esp_world_t* out) {
   ESP_API_END
 }
 
+esp_status_t esp_world_create_loopback(int nranks, int cuda_dev, esp_world_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(out, ESP_ERR_INVALID_ARG, "out is NULL");
+  ESP_REQUIRE(nranks >= 2 && nranks <= 64 && cuda_dev >= 0, ESP_ERR_INVALID_ARG, "bad nranks/device");
+  std::vector<std::unique_ptr<esp_world_s>> ws;
+  for (int r = 0; r < nranks; ++r) {
+    auto w = std::make_unique<esp_world_s>();
+    w->loopback = true;
+    w->nranks = nranks;
+    w->rank = r;
+    w->nlocal = 1;
+    w->dev = cuda_dev;
+    w->wait_timeout_ns = 5ull * 1000000000ull;   // every wait is satisfied at launch: 5 s means a bug
+    world_common_init(w.get());
+    ws.push_back(std::move(w));
+  }
+  for (int r = 0; r < nranks; ++r) out[r] = ws[r].release();
+  ESP_API_END
+}
+
 esp_status_t esp_world_destroy(esp_world_t w) {
   ESP_API_BEGIN
   ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");

@@ -27,7 +27,7 @@ SYMBOLS = (
     "esp_world_check", "esp_world_info", "esp_world_counters", "esp_world_counters_local",
     "esp_world_reset_counters", "esp_world_set_timing", "esp_last_timing", "esp_world_set_bucket_elems",
     "esp_world_set_probe", "esp_probe_read", "esp_world_set_timeout", "esp_world_set_plan_cache",
-    "esp_world_drop_plans",
+    "esp_world_drop_plans", "esp_world_create_loopback", "esp_sync_many_loopback",
     "esp_ctx_create", "esp_ctx_destroy", "esp_ctx_payload_bytes", "esp_ctx_get_state",
     "esp_ctx_set_state", "esp_ctx_get_momentum", "esp_ctx_set_momentum", "esp_compress", "esp_decompress", "esp_sync", "esp_sync_many",
     "esp_compressed_bytes", "esp_wire_bytes", "esp_model_time", "esp_status_string",
@@ -52,7 +52,7 @@ class Option(C.Structure):
 
 class Counters(C.Structure):
     _fields_ = [("calls", C.c_uint64 * 7), ("sent", C.c_uint64 * 7), ("recv", C.c_uint64 * 7),
-                ("h1_calls", C.c_uint64), ("h2_pieces", C.c_uint64)]
+                ("h1_calls", C.c_uint64), ("h2_pieces", C.c_uint64), ("pushed", C.c_uint64)]
 
 
 class Timing(C.Structure):
@@ -89,6 +89,8 @@ def lib():
             "esp_world_set_probe": [vp, i32],
             "esp_world_set_timeout": [vp, dbl], "esp_world_set_plan_cache": [vp, i32],
             "esp_world_drop_plans": [vp],
+            "esp_world_create_loopback": [i32, i32, C.POINTER(vp)],
+            "esp_sync_many_loopback": [C.POINTER(vp), i32, C.POINTER(vp), C.POINTER(vp), i32, vp],
             "esp_probe_read": [vp, C.POINTER(dbl), C.POINTER(u64), C.POINTER(u64)],
             "esp_ctx_create": [vp, C.POINTER(CompressorCfg), i32, u64, sz, C.POINTER(vp)],
             "esp_ctx_destroy": [vp], "esp_ctx_payload_bytes": [vp, C.POINTER(sz)],
@@ -213,6 +215,14 @@ class World:
         return cls(h, device)
 
     @classmethod
+    def loopback(cls, nranks: int, device: int = 0):
+        """A loopback group: nranks worlds on one GPU acting as ranks 0..n-1 of
+        a fused-collective job (tests; see esp_world_create_loopback)."""
+        hs = (C.c_void_p * nranks)()
+        _check(lib().esp_world_create_loopback(nranks, device, hs))
+        return [cls(C.c_void_p(hs[r]), device) for r in range(nranks)]
+
+    @classmethod
     def nccl(cls, device: int | None = None, group=None):
         import torch
         import torch.distributed as dist
@@ -235,7 +245,7 @@ class World:
     def counters(self, lr: int = 0) -> dict:
         c = Counters()
         _check(lib().esp_world_counters_local(self.h, lr, C.byref(c)))
-        d = {"h1_calls": c.h1_calls, "h2_pieces": c.h2_pieces}
+        d = {"h1_calls": c.h1_calls, "h2_pieces": c.h2_pieces, "pushed": c.pushed}
         for i, op in enumerate(OPS):
             d[op] = {"calls": c.calls[i], "sent": c.sent[i], "recv": c.recv[i]}
         d["sent"] = sum(c.sent)
@@ -382,6 +392,22 @@ def esp_sync_many(world: World, ctxs, grads, stream=None):
     hs = (C.c_void_p * n)(*[c.h.value for c in ctxs])
     gs = (C.c_void_p * n)(*[g.data_ptr() for g in grads])
     _check(lib().esp_sync_many(world.h, hs, gs, n, _stream(stream)))
+    return grads
+
+
+def esp_sync_many_loopback(worlds, ctxs, grads, stream=None):
+    """ctxs[r][i], grads[r][i]: rank r's tensors (ctxs[r] created on worlds[r])."""
+    import torch
+    n, m = len(worlds), len(ctxs[0])
+    for r in range(n):
+        if len(ctxs[r]) != m or len(grads[r]) != m:
+            raise ValueError("every rank needs the same number of tensors")
+        for i, (c, g) in enumerate(zip(ctxs[r], grads[r])):
+            _require(g, f"grads[{r}][{i}]", torch.float32, worlds[r].device, numel=c.numel)
+    ws = (C.c_void_p * n)(*[w.h.value for w in worlds])
+    hs = (C.c_void_p * (n * m))(*[c.h.value for row in ctxs for c in row])
+    gs = (C.c_void_p * (n * m))(*[g.data_ptr() for row in grads for g in row])
+    _check(lib().esp_sync_many_loopback(ws, n, hs, gs, m, _stream(stream)))
     return grads
 
 

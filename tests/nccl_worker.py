@@ -154,9 +154,17 @@ def main():
     w.check()
     w.destroy()
 
-    # a peer that never arrives: rank 0 calls once more than the others; its
-    # wait gives up after the timeout instead of hanging or trapping, and the
-    # world reports the failure (the CUDA context stays usable)
+    if n > 1:
+        missing_peer(rank, local)
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"rank {rank}: {checked} pair-steps + sync_many ok", flush=True)
+
+
+def missing_peer(rank, local):
+    """A peer that never arrives: rank 0 calls once more than the others; its
+    wait gives up after the timeout instead of hanging or trapping, and the
+    world reports the failure (the CUDA context stays usable)."""
     w2 = E.World.nccl(local)
     w2.set_timeout(2.0)
     c2 = E.Ctx(w2, "dgc", "allgather", 5000, tensor_id=400, ratio=0.01)
@@ -177,9 +185,6 @@ def main():
     dist.barrier()
     c2.destroy()
     w2.destroy()
-    dist.barrier()
-    dist.destroy_process_group()
-    print(f"rank {rank}: {checked} pair-steps + sync_many ok", flush=True)
 
 
 if __name__ == "__main__":

@@ -142,6 +142,18 @@ def test_sign_sizes(kind, N):
     run_sim(kind, "alltoall_allgather", 4, N, steps=2)
 
 
+@pytest.mark.parametrize("kind", ["efsignsgd", "onebit"])
+@pytest.mark.parametrize("routine,process", [("allgather", 0), ("alltoall_allgather", 2), ("alltoall_allgather", 1),
+                                             ("gather_broadcast", 2)])
+def test_sign_segments_beyond_one_finalize_chunk(kind, routine, process):
+    """Segments longer than kFinRuns x 512 = 8,388,608 elements take the
+    finalize kernel's two-level (chunked) reduction of the per-run partials,
+    in h1 and in a7 -- the path config 2's 2^26..2^30-byte sweep points and
+    large tensors run.  N = 2^24 + 2^20 + 77: whole-tensor segments of 17.8 M
+    elements, Alltoall partitions of 8.9 M (n = 2)."""
+    run_sim(kind, routine, 2, (1 << 24) + (1 << 20) + 77, steps=2, process=process)
+
+
 def test_randomk_unshared_and_sum():
     run_sim("randomk", "allgather", 4, 10_000, steps=3, ratio=0.03, shared=False)
     run_sim("dgc", "allgather", 4, 10_000, steps=2, reduce="sum")
