@@ -446,9 +446,10 @@ def main():
 
     # ---- timed region: K steps, per-step CUDA events on the launching stream.
     # Before every step: the input restore (the "backward pass" that produces
-    # fresh gradients) and the L2 flush, a device synchronize and a barrier
-    # across ranks, so that every rank starts the step together; the step's
-    # time is then the max over ranks of its event time
+    # fresh gradients), the L2 flush and, with several ranks, a barrier ON THE
+    # GPU (a one-element NCCL all-reduce on the stream), so that every rank's
+    # step starts together while the host keeps enqueueing ahead; the step's
+    # time is the max over ranks of its event time
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local) if rank == 0 else None
     if clocks:
@@ -460,11 +461,12 @@ def main():
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     nvl0 = nvlink_bytes(local) if ws > 1 else None
+    gbar = torch.zeros(1, device="cuda")
     for i in range(args.steps):
         restore()
         if ws > 1:
-            torch.cuda.synchronize()
-            barrier(ws)
+            import torch.distributed as dist
+            dist.all_reduce(gbar)   # device-side barrier: the step starts when every rank got here
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)

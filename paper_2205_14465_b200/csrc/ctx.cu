@@ -375,8 +375,8 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
       launch_h2_sparse(dseg, dunits, (int)u0, reinterpret_cast<const uint4*>(d + off_ps), njobs, dpp, npieces, st);
       break;
     case ESP_RANDOMK: launch_h2_randomk(dseg, dunits, (int)u0, dpp, drt, st); break;
-    case ESP_EFSIGNSGD: launch_h2_sign(K_EFSIGN, dseg, dunits, (int)u0, dpp, st); break;
-    default: launch_h2_sign(K_ONEBIT, dseg, dunits, (int)u0, dpp, st); break;
+    case ESP_EFSIGNSGD: launch_h2_sign(K_EFSIGN, dseg, dunits, (int)u0, dpp, npieces, st); break;
+    default: launch_h2_sign(K_ONEBIT, dseg, dunits, (int)u0, dpp, npieces, st); break;
   }
   ESP_CUDA(cudaGetLastError());
   ESP_API_END
@@ -387,15 +387,20 @@ esp_status_t esp_sync_many(esp_world_t w, const esp_ctx_t* ctxs, float* const* g
   ESP_API_BEGIN
   ESP_REQUIRE(w && ctxs && grads && ntensors >= 1, ESP_ERR_INVALID_ARG, "bad argument");
   std::vector<esp_ctx_s*> v(ctxs, ctxs + ntensors);
-  for (int i = 0; i < ntensors; ++i) {
-    ESP_REQUIRE(v[i], ESP_ERR_INVALID_ARG, "ctx is NULL");
-    ESP_REQUIRE(v[i]->w == w, ESP_ERR_STATE, "ctx belongs to another world");
-    check_ptr4(grads[i], "grad");
-    for (int j = 0; j < i; ++j) ESP_REQUIRE(v[j] != v[i], ESP_ERR_INVALID_ARG, "ctx listed twice");
-  }
+  for (int i = 0; i < ntensors; ++i) check_ptr4(grads[i], "grad");
   ESP_REQUIRE(!w->loopback, ESP_ERR_STATE, "a loopback world syncs through esp_sync_many_loopback");
+  // a cached plan was built from exactly this validated ctx list
+  Plan* p = find_plan(w, v);
+  if (!p) {
+    std::set<esp_ctx_s*> seen;
+    for (int i = 0; i < ntensors; ++i) {
+      ESP_REQUIRE(v[i], ESP_ERR_INVALID_ARG, "ctx is NULL");
+      ESP_REQUIRE(w->ctxs.count(v[i]) && v[i]->w == w, ESP_ERR_STATE, "ctx belongs to another world");
+      ESP_REQUIRE(seen.insert(v[i]).second, ESP_ERR_INVALID_ARG, "ctx listed twice");
+    }
+  }
   ESP_CUDA(cudaSetDevice(w->dev));
-  Plan* p = get_plan(w, v);
+  if (!p) p = get_plan(w, v);
   execute_plan(p, grads, as_stream(stream));
   ESP_API_END
 }

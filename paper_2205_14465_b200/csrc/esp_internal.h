@@ -170,6 +170,7 @@ void coll_allgather_inplace_f32(esp_world_s* w, LocalBufs buf, size_t count_per_
 
 // ---- plans ------------------------------------------------------------------
 Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs);
+Plan* find_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs);   // nullptr if not cached
 void drop_plans_with(esp_world_s* w, esp_ctx_s* c);
 void execute_plan(Plan* p, float* const* grads, cudaStream_t st);
 // the n worlds of a loopback group as ranks 0..n-1 on one GPU (plans[r] of world r)

@@ -40,8 +40,9 @@ void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaSt
 // shared-memory accumulation path and its dynamic shared memory)
 void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
                       const unsigned char* const* pieces, int max_pieces, cudaStream_t st);
+// max_pieces: the largest npieces of the launch's segments (sizes the shared-memory word stage)
 void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
-                    const unsigned char* const* pieces, cudaStream_t st);
+                    const unsigned char* const* pieces, int max_pieces, cudaStream_t st);
 void launch_h2_randomk(const SegH2* segs, const uint32_t* unit_seg, int nunits,
                        const unsigned char* const* pieces, const uint32_t* rankterms, cudaStream_t st);
 void launch_h2_dense(const SegH2* segs, const uint32_t* unit_seg, int nunits,

@@ -145,18 +145,39 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
       for (int i = lane * 4; i < kTile; i += 128)
         *reinterpret_cast<float4*>(acc + i) = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncwarp();
-      for (uint32_t r = 0; r < np; ++r) {
-        const unsigned char* pc = reinterpret_cast<const unsigned char*>(__shfl_sync(
-            kFull, reinterpret_cast<unsigned long long>(r < 32 ? pp0 : pp1), r & 31));
-        const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
-        const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
-        uint32_t a, b;
-        range(r, &a, &b);
-        for (uint32_t i = a + lane; i < b; i += 32) {
-          const uint32_t w = __ldg(idx + i) - lo;
-          acc[w] = __fadd_rn(acc[w], __ldg(val + i));   // distinct indices within a piece
+      // pieces in batches of kH2Batch: the first 32 entries of every piece of
+      // the batch are loaded (all in flight) before the first is added; the
+      // adds then run piece by piece in rank order (indices are distinct
+      // within a piece, __syncwarp orders the pieces)
+      constexpr int kH2Batch = 8;
+      for (uint32_t r0 = 0; r0 < np; r0 += kH2Batch) {
+        uint32_t wi[kH2Batch];
+        float wv[kH2Batch];
+        const unsigned char* pcs[kH2Batch];
+        uint32_t ra[kH2Batch], rb[kH2Batch];
+#pragma unroll
+        for (int m = 0; m < kH2Batch; ++m) {
+          const uint32_t r = r0 + m < np ? r0 + m : np - 1;   // warp-uniform
+          pcs[m] = reinterpret_cast<const unsigned char*>(__shfl_sync(
+              kFull, reinterpret_cast<unsigned long long>(r < 32 ? pp0 : pp1), r & 31));
+          range(r, &ra[m], &rb[m]);
+          const uint32_t i = ra[m] + lane;
+          const bool ok = r0 + m < np && i < rb[m];
+          wi[m] = ok ? __ldg(reinterpret_cast<const uint32_t*>(pcs[m]) + i) : 0u;
+          wv[m] = ok ? __ldg(reinterpret_cast<const float*>(pcs[m] + 4 * (size_t)S.kpad) + i) : 0.f;
         }
-        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < kH2Batch; ++m) {
+          if (r0 + m >= np) break;   // warp-uniform
+          if (ra[m] + lane < rb[m]) acc[wi[m] - lo] = __fadd_rn(acc[wi[m] - lo], wv[m]);
+          const uint32_t* idx = reinterpret_cast<const uint32_t*>(pcs[m]);
+          const float* val = reinterpret_cast<const float*>(pcs[m] + 4 * (size_t)S.kpad);
+          for (uint32_t i = ra[m] + lane + 32; i < rb[m]; i += 32) {   // dense tiles (TOPK, large ratios)
+            const uint32_t w = __ldg(idx + i) - lo;
+            acc[w] = __fadd_rn(acc[w], __ldg(val + i));
+          }
+          __syncwarp();
+        }
       }
       for (uint32_t i = lane * 4; lo + i < hi; i += 128) {
         float4 v = *reinterpret_cast<const float4*>(acc + i);
@@ -219,14 +240,23 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
 // Sign h2: a grid of a few CTAs per SM, each over a contiguous range of the
 // bucket's units (mostly inside one segment), so the dependent prologue of a
 // segment (its table entry, the piece pointers and scales) is paid once per
-// (CTA, segment) instead of once per unit.  Per unit: pieces outer, the
-// thread's kJ float4 inner, so all kJ word loads of a piece are in flight
-// together; rank-order fp32 sum from +0, then / divisor (R9).
+// (CTA, segment) instead of once per unit.  Per unit (8192 elements = 256
+// words = 1 KB per piece) the words of ALL pieces are loaded with coalesced
+// 16-byte loads, one round trip for the whole unit, and parked in shared
+// memory; the next unit's words are already in flight (registers) while this
+// unit is decoded and stored, so the 4 B/elem output stream never waits on a
+// word load.  Decode: rank-order fp32 sum from +0 over the pieces, then /
+// divisor (R9); a word is read from shared memory by the 8 lanes that decode
+// it (broadcast).
+constexpr int kSignWords = kSignUnit / 32;           // words per piece and unit
+constexpr int kSignVec = kSignWords / 4;             // uint4 per piece and unit
+constexpr int kSignPre = 4;                          // uint4 per thread in flight (pieces <= 16)
 template <int KIND>
 __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restrict__ segs,
                                                            const uint32_t* __restrict__ unit_seg,
                                                            uint32_t nunits,
                                                            const unsigned char* const* __restrict__ pieces) {
+  extern __shared__ __align__(16) uint32_t sh_words[];   // [npieces][kSignWords]
   __shared__ float sh_sp[kMaxPieces], sh_sn[kMaxPieces];
   __shared__ const uint32_t* sh_w[kMaxPieces];
   constexpr int kJ = kSignUnit / (kThreads * 4);
@@ -234,17 +264,20 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
   const uint32_t u1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nunits / gridDim.x);
   uint32_t cur = 0xFFFFFFFFu;
   SegH2 S{};
-  // single-piece segments (the owner's recompressed partition, one broadcast
-  // payload): the next unit's words are loaded while this unit is computed and
-  // stored (the loop was bound by one word-load latency per unit)
-  uint32_t wnext[kJ];
-  bool have_next = false;
+  uint4 pre[kSignPre];       // the next unit's words (vector v = threadIdx.x + m * kThreads)
+  bool have = false;         // pre[] holds the words of unit gu
   uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
+  // vector v of unit (start word w0) of the current segment: piece v / kSignVec
+  auto load_vec = [&](uint32_t v, uint32_t w0, uint32_t nwords) -> uint4 {
+    const uint32_t r = v / kSignVec, q = v % kSignVec;
+    const uint32_t w = w0 + q * 4;
+    return w < nwords ? __ldg(reinterpret_cast<const uint4*>(sh_w[r] + w)) : make_uint4(0u, 0u, 0u, 0u);
+  };
   for (uint32_t gu = u0; gu < u1; ++gu) {
     const uint32_t sid = sid_next;
     if (gu + 1 < u1) sid_next = unit_seg[gu + 1];
     if (sid != cur) {
-      __syncthreads();   // the previous segment's table is no longer read
+      __syncthreads();   // the previous segment's tables and words are no longer read
       cur = sid;
       S = segs[sid];
       for (uint32_t r = threadIdx.x; r < S.npieces; r += kThreads) {
@@ -255,61 +288,66 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
         sh_w[r] = reinterpret_cast<const uint32_t*>(h + 16);
       }
       __syncthreads();
-      have_next = false;
+      have = false;
     }
-    const uint32_t n = S.n;
+    const uint32_t n = S.n, np = S.npieces;
+    const uint32_t nwords = (n + 31) / 32;   // words a piece carries for this segment
+    const uint32_t nvec = np * kSignVec;
+    const uint32_t w0 = (gu - S.unit0) * kSignWords;
+    const bool prefetch = nvec <= (uint32_t)(kSignPre * kThreads);
+    __syncthreads();   // the previous unit's words are decoded
+    if (prefetch) {
+      if (!have) {
+#pragma unroll
+        for (int m = 0; m < kSignPre; ++m) {
+          const uint32_t v = threadIdx.x + m * kThreads;
+          if (v < nvec) pre[m] = load_vec(v, w0, nwords);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < kSignPre; ++m) {
+        const uint32_t v = threadIdx.x + m * kThreads;
+        if (v < nvec) reinterpret_cast<uint4*>(sh_words)[v] = pre[m];
+      }
+      // the next unit of the same segment: its loads fly while this one is decoded
+      have = gu + 1 < u1 && sid_next == cur;
+      if (have) {
+#pragma unroll
+        for (int m = 0; m < kSignPre; ++m) {
+          const uint32_t v = threadIdx.x + m * kThreads;
+          if (v < nvec) pre[m] = load_vec(v, w0 + kSignWords, nwords);
+        }
+      }
+    } else {
+      for (uint32_t v0 = threadIdx.x; v0 < nvec; v0 += kSignPre * kThreads) {
+        uint4 t[kSignPre];
+#pragma unroll
+        for (int m = 0; m < kSignPre; ++m)
+          if (v0 + m * kThreads < nvec) t[m] = load_vec(v0 + m * kThreads, w0, nwords);
+#pragma unroll
+        for (int m = 0; m < kSignPre; ++m)
+          if (v0 + m * kThreads < nvec) reinterpret_cast<uint4*>(sh_words)[v0 + m * kThreads] = t[m];
+      }
+    }
+    __syncthreads();
     const Divisor div(S.divisor);
     const bool ones = S.divisor == 1.0f;
-    const uint32_t e0 = (gu - S.unit0) * kSignUnit + threadIdx.x * 4;
+    const uint32_t lt = threadIdx.x * 4;   // unit-relative element of j = 0
+    const uint32_t e0 = w0 * 32 + lt;
     float4 acc[kJ];
 #pragma unroll
     for (int j = 0; j < kJ; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (S.npieces == 1) {
-      const uint32_t* w = sh_w[0];
-      uint32_t wd[kJ];
+    for (uint32_t r = 0; r < np; ++r) {
+      const float sp = sh_sp[r], sn = sh_sn[r];
+      const uint32_t* wr = sh_words + r * kSignWords;
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
-        const uint32_t e = e0 + j * kThreads * 4;
-        wd[j] = have_next ? wnext[j] : (e < n ? __ldg(w + (e >> 5)) : 0u);
-      }
-      // prefetch the next unit of the same segment
-      have_next = gu + 1 < u1 && sid_next == cur;
-      if (have_next) {
-#pragma unroll
-        for (int j = 0; j < kJ; ++j) {
-          const uint32_t e = e0 + kSignUnit + j * kThreads * 4;
-          wnext[j] = e < n ? __ldg(w + (e >> 5)) : 0u;
-        }
-      }
-      const float sp = sh_sp[0], sn = sh_sn[0];
-#pragma unroll
-      for (int j = 0; j < kJ; ++j) {
-        const uint32_t e = e0 + j * kThreads * 4;
-        const uint32_t nib = (wd[j] >> (e & 31)) & 0xFu;
-        acc[j].x = __fadd_rn(0.f, (nib & 1) ? sp : sn);
-        acc[j].y = __fadd_rn(0.f, (nib & 2) ? sp : sn);
-        acc[j].z = __fadd_rn(0.f, (nib & 4) ? sp : sn);
-        acc[j].w = __fadd_rn(0.f, (nib & 8) ? sp : sn);
-      }
-    } else {
-      for (uint32_t r = 0; r < S.npieces; ++r) {
-        const uint32_t* w = sh_w[r];
-        const float sp = sh_sp[r], sn = sh_sn[r];
-        uint32_t wd[kJ];
-#pragma unroll
-        for (int j = 0; j < kJ; ++j) {
-          const uint32_t e = e0 + j * kThreads * 4;
-          wd[j] = e < n ? __ldg(w + (e >> 5)) : 0u;
-        }
-#pragma unroll
-        for (int j = 0; j < kJ; ++j) {
-          const uint32_t e = e0 + j * kThreads * 4;
-          const uint32_t nib = (wd[j] >> (e & 31)) & 0xFu;
-          acc[j].x = __fadd_rn(acc[j].x, (nib & 1) ? sp : sn);
-          acc[j].y = __fadd_rn(acc[j].y, (nib & 2) ? sp : sn);
-          acc[j].z = __fadd_rn(acc[j].z, (nib & 4) ? sp : sn);
-          acc[j].w = __fadd_rn(acc[j].w, (nib & 8) ? sp : sn);
-        }
+        const uint32_t l = lt + j * kThreads * 4;
+        const uint32_t nib = (wr[l >> 5] >> (l & 31)) & 0xFu;
+        acc[j].x = __fadd_rn(acc[j].x, (nib & 1) ? sp : sn);
+        acc[j].y = __fadd_rn(acc[j].y, (nib & 2) ? sp : sn);
+        acc[j].z = __fadd_rn(acc[j].z, (nib & 4) ? sp : sn);
+        acc[j].w = __fadd_rn(acc[j].w, (nib & 8) ? sp : sn);
       }
     }
     float* out = seg_out(S);
@@ -383,18 +421,25 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
 }
 
 void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
-                    const unsigned char* const* pieces, cudaStream_t st) {
+                    const unsigned char* const* pieces, int max_pieces, cudaStream_t st) {
   if (nunits == 0) return;
-  static const int cap = [] {
-    int dev = 0, sms = 148, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sign_kernel<K_EFSIGN>, kThreads, 0);
-    return sms * (per_sm > 0 ? per_sm : 4);
+  const int smem = (max_pieces < 1 ? 1 : max_pieces) * kSignWords * 4;   // <= 64 KB (64 pieces)
+  static const bool attr = [] {
+    const int mx = kMaxPieces * kSignWords * 4;
+    return cudaFuncSetAttribute(h2_sign_kernel<K_EFSIGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(h2_sign_kernel<K_ONEBIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) ==
+               cudaSuccess;
   }();
+  (void)attr;
+  int dev = 0, sms = 148, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sign_kernel<K_EFSIGN>, kThreads, smem);
+  const int cap = sms * (per_sm > 0 ? per_sm : 4);
   const int grid = nunits < cap ? nunits : cap;
-  if (kind == K_EFSIGN) h2_sign_kernel<K_EFSIGN><<<grid, kThreads, 0, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
-  else h2_sign_kernel<K_ONEBIT><<<grid, kThreads, 0, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
+  if (kind == K_EFSIGN) h2_sign_kernel<K_EFSIGN><<<grid, kThreads, smem, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
+  else h2_sign_kernel<K_ONEBIT><<<grid, kThreads, smem, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
   count_launches(1);
 }
 

@@ -103,34 +103,79 @@ struct RandomkOp {
 
 // ------------------------------------------------------------------ h2
 // out = reduce(sum over pieces of the scattered values); each piece carries
-// its own hash (identical for all pieces when indices are shared).
+// its own hash (identical for all pieces when indices are shared).  Strata are
+// disjoint ranges, so every output position can only be picked by ONE stratum
+// (whatever the piece): one thread per stratum owns its positions and sums the
+// pieces' values there in rank order from +0 -- no barrier between pieces.
+// The stratum bounds are computed once, the pick once when every piece shares
+// the indices (else one per piece, independent, so they overlap), and all of
+// a batch's value loads are in flight before the first is added.
+constexpr int kRkBatch = 8;
 __global__ void __launch_bounds__(kThreads) h2_randomk_kernel(const SegH2* __restrict__ segs,
                                                               const uint32_t* __restrict__ unit_seg,
                                                               const unsigned char* const* __restrict__ pieces,
                                                               const uint32_t* __restrict__ rankterms) {
   __shared__ __align__(16) float acc[kUnit];
   __shared__ uint64_t sh_h[64];
+  __shared__ const float* sh_v[64];
+  __shared__ int sh_shared;
   const uint32_t sid = unit_seg[blockIdx.x];
   const SegH2 S = segs[sid];
   const uint32_t u = blockIdx.x - S.unit0;
-  const uint32_t n = S.n, k = S.k;
+  const uint32_t n = S.n, k = S.k, np = S.npieces;
   const uint32_t lo = u * kUnit, hi = min(lo + (uint32_t)kUnit, n) - 1;
   const uint64_t step = *S.step;
-  for (uint32_t r = threadIdx.x; r < S.npieces; r += kThreads)
+  for (uint32_t r = threadIdx.x; r < np; r += kThreads) {
     sh_h[r] = randomk_hash(S.hash, step, S.part, rankterms[S.piece0 + r]);
+    sh_v[r] = reinterpret_cast<const float*>(pieces[S.piece0 + r]);
+  }
   for (int i = threadIdx.x; i < kUnit / 4; i += kThreads)
     reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncthreads();
-  const uint64_t j0 = stratum_of(lo, k, n), j1 = stratum_of(hi, k, n);
-  for (uint32_t r = 0; r < S.npieces; ++r) {
-    const float* val = reinterpret_cast<const float*>(pieces[S.piece0 + r]);
-    const uint64_t h = sh_h[r];
-    for (uint64_t jj = j0 + threadIdx.x; jj <= j1; jj += kThreads) {
-      const uint32_t p = randomk_pick(h, jj, k, n);
-      if (p >= lo && p <= hi) acc[p - lo] = __fadd_rn(acc[p - lo], __ldg(val + jj));
-    }
-    __syncthreads();
+  if (threadIdx.x == 0) {
+    int same = 1;
+    for (uint32_t r = 1; r < np; ++r) same &= sh_h[r] == sh_h[0];
+    sh_shared = same;
   }
+  __syncthreads();
+  const bool shared = sh_shared != 0;
+  const uint64_t j0 = stratum_of(lo, k, n), j1 = stratum_of(hi, k, n);
+  for (uint64_t jj = j0 + threadIdx.x; jj <= j1; jj += kThreads) {
+    const uint64_t a = jj * n / k, len = (jj + 1) * n / k - a;
+    uint32_t p0 = (uint32_t)(a + splitmix64(sh_h[0] ^ jj) % len);
+    float sum = 0.f;
+    bool any = false;
+    uint32_t pos = 0;
+    for (uint32_t r0 = 0; r0 < np; r0 += kRkBatch) {
+      uint32_t p[kRkBatch];
+      float v[kRkBatch];
+#pragma unroll
+      for (int m = 0; m < kRkBatch; ++m) {
+        const uint32_t r = r0 + m;
+        p[m] = (r < np) ? (shared || r == 0 ? p0 : (uint32_t)(a + splitmix64(sh_h[r] ^ jj) % len)) : 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int m = 0; m < kRkBatch; ++m) {
+        const uint32_t r = r0 + m;
+        v[m] = (r < np && p[m] >= lo && p[m] <= hi) ? __ldg(sh_v[r] + jj) : 0.f;
+      }
+#pragma unroll
+      for (int m = 0; m < kRkBatch; ++m) {
+        const uint32_t r = r0 + m;
+        if (r < np && p[m] >= lo && p[m] <= hi) {
+          if (shared) {
+            sum = __fadd_rn(sum, v[m]);
+            any = true;
+            pos = p[m] - lo;
+          } else {
+            acc[p[m] - lo] = __fadd_rn(acc[p[m] - lo], v[m]);   // this thread owns the stratum's positions
+          }
+        }
+      }
+    }
+    if (shared && any) acc[pos] = sum;
+  }
+  __syncthreads();
   const Divisor div(S.divisor);
   const bool ones = S.divisor == 1.0f;
   for (uint32_t i = threadIdx.x * 4; lo + i <= hi; i += kThreads * 4) {

@@ -936,14 +936,21 @@ void trim_plans(esp_world_s* w) {
   }
 }
 
-Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
-  for (size_t i = 0; i < w->plans.size(); ++i)
+Plan* find_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
+  for (size_t i = w->plans.size(); i-- > 0;)   // most recently used first
     if (w->plans[i]->ctxs == ctxs) {
       Plan* up = w->plans[i];
-      w->plans.erase(w->plans.begin() + i);
-      w->plans.push_back(up);
+      if (i + 1 != w->plans.size()) {
+        w->plans.erase(w->plans.begin() + i);
+        w->plans.push_back(up);
+      }
       return up;
     }
+  return nullptr;
+}
+
+Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
+  if (Plan* up = find_plan(w, ctxs)) return up;
   auto p = std::make_unique<Plan>();
   p->w = w;
   p->ctxs = ctxs;
@@ -1277,7 +1284,7 @@ static void run_h2(Plan& p, Bucket& b, cudaStream_t st) {
     case ESP_EFSIGNSGD:
     case ESP_ONEBIT:
       launch_h2_sign(b.kind == ESP_EFSIGNSGD ? K_EFSIGN : K_ONEBIT, b.h2, b.h2_units, b.nh2_units,
-                     (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, st);
+                     (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, b.h2_max_pieces, st);
       break;
     default: launch_h2_dense(b.h2, b.h2_units, b.nh2_units, b.h2_pieces, st); break;
   }

@@ -298,11 +298,19 @@ def test_abi_errors():
         assert st_ == 1
         w2 = E.World.sim(2, 0)
         try:
-            with pytest.raises(E.EspError) as ei:
-                E.esp_sync(w2, ctx, g)          # ctx of another world
-            assert ei.value.status == 7
+            st_ = E.lib().esp_sync(w2.h, ctx.h, ctypes.c_void_p(g.data_ptr()), None)   # ctx of another world
+            assert st_ == 7
         finally:
             w2.destroy()
+        # the binding rejects what the raw-pointer ABI cannot see
+        with pytest.raises(TypeError):
+            E.esp_sync(w, ctx, torch.zeros(200, device="cuda", dtype=torch.float16))
+        with pytest.raises(ValueError):
+            E.esp_sync(w, ctx, torch.zeros(199, device="cuda"))                  # nlocal * numel = 200
+        with pytest.raises(ValueError):
+            E.esp_sync(w, ctx, torch.zeros(400, device="cuda")[::2])             # not contiguous
+        with pytest.raises(ValueError):
+            E.esp_sync(w, ctx, torch.zeros(200))                                  # host memory
     finally:
         w.destroy()
 
