@@ -184,7 +184,7 @@ esp_status_t esp_world_set_probe(esp_world_t w, int enable);
 esp_status_t esp_world_set_timeout(esp_world_t w, double seconds);
 /* Execution plans (bucketing, device tables, buffers) are cached per tensor
  * list.  set_plan_cache bounds the cache (least recently used plans are freed;
- * default 16); drop_plans frees all of them (e.g. when a training framework
+ * default 64); drop_plans frees all of them (e.g. when a training framework
  * rebuilds its gradient buckets).  Every rank must make the same calls. */
 esp_status_t esp_world_set_plan_cache(esp_world_t w, int max_plans);
 esp_status_t esp_world_drop_plans(esp_world_t w);

@@ -2,6 +2,7 @@
 // (The CPU oracle under oracle/ shares none of this.)
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "esp_tables.h"
@@ -252,6 +253,45 @@ __device__ __forceinline__ bool last_cta(uint32_t* counter, uint32_t expected, i
   bool last = *sh_flag != 0;
   if (last) __threadfence();
   return last;
+}
+
+// ---- sign decode through a lookup table ------------------------------------------
+// With np <= 8 pieces an element's decoded rank-order sum depends only on its
+// np sign bits: lut[t] = (((+0 + x_0(t)) + x_1(t)) + ...) / divisor with
+// x_r(t) = bit r of t ? pos_r : neg_r -- the same fp32 operations in the same
+// order as the sequential decode, so bit-identical to it.  The np bits of 4
+// consecutive elements are gathered as 4 index bytes: spread4(nib) moves bit c
+// of a nibble to bit 8c (the partial products of nib * 0x204081 do not
+// overlap), shifted to bit r for piece r.
+constexpr int kSignLutPieces = 8;
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+// ---- programmatic dependent launch (PDL) ------------------------------------------
+// The kernels of a call form one chain on the caller's stream (sample ->
+// stream -> fallback -> refine -> write -> h2 ...).  Each is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization (launch_pdl), so its
+// CTAs are scheduled while its predecessor drains instead of after it:
+// pdl_trigger() lets the successor launch; pdl_wait() (griddepcontrol.wait)
+// blocks until every predecessor grid has completed and its memory is
+// visible.  EVERY kernel launched with launch_pdl calls pdl_wait() before it
+// touches memory a predecessor writes (static tables may be read before).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace esp

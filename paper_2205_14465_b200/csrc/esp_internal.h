@@ -88,6 +88,8 @@ struct esp_world_s {
   int nranks = 1, rank = 0, nlocal = 1, dev = 0;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  cudaStream_t fin_stream = nullptr;       // DGC finalize chains of a multi-bucket call (a9)       // CUDA-graph capture of a plan's call (non-blocking)
   cudaEvent_t ev_join = nullptr, ev_fork = nullptr;
   std::vector<esp_counters_t> counters;   // per local rank
   bool timing = false;
@@ -101,7 +103,7 @@ struct esp_world_s {
   size_t probe_used = 0;
   std::vector<uint64_t> probe_bytes;
   std::vector<esp::Plan*> plans;           // owned; freed by esp::clear_plans (LRU order, most recent last)
-  size_t plan_cap = 16;                    // cached plans kept per world (least recently used evicted)
+  size_t plan_cap = 64;                    // cached plans kept per world (least recently used evicted)
   // fused collectives: a wait kernel that saw no arrival within wait_timeout_ns
   // sets the mapped word *wait_err_host (device alias wait_err)
   unsigned int* wait_err_host = nullptr;

@@ -85,6 +85,8 @@ __device__ void select_bin(const uint32_t* hist, int nbins, uint32_t need, uint3
 // that every segment with k > 0 takes the fallback; bit 1 does the same to thr_lo
 __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __restrict__ segs, int force,
                                                              float margin) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   __shared__ uint32_t keys[kSample];
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t sh[280];
@@ -374,6 +376,10 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
   }
   for (int i = threadIdx.x; i < NCG * 2048; i += blockDim.x) sm.grp[i / 2048].hist[i % 2048] = 0;
   __syncthreads();
+  // the prologue above (barrier init, histogram zeroing) overlapped the
+  // predecessor's tail (PDL); everything below reads what it wrote
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == NCG * kThreads / 32) {
     // ---- producer warp: one elected lane streams tiles into the ring
@@ -659,6 +665,8 @@ __device__ void fallback_pass(const SegH1* __restrict__ segs, int nsegs, uint32_
 
 // Thin kernel over the fallback pass (every CTA scans the segment list).
 __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __restrict__ segs, int nsegs) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   fallback_pass(segs, nsegs, blockIdx.x, gridDim.x);
 }
 
@@ -671,7 +679,12 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
 // off[i] = first flat position of run i (lane l holds runs 2l and 2l+1).
 static_assert(kRunsPerGroup == 64, "two run counts per lane");
 constexpr int kBatch = 4;   // candidate loads in flight per lane
-constexpr uint32_t kDirect = 2048;   // refine: up to this many candidates, global atomics directly
+// refine: a group with up to this many candidates adds its matches to the
+// global round histogram directly; larger groups (1% ratios, TOPK, fallbacks)
+// count into a warp-private shared histogram flushed once, so that a round
+// with millions of matches (a 2^28-element tensor at 1%) costs one atomic per
+// (group, non-empty bin) instead of one per match on a few hot bins
+constexpr uint32_t kDirect = 64;
 constexpr int kWarpsPerCta = kThreads / 32;
 
 struct WarpGroup {
@@ -789,6 +802,8 @@ template <int ROUND>
 __global__ void __launch_bounds__(kThreads, 8) dgc_refine_kernel(const SegH1* __restrict__ segs,
                                                               const uint32_t* __restrict__ group_seg,
                                                               uint32_t ngroups) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   __shared__ uint32_t sh_off[kWarpsPerCta][kRunsPerGroup + 1];
   // 1024 16-bit bins per warp, two per word (a group has <= 64 x 512 candidates < 2^16)
   __shared__ uint32_t sh_hist[kWarpsPerCta][512];
@@ -880,6 +895,8 @@ __device__ __forceinline__ unsigned long long lb_pack(uint32_t flag, uint32_t ab
 __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __restrict__ segs,
                                                              const uint32_t* __restrict__ group_seg,
                                                              uint32_t ngroups) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t gi = blockIdx.x * kWarpsPerCta + w;
@@ -1045,6 +1062,12 @@ static void debug_sync(const char* what, cudaStream_t st) {
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
                    cudaEvent_t probe1, bool mom) {
+  launch_dgc_stream(segs, nsegs, unit_seg, nunits, st, probe0, probe1, mom);
+  launch_dgc_finalize(segs, nsegs, group_seg, ngroups, st);
+}
+
+void launch_dgc_stream(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits, cudaStream_t st,
+                       cudaEvent_t probe0, cudaEvent_t probe1, bool mom) {
   if (nsegs == 0) return;
   // three consumer groups of 8 warps over a 3-stage ring of 32 KB (plain EF);
   // two groups over 4 stages of 48 KB with the momentum stream (R20) -- the
@@ -1064,28 +1087,34 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
   // sample-rank margin in standard deviations of the sample count (4: 2 and 1
   // measured to send segments through the fallback recompaction)
   constexpr float kMargin = 4.0f;
-  dgc_sample_kernel<<<nsegs, kThreads, 0, st>>>(segs, ff ? atoi(ff) : 0, kMargin);
+  launch_pdl(dgc_sample_kernel, nsegs, kThreads, 0, st, segs, ff ? atoi(ff) : 0, kMargin);
   debug_sync("dgc_sample", st);
   if (probe0) cudaEventRecord(probe0, st);
   const int grid = nunits < g_num_sms ? nunits : g_num_sms;
   if (mom)
-    dgc_stream_kernel<2, true><<<grid, 2 * kThreads + 32, mom_smem, st>>>(segs, unit_seg, (uint32_t)nunits, kNsMom);
+    launch_pdl(dgc_stream_kernel<2, true>, grid, 2 * kThreads + 32, mom_smem, st, segs, unit_seg, (uint32_t)nunits, kNsMom);
   else
-    dgc_stream_kernel<3><<<grid, 3 * kThreads + 32, smem, st>>>(segs, unit_seg, (uint32_t)nunits, kNs);
+    launch_pdl(dgc_stream_kernel<3>, grid, 3 * kThreads + 32, smem, st, segs, unit_seg, (uint32_t)nunits, kNs);
   debug_sync("dgc_stream", st);
   if (probe1) cudaEventRecord(probe1, st);
-  dgc_fallback_kernel<<<g_num_sms, kThreads, 0, st>>>(segs, nsegs);
+  count_launches(2);
+}
+
+void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg, int ngroups, cudaStream_t st) {
+  if (nsegs == 0) return;
+  num_sms();
+  launch_pdl(dgc_fallback_kernel, g_num_sms, kThreads, 0, st, segs, nsegs);
   debug_sync("dgc_fallback", st);
   const int wgrid = (ngroups + kWarpsPerCta - 1) / kWarpsPerCta;   // one warp per finalize group
   if (wgrid > 0) {
-    dgc_refine_kernel<2><<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
+    launch_pdl(dgc_refine_kernel<2>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_refine<2>", st);
-    dgc_refine_kernel<3><<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
+    launch_pdl(dgc_refine_kernel<3>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_refine<3>", st);
-    dgc_write_kernel<<<wgrid, kThreads, 0, st>>>(segs, group_seg, (uint32_t)ngroups);
+    launch_pdl(dgc_write_kernel, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_write", st);
   }
-  count_launches(6);
+  count_launches(wgrid > 0 ? 4 : 1);
 }
 
 }  // namespace esp

@@ -23,6 +23,8 @@ constexpr int kMaxPieces = 64;
 __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2* __restrict__ segs,
                                                                      const uint4* __restrict__ jobs,
                                                                      const unsigned char* const* __restrict__ pieces) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   constexpr int kPer = kOffJob / kThreads;
   const uint4 job = jobs[blockIdx.x];
   const SegH2 S = segs[job.x];
@@ -71,6 +73,8 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
                                                                  const uint32_t* __restrict__ tile_seg,
                                                                  uint32_t ntiles,
                                                                  const unsigned char* const* __restrict__ pieces) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   constexpr int kWarps = kTileThreads / 32;
   constexpr unsigned kFull = 0xffffffffu;
   // the per-warp accumulation tiles (dynamic: absent when every segment of the
@@ -256,9 +260,12 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
                                                            const uint32_t* __restrict__ unit_seg,
                                                            uint32_t nunits,
                                                            const unsigned char* const* __restrict__ pieces) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   extern __shared__ __align__(16) uint32_t sh_words[];   // [npieces][kSignWords]
   __shared__ float sh_sp[kMaxPieces], sh_sn[kMaxPieces];
   __shared__ const uint32_t* sh_w[kMaxPieces];
+  __shared__ float sh_lut[1 << kSignLutPieces];   // np <= 8: decoded sum (÷ divisor) per bit pattern
   constexpr int kJ = kSignUnit / (kThreads * 4);
   const uint32_t u0 = (uint32_t)((uint64_t)blockIdx.x * nunits / gridDim.x);
   const uint32_t u1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nunits / gridDim.x);
@@ -288,6 +295,15 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
         sh_w[r] = reinterpret_cast<const uint32_t*>(h + 16);
       }
       __syncthreads();
+      if (S.npieces <= (uint32_t)kSignLutPieces) {
+        const Divisor dv(S.divisor);
+        for (uint32_t t = threadIdx.x; t < (1u << S.npieces); t += kThreads) {
+          float a = 0.f;
+          for (uint32_t r = 0; r < S.npieces; ++r) a = __fadd_rn(a, ((t >> r) & 1u) ? sh_sp[r] : sh_sn[r]);
+          sh_lut[t] = S.divisor == 1.0f ? a : dv(a);
+        }
+        __syncthreads();
+      }
       have = false;
     }
     const uint32_t n = S.n, np = S.npieces;
@@ -334,6 +350,22 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
     const bool ones = S.divisor == 1.0f;
     const uint32_t lt = threadIdx.x * 4;   // unit-relative element of j = 0
     const uint32_t e0 = w0 * 32 + lt;
+    float* out = seg_out(S);
+    if (np <= (uint32_t)kSignLutPieces) {
+      // 4 index bytes per float4: bit r of byte c = piece r's bit of element c
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const uint32_t l = lt + j * kThreads * 4;
+        const uint32_t wi = l >> 5, sh = l & 31;
+        uint32_t idx4 = 0;
+        for (uint32_t r = 0; r < np; ++r) idx4 |= spread4((sh_words[r * kSignWords + wi] >> sh) & 0xFu) << r;
+        const float4 v = make_float4(sh_lut[idx4 & 0xFFu], sh_lut[(idx4 >> 8) & 0xFFu], sh_lut[(idx4 >> 16) & 0xFFu],
+                                     sh_lut[idx4 >> 24]);
+        const uint32_t e = e0 + j * kThreads * 4;
+        if (e < n) store4_guard(out, e, n, v);
+      }
+      continue;
+    }
     float4 acc[kJ];
 #pragma unroll
     for (int j = 0; j < kJ; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -350,7 +382,6 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
         acc[j].w = __fadd_rn(acc[j].w, (nib & 8) ? sp : sn);
       }
     }
-    float* out = seg_out(S);
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
       const uint32_t e = e0 + j * kThreads * 4;
@@ -364,6 +395,8 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
 __global__ void __launch_bounds__(kThreads) h2_dense_kernel(const SegH2* __restrict__ segs,
                                                             const uint32_t* __restrict__ unit_seg,
                                                             const unsigned char* const* __restrict__ pieces) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   const uint32_t sid = unit_seg[blockIdx.x];
   const SegH2 S = segs[sid];
   const uint32_t u = blockIdx.x - S.unit0;
@@ -388,6 +421,8 @@ __global__ void __launch_bounds__(kThreads) h2_dense_kernel(const SegH2* __restr
 
 __global__ void __launch_bounds__(kThreads) pack_kernel(const SegH1* __restrict__ segs,
                                                         const uint32_t* __restrict__ unit_seg) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   const uint32_t sid = unit_seg[blockIdx.x];
   const SegH1 S = segs[sid];
   const uint32_t u = blockIdx.x - S.unit0;
@@ -402,7 +437,7 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const SegH1* __restrict_
 void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
                       const unsigned char* const* pieces, int max_pieces, cudaStream_t st) {
   if (ntiles == 0) return;
-  h2_sparse_offsets_kernel<<<njobs, kThreads, 0, st>>>(segs, jobs, pieces);
+  launch_pdl(h2_sparse_offsets_kernel, njobs, kThreads, 0, st, segs, jobs, pieces);
   constexpr int kSmem = kTileThreads / 32 * kTile * (int)sizeof(float);
   auto cap = [](int smem) {
     int dev = 0, sms = 148, per_sm = 0;
@@ -416,7 +451,7 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
   const int grid_cap = max_pieces > 1 ? capn : cap1;
   const int need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);   // one warp per tile
   const int grid = need < grid_cap ? need : grid_cap;
-  h2_sparse_kernel<<<grid, kTileThreads, smem, st>>>(segs, tile_seg, (uint32_t)ntiles, pieces);
+  launch_pdl(h2_sparse_kernel, grid, kTileThreads, smem, st, segs, tile_seg, (uint32_t)ntiles, pieces);
   count_launches(2);
 }
 
@@ -438,21 +473,21 @@ void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int n
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sign_kernel<K_EFSIGN>, kThreads, smem);
   const int cap = sms * (per_sm > 0 ? per_sm : 4);
   const int grid = nunits < cap ? nunits : cap;
-  if (kind == K_EFSIGN) h2_sign_kernel<K_EFSIGN><<<grid, kThreads, smem, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
-  else h2_sign_kernel<K_ONEBIT><<<grid, kThreads, smem, st>>>(segs, unit_seg, (uint32_t)nunits, pieces);
+  if (kind == K_EFSIGN) launch_pdl(h2_sign_kernel<K_EFSIGN>, grid, kThreads, smem, st, segs, unit_seg, (uint32_t)nunits, pieces);
+  else launch_pdl(h2_sign_kernel<K_ONEBIT>, grid, kThreads, smem, st, segs, unit_seg, (uint32_t)nunits, pieces);
   count_launches(1);
 }
 
 void launch_h2_dense(const SegH2* segs, const uint32_t* unit_seg, int nunits,
                      const unsigned char* const* pieces, cudaStream_t st) {
   if (nunits == 0) return;
-  h2_dense_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces);
+  launch_pdl(h2_dense_kernel, nunits, kThreads, 0, st, segs, unit_seg, pieces);
   count_launches(1);
 }
 
 void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st) {
   if (nunits == 0) return;
-  pack_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg);
+  launch_pdl(pack_kernel, nunits, kThreads, 0, st, segs, unit_seg);
   count_launches(1);
 }
 

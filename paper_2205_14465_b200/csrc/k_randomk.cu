@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(kThreads) h2_randomk_kernel(const SegH2* __res
                                                               const uint32_t* __restrict__ unit_seg,
                                                               const unsigned char* const* __restrict__ pieces,
                                                               const uint32_t* __restrict__ rankterms) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   __shared__ __align__(16) float acc[kUnit];
   __shared__ uint64_t sh_h[64];
   __shared__ const float* sh_v[64];
@@ -193,7 +195,7 @@ void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, 
 void launch_h2_randomk(const SegH2* segs, const uint32_t* unit_seg, int nunits,
                        const unsigned char* const* pieces, const uint32_t* rankterms, cudaStream_t st) {
   if (nunits == 0) return;
-  h2_randomk_kernel<<<nunits, kThreads, 0, st>>>(segs, unit_seg, pieces, rankterms);
+  launch_pdl(h2_randomk_kernel, nunits, kThreads, 0, st, segs, unit_seg, pieces, rankterms);
   count_launches(1);
 }
 

@@ -58,7 +58,7 @@ struct SignOp {
     const uint32_t* qw1;
   };
   template <int BAR>
-  __device__ void begin_segment(const SegH1& S, State& st, TmaGroup&) const {
+  __device__ void begin_segment(const SegH1& S, State& st, TmaGroup& gh) const {
     st.sp = st.sn = 0.f;
     if (S.ef) {
       const float a = __ldcg(S.lazy_in), b = __ldcg(S.lazy_in + 1);
@@ -79,18 +79,46 @@ struct SignOp {
         piece_scales<KIND>(p, &st.qsp1, &st.qsn1);
         st.qw1 = reinterpret_cast<const uint32_t*>(p + 16);
       }
+      if (S.npieces <= (uint32_t)kSignLutPieces) {
+        // the group's decode table (esp_device.cuh): entry t = decoded mean of
+        // bit pattern t, in the group's (otherwise unused) warp scratch
+        csync<BAR>();   // the previous segment's table is no longer read
+        float* lut = &gh.wscr[0][0];
+        const uint32_t t = ctid<BAR>();
+        float a = 0.f;
+        for (uint32_t r = 0; r < S.npieces; ++r) {
+          const float psp = __shfl_sync(0xffffffffu, st.qsp0, r);
+          const float psn = __shfl_sync(0xffffffffu, st.qsn0, r);
+          a = __fadd_rn(a, ((t >> r) & 1u) ? psp : psn);
+        }
+        if (t < (1u << S.npieces)) lut[t] = S.divisor == 1.0f ? a : Divisor(S.divisor)(a);
+        csync<BAR>();
+      }
     }
   }
   template <bool FULL>
   __device__ void run(const SegH1& S, const float4 (&gv)[kNJ], const float4 (&rv)[kNJ], uint32_t base,
-                      State& st, TmaGroup&, const uint32_t* sw) const {
+                      State& st, TmaGroup& gh, const uint32_t* sw) const {
     const uint32_t n = S.n;
     if (base >= n) return;   // warp-uniform
     const int lane = threadIdx.x & 31;
     float4 xv[kNJ];
 #pragma unroll
     for (int j = 0; j < kNJ; ++j) xv[j] = gv[j];
-    if (DECODE) {
+    if (DECODE && sw && S.npieces <= (uint32_t)kSignLutPieces) {
+      // staged words, few pieces: the decoded mean by table lookup (identical
+      // to the sequential rank-order sum + division below)
+      const float* lut = &gh.wscr[0][0];
+      const uint32_t lt = (base & (kDgcTile - 1)) + lane * 4;
+#pragma unroll
+      for (int j = 0; j < kNJ; ++j) {
+        const uint32_t l = lt + j * 128;
+        uint32_t idx4 = 0;
+        for (uint32_t q = 0; q < S.npieces; ++q)
+          idx4 |= spread4((sw[q * (kDgcTile / 32) + (l >> 5)] >> (l & 31)) & 0xFu) << q;
+        xv[j] = make_float4(lut[idx4 & 0xFFu], lut[(idx4 >> 8) & 0xFFu], lut[(idx4 >> 16) & 0xFFu], lut[idx4 >> 24]);
+      }
+    } else if (DECODE) {
       // rank-order fp32 sum of the decoded chunks from +0, then / divisor (R9);
       // the pieces' words come from the stage (TMA) or, unstaged, by LDG
 #pragma unroll
@@ -211,6 +239,8 @@ struct SignOp {
 constexpr uint32_t kFinRuns = 16384;
 template <int KIND>
 __global__ void __launch_bounds__(kThreads) sign_finalize_kernel(const SegH1* __restrict__ segs) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
   __shared__ double shd[8];
   __shared__ uint32_t shu[16];
   __shared__ int last;
@@ -317,8 +347,8 @@ void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* 
   if (probe1) cudaEventRecord(probe1, st);
   const uint32_t max_runs = (max_len + kRun - 1) / kRun;
   const dim3 fgrid((unsigned)nsegs, max_runs > kFinRuns ? (max_runs + kFinRuns - 1) / kFinRuns : 1u);
-  if (kind == K_EFSIGN) sign_finalize_kernel<K_EFSIGN><<<fgrid, kThreads, 0, st>>>(segs);
-  else sign_finalize_kernel<K_ONEBIT><<<fgrid, kThreads, 0, st>>>(segs);
+  if (kind == K_EFSIGN) launch_pdl(sign_finalize_kernel<K_EFSIGN>, fgrid, kThreads, 0, st, segs);
+  else launch_pdl(sign_finalize_kernel<K_ONEBIT>, fgrid, kThreads, 0, st, segs);
   count_launches(1);
 }
 

@@ -50,7 +50,7 @@ struct Bucket {
   uint4* h2_off_jobs = nullptr; int nh2_off_jobs = 0;
   int h2_max_pieces = 0;
   uint32_t h1_max_len = 0, a7_max_len = 0;   // longest h1 / a7 segment
-  cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr;
+  cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr, ev_stream = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
   // ---- compression fused with the collective over NVLink peer memory
@@ -93,8 +93,26 @@ struct Bucket {
   uint64_t epoch = 0;
 };
 
+// A CUDA graph of one call's device work (every launch, copy and memset after
+// the gradient-pointer upload), captured on the first call and replayed after:
+// one cudaGraphLaunch instead of a dozen API calls per call (the per-call
+// "constant overhead to launch GPU kernels").  Only plans whose work
+// never changes between calls are graphed (no fused collective: those use
+// call-parity buffers and targets); the host-side counters a call adds are
+// recorded at capture and re-added on every replay.
+struct GraphCache {
+  cudaGraphExec_t exec = nullptr;
+  int key = -1;                          // launch-time inputs baked into the graph (test hooks)
+  uint64_t launches = 0;                 // kernels per replay (esp_launch_count)
+  std::vector<esp_counters_t> delta;     // per local rank
+  ~GraphCache() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
 struct Plan {
   esp_world_s* w = nullptr;
+  GraphCache g_sync, g_compress;
   std::vector<esp_ctx_s*> ctxs;
   std::vector<Bucket> buckets;
   Arena arena;
@@ -118,6 +136,7 @@ struct Plan {
     for (auto& b : buckets) {
       if (b.ev_h1) cudaEventDestroy(b.ev_h1);
       if (b.ev_comm) cudaEventDestroy(b.ev_comm);
+      if (b.ev_stream) cudaEventDestroy(b.ev_stream);
       if (b.dsts) cudaFree(b.dsts);
       if (b.dsts2) cudaFree(b.dsts2);
       if (b.cnts) cudaFree(b.cnts);
@@ -991,6 +1010,7 @@ Plan* get_plan(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs) {
   for (auto& b : p->buckets) {
     ESP_CUDA(cudaEventCreateWithFlags(&b.ev_h1, cudaEventDisableTiming));
     ESP_CUDA(cudaEventCreateWithFlags(&b.ev_comm, cudaEventDisableTiming));
+    ESP_CUDA(cudaEventCreateWithFlags(&b.ev_stream, cudaEventDisableTiming));
   }
   ESP_CUDA(cudaMallocHost(&p->dyn_host,
                           sizeof(uint64_t) * 2 * std::max<size_t>(1, ctxs.size()) * Plan::kDynSlots));
@@ -1058,8 +1078,13 @@ static void probe_pair(esp_world_s* w, cudaEvent_t* e0, cudaEvent_t* e1, uint64_
 }
 
 // h1 of a bucket: the payload is written locally (send); in a fused bucket
-// push_kernel then moves it to the peers (run_comm)
-static void run_h1(Plan& p, Bucket& b, cudaStream_t st) {
+// push_kernel then moves it to the peers (run_comm).  `fin` (DGC, several
+// buckets): the finalize chain (latency-bound: radix select and ordered write
+// over the candidates) runs there after the streaming pass, so that it
+// overlaps the next bucket's HBM-bound streaming pass on `st` (a9).
+// Returns the stream on which the bucket's payload is complete.
+static cudaStream_t run_h1(Plan& p, Bucket& b, cudaStream_t st, cudaStream_t fin = nullptr) {
+  cudaStream_t done = st;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p.w->probe && b.nh1_units) probe_pair(p.w, &e0, &e1, b.h1_bytes);
   const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
@@ -1067,8 +1092,16 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st) {
   if (e0 && !dgc && !sign) ESP_CUDA(cudaEventRecord(e0, st));
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
-      launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1,
-                    b.momentum != 0.0);
+      if (fin) {
+        launch_dgc_stream(b.h1, b.nh1, b.h1_units, b.nh1_units, st, e0, e1, b.momentum != 0.0);
+        ESP_CUDA(cudaEventRecord(b.ev_stream, st));
+        ESP_CUDA(cudaStreamWaitEvent(fin, b.ev_stream, 0));
+        launch_dgc_finalize(b.h1, b.nh1, b.h1_groups, b.nh1_groups, fin);
+        done = fin;
+      } else {
+        launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1,
+                      b.momentum != 0.0);
+      }
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
     case ESP_EFSIGNSGD:
@@ -1082,6 +1115,7 @@ static void run_h1(Plan& p, Bucket& b, cudaStream_t st) {
   if (e1 && !dgc && !sign) ESP_CUDA(cudaEventRecord(e1, st));
   ESP_CUDA(cudaGetLastError());
   for (int lr = 0; lr < p.w->nlocal; ++lr) p.w->counters[lr].h1_calls += b.h1_calls * b.tens.size();
+  return done;
 }
 
 // ESP_DEBUG_SYNC=1: synchronize after each phase of the collective layer and
@@ -1301,6 +1335,90 @@ static cudaEvent_t tev(esp_world_s* w, size_t i) {
   return w->tev[i];
 }
 
+static bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("ESP_GRAPHS");   // ESP_GRAPHS=0: launch every kernel directly (debugging)
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static int graph_key() {
+  const char* ff = getenv("ESP_DGC_FORCE_FALLBACK");   // a test hook read at launch time
+  return ff ? atoi(ff) : 0;
+}
+
+// run `body(stream)` as a graph: replay the cached one, or capture it on the
+// world's capture stream (the caller's stream may be the legacy default
+// stream, which cannot be captured) and launch it on `st`
+template <class F>
+static void run_graphed(Plan& p, GraphCache& g, cudaStream_t st, F body) {
+  esp_world_s* w = p.w;
+  const int key = graph_key();
+  if (!g.exec || g.key != key) {
+    if (g.exec) ESP_CUDA(cudaGraphExecDestroy(g.exec));
+    g.exec = nullptr;
+    const std::vector<esp_counters_t> before = w->counters;
+    const uint64_t l0 = esp_launch_count();
+    ESP_CUDA(cudaStreamBeginCapture(w->cap_stream, cudaStreamCaptureModeRelaxed));
+    try {
+      body(w->cap_stream);
+    } catch (...) {
+      cudaGraph_t gr = nullptr;
+      cudaStreamEndCapture(w->cap_stream, &gr);
+      if (gr) cudaGraphDestroy(gr);
+      throw;
+    }
+    cudaGraph_t graph = nullptr;
+    ESP_CUDA(cudaStreamEndCapture(w->cap_stream, &graph));
+    const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    ESP_CUDA(e);
+    g.key = key;
+    g.launches = esp_launch_count() - l0;
+    g.delta.assign(w->counters.size(), esp_counters_t{});
+    for (size_t lr = 0; lr < w->counters.size(); ++lr) {
+      const esp_counters_t &a = before[lr], &b = w->counters[lr];
+      esp_counters_t& d = g.delta[lr];
+      for (int o = 0; o < ESP_NUM_OPS; ++o) {
+        d.calls[o] = b.calls[o] - a.calls[o];
+        d.sent[o] = b.sent[o] - a.sent[o];
+        d.recv[o] = b.recv[o] - a.recv[o];
+      }
+      d.h1_calls = b.h1_calls - a.h1_calls;
+      d.h2_pieces = b.h2_pieces - a.h2_pieces;
+      d.pushed = b.pushed - a.pushed;
+    }
+    ESP_CUDA(cudaGraphLaunch(g.exec, st));   // this call's work (the capture executed nothing)
+    return;
+  }
+  ESP_CUDA(cudaGraphLaunch(g.exec, st));
+  count_launches((int)g.launches);
+  for (size_t lr = 0; lr < w->counters.size(); ++lr) {
+    esp_counters_t& c = w->counters[lr];
+    const esp_counters_t& d = g.delta[lr];
+    for (int o = 0; o < ESP_NUM_OPS; ++o) {
+      c.calls[o] += d.calls[o];
+      c.sent[o] += d.sent[o];
+      c.recv[o] += d.recv[o];
+    }
+    c.h1_calls += d.h1_calls;
+    c.h2_pieces += d.h2_pieces;
+    c.pushed += d.pushed;
+  }
+}
+
+// a plan whose device work is identical on every call: no fused collective
+// (call parities) and no NCCL call (sim worlds and single-rank worlds only)
+static bool graphable(const Plan& p) {
+  const esp_world_s* w = p.w;
+  if (!graphs_enabled() || w->timing || w->probe || w->loopback) return false;
+  if (!w->sim && w->nranks > 1) return false;
+  return true;
+}
+
+static void enqueue_pipelined(Plan& p, cudaStream_t st);
+
 void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
   Plan& p = *pp;
   esp_world_s* w = p.w;
@@ -1310,6 +1428,14 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
   if (!p.peers_ready && std::any_of(p.buckets.begin(), p.buckets.end(), [](const Bucket& b) { return b.fused; }))
     open_peers(p, cs);
   upload_dyn(p, grads, st);
+  if (graphable(p)) {
+    run_graphed(p, p.g_sync, st, [&](cudaStream_t s) {
+      if (p.zero_bytes) ESP_CUDA(cudaMemsetAsync(p.zero, 0, p.zero_bytes, s));
+      enqueue_pipelined(p, s);
+    });
+    for (auto* c : p.ctxs) c->step += 1;
+    return;
+  }
   if (p.zero_bytes) ESP_CUDA(cudaMemsetAsync(p.zero, 0, p.zero_bytes, st));
   const bool timing = w->timing;
   if (timing) {
@@ -1350,29 +1476,35 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
     }
     w->last = t;
   } else {
-    // pipelined: h1(b+1) is issued before h2(b), so compression of the next
-    // bucket overlaps the collective of the previous one
-    ESP_CUDA(cudaEventRecord(w->ev_fork, st));
-    ESP_CUDA(cudaStreamWaitEvent(cs, w->ev_fork, 0));
-    const size_t nb = p.buckets.size();
-    for (size_t i = 0; i <= nb; ++i) {
-      if (i < nb) {
-        Bucket& b = p.buckets[i];
-        run_h1(p, b, st);
-        ESP_CUDA(cudaEventRecord(b.ev_h1, st));
-        ESP_CUDA(cudaStreamWaitEvent(cs, b.ev_h1, 0));
-        run_comm(p, b, cs, nullptr, nullptr);
-        ESP_CUDA(cudaEventRecord(b.ev_comm, cs));
-      }
-      if (i >= 1) {
-        Bucket& b = p.buckets[i - 1];
-        ESP_CUDA(cudaStreamWaitEvent(st, b.ev_comm, 0));
-        run_h2(p, b, st);
-        if (b.fused) ++b.epoch;
-      }
-    }
+    enqueue_pipelined(p, st);
   }
   for (auto* c : p.ctxs) c->step += 1;
+}
+
+// pipelined: h1(b+1) is issued before h2(b), so compression of the next
+// bucket overlaps the collective of the previous one
+static void enqueue_pipelined(Plan& p, cudaStream_t st) {
+  esp_world_s* w = p.w;
+  const cudaStream_t cs = w->comm_stream;
+  ESP_CUDA(cudaEventRecord(w->ev_fork, st));
+  ESP_CUDA(cudaStreamWaitEvent(cs, w->ev_fork, 0));
+  const size_t nb = p.buckets.size();
+  for (size_t i = 0; i <= nb; ++i) {
+    if (i < nb) {
+      Bucket& b = p.buckets[i];
+      const cudaStream_t done = run_h1(p, b, st, nb > 1 ? w->fin_stream : nullptr);
+      ESP_CUDA(cudaEventRecord(b.ev_h1, done));
+      ESP_CUDA(cudaStreamWaitEvent(cs, b.ev_h1, 0));
+      run_comm(p, b, cs, nullptr, nullptr);
+      ESP_CUDA(cudaEventRecord(b.ev_comm, cs));
+    }
+    if (i >= 1) {
+      Bucket& b = p.buckets[i - 1];
+      ESP_CUDA(cudaStreamWaitEvent(st, b.ev_comm, 0));
+      run_h2(p, b, st);
+      if (b.fused) ++b.epoch;
+    }
+  }
 }
 
 // Loopback: the n worlds of one process on one GPU act as ranks 0..n-1 of a
@@ -1423,9 +1555,13 @@ void execute_compress(Plan* pp, const float* grad, void* payload, cudaStream_t s
   esp_ctx_s* c = p.ctxs[0];
   float* g = const_cast<float*>(grad);
   upload_dyn(p, &g, st);
-  if (p.zero_bytes) ESP_CUDA(cudaMemsetAsync(p.zero, 0, p.zero_bytes, st));
   Bucket& b = p.buckets[0];
-  run_h1(p, b, st);
+  auto body = [&](cudaStream_t s) {
+    if (p.zero_bytes) ESP_CUDA(cudaMemsetAsync(p.zero, 0, p.zero_bytes, s));
+    run_h1(p, b, s);
+  };
+  if (graphable(p)) run_graphed(p, p.g_compress, st, body);
+  else body(st);
   for (int lr = 0; lr < p.w->nlocal; ++lr)
     ESP_CUDA(cudaMemcpyAsync((unsigned char*)payload + (size_t)lr * c->payload_bytes, b.send.at(lr),
                              c->payload_bytes, cudaMemcpyDeviceToDevice, st));

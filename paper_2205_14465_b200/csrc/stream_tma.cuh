@@ -62,6 +62,8 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1)
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();   // the prologue above overlapped the predecessor's tail (PDL)
+  pdl_trigger();
 
   if (warp == NCG * kThreads / 32) {
     if (lane == 0) {
@@ -226,8 +228,8 @@ static void launch_tma_op_n(const SegH1* segs, const uint32_t* unit_seg, int nun
   (void)init;
   int ns = tma_stream_stages();
   ns = ns < NCG ? NCG : (ns > kMaxNs ? kMaxNs : ns - ns % NCG);
-  tma_stream_kernel<Op, NCG><<<tma_stream_grid(nunits), NCG * kThreads + 32, kTmaHdrBytes + ns * kTmaStageBytes,
-                               st>>>(segs, unit_seg, (uint32_t)nunits, ns, op);
+  launch_pdl(tma_stream_kernel<Op, NCG>, tma_stream_grid(nunits), NCG * kThreads + 32,
+             kTmaHdrBytes + ns * kTmaStageBytes, st, segs, unit_seg, (uint32_t)nunits, ns, op);
   count_launches(1);
 }
 

@@ -250,6 +250,8 @@ static void world_common_init(esp_world_s* w) {
   // communication gets the higher priority so collectives are not starved by
   // the next bucket's compression kernels (SURVEY.md 7 hard part 7)
   ESP_CUDA(cudaStreamCreateWithPriority(&w->comm_stream, cudaStreamNonBlocking, hi));
+  ESP_CUDA(cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking));
+  ESP_CUDA(cudaStreamCreateWithPriority(&w->fin_stream, cudaStreamNonBlocking, hi));
   ESP_CUDA(cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming));
   ESP_CUDA(cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming));
   w->counters.assign(w->nlocal, esp_counters_t{});
@@ -326,6 +328,8 @@ esp_status_t esp_world_destroy(esp_world_t w) {
   cudaEventDestroy(w->ev_fork);
   if (w->wait_err_host) cudaFreeHost(w->wait_err_host);
   cudaStreamDestroy(w->comm_stream);
+  cudaStreamDestroy(w->cap_stream);
+  cudaStreamDestroy(w->fin_stream);
   delete w;
   ESP_API_END
 }
