@@ -110,6 +110,19 @@ typedef struct {
    * v[sel] <- 0, u[sel] <- 0.  0 = off (plain error feedback, R4).  Requires
    * error_feedback = 1 and kind DGC or TOPK, else ESP_ERR_INVALID_ARG. */
   double momentum;
+  /* DGC sampled threshold (the DGC algorithm cited at P:828, SURVEY.md 8f
+   * NEXT-2, reading R22).  The sample of a segment of N > 4096 elements is S
+   * strata of 8 consecutive elements at hashed offsets; dgc_sample_rate = 0
+   * gives S = 512 (4096 samples), else S = ceil(rate * N / 8) clipped to
+   * [1, 512].  dgc_approx = 0 (exact, the default): the threshold only
+   * accelerates and exactly the top-k is selected (R3).  dgc_approx = 1
+   * (approximate-count mode, DGC's own selection): every element whose key
+   * passes the threshold of the round(rho * s)-th largest sampled key is
+   * selected, the exact top-k of them if more than k pass; fewer than k entries
+   * are then sent and the rest of the chunk is padding.  DGC only, else
+   * ESP_ERR_INVALID_ARG (as is a rate outside [0, 1]). */
+  int32_t dgc_approx;
+  double dgc_sample_rate;
 } esp_compressor_cfg_t;
 
 typedef struct esp_world_s* esp_world_t;

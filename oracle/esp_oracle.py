@@ -62,6 +62,8 @@ class Cfg:
     reduce: str = "mean"          # R9
     process: int = 0              # Alltoall/Allgather, Gather/Broadcast: 1 or 2 (0: the table's choice, R19)
     momentum: float = 0.0         # DGC momentum correction factor m (R20); 0 = plain error feedback
+    approx: bool = False          # DGC approximate-count mode (R22): keep what passes the sampled threshold
+    sample_rate: float = 0.0      # DGC sampler size (R22): 0 = 4096 samples, else about rate * N (<= 4096)
 
 
 def process_of(cfg: Cfg) -> int:
@@ -184,6 +186,76 @@ def topk_select(acc: np.ndarray, k: int) -> np.ndarray:
 
 MASK64 = (1 << 64) - 1
 
+# --------------------------------------------------------------------------
+# DGC sampled threshold (reading R22; DGC is cited at P:828 and run at 1%,
+# P:1426).  Only the approximate-count mode's RESULT depends on it; the exact
+# mode uses it as an accelerator and the oracle does not compute it there.
+# --------------------------------------------------------------------------
+DGC_SAMPLE = 4096          # samples per segment: 512 strata x 8 consecutive elements
+DGC_MARGIN = 4.0           # exact mode: j* = ceil(rho s + 4 sqrt(rho s)) (over-sampled)
+
+
+def dgc_segment_hash(tensor_id: int, part: int, recompress: bool = False) -> int:
+    """Per-segment sampler key (R22): splitmix64(tensor * 0x100000001b3 + part)
+    for the first compression, + 0x9e37 for the mid-scheme recompression."""
+    return splitmix64((tensor_id * 0x100000001B3 + (0x9E37 if recompress else 0) + part) & MASK64)
+
+
+def dgc_strata(n: int, sample_rate: float) -> int:
+    """R22: strata of 8 samples each: 512 by default (4096 samples), else
+    ceil(rate * n / 8) clipped to [1, 512]."""
+    if sample_rate <= 0.0:
+        return DGC_SAMPLE // 8
+    return max(1, min(DGC_SAMPLE // 8, math.ceil(sample_rate * n / 8)))
+
+
+def dgc_sample_positions(n: int, seg_hash: int, strata: int = DGC_SAMPLE // 8) -> np.ndarray:
+    """R22: for n > 4096, stratum G = [floor(G n / S), floor((G+1) n / S))
+    (G < S strata) contributes the 8 consecutive elements starting at
+    a_G + floor(u32(splitmix64(hash ^ G)) * (b_G - a_G - 7) / 2^32); for
+    n <= 4096 the sample is the whole segment."""
+    if n <= DGC_SAMPLE:
+        return np.arange(n, dtype=np.int64)
+    j = np.arange(8 * strata, dtype=np.uint64)
+    G = j >> np.uint64(3)
+    a = (G * np.uint64(n)) // np.uint64(strata)
+    b = ((G + np.uint64(1)) * np.uint64(n)) // np.uint64(strata)
+    h = splitmix64(np.uint64(seg_hash) ^ G) & np.uint64(0xFFFFFFFF)
+    off = (h * (b - a - np.uint64(7))) >> np.uint64(32)
+    return (a + off + (j & np.uint64(7))).astype(np.int64)
+
+
+def dgc_threshold(acc: np.ndarray, k: int, ratio: float, seg_hash: int, approx: bool,
+                  sample_rate: float = 0.0) -> int:
+    """R22: the key threshold of the sampled-threshold selection: the need-th
+    largest sampled key with its low 10 bits cleared (the 21-bit radix prefix
+    the GPU selects in two histogram rounds).  need = k when the sample is the
+    whole segment; else ceil(rho s + 4 sqrt(rho s)) (exact mode: enough that
+    >= k pass w.h.p.) or max(1, round(rho s)) (approximate-count mode: about
+    k pass in expectation); clipped to [1, s]."""
+    n = acc.size
+    pos = dgc_sample_positions(n, seg_hash, dgc_strata(n, sample_rate))
+    sk = np.sort(key(acc)[pos])[::-1]
+    s = sk.size
+    if n <= DGC_SAMPLE:
+        need = k
+    else:
+        rs = ratio * s
+        need = int(math.floor(rs + 0.5)) if approx else int(math.ceil(rs + DGC_MARGIN * math.sqrt(rs)))
+        need = max(1, min(s, need))
+    return int(sk[need - 1]) & ~0x3FF
+
+
+def dgc_approx_select(acc: np.ndarray, k: int, thr: int) -> np.ndarray:
+    """Approximate-count DGC (R22, DGC's own selection): every element whose
+    key passes the sampled threshold; when more than k pass, exactly the top-k
+    of them (DGC's hierarchical re-selection) -- which is the segment's top-k.
+    Emitted sorted by index."""
+    passing = np.nonzero(key(acc) >= np.uint32(thr))[0]
+    if passing.size <= k:
+        return passing.astype(np.uint32)
+    return topk_select(acc, k)
+
 
 def splitmix64(z):
     """splitmix64 finaliser (Steele et al.), on Python ints or uint64 arrays."""
@@ -263,12 +335,18 @@ class Chunk:
     mpos: np.float32 | None = None
 
 
-def compress_segment(cfg: Cfg, acc: np.ndarray, *, tensor_id=0, step=0, part=0, rank=0):
+def compress_segment(cfg: Cfg, acc: np.ndarray, *, tensor_id=0, step=0, part=0, rank=0, recompress=False):
     """h1 on one segment.  Returns (chunk, transmitted) where `transmitted` is the
     dense fp32 vector the chunk decodes to (so that r_new = acc - transmitted for
     EF, G5 / P:1427: e <- (g+e) - C(g+e))."""
     n = acc.size
-    if cfg.kind in ("dgc", "topk"):
+    if cfg.kind == "dgc" and cfg.approx:
+        k = k_of(n, cfg.ratio)
+        thr = (dgc_threshold(acc, k, cfg.ratio, dgc_segment_hash(tensor_id, part, recompress), True,
+                             cfg.sample_rate) if n else 0)
+        idx = dgc_approx_select(acc, k, thr)
+        ch = Chunk(cfg.kind, n, idx=idx, val=acc[idx].copy())
+    elif cfg.kind in ("dgc", "topk"):
         k = k_of(n, cfg.ratio)
         idx = topk_select(acc, k)
         ch = Chunk(cfg.kind, n, idx=idx, val=acc[idx].copy())
@@ -493,7 +571,7 @@ def sync(routine: str, cfg: Cfg, grads, states, tensor_id: int = 0) -> SyncResul
             cnt[j].h2 += n
             st = states[j]
             q = (A + st.r2).astype(np.float32) if cfg.error_feedback else A
-            ch, t = compress_segment(cfg, q, tensor_id=tensor_id, step=st.step, part=j, rank=j)
+            ch, t = compress_segment(cfg, q, tensor_id=tensor_id, step=st.step, part=j, rank=j, recompress=True)
             if cfg.error_feedback:
                 st.r2 = residual_update(q, t)
             cnt[j].h1 += 1
@@ -530,7 +608,7 @@ def sync(routine: str, cfg: Cfg, grads, states, tensor_id: int = 0) -> SyncResul
         cnt[0].h2 += n
         st = states[0]
         q = (A + st.r2).astype(np.float32) if cfg.error_feedback else A
-        ch, t = compress_segment(cfg, q, tensor_id=tensor_id, step=st.step, part=0, rank=0)
+        ch, t = compress_segment(cfg, q, tensor_id=tensor_id, step=st.step, part=0, rank=0, recompress=True)
         if cfg.error_feedback:
             st.r2 = residual_update(q, t)
         cnt[0].h1 += 1

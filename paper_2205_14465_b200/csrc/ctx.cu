@@ -28,6 +28,11 @@ void check_cfg(const esp_compressor_cfg_t* cfg) {
                 "momentum correction needs DGC/TOPK with error feedback (R20)");
   if (is_sparse(cfg->kind))
     ESP_REQUIRE(cfg->ratio > 0.0 && cfg->ratio <= 1.0, ESP_ERR_INVALID_ARG, "ratio must be in (0, 1]");
+  ESP_REQUIRE(cfg->dgc_approx == 0 || cfg->dgc_approx == 1, ESP_ERR_INVALID_ARG, "dgc_approx must be 0 or 1");
+  ESP_REQUIRE(!cfg->dgc_approx || cfg->kind == ESP_DGC, ESP_ERR_INVALID_ARG,
+              "the approximate-count mode is DGC's (R22)");
+  ESP_REQUIRE(cfg->dgc_sample_rate >= 0.0 && cfg->dgc_sample_rate <= 1.0, ESP_ERR_INVALID_ARG,
+              "dgc_sample_rate must be in [0, 1]");
 }
 
 void check_ptr16(const void* p, const char* what) {

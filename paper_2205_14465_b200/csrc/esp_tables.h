@@ -83,7 +83,10 @@ struct SegH1 {
   // DGC momentum correction (R20): u buffer of the segment (nullptr = off), factor m
   float* mom;
   float mcoef;
-  uint32_t pad1_;
+  // DGC sampled threshold (R22): strata of 8 samples (512 = 4096 samples) and
+  // the approximate-count mode (keep what passes the threshold, at most k)
+  uint16_t strata;
+  uint16_t approx;
 };
 
 // DGC histogram words of a segment: 2048 (stream) + 2048 (fallback) + 1024 x hrep

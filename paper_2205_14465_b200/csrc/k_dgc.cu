@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
   const uint32_t n = S.n;
   const float* g = seg_g(S);
   const bool exact = n <= (uint32_t)kSample;
-  const uint32_t s = exact ? n : (uint32_t)kSample;
+  const uint32_t strata = S.strata;                     // R22: strata of 8 samples
+  const uint32_t s = exact ? n : 8u * strata;
   {
     // all 2 x 16 loads of a thread are issued before any is consumed (latency-bound kernel)
     constexpr int kPer = kSample / kThreads;
@@ -108,13 +109,13 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
       const uint32_t j = threadIdx.x + q * kThreads;
       uint32_t pos = j;
       if (!exact && j < s) {
-        // 512 strata [GN/512, (G+1)N/512) (shifts, no division), 8 consecutive
-        // samples from each at a hashed offset: a random 4-byte gather costs a
-        // whole DRAM sector, a run of 8 costs one or two (a sampler only; the
-        // selection stays exact whatever threshold it yields)
+        // strata [GN/S, (G+1)N/S), 8 consecutive samples from each at a hashed
+        // offset: a random 4-byte gather costs a whole DRAM sector, a run of 8
+        // costs one or two (exact mode: a sampler only, the selection stays
+        // exact whatever threshold it yields; approximate mode: R22)
         static_assert(kSample == 4096, "512 strata x 8 assumes kSample == 2^12");
         const uint32_t G = j >> 3;
-        const uint32_t a = (uint32_t)(((uint64_t)G * n) >> 9), b = (uint32_t)(((uint64_t)(G + 1) * n) >> 9);
+        const uint32_t a = (uint32_t)(((uint64_t)G * n) / strata), b = (uint32_t)(((uint64_t)(G + 1) * n) / strata);
         pos = a + (uint32_t)(((uint64_t)(uint32_t)splitmix64(S.hash ^ G) * (b - a - 7)) >> 32) + (j & 7u);
       }
       gv[q] = j < s ? __ldg(g + pos) : 0.f;
@@ -140,7 +141,9 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
     need = S.k;
   } else {
     const double rs = S.ratio * (double)s;
-    const double js = ceil(rs + (double)margin * sqrt(rs));
+    // exact mode: over-sampled rank (>= k pass w.h.p.); approximate mode: the
+    // expected rank of the k-th key (R22)
+    const double js = S.approx ? floor(rs + 0.5) : ceil(rs + (double)margin * sqrt(rs));
     need = js >= (double)s ? s : (uint32_t)js;
     if (need < 1) need = 1;
   }
@@ -286,18 +289,20 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& s
         S.st->fallback = 1;
         atomicAdd(S.bflag, 1u);
       }
-    } else if (total < S.k) {
+    } else if (total < S.k && !S.approx) {
       if (tid == 0) {
         S.st->fallback = 1;
         atomicAdd(S.bflag, 1u);
       }
     } else {
+      // approximate mode with fewer than k candidates: all of them (R22)
+      const uint32_t keff = min(total, S.k);
       uint32_t bin, above;
-      select_bin<BAR, false>(sm.hist, 2048, S.k, &bin, &above, sm.scan);
+      select_bin<BAR, false>(sm.hist, 2048, keff, &bin, &above, sm.scan);
       if (tid == 0) {
         S.st->prefix = bin;
         S.st->above = above;
-        S.st->need = S.k - above;
+        S.st->need = keff - above;
       }
     }
     csync<BAR>();
@@ -334,7 +339,7 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& s
     }
     return;
   }
-  if (total < S.k) {
+  if (total < S.k && !S.approx) {
     if (tid == 0) {
       S.st->fallback = 1;
       atomicAdd(S.bflag, 1u);
@@ -342,12 +347,13 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& s
     csync<BAR>();
     return;
   }
+  const uint32_t keff = min(total, S.k);   // approximate mode: all candidates if fewer than k (R22)
   uint32_t bin, above;
-  select_bin<BAR, true>(S.hist, 2048, S.k, &bin, &above, sm.scan);
+  select_bin<BAR, true>(S.hist, 2048, keff, &bin, &above, sm.scan);
   if (tid == 0) {
     S.st->prefix = bin;
     S.st->above = above;
-    S.st->need = S.k - above;
+    S.st->need = keff - above;
   }
 }
 
@@ -987,6 +993,15 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __r
       }
       tie_run += __popc(tb);
       sel_run += __popc(sb);
+    }
+    // approximate-count mode (R22): fewer than k entries may have been sent;
+    // the segment's last group pads the rest of [0, k) (the chunk is reused)
+    if (S.approx && g == S.ngroups - 1) {
+      const uint32_t total = __ldcg(&S.st->above) + need;
+      for (uint32_t q = total + lane; q < S.k; q += 32) {
+        out_idx[q] = 0xFFFFFFFFu;
+        out_val[q] = 0.0f;
+      }
     }
   }
 }

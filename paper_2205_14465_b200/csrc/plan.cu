@@ -187,6 +187,14 @@ static void add_push(std::vector<PushJob>& v, size_t src_off, size_t dst_off, si
     v.push_back(PushJob{src_off + c, dst_off + c, (uint32_t)std::min<size_t>(kPushChunk, bytes - c), (uint32_t)d});
 }
 
+// DGC sampler strata of a segment (reading R22): 512 (4096 samples) by
+// default, else ceil(rate * n / 8) clipped to [1, 512]
+static uint16_t dgc_strata(uint64_t n, double rate) {
+  if (rate <= 0.0) return (uint16_t)(kSample / 8);
+  const double c = std::ceil(rate * (double)n / 8.0);
+  return (uint16_t)(c < 1.0 ? 1.0 : (c > kSample / 8 ? kSample / 8 : c));
+}
+
 static void fill_unit_table(std::vector<uint32_t>& units, uint32_t seg, uint32_t count) {
   for (uint32_t i = 0; i < count; ++i) units.push_back(seg);
 }
@@ -420,6 +428,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.part = (uint32_t)part;
         s.rankterm = (b.kind == ESP_RANDOMK && !c->cfg.randomk_shared_indices) ? grank(w, lr) + 1 : 0;
         s.ratio = c->cfg.ratio;
+        s.strata = dgc_strata(len, c->cfg.dgc_sample_rate);
+        s.approx = c->cfg.dgc_approx ? 1 : 0;
         s.mom = c->u ? c->u + (size_t)lr * c->N + lo : nullptr;
         s.mcoef = (float)c->cfg.momentum;
         // per-segment state (zeroed every call)
@@ -587,6 +597,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
                                          : host_splitmix64(c->tensor_id * 0x100000001b3ull + 0x9e37u + d.part);
           s.rankterm = (b.kind == ESP_RANDOMK && !c->cfg.randomk_shared_indices) ? (uint32_t)j + 1 : 0;
           s.ratio = c->cfg.ratio;
+          s.strata = dgc_strata(len, c->cfg.dgc_sample_rate);
+          s.approx = c->cfg.dgc_approx ? 1 : 0;
           if (dgc) {
             s.cand = L.ptr<uint2>(L.reserve((size_t)nruns * kRun * sizeof(uint2)));
             s.runcnt = L.ptr<uint32_t>(L.reserve((size_t)nruns * 4));

@@ -39,7 +39,8 @@ SYMBOLS = (
 class CompressorCfg(C.Structure):
     _fields_ = [("kind", C.c_int32), ("error_feedback", C.c_int32), ("ratio", C.c_double),
                 ("seed", C.c_uint64), ("randomk_shared_indices", C.c_int32), ("reduce", C.c_int32),
-                ("process", C.c_int32), ("momentum", C.c_double)]
+                ("process", C.c_int32), ("momentum", C.c_double), ("dgc_approx", C.c_int32),
+                ("dgc_sample_rate", C.c_double)]
 
 
 class Curve(C.Structure):
@@ -127,9 +128,10 @@ def _check(status):
 
 
 def cfg_of(kind="dgc", ratio=0.01, error_feedback=True, seed=0, shared_indices=True, reduce="mean", process=0,
-           momentum=0.0):
+           momentum=0.0, approx=False, sample_rate=0.0):
     return CompressorCfg(KINDS[kind], int(bool(error_feedback)), float(ratio), int(seed),
-                         int(bool(shared_indices)), REDUCE[reduce], int(process), float(momentum))
+                         int(bool(shared_indices)), REDUCE[reduce], int(process), float(momentum),
+                         int(bool(approx)), float(sample_rate))
 
 
 def _ptr(t):
@@ -300,10 +302,12 @@ class Ctx:
     """esp_ctx_t: one tensor's (compressor, ratio, routine) option and EF state."""
 
     def __init__(self, world: World, kind="dgc", routine="allgather", numel=1, tensor_id=0, ratio=0.01,
-                 error_feedback=True, seed=0, shared_indices=True, reduce="mean", process=0, momentum=0.0):
+                 error_feedback=True, seed=0, shared_indices=True, reduce="mean", process=0, momentum=0.0,
+                 approx=False, sample_rate=0.0):
         self.world = world
         self.kind, self.routine, self.numel = kind, routine, numel
-        self.cfg = cfg_of(kind, ratio, error_feedback, seed, shared_indices, reduce, process, momentum)
+        self.cfg = cfg_of(kind, ratio, error_feedback, seed, shared_indices, reduce, process, momentum, approx,
+                          sample_rate)
         self.h = C.c_void_p()
         _check(lib().esp_ctx_create(world.h, C.byref(self.cfg), ROUTINES[routine], tensor_id, numel,
                                     C.byref(self.h)))

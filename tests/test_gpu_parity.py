@@ -42,7 +42,8 @@ def check_out(kind, got, ref, where):
 
 
 def run_sim(kind, routine, n, N, steps=3, ratio=0.01, dist="D1", mode="mixed", ef=True,
-            reduce="mean", shared=True, lockstep=None, tensor_id=3, seed=11, process=0):
+            reduce="mean", shared=True, lockstep=None, tensor_id=3, seed=11, process=0, approx=False,
+            sample_rate=0.0):
     """Run `steps` syncs in a sim world and compare every rank's output and
     residual with the oracle after each step."""
     E = esp()
@@ -50,8 +51,8 @@ def run_sim(kind, routine, n, N, steps=3, ratio=0.01, dist="D1", mode="mixed", e
         lockstep = kind in O.QUANTIZED
     w = E.World.sim(n, 0)
     ctx = E.Ctx(w, kind, routine, N, tensor_id=tensor_id, ratio=ratio, error_feedback=ef, seed=seed,
-                shared_indices=shared, reduce=reduce, process=process)
-    cfg = O.Cfg(kind, ratio, ef, seed, shared, reduce, process)
+                shared_indices=shared, reduce=reduce, process=process, approx=approx, sample_rate=sample_rate)
+    cfg = O.Cfg(kind, ratio, ef, seed, shared, reduce, process, approx=approx, sample_rate=sample_rate)
     st = O.new_states(n, N, routine, cfg)
     try:
         for s in range(steps):
@@ -152,6 +153,24 @@ def test_sign_segments_beyond_one_finalize_chunk(kind, routine, process):
     large tensors run.  N = 2^24 + 2^20 + 77: whole-tensor segments of 17.8 M
     elements, Alltoall partitions of 8.9 M (n = 2)."""
     run_sim(kind, routine, 2, (1 << 24) + (1 << 20) + 77, steps=2, process=process)
+
+
+# ---------------------------------------------- DGC approximate-count mode (R22, NEXT-2)
+@pytest.mark.parametrize("N,ratio,rate", [(1000, 0.01, 0.0), (50_001, 0.01, 0.0), (1 << 20, 0.01, 0.0),
+                                          (1 << 20, 0.001, 0.0), (300_007, 0.01, 0.005), (2_000_003, 0.001, 0.0005)])
+@pytest.mark.parametrize("routine,process", [("allgather", 0), ("alltoall_allgather", 1),
+                                             ("alltoall_allgather", 2), ("gather_broadcast", 2)])
+def test_dgc_approx_mode(N, ratio, rate, routine, process):
+    """The sampled threshold decides the result here, so the GPU sampler (hashed
+    strata, the round(rho s)-th sampled key's 21-bit prefix) must match the
+    oracle's bit for bit; fewer than k entries are padded.  Bit-exact outputs
+    and residuals over 3 steps (EF carried)."""
+    run_sim("dgc", routine, 2, N, steps=3, ratio=ratio, process=process, approx=True, sample_rate=rate)
+
+
+def test_dgc_approx_more_ranks_and_exact_rate():
+    run_sim("dgc", "allgather", 8, 200_003, steps=3, ratio=0.01, approx=True)
+    run_sim("dgc", "alltoall_allgather", 4, 200_003, steps=2, ratio=0.01, sample_rate=0.003)   # exact, other sampler
 
 
 def test_randomk_unshared_and_sum():

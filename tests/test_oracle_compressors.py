@@ -282,3 +282,96 @@ def test_momentum_ef_identity_and_masking():
         sel[O.topk_select(acc, O.k_of(N, 0.01)).astype(np.int64)] = True
         assert np.all(st[0].u[sel] == 0)
         assert np.array_equal(st[0].u[~sel].view(np.uint32), u_pred[~sel].view(np.uint32))
+
+
+# ---------------------------------------------------------------- approximate-count DGC (R22)
+def _py_splitmix(z):
+    z = (z + 0x9E3779B97F4A7C15) % 2 ** 64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) % 2 ** 64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) % 2 ** 64
+    return z ^ (z >> 31)
+
+
+@pytest.mark.parametrize("n,rate", [(4097, 0.0), (5000, 0.0), (100_003, 0.0), (1 << 20, 0.0), (100_003, 0.01),
+                                    (1 << 20, 0.001), (9000, 0.5)])
+def test_dgc_sample_positions_strata(n, rate):
+    """Each of the S strata [floor(Gn/S), floor((G+1)n/S)) contributes 8
+    consecutive in-range positions at the offset its hash gives -- recomputed
+    with Python integers (not numpy uint64).  S = 512, or ceil(rate n / 8)
+    capped at 512."""
+    h = O.dgc_segment_hash(7, 1)
+    S = 512 if rate == 0 else min(512, max(1, -(-int(rate * n * 1000) // 8000)))
+    assert O.dgc_strata(n, rate) == S
+    pos = O.dgc_sample_positions(n, h, S)
+    assert pos.size == 8 * S
+    for G in range(S):
+        a, b = G * n // S, (G + 1) * n // S
+        off = ((_py_splitmix(h ^ G) & 0xFFFFFFFF) * (b - a - 7)) >> 32
+        want = [a + off + c for c in range(8)]
+        assert list(pos[8 * G:8 * G + 8]) == want
+        assert a <= want[0] and want[-1] < b
+    assert np.all(np.diff(pos) > 0)
+
+
+@pytest.mark.parametrize("approx", [False, True])
+@pytest.mark.parametrize("ratio", [0.001, 0.01])
+def test_dgc_threshold_is_prefix_of_sampled_rank(approx, ratio):
+    """The threshold is the need-th largest sampled key with its low 10 bits
+    cleared; recomputed with Python's sorted() over struct-derived keys."""
+    n = 300_001
+    acc = gradient(n, dist="D2")
+    k = O.k_of(n, ratio)
+    h = O.dgc_segment_hash(3, 0)
+    thr = O.dgc_threshold(acc, k, ratio, h, approx)
+    pos = O.dgc_sample_positions(n, h)
+    keys = sorted((struct_key(acc[p]) for p in pos), reverse=True)
+    rs = ratio * 4096
+    need = int(rs + 0.5) if approx else math.ceil(rs + 4 * math.sqrt(rs))
+    assert thr == keys[need - 1] // 1024 * 1024
+
+
+@pytest.mark.parametrize("dist", ["D1", "D2", "D3"])
+@pytest.mark.parametrize("ratio", [0.001, 0.01, 0.1])
+def test_dgc_approx_is_top_m(dist, ratio):
+    """Approximate-count DGC keeps m = min(k, #{key >= thr}) elements, and they
+    are the top-m in (key desc, idx asc) order: the brute-force stable sort's
+    first m; the sparse EF identity holds exactly."""
+    n = 100_003
+    acc = gradient(n, dist=dist, tensor=5)
+    cfg = O.Cfg("dgc", ratio, approx=True)
+    k = O.k_of(n, ratio)
+    thr = O.dgc_threshold(acc, k, ratio, O.dgc_segment_hash(5, 0), True)
+    ch, t = O.compress_segment(cfg, acc, tensor_id=5)
+    keys = np.array([struct_key(v) for v in acc], np.int64)   # struct-derived, not O.key
+    m = min(k, int((keys >= thr).sum()))
+    order = sorted(range(n), key=lambda i: (-keys[i], i))[:m]
+    assert ch.idx.size == m
+    assert np.array_equal(ch.idx, np.sort(np.array(order, np.uint32)))
+    r = O.residual_update(acc, t)
+    assert np.array_equal((t + r).view(np.uint32), acc.view(np.uint32))
+
+
+def test_dgc_approx_count_unbiased():
+    """With the expected rank j* = round(rho s), the number kept averages about
+    k over many independent segments (the sampled threshold is unbiased up to
+    the bin rounding), and is capped at k."""
+    n, ratio = 60_000, 0.01
+    k = O.k_of(n, ratio)
+    counts = []
+    for t in range(150):
+        acc = gradient(n, tensor=t)
+        ch, _ = O.compress_segment(O.Cfg("dgc", ratio, approx=True), acc, tensor_id=t)
+        counts.append(ch.idx.size)
+    counts = np.array(counts)
+    assert counts.max() <= k
+    # capped at k, the mean sits a little below k; uncapped it would be ~k
+    assert 0.80 * k < counts.mean() <= k
+
+
+def test_dgc_approx_small_segments_are_exact():
+    """Segments of <= 4096 elements are their own sample with need = k: the
+    approximate mode returns the exact top-k."""
+    for n, ratio in ((33, 0.1), (1000, 0.01), (4096, 0.05)):
+        acc = gradient(n, dist="D3")
+        a, _ = O.compress_segment(O.Cfg("dgc", ratio, approx=True), acc)
+        assert np.array_equal(a.idx, O.topk_select(acc, O.k_of(n, ratio)))
