@@ -244,37 +244,47 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
 // Sign h2: a grid of a few CTAs per SM, each over a contiguous range of the
 // bucket's units (mostly inside one segment), so the dependent prologue of a
 // segment (its table entry, the piece pointers and scales) is paid once per
-// (CTA, segment) instead of once per unit.  Per unit (8192 elements = 256
-// words = 1 KB per piece) the words of ALL pieces are loaded with coalesced
-// 16-byte loads, one round trip for the whole unit, and parked in shared
-// memory; the next unit's words are already in flight (registers) while this
-// unit is decoded and stored, so the 4 B/elem output stream never waits on a
-// word load.  Decode: rank-order fp32 sum from +0 over the pieces, then /
-// divisor (R9); a word is read from shared memory by the 8 lanes that decode
-// it (broadcast).
+// (CTA, segment) instead of once per unit.  A unit is 8192 elements (256
+// words = 1 KB per piece); a thread decodes 8 float4 of it.  Rank-order fp32
+// sum from +0 over the pieces, then / divisor (R9), by one of:
+//  * 1 piece: the words straight from global memory into registers, the next
+//    unit's already in flight while this one is decoded (a select per element);
+//  * 2..8 pieces: the words of all pieces staged in shared memory with
+//    coalesced 16-byte loads (one round trip per unit, the next unit's in
+//    flight), and the decoded sum looked up by bit pattern (esp_device.cuh)
+//    in a table replicated 32 times, [pattern][lane], so that the 32 lanes'
+//    random lookups never share a bank;
+//  * more pieces: staged words, sequential select + add per piece.
 constexpr int kSignWords = kSignUnit / 32;           // words per piece and unit
 constexpr int kSignVec = kSignWords / 4;             // uint4 per piece and unit
 constexpr int kSignPre = 4;                          // uint4 per thread in flight (pieces <= 16)
+constexpr int kSignLutBytes = (1 << kSignLutPieces) * 32 * 4;   // 32 KB
+__host__ __device__ constexpr size_t sign_h2_smem(int max_pieces) {
+  return (size_t)(max_pieces < 1 ? 1 : max_pieces) * kSignWords * 4 + (max_pieces >= 2 ? kSignLutBytes : 0);
+}
 template <int KIND>
 __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restrict__ segs,
                                                            const uint32_t* __restrict__ unit_seg,
                                                            uint32_t nunits,
-                                                           const unsigned char* const* __restrict__ pieces) {
+                                                           const unsigned char* const* __restrict__ pieces,
+                                                           int max_pieces) {
   pdl_wait();     // predecessors in the stream are complete (PDL)
   pdl_trigger();
-  extern __shared__ __align__(16) uint32_t sh_words[];   // [npieces][kSignWords]
+  extern __shared__ __align__(16) uint32_t sh_dyn[];
+  uint32_t* sh_words = sh_dyn;                                   // [npieces][kSignWords]
+  float* sh_lut = reinterpret_cast<float*>(sh_dyn + (max_pieces < 1 ? 1 : max_pieces) * kSignWords);   // [256][32]
   __shared__ float sh_sp[kMaxPieces], sh_sn[kMaxPieces];
   __shared__ const uint32_t* sh_w[kMaxPieces];
-  __shared__ float sh_lut[1 << kSignLutPieces];   // np <= 8: decoded sum (÷ divisor) per bit pattern
   constexpr int kJ = kSignUnit / (kThreads * 4);
+  const int lane = threadIdx.x & 31;
   const uint32_t u0 = (uint32_t)((uint64_t)blockIdx.x * nunits / gridDim.x);
   const uint32_t u1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nunits / gridDim.x);
   uint32_t cur = 0xFFFFFFFFu;
   SegH2 S{};
-  uint4 pre[kSignPre];       // the next unit's words (vector v = threadIdx.x + m * kThreads)
-  bool have = false;         // pre[] holds the words of unit gu
+  uint4 pre[kSignPre];       // staged paths: the next unit's words (vector v = threadIdx.x + m * kThreads)
+  uint32_t wnext[kJ];        // one piece: the next unit's words
+  bool have = false;         // pre[] / wnext[] hold the words of unit gu
   uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
-  // vector v of unit (start word w0) of the current segment: piece v / kSignVec
   auto load_vec = [&](uint32_t v, uint32_t w0, uint32_t nwords) -> uint4 {
     const uint32_t r = v / kSignVec, q = v % kSignVec;
     const uint32_t w = w0 + q * 4;
@@ -295,12 +305,14 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
         sh_w[r] = reinterpret_cast<const uint32_t*>(h + 16);
       }
       __syncthreads();
-      if (S.npieces <= (uint32_t)kSignLutPieces) {
+      if (S.npieces >= 2 && S.npieces <= (uint32_t)kSignLutPieces) {
         const Divisor dv(S.divisor);
         for (uint32_t t = threadIdx.x; t < (1u << S.npieces); t += kThreads) {
           float a = 0.f;
           for (uint32_t r = 0; r < S.npieces; ++r) a = __fadd_rn(a, ((t >> r) & 1u) ? sh_sp[r] : sh_sn[r]);
-          sh_lut[t] = S.divisor == 1.0f ? a : dv(a);
+          if (S.divisor != 1.0f) a = dv(a);
+#pragma unroll 8
+          for (int c = 0; c < 32; ++c) sh_lut[t * 32 + c] = a;
         }
         __syncthreads();
       }
@@ -308,8 +320,41 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
     }
     const uint32_t n = S.n, np = S.npieces;
     const uint32_t nwords = (n + 31) / 32;   // words a piece carries for this segment
-    const uint32_t nvec = np * kSignVec;
     const uint32_t w0 = (gu - S.unit0) * kSignWords;
+    const uint32_t lt = threadIdx.x * 4;      // unit-relative element of j = 0
+    const uint32_t e0 = w0 * 32 + lt;
+    const Divisor div(S.divisor);
+    const bool ones = S.divisor == 1.0f;
+    float* out = seg_out(S);
+    if (np == 1) {
+      const uint32_t* w = sh_w[0];
+      uint32_t wd[kJ];
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const uint32_t e = e0 + j * kThreads * 4;
+        wd[j] = have ? wnext[j] : (e < n ? __ldg(w + (e >> 5)) : 0u);
+      }
+      have = gu + 1 < u1 && sid_next == cur;   // prefetch the next unit of the segment
+      if (have) {
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+          const uint32_t e = e0 + kSignUnit + j * kThreads * 4;
+          wnext[j] = e < n ? __ldg(w + (e >> 5)) : 0u;
+        }
+      }
+      const float sp = sh_sp[0], sn = sh_sn[0];
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const uint32_t e = e0 + j * kThreads * 4;
+        const uint32_t nib = (wd[j] >> (e & 31)) & 0xFu;
+        float4 v = make_float4(__fadd_rn(0.f, (nib & 1) ? sp : sn), __fadd_rn(0.f, (nib & 2) ? sp : sn),
+                               __fadd_rn(0.f, (nib & 4) ? sp : sn), __fadd_rn(0.f, (nib & 8) ? sp : sn));
+        if (e < n) store4_guard(out, e, n, ones ? v : div(v));
+      }
+      continue;
+    }
+    // ---- stage every piece's words of this unit in shared memory
+    const uint32_t nvec = np * kSignVec;
     const bool prefetch = nvec <= (uint32_t)(kSignPre * kThreads);
     __syncthreads();   // the previous unit's words are decoded
     if (prefetch) {
@@ -325,8 +370,7 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
         const uint32_t v = threadIdx.x + m * kThreads;
         if (v < nvec) reinterpret_cast<uint4*>(sh_words)[v] = pre[m];
       }
-      // the next unit of the same segment: its loads fly while this one is decoded
-      have = gu + 1 < u1 && sid_next == cur;
+      have = gu + 1 < u1 && sid_next == cur;   // the next unit's loads fly while this one is decoded
       if (have) {
 #pragma unroll
         for (int m = 0; m < kSignPre; ++m) {
@@ -346,21 +390,17 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
       }
     }
     __syncthreads();
-    const Divisor div(S.divisor);
-    const bool ones = S.divisor == 1.0f;
-    const uint32_t lt = threadIdx.x * 4;   // unit-relative element of j = 0
-    const uint32_t e0 = w0 * 32 + lt;
-    float* out = seg_out(S);
     if (np <= (uint32_t)kSignLutPieces) {
       // 4 index bytes per float4: bit r of byte c = piece r's bit of element c
+      const float* lut = sh_lut + lane;
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
         const uint32_t l = lt + j * kThreads * 4;
         const uint32_t wi = l >> 5, sh = l & 31;
         uint32_t idx4 = 0;
         for (uint32_t r = 0; r < np; ++r) idx4 |= spread4((sh_words[r * kSignWords + wi] >> sh) & 0xFu) << r;
-        const float4 v = make_float4(sh_lut[idx4 & 0xFFu], sh_lut[(idx4 >> 8) & 0xFFu], sh_lut[(idx4 >> 16) & 0xFFu],
-                                     sh_lut[idx4 >> 24]);
+        const float4 v = make_float4(lut[(idx4 & 0xFFu) * 32], lut[((idx4 >> 8) & 0xFFu) * 32],
+                                     lut[((idx4 >> 16) & 0xFFu) * 32], lut[(idx4 >> 24) * 32]);
         const uint32_t e = e0 + j * kThreads * 4;
         if (e < n) store4_guard(out, e, n, v);
       }
@@ -458,9 +498,10 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
 void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
                     const unsigned char* const* pieces, int max_pieces, cudaStream_t st) {
   if (nunits == 0) return;
-  const int smem = (max_pieces < 1 ? 1 : max_pieces) * kSignWords * 4;   // <= 64 KB (64 pieces)
+  if (max_pieces < 1) max_pieces = 1;
+  const int smem = (int)sign_h2_smem(max_pieces);   // words of every piece + the 32 KB table (>= 2 pieces)
   static const bool attr = [] {
-    const int mx = kMaxPieces * kSignWords * 4;
+    const int mx = (int)sign_h2_smem(kMaxPieces);
     return cudaFuncSetAttribute(h2_sign_kernel<K_EFSIGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) ==
                cudaSuccess &&
            cudaFuncSetAttribute(h2_sign_kernel<K_ONEBIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) ==
@@ -473,8 +514,10 @@ void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int n
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sign_kernel<K_EFSIGN>, kThreads, smem);
   const int cap = sms * (per_sm > 0 ? per_sm : 4);
   const int grid = nunits < cap ? nunits : cap;
-  if (kind == K_EFSIGN) launch_pdl(h2_sign_kernel<K_EFSIGN>, grid, kThreads, smem, st, segs, unit_seg, (uint32_t)nunits, pieces);
-  else launch_pdl(h2_sign_kernel<K_ONEBIT>, grid, kThreads, smem, st, segs, unit_seg, (uint32_t)nunits, pieces);
+  if (kind == K_EFSIGN)
+    launch_pdl(h2_sign_kernel<K_EFSIGN>, grid, kThreads, smem, st, segs, unit_seg, (uint32_t)nunits, pieces, max_pieces);
+  else
+    launch_pdl(h2_sign_kernel<K_ONEBIT>, grid, kThreads, smem, st, segs, unit_seg, (uint32_t)nunits, pieces, max_pieces);
   count_launches(1);
 }
 

@@ -111,8 +111,13 @@ struct RandomkOp {
 // the indices (else one per piece, independent, so they overlap), and all of
 // a batch's value loads are in flight before the first is added.
 constexpr int kRkBatch = 8;
+// Persistent: a few CTAs per SM, each over a contiguous range of the bucket's
+// units, the segment prologue (piece hashes and pointers) once per (CTA,
+// segment); per unit the 32 KB output tile is built in shared memory and
+// stored once, while the next unit's picks are already being computed.
 __global__ void __launch_bounds__(kThreads) h2_randomk_kernel(const SegH2* __restrict__ segs,
                                                               const uint32_t* __restrict__ unit_seg,
+                                                              uint32_t nunits,
                                                               const unsigned char* const* __restrict__ pieces,
                                                               const uint32_t* __restrict__ rankterms) {
   pdl_wait();     // predecessors in the stream are complete (PDL)
@@ -121,69 +126,81 @@ __global__ void __launch_bounds__(kThreads) h2_randomk_kernel(const SegH2* __res
   __shared__ uint64_t sh_h[64];
   __shared__ const float* sh_v[64];
   __shared__ int sh_shared;
-  const uint32_t sid = unit_seg[blockIdx.x];
-  const SegH2 S = segs[sid];
-  const uint32_t u = blockIdx.x - S.unit0;
-  const uint32_t n = S.n, k = S.k, np = S.npieces;
-  const uint32_t lo = u * kUnit, hi = min(lo + (uint32_t)kUnit, n) - 1;
-  const uint64_t step = *S.step;
-  for (uint32_t r = threadIdx.x; r < np; r += kThreads) {
-    sh_h[r] = randomk_hash(S.hash, step, S.part, rankterms[S.piece0 + r]);
-    sh_v[r] = reinterpret_cast<const float*>(pieces[S.piece0 + r]);
-  }
-  for (int i = threadIdx.x; i < kUnit / 4; i += kThreads)
-    reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int same = 1;
-    for (uint32_t r = 1; r < np; ++r) same &= sh_h[r] == sh_h[0];
-    sh_shared = same;
-  }
-  __syncthreads();
-  const bool shared = sh_shared != 0;
-  const uint64_t j0 = stratum_of(lo, k, n), j1 = stratum_of(hi, k, n);
-  for (uint64_t jj = j0 + threadIdx.x; jj <= j1; jj += kThreads) {
-    const uint64_t a = jj * n / k, len = (jj + 1) * n / k - a;
-    uint32_t p0 = (uint32_t)(a + splitmix64(sh_h[0] ^ jj) % len);
-    float sum = 0.f;
-    bool any = false;
-    uint32_t pos = 0;
-    for (uint32_t r0 = 0; r0 < np; r0 += kRkBatch) {
-      uint32_t p[kRkBatch];
-      float v[kRkBatch];
-#pragma unroll
-      for (int m = 0; m < kRkBatch; ++m) {
-        const uint32_t r = r0 + m;
-        p[m] = (r < np) ? (shared || r == 0 ? p0 : (uint32_t)(a + splitmix64(sh_h[r] ^ jj) % len)) : 0xFFFFFFFFu;
+  const uint32_t u0 = (uint32_t)((uint64_t)blockIdx.x * nunits / gridDim.x);
+  const uint32_t u1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nunits / gridDim.x);
+  uint32_t cur = 0xFFFFFFFFu;
+  SegH2 S{};
+  bool shared = true;
+  for (uint32_t gu = u0; gu < u1; ++gu) {
+    const uint32_t sid = unit_seg[gu];
+    __syncthreads();   // the previous unit's tile has been stored (and its segment's tables read)
+    if (sid != cur) {
+      cur = sid;
+      S = segs[sid];
+      const uint64_t step = *S.step;
+      for (uint32_t r = threadIdx.x; r < S.npieces; r += kThreads) {
+        sh_h[r] = randomk_hash(S.hash, step, S.part, rankterms[S.piece0 + r]);
+        sh_v[r] = reinterpret_cast<const float*>(pieces[S.piece0 + r]);
       }
-#pragma unroll
-      for (int m = 0; m < kRkBatch; ++m) {
-        const uint32_t r = r0 + m;
-        v[m] = (r < np && p[m] >= lo && p[m] <= hi) ? __ldg(sh_v[r] + jj) : 0.f;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int same = 1;
+        for (uint32_t r = 1; r < S.npieces; ++r) same &= sh_h[r] == sh_h[0];
+        sh_shared = same;
       }
+    }
+    for (int i = threadIdx.x; i < kUnit / 4; i += kThreads)
+      reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    shared = sh_shared != 0;
+    const uint32_t n = S.n, k = S.k, np = S.npieces;
+    const uint32_t u = gu - S.unit0;
+    const uint32_t lo = u * kUnit, hi = min(lo + (uint32_t)kUnit, n) - 1;
+    const uint64_t j0 = stratum_of(lo, k, n), j1 = stratum_of(hi, k, n);
+    for (uint64_t jj = j0 + threadIdx.x; jj <= j1; jj += kThreads) {
+      const uint64_t a = jj * n / k, len = (jj + 1) * n / k - a;
+      const uint32_t p0 = (uint32_t)(a + splitmix64(sh_h[0] ^ jj) % len);
+      float sum = 0.f;
+      bool any = false;
+      uint32_t pos = 0;
+      for (uint32_t r0 = 0; r0 < np; r0 += kRkBatch) {
+        uint32_t p[kRkBatch];
+        float v[kRkBatch];
 #pragma unroll
-      for (int m = 0; m < kRkBatch; ++m) {
-        const uint32_t r = r0 + m;
-        if (r < np && p[m] >= lo && p[m] <= hi) {
-          if (shared) {
-            sum = __fadd_rn(sum, v[m]);
-            any = true;
-            pos = p[m] - lo;
-          } else {
-            acc[p[m] - lo] = __fadd_rn(acc[p[m] - lo], v[m]);   // this thread owns the stratum's positions
+        for (int m = 0; m < kRkBatch; ++m) {
+          const uint32_t r = r0 + m;
+          p[m] = (r < np) ? (shared || r == 0 ? p0 : (uint32_t)(a + splitmix64(sh_h[r] ^ jj) % len)) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int m = 0; m < kRkBatch; ++m) {
+          const uint32_t r = r0 + m;
+          v[m] = (r < np && p[m] >= lo && p[m] <= hi) ? __ldg(sh_v[r] + jj) : 0.f;
+        }
+#pragma unroll
+        for (int m = 0; m < kRkBatch; ++m) {
+          const uint32_t r = r0 + m;
+          if (r < np && p[m] >= lo && p[m] <= hi) {
+            if (shared) {
+              sum = __fadd_rn(sum, v[m]);
+              any = true;
+              pos = p[m] - lo;
+            } else {
+              acc[p[m] - lo] = __fadd_rn(acc[p[m] - lo], v[m]);   // this thread owns the stratum's positions
+            }
           }
         }
       }
+      if (shared && any) acc[pos] = sum;
     }
-    if (shared && any) acc[pos] = sum;
-  }
-  __syncthreads();
-  const Divisor div(S.divisor);
-  const bool ones = S.divisor == 1.0f;
-  for (uint32_t i = threadIdx.x * 4; lo + i <= hi; i += kThreads * 4) {
-    float4 v = *reinterpret_cast<const float4*>(acc + i);
-    if (!ones && (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)) v = div(v);
-    store4_guard(seg_out(S), lo + i, n, v);
+    __syncthreads();
+    const Divisor div(S.divisor);
+    const bool ones = S.divisor == 1.0f;
+    float* out = seg_out(S);
+    for (uint32_t i = threadIdx.x * 4; lo + i <= hi; i += kThreads * 4) {
+      float4 v = *reinterpret_cast<const float4*>(acc + i);
+      if (!ones && (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)) v = div(v);
+      store4_guard(out, lo + i, n, v);
+    }
   }
 }
 
@@ -195,7 +212,15 @@ void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, 
 void launch_h2_randomk(const SegH2* segs, const uint32_t* unit_seg, int nunits,
                        const unsigned char* const* pieces, const uint32_t* rankterms, cudaStream_t st) {
   if (nunits == 0) return;
-  launch_pdl(h2_randomk_kernel, nunits, kThreads, 0, st, segs, unit_seg, pieces, rankterms);
+  static const int cap = [] {
+    int dev = 0, sms = 148, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_randomk_kernel, kThreads, 0);
+    return sms * (per_sm > 0 ? per_sm : 4);
+  }();
+  const int grid = nunits < cap ? nunits : cap;
+  launch_pdl(h2_randomk_kernel, grid, kThreads, 0, st, segs, unit_seg, (uint32_t)nunits, pieces, rankterms);
   count_launches(1);
 }
 
