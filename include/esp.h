@@ -255,15 +255,30 @@ esp_status_t esp_sync_many_loopback(const esp_world_t* worlds, int nranks, const
 
 /* ---- sizes / cost table ----------------------------------------------
  * esp_compressed_bytes: bytes of one rank's payload for numel elements split
- * into nparts partitions (R10).  esp_wire_bytes: communication volume per rank
- * of a cost-table row (row: 0 Allreduce, 1 Allgather, 2 Alltoall/Allgather
- * sparse, 3 Alltoall/Allgather quantized, 4 Gather/Broadcast sparse,
- * 5 Gather/Broadcast quantized).  esp_model_time: that volume / B seconds.
+ * into nparts partitions (R10).
+ * esp_wire_bytes: the communication volume of a routine for a tensor type,
+ *   per rank on the critical path, for a payload (or, uncompressed, a tensor)
+ *   of M bytes over n ranks -- the cost table's communication column times B
+ *   (S:126 for the uncompressed pairs).  tensor_type:
+ *   ESP_TT_ALLREDUCIBLE (uncompressed fp32, or Randomk values with shared
+ *   indices), ESP_TT_SPARSE (first process of a divisible routine, P:70-76 /
+ *   P:97-103; any compressed payload for Allgather), ESP_TT_QUANTIZED (second
+ *   process, P:78-87 / P:105-115).  The table models every row as one volume
+ *   over a full-duplex link, so *sent == *recv.  Volumes:
+ *     ALLREDUCE, allreducible            2(n-1)M/n
+ *     REDUCESCATTER_ALLGATHER, allred.   (n-1)M/n + (n-1)M/n
+ *     REDUCE_BROADCAST, allreducible     (n-1)M + M
+ *     ALLGATHER, sparse or quantized     (n-1)M
+ *     ALLTOALL_ALLGATHER, sparse         (n^2-1)M/n;  quantized 2(n-1)M/n (R13)
+ *     GATHER_BROADCAST, sparse           (2n-1)M;     quantized nM
+ *   0 for n = 1.  Any other (routine, type) pair -> ESP_ERR_UNSUPPORTED.
+ * esp_model_time: that volume / B seconds (B in bytes/s).
  */
+enum { ESP_TT_ALLREDUCIBLE = 0, ESP_TT_SPARSE = 1, ESP_TT_QUANTIZED = 2 };
 esp_status_t esp_compressed_bytes(const esp_compressor_cfg_t* cfg, size_t numel, int nparts,
                                   size_t* out);
-esp_status_t esp_wire_bytes(int row, double M, int n, double* out);
-esp_status_t esp_model_time(int row, double M, int n, double B, double* out_seconds);
+esp_status_t esp_wire_bytes(int routine, int tensor_type, double M, int n, double* sent, double* recv);
+esp_status_t esp_model_time(int routine, int tensor_type, double M, int n, double B, double* out_seconds);
 
 /* ---- strategy selection (App. A; Algorithm 1
  * P:1299-1361; readings R15, R21) -----------------------------------------------

@@ -677,13 +677,17 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
 }
 
 // ------------------------------------------------------------------ 4. refine
-// A finalize group = kRunsPerGroup (64) consecutive runs of one segment, owned
-// by ONE WARP: the finalize is a chain of dependent small loads (descriptor,
-// run counts, candidates, counters), so it is throughput-bound on the number of
-// independent chains in flight -- 64 warps per SM, no CTA barriers.  The
-// group's candidates are addressed as one flat, index-ordered list:
-// off[i] = first flat position of run i (lane l holds runs 2l and 2l+1).
-static_assert(kRunsPerGroup == 64, "two run counts per lane");
+// A finalize group = S.rpg (8..64, a power of two) consecutive runs of one
+// segment, owned by ONE WARP: the finalize is a chain of dependent small loads
+// (descriptor, run counts, candidates, counters), so it is throughput-bound on
+// the number of independent chains in flight -- 64 warps per SM, no CTA
+// barriers.  The planner sizes rpg so that a group expects about one batch of
+// candidates (kBatch x 32): dense candidate segments (1% ratios) get short
+// groups, so each warp's chain of dependent candidate loads stays one or two
+// round trips long.  The group's candidates are addressed as one flat,
+// index-ordered list: off[i] = first flat position of run i (lane l holds
+// runs l * ppl .. l * ppl + ppl - 1, ppl = rpg / 32 or 1).
+static_assert(kRunsPerGroup == 64, "at most two run counts per lane");
 constexpr int kBatch = 4;   // candidate loads in flight per lane
 // refine: a group with up to this many candidates adds its matches to the
 // global round histogram directly; larger groups (1% ratios, TOPK, fallbacks)
@@ -719,17 +723,19 @@ __device__ __forceinline__ WarpGroup warp_group_offsets(const SegH1* segs, const
   const SegH1& S = *G.S;
   G.g = gi - S.group0;
   const uint32_t nruns = (S.n + kRun - 1) / kRun;
-  const uint32_t run0 = G.g * kRunsPerGroup;
-  G.nr = min((uint32_t)kRunsPerGroup, nruns - run0);
-  const uint32_t i0 = 2 * lane, i1 = 2 * lane + 1;
+  const uint32_t rpg = S.rpg;
+  const uint32_t run0 = G.g * rpg;
+  G.nr = min(rpg, nruns - run0);
+  const uint32_t ppl = rpg > 32 ? 2u : 1u;   // runs per lane
+  const uint32_t i0 = ppl * lane, i1 = i0 + 1;
   const uint32_t c0 = i0 < G.nr ? __ldcg(S.runcnt + run0 + i0) : 0u;
-  const uint32_t c1 = i1 < G.nr ? __ldcg(S.runcnt + run0 + i1) : 0u;
+  const uint32_t c1 = (ppl == 2 && i1 < G.nr) ? __ldcg(S.runcnt + run0 + i1) : 0u;
   const uint32_t incl = warp_incl_scan(c0 + c1);
   const uint32_t ex = incl - c0 - c1;
-  off[i0] = ex;
-  off[i1] = ex + c0;
+  if (i0 < rpg) off[i0] = ex;
+  if (ppl == 2) off[i1] = ex + c0;
   G.C = __shfl_sync(0xffffffffu, incl, 31);
-  if (lane == 31) off[64] = incl;
+  if (lane == 31) off[rpg] = incl;
   __syncwarp();
   return G;
 }
@@ -740,7 +746,7 @@ __device__ __forceinline__ uint2 warp_group_cand(const WarpGroup& G, const uint3
     const uint32_t mid = (lo + hi) >> 1;
     if (off[mid] <= q) lo = mid; else hi = mid;
   }
-  return __ldcg(G.S->cand + (size_t)(G.g * kRunsPerGroup + lo) * kRun + (q - off[lo]));
+  return __ldcg(G.S->cand + (size_t)(G.g * G.S->rpg + lo) * kRun + (q - off[lo]));
 }
 
 // After round 2 a group's candidates are DENSE: compacted in place to the
@@ -750,11 +756,11 @@ __device__ __forceinline__ WarpGroup warp_group_dense(const SegH1* segs, const u
   G.S = segs + group_seg[gi];
   G.g = gi - G.S->group0;
   G.nr = 0;
-  G.C = __ldcg(G.S->runcnt + (size_t)G.g * kRunsPerGroup);
+  G.C = __ldcg(G.S->runcnt + (size_t)G.g * G.S->rpg);
   return G;
 }
 __device__ __forceinline__ uint2* group_slots(const WarpGroup& G) {
-  return G.S->cand + (size_t)G.g * kRunsPerGroup * kRun;
+  return G.S->cand + (size_t)G.g * G.S->rpg * kRun;
 }
 
 // Warp-wide: bin b of a 1024-bin global histogram, the sum of `rep` replicas
@@ -863,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_refine_kernel(const SegH1* __
       }
     }
   }
-  if (ROUND == 2 && lane == 0) S.runcnt[(size_t)G.g * kRunsPerGroup] = G.C;   // the dense count
+  if (ROUND == 2 && lane == 0) S.runcnt[(size_t)G.g * S.rpg] = G.C;   // the dense count
   if (!direct) {
     __syncwarp();
     for (int i = lane; i < 512; i += 32) {

@@ -195,6 +195,29 @@ static uint16_t dgc_strata(uint64_t n, double rate) {
   return (uint16_t)(c < 1.0 ? 1.0 : (c > kSample / 8 ? kSample / 8 : c));
 }
 
+// DGC finalize group length (runs) of a segment: the largest power of two in
+// [8, 64] whose expected candidate count stays within one refine batch (128):
+// candidates per 512-element run ~ 512 x (sampled rank / sample size) when
+// sampled, ~ 512 k / n for a whole-segment sample, ~ 1024 k / n for TOPK
+// (the k-th key's 11-bit bin and above)
+static uint32_t dgc_rpg(uint64_t len, uint32_t k, const esp_compressor_cfg_t& cfg) {
+  double frac;
+  if (cfg.kind == ESP_TOPK) {
+    frac = 2.0 * k / (double)len;
+  } else if (len <= (uint64_t)kSample) {
+    frac = (double)k / (double)len;
+  } else {
+    const double s = 8.0 * dgc_strata(len, cfg.dgc_sample_rate), rs = cfg.ratio * s;
+    double need = cfg.dgc_approx ? std::floor(rs + 0.5) : std::ceil(rs + 4.0 * std::sqrt(rs));
+    need = need < 1.0 ? 1.0 : (need > s ? s : need);
+    frac = need / s;
+  }
+  const double c_run = (double)kRun * (frac > 1.0 ? 1.0 : frac);
+  uint32_t rpg = kRunsPerGroup;
+  while (rpg > 8 && rpg * c_run > 128.0) rpg /= 2;
+  return rpg;
+}
+
 static void fill_unit_table(std::vector<uint32_t>& units, uint32_t seg, uint32_t count) {
   for (uint32_t i = 0; i < count; ++i) units.push_back(seg);
 }
@@ -419,7 +442,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.unit0 = unit_cursor;
         s.nunits = nunits;
         const uint32_t nruns = div_up(len, kRun);
-        s.ngroups = div_up(nruns, kRunsPerGroup);
+        s.rpg = dgc ? dgc_rpg(len, s.k, c->cfg) : kRunsPerGroup;
+        s.ngroups = div_up(nruns, s.rpg);
         s.group0 = group_cursor;
         s.ef = c->cfg.error_feedback ? 1 : 0;
         s.unsampled = b.kind == ESP_TOPK ? 1 : 0;
@@ -589,7 +613,8 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           s.step = p.dyn_dev + nslots + slot_idx;
           s.k = k_of(len, c->cfg.ratio);
           const uint32_t nruns = div_up(len, kRun);
-          s.ngroups = div_up(nruns, kRunsPerGroup);
+          s.rpg = dgc ? dgc_rpg(len, s.k, c->cfg) : kRunsPerGroup;
+          s.ngroups = div_up(nruns, s.rpg);
           s.group0 = g0;
           s.unsampled = b.kind == ESP_TOPK ? 1 : 0;
           s.part = d.part;
@@ -767,7 +792,7 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
         ++segs;
         // DGC: histograms + look-back status (one u64 per group of runs)
         if (dgc) {
-          const uint32_t ng = (uint32_t)div_up(div_up(len, kRun), kRunsPerGroup);
+          const uint32_t ng = (uint32_t)div_up(div_up(len, kRun), dgc_rpg(len, c->pk[part], c->cfg));
           nhist += (round_up((size_t)dgc_hist_words(dgc_hrep(c->pk[part], ng)) * 4, 256) +
                     round_up((size_t)ng * 8, 256)) * p.w->nlocal;
         }
@@ -781,7 +806,8 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
             const int j = grank(p.w, lr);
             const uint64_t len = c->routine == ESP_ALLTOALL_ALLGATHER ? c->phi[j] - c->plo[j] : (j == 0 ? c->N : 0);
             if (!len) continue;
-            const uint32_t ng = (uint32_t)div_up(div_up(len, kRun), kRunsPerGroup);
+            const uint32_t ng =
+                (uint32_t)div_up(div_up(len, kRun), dgc_rpg(len, k_of(len, c->cfg.ratio), c->cfg));
             nhist += round_up((size_t)dgc_hist_words(dgc_hrep(k_of(len, c->cfg.ratio), ng)) * 4, 256) +
                      round_up((size_t)ng * 8, 256);
           }

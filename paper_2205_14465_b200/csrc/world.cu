@@ -454,22 +454,33 @@ esp_status_t esp_compressed_bytes(const esp_compressor_cfg_t* cfg, size_t numel,
   ESP_API_END
 }
 
-esp_status_t esp_wire_bytes(int row, double M, int n, double* out) {
+esp_status_t esp_wire_bytes(int routine, int tensor_type, double M, int n, double* sent, double* recv) {
   ESP_API_BEGIN
-  ESP_REQUIRE(out && n >= 1 && M >= 0 && row >= 0 && row <= 5, ESP_ERR_INVALID_ARG, "bad argument");
-  // cost table of flat communication, P:38-43 (communication volume = time * B)
+  ESP_REQUIRE(sent && recv && n >= 1 && M >= 0 && routine >= ESP_ALLREDUCE && routine <= ESP_REDUCE_BROADCAST &&
+                  tensor_type >= ESP_TT_ALLREDUCIBLE && tensor_type <= ESP_TT_QUANTIZED,
+              ESP_ERR_INVALID_ARG, "bad argument");
+  const bool allred = tensor_type == ESP_TT_ALLREDUCIBLE;
+  const bool uncompressed_routine = routine == ESP_ALLREDUCE || routine == ESP_REDUCESCATTER_ALLGATHER ||
+                                    routine == ESP_REDUCE_BROADCAST;
+  ESP_REQUIRE(allred == uncompressed_routine, ESP_ERR_UNSUPPORTED,
+              "allreducible data takes Allreduce, Reduce-scatter/Allgather or Reduce/Broadcast; compressed "
+              "payloads the other routines (P:1064-1065, P:1073)");
+  // cost table of flat communication, P:38-43 (communication volume = time * B);
+  // the uncompressed pairs per S:126
   double v = 0;
   if (n > 1) {
-    switch (row) {
-      case 0: v = 2.0 * (n - 1) * M / n; break;            // Allreduce
-      case 1: v = (n - 1) * M; break;                      // Allgather
-      case 2: v = ((double)n * n - 1) * M / n; break;      // Alltoall/Allgather, sparse
-      case 3: v = 2.0 * (n - 1) * M / n; break;            // Alltoall/Allgather, quantized (R13)
-      case 4: v = (2.0 * n - 1) * M; break;                // Gather/Broadcast, sparse
-      case 5: v = (double)n * M; break;                    // Gather/Broadcast, quantized
+    const bool q = tensor_type == ESP_TT_QUANTIZED;
+    switch (routine) {
+      case ESP_ALLREDUCE: v = 2.0 * (n - 1) * M / n; break;
+      case ESP_REDUCESCATTER_ALLGATHER: v = (n - 1) * M / n + (n - 1) * (M / n); break;
+      case ESP_REDUCE_BROADCAST: v = (n - 1) * M + M; break;
+      case ESP_ALLGATHER: v = (n - 1) * M; break;
+      case ESP_ALLTOALL_ALLGATHER: v = q ? 2.0 * (n - 1) * M / n : ((double)n * n - 1) * M / n; break;   // R13
+      default: v = q ? (double)n * M : (2.0 * n - 1) * M; break;                                   // G/B
     }
   }
-  *out = v;
+  *sent = v;
+  *recv = v;
   ESP_API_END
 }
 
@@ -521,8 +532,9 @@ esp_status_t esp_option_time(const esp_option_t* o, size_t numel, int n, double 
     case ESP_ALLTOALL_ALLGATHER: row = p2 ? 3 : 2; break;
     default: row = p2 ? 5 : 4; break;   // Gather/Broadcast
   }
+  const int tt = row == 0 ? ESP_TT_ALLREDUCIBLE : (p2 ? ESP_TT_QUANTIZED : ESP_TT_SPARSE);
   double comm = 0;
-  esp_status_t s = esp_model_time(row, M, n, B, &comm);
+  esp_status_t s = esp_model_time(o->routine, tt, M, n, B, &comm);
   if (s != ESP_OK) return s;
   auto ev = [&](const esp_curve_t& c, double b) {
     double t = 0;
@@ -564,13 +576,13 @@ esp_status_t esp_select_option(const esp_option_t* opts, int nopt, size_t numel,
   ESP_API_END
 }
 
-esp_status_t esp_model_time(int row, double M, int n, double B, double* out_seconds) {
+esp_status_t esp_model_time(int routine, int tensor_type, double M, int n, double B, double* out_seconds) {
   ESP_API_BEGIN
   ESP_REQUIRE(out_seconds && B > 0, ESP_ERR_INVALID_ARG, "bad argument");
-  double v = 0;
-  esp_status_t s = esp_wire_bytes(row, M, n, &v);
+  double sent = 0, recv = 0;
+  esp_status_t s = esp_wire_bytes(routine, tensor_type, M, n, &sent, &recv);
   if (s != ESP_OK) return s;
-  *out_seconds = v / B;
+  *out_seconds = recv / B;
   ESP_API_END
 }
 

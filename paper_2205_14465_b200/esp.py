@@ -100,8 +100,8 @@ def lib():
             "esp_compress": [vp, vp, vp, vp], "esp_decompress": [vp, C.POINTER(vp), i32, vp, vp],
             "esp_sync": [vp, vp, vp, vp], "esp_sync_many": [vp, C.POINTER(vp), C.POINTER(vp), i32, vp],
             "esp_compressed_bytes": [C.POINTER(CompressorCfg), sz, i32, C.POINTER(sz)],
-            "esp_wire_bytes": [i32, dbl, i32, C.POINTER(dbl)],
-            "esp_model_time": [i32, dbl, i32, dbl, C.POINTER(dbl)],
+            "esp_wire_bytes": [i32, i32, dbl, i32, C.POINTER(dbl), C.POINTER(dbl)],
+            "esp_model_time": [i32, i32, dbl, i32, dbl, C.POINTER(dbl)],
             "esp_curve_eval": [C.POINTER(Curve), dbl, C.POINTER(dbl)],
             "esp_option_time": [C.POINTER(Option), sz, i32, dbl, C.POINTER(dbl)],
             "esp_select_option": [C.POINTER(Option), i32, sz, i32, dbl, C.POINTER(i32), C.POINTER(dbl)],
@@ -170,15 +170,19 @@ def esp_compressed_bytes(cfg: CompressorCfg, numel: int, nparts: int) -> int:
     return out.value
 
 
-def esp_wire_bytes(row: int, M: float, n: int) -> float:
-    out = C.c_double()
-    _check(lib().esp_wire_bytes(row, M, n, C.byref(out)))
-    return out.value
+TENSOR_TYPES = {"allreducible": 0, "sparse": 1, "quantized": 2}
 
 
-def esp_model_time(row: int, M: float, n: int, B: float) -> float:
+def esp_wire_bytes(routine: str, tensor_type: str, M: float, n: int):
+    """-> (sent, recv) bytes per rank on the critical path (cost table)."""
+    sent, recv = C.c_double(), C.c_double()
+    _check(lib().esp_wire_bytes(ROUTINES[routine], TENSOR_TYPES[tensor_type], M, n, C.byref(sent), C.byref(recv)))
+    return sent.value, recv.value
+
+
+def esp_model_time(routine: str, tensor_type: str, M: float, n: int, B: float) -> float:
     out = C.c_double()
-    _check(lib().esp_model_time(row, M, n, B, C.byref(out)))
+    _check(lib().esp_model_time(ROUTINES[routine], TENSOR_TYPES[tensor_type], M, n, B, C.byref(out)))
     return out.value
 
 

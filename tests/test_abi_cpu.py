@@ -43,11 +43,22 @@ def test_too_large(E):
 
 
 def test_wire_bytes_vs_oracle(E):
-    rows = ["allreduce", "allgather", "alltoall_allgather_sparse", "alltoall_allgather_quantized",
-            "gather_broadcast_sparse", "gather_broadcast_quantized"]
-    for i, row in enumerate(rows):
+    rows = {("allreduce", "allreducible"): "allreduce", ("allgather", "sparse"): "allgather",
+            ("allgather", "quantized"): "allgather",
+            ("alltoall_allgather", "sparse"): "alltoall_allgather_sparse",
+            ("alltoall_allgather", "quantized"): "alltoall_allgather_quantized",
+            ("gather_broadcast", "sparse"): "gather_broadcast_sparse",
+            ("gather_broadcast", "quantized"): "gather_broadcast_quantized"}
+    for (routine, tt), row in rows.items():
         for n in (1, 2, 4, 8):
             for M in (2 ** 16, 2 ** 20, 2 ** 24, 1e8):
-                assert E.esp_wire_bytes(i, M, n) == pytest.approx(O.table_comm_bytes(row, M, n))
-    # S:132 worked example through the library
-    assert E.esp_model_time(0, 1e8, 4, 1.25e10) == pytest.approx(0.012)
+                sent, recv = E.esp_wire_bytes(routine, tt, M, n)
+                assert recv == pytest.approx(O.table_comm_bytes(row, M, n)) and sent == recv
+    # S:132 worked example through the library; S:126 for the uncompressed pairs
+    assert E.esp_model_time("allreduce", "allreducible", 1e8, 4, 1.25e10) == pytest.approx(0.012)
+    assert E.esp_model_time("reducescatter_allgather", "allreducible", 1e8, 4, 1.25e10) == pytest.approx(0.012)
+    assert E.esp_model_time("reduce_broadcast", "allreducible", 1e8, 4, 1.25e10) == pytest.approx(0.032)
+    for routine, tt in (("allreduce", "sparse"), ("allgather", "allreducible"), ("reduce_broadcast", "quantized")):
+        with pytest.raises(E.EspError) as ei:
+            E.esp_wire_bytes(routine, tt, 1e6, 4)
+        assert ei.value.status == 2
