@@ -200,6 +200,12 @@ esp_status_t esp_world_set_timeout(esp_world_t w, double seconds);
  * default 64); drop_plans frees all of them (e.g. when a training framework
  * rebuilds its gradient buckets).  Every rank must make the same calls. */
 esp_status_t esp_world_set_plan_cache(esp_world_t w, int max_plans);
+/* NVLS multicast for the fused Allgather (NVSwitch replicates one store of a
+ * rank's payload into every GPU's receive buffer): -1 auto (default; on when
+ * every rank's GPU supports multicast and n >= 3), 0 off (unicast peer
+ * copies), 1 on whenever supported.  Same value on every rank; frees the
+ * world's cached plans. */
+esp_status_t esp_world_set_multicast(esp_world_t w, int mode);
 esp_status_t esp_world_drop_plans(esp_world_t w);
 esp_status_t esp_probe_read(esp_world_t w, double* ms, uint64_t* launches, uint64_t* bytes);
 

@@ -103,6 +103,8 @@ struct esp_world_s {
   size_t probe_used = 0;
   std::vector<uint64_t> probe_bytes;
   std::vector<esp::Plan*> plans;           // owned; freed by esp::clear_plans (LRU order, most recent last)
+  int mc_mode = -1;                        // NVLS multicast for fused Allgather: -1 auto (n >= 3), 0 off, 1 on
+  uint32_t mc_seq = 0;                     // multicast regions created (rendezvous names)
   size_t plan_cap = 64;                    // cached plans kept per world (least recently used evicted)
   // fused collectives: a wait kernel that saw no arrival within wait_timeout_ns
   // sets the mapped word *wait_err_host (device alias wait_err)

@@ -28,6 +28,10 @@ void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long targ
 // system-scope release + arrival per job on the destination's counter (k_push.cu)
 void launch_push(const PushJob* jobs, int njobs, const unsigned char* src, unsigned char* const* dsts,
                  unsigned long long* const* cnts, cudaStream_t st);
+// multicast fused collective: each job's bytes stored once to the multicast
+// alias mc_dst + dst_off (every rank's copy), one multicast arrival per job
+void launch_push_mc(const PushJob* jobs, int njobs, const unsigned char* src, unsigned char* mc_dst,
+                    unsigned long long* mc_cnt, cudaStream_t st);
 // Randomk h1 (k_randomk.cu)
 void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 // h1 on the persistent TMA streaming driver, tiles of kDgcTile (k_sign.cu)

@@ -769,19 +769,15 @@ __device__ __forceinline__ uint2* group_slots(const WarpGroup& G) {
 __device__ __forceinline__ void warp_select_bin(const uint32_t* hist, uint32_t rep, uint32_t need,
                                                 uint32_t* out_bin, uint32_t* out_above) {
   const int lane = threadIdx.x & 31;
-  uint32_t h[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) h[i] = 0;
+  // lane sums first (no 32-entry array: the refine kernels run at 32 registers)
+  uint32_t sum = 0;
   for (uint32_t r = 0; r < rep; ++r) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint4 v = __ldcg(reinterpret_cast<const uint4*>(hist + 1024u * r) + lane * 8 + i);
-      h[4 * i] += v.x; h[4 * i + 1] += v.y; h[4 * i + 2] += v.z; h[4 * i + 3] += v.w;
+      sum += v.x + v.y + v.z + v.w;
     }
   }
-  uint32_t sum = 0;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) sum += h[i];
   // above this lane's bins = sum over lanes > lane (suffix scan)
   uint32_t x = sum;
 #pragma unroll
@@ -792,12 +788,13 @@ __device__ __forceinline__ void warp_select_bin(const uint32_t* hist, uint32_t r
   const uint32_t above = x - sum;
   uint32_t bin = 0, ab = 0;
   const bool mine = above < need && need <= above + sum;
-  if (mine) {
+  if (mine) {   // this lane's 32 bins again, from the top
     uint32_t cum = above;
-#pragma unroll
     for (int i = 31; i >= 0; --i) {
-      if (cum + h[i] >= need) { bin = lane * 32 + i; ab = cum; break; }
-      cum += h[i];
+      uint32_t hi = 0;
+      for (uint32_t r = 0; r < rep; ++r) hi += __ldcg(hist + 1024u * r + lane * 32 + i);
+      if (cum + hi >= need) { bin = lane * 32 + i; ab = cum; break; }
+      cum += hi;
     }
   }
   const uint32_t m = __ballot_sync(0xffffffffu, mine);

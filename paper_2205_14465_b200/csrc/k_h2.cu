@@ -69,7 +69,11 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2
 //                  piece; __syncwarp orders the pieces), then the tile is
 //                  divided and written once with coalesced float4 stores -- no
 //                  global read-modify-write.
-__global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __restrict__ segs,
+// MULTI = false (every segment of the launch has one piece, e.g. a single
+// rank's payload): only the first path, compiled lean (<= 40 registers) so that
+// 12 CTAs = 48 warps per SM keep the zero-fill stores in flight.
+template <bool MULTI>
+__global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 12) h2_sparse_kernel(const SegH2* __restrict__ segs,
                                                                  const uint32_t* __restrict__ tile_seg,
                                                                  uint32_t ntiles,
                                                                  const unsigned char* const* __restrict__ pieces) {
@@ -132,7 +136,7 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
     }
     // the tile's entries of all pieces, in rank order: lane l takes the l-th
     uint32_t tot = 0, my_r = 0xFFFFFFFFu, my_i = 0;
-    if (np > 1) {
+    if (MULTI && np > 1) {
       for (uint32_t r = 0; r < np; ++r) {
         uint32_t a, b;
         range(r, &a, &b);
@@ -143,7 +147,7 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
         tot += b - a;
       }
     }
-    if (np > 1 && tot > 32) {
+    if (MULTI && np > 1 && tot > 32) {
       // shared-memory accumulation in rank order, one coalesced write
 #pragma unroll
       for (int i = lane * 4; i < kTile; i += 128)
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
       // the batch are loaded (all in flight) before the first is added; the
       // adds then run piece by piece in rank order (indices are distinct
       // within a piece, __syncwarp orders the pieces)
-      constexpr int kH2Batch = 8;
+      constexpr int kH2Batch = 4;
       for (uint32_t r0 = 0; r0 < np; r0 += kH2Batch) {
         uint32_t wi[kH2Batch];
         float wv[kH2Batch];
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse_kernel(const SegH2* __
     } else {
       for (uint32_t i = lane * 4; lo + i < hi; i += 128) store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
       __syncwarp();   // zero stores before the touched-word stores
-      if (np == 1) {
+      if (!MULTI || np == 1) {
         const unsigned char* pc = pieces[S.piece0];
         const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
         const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
@@ -262,8 +266,10 @@ constexpr int kSignLutBytes = (1 << kSignLutPieces) * 32 * 4;   // 32 KB
 __host__ __device__ constexpr size_t sign_h2_smem(int max_pieces) {
   return (size_t)(max_pieces < 1 ? 1 : max_pieces) * kSignWords * 4 + (max_pieces >= 2 ? kSignLutBytes : 0);
 }
+// 4 CTAs (32 warps) per SM: the output stream needs the stores of many warps
+// in flight (126 registers and 2 CTAs per SM measured 4.5 TB/s)
 template <int KIND>
-__global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restrict__ segs,
+__global__ void __launch_bounds__(kThreads, 4) h2_sign_kernel(const SegH2* __restrict__ segs,
                                                            const uint32_t* __restrict__ unit_seg,
                                                            uint32_t nunits,
                                                            const unsigned char* const* __restrict__ pieces,
@@ -281,9 +287,12 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
   const uint32_t u1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nunits / gridDim.x);
   uint32_t cur = 0xFFFFFFFFu;
   SegH2 S{};
-  uint4 pre[kSignPre];       // staged paths: the next unit's words (vector v = threadIdx.x + m * kThreads)
-  uint32_t wnext[kJ];        // one piece: the next unit's words
-  bool have = false;         // pre[] / wnext[] hold the words of unit gu
+  // the next unit's words in flight, one register buffer for both paths:
+  // staged paths: pre[m] = vector threadIdx.x + m * kThreads of the unit;
+  // one piece: word j of this thread = component j % 4 of pre[j / 4]
+  static_assert(kJ <= 4 * kSignPre, "one-piece words fit the prefetch buffer");
+  uint4 pre[kSignPre];
+  bool have = false;         // pre[] holds the words of unit gu
   uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
   auto load_vec = [&](uint32_t v, uint32_t w0, uint32_t nwords) -> uint4 {
     const uint32_t r = v / kSignVec, q = v % kSignVec;
@@ -328,18 +337,19 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
     float* out = seg_out(S);
     if (np == 1) {
       const uint32_t* w = sh_w[0];
+      auto comp = [](uint4& v, int c) -> uint32_t& { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; };
       uint32_t wd[kJ];
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
         const uint32_t e = e0 + j * kThreads * 4;
-        wd[j] = have ? wnext[j] : (e < n ? __ldg(w + (e >> 5)) : 0u);
+        wd[j] = have ? comp(pre[j / 4], j % 4) : (e < n ? __ldg(w + (e >> 5)) : 0u);
       }
       have = gu + 1 < u1 && sid_next == cur;   // prefetch the next unit of the segment
       if (have) {
 #pragma unroll
         for (int j = 0; j < kJ; ++j) {
           const uint32_t e = e0 + kSignUnit + j * kThreads * 4;
-          wnext[j] = e < n ? __ldg(w + (e >> 5)) : 0u;
+          comp(pre[j / 4], j % 4) = e < n ? __ldg(w + (e >> 5)) : 0u;
         }
       }
       const float sp = sh_sp[0], sn = sh_sn[0];
@@ -406,26 +416,20 @@ __global__ void __launch_bounds__(kThreads) h2_sign_kernel(const SegH2* __restri
       }
       continue;
     }
-    float4 acc[kJ];
-#pragma unroll
-    for (int j = 0; j < kJ; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t r = 0; r < np; ++r) {
-      const float sp = sh_sp[r], sn = sh_sn[r];
-      const uint32_t* wr = sh_words + r * kSignWords;
-#pragma unroll
-      for (int j = 0; j < kJ; ++j) {
-        const uint32_t l = lt + j * kThreads * 4;
-        const uint32_t nib = (wr[l >> 5] >> (l & 31)) & 0xFu;
-        acc[j].x = __fadd_rn(acc[j].x, (nib & 1) ? sp : sn);
-        acc[j].y = __fadd_rn(acc[j].y, (nib & 2) ? sp : sn);
-        acc[j].z = __fadd_rn(acc[j].z, (nib & 4) ? sp : sn);
-        acc[j].w = __fadd_rn(acc[j].w, (nib & 8) ? sp : sn);
-      }
-    }
-#pragma unroll
+    // more pieces: per float4, the pieces in rank order (the words are staged)
     for (int j = 0; j < kJ; ++j) {
+      const uint32_t l = lt + j * kThreads * 4;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t r = 0; r < np; ++r) {
+        const float sp = sh_sp[r], sn = sh_sn[r];
+        const uint32_t nib = (sh_words[r * kSignWords + (l >> 5)] >> (l & 31)) & 0xFu;
+        acc.x = __fadd_rn(acc.x, (nib & 1) ? sp : sn);
+        acc.y = __fadd_rn(acc.y, (nib & 2) ? sp : sn);
+        acc.z = __fadd_rn(acc.z, (nib & 4) ? sp : sn);
+        acc.w = __fadd_rn(acc.w, (nib & 8) ? sp : sn);
+      }
       const uint32_t e = e0 + j * kThreads * 4;
-      if (e < n) store4_guard(out, e, n, ones ? acc[j] : div(acc[j]));
+      if (e < n) store4_guard(out, e, n, ones ? acc : div(acc));
     }
   }
 }
@@ -479,19 +483,22 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
   if (ntiles == 0) return;
   launch_pdl(h2_sparse_offsets_kernel, njobs, kThreads, 0, st, segs, jobs, pieces);
   constexpr int kSmem = kTileThreads / 32 * kTile * (int)sizeof(float);
-  auto cap = [](int smem) {
+  auto cap = [](const void* fn, int smem) {
     int dev = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sparse_kernel, kTileThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTileThreads, smem);
     return sms * (per_sm > 0 ? per_sm : 8);
   };
-  static const int cap1 = cap(0), capn = cap(kSmem);
-  const int smem = max_pieces > 1 ? kSmem : 0;
-  const int grid_cap = max_pieces > 1 ? capn : cap1;
+  static const int cap1 = cap((const void*)h2_sparse_kernel<false>, 0);
+  static const int capn = cap((const void*)h2_sparse_kernel<true>, kSmem);
   const int need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);   // one warp per tile
-  const int grid = need < grid_cap ? need : grid_cap;
-  launch_pdl(h2_sparse_kernel, grid, kTileThreads, smem, st, segs, tile_seg, (uint32_t)ntiles, pieces);
+  if (max_pieces > 1)
+    launch_pdl(h2_sparse_kernel<true>, need < capn ? need : capn, kTileThreads, kSmem, st, segs, tile_seg,
+               (uint32_t)ntiles, pieces);
+  else
+    launch_pdl(h2_sparse_kernel<false>, need < cap1 ? need : cap1, kTileThreads, 0, st, segs, tile_seg,
+               (uint32_t)ntiles, pieces);
   count_launches(2);
 }
 

@@ -48,6 +48,49 @@ __global__ void __launch_bounds__(kPushThreads) push_kernel(const PushJob* __res
   }
 }
 
+// Multicast variant (NVLS, mcast.cu): every job's bytes are stored ONCE to
+// the multicast alias of the destination slot (the NVSwitch writes them into
+// every rank's copy), then one system-scope release + multicast reduction
+// bumps every rank's arrival counter at once.
+__global__ void __launch_bounds__(kPushThreads) push_mc_kernel(const PushJob* __restrict__ jobs,
+                                                               const unsigned char* __restrict__ src,
+                                                               unsigned char* mc_dst, unsigned long long* mc_cnt) {
+  const PushJob J = jobs[blockIdx.x];
+  const uint4* s = reinterpret_cast<const uint4*>(src + J.src_off);
+  unsigned char* d = mc_dst + J.dst_off;
+  const uint32_t nv = J.bytes / 16;
+  constexpr int kV = 8;
+  for (uint32_t e0 = 0; e0 < nv; e0 += kV * kPushThreads) {
+    uint4 v[kV];
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const uint32_t e = e0 + i * kPushThreads + threadIdx.x;
+      if (e < nv) v[i] = __ldcg(s + e);
+    }
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const uint32_t e = e0 + i * kPushThreads + threadIdx.x;
+      if (e < nv)   // a 128-bit store to the multicast alias (bits move unchanged)
+        asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d + 16ull * e),
+                     "f"(__uint_as_float(v[i].x)), "f"(__uint_as_float(v[i].y)), "f"(__uint_as_float(v[i].z)),
+                     "f"(__uint_as_float(v[i].w))
+                     : "memory");
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    asm volatile("multimem.red.release.sys.global.add.u64 [%0], %1;" ::"l"(mc_cnt), "l"(1ull) : "memory");
+  }
+}
+
+void launch_push_mc(const PushJob* jobs, int njobs, const unsigned char* src, unsigned char* mc_dst,
+                    unsigned long long* mc_cnt, cudaStream_t st) {
+  if (njobs == 0) return;
+  push_mc_kernel<<<njobs, kPushThreads, 0, st>>>(jobs, src, mc_dst, mc_cnt);
+  count_launches(1);
+}
+
 void launch_push(const PushJob* jobs, int njobs, const unsigned char* src, unsigned char* const* dsts,
                  unsigned long long* const* cnts, cudaStream_t st) {
   if (njobs == 0) return;

@@ -9,9 +9,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <unistd.h>
 
 #include "esp_internal.h"
 #include "esp_kernels.h"
+#include "mcast.h"
 
 namespace esp {
 
@@ -77,6 +79,13 @@ struct Bucket {
   PushJob* push1 = nullptr; int npush1 = 0;
   PushJob* push2 = nullptr; int npush2 = 0;
   uint64_t push1_bytes = 0, push2_bytes = 0, push2_odd_bytes = 0;   // bytes moved per call
+  // NVLS multicast (Allgather; mcast.cu): my slot's jobs once, to the
+  // multicast alias of every rank's receive buffer in the plan's region
+  bool mc = false;
+  PushJob* push1_mc = nullptr; int npush1_mc = 0;
+  unsigned char* mc_recv = nullptr;             // multicast alias of this bucket's [2][n][S] receive buffer
+  unsigned long long* mc_cnt = nullptr;         // multicast alias of the bucket's 4 counters
+  int npiece_ptrs = 0;                          // entries of h2_pieces (and h2_pieces_odd)
   // process-1 Gather/Broadcast: the root forwards all n payloads; its jobs read
   // from anywhere in its arena (own payload: send, the others: recv1 of the
   // call's parity), so there is one table per parity and src = arena base
@@ -129,6 +138,7 @@ struct Plan {
   bool needs_step = false;             // some kernel reads the step words (Randomk)
   std::vector<const float*> dyn_last;  // gradient pointers of the last upload
   bool peers_ready = false;             // fused buckets: peer arenas opened (first collective call)
+  std::unique_ptr<McRegion> mcr;        // NVLS multicast region of the plan's Allgather buckets
   std::vector<void*> peer_bases;        // IPC-opened arenas of the other ranks
   ~Plan() {
     for (void* pb : peer_bases)
@@ -170,7 +180,7 @@ struct HostTables {
   std::vector<const unsigned char*> a7_pieces, a7_pieces_odd, h2_pieces, h2_pieces_odd;
   std::vector<uint32_t> rankterms;
   std::vector<uint4> off_jobs;
-  std::vector<PushJob> push1, push2, push2_odd;
+  std::vector<PushJob> push1, push2, push2_odd, push1_mc;
 };
 
 static bool fused_allgather_enabled() {
@@ -326,6 +336,7 @@ static void layout_buffers(Layout& L, Bucket& b, HostTables& T) {
         case ESP_ALLGATHER:
           for (int d = 0; d < n; ++d)
             if (d != me) add_push(T.push1, 0, 0, S, d);
+          add_push(T.push1_mc, 0, 0, S, 0);   // multicast: my slot once (open_peers decides)
           b.target1 = (n - 1) * J;
           break;
         case ESP_ALLTOALL_ALLGATHER:
@@ -861,6 +872,9 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     up(TB.push1, b.push1);
     up(TB.push2, b.push2);
     up(TB.push2_odd, b.push2_odd);
+    up(TB.push1_mc, b.push1_mc);
+    b.npush1_mc = (int)TB.push1_mc.size();
+    b.npiece_ptrs = (int)TB.h2_pieces.size();
     b.npush1 = (int)TB.push1.size();
     b.npush2 = (int)TB.push2.size();
     b.push1_bytes = b.push2_bytes = b.push2_odd_bytes = 0;
@@ -920,6 +934,70 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
 // destination / counter tables.
 static void build_peer_tables(Plan& p, const std::vector<unsigned char*>& base);
 
+// NVLS multicast for the plan's fused Allgather buckets (mcast.cu), decided
+// collectively: every rank must support it and the world's mode must ask for
+// it (auto: n >= 3, where one multicast store beats n - 1 unicast copies out
+// of the sender's links; measured slower than one unicast copy at n = 2).
+// The buckets' receive buffers and arrival counters move into the region
+// (identical layout on every rank); h2's piece pointers are re-pointed there.
+static void open_multicast(Plan& p, cudaStream_t st) {
+  esp_world_s* w = p.w;
+  const int n = w->nranks;
+  const bool want = w->mc_mode == 1 || (w->mc_mode < 0 && n >= 3);
+  bool any = false;
+  for (const Bucket& b : p.buckets) any |= b.fused && b.routine == ESP_ALLGATHER;
+  if (!want || !any || w->loopback) return;
+  // every rank's verdict and rank 0's rendezvous token
+  struct Info { uint64_t token; int32_t ok; int32_t pad; };
+  Info mine{0, multicast_supported(w->dev) ? 1 : 0, 0};
+  if (w->rank == 0) mine.token = host_splitmix64((uint64_t)getpid() * 0x9E3779B97F4A7C15ull ^ (uint64_t)(uintptr_t)&p);
+  Info* d = nullptr;
+  ESP_CUDA(cudaMalloc(&d, sizeof(Info) * (n + 1)));
+  ESP_CUDA(cudaMemcpy(d + n, &mine, sizeof(Info), cudaMemcpyHostToDevice));
+  ESP_NCCL(ncclAllGather(d + n, d, sizeof(Info), ncclUint8, w->comm, st));
+  std::vector<Info> all(n);
+  ESP_CUDA(cudaStreamSynchronize(st));
+  ESP_CUDA(cudaMemcpy(all.data(), d, sizeof(Info) * n, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  for (const Info& i : all)
+    if (!i.ok) return;   // one rank without multicast: unicast pushes everywhere
+  // region layout: per Allgather bucket [2 parities][n slots][S] then 4 counters
+  std::vector<size_t> off(p.buckets.size(), 0);
+  size_t cursor = 0;
+  for (size_t i = 0; i < p.buckets.size(); ++i) {
+    const Bucket& b = p.buckets[i];
+    if (!(b.fused && b.routine == ESP_ALLGATHER)) continue;
+    off[i] = round_up(cursor, 256);
+    cursor = off[i] + round_up(2ull * n * b.slot, 256) + 256;
+  }
+  p.mcr.reset(mcast_create(w, cursor, all[0].token, w->mc_seq++, st));
+  unsigned char* uc = reinterpret_cast<unsigned char*>(p.mcr->uc_va);
+  unsigned char* mcv = reinterpret_cast<unsigned char*>(p.mcr->mc_va);
+  for (size_t i = 0; i < p.buckets.size(); ++i) {
+    Bucket& b = p.buckets[i];
+    if (!(b.fused && b.routine == ESP_ALLGATHER)) continue;
+    const size_t recv_bytes = 2ull * n * b.slot;
+    const size_t cnt_off = off[i] + round_up(recv_bytes, 256);
+    // h2 reads the pieces from this rank's copy of the region
+    auto repoint = [&](const unsigned char** dev_arr) {
+      if (!dev_arr || b.npiece_ptrs == 0) return;
+      std::vector<const unsigned char*> h(b.npiece_ptrs);
+      ESP_CUDA(cudaMemcpy(h.data(), dev_arr, sizeof(void*) * h.size(), cudaMemcpyDeviceToHost));
+      for (auto& q : h)
+        if (q >= b.recv1.base && q < b.recv1.base + recv_bytes) q = uc + off[i] + (q - b.recv1.base);
+      ESP_CUDA(cudaMemcpy(dev_arr, h.data(), sizeof(void*) * h.size(), cudaMemcpyHostToDevice));
+    };
+    repoint(b.h2_pieces);
+    repoint(b.h2_pieces_odd);
+    b.recv1.base = uc + off[i];
+    b.my_cnt = reinterpret_cast<unsigned long long*>(uc + cnt_off);
+    b.mc_recv = mcv + off[i];
+    b.mc_cnt = reinterpret_cast<unsigned long long*>(mcv + cnt_off);
+    b.target1 = (uint64_t)n * b.npush1_mc;   // every rank's jobs bump every counter, mine included
+    b.mc = true;
+  }
+}
+
 static void open_peers(Plan& p, cudaStream_t st) {
   esp_world_s* w = p.w;
   const int n = w->nranks;
@@ -946,6 +1024,7 @@ static void open_peers(Plan& p, cudaStream_t st) {
     }
   }
   build_peer_tables(p, base);
+  open_multicast(p, st);
 }
 
 // destination / counter tables of every fused bucket from the n arena bases
@@ -1230,8 +1309,14 @@ static void fused_stage(Plan& p, Bucket& b, int stage, cudaStream_t cs, cudaEven
     dbg("wait", cs);
   };
   if (stage == 1) {
-    launch_push(b.push1, b.npush1, b.send.at(0), b.dsts + par * n, b.cnts + par * n, cs);
-    w->counters[0].pushed += b.push1_bytes;
+    if (b.mc) {   // one multicast store of my slot into every rank's receive buffer
+      launch_push_mc(b.push1_mc, b.npush1_mc, b.send.at(0), b.mc_recv + (size_t)par * n * S + (size_t)w->rank * S,
+                     b.mc_cnt + par, cs);
+      w->counters[0].pushed += S;
+    } else {
+      launch_push(b.push1, b.npush1, b.send.at(0), b.dsts + par * n, b.cnts + par * n, cs);
+      w->counters[0].pushed += b.push1_bytes;
+    }
     dbg("push phase 1", cs);
     return;
   }

@@ -410,6 +410,15 @@ esp_status_t esp_world_set_plan_cache(esp_world_t w, int max_plans) {
   ESP_API_END
 }
 
+esp_status_t esp_world_set_multicast(esp_world_t w, int mode) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(w && mode >= -1 && mode <= 1, ESP_ERR_INVALID_ARG, "mode must be -1, 0 or 1");
+  cudaSetDevice(w->dev);
+  clear_plans(w);
+  w->mc_mode = mode;
+  ESP_API_END
+}
+
 esp_status_t esp_world_drop_plans(esp_world_t w) {
   ESP_API_BEGIN
   ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");

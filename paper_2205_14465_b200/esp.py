@@ -27,7 +27,7 @@ SYMBOLS = (
     "esp_world_check", "esp_world_info", "esp_world_counters", "esp_world_counters_local",
     "esp_world_reset_counters", "esp_world_set_timing", "esp_last_timing", "esp_world_set_bucket_elems",
     "esp_world_set_probe", "esp_probe_read", "esp_world_set_timeout", "esp_world_set_plan_cache",
-    "esp_world_drop_plans", "esp_world_create_loopback", "esp_sync_many_loopback",
+    "esp_world_drop_plans", "esp_world_set_multicast", "esp_world_create_loopback", "esp_sync_many_loopback",
     "esp_ctx_create", "esp_ctx_destroy", "esp_ctx_payload_bytes", "esp_ctx_get_state",
     "esp_ctx_set_state", "esp_ctx_get_momentum", "esp_ctx_set_momentum", "esp_compress", "esp_decompress", "esp_sync", "esp_sync_many",
     "esp_compressed_bytes", "esp_wire_bytes", "esp_model_time", "esp_status_string",
@@ -89,7 +89,7 @@ def lib():
             "esp_last_timing": [vp, C.POINTER(Timing)], "esp_world_set_bucket_elems": [vp, u64],
             "esp_world_set_probe": [vp, i32],
             "esp_world_set_timeout": [vp, dbl], "esp_world_set_plan_cache": [vp, i32],
-            "esp_world_drop_plans": [vp],
+            "esp_world_drop_plans": [vp], "esp_world_set_multicast": [vp, i32],
             "esp_world_create_loopback": [i32, i32, C.POINTER(vp)],
             "esp_sync_many_loopback": [C.POINTER(vp), i32, C.POINTER(vp), C.POINTER(vp), i32, vp],
             "esp_probe_read": [vp, C.POINTER(dbl), C.POINTER(u64), C.POINTER(u64)],
@@ -292,6 +292,11 @@ class World:
 
     def drop_plans(self):
         _check(lib().esp_world_drop_plans(self.h))
+
+    def set_multicast(self, mode: int):
+        """-1 auto (n >= 3), 0 off, 1 on when every GPU supports NVLS multicast."""
+        self._last_many = None
+        _check(lib().esp_world_set_multicast(self.h, int(mode)))
 
     def destroy(self):
         self._last_many = None

@@ -155,10 +155,48 @@ def main():
     w.destroy()
 
     if n > 1:
+        multicast_allgather(rank, local, n)
         missing_peer(rank, local)
     dist.barrier()
     dist.destroy_process_group()
     print(f"rank {rank}: {checked} pair-steps + sync_many ok", flush=True)
+
+
+def multicast_allgather(rank, local, n):
+    """NVLS multicast forced on (esp_world_set_multicast(1); unicast peer copies
+    wherever a GPU lacks it): every Allgather compressor in one esp_sync_many,
+    4 back-to-back steps (both call parities twice), bit-exact against the
+    oracle; with multicast a rank stores its slot once ("pushed" = the slot,
+    not (n-1) slots)."""
+    w = E.World.nccl(local)
+    w.set_multicast(1)
+    specs = [("dgc", 40_000, {}), ("topk", 3000, {}), ("randomk", 20_000, {"shared_indices": False}),
+             ("efsignsgd", 9000, {}), ("onebit", 5000, {}), ("dgc", 77, {"approx": True})]
+    ctxs = [E.Ctx(w, k, "allgather", N_, tensor_id=500 + i, ratio=0.01, **ex) for i, (k, N_, ex) in enumerate(specs)]
+    cfgs = [O.Cfg(k, 0.01, shared_indices=ex.get("shared_indices", True), approx=ex.get("approx", False))
+            for (k, N_, ex) in specs]
+    sts = [O.new_states(n, N_, "allgather", cfgs[i]) for i, (k, N_, _) in enumerate(specs)]
+    T = 4
+    allg = [[[gradient(N_, step=s, rank=q, tensor=500 + i) for q in range(n)] for i, (_, N_, _) in enumerate(specs)]
+            for s in range(T)]
+    dev = [[torch.from_numpy(allg[s][i][rank].copy()).cuda() for i in range(len(specs))] for s in range(T)]
+    torch.cuda.synchronize()
+    w.reset_counters()
+    for s in range(T):
+        for i, (k, _, _) in enumerate(specs):
+            if k in O.QUANTIZED and s > 0:   # lock-step from the oracle (after the previous call completed)
+                torch.cuda.synchronize()
+                ctxs[i].set_state(sts[i][rank].step, sts[i][rank].r[None])
+        E.esp_sync_many(w, ctxs, dev[s])
+        torch.cuda.synchronize()
+        for i, (k, _, _) in enumerate(specs):
+            ref = O.sync("allgather", cfgs[i], allg[s][i], sts[i], tensor_id=500 + i)
+            check(k, "allgather", dev[s][i].cpu().numpy(), ref.outs[rank], allg[s][i], f"multicast {k} step {s}")
+    c = w.counters()
+    slot = sum(x.payload_bytes for x in ctxs)
+    print(f"rank {rank}: multicast allgather ok, pushed {c['pushed'] / T:.0f} B/step, slot ~{slot} B", flush=True)
+    w.check()
+    w.destroy()
 
 
 def missing_peer(rank, local):

@@ -26,9 +26,10 @@ def test_nccl_world_parity(nproc):
     assert r.stdout.count("sync_many ok") == nproc
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
+@pytest.mark.parametrize("nproc", [1, 2, 4])
 def test_ddp_comm_hook(nproc):
-    """NEXT-4: the libesp DDP communication hook (paper_2205_14465_b200/ddp.py)."""
+    """NEXT-4: the libesp DDP communication hook (paper_2205_14465_b200/ddp.py);
+    one rank on a 1-GPU box (DDP still runs its reducer and the hook)."""
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs, found {torch.cuda.device_count()}")
     import __graft_entry__
