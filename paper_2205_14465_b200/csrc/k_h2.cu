@@ -81,8 +81,7 @@ __global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 12) h2_sparse_kernel
   pdl_trigger();
   constexpr int kWarps = kTileThreads / 32;
   constexpr unsigned kFull = 0xffffffffu;
-  // the per-warp accumulation tiles (dynamic: absent when every segment of the
-  // launch has a single piece, so that case keeps its full occupancy)
+  // the per-warp 4 KB output tiles (dynamic shared memory)
   extern __shared__ __align__(16) float acc_all[];
   const int lane = threadIdx.x & 31;
   float* acc = acc_all + (threadIdx.x >> 5) * kTile;
@@ -192,20 +191,36 @@ __global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 12) h2_sparse_kernel
         if (!ones) v = div(v);
         store4_guard(out, lo + i, S.n, v);
       }
+    } else if (!MULTI || np == 1) {
+      // one piece: a tile with entries is assembled in the warp's shared tile
+      // (+0, then (+0 + v) / d at each entry) and written once with full-line
+      // stores, so no 4-byte store lands on a line after its zero fill; an
+      // empty tile is zero-filled straight from registers
+      const unsigned char* pc = pieces[S.piece0];
+      const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
+      const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
+      uint32_t a, b;
+      range(0, &a, &b);
+      if (b > a) {
+#pragma unroll
+        for (int i = lane * 4; i < kTile; i += 128)
+          *reinterpret_cast<float4*>(acc + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
+        for (uint32_t i = a + lane; i < b; i += 32) {
+          const float v = __fadd_rn(0.f, __ldg(val + i));   // +0 + v: the oracle's sum from +0
+          acc[__ldg(idx + i) - lo] = ones ? v : div(v);
+        }
+        __syncwarp();
+        for (uint32_t i = lane * 4; lo + i < hi; i += 128)
+          store4_guard(out, lo + i, S.n, *reinterpret_cast<const float4*>(acc + i));
+      } else {
+        for (uint32_t i = lane * 4; lo + i < hi; i += 128)
+          store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
+      }
     } else {
       for (uint32_t i = lane * 4; lo + i < hi; i += 128) store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
       __syncwarp();   // zero stores before the touched-word stores
-      if (!MULTI || np == 1) {
-        const unsigned char* pc = pieces[S.piece0];
-        const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
-        const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
-        uint32_t a, b;
-        range(0, &a, &b);
-        for (uint32_t i = a + lane; i < b; i += 32) {
-          const float v = __fadd_rn(0.f, __ldg(val + i));   // +0 + v: the oracle's sum from +0
-          out[__ldg(idx + i)] = ones ? v : div(v);
-        }
-      } else {
+      {
         // one entry per lane: lanes holding the same index form a group
         // (__match_any_sync), whose lowest lane sums it in lane = rank order
         // from +0 and stores it once -- no read-modify-write round trips
@@ -490,14 +505,14 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTileThreads, smem);
     return sms * (per_sm > 0 ? per_sm : 8);
   };
-  static const int cap1 = cap((const void*)h2_sparse_kernel<false>, 0);
+  static const int cap1 = cap((const void*)h2_sparse_kernel<false>, kSmem);
   static const int capn = cap((const void*)h2_sparse_kernel<true>, kSmem);
   const int need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);   // one warp per tile
   if (max_pieces > 1)
     launch_pdl(h2_sparse_kernel<true>, need < capn ? need : capn, kTileThreads, kSmem, st, segs, tile_seg,
                (uint32_t)ntiles, pieces);
   else
-    launch_pdl(h2_sparse_kernel<false>, need < cap1 ? need : cap1, kTileThreads, 0, st, segs, tile_seg,
+    launch_pdl(h2_sparse_kernel<false>, need < cap1 ? need : cap1, kTileThreads, kSmem, st, segs, tile_seg,
                (uint32_t)ntiles, pieces);
   count_launches(2);
 }

@@ -219,6 +219,7 @@ McRegion* mcast_create(esp_world_s* w, size_t bytes, uint64_t token, uint32_t se
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = w->dev;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;   // as the multicast object's
   ESP_CU(d.memCreate(&r->phys, r->size, &ap, 0));
   r->have_phys = true;
   ESP_CU(d.multicastBindMem(r->mc, 0, r->phys, 0, r->size, 0));
