@@ -761,3 +761,79 @@ def select_option(options, numel: int, n: int, B: float):
         if best < 0 or t < bt:
             best, bt = i, t
     return best, bt
+
+
+# --------------------------------------------------------------------------
+# hierarchical communication (P:722-728 three phases,
+# P:1085-1091 "only considers division schemes for intra-machine
+# communications in hierarchical communication"; reading R23): n = m machines
+# x g GPUs, rank r = machine r // g, local index r % g
+# --------------------------------------------------------------------------
+def hier_shard_tensor_id(tensor_id: int, shard: int) -> int:
+    """R23: the inter-machine sync of shard i is its own tensor for the
+    compressors' counter-based draws: id = tensor_id * 4096 + i."""
+    return tensor_id * 4096 + shard
+
+
+def new_states_hier(n: int, numel: int, routine: str, cfg: Cfg, g: int):
+    """Rank (a, i) keeps the EF state of shard i as rank a of the m-rank
+    inter-machine sync of that shard."""
+    m = n // g
+    shards = partitions(numel, g)
+    return [new_states(m, shards[r % g][1] - shards[r % g][0], routine, cfg)[r // g] for r in range(n)]
+
+
+def sync_hierarchical(routine: str, cfg: Cfg, grads, states, g: int, tensor_id: int = 0) -> SyncResult:
+    """Three phases: (1) intra-machine Reduce-scatter of the
+    uncompressed tensor -- shard i (R10 partitions into g parts) of machine a
+    = rank-order fp32 mean over its g GPUs (SUM: the sum); (2) inter-machine:
+    the m GPUs holding shard i run the compressed routine on it (any process;
+    compression, EF and aggregation as in sync(), mean over the m machines);
+    (3) intra-machine Allgather of the g shards.  The result is the mean of
+    the machines' means."""
+    n = len(grads)
+    if g < 1 or n % g:
+        raise ValueError("g must divide n")
+    m = n // g
+    N = grads[0].size
+    if cfg.kind == "none" or not legal(cfg, routine) or routine not in ("allgather", "alltoall_allgather",
+                                                                          "gather_broadcast"):
+        raise ValueError(f"hierarchical sync of {cfg.kind}/{routine}")
+    shards = partitions(N, g)
+    cnt = [Counters() for _ in range(n)]
+    # (1) intra-machine reduce-scatter (uncompressed): 4 (g-1)/g N bytes per rank
+    mid = {}
+    for a in range(m):
+        for i, (lo, hi) in enumerate(shards):
+            mid[a, i] = aggregate([grads[a * g + j][lo:hi].astype(np.float32) for j in range(g)], cfg.reduce, g) \
+                if hi > lo else np.zeros(0, np.float32)
+    for r in range(n):
+        rs = sum(4 * (hi - lo) for j, (lo, hi) in enumerate(shards) if j != r % g)
+        cnt[r].comm("intra_reducescatter", rs, 4 * (shards[r % g][1] - shards[r % g][0]) * (g - 1))
+    # (2) inter-machine compressed sync of each shard
+    final = {}
+    for i, (lo, hi) in enumerate(shards):
+        if hi == lo:
+            for a in range(m):
+                final[a, i] = np.zeros(0, np.float32)
+            continue
+        res = sync(routine, cfg, [mid[a, i] for a in range(m)], [states[a * g + i] for a in range(m)],
+                   tensor_id=hier_shard_tensor_id(tensor_id, i))
+        for a in range(m):
+            final[a, i] = res.outs[a]
+            c = res.counters[a]
+            r = a * g + i
+            cnt[r].h1 += c.h1
+            cnt[r].h2 += c.h2
+            cnt[r].comm("inter_" + routine, c.sent, c.recv)
+    # (3) intra-machine allgather of the shards
+    outs = []
+    for r in range(n):
+        a, i = divmod(r, g)
+        out = np.zeros(N, np.float32)
+        for j, (lo, hi) in enumerate(shards):
+            out[lo:hi] = final[a, j]
+        outs.append(out)
+        mine = 4 * (shards[i][1] - shards[i][0])
+        cnt[r].comm("intra_allgather", mine * (g - 1), sum(4 * (hi - lo) for j, (lo, hi) in enumerate(shards) if j != i))
+    return SyncResult(outs, [None] * n, [None] * n, cnt)

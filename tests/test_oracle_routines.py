@@ -367,3 +367,85 @@ def test_quantized_a7_closed_form_with_nonzero_r2(kind, routine):
         assert np.array_equal(res.outs[0][lo:hi], want), (j, kind, routine)
         want_r2 = np.array([float(x) for x in q], np.float32) - want
         assert np.array_equal(st[j].r2, want_r2.astype(np.float32))
+
+
+# ---- hierarchical communication (reading R23) ------
+HIER = [("dgc", "allgather"), ("dgc", "alltoall_allgather"), ("randomk", "gather_broadcast"),
+        ("efsignsgd", "alltoall_allgather"), ("onebit", "allgather"), ("topk", "gather_broadcast")]
+
+
+@pytest.mark.parametrize("kind,routine", HIER)
+def test_hier_one_gpu_per_machine_is_flat(kind, routine):
+    """g = 1: the intra-machine phases are identities and the inter-machine
+    phase is the flat routine over all n ranks (flat = one phase)."""
+    n, N = 4, 3001
+    cfg = O.Cfg(kind, 0.02)
+    grads = _grads(n, N)
+    h = O.sync_hierarchical(routine, cfg, grads, O.new_states_hier(n, N, routine, cfg, 1), 1, tensor_id=5)
+    f = O.sync(routine, cfg, grads, O.new_states(n, N, routine, cfg), tensor_id=O.hier_shard_tensor_id(5, 0))
+    for r in range(n):
+        assert np.array_equal(h.outs[r], f.outs[r])
+
+
+@pytest.mark.parametrize("n,g", [(4, 2), (8, 4), (8, 2), (6, 3), (4, 4)])
+@pytest.mark.parametrize("kind", ["dgc", "randomk"])
+def test_hier_rho1_is_the_global_mean(n, g, kind):
+    """rho = 1: nothing is dropped, so after the three phases every rank holds
+    the mean of all n gradients (mean of the machines' means), within the
+    fp32 rounding of two averaging stages -- pins which shard goes where."""
+    N = 2999
+    cfg = O.Cfg(kind, 1.0)
+    grads = _grads(n, N, dist="D2")
+    res = O.sync_hierarchical("allgather", cfg, grads, O.new_states_hier(n, N, "allgather", cfg, g), g)
+    x = np.stack([gg.astype(np.float64) for gg in grads])
+    exact, scale = x.mean(0), np.abs(x).mean(0)
+    for r in range(n):
+        assert np.all(np.abs(res.outs[r].astype(np.float64) - exact) <= 4e-7 * scale + 1e-38)
+
+
+@pytest.mark.parametrize("kind,routine", HIER)
+@pytest.mark.parametrize("n,g", [(4, 2), (8, 4)])
+def test_hier_bytes_closed_form(kind, routine, n, g):
+    """Per rank: the intra Reduce-scatter and Allgather each receive the other
+    g-1 shards (4 (g-1) N / g bytes up to partition rounding), and the
+    inter-machine phase moves the cost-table volume of the routine for the
+    shard's payload over m = n / g ranks."""
+    N = 8192
+    cfg = O.Cfg(kind, 0.02)
+    res = O.sync_hierarchical(routine, cfg, _grads(n, N), O.new_states_hier(n, N, routine, cfg, g), g)
+    m = n // g
+    L = O.partitions(N, g)[0][1]
+    P = O.nparts_of(routine, m)
+    M = O.chunk_bytes(cfg, L, P) * P
+    row = O.table_row(cfg, routine)
+    c = res.counters[0]   # rank (0, 0): root of its inter group
+    ph = {name: (s, rcv) for name, s, rcv in c.phases}
+    assert ph["intra_reducescatter"][1] == 4 * L * (g - 1)
+    assert ph["intra_allgather"][1] == 4 * (N - L)
+    inter_recv = ph["inter_" + routine][1]
+    if routine != "gather_broadcast":
+        assert inter_recv == pytest.approx(O.table_comm_bytes(row, M, m), abs=m)
+
+
+@pytest.mark.parametrize("kind", ["dgc", "randomk"])
+def test_hier_ef_telescopes(kind):
+    """Error feedback lives per (machine, shard): over T steps the output plus
+    the machines' mean residual of each shard equals the sum of the global
+    mean gradients (within fp32 rounding)."""
+    n, g, N, T = 8, 4, 4000, 5
+    cfg = O.Cfg(kind, 0.05, shared_indices=False)
+    st = O.new_states_hier(n, N, "allgather", cfg, g)
+    s_out, s_g = np.zeros(N), np.zeros(N)
+    mag = 0.0
+    for t in range(T):
+        grads = [gradient(N, rank=r, step=t) for r in range(n)]
+        res = O.sync_hierarchical("allgather", cfg, grads, st, g)
+        s_out += res.outs[0].astype(np.float64)
+        s_g += sum(gg.astype(np.float64) for gg in grads) / n
+        mag = max(mag, max(float(np.abs(gg).max()) for gg in grads))
+    resid = np.zeros(N)
+    for i, (lo, hi) in enumerate(O.partitions(N, g)):
+        resid[lo:hi] = sum(st[a * g + i].r.astype(np.float64) for a in range(n // g)) / (n // g)
+    tol = 16 * T * float(np.spacing(np.float32(4 * mag)))
+    assert np.max(np.abs(s_out + resid - s_g)) <= tol
+    assert np.abs(resid).max() > 100 * tol
