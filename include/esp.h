@@ -170,6 +170,22 @@ esp_status_t esp_world_create_sim(int nranks, int cuda_dev, esp_world_t* out);
  * a later one).  NCCL-reduced buckets (NONE, Randomk Allreduce) are
  * ESP_ERR_UNSUPPORTED here.  Each world is destroyed with esp_world_destroy. */
 esp_status_t esp_world_create_loopback(int nranks, int cuda_dev, esp_world_t* out /* [nranks] */);
+/* Hierarchical communication (aggregate within each machine, then
+ * across machines, then within each machine again; SURVEY.md 8f NEXT-4,
+ * reading R23).  The parent's n ranks form m = n / group "machines" of group
+ * consecutive ranks (emulated on one NVLink box).  On the returned world a
+ * ctx (compressed kinds; routine = the inter-machine routine: ALLGATHER,
+ * ALLTOALL_ALLGATHER or GATHER_BROADCAST) synchronises its tensor in three
+ * phases: an uncompressed intra-machine Reduce-scatter into group shards
+ * (R10 partitions; shard i on local rank i, the machine's mean for MEAN), the
+ * compressed inter-machine routine of each shard among the m ranks holding
+ * it (error feedback per rank and shard), and an intra-machine Allgather of
+ * the shards.  The parent stays the caller's; esp_world_create_hier is
+ * collective over it (two ncclCommSplit).  esp_world_create_loopback_hier:
+ * the same as a loopback group on one GPU (tests; esp_sync_many_loopback).
+ * ctx state (get/set_state) is that of the rank's shard. */
+esp_status_t esp_world_create_hier(esp_world_t parent, int group, esp_world_t* out);
+esp_status_t esp_world_create_loopback_hier(int nranks, int group, int cuda_dev, esp_world_t* out /* [nranks] */);
 esp_status_t esp_world_destroy(esp_world_t w);
 esp_status_t esp_world_check(esp_world_t w);   /* async CUDA/NCCL errors */
 esp_status_t esp_world_info(esp_world_t w, int* nranks, int* rank, int* nlocal);

@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libesp.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["world.cu", "ctx.cu", "plan.cu", "mcast.cu", "k_dgc.cu", "k_sign.cu", "k_randomk.cu", "k_h2.cu",
+SOURCES = ["world.cu", "ctx.cu", "plan.cu", "hier.cu", "mcast.cu", "k_dgc.cu", "k_sign.cu", "k_randomk.cu", "k_h2.cu",
            "k_push.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

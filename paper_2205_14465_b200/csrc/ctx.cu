@@ -65,6 +65,33 @@ esp_status_t esp_ctx_create(esp_world_t w, const esp_compressor_cfg_t* cfg, int 
   ESP_REQUIRE(pair_legal(*cfg, routine), ESP_ERR_UNSUPPORTED,
               "illegal (compressor, routine) pair (P:1064-1065, P:1073)");
   ESP_CUDA(cudaSetDevice(w->dev));
+  if (w->hier_g > 0) {
+    // hierarchical world (R23): the tensor's state is that of this rank's
+    // shard, a ctx of the inter-machine world (tensor id * 4096 + shard)
+    ESP_REQUIRE(cfg->kind != ESP_NONE && routine != ESP_ALLREDUCE, ESP_ERR_UNSUPPORTED,
+                "hierarchical sync compresses the inter-machine phase: a compressed kind with Allgather, "
+                "Alltoall/Allgather or Gather/Broadcast");
+    const int g = w->hier_g, i = w->rank % g;
+    const uint64_t L = partition_len(numel, g);
+    const uint64_t lo = g == 1 ? 0 : std::min<uint64_t>(numel, (uint64_t)i * L);
+    const uint64_t hi = g == 1 ? numel : std::min<uint64_t>(numel, lo + L);
+    auto c = std::make_unique<esp_ctx_s>();
+    c->w = w;
+    c->cfg = *cfg;
+    c->routine = routine;
+    c->tensor_id = tensor_id;
+    c->N = numel;
+    if (hi > lo) {
+      esp_ctx_t in = nullptr;
+      const esp_status_t s = esp_ctx_create(w->inter, cfg, routine, tensor_id * 4096 + (uint64_t)i, hi - lo, &in);
+      if (s != ESP_OK) return s;
+      c->inner = in;
+      c->payload_bytes = in->payload_bytes;
+    }
+    w->ctxs.insert(c.get());
+    *out = c.release();
+    return ESP_OK;
+  }
   auto c = std::make_unique<esp_ctx_s>();
   c->w = w;
   c->cfg = *cfg;
@@ -113,7 +140,9 @@ esp_status_t esp_ctx_destroy(esp_ctx_t c) {
   ESP_REQUIRE(c, ESP_ERR_INVALID_ARG, "ctx is NULL");
   cudaSetDevice(c->w->dev);
   drop_plans_with(c->w, c);
+  drop_hier_plans_with(c->w, c);
   cudaDeviceSynchronize();
+  if (c->inner) esp_ctx_destroy(c->inner);
   cudaFree(c->r);
   cudaFree(c->lazy);
   cudaFree(c->r2);
@@ -145,6 +174,10 @@ static uint64_t r2_valid(esp_ctx_t c, int lr) {
 esp_status_t esp_ctx_get_state(esp_ctx_t c, void* host_buf, size_t* nbytes) {
   ESP_API_BEGIN
   ESP_REQUIRE(c && nbytes, ESP_ERR_INVALID_ARG, "null argument");
+  if (c->w->hier_g > 0) {   // the rank's shard
+    ESP_REQUIRE(c->inner, ESP_ERR_STATE, "this rank's shard of the tensor is empty");
+    return esp_ctx_get_state(c->inner, host_buf, nbytes);
+  }
   const int nl = c->w->nlocal;
   const size_t need = sizeof(StateHeader) + (size_t)nl * 4 * (c->N + c->r2_len);
   if (!host_buf) {
@@ -192,6 +225,10 @@ esp_status_t esp_ctx_get_state(esp_ctx_t c, void* host_buf, size_t* nbytes) {
 esp_status_t esp_ctx_set_state(esp_ctx_t c, const void* host_buf, size_t nbytes) {
   ESP_API_BEGIN
   ESP_REQUIRE(c && host_buf, ESP_ERR_INVALID_ARG, "null argument");
+  if (c->w->hier_g > 0) {
+    ESP_REQUIRE(c->inner, ESP_ERR_STATE, "this rank's shard of the tensor is empty");
+    return esp_ctx_set_state(c->inner, host_buf, nbytes);
+  }
   StateHeader h;
   ESP_REQUIRE(nbytes >= sizeof(h), ESP_ERR_INVALID_ARG, "state blob too small");
   std::memcpy(&h, host_buf, sizeof(h));
@@ -242,6 +279,7 @@ esp_status_t esp_compress(esp_ctx_t c, const float* grad, void* payload, void* s
   check_ptr16(grad, "grad");
   check_ptr16(payload, "payload");
   ESP_REQUIRE(c->cfg.kind != ESP_NONE, ESP_ERR_UNSUPPORTED, "NONE has no compressed payload");
+  ESP_REQUIRE(c->w->hier_g == 0, ESP_ERR_UNSUPPORTED, "h1 of a hierarchical ctx: use its shard's world");
   ESP_CUDA(cudaSetDevice(c->w->dev));
   execute_compress(get_plan(c->w, {c}), grad, payload, as_stream(stream));
   ESP_API_END
@@ -252,6 +290,7 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
   ESP_REQUIRE(c && pieces && npieces >= 1 && npieces <= 64, ESP_ERR_INVALID_ARG, "bad argument");
   check_ptr16(out, "out");
   ESP_REQUIRE(c->cfg.kind != ESP_NONE, ESP_ERR_UNSUPPORTED, "NONE has no compressed payload");
+  ESP_REQUIRE(c->w->hier_g == 0, ESP_ERR_UNSUPPORTED, "h2 of a hierarchical ctx: use its shard's world");
   for (int i = 0; i < npieces; ++i) check_ptr16(pieces[i], "piece");
   ESP_CUDA(cudaSetDevice(c->w->dev));
   cudaStream_t st = as_stream(stream);
@@ -405,6 +444,10 @@ esp_status_t esp_sync_many(esp_world_t w, const esp_ctx_t* ctxs, float* const* g
     }
   }
   ESP_CUDA(cudaSetDevice(w->dev));
+  if (w->hier_g > 0) {
+    execute_hier(w, v, grads, as_stream(stream));
+    return ESP_OK;
+  }
   if (!p) p = get_plan(w, v);
   execute_plan(p, grads, as_stream(stream));
   ESP_API_END
@@ -427,8 +470,16 @@ esp_status_t esp_sync_many_loopback(const esp_world_t* worlds, int nranks, const
       check_ptr4(grads[(size_t)r * ntensors + i], "grad");
     }
     ESP_CUDA(cudaSetDevice(w->dev));
-    plans[r] = get_plan(w, v);
     gr[r] = grads + (size_t)r * ntensors;
+    if (worlds[0]->hier_g > 0) continue;
+    plans[r] = get_plan(w, v);
+  }
+  if (worlds[0]->hier_g > 0) {
+    std::vector<esp_world_s*> ws(worlds, worlds + nranks);
+    std::vector<std::vector<esp_ctx_s*>> cs(nranks);
+    for (int r = 0; r < nranks; ++r) cs[r].assign(ctxs + (size_t)r * ntensors, ctxs + (size_t)(r + 1) * ntensors);
+    execute_hier_loopback(ws, cs, gr, as_stream(stream));
+    return ESP_OK;
   }
   execute_loopback(plans, gr, as_stream(stream));
   ESP_API_END
@@ -441,6 +492,10 @@ esp_status_t esp_sync(esp_world_t w, esp_ctx_t c, float* grad_inout, void* strea
   ESP_REQUIRE(c->w == w, ESP_ERR_STATE, "ctx belongs to another world");
   check_ptr4(grad_inout, "grad");
   ESP_CUDA(cudaSetDevice(w->dev));
+  if (w->hier_g > 0) {
+    execute_hier(w, {c}, &grad_inout, as_stream(stream));
+    return ESP_OK;
+  }
   execute_plan(get_plan(w, {c}), &grad_inout, as_stream(stream));
   ESP_API_END
 }

@@ -79,6 +79,7 @@ struct Arena {
 };
 
 struct Plan;
+struct HierPlan;
 
 }  // namespace esp
 
@@ -88,8 +89,8 @@ struct esp_world_s {
   int nranks = 1, rank = 0, nlocal = 1, dev = 0;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
-  cudaStream_t cap_stream = nullptr;
-  cudaStream_t fin_stream = nullptr;       // DGC finalize chains of a multi-bucket call (a9)       // CUDA-graph capture of a plan's call (non-blocking)
+  cudaStream_t cap_stream = nullptr;       // CUDA-graph capture of a plan's call (non-blocking)
+  cudaStream_t fin_stream = nullptr;       // DGC finalize chains of a multi-bucket call (a9)
   cudaEvent_t ev_join = nullptr, ev_fork = nullptr;
   std::vector<esp_counters_t> counters;   // per local rank
   bool timing = false;
@@ -112,6 +113,13 @@ struct esp_world_s {
   unsigned int* wait_err = nullptr;
   unsigned long long wait_timeout_ns = 300ull * 1000000000ull;
   std::set<esp_ctx_s*> ctxs;
+  // hierarchical communication (reading R23): n = m machines x g
+  // GPUs; the intra-machine phases run on `intra`, the compressed
+  // inter-machine phase on `inter` (both owned)
+  int hier_g = 0;                          // > 0: a hierarchical world
+  esp_world_s* intra = nullptr;            // the g GPUs of this rank's machine
+  esp_world_s* inter = nullptr;            // the m GPUs with this rank's local index
+  std::vector<esp::HierPlan*> hplans;      // owned
 };
 
 struct esp_ctx_s {
@@ -133,6 +141,7 @@ struct esp_ctx_s {
   uint64_t r2_len = 0;
   uint64_t step = 0;
   uint64_t hash_base = 0;            // mix(mix(seed) ^ tensor_id)
+  esp_ctx_s* inner = nullptr;        // hierarchical world: this rank's shard as a ctx of w->inter (owned)
   // esp_decompress: device tables of the last (pieces, out) seen, reused while
   // the caller passes the same buffers; staged through pinned memory
   struct DecCache {
@@ -183,6 +192,12 @@ void execute_loopback(const std::vector<Plan*>& plans, const std::vector<float* 
 void execute_compress(Plan* p, const float* grad, void* payload, cudaStream_t st);
 void clear_plans(esp_world_s* w);
 void trim_plans(esp_world_s* w);   // evict least recently used plans down to w->plan_cap
+// hierarchical worlds (hier.cu)
+void execute_hier(esp_world_s* w, const std::vector<esp_ctx_s*>& ctxs, float* const* grads, cudaStream_t st);
+void execute_hier_loopback(const std::vector<esp_world_s*>& ws, const std::vector<std::vector<esp_ctx_s*>>& ctxs,
+                           const std::vector<float* const*>& grads, cudaStream_t st);
+void clear_hier_plans(esp_world_s* w);
+void drop_hier_plans_with(esp_world_s* w, esp_ctx_s* c);
 
 }  // namespace esp
 

@@ -314,12 +314,72 @@ esp_status_t esp_world_create_loopback(int nranks, int cuda_dev, esp_world_t* ou
   ESP_API_END
 }
 
+// a world object with its streams and events (no communicator yet)
+static std::unique_ptr<esp_world_s> make_world(int nranks, int rank, int dev, bool loopback) {
+  auto w = std::make_unique<esp_world_s>();
+  w->loopback = loopback;
+  w->nranks = nranks;
+  w->rank = rank;
+  w->nlocal = 1;
+  w->dev = dev;
+  if (loopback) w->wait_timeout_ns = 5ull * 1000000000ull;
+  world_common_init(w.get());
+  return w;
+}
+
+esp_status_t esp_world_create_hier(esp_world_t parent, int group, esp_world_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(parent && out, ESP_ERR_INVALID_ARG, "null argument");
+  ESP_REQUIRE(parent->comm && !parent->sim && !parent->loopback && parent->hier_g == 0, ESP_ERR_STATE,
+              "a hierarchical world splits a flat NCCL world");
+  const int n = parent->nranks;
+  ESP_REQUIRE(group >= 1 && n % group == 0, ESP_ERR_INVALID_ARG, "group must divide the number of ranks");
+  ESP_CUDA(cudaSetDevice(parent->dev));
+  const int a = parent->rank / group, i = parent->rank % group, m = n / group;
+  auto w = make_world(n, parent->rank, parent->dev, false);
+  w->hier_g = group;
+  auto intra = make_world(group, i, parent->dev, false);
+  auto inter = make_world(m, a, parent->dev, false);
+  // machine = color a (key i), inter-machine group = color i (key a); both
+  // splits are collective over the parent communicator, in this order
+  ESP_NCCL(ncclCommSplit(parent->comm, a, i, &intra->comm, nullptr));
+  ESP_NCCL(ncclCommSplit(parent->comm, i, a, &inter->comm, nullptr));
+  w->intra = intra.release();
+  w->inter = inter.release();
+  *out = w.release();
+  ESP_API_END
+}
+
+esp_status_t esp_world_create_loopback_hier(int nranks, int group, int cuda_dev, esp_world_t* out) {
+  ESP_API_BEGIN
+  ESP_REQUIRE(out, ESP_ERR_INVALID_ARG, "out is NULL");
+  ESP_REQUIRE(nranks >= 2 && nranks <= 64 && group >= 1 && nranks % group == 0 && cuda_dev >= 0,
+              ESP_ERR_INVALID_ARG, "bad nranks/group/device");
+  const int m = nranks / group;
+  std::vector<std::unique_ptr<esp_world_s>> ws;
+  for (int r = 0; r < nranks; ++r) {
+    auto w = make_world(nranks, r, cuda_dev, true);
+    w->hier_g = group;
+    // the machine's phases address each other's arenas directly; the
+    // inter-machine group of local index i is a loopback group of m ranks
+    // (a single rank: a solo world, its collectives are identities)
+    w->intra = make_world(group, r % group, cuda_dev, true).release();
+    w->inter = make_world(m, r / group, cuda_dev, m > 1).release();
+    ws.push_back(std::move(w));
+  }
+  for (int r = 0; r < nranks; ++r) out[r] = ws[r].release();
+  ESP_API_END
+}
+
 esp_status_t esp_world_destroy(esp_world_t w) {
   ESP_API_BEGIN
   ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
   ESP_REQUIRE(w->ctxs.empty(), ESP_ERR_STATE, "destroy every ctx of the world first");
   cudaSetDevice(w->dev);
   cudaStreamSynchronize(w->comm_stream);
+  clear_hier_plans(w);
+  if (w->intra) esp_world_destroy(w->intra);
+  if (w->inter) esp_world_destroy(w->inter);
   clear_plans(w);
   if (w->comm) ncclCommDestroy(w->comm);
   for (auto e : w->tev) cudaEventDestroy(e);

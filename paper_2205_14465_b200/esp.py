@@ -27,7 +27,8 @@ SYMBOLS = (
     "esp_world_check", "esp_world_info", "esp_world_counters", "esp_world_counters_local",
     "esp_world_reset_counters", "esp_world_set_timing", "esp_last_timing", "esp_world_set_bucket_elems",
     "esp_world_set_probe", "esp_probe_read", "esp_world_set_timeout", "esp_world_set_plan_cache",
-    "esp_world_drop_plans", "esp_world_set_multicast", "esp_world_create_loopback", "esp_sync_many_loopback",
+    "esp_world_drop_plans", "esp_world_set_multicast", "esp_world_create_loopback", "esp_world_create_hier",
+    "esp_world_create_loopback_hier", "esp_sync_many_loopback",
     "esp_ctx_create", "esp_ctx_destroy", "esp_ctx_payload_bytes", "esp_ctx_get_state",
     "esp_ctx_set_state", "esp_ctx_get_momentum", "esp_ctx_set_momentum", "esp_compress", "esp_decompress", "esp_sync", "esp_sync_many",
     "esp_compressed_bytes", "esp_wire_bytes", "esp_model_time", "esp_status_string",
@@ -91,6 +92,8 @@ def lib():
             "esp_world_set_timeout": [vp, dbl], "esp_world_set_plan_cache": [vp, i32],
             "esp_world_drop_plans": [vp], "esp_world_set_multicast": [vp, i32],
             "esp_world_create_loopback": [i32, i32, C.POINTER(vp)],
+            "esp_world_create_hier": [vp, i32, C.POINTER(vp)],
+            "esp_world_create_loopback_hier": [i32, i32, i32, C.POINTER(vp)],
             "esp_sync_many_loopback": [C.POINTER(vp), i32, C.POINTER(vp), C.POINTER(vp), i32, vp],
             "esp_probe_read": [vp, C.POINTER(dbl), C.POINTER(u64), C.POINTER(u64)],
             "esp_ctx_create": [vp, C.POINTER(CompressorCfg), i32, u64, sz, C.POINTER(vp)],
@@ -227,6 +230,21 @@ class World:
         hs = (C.c_void_p * nranks)()
         _check(lib().esp_world_create_loopback(nranks, device, hs))
         return [cls(C.c_void_p(hs[r]), device) for r in range(nranks)]
+
+    @classmethod
+    def loopback_hier(cls, nranks: int, group: int, device: int = 0):
+        """A loopback group of hierarchical worlds: nranks / group machines of
+        `group` GPUs, all on one GPU (tests; see esp_world_create_hier)."""
+        hs = (C.c_void_p * nranks)()
+        _check(lib().esp_world_create_loopback_hier(nranks, group, device, hs))
+        return [cls(C.c_void_p(hs[r]), device) for r in range(nranks)]
+
+    def hier(self, group: int):
+        """The hierarchical world over this NCCL world's ranks: machines of
+        `group` consecutive ranks (collective over all ranks)."""
+        h = C.c_void_p()
+        _check(lib().esp_world_create_hier(self.h, int(group), C.byref(h)))
+        return World(h, self.device)
 
     @classmethod
     def nccl(cls, device: int | None = None, group=None):
