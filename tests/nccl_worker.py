@@ -156,6 +156,7 @@ def main():
 
     if n > 1:
         multicast_allgather(rank, local, n)
+        hierarchical(rank, local, n)
         missing_peer(rank, local)
     dist.barrier()
     dist.destroy_process_group()
@@ -197,6 +198,40 @@ def multicast_allgather(rank, local, n):
     print(f"rank {rank}: multicast allgather ok, pushed {c['pushed'] / T:.0f} B/step, slot ~{slot} B", flush=True)
     w.check()
     w.destroy()
+
+
+def hierarchical(rank, local, n):
+    """Hierarchical sync on real ranks (esp_world_create_hier over NCCL, CUDA
+    IPC inside each machine): machines of 2 GPUs (n = 2: one machine; n = 4:
+    2 x 2), DGC / EFSignSGD / Randomk, 3 steps, against the oracle."""
+    flat = E.World.nccl(local)
+    hw = flat.hier(2)
+    specs = [("dgc", "allgather", 0, 30_011), ("efsignsgd", "alltoall_allgather", 0, 9000),
+             ("randomk", "gather_broadcast", 0, 5000), ("dgc", "alltoall_allgather", 2, 70)]
+    ctxs = [E.Ctx(hw, k, ro, N_, tensor_id=600 + i, ratio=0.02, process=p) for i, (k, ro, p, N_) in enumerate(specs)]
+    cfgs = [O.Cfg(k, 0.02, process=p) for (k, ro, p, N_) in specs]
+    sts = [O.new_states_hier(n, N_, ro, cfgs[i], 2) for i, (k, ro, p, N_) in enumerate(specs)]
+    for s in range(3):
+        for i, (k, ro, p, N_) in enumerate(specs):
+            if k in O.QUANTIZED and s > 0:
+                st = sts[i][rank]
+                r2len = ctxs[i].get_state()[2].shape[1]
+                r2 = np.zeros((1, r2len), np.float32)
+                if st.r2 is not None:
+                    r2[0, :st.r2.size] = st.r2
+                ctxs[i].set_state(st.step, st.r[None], r2)
+        grads = [[gradient(N_, step=s, rank=q, tensor=600 + i) for q in range(n)] for i, (_, _, _, N_) in enumerate(specs)]
+        refs = [O.sync_hierarchical(ro, cfgs[i], grads[i], sts[i], 2, tensor_id=600 + i)
+                for i, (k, ro, p, N_) in enumerate(specs)]
+        gs = [torch.from_numpy(grads[i][rank].copy()).cuda() for i in range(len(specs))]
+        E.esp_sync_many(hw, ctxs, gs)
+        torch.cuda.synchronize()
+        for i, (k, ro, _, _) in enumerate(specs):
+            check(k, ro, gs[i].cpu().numpy(), refs[i].outs[rank], grads[i], f"hierarchical {k}/{ro} step {s}")
+    hw.check()
+    hw.destroy()
+    flat.destroy()
+    print(f"rank {rank}: hierarchical ok", flush=True)
 
 
 def missing_peer(rank, local):
