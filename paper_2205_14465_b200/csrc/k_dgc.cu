@@ -366,7 +366,8 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& s
 template <int NCG, bool MOM = false>
 __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(const SegH1* __restrict__ segs,
                                                                             const uint32_t* __restrict__ unit_seg,
-                                                                            uint32_t nunits, int ns) {
+                                                                            uint32_t nunits, int ns,
+                                                                            int prefill) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -544,6 +545,21 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
       phase ^= 1;
     }
     if (base < n) {
+      // prefill (esp_sync with EF): the gradient's values now live in r, and
+      // the sync's output overwrites the gradient in place -- write its zeros
+      // here, in this pass's store stream, so that h2 only scatters the
+      // selected entries (2 reads + 2 writes per element in one pass instead
+      // of 2R+1W here and a separate 4 B/elem zero-fill pass)
+      if (prefill && S.ef) {
+        float* gz = const_cast<float*>(g);
+        if (full) {
+#pragma unroll
+          for (int j = 0; j < kNJ; ++j) st4(gz + base + lane * 4 + j * 128, make_float4(0.f, 0.f, 0.f, 0.f));
+        } else {
+#pragma unroll
+          for (int j = 0; j < kNJ; ++j) store4_guard(gz, base + j * 128 + lane * 4, n, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+      }
       if (full) {
         float* rp = S.r + base + lane * 4;
 #pragma unroll
@@ -769,15 +785,17 @@ __device__ __forceinline__ uint2* group_slots(const WarpGroup& G) {
 __device__ __forceinline__ void warp_select_bin(const uint32_t* hist, uint32_t rep, uint32_t need,
                                                 uint32_t* out_bin, uint32_t* out_above) {
   const int lane = threadIdx.x & 31;
-  // lane sums first (no 32-entry array: the refine kernels run at 32 registers)
-  uint32_t sum = 0;
+  // a lane's 32 bins as 4 chunk sums of 8 (no 32-entry array: the refine
+  // kernels run at 32 registers); the selected lane reloads one chunk
+  uint32_t cs[4] = {0u, 0u, 0u, 0u};
   for (uint32_t r = 0; r < rep; ++r) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint4 v = __ldcg(reinterpret_cast<const uint4*>(hist + 1024u * r) + lane * 8 + i);
-      sum += v.x + v.y + v.z + v.w;
+      cs[i >> 1] += v.x + v.y + v.z + v.w;
     }
   }
+  const uint32_t sum = cs[0] + cs[1] + cs[2] + cs[3];
   // above this lane's bins = sum over lanes > lane (suffix scan)
   uint32_t x = sum;
 #pragma unroll
@@ -788,13 +806,26 @@ __device__ __forceinline__ void warp_select_bin(const uint32_t* hist, uint32_t r
   const uint32_t above = x - sum;
   uint32_t bin = 0, ab = 0;
   const bool mine = above < need && need <= above + sum;
-  if (mine) {   // this lane's 32 bins again, from the top
+  if (mine) {   // the chunk holding the bin (from the top), then its 8 bins
     uint32_t cum = above;
-    for (int i = 31; i >= 0; --i) {
-      uint32_t hi = 0;
-      for (uint32_t r = 0; r < rep; ++r) hi += __ldcg(hist + 1024u * r + lane * 32 + i);
-      if (cum + hi >= need) { bin = lane * 32 + i; ab = cum; break; }
-      cum += hi;
+    int c = 3;
+#pragma unroll
+    for (int q = 3; q > 0; --q)
+      if (c == q && cum + cs[q] < need) {
+        cum += cs[q];
+        c = q - 1;
+      }
+    uint32_t h8[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    for (uint32_t r = 0; r < rep; ++r) {
+      const uint4* p = reinterpret_cast<const uint4*>(hist + 1024u * r + lane * 32 + 8 * c);
+      const uint4 a = __ldcg(p), b = __ldcg(p + 1);
+      h8[0] += a.x; h8[1] += a.y; h8[2] += a.z; h8[3] += a.w;
+      h8[4] += b.x; h8[5] += b.y; h8[6] += b.z; h8[7] += b.w;
+    }
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+      if (cum + h8[i] >= need) { bin = lane * 32 + 8 * c + i; ab = cum; break; }
+      cum += h8[i];
     }
   }
   const uint32_t m = __ballot_sync(0xffffffffu, mine);
@@ -808,7 +839,7 @@ __device__ __forceinline__ void warp_select_bin(const uint32_t* hist, uint32_t r
 }
 
 template <int ROUND>
-__global__ void __launch_bounds__(kThreads, 8) dgc_refine_kernel(const SegH1* __restrict__ segs,
+__global__ void __launch_bounds__(kThreads, 6) dgc_refine_kernel(const SegH1* __restrict__ segs,
                                                               const uint32_t* __restrict__ group_seg,
                                                               uint32_t ngroups) {
   pdl_wait();     // predecessors in the stream are complete (PDL)
@@ -1079,13 +1110,13 @@ static void debug_sync(const char* what, cudaStream_t st) {
 
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
-                   cudaEvent_t probe1, bool mom) {
-  launch_dgc_stream(segs, nsegs, unit_seg, nunits, st, probe0, probe1, mom);
+                   cudaEvent_t probe1, bool mom, bool prefill) {
+  launch_dgc_stream(segs, nsegs, unit_seg, nunits, st, probe0, probe1, mom, prefill);
   launch_dgc_finalize(segs, nsegs, group_seg, ngroups, st);
 }
 
 void launch_dgc_stream(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits, cudaStream_t st,
-                       cudaEvent_t probe0, cudaEvent_t probe1, bool mom) {
+                       cudaEvent_t probe0, cudaEvent_t probe1, bool mom, bool prefill) {
   if (nsegs == 0) return;
   // three consumer groups of 8 warps over a 3-stage ring of 32 KB (plain EF);
   // two groups over 4 stages of 48 KB with the momentum stream (R20) -- the
@@ -1110,9 +1141,11 @@ void launch_dgc_stream(const SegH1* segs, int nsegs, const uint32_t* unit_seg, i
   if (probe0) cudaEventRecord(probe0, st);
   const int grid = nunits < g_num_sms ? nunits : g_num_sms;
   if (mom)
-    launch_pdl(dgc_stream_kernel<2, true>, grid, 2 * kThreads + 32, mom_smem, st, segs, unit_seg, (uint32_t)nunits, kNsMom);
+    launch_pdl(dgc_stream_kernel<2, true>, grid, 2 * kThreads + 32, mom_smem, st, segs, unit_seg, (uint32_t)nunits,
+               kNsMom, (int)prefill);
   else
-    launch_pdl(dgc_stream_kernel<3>, grid, 3 * kThreads + 32, smem, st, segs, unit_seg, (uint32_t)nunits, kNs);
+    launch_pdl(dgc_stream_kernel<3>, grid, 3 * kThreads + 32, smem, st, segs, unit_seg, (uint32_t)nunits, kNs,
+               (int)prefill);
   debug_sync("dgc_stream", st);
   if (probe1) cudaEventRecord(probe1, st);
   count_launches(2);
