@@ -53,7 +53,17 @@ WORKLOADS = {
     "gpt2_medium_selected": ("gpt2_medium", ("selected", "paper", "dgc")),
     "gpt2_medium_selected_bucketed": ("gpt2_medium", ("selected", "bucketed", "dgc")),
     "gpt2_medium_selected_bucketed_all": ("gpt2_medium", ("selected", "bucketed", None)),
+    # NEXT-4: hierarchical communication, "machines" of 2 GPUs (1 when n is
+    # odd): intra Reduce-scatter, inter-machine DGC 0.1% Allgather per shard,
+    # intra Allgather (esp_world_create_hier)
+    "bert_large_dgc_hier2": ("bert_large", lambda N: ("dgc", 0.001, "allgather")),
 }
+HIER_GROUP = {"bert_large_dgc_hier2": 2}
+
+
+def hier_group(name, n):
+    g = HIER_GROUP.get(name, 0)
+    return (g if n % g == 0 else 1) if g else 0
 
 
 def workload(name, n):
@@ -326,11 +336,16 @@ def _oracle_job(job):
     rule = _W[("rule", name, n)]
     kind, ratio, routine, ex = opt(rule, N)
     cfg = O.Cfg(kind, ratio, **ex)
+    g = hier_group(name, n)
     if (name, i) not in _W:
-        _W[(name, i)] = ([gradient(N, rank=r, tensor=i) for r in range(n)], O.new_states(n, N, routine, cfg))
+        st = O.new_states_hier(n, N, routine, cfg, g) if g else O.new_states(n, N, routine, cfg)
+        _W[(name, i)] = ([gradient(N, rank=r, tensor=i) for r in range(n)], st)
     grads, st = _W[(name, i)]
     t0 = time.perf_counter()
-    O.sync(routine, cfg, grads, st, tensor_id=i)
+    if g:
+        O.sync_hierarchical(routine, cfg, grads, st, g, tensor_id=i)
+    else:
+        O.sync(routine, cfg, grads, st, tensor_id=i)
     return time.perf_counter() - t0
 
 
@@ -405,6 +420,9 @@ def main():
     sizes = shapes.numels(model)
     total = sum(sizes)
     world = E.World.nccl(local) if ws > 1 else E.World.nccl_single(local)
+    flat_world = None
+    if hier_group(args.workload, ws):
+        flat_world, world = world, world.hier(hier_group(args.workload, ws))
     if args.bucket_elems:
         world.set_bucket_elems(args.bucket_elems)
     ctxs = []
@@ -622,6 +640,8 @@ def main():
             line["cpu_baseline"] = cpu_baseline(args, model, rule, sizes, names, 1)
         emit(line)
     world.destroy()
+    if flat_world is not None:
+        flat_world.destroy()
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

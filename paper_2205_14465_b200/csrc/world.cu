@@ -452,6 +452,7 @@ esp_status_t esp_world_set_bucket_elems(esp_world_t w, uint64_t elems) {
   ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
   w->bucket_elems = elems;
   clear_plans(w);
+  if (w->inter) esp_world_set_bucket_elems(w->inter, elems);
   ESP_API_END
 }
 
@@ -492,12 +493,14 @@ esp_status_t esp_world_set_probe(esp_world_t w, int enable) {
   ESP_REQUIRE(w, ESP_ERR_INVALID_ARG, "world is NULL");
   w->probe = enable != 0;
   w->probe_used = 0;
+  if (w->inter) esp_world_set_probe(w->inter, enable);   // hierarchical: the h1 kernels run in the inter world
   ESP_API_END
 }
 
 esp_status_t esp_probe_read(esp_world_t w, double* ms, uint64_t* launches, uint64_t* bytes) {
   ESP_API_BEGIN
   ESP_REQUIRE(w && ms && launches && bytes, ESP_ERR_INVALID_ARG, "null argument");
+  if (w->inter) return esp_probe_read(w->inter, ms, launches, bytes);
   double t = 0;
   uint64_t b = 0;
   for (size_t i = 0; i < w->probe_used; ++i) {
