@@ -11,18 +11,14 @@ void count_launches(int n);   // process-wide counter behind esp_launch_count()
 
 // DGC / TOPK h1 (k_dgc.cu)
 // probe0/probe1 (optional): events recorded around the streaming pass.
-// prefill: the streaming pass also zeroes the gradient of segments with EF
-// (esp_sync: the output overwrites it; h2 then skips its zero fill)
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st,
-                   cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr, bool mom = false,
-                   bool prefill = false);
+                   cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr, bool mom = false);
 // the two halves of launch_dgc_h1: sampled threshold + streaming pass, then the
 // finalize chain (fallback, exact radix select, ordered write + EF zeroing),
 // which may run on another stream after the first half (bucket pipelining)
 void launch_dgc_stream(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits, cudaStream_t st,
-                       cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr, bool mom = false,
-                       bool prefill = false);
+                       cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr, bool mom = false);
 void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg, int ngroups, cudaStream_t st);
 // block the stream until *cnt >= target (arrivals of a fused collective); after
 // timeout_ns of wall time without them, set *err (mapped host memory) and return
@@ -52,10 +48,8 @@ void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaSt
 // jobs: {segment, piece within segment, first entry, 0}, kOffJob entries each
 // max_pieces: the largest npieces of the launch's segments (> 1 enables the
 // shared-memory accumulation path and its dynamic shared memory)
-// prefilled: the output is already +0 everywhere (the DGC streaming pass
-// zeroed it): only the entries are written
 void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
-                      const unsigned char* const* pieces, int max_pieces, cudaStream_t st, bool prefilled = false);
+                      const unsigned char* const* pieces, int max_pieces, cudaStream_t st);
 // max_pieces: the largest npieces of the launch's segments (sizes the shared-memory word stage)
 void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
                     const unsigned char* const* pieces, int max_pieces, cudaStream_t st);

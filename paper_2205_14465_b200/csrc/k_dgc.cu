@@ -366,8 +366,7 @@ __device__ void stream_segment_done(const SegH1& S, uint32_t units, GroupSmem& s
 template <int NCG, bool MOM = false>
 __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(const SegH1* __restrict__ segs,
                                                                             const uint32_t* __restrict__ unit_seg,
-                                                                            uint32_t nunits, int ns,
-                                                                            int prefill) {
+                                                                            uint32_t nunits, int ns) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -545,21 +544,6 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
       phase ^= 1;
     }
     if (base < n) {
-      // prefill (esp_sync with EF): the gradient's values now live in r, and
-      // the sync's output overwrites the gradient in place -- write its zeros
-      // here, in this pass's store stream, so that h2 only scatters the
-      // selected entries (2 reads + 2 writes per element in one pass instead
-      // of 2R+1W here and a separate 4 B/elem zero-fill pass)
-      if (prefill && S.ef) {
-        float* gz = const_cast<float*>(g);
-        if (full) {
-#pragma unroll
-          for (int j = 0; j < kNJ; ++j) st4(gz + base + lane * 4 + j * 128, make_float4(0.f, 0.f, 0.f, 0.f));
-        } else {
-#pragma unroll
-          for (int j = 0; j < kNJ; ++j) store4_guard(gz, base + j * 128 + lane * 4, n, make_float4(0.f, 0.f, 0.f, 0.f));
-        }
-      }
       if (full) {
         float* rp = S.r + base + lane * 4;
 #pragma unroll
@@ -1110,13 +1094,13 @@ static void debug_sync(const char* what, cudaStream_t st) {
 
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
-                   cudaEvent_t probe1, bool mom, bool prefill) {
-  launch_dgc_stream(segs, nsegs, unit_seg, nunits, st, probe0, probe1, mom, prefill);
+                   cudaEvent_t probe1, bool mom) {
+  launch_dgc_stream(segs, nsegs, unit_seg, nunits, st, probe0, probe1, mom);
   launch_dgc_finalize(segs, nsegs, group_seg, ngroups, st);
 }
 
 void launch_dgc_stream(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits, cudaStream_t st,
-                       cudaEvent_t probe0, cudaEvent_t probe1, bool mom, bool prefill) {
+                       cudaEvent_t probe0, cudaEvent_t probe1, bool mom) {
   if (nsegs == 0) return;
   // three consumer groups of 8 warps over a 3-stage ring of 32 KB (plain EF);
   // two groups over 4 stages of 48 KB with the momentum stream (R20) -- the
@@ -1142,10 +1126,9 @@ void launch_dgc_stream(const SegH1* segs, int nsegs, const uint32_t* unit_seg, i
   const int grid = nunits < g_num_sms ? nunits : g_num_sms;
   if (mom)
     launch_pdl(dgc_stream_kernel<2, true>, grid, 2 * kThreads + 32, mom_smem, st, segs, unit_seg, (uint32_t)nunits,
-               kNsMom, (int)prefill);
+               kNsMom);
   else
-    launch_pdl(dgc_stream_kernel<3>, grid, 3 * kThreads + 32, smem, st, segs, unit_seg, (uint32_t)nunits, kNs,
-               (int)prefill);
+    launch_pdl(dgc_stream_kernel<3>, grid, 3 * kThreads + 32, smem, st, segs, unit_seg, (uint32_t)nunits, kNs);
   debug_sync("dgc_stream", st);
   if (probe1) cudaEventRecord(probe1, st);
   count_launches(2);

@@ -76,8 +76,7 @@ template <bool MULTI>
 __global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 12) h2_sparse_kernel(const SegH2* __restrict__ segs,
                                                                  const uint32_t* __restrict__ tile_seg,
                                                                  uint32_t ntiles,
-                                                                 const unsigned char* const* __restrict__ pieces,
-                                                                 int prefilled) {
+                                                                 const unsigned char* const* __restrict__ pieces) {
   pdl_wait();     // predecessors in the stream are complete (PDL)
   pdl_trigger();
   constexpr int kWarps = kTileThreads / 32;
@@ -203,12 +202,7 @@ __global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 12) h2_sparse_kernel
       const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
       uint32_t a, b;
       range(0, &a, &b);
-      if (prefilled) {   // the output is already +0: the entries only
-        for (uint32_t i = a + lane; i < b; i += 32) {
-          const float v = __fadd_rn(0.f, __ldg(val + i));
-          out[__ldg(idx + i)] = ones ? v : div(v);
-        }
-      } else if (b - a >= 8) {
+      if (b - a >= 8) {
 #pragma unroll
         for (int i = lane * 4; i < kTile; i += 128)
           *reinterpret_cast<float4*>(acc + i) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -230,8 +224,7 @@ __global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 12) h2_sparse_kernel
         }
       }
     } else {
-      if (!prefilled)
-        for (uint32_t i = lane * 4; lo + i < hi; i += 128) store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
+      for (uint32_t i = lane * 4; lo + i < hi; i += 128) store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
       __syncwarp();   // zero stores before the touched-word stores
       {
         // one entry per lane: lanes holding the same index form a group
@@ -507,7 +500,7 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const SegH1* __restrict_
 }
 
 void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
-                      const unsigned char* const* pieces, int max_pieces, cudaStream_t st, bool prefilled) {
+                      const unsigned char* const* pieces, int max_pieces, cudaStream_t st) {
   if (ntiles == 0) return;
   launch_pdl(h2_sparse_offsets_kernel, njobs, kThreads, 0, st, segs, jobs, pieces);
   constexpr int kSmem = kTileThreads / 32 * kTile * (int)sizeof(float);
@@ -523,10 +516,10 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
   const int need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);   // one warp per tile
   if (max_pieces > 1)
     launch_pdl(h2_sparse_kernel<true>, need < capn ? need : capn, kTileThreads, kSmem, st, segs, tile_seg,
-               (uint32_t)ntiles, pieces, (int)prefilled);
+               (uint32_t)ntiles, pieces);
   else
     launch_pdl(h2_sparse_kernel<false>, need < cap1 ? need : cap1, kTileThreads, kSmem, st, segs, tile_seg,
-               (uint32_t)ntiles, pieces, (int)prefilled);
+               (uint32_t)ntiles, pieces);
   count_launches(2);
 }
 

@@ -56,7 +56,6 @@ struct Bucket {
   cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr, ev_stream = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
-  uint64_t h1_elems = 0;      // elements it streams (+4 B each when it also zeroes the output, prefill)
   // ---- compression fused with the collective over NVLink peer memory
   // (DESIGN.md 9): the producers (DGC write, sign h1 /
   // a7) write their payload locally, then push_kernel copies each slot
@@ -507,7 +506,6 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     uint64_t elems = 0;
     for (int i = 0; i < b.nh1; ++i) elems += T.h1[h1_first + i].n;
     const bool ef = p.ctxs[b.tens[0]]->cfg.error_feedback != 0;
-    b.h1_elems = elems;
     if (none) b.h1_bytes = 8 * elems;
     else if (quant) b.h1_bytes = (ef ? 12 : 4) * elems + elems / 8;
     else if (b.momentum != 0.0) b.h1_bytes = 20 * elems;   // + read u, write u (R20)
@@ -1204,27 +1202,24 @@ static void probe_pair(esp_world_s* w, cudaEvent_t* e0, cudaEvent_t* e1, uint64_
 // over the candidates) runs there after the streaming pass, so that it
 // overlaps the next bucket's HBM-bound streaming pass on `st` (a9).
 // Returns the stream on which the bucket's payload is complete.
-// prefill (the esp_sync paths): the DGC streaming pass also zeroes the
-// gradient, which the sync's h2 then only scatters the entries into
-static cudaStream_t run_h1(Plan& p, Bucket& b, cudaStream_t st, cudaStream_t fin = nullptr, bool prefill = false) {
+static cudaStream_t run_h1(Plan& p, Bucket& b, cudaStream_t st, cudaStream_t fin = nullptr) {
   cudaStream_t done = st;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  const bool zeroes = prefill && b.ef && (b.kind == ESP_DGC || b.kind == ESP_TOPK);
-  if (p.w->probe && b.nh1_units) probe_pair(p.w, &e0, &e1, b.h1_bytes + (zeroes ? 4 * b.h1_elems : 0));
+  if (p.w->probe && b.nh1_units) probe_pair(p.w, &e0, &e1, b.h1_bytes);
   const bool dgc = b.kind == ESP_DGC || b.kind == ESP_TOPK;
   const bool sign = b.kind == ESP_EFSIGNSGD || b.kind == ESP_ONEBIT;
   if (e0 && !dgc && !sign) ESP_CUDA(cudaEventRecord(e0, st));
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
       if (fin) {
-        launch_dgc_stream(b.h1, b.nh1, b.h1_units, b.nh1_units, st, e0, e1, b.momentum != 0.0, prefill);
+        launch_dgc_stream(b.h1, b.nh1, b.h1_units, b.nh1_units, st, e0, e1, b.momentum != 0.0);
         ESP_CUDA(cudaEventRecord(b.ev_stream, st));
         ESP_CUDA(cudaStreamWaitEvent(fin, b.ev_stream, 0));
         launch_dgc_finalize(b.h1, b.nh1, b.h1_groups, b.nh1_groups, fin);
         done = fin;
       } else {
         launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1,
-                      b.momentum != 0.0, prefill);
+                      b.momentum != 0.0);
       }
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
@@ -1438,9 +1433,8 @@ static void run_comm(Plan& p, Bucket& b, cudaStream_t cs, cudaEvent_t mid0, cuda
 static void run_h2(Plan& p, Bucket& b, cudaStream_t st) {
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
-      // the streaming pass zeroed the gradients of an EF bucket (prefill)
       launch_h2_sparse(b.h2, b.h2_units, b.nh2_units, b.h2_off_jobs, b.nh2_off_jobs,
-                       (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, b.h2_max_pieces, st, b.ef);
+                       (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, b.h2_max_pieces, st);
       break;
     case ESP_RANDOMK:
       launch_h2_randomk(b.h2, b.h2_units, b.nh2_units, (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces,
@@ -1578,7 +1572,7 @@ void execute_plan(Plan* pp, float* const* grads, cudaStream_t st) {
       cudaEvent_t e0 = tev(w, 1 + 6 * i), e1 = tev(w, 2 + 6 * i), e2 = tev(w, 3 + 6 * i);
       cudaEvent_t e3 = tev(w, 4 + 6 * i), m0 = tev(w, 5 + 6 * i), m1 = tev(w, 6 + 6 * i);
       ESP_CUDA(cudaEventRecord(e0, st));
-      run_h1(p, b, st, nullptr, true);
+      run_h1(p, b, st);
       ESP_CUDA(cudaEventRecord(e1, st));
       ESP_CUDA(cudaStreamWaitEvent(cs, e1, 0));
       ESP_CUDA(cudaEventRecord(m0, cs));
@@ -1623,7 +1617,7 @@ static void enqueue_pipelined(Plan& p, cudaStream_t st) {
   for (size_t i = 0; i <= nb; ++i) {
     if (i < nb) {
       Bucket& b = p.buckets[i];
-      const cudaStream_t done = run_h1(p, b, st, nb > 1 ? w->fin_stream : nullptr, true);
+      const cudaStream_t done = run_h1(p, b, st, nb > 1 ? w->fin_stream : nullptr);
       ESP_CUDA(cudaEventRecord(b.ev_h1, done));
       ESP_CUDA(cudaStreamWaitEvent(cs, b.ev_h1, 0));
       run_comm(p, b, cs, nullptr, nullptr);
@@ -1669,7 +1663,7 @@ void execute_loopback(const std::vector<Plan*>& plans, const std::vector<float* 
     if (p.zero_bytes) ESP_CUDA(cudaMemsetAsync(p.zero, 0, p.zero_bytes, st));
   }
   for (size_t i = 0; i < plans[0]->buckets.size(); ++i) {
-    for (int r = 0; r < n; ++r) run_h1(*plans[r], plans[r]->buckets[i], st, nullptr, true);
+    for (int r = 0; r < n; ++r) run_h1(*plans[r], plans[r]->buckets[i], st);
     for (int stage = 1; stage <= 3; ++stage)
       for (int r = 0; r < n; ++r) fused_stage(*plans[r], plans[r]->buckets[i], stage, st, nullptr, nullptr);
     for (int r = 0; r < n; ++r) {
