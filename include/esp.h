@@ -254,13 +254,15 @@ esp_status_t esp_ctx_set_momentum(esp_ctx_t c, const float* host, size_t count);
  * esp_compress: EF-fused compression of one rank's tensor (every local rank in a
  * sim world).  payload: esp_ctx_payload_bytes bytes per rank, caller-owned.
  * Advances the ctx step counter (Randomk draws).
- * esp_decompress: out[numel] = reduce(sum over pieces in order of decompress(
- * pieces[i])) — rank-order fp32 sum from +0.0f, then / npieces for MEAN.
+ * esp_decompress: agg[numel] = reduce(sum over pieces in order of decompress(
+ * pieces[i])) — rank-order fp32 sum from +0.0f, then / npieces for MEAN;
+ * accumulate = 0: out := agg; accumulate = 1: out[i] := fl(out[i] + agg[i])
+ * for every i (through a per-ctx temporary).
  * pieces: npieces device pointers (host array) to full payloads of this ctx.
  */
 esp_status_t esp_compress(esp_ctx_t c, const float* grad, void* payload, void* stream);
 esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces, float* out,
-                            void* stream);
+                            int accumulate, void* stream);
 
 /* ---- sync ---------------------------------------------------------------------
  * h1 -> routine -> h2.  grad_inout := the aggregated gradient on every rank.

@@ -149,6 +149,7 @@ esp_status_t esp_ctx_destroy(esp_ctx_t c) {
   cudaFree(c->lazy2);
   cudaFree(c->u);
   if (c->dec.d) cudaFree(c->dec.d);
+  if (c->dec.acc) cudaFree(c->dec.acc);
   if (c->dec.h) cudaFreeHost(c->dec.h);
   if (c->dec.ev) cudaEventDestroy(c->dec.ev);
   c->w->ctxs.erase(c);
@@ -285,16 +286,21 @@ esp_status_t esp_compress(esp_ctx_t c, const float* grad, void* payload, void* s
   ESP_API_END
 }
 
-esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces, float* out, void* stream) {
+esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces, float* out_user, int accumulate,
+                            void* stream) {
   ESP_API_BEGIN
+  ESP_REQUIRE(accumulate == 0 || accumulate == 1, ESP_ERR_INVALID_ARG, "accumulate must be 0 or 1");
   ESP_REQUIRE(c && pieces && npieces >= 1 && npieces <= 64, ESP_ERR_INVALID_ARG, "bad argument");
-  check_ptr16(out, "out");
+  check_ptr16(out_user, "out");
   ESP_REQUIRE(c->cfg.kind != ESP_NONE, ESP_ERR_UNSUPPORTED, "NONE has no compressed payload");
   ESP_REQUIRE(c->w->hier_g == 0, ESP_ERR_UNSUPPORTED, "h2 of a hierarchical ctx: use its shard's world");
   for (int i = 0; i < npieces; ++i) check_ptr16(pieces[i], "piece");
   ESP_CUDA(cudaSetDevice(c->w->dev));
   cudaStream_t st = as_stream(stream);
   auto& D = c->dec;
+  // accumulate: the aggregate goes to a per-ctx temporary, then out += it
+  if (accumulate && !D.acc) ESP_CUDA(cudaMalloc(&D.acc, sizeof(float) * std::max<uint64_t>(c->N, 4)));
+  float* out = accumulate ? D.acc : out_user;
   const bool tiles = c->cfg.kind == ESP_DGC || c->cfg.kind == ESP_TOPK;
   const bool hit = D.valid && D.out == out && D.pieces.size() == (size_t)npieces &&
                    std::equal(D.pieces.begin(), D.pieces.end(), pieces);
@@ -422,6 +428,7 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
     case ESP_EFSIGNSGD: launch_h2_sign(K_EFSIGN, dseg, dunits, (int)u0, dpp, npieces, st); break;
     default: launch_h2_sign(K_ONEBIT, dseg, dunits, (int)u0, dpp, npieces, st); break;
   }
+  if (accumulate) launch_add(out_user, D.acc, (uint32_t)c->N, st);   // out = fl(out + aggregate)
   ESP_CUDA(cudaGetLastError());
   ESP_API_END
 }

@@ -158,6 +158,7 @@ struct esp_ctx_s {
     uint32_t nunits = 0;
     int njobs = 0;
     uint64_t step_uploaded = ~0ull;  // Randomk: step of the dyn word on the device
+    float* acc = nullptr;            // accumulate mode: the aggregate before out += it
   } dec;
 };
 

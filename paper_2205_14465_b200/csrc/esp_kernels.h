@@ -41,6 +41,8 @@ void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* 
                         const unsigned char* const* pieces, cudaStream_t st,
                         uint32_t max_len = 0,    // the longest segment (sizes the finalize grid)
                         cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr);
+// out[i] = fl(out[i] + x[i]) (esp_decompress with accumulate)
+void launch_add(float* out, const float* x, uint32_t n, cudaStream_t st);
 // NONE: pack gradients into a contiguous buffer (k_h2.cu)
 void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaStream_t st);
 

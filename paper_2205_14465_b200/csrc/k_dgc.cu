@@ -115,7 +115,10 @@ __global__ void __launch_bounds__(kThreads) dgc_sample_kernel(const SegH1* __res
         // exact whatever threshold it yields; approximate mode: R22)
         static_assert(kSample == 4096, "512 strata x 8 assumes kSample == 2^12");
         const uint32_t G = j >> 3;
-        const uint32_t a = (uint32_t)(((uint64_t)G * n) / strata), b = (uint32_t)(((uint64_t)(G + 1) * n) / strata);
+        // (512 strata, the default: shifts instead of 64-bit divisions)
+        const uint32_t a = strata == 512 ? (uint32_t)(((uint64_t)G * n) >> 9) : (uint32_t)(((uint64_t)G * n) / strata);
+        const uint32_t b = strata == 512 ? (uint32_t)(((uint64_t)(G + 1) * n) >> 9)
+                                         : (uint32_t)(((uint64_t)(G + 1) * n) / strata);
         pos = a + (uint32_t)(((uint64_t)(uint32_t)splitmix64(S.hash ^ G) * (b - a - 7)) >> 32) + (j & 7u);
       }
       gv[q] = j < s ? __ldg(g + pos) : 0.f;

@@ -100,7 +100,7 @@ def lib():
             "esp_ctx_destroy": [vp], "esp_ctx_payload_bytes": [vp, C.POINTER(sz)],
             "esp_ctx_get_state": [vp, vp, C.POINTER(sz)], "esp_ctx_set_state": [vp, vp, sz],
             "esp_ctx_get_momentum": [vp, vp, sz], "esp_ctx_set_momentum": [vp, vp, sz],
-            "esp_compress": [vp, vp, vp, vp], "esp_decompress": [vp, C.POINTER(vp), i32, vp, vp],
+            "esp_compress": [vp, vp, vp, vp], "esp_decompress": [vp, C.POINTER(vp), i32, vp, i32, vp],
             "esp_sync": [vp, vp, vp, vp], "esp_sync_many": [vp, C.POINTER(vp), C.POINTER(vp), i32, vp],
             "esp_compressed_bytes": [C.POINTER(CompressorCfg), sz, i32, C.POINTER(sz)],
             "esp_wire_bytes": [i32, i32, dbl, i32, C.POINTER(dbl), C.POINTER(dbl)],
@@ -398,13 +398,13 @@ def esp_compress(ctx: Ctx, grad, payload=None, stream=None):
     return payload
 
 
-def esp_decompress(ctx: Ctx, pieces, out, stream=None):
+def esp_decompress(ctx: Ctx, pieces, out, stream=None, accumulate=False):
     import torch
     for i, p in enumerate(pieces):
         _require(p, f"pieces[{i}]", torch.uint8, ctx.world.device, min_numel=ctx.payload_bytes)
     _require(out, "out", torch.float32, ctx.world.device, numel=ctx.numel)
     arr = (C.c_void_p * len(pieces))(*[p.data_ptr() for p in pieces])
-    _check(lib().esp_decompress(ctx.h, arr, len(pieces), _ptr(out), _stream(stream)))
+    _check(lib().esp_decompress(ctx.h, arr, len(pieces), _ptr(out), int(bool(accumulate)), _stream(stream)))
     return out
 
 

@@ -229,6 +229,33 @@ def test_compress_payload_bytes(kind):
         w.destroy()
 
 
+@pytest.mark.parametrize("kind", ["dgc", "randomk", "efsignsgd", "onebit"])
+def test_decompress_accumulate(kind):
+    """esp_decompress(..., accumulate=1): out[i] := fl(out[i] + agg[i]) for every
+    i, agg = the rank-order mean of the pieces' decodes.  The
+    three pieces are fresh-state compressions of three gradients (one ctx each,
+    the same tensor id), so the oracle's compress_segment of each gradient is
+    the exact payload."""
+    E = esp()
+    N = 50_003
+    w = E.World.nccl_single(0)
+    try:
+        grads = [gradient(N, rank=r, tensor=4) for r in range(3)]
+        cfg = O.Cfg(kind, 0.02)
+        ctxs = [E.Ctx(w, kind, "allgather", N, tensor_id=4, ratio=0.02) for _ in range(3)]
+        pays = [E.esp_compress(c, torch.from_numpy(g.copy()).cuda()) for c, g in zip(ctxs, grads)]
+        dec = [O.compress_segment(cfg, g, tensor_id=4)[1] for g in grads]
+        agg = O.aggregate(dec, "mean", 3)
+        out0 = gradient(N, rank=9, tensor=5, dist="D2")
+        out = torch.from_numpy(out0.copy()).cuda()
+        E.esp_decompress(ctxs[0], pays, out, accumulate=True)
+        torch.cuda.synchronize()
+        want = (out0 + agg).astype(np.float32)
+        check_out(kind, out.cpu().numpy(), want, f"accumulate {kind}")
+    finally:
+        w.destroy()
+
+
 def test_sync_many_equals_single():
     """A mixed strategy over a tensor set (bucketing, multi-tensor tables, small
     buckets to exercise the pipeline) equals per-tensor oracle syncs."""
