@@ -11,21 +11,15 @@ void count_launches(int n);   // process-wide counter behind esp_launch_count()
 
 // DGC / TOPK h1 (k_dgc.cu)
 // probe0/probe1 (optional): events recorded around the streaming pass.
-// group_seg / ngroups: the finalize groups of the group-path segments;
-// seg_list / nseg_list: the segment-path segments (one CTA each)
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st,
-                   cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr, bool mom = false,
-                   const uint32_t* seg_list = nullptr, int nseg_list = 0);
+                   cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr, bool mom = false);
 // the two halves of launch_dgc_h1: sampled threshold + streaming pass, then the
 // finalize chain (fallback, exact radix select, ordered write + EF zeroing),
 // which may run on another stream after the first half (bucket pipelining)
 void launch_dgc_stream(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits, cudaStream_t st,
                        cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr, bool mom = false);
-void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg, int ngroups, cudaStream_t st,
-                         const uint32_t* seg_list = nullptr, int nseg_list = 0);
-// the segment path's limits (k_dgc.cu): runs whose offsets fit shared memory
-constexpr uint32_t kSegPathMaxRuns = 8192;
+void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg, int ngroups, cudaStream_t st);
 // block the stream until *cnt >= target (arrivals of a fused collective); after
 // timeout_ns of wall time without them, set *err (mapped host memory) and return
 void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, unsigned int* err,

@@ -1033,143 +1033,6 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __r
 // and returns; esp_world_check and the next esp_sync* call report it (the
 // consumers of this call then read an incomplete payload).  No __trap: a trap
 // would destroy the CUDA context of the whole process.
-// ------------------------------------------------------------------ 4'. segment path
-// One CTA per segment does radix rounds 2 and 3 and the ordered write -- the
-// three group-path kernels' work -- from a dense, index-ordered copy of the
-// segment's candidates in shared memory (kSegChunk at a time, re-gathered per
-// pass when there are more): no global histogram atomics, no look-back, no
-// kernel boundary between the steps.  The planner routes a segment here when
-// its run-offset table fits (<= kSegMaxRuns runs, 4M elements) and its
-// expected candidate count is at most kSegPathMax; the rest (e.g. a 31M-element
-// embedding) keep the group path.
-constexpr uint32_t kSegChunk = 8192;    // candidates staged per pass (64 KB)
-constexpr uint32_t kSegMaxRuns = 8192;  // run offsets kept in shared memory (32 KB)
-struct SegFinSmem {
-  uint2 cand[kSegChunk];
-  uint32_t off[kSegMaxRuns + 1];
-  uint32_t hist[1024];
-  uint32_t sh[288];
-};
-constexpr size_t kSegFinSmem = sizeof(SegFinSmem);
-
-__global__ void __launch_bounds__(kThreads, 2) dgc_seg_finalize_kernel(const SegH1* __restrict__ segs,
-                                                                       const uint32_t* __restrict__ seg_list) {
-  pdl_wait();     // predecessors in the stream are complete (PDL)
-  pdl_trigger();
-  extern __shared__ __align__(16) unsigned char seg_smem_raw[];
-  SegFinSmem& sm = *reinterpret_cast<SegFinSmem*>(seg_smem_raw);
-  const SegH1& S = segs[seg_list[blockIdx.x]];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t nruns = (S.n + kRun - 1) / kRun;
-  // run offsets: exclusive scan of the runs' candidate counts
-  uint32_t carry = 0;
-  for (uint32_t r0 = 0; r0 < nruns; r0 += kThreads) {
-    const uint32_t r = r0 + tid;
-    const uint32_t c = r < nruns ? __ldcg(S.runcnt + r) : 0u;
-    uint32_t tot;
-    const uint32_t ex = block_excl_scan<0>(c, &tot, sm.sh);
-    if (r < nruns) sm.off[r] = carry + ex;
-    carry += tot;
-  }
-  if (tid == 0) sm.off[nruns] = carry;
-  __syncthreads();
-  const uint32_t C = carry;
-  uint32_t prefix = __ldcg(&S.st->prefix), above = __ldcg(&S.st->above), need = __ldcg(&S.st->need);
-  // stage flat candidates [c0, c1) (index order) into sm.cand
-  auto gather = [&](uint32_t c0, uint32_t c1) {
-    for (uint32_t p0 = c0 + tid; p0 < c1; p0 += 4 * kThreads) {
-      uint2 v[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const uint32_t p = p0 + m * kThreads;
-        if (p < c1) {
-          uint32_t lo = 0, hi = nruns;   // the run holding flat position p
-          while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (sm.off[mid] <= p) lo = mid; else hi = mid;
-          }
-          v[m] = __ldcg(S.cand + (size_t)lo * kRun + (p - sm.off[lo]));
-        }
-      }
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const uint32_t p = p0 + m * kThreads;
-        if (p < c1) sm.cand[p - c0] = v[m];
-      }
-    }
-    __syncthreads();
-  };
-  const bool one_chunk = C <= kSegChunk;
-  if (one_chunk) gather(0, C);
-  // radix rounds 2 and 3 over the candidates of the current prefix
-#pragma unroll 1
-  for (int round = 2; round <= 3; ++round) {
-    const int shift_match = round == 2 ? 20 : 10, shift_bin = round == 2 ? 10 : 0;
-    for (int b = tid; b < 1024; b += kThreads) sm.hist[b] = 0;
-    __syncthreads();
-    for (uint32_t c0 = 0; c0 < C; c0 += kSegChunk) {
-      const uint32_t c1 = min(C, c0 + kSegChunk);
-      if (!one_chunk) gather(c0, c1);
-      for (uint32_t q = tid; q < c1 - c0; q += kThreads) {
-        const uint32_t key = sm.cand[q].y & 0x7FFFFFFFu;
-        if ((key >> shift_match) == prefix) atomicAdd(&sm.hist[(key >> shift_bin) & 1023u], 1u);
-      }
-      __syncthreads();
-    }
-    uint32_t bin, ab;
-    select_bin<0, false>(sm.hist, 1024, need, &bin, &ab, sm.sh);
-    prefix = (prefix << 10) | bin;
-    above += ab;
-    need -= ab;
-  }
-  const uint32_t T = prefix;   // the exact k-th key; select key > T, and the first `need` ties by index
-  uint32_t* out_idx = reinterpret_cast<uint32_t*>(S.chunk);
-  float* out_val = reinterpret_cast<float*>(S.chunk + 4 * (size_t)S.kpad);
-  uint32_t a_before = 0, t_before = 0;   // above / ties in earlier chunks
-  for (uint32_t c0 = 0; c0 < C; c0 += kSegChunk) {
-    const uint32_t c1 = min(C, c0 + kSegChunk);
-    if (!one_chunk) gather(c0, c1);
-    const uint32_t len = c1 - c0, per = (len + kThreads - 1) / kThreads;
-    const uint32_t q0 = min(len, tid * per), q1 = min(len, q0 + per);
-    uint32_t na = 0, nt = 0;
-    for (uint32_t q = q0; q < q1; ++q) {
-      const uint32_t key = sm.cand[q].y & 0x7FFFFFFFu;
-      na += key > T;
-      nt += key == T;
-    }
-    uint32_t ta, tt;
-    const uint32_t ea = block_excl_scan<0>(na, &ta, sm.sh);
-    const uint32_t et = block_excl_scan<0>(nt, &tt, sm.sh);
-    uint32_t ab = a_before + ea, tb = t_before + et;   // before this thread's first candidate
-    for (uint32_t q = q0; q < q1; ++q) {
-      const uint2 c = sm.cand[q];
-      const uint32_t key = c.y & 0x7FFFFFFFu;
-      const bool is_above = key > T, is_tie = key == T;
-      if (is_above || (is_tie && tb < need)) {
-        const uint32_t pos = ab + min(tb, need);   // selected entries before this one
-        out_idx[pos] = c.x;
-        out_val[pos] = __uint_as_float(c.y);
-        if (S.ef) S.r[c.x] = 0.0f;
-        if (S.mom) S.mom[c.x] = 0.0f;   // momentum factor masking (R20)
-      }
-      ab += is_above;
-      tb += is_tie;
-    }
-    a_before += ta;
-    t_before += tt;
-    __syncthreads();   // the chunk's candidates are no longer read
-  }
-  // approximate-count mode (R22): fewer than k may have been selected
-  if (S.approx) {
-    const uint32_t total = above + need;
-    for (uint32_t q = total + tid; q < S.k; q += kThreads) {
-      out_idx[q] = 0xFFFFFFFFu;
-      out_val[q] = 0.0f;
-    }
-  }
-  (void)lane;
-}
-
 __global__ void wait_arrivals_kernel(const unsigned long long* cnt, unsigned long long target,
                                      unsigned int* err, unsigned long long timeout_ns) {
   if (threadIdx.x != 0) return;
@@ -1234,9 +1097,9 @@ static void debug_sync(const char* what, cudaStream_t st) {
 
 void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                    const uint32_t* group_seg, int ngroups, cudaStream_t st, cudaEvent_t probe0,
-                   cudaEvent_t probe1, bool mom, const uint32_t* seg_list, int nseg_list) {
+                   cudaEvent_t probe1, bool mom) {
   launch_dgc_stream(segs, nsegs, unit_seg, nunits, st, probe0, probe1, mom);
-  launch_dgc_finalize(segs, nsegs, group_seg, ngroups, st, seg_list, nseg_list);
+  launch_dgc_finalize(segs, nsegs, group_seg, ngroups, st);
 }
 
 void launch_dgc_stream(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits, cudaStream_t st,
@@ -1274,20 +1137,11 @@ void launch_dgc_stream(const SegH1* segs, int nsegs, const uint32_t* unit_seg, i
   count_launches(2);
 }
 
-void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg, int ngroups, cudaStream_t st,
-                         const uint32_t* seg_list, int nseg_list) {
+void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg, int ngroups, cudaStream_t st) {
   if (nsegs == 0) return;
   num_sms();
   launch_pdl(dgc_fallback_kernel, g_num_sms, kThreads, 0, st, segs, nsegs);
   debug_sync("dgc_fallback", st);
-  if (nseg_list > 0) {
-    static const bool attr = cudaFuncSetAttribute(dgc_seg_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)kSegFinSmem) == cudaSuccess;
-    (void)attr;
-    launch_pdl(dgc_seg_finalize_kernel, nseg_list, kThreads, kSegFinSmem, st, segs, seg_list);
-    debug_sync("dgc_seg_finalize", st);
-    count_launches(1);
-  }
   const int wgrid = (ngroups + kWarpsPerCta - 1) / kWarpsPerCta;   // one warp per finalize group
   if (wgrid > 0) {
     launch_pdl(dgc_refine_kernel<2>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);

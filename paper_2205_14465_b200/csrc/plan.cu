@@ -34,7 +34,6 @@ struct Bucket {
   SegH1* h1 = nullptr; int nh1 = 0;
   uint32_t* h1_units = nullptr; int nh1_units = 0;
   uint32_t* h1_groups = nullptr; int nh1_groups = 0;
-  uint32_t* h1_seglist = nullptr; int nh1_seglist = 0;   // DGC segment-path segments (one finalize CTA each)
   SegH1* a7 = nullptr; int na7 = 0;
   uint32_t* a7_units = nullptr; int na7_units = 0;
   const unsigned char** a7_pieces = nullptr;
@@ -175,7 +174,7 @@ struct Layout {
 
 struct HostTables {
   std::vector<SegH1> h1, a7;
-  std::vector<uint32_t> h1_units, h1_groups, h1_seglist, a7_units, a7_groups, h2_units, a7h2_units, a7h2_rankterms;
+  std::vector<uint32_t> h1_units, h1_groups, a7_units, a7_groups, h2_units, a7h2_units, a7h2_rankterms;
   std::vector<SegH2> a7h2;
   std::vector<uint4> a7h2_off_jobs;
   std::vector<SegH2> h2;
@@ -212,25 +211,7 @@ static uint16_t dgc_strata(uint64_t n, double rate) {
 // candidates per 512-element run ~ 512 x (sampled rank / sample size) when
 // sampled, ~ 512 k / n for a whole-segment sample, ~ 1024 k / n for TOPK
 // (the k-th key's 11-bit bin and above)
-static double dgc_cand_frac(uint64_t len, uint32_t k, const esp_compressor_cfg_t& cfg);
-
 static uint32_t dgc_rpg(uint64_t len, uint32_t k, const esp_compressor_cfg_t& cfg) {
-  const double c_run = (double)kRun * dgc_cand_frac(len, k, cfg);
-  uint32_t rpg = kRunsPerGroup;
-  while (rpg > 8 && rpg * c_run > 128.0) rpg /= 2;
-  return rpg;
-}
-
-// the DGC finalize's segment path (one CTA per segment, k_dgc.cu) takes a
-// segment whose run offsets fit shared memory and whose expected candidates
-// fill at most three staging chunks
-static bool dgc_seg_path(uint64_t len, uint32_t k, const esp_compressor_cfg_t& cfg) {
-  const uint64_t nruns = div_up(len, kRun);
-  return nruns <= kSegPathMaxRuns && (double)len * dgc_cand_frac(len, k, cfg) <= 3.0 * 8192.0;
-}
-
-// expected fraction of a segment's elements that become candidates
-static double dgc_cand_frac(uint64_t len, uint32_t k, const esp_compressor_cfg_t& cfg) {
   double frac;
   if (cfg.kind == ESP_TOPK) {
     frac = 2.0 * k / (double)len;
@@ -242,7 +223,10 @@ static double dgc_cand_frac(uint64_t len, uint32_t k, const esp_compressor_cfg_t
     need = need < 1.0 ? 1.0 : (need > s ? s : need);
     frac = need / s;
   }
-  return frac > 1.0 ? 1.0 : frac;
+  const double c_run = (double)kRun * (frac > 1.0 ? 1.0 : frac);
+  uint32_t rpg = kRunsPerGroup;
+  while (rpg > 8 && rpg * c_run > 128.0) rpg /= 2;
+  return rpg;
 }
 
 static void fill_unit_table(std::vector<uint32_t>& units, uint32_t seg, uint32_t count) {
@@ -444,7 +428,6 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
 
   // ---- h1 segments
   const uint32_t h1_first = (uint32_t)T.h1.size();
-  std::vector<bool> segpath;   // DGC: finalized by the segment path (no groups)
   uint32_t unit_cursor = (uint32_t)T.h1_units.size();
   uint32_t group_cursor = (uint32_t)T.h1_groups.size();
   for (int lr = 0; lr < nl; ++lr) {
@@ -505,14 +488,11 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           s.pcount = L.ptr<uint32_t>(L.reserve((size_t)nruns * 8));
         }
         if (none) s.chunk = b.send.base ? b.send.at(lr) + b.coff[ti] : nullptr;
-        const bool segp = dgc && dgc_seg_path(len, s.k, c->cfg);
-        segpath.push_back(segp);
-        if (segp) T.h1_seglist.push_back((uint32_t)(T.h1.size() - h1_first));
         T.h1.push_back(s);
         unit_cursor += nunits;
-        if (dgc && !segp) group_cursor += s.ngroups;
+        if (dgc) group_cursor += s.ngroups;
         fill_unit_table(T.h1_units, (uint32_t)(T.h1.size() - 1 - h1_first), nunits);
-        if (dgc && !segp) fill_unit_table(T.h1_groups, (uint32_t)(T.h1.size() - 1 - h1_first), s.ngroups);
+        if (dgc) fill_unit_table(T.h1_groups, (uint32_t)(T.h1.size() - 1 - h1_first), s.ngroups);
       }
     }
   }
@@ -540,7 +520,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
       s.unit0 = u0;
       u0 += s.nunits;
       s.group0 = g0;
-      if (dgc && !segpath[i]) g0 += s.ngroups;
+      if (dgc) g0 += s.ngroups;
     }
     b.nh1_units = (int)u0;
     b.nh1_groups = dgc ? (int)g0 : 0;
@@ -869,8 +849,6 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
     up(TB.h1, b.h1);
     up(TB.h1_units, b.h1_units);
     up(TB.h1_groups, b.h1_groups);
-    up(TB.h1_seglist, b.h1_seglist);
-    b.nh1_seglist = (int)TB.h1_seglist.size();
     up(TB.a7, b.a7);
     up(TB.a7_units, b.a7_units);
     up(TB.a7_groups, b.a7_groups);
@@ -1237,11 +1215,11 @@ static cudaStream_t run_h1(Plan& p, Bucket& b, cudaStream_t st, cudaStream_t fin
         launch_dgc_stream(b.h1, b.nh1, b.h1_units, b.nh1_units, st, e0, e1, b.momentum != 0.0);
         ESP_CUDA(cudaEventRecord(b.ev_stream, st));
         ESP_CUDA(cudaStreamWaitEvent(fin, b.ev_stream, 0));
-        launch_dgc_finalize(b.h1, b.nh1, b.h1_groups, b.nh1_groups, fin, b.h1_seglist, b.nh1_seglist);
+        launch_dgc_finalize(b.h1, b.nh1, b.h1_groups, b.nh1_groups, fin);
         done = fin;
       } else {
         launch_dgc_h1(b.h1, b.nh1, b.h1_units, b.nh1_units, b.h1_groups, b.nh1_groups, st, e0, e1,
-                      b.momentum != 0.0, b.h1_seglist, b.nh1_seglist);
+                      b.momentum != 0.0);
       }
       break;
     case ESP_RANDOMK: launch_randomk_h1(b.h1, b.h1_units, b.nh1_units, st); break;
