@@ -72,10 +72,10 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2
 //                  divided and written once with coalesced float4 stores -- no
 //                  global read-modify-write.
 // MULTI = false (every segment of the launch has one piece, e.g. a single
-// rank's payload): only the first path, compiled lean (<= 40 registers) so that
-// 12 CTAs = 48 warps per SM keep the zero-fill stores in flight.
+// rank's payload): only the zero fill + touched-word path, no shared memory
+// (assembling dense tiles in shared memory measured slower on BERT-large).
 template <bool MULTI>
-__global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 12) h2_sparse_kernel(const SegH2* __restrict__ segs,
+__global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 1) h2_sparse_kernel(const SegH2* __restrict__ segs,
                                                                  const uint32_t* __restrict__ tile_seg,
                                                                  uint32_t ntiles,
                                                                  const unsigned char* const* __restrict__ pieces) {
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 12) h2_sparse_kernel
   pdl_trigger();
   constexpr int kWarps = kTileThreads / 32;
   constexpr unsigned kFull = 0xffffffffu;
-  // the per-warp 4 KB output tiles (dynamic shared memory)
+  // the per-warp 4 KB accumulation tiles (dynamic shared memory, MULTI only)
   extern __shared__ __align__(16) float acc_all[];
   const int lane = threadIdx.x & 31;
   float* acc = acc_all + (threadIdx.x >> 5) * kTile;
@@ -194,36 +194,18 @@ __global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 12) h2_sparse_kernel
         store4_guard(out, lo + i, S.n, v);
       }
     } else if (!MULTI || np == 1) {
-      // one piece: a tile with many entries (>= 8: 1% ratios) is assembled in
-      // the warp's shared tile (+0, then (+0 + v) / d at each entry) and
-      // written once with full-line stores, so no 4-byte store lands on a line
-      // after its zero fill; a sparser tile is zero-filled straight from
-      // registers and its few entries stored after (measured faster at 0.1%)
+      // one piece: zero fill from registers, then the touched words
       const unsigned char* pc = pieces[S.piece0];
       const uint32_t* idx = reinterpret_cast<const uint32_t*>(pc);
       const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
       uint32_t a, b;
       range(0, &a, &b);
-      if (b - a >= 8) {
-#pragma unroll
-        for (int i = lane * 4; i < kTile; i += 128)
-          *reinterpret_cast<float4*>(acc + i) = make_float4(0.f, 0.f, 0.f, 0.f);
-        __syncwarp();
-        for (uint32_t i = a + lane; i < b; i += 32) {
-          const float v = __fadd_rn(0.f, __ldg(val + i));   // +0 + v: the oracle's sum from +0
-          acc[__ldg(idx + i) - lo] = ones ? v : div(v);
-        }
-        __syncwarp();
-        for (uint32_t i = lane * 4; lo + i < hi; i += 128)
-          store4_guard(out, lo + i, S.n, *reinterpret_cast<const float4*>(acc + i));
-      } else {
-        for (uint32_t i = lane * 4; lo + i < hi; i += 128)
-          store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
-        __syncwarp();   // zero stores before the touched-word stores
-        for (uint32_t i = a + lane; i < b; i += 32) {
-          const float v = __fadd_rn(0.f, __ldg(val + i));
-          out[__ldg(idx + i)] = ones ? v : div(v);
-        }
+      for (uint32_t i = lane * 4; lo + i < hi; i += 128)
+        store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
+      __syncwarp();   // zero stores before the touched-word stores
+      for (uint32_t i = a + lane; i < b; i += 32) {
+        const float v = __fadd_rn(0.f, __ldg(val + i));   // +0 + v: the oracle's sum from +0
+        out[__ldg(idx + i)] = ones ? v : div(v);
       }
     } else {
       for (uint32_t i = lane * 4; lo + i < hi; i += 128) store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
@@ -524,7 +506,7 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
     launch_pdl(h2_sparse_kernel<true>, need < capn ? need : capn, kTileThreads, kSmem, st, segs, tile_seg,
                (uint32_t)ntiles, pieces);
   else
-    launch_pdl(h2_sparse_kernel<false>, need < cap1 ? need : cap1, kTileThreads, kSmem, st, segs, tile_seg,
+    launch_pdl(h2_sparse_kernel<false>, need < cap1 ? need : cap1, kTileThreads, 0, st, segs, tile_seg,
                (uint32_t)ntiles, pieces);
   count_launches(2);
 }
