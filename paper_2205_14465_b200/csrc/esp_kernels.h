@@ -20,6 +20,9 @@ void launch_dgc_h1(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int n
 void launch_dgc_stream(const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits, cudaStream_t st,
                        cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr, bool mom = false);
 void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg, int ngroups, cudaStream_t st);
+// DGC / TOPK h1 of a bucket whose segments all have <= 4096 elements: one
+// kernel, one CTA per segment (k_dgc.cu)
+void launch_dgc_small(const SegH1* segs, int nsegs, cudaStream_t st);
 // block the stream until *cnt >= target (arrivals of a fused collective); after
 // timeout_ns of wall time without them, set *err (mapped host memory) and return
 void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, unsigned int* err,

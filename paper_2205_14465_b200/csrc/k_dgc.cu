@@ -1033,6 +1033,91 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __r
 // and returns; esp_world_check and the next esp_sync* call report it (the
 // consumers of this call then read an incomplete payload).  No __trap: a trap
 // would destroy the CUDA context of the whole process.
+// ------------------------------------------------------------------ small segments
+// A bucket whose segments all have n <= kSample elements (one CTA per segment):
+// the whole h1 -- acc = g + r (momentum: u = m u + g first), the exact k-th
+// key by three radix rounds over the segment in shared memory, the ordered
+// write and the EF update -- in ONE kernel instead of the sample / stream /
+// fallback / refine / write chain, whose per-launch costs dominate at these
+// sizes (P:1280's constant per-kernel overhead).  Same selection as the large
+// pipeline: the top-k by (key desc, idx asc), emitted sorted by index.
+__global__ void __launch_bounds__(kThreads) dgc_small_kernel(const SegH1* __restrict__ segs) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
+  __shared__ float acc[kSample];
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t sh[288];
+  const SegH1& S = segs[blockIdx.x];
+  const uint32_t n = S.n, k = S.k;
+  const int tid = threadIdx.x;
+  const float* g = seg_g(S);
+  for (uint32_t i = tid; i < n; i += kThreads) {
+    float x = __ldg(g + i);
+    if (S.mom) {   // momentum correction (R20): u = fl(fl(m u) + g)
+      x = __fadd_rn(__fmul_rn(S.mcoef, S.mom[i]), x);
+      S.mom[i] = x;
+    }
+    acc[i] = S.ef ? __fadd_rn(x, S.r[i]) : x;
+  }
+  __syncthreads();
+  // exact k-th key: 11 + 10 + 10 bits
+  uint32_t prefix = 0, need = k, above = 0;
+#pragma unroll 1
+  for (int round = 1; round <= 3; ++round) {
+    const int nb = round == 1 ? 2048 : 1024;
+    const int shift_bin = round == 1 ? 20 : round == 2 ? 10 : 0;
+    const int shift_match = round == 2 ? 20 : 10;
+    for (int b = tid; b < nb; b += kThreads) hist[b] = 0;
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += kThreads) {
+      const uint32_t key = fkey(acc[i]);
+      if (round == 1 || (key >> shift_match) == prefix) atomicAdd(&hist[(key >> shift_bin) & (nb - 1)], 1u);
+    }
+    __syncthreads();
+    uint32_t bin, ab;
+    select_bin<0, false>(hist, nb, need, &bin, &ab, sh);
+    prefix = round == 1 ? bin : ((prefix << 10) | bin);
+    above += ab;
+    need -= ab;
+  }
+  const uint32_t T = prefix;
+  // ordered write: a contiguous run of elements per thread
+  const uint32_t per = (n + kThreads - 1) / kThreads;
+  const uint32_t q0 = min(n, tid * per), q1 = min(n, q0 + per);
+  uint32_t na = 0, nt = 0;
+  for (uint32_t q = q0; q < q1; ++q) {
+    const uint32_t key = fkey(acc[q]);
+    na += key > T;
+    nt += key == T;
+  }
+  uint32_t ta, tt;
+  uint32_t ab = block_excl_scan<0>(na, &ta, sh);
+  uint32_t tb = block_excl_scan<0>(nt, &tt, sh);
+  uint32_t* out_idx = reinterpret_cast<uint32_t*>(S.chunk);
+  float* out_val = reinterpret_cast<float*>(S.chunk + 4 * (size_t)S.kpad);
+  for (uint32_t q = q0; q < q1; ++q) {
+    const float a = acc[q];
+    const uint32_t key = fkey(a);
+    const bool is_above = key > T, is_tie = key == T;
+    const bool sel = is_above || (is_tie && tb < need);
+    if (sel) {
+      const uint32_t pos = ab + min(tb, need);
+      out_idx[pos] = q;
+      out_val[pos] = a;
+      if (S.mom) S.mom[q] = 0.0f;   // momentum factor masking (R20)
+    }
+    if (S.ef) S.r[q] = sel ? 0.0f : a;
+    ab += is_above;
+    tb += is_tie;
+  }
+}
+
+void launch_dgc_small(const SegH1* segs, int nsegs, cudaStream_t st) {
+  if (nsegs == 0) return;
+  launch_pdl(dgc_small_kernel, nsegs, kThreads, 0, st, segs);
+  count_launches(1);
+}
+
 __global__ void wait_arrivals_kernel(const unsigned long long* cnt, unsigned long long target,
                                      unsigned int* err, unsigned long long timeout_ns) {
   if (threadIdx.x != 0) return;

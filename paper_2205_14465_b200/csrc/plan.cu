@@ -53,6 +53,7 @@ struct Bucket {
   uint4* h2_off_jobs = nullptr; int nh2_off_jobs = 0;
   int h2_max_pieces = 0;
   uint32_t h1_max_len = 0, a7_max_len = 0;   // longest h1 / a7 segment
+  bool small = false;          // DGC: every h1 segment has <= kSample elements (one-kernel h1)
   cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr, ev_stream = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
@@ -499,6 +500,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
   b.nh1 = (int)(T.h1.size() - h1_first);
   b.h1_max_len = 0;
   for (int i = 0; i < b.nh1; ++i) b.h1_max_len = std::max(b.h1_max_len, T.h1[h1_first + i].n);
+  b.small = dgc && b.h1_max_len <= (uint32_t)kSample;
   {
     // algorithmic bytes of the streaming h1 pass: read g, read r,
     // write r = 12 B/elem with EF (4 B/elem without); sign adds 1/8 B/elem of
@@ -1211,7 +1213,11 @@ static cudaStream_t run_h1(Plan& p, Bucket& b, cudaStream_t st, cudaStream_t fin
   if (e0 && !dgc && !sign) ESP_CUDA(cudaEventRecord(e0, st));
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
-      if (fin) {
+      if (b.small) {   // every segment fits one CTA: the whole h1 in one kernel
+        if (e0) ESP_CUDA(cudaEventRecord(e0, st));
+        launch_dgc_small(b.h1, b.nh1, st);
+        if (e1) ESP_CUDA(cudaEventRecord(e1, st));
+      } else if (fin) {
         launch_dgc_stream(b.h1, b.nh1, b.h1_units, b.nh1_units, st, e0, e1, b.momentum != 0.0);
         ESP_CUDA(cudaEventRecord(b.ev_stream, st));
         ESP_CUDA(cudaStreamWaitEvent(fin, b.ev_stream, 0));
