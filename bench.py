@@ -395,12 +395,18 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
         # one process per GPU: re-launch under torch.distributed.run; rank 0 prints the line
         import socket
-        with socket.socket() as so:
-            so.bind(("127.0.0.1", 0))
-            port = so.getsockname()[1]
-        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
-        sys.exit(subprocess.run(cmd).returncode)
+        for attempt in range(3):   # a fresh port again if the rendezvous never came up (port taken meanwhile)
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+            p = subprocess.run(cmd, stdout=subprocess.PIPE, text=True)
+            sys.stdout.write(p.stdout)
+            sys.stdout.flush()
+            if p.returncode == 0 or p.stdout.strip():
+                break
+        sys.exit(p.returncode)
     _claim_stdout()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -600,7 +606,11 @@ def main():
                     "achieved_GBps": push_b / (comm_ms * 1e-3) / 1e9 if comm_ms else None,
                     "peak_GBps": 770.0, "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
                     "frac": (push_b / (comm_ms * 1e-3) / 1e9) / 770.0 if comm_ms else None}
-            if nvl0 and nvl1 and "tx" in nvl0 and "tx" in nvl1:
+            if (nvl0 and nvl1 and "tx" in nvl0 and "tx" in nvl1 and nvl1["tx"] == nvl0["tx"]
+                    and nvl1["rx"] == nvl0["rx"] and push_b > 0):
+                link["nvml"] = ("NVML NVLink byte counters do not advance on this pool; the link bytes are "
+                                "measured with ncu nvltx__bytes (profiles/r02_push_nvlink.md)")
+            elif nvl0 and nvl1 and "tx" in nvl0 and "tx" in nvl1:
                 link["nvml_tx_bytes_per_step"] = (nvl1["tx"] - nvl0["tx"]) / args.steps
                 link["nvml_rx_bytes_per_step"] = (nvl1["rx"] - nvl0["rx"]) / args.steps
                 link["nvml_source"] = nvl1["source"]

@@ -266,6 +266,31 @@ __device__ __forceinline__ bool last_cta(uint32_t* counter, uint32_t expected, i
 constexpr int kSignLutPieces = 8;
 __device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
+// The 8 index bytes of 8 consecutive elements at once: byte q of each of the
+// 8 pieces' words (zero words for absent pieces) gathered into a 64-bit 8x8
+// bit matrix M[r][e] = piece r's bit of element e (byte r = lo/hi byte r & 3),
+// transposed in registers (three delta swaps) so that byte e holds element e's
+// np bits = its table index.  ~27 integer ops per 8 elements instead of 4 per
+// piece and element.
+__device__ __forceinline__ void sign_index8(const uint32_t (&w)[8], uint32_t q, uint32_t& lo, uint32_t& hi) {
+  const uint32_t sel = q | ((q + 4u) << 4);   // [a.q, b.q]
+  lo = __byte_perm(__byte_perm(w[0], w[1], sel), __byte_perm(w[2], w[3], sel), 0x5410);
+  hi = __byte_perm(__byte_perm(w[4], w[5], sel), __byte_perm(w[6], w[7], sel), 0x5410);
+  uint32_t t;
+  t = (lo ^ (lo >> 7)) & 0x00AA00AAu; lo ^= t ^ (t << 7);
+  t = (hi ^ (hi >> 7)) & 0x00AA00AAu; hi ^= t ^ (t << 7);
+  t = (lo ^ (lo >> 14)) & 0x0000CCCCu; lo ^= t ^ (t << 14);
+  t = (hi ^ (hi >> 14)) & 0x0000CCCCu; hi ^= t ^ (t << 14);
+  t = (lo ^ (hi << 4)) & 0xF0F0F0F0u; lo ^= t; hi ^= t >> 4;
+}
+
+// one 32-byte store (STG.256 on sm_100) of 8 consecutive floats; p 32-byte aligned
+__device__ __forceinline__ void st8(float* p, const float (&v)[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
 // ---- programmatic dependent launch (PDL) ------------------------------------------
 // The kernels of a call form one chain on the caller's stream (sample ->
 // stream -> fallback -> refine -> write -> h2 ...).  Each is launched with

@@ -286,6 +286,7 @@ void stage_A_push(HierPlan& h, cudaStream_t st) {
   launch_push(h.pushA, h.npushA, h.sendA, h.dstA + par * h.g, h.cntA + par * h.g, st);
   const uint64_t v = 4ull * (h.S / 4) * (h.g - 1);   // logical: my g - 1 shards out, theirs in
   count_coll(h.w, 0, ESP_OP_REDUCESCATTER, v, v);
+  h.w->counters[0].pushed += v;
 }
 void stage_A_sum(HierPlan& h, cudaStream_t st) {
   const int par = (int)(h.epoch & 1);
@@ -297,6 +298,7 @@ void stage_C_push(HierPlan& h, cudaStream_t st) {
   launch_push(h.pushC, h.npushC, h.mid, h.dstC + par * h.g, h.cntC + par * h.g, st);
   const uint64_t v = 4ull * (h.S / 4) * (h.g - 1);
   count_coll(h.w, 0, ESP_OP_ALLGATHER, v, v);
+  h.w->counters[0].pushed += v;
 }
 void stage_C_unpack(HierPlan& h, cudaStream_t st) {
   const int par = (int)(h.epoch & 1);
