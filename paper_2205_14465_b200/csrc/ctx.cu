@@ -422,7 +422,8 @@ esp_status_t esp_decompress(esp_ctx_t c, const void* const* pieces, int npieces,
   const uint32_t* drt = reinterpret_cast<const uint32_t*>(d + off_rt);
   switch (c->cfg.kind) {
     case ESP_DGC: case ESP_TOPK:
-      launch_h2_sparse(dseg, dunits, (int)u0, reinterpret_cast<const uint4*>(d + off_ps), njobs, dpp, npieces, st);
+      launch_h2_sparse(dseg, dunits, (int)u0, reinterpret_cast<const uint4*>(d + off_ps), njobs, dpp, npieces,
+                       h2_sparse_dense((double)c->kpad * npieces, (double)c->N), st);
       break;
     case ESP_RANDOMK: launch_h2_randomk(dseg, dunits, (int)u0, dpp, drt, st); break;
     case ESP_EFSIGNSGD: launch_h2_sign(K_EFSIGN, dseg, dunits, (int)u0, dpp, npieces, st); break;

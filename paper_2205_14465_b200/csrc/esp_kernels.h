@@ -53,8 +53,13 @@ void launch_pack(const SegH1* segs, const uint32_t* unit_seg, int nunits, cudaSt
 // jobs: {segment, piece within segment, first entry, 0}, kOffJob entries each
 // max_pieces: the largest npieces of the launch's segments (> 1 enables the
 // shared-memory accumulation path and its dynamic shared memory)
+// dense: several pieces expected to put > 32 entries into a 1024-element tile
+// (the shared-memory CTA-tile kernel, no tile-offset pass); else the offset
+// pass + one warp per 1024-element tile
 void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
-                      const unsigned char* const* pieces, int max_pieces, cudaStream_t st);
+                      const unsigned char* const* pieces, int max_pieces, bool dense, cudaStream_t st);
+// the bucket-level choice of launch_h2_sparse: sum(kpad x npieces) x 1024 > 32 x sum(n)
+inline bool h2_sparse_dense(double entries, double elems) { return entries * 1024.0 > 32.0 * elems; }
 // max_pieces: the largest npieces of the launch's segments (sizes the shared-memory word stage)
 void launch_h2_sign(int kind, const SegH2* segs, const uint32_t* unit_seg, int nunits,
                     const unsigned char* const* pieces, int max_pieces, cudaStream_t st);

@@ -16,7 +16,7 @@ constexpr int kDgcTile = 8 * kRun;       // DGC streaming tile (one run per cons
 constexpr int kSignSpan = 1024;          // sign h1: elements per warp per unit
 constexpr int kUnit = 8192;              // 8 runs per CTA
 constexpr int kSignUnit = 8192;  // sign h2: elements per CTA (one prologue per 128 KB of output)
-constexpr int kRunsPerGroup = 64;        // DGC finalize: the longest group (32768 elements); SegH1::rpg per segment
+constexpr int kRunsPerGroup = 128;       // DGC finalize: the longest group (65536 elements); SegH1::rpg per segment
 constexpr int kSample = 4096;            // DGC sampled-threshold sample size
 constexpr int kTile = 1024;      // sparse h2 output tile (one warp each)
 constexpr int kTileThreads = 128;        // sparse h2 CTA size (4 warps = 4 tiles in flight)
@@ -87,7 +87,7 @@ struct SegH1 {
   // the approximate-count mode (keep what passes the threshold, at most k)
   uint16_t strata;
   uint16_t approx;
-  uint32_t rpg;          // DGC finalize: runs per group (8..64, power of two; planner's choice)
+  uint32_t rpg;          // DGC finalize: runs per group (8..128, power of two; planner's choice)
   uint32_t pad2_;
 };
 

@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
 }
 
 // ------------------------------------------------------------------ 4. refine
-// A finalize group = S.rpg (8..64, a power of two) consecutive runs of one
+// A finalize group = S.rpg (8..128, a power of two) consecutive runs of one
 // segment, owned by ONE WARP: the finalize is a chain of dependent small loads
 // (descriptor, run counts, candidates, counters), so it is throughput-bound on
 // the number of independent chains in flight -- 64 warps per SM, no CTA
@@ -689,8 +689,9 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
 // groups, so each warp's chain of dependent candidate loads stays one or two
 // round trips long.  The group's candidates are addressed as one flat,
 // index-ordered list: off[i] = first flat position of run i (lane l holds
-// runs l * ppl .. l * ppl + ppl - 1, ppl = rpg / 32 or 1).
-static_assert(kRunsPerGroup == 64, "at most two run counts per lane");
+// runs l * ppl .. l * ppl + ppl - 1, ppl = rpg / 32 or 1).  128-run groups
+// (0.1% ratios) keep BERT-large's ~5300 groups within one wave of warps.
+static_assert(kRunsPerGroup == 128, "at most four run counts per lane");
 constexpr int kBatch = 4;   // candidate loads in flight per lane
 // refine: a group with up to this many candidates adds its matches to the
 // global round histogram directly; larger groups (1% ratios, TOPK, fallbacks)
@@ -698,6 +699,7 @@ constexpr int kBatch = 4;   // candidate loads in flight per lane
 // with millions of matches (a 2^28-element tensor at 1%) costs one atomic per
 // (group, non-empty bin) instead of one per match on a few hot bins
 constexpr uint32_t kDirect = 64;
+constexpr int kSepGroupsPerSeg = 256;   // above this mean, the round selects run as kernels
 constexpr int kWarpsPerCta = kThreads / 32;
 
 struct WarpGroup {
@@ -729,14 +731,18 @@ __device__ __forceinline__ WarpGroup warp_group_offsets(const SegH1* segs, const
   const uint32_t rpg = S.rpg;
   const uint32_t run0 = G.g * rpg;
   G.nr = min(rpg, nruns - run0);
-  const uint32_t ppl = rpg > 32 ? 2u : 1u;   // runs per lane
-  const uint32_t i0 = ppl * lane, i1 = i0 + 1;
-  const uint32_t c0 = i0 < G.nr ? __ldcg(S.runcnt + run0 + i0) : 0u;
-  const uint32_t c1 = (ppl == 2 && i1 < G.nr) ? __ldcg(S.runcnt + run0 + i1) : 0u;
-  const uint32_t incl = warp_incl_scan(c0 + c1);
-  const uint32_t ex = incl - c0 - c1;
-  if (i0 < rpg) off[i0] = ex;
-  if (ppl == 2) off[i1] = ex + c0;
+  const uint32_t ppl = rpg > 32 ? rpg / 32 : 1u;   // runs per lane (1, 2 or 4)
+  const uint32_t i0 = ppl * lane;
+  uint32_t c[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) c[j] = ((uint32_t)j < ppl && i0 + j < G.nr) ? __ldcg(S.runcnt + run0 + i0 + j) : 0u;
+  const uint32_t incl = warp_incl_scan(c[0] + c[1] + c[2] + c[3]);
+  uint32_t ex = incl - (c[0] + c[1] + c[2] + c[3]);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if ((uint32_t)j < ppl && i0 + j < rpg) off[i0 + j] = ex;
+    ex += c[j];
+  }
   G.C = __shfl_sync(0xffffffffu, incl, 31);
   if (lane == 31) off[rpg] = incl;
   __syncwarp();
@@ -825,14 +831,19 @@ __device__ __forceinline__ void warp_select_bin(const uint32_t* hist, uint32_t r
   *out_above = m ? ab : 0u;
 }
 
-template <int ROUND>
+// LAST: the warp that completes a segment's round (fence + counter) selects
+// the next 10 bits; else dgc_select_kernel does it after the kernel (segments
+// with thousands of groups: one contended counter and a fence per warp cost
+// more than a launch)
+template <int ROUND, bool LAST>
 __global__ void __launch_bounds__(kThreads, 6) dgc_refine_kernel(const SegH1* __restrict__ segs,
                                                               const uint32_t* __restrict__ group_seg,
                                                               uint32_t ngroups) {
   pdl_wait();     // predecessors in the stream are complete (PDL)
   pdl_trigger();
   __shared__ uint32_t sh_off[kWarpsPerCta][kRunsPerGroup + 1];
-  // 1024 16-bit bins per warp, two per word (a group has <= 64 x 512 candidates < 2^16)
+  // 1024 16-bit bins per warp, two per word (groups of more than 65535
+  // candidates count directly in global memory)
   __shared__ uint32_t sh_hist[kWarpsPerCta][512];
   constexpr int kShiftMatch = ROUND == 2 ? 20 : 10;
   constexpr int kShiftBin = ROUND == 2 ? 10 : 0;
@@ -851,7 +862,8 @@ __global__ void __launch_bounds__(kThreads, 6) dgc_refine_kernel(const SegH1* __
   uint32_t* ghist = ghist_all + 1024u * (G.g % S.hrep);
   // few candidates (the sampled DGC case): global atomics per match; many
   // (TOPK, fallbacks): a warp-private shared histogram, flushed once
-  const bool direct = G.C <= kDirect;
+  // (16-bit warp bins: a group of 128 runs can hold 65536 candidates)
+  const bool direct = G.C <= kDirect || G.C > 0xFFFFu;
   uint32_t* wh = sh_hist[w];
   if (!direct) {
     for (int i = lane; i < 512; i += 32) wh[i] = 0;
@@ -893,6 +905,7 @@ __global__ void __launch_bounds__(kThreads, 6) dgc_refine_kernel(const SegH1* __
       if (h >> 16) atomicAdd(&ghist[2 * i + 1], h >> 16);
     }
   }
+  if (!LAST) return;
   // the warp that completes the segment's round selects the next 10 bits
   uint32_t last = 0;
   __syncwarp();
@@ -906,6 +919,25 @@ __global__ void __launch_bounds__(kThreads, 6) dgc_refine_kernel(const SegH1* __
   uint32_t bin, above;
   warp_select_bin(ghist_all, S.hrep, need, &bin, &above);
   if (lane == 0) {
+    S.st->prefix = (prefix << 10) | bin;
+    S.st->above = __ldcg(&S.st->above) + above;
+    S.st->need = need - above;
+  }
+}
+
+// The round's bin selection for every segment with finalize groups, one warp
+// each, after the refine kernel (the kernel boundary orders the histogram).
+template <int ROUND>
+__global__ void __launch_bounds__(32) dgc_select_kernel(const SegH1* __restrict__ segs) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
+  const SegH1& S = segs[blockIdx.x];
+  if (S.ngroups == 0) return;
+  const uint32_t prefix = __ldcg(&S.st->prefix);
+  const uint32_t need = __ldcg(&S.st->need);
+  uint32_t bin, above;
+  warp_select_bin(S.hist + 4096 + (ROUND == 2 ? 0u : 1024u * S.hrep), S.hrep, need, &bin, &above);
+  if (threadIdx.x == 0) {
     S.st->prefix = (prefix << 10) | bin;
     S.st->above = __ldcg(&S.st->above) + above;
     S.st->need = need - above;
@@ -993,27 +1025,35 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __r
     uint32_t sel_run = ea + min(et, need);
     uint32_t* out_idx = reinterpret_cast<uint32_t*>(S.chunk);
     float* out_val = reinterpret_cast<float*>(S.chunk + 4 * (size_t)S.kpad);
-    uint2 c_next = lane < C ? __ldcg(dense + lane) : make_uint2(0, 0);
-    for (uint32_t q0 = 0; q0 < C; q0 += 32) {
-      const uint32_t q = q0 + lane;
-      const uint2 c = c_next;
-      if (q + 32 < C) c_next = __ldcg(dense + q + 32);
-      const uint32_t key = c.y & 0x7FFFFFFFu;
-      const bool in = q < C;
-      const bool is_above = in && key > T, is_tie = in && key == T;
-      const uint32_t tb = __ballot_sync(0xffffffffu, is_tie);
-      const uint32_t trank = tie_run + __popc(tb & lt_mask);
-      const bool sel = is_above || (is_tie && trank < need);
-      const uint32_t sb = __ballot_sync(0xffffffffu, sel);
-      const uint32_t pos = sel_run + __popc(sb & lt_mask);
-      if (sel) {
-        out_idx[pos] = c.x;
-        out_val[pos] = __uint_as_float(c.y);
-        if (S.ef) S.r[c.x] = 0.0f;
-        if (S.mom) S.mom[c.x] = 0.0f;   // momentum factor masking (R20)
+    // kBatch x 32 candidates in flight per step (large groups at 1% ratios)
+    for (uint32_t q0 = 0; q0 < C; q0 += kBatch * 32) {
+      uint2 cb[kBatch];
+#pragma unroll
+      for (int m = 0; m < kBatch; ++m) {
+        const uint32_t q = q0 + m * 32 + lane;
+        cb[m] = q < C ? __ldcg(dense + q) : make_uint2(0, 0);
       }
-      tie_run += __popc(tb);
-      sel_run += __popc(sb);
+#pragma unroll
+      for (int m = 0; m < kBatch; ++m) {
+        if (q0 + m * 32 >= C) break;   // warp-uniform
+        const uint2 c = cb[m];
+        const uint32_t key = c.y & 0x7FFFFFFFu;
+        const bool in = q0 + m * 32 + lane < C;
+        const bool is_above = in && key > T, is_tie = in && key == T;
+        const uint32_t tb = __ballot_sync(0xffffffffu, is_tie);
+        const uint32_t trank = tie_run + __popc(tb & lt_mask);
+        const bool sel = is_above || (is_tie && trank < need);
+        const uint32_t sb = __ballot_sync(0xffffffffu, sel);
+        const uint32_t pos = sel_run + __popc(sb & lt_mask);
+        if (sel) {
+          out_idx[pos] = c.x;
+          out_val[pos] = __uint_as_float(c.y);
+          if (S.ef) S.r[c.x] = 0.0f;
+          if (S.mom) S.mom[c.x] = 0.0f;   // momentum factor masking (R20)
+        }
+        tie_run += __popc(tb);
+        sel_run += __popc(sb);
+      }
     }
     // approximate-count mode (R22): fewer than k entries may have been sent;
     // the segment's last group pads the rest of [0, k) (the chunk is reused)
@@ -1228,15 +1268,24 @@ void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg
   launch_pdl(dgc_fallback_kernel, g_num_sms, kThreads, 0, st, segs, nsegs);
   debug_sync("dgc_fallback", st);
   const int wgrid = (ngroups + kWarpsPerCta - 1) / kWarpsPerCta;   // one warp per finalize group
+  // many groups per segment (1% ratios on large tensors): selects as kernels
+  const bool sep = ngroups > kSepGroupsPerSeg * nsegs;
   if (wgrid > 0) {
-    launch_pdl(dgc_refine_kernel<2>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
-    debug_sync("dgc_refine<2>", st);
-    launch_pdl(dgc_refine_kernel<3>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
+    if (sep) {
+      launch_pdl(dgc_refine_kernel<2, false>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
+      launch_pdl(dgc_select_kernel<2>, nsegs, 32, 0, st, segs);
+      launch_pdl(dgc_refine_kernel<3, false>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
+      launch_pdl(dgc_select_kernel<3>, nsegs, 32, 0, st, segs);
+    } else {
+      launch_pdl(dgc_refine_kernel<2, true>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
+      debug_sync("dgc_refine<2>", st);
+      launch_pdl(dgc_refine_kernel<3, true>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
+    }
     debug_sync("dgc_refine<3>", st);
     launch_pdl(dgc_write_kernel, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_write", st);
   }
-  count_launches(wgrid > 0 ? 4 : 1);
+  count_launches(wgrid > 0 ? (sep ? 6 : 4) : 1);
 }
 
 }  // namespace esp

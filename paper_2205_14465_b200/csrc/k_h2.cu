@@ -66,16 +66,17 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2
 //                  one entry per lane, equal indices grouped by
 //                  __match_any_sync, each group summed from +0 in lane (= rank)
 //                  order by its lowest lane and stored once;
-//   several, more: the warp's 1024-float shared-memory tile starts at +0, the
-//                  pieces are added in rank order (indices are distinct within a
-//                  piece; __syncwarp orders the pieces), then the tile is
+//   several, more: the warp's 1024-float shared-memory tile starts at +0; the
+//                  entries in rank-major order are added 32 per round (equal
+//                  indices within a round grouped as above, summed in lane =
+//                  rank order onto the earlier rounds' value); then the tile is
 //                  divided and written once with coalesced float4 stores -- no
 //                  global read-modify-write.
 // MULTI = false (every segment of the launch has one piece, e.g. a single
 // rank's payload): only the zero fill + touched-word path, no shared memory
 // (assembling dense tiles in shared memory measured slower on BERT-large).
 template <bool MULTI>
-__global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 1) h2_sparse_kernel(const SegH2* __restrict__ segs,
+__global__ void __launch_bounds__(kTileThreads, MULTI ? 8 : 1) h2_sparse_kernel(const SegH2* __restrict__ segs,
                                                                  const uint32_t* __restrict__ tile_seg,
                                                                  uint32_t ntiles,
                                                                  const unsigned char* const* __restrict__ pieces) {
@@ -149,42 +150,63 @@ __global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 1) h2_sparse_kernel(
       }
     }
     if (MULTI && np > 1 && tot > 32) {
-      // shared-memory accumulation in rank order, one coalesced write
+      // shared-memory accumulation in rank order, one coalesced write.  The
+      // tile's entries in rank-major order (piece, then index) are taken 32 per
+      // round, kRounds rounds' loads in flight at once; inside a round the
+      // lanes holding one index form a group (__match_any_sync) whose lowest
+      // lane adds the members' values in lane (= rank) order to the tile value
+      // left by the earlier rounds (= lower ranks); __syncwarp between rounds.
 #pragma unroll
       for (int i = lane * 4; i < kTile; i += 128)
         *reinterpret_cast<float4*>(acc + i) = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncwarp();
-      // pieces in batches of kH2Batch: the first 32 entries of every piece of
-      // the batch are loaded (all in flight) before the first is added; the
-      // adds then run piece by piece in rank order (indices are distinct
-      // within a piece, __syncwarp orders the pieces)
-      constexpr int kH2Batch = 4;
-      for (uint32_t r0 = 0; r0 < np; r0 += kH2Batch) {
-        uint32_t wi[kH2Batch];
-        float wv[kH2Batch];
-        const unsigned char* pcs[kH2Batch];
-        uint32_t ra[kH2Batch], rb[kH2Batch];
+      constexpr int kRounds = 3;
+      for (uint32_t x0 = 0; x0 < tot; x0 += 32 * kRounds) {
+        uint32_t pr[kRounds], li[kRounds];   // piece and entry of position x0 + 32 q + lane
 #pragma unroll
-        for (int m = 0; m < kH2Batch; ++m) {
-          const uint32_t r = r0 + m < np ? r0 + m : np - 1;   // warp-uniform
-          pcs[m] = reinterpret_cast<const unsigned char*>(__shfl_sync(
-              kFull, reinterpret_cast<unsigned long long>(r < 32 ? pp0 : pp1), r & 31));
-          range(r, &ra[m], &rb[m]);
-          const uint32_t i = ra[m] + lane;
-          const bool ok = r0 + m < np && i < rb[m];
-          wi[m] = ok ? __ldg(reinterpret_cast<const uint32_t*>(pcs[m]) + i) : 0u;
-          wv[m] = ok ? __ldg(reinterpret_cast<const float*>(pcs[m] + 4 * (size_t)S.kpad) + i) : 0.f;
+        for (int q = 0; q < kRounds; ++q) pr[q] = 0xFFFFFFFFu;
+        uint32_t start = 0;
+        for (uint32_t r = 0; r < np; ++r) {
+          uint32_t a, b;
+          range(r, &a, &b);
+#pragma unroll
+          for (int q = 0; q < kRounds; ++q) {
+            const uint32_t x = x0 + 32 * q + lane;
+            if (x - start < b - a) { pr[q] = r; li[q] = a + (x - start); }   // unsigned: start <= x < start + cnt
+          }
+          start += b - a;
+        }
+        uint32_t e[kRounds];
+        float v[kRounds];
+#pragma unroll
+        for (int q = 0; q < kRounds; ++q) {
+          const uint32_t r = pr[q] == 0xFFFFFFFFu ? 0u : pr[q];
+          const unsigned char* pc = reinterpret_cast<const unsigned char*>(
+              __shfl_sync(kFull, reinterpret_cast<unsigned long long>(r < 32 ? pp0 : pp1), r & 31));
+          e[q] = 0x80000000u | (uint32_t)lane;   // no entry: a key no index has
+          v[q] = 0.f;
+          if (pr[q] != 0xFFFFFFFFu) {
+            e[q] = __ldg(reinterpret_cast<const uint32_t*>(pc) + li[q]);
+            v[q] = __ldg(reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad) + li[q]);
+          }
         }
 #pragma unroll
-        for (int m = 0; m < kH2Batch; ++m) {
-          if (r0 + m >= np) break;   // warp-uniform
-          if (ra[m] + lane < rb[m]) acc[wi[m] - lo] = __fadd_rn(acc[wi[m] - lo], wv[m]);
-          const uint32_t* idx = reinterpret_cast<const uint32_t*>(pcs[m]);
-          const float* val = reinterpret_cast<const float*>(pcs[m] + 4 * (size_t)S.kpad);
-          for (uint32_t i = ra[m] + lane + 32; i < rb[m]; i += 32) {   // dense tiles (TOPK, large ratios)
-            const uint32_t w = __ldg(idx + i) - lo;
-            acc[w] = __fadd_rn(acc[w], __ldg(val + i));
+        for (int q = 0; q < kRounds; ++q) {
+          if (x0 + 32 * q >= tot) break;   // warp-uniform
+          const bool mine = pr[q] != 0xFFFFFFFFu;
+          const uint32_t grp = __match_any_sync(kFull, e[q]);
+          const bool lead = mine && __ffs(grp) - 1 == lane;
+          const int gmax = __reduce_max_sync(kFull, (uint32_t)__popc(grp));
+          float s = lead ? acc[e[q] - lo] : 0.f;
+          uint32_t rest = grp;
+          for (int m = 0; m < gmax; ++m) {
+            const float y = __shfl_sync(kFull, v[q], rest ? __ffs(rest) - 1 : lane);
+            if (rest) {
+              s = __fadd_rn(s, y);
+              rest &= rest - 1;
+            }
           }
+          if (lead) acc[e[q] - lo] = s;
           __syncwarp();
         }
       }
@@ -250,6 +272,127 @@ __global__ void __launch_bounds__(kTileThreads, MULTI ? 6 : 1) h2_sparse_kernel(
   }
 }
 
+// Several pieces, dense tiles (expected > 32 entries per 1024 elements, e.g.
+// DGC 1% at n >= 4): one CTA per 8192-element tile, persistent over a
+// CONTIGUOUS range of tiles, assembled in a 32 KB shared-memory accumulator:
+// zero fill; warp w streams piece pc + w's entries from a cursor (the
+// entries are sorted by index: those below the tile's end are the tile's, the
+// rest stay for the next tile -- no tile-offset pass; one warp-wide 32-ary
+// lower_bound per piece where a CTA starts inside a segment); the pieces are
+// added in rank order, one CTA phase per piece (indices are distinct within a
+// piece, so a phase has no conflicts); then divided and written once with
+// coalesced stores.
+constexpr int kCtaTile = 8 * kTile;
+// first position in idx[0, len) holding a value >= target (sorted, warp-wide)
+__device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* idx, uint32_t len, uint32_t target) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = len;   // idx[< lo] < target <= idx[>= hi]
+  while (hi - lo > 32) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t p = lo + lane * step;
+    const bool below = p < hi && __ldg(idx + p) < target;
+    const uint32_t c = __popc(__ballot_sync(0xffffffffu, below));   // probes below: lanes 0..c-1
+    const uint32_t nlo = c ? lo + (c - 1) * step + 1 : lo;
+    const uint32_t nhi = lo + c * step < hi ? lo + c * step : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  const bool below = lo + lane < hi && __ldg(idx + lo + lane) < target;
+  return lo + __popc(__ballot_sync(0xffffffffu, below));
+}
+
+__global__ void __launch_bounds__(kThreads, 5) h2_sparse_cta_kernel(const SegH2* __restrict__ segs,
+                                                                    const uint32_t* __restrict__ tile_seg,
+                                                                    uint32_t ntiles,
+                                                                    const unsigned char* const* __restrict__ pieces) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
+  __shared__ __align__(16) float acc[kCtaTile];
+  __shared__ uint32_t sh_cur[kMaxPieces];   // per piece: the next entry not yet consumed
+  constexpr int L = 4;   // entries per lane in flight
+  constexpr int kW = kThreads / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t nct = (ntiles + 7) / 8;
+  const uint32_t c0 = (uint32_t)((uint64_t)blockIdx.x * nct / gridDim.x);
+  const uint32_t c1 = (uint32_t)((uint64_t)(blockIdx.x + 1) * nct / gridDim.x);
+  uint32_t cur_seg = 0xFFFFFFFFu;
+  for (uint32_t t = c0 * 8; t < min(c1 * 8, ntiles);) {
+    const uint32_t tend = min(c1 * 8, ntiles);
+    const uint32_t sid = tile_seg[t];
+    const SegH2 S = segs[sid];
+    const uint32_t u0 = t - S.unit0;
+    const uint32_t u1 = min(min(tend, S.unit0 + S.nunits), (t & ~7u) + 8) - S.unit0;   // one CTA tile at most
+    t = S.unit0 + u1;
+    const uint32_t lo = u0 * kTile, hi = min(u1 * kTile, S.n), len = hi - lo;   // elements [lo, hi)
+    const uint32_t np = S.npieces;
+    if (sid != cur_seg) {   // a new segment: the cursors at lo (0 at the segment's start)
+      cur_seg = sid;
+      __syncthreads();   // the previous segment's cursors are no longer read
+      for (uint32_t r = w; r < np; r += kW) {
+        const uint32_t c = u0 == 0 ? 0u : warp_lower_bound(reinterpret_cast<const uint32_t*>(pieces[S.piece0 + r]), S.kpad, lo);
+        if (lane == 0) sh_cur[r] = c;
+      }
+    }
+    for (uint32_t i = threadIdx.x * 4; i < len; i += kThreads * 4)
+      *reinterpret_cast<float4*>(acc + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();   // zero fill and cursors
+    for (uint32_t pc = 0; pc < np; pc += kW) {
+      const uint32_t r = pc + w;
+      const uint32_t* idx = nullptr;
+      const float* val = nullptr;
+      uint32_t a = 0;
+      if (r < np) {
+        const unsigned char* pr = pieces[S.piece0 + r];
+        idx = reinterpret_cast<const uint32_t*>(pr);
+        val = reinterpret_cast<const float*>(pr + 4 * (size_t)S.kpad);
+        a = sh_cur[r];
+      }
+      uint32_t e[L];
+      float v[L];
+#pragma unroll
+      for (int m = 0; m < L; ++m) {
+        const uint32_t q = a + lane + 32 * m;
+        e[m] = (r < np && q < S.kpad) ? __ldg(idx + q) : 0xFFFFFFFFu;   // (padding entries are 0xFFFFFFFF)
+        v[m] = (r < np && q < S.kpad) ? __ldg(val + q) : 0.f;
+      }
+      for (uint32_t p = 0; p < (uint32_t)kW && pc + p < np; ++p) {
+        if ((uint32_t)w == p) {
+          uint32_t used = 0;
+          bool more = true;
+#pragma unroll
+          for (int m = 0; m < L; ++m) {
+            const bool in = e[m] < hi;   // sorted: the tile's entries come first
+            if (in) acc[e[m] - lo] = __fadd_rn(acc[e[m] - lo], v[m]);
+            const uint32_t bm = __ballot_sync(0xffffffffu, in);
+            used += __popc(bm);
+            more = more && bm == 0xffffffffu;
+          }
+          for (uint32_t q0 = a + 32 * L; more; q0 += 32) {   // dense tiles (TOPK, large ratios)
+            const uint32_t q = q0 + lane;
+            const uint32_t x = q < S.kpad ? __ldg(idx + q) : 0xFFFFFFFFu;
+            const bool in = x < hi;
+            if (in) acc[x - lo] = __fadd_rn(acc[x - lo], __ldg(val + q));
+            const uint32_t bm = __ballot_sync(0xffffffffu, in);
+            used += __popc(bm);
+            more = bm == 0xffffffffu;
+          }
+          if (lane == 0) sh_cur[r] = a + used;
+        }
+        __syncthreads();
+      }
+    }
+    const bool ones = S.divisor == 1.0f;
+    const Divisor div(S.divisor);
+    float* out = seg_out(S);
+    for (uint32_t i = threadIdx.x * 4; i < len; i += kThreads * 4) {
+      float4 x = *reinterpret_cast<const float4*>(acc + i);
+      if (!ones) x = div(x);
+      store4_guard(out, lo + i, S.n, x);
+    }
+    __syncthreads();   // the accumulator is read before the next tile's zero fill
+  }
+}
+
 // Sign h2: a grid of a few CTAs per SM, each over a contiguous range of the
 // bucket's units (mostly inside one segment), so the dependent prologue of a
 // segment (its table entry, the piece pointers and scales) is paid once per
@@ -268,8 +411,12 @@ constexpr int kSignWords = kSignUnit / 32;           // words per piece and unit
 constexpr int kSignVec = kSignWords / 4;             // uint4 per piece and unit
 constexpr int kSignPre = 4;                          // uint4 per thread in flight (pieces <= 16)
 constexpr int kSignLutBytes = (1 << kSignLutPieces) * 32 * 4;   // 32 KB
+// staged word rows: 8 (zero rows for absent pieces) when the table path can run
+__host__ __device__ constexpr int sign_h2_rows(int max_pieces) {
+  return max_pieces < 2 ? 1 : (max_pieces < kSignLutPieces ? kSignLutPieces : max_pieces);
+}
 __host__ __device__ constexpr size_t sign_h2_smem(int max_pieces) {
-  return (size_t)(max_pieces < 1 ? 1 : max_pieces) * kSignWords * 4 + (max_pieces >= 2 ? kSignLutBytes : 0);
+  return (size_t)sign_h2_rows(max_pieces) * kSignWords * 4 + (max_pieces >= 2 ? kSignLutBytes : 0);
 }
 // 4 CTAs (32 warps) per SM: the output stream needs the stores of many warps
 // in flight (126 registers and 2 CTAs per SM measured 4.5 TB/s)
@@ -283,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 4) h2_sign_kernel(const SegH2* __res
   pdl_trigger();
   extern __shared__ __align__(16) uint32_t sh_dyn[];
   uint32_t* sh_words = sh_dyn;                                   // [npieces][kSignWords]
-  float* sh_lut = reinterpret_cast<float*>(sh_dyn + (max_pieces < 1 ? 1 : max_pieces) * kSignWords);   // [256][32]
+  float* sh_lut = reinterpret_cast<float*>(sh_dyn + sign_h2_rows(max_pieces) * kSignWords);   // [256][32]
   __shared__ float sh_sp[kMaxPieces], sh_sn[kMaxPieces];
   __shared__ const uint32_t* sh_w[kMaxPieces];
   constexpr int kJ = kSignUnit / (kThreads * 4);
@@ -328,6 +475,8 @@ __global__ void __launch_bounds__(kThreads, 4) h2_sign_kernel(const SegH2* __res
 #pragma unroll 8
           for (int c = 0; c < 32; ++c) sh_lut[t * 32 + c] = a;
         }
+        for (uint32_t i = S.npieces * kSignWords + threadIdx.x; i < kSignLutPieces * kSignWords; i += kThreads)
+          sh_words[i] = 0u;   // absent pieces' rows: index bit 0
         __syncthreads();
       }
       have = false;
@@ -406,18 +555,35 @@ __global__ void __launch_bounds__(kThreads, 4) h2_sign_kernel(const SegH2* __res
     }
     __syncthreads();
     if (np <= (uint32_t)kSignLutPieces) {
-      // 4 index bytes per float4: bit r of byte c = piece r's bit of element c
-      const float* lut = sh_lut + lane;
+      // a thread decodes 8 consecutive elements (byte q of a word) per group:
+      // the 8 pieces' bytes transposed into 8 index bytes (sign_index8; words
+      // of pieces >= np are staged zeros), 8 lookups, one 32-byte store --
+      // a warp writes 1 KB contiguous per group
+      const char* lutb = reinterpret_cast<const char*>(sh_lut + lane);
+      const uint32_t q = threadIdx.x & 3u;
+      const bool a32 = (reinterpret_cast<uintptr_t>(out) & 31) == 0;
 #pragma unroll
-      for (int j = 0; j < kJ; ++j) {
-        const uint32_t l = lt + j * kThreads * 4;
-        const uint32_t wi = l >> 5, sh = l & 31;
-        uint32_t idx4 = 0;
-        for (uint32_t r = 0; r < np; ++r) idx4 |= spread4((sh_words[r * kSignWords + wi] >> sh) & 0xFu) << r;
-        const float4 v = make_float4(lut[(idx4 & 0xFFu) * 32], lut[((idx4 >> 8) & 0xFFu) * 32],
-                                     lut[((idx4 >> 16) & 0xFFu) * 32], lut[(idx4 >> 24) * 32]);
-        const uint32_t e = e0 + j * kThreads * 4;
-        if (e < n) store4_guard(out, e, n, v);
+      for (int g = 0; g < kSignUnit / (kThreads * 8); ++g) {
+        const uint32_t grp = g * kThreads + threadIdx.x;   // 8-element group of the unit
+        uint32_t w[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) w[r] = sh_words[r * kSignWords + (grp >> 2)];
+        uint32_t lo, hi;
+        sign_index8(w, q, lo, hi);
+        float v[8];   // table entry [idx][lane]: byte offset idx * 128 + lane * 4
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          v[c] = *reinterpret_cast<const float*>(lutb + (((lo >> (8 * c)) << 7) & 0x7F80u));
+          v[c + 4] = *reinterpret_cast<const float*>(lutb + (((hi >> (8 * c)) << 7) & 0x7F80u));
+        }
+        const uint32_t e = w0 * 32 + grp * 8;
+        if (a32 && e + 8 <= n) {
+          st8(out + e, v);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (e + c < n) out[e + c] = v[c];
+        }
       }
       continue;
     }
@@ -484,8 +650,21 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const SegH1* __restrict_
 }
 
 void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, const uint4* jobs, int njobs,
-                      const unsigned char* const* pieces, int max_pieces, cudaStream_t st) {
+                      const unsigned char* const* pieces, int max_pieces, bool dense, cudaStream_t st) {
   if (ntiles == 0) return;
+  if (max_pieces > 1 && dense) {
+    static const int capc = [] {
+      int dev = 0, sms = 148, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h2_sparse_cta_kernel, kThreads, 0);
+      return sms * (per_sm > 0 ? per_sm : 4);
+    }();
+    const int nct = (ntiles + 7) / 8;
+    launch_pdl(h2_sparse_cta_kernel, nct < capc ? nct : capc, kThreads, 0, st, segs, tile_seg, (uint32_t)ntiles, pieces);
+    count_launches(1);
+    return;
+  }
   launch_pdl(h2_sparse_offsets_kernel, njobs, kThreads, 0, st, segs, jobs, pieces);
   constexpr int kSmem = kTileThreads / 32 * kTile * (int)sizeof(float);
   auto cap = [](const void* fn, int smem) {

@@ -91,7 +91,12 @@ struct SignOp {
           const float psn = __shfl_sync(0xffffffffu, st.qsn0, r);
           a = __fadd_rn(a, ((t >> r) & 1u) ? psp : psn);
         }
-        if (t < (1u << S.npieces)) lut[t] = S.divisor == 1.0f ? a : Divisor(S.divisor)(a);
+        // replicated 16 times, [pattern][lane & 15]: the whole 16 KB scratch
+        if (t < (1u << S.npieces)) {
+          const float v = S.divisor == 1.0f ? a : Divisor(S.divisor)(a);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) lut[t * 16 + c] = v;
+        }
         csync<BAR>();
       }
     }
@@ -105,10 +110,9 @@ struct SignOp {
     float4 xv[kNJ];
 #pragma unroll
     for (int j = 0; j < kNJ; ++j) xv[j] = gv[j];
-    if (DECODE && sw && S.npieces <= (uint32_t)kSignLutPieces) {
-      // staged words, few pieces: the decoded mean by table lookup (identical
-      // to the sequential rank-order sum + division below)
-      const float* lut = &gh.wscr[0][0];
+    if (DECODE && sw && S.npieces <= 3) {
+      // staged words, 1..3 pieces: the index nibbles gathered per piece
+      const float* lut = &gh.wscr[0][0] + (lane & 15);
       const uint32_t lt = (base & (kDgcTile - 1)) + lane * 4;
 #pragma unroll
       for (int j = 0; j < kNJ; ++j) {
@@ -116,7 +120,36 @@ struct SignOp {
         uint32_t idx4 = 0;
         for (uint32_t q = 0; q < S.npieces; ++q)
           idx4 |= spread4((sw[q * (kDgcTile / 32) + (l >> 5)] >> (l & 31)) & 0xFu) << q;
-        xv[j] = make_float4(lut[idx4 & 0xFFu], lut[(idx4 >> 8) & 0xFFu], lut[(idx4 >> 16) & 0xFFu], lut[idx4 >> 24]);
+        xv[j] = make_float4(lut[(idx4 & 0xFFu) * 16], lut[((idx4 >> 8) & 0xFFu) * 16],
+                            lut[((idx4 >> 16) & 0xFFu) * 16], lut[(idx4 >> 24) * 16]);
+      }
+    } else if (DECODE && sw && S.npieces <= (uint32_t)kSignLutPieces) {
+      // staged words, few pieces: the decoded mean by table lookup (identical
+      // to the sequential rank-order sum + division below)
+      // the run's 64 byte groups (8 elements each): lane decodes groups lane
+      // and lane + 32 into 8 index bytes (sign_index8, absent pieces' words
+      // read as 0), then each lane takes the 4 index bytes of its float4 j
+      // from the group's lane (group j * 16 + lane / 2, half lane & 1)
+      const float* lut = &gh.wscr[0][0] + (lane & 15);
+      const uint32_t tw = (base & (kDgcTile - 1)) >> 5;   // the run's first word in the tile
+      const uint32_t np = S.npieces;
+      uint32_t ilo[2], ihi[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t b = lane + 32 * h;
+        uint32_t w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = (uint32_t)q < np ? sw[q * (kDgcTile / 32) + tw + (b >> 2)] : 0u;
+        sign_index8(w, b & 3u, ilo[h], ihi[h]);
+      }
+#pragma unroll
+      for (int j = 0; j < kNJ; ++j) {
+        const int src = (j * 16 + (lane >> 1)) & 31;
+        const uint32_t a = __shfl_sync(0xffffffffu, ilo[j >> 1], src);
+        const uint32_t b = __shfl_sync(0xffffffffu, ihi[j >> 1], src);
+        const uint32_t idx4 = (lane & 1) ? b : a;
+        xv[j] = make_float4(lut[(idx4 & 0xFFu) * 16], lut[((idx4 >> 8) & 0xFFu) * 16], lut[((idx4 >> 16) & 0xFFu) * 16],
+                            lut[(idx4 >> 24) * 16]);
       }
     } else if (DECODE) {
       // rank-order fp32 sum of the decoded chunks from +0, then / divisor (R9);

@@ -51,6 +51,8 @@ struct Bucket {
   const unsigned char** h2_pieces = nullptr;
   uint32_t* h2_rankterms = nullptr;
   uint4* h2_off_jobs = nullptr; int nh2_off_jobs = 0;
+  bool h2_dense = false;     // sparse h2: the CTA-tile kernel (launch_h2_sparse)
+  bool a7h2_dense = false;
   int h2_max_pieces = 0;
   uint32_t h1_max_len = 0, a7_max_len = 0;   // longest h1 / a7 segment
   bool small = false;          // DGC: every h1 segment has <= kSample elements (one-kernel h1)
@@ -208,7 +210,9 @@ static uint16_t dgc_strata(uint64_t n, double rate) {
 }
 
 // DGC finalize group length (runs) of a segment: the largest power of two in
-// [8, 64] whose expected candidate count stays within one refine batch (128):
+// [8, 128] whose expected candidate count stays within 16 refine batches
+// (2048; measured: 8-run groups at 1% made GPT-2's refine + write 180 us --
+// tens of thousands of groups, a long look-back):
 // candidates per 512-element run ~ 512 x (sampled rank / sample size) when
 // sampled, ~ 512 k / n for a whole-segment sample, ~ 1024 k / n for TOPK
 // (the k-th key's 11-bit bin and above)
@@ -226,7 +230,7 @@ static uint32_t dgc_rpg(uint64_t len, uint32_t k, const esp_compressor_cfg_t& cf
   }
   const double c_run = (double)kRun * (frac > 1.0 ? 1.0 : frac);
   uint32_t rpg = kRunsPerGroup;
-  while (rpg > 8 && rpg * c_run > 128.0) rpg /= 2;
+  while (rpg > 8 && rpg * c_run > 2048.0) rpg /= 2;
   return rpg;
 }
 
@@ -661,6 +665,12 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     b.na7_groups = (int)g0;
     b.na7h2 = (int)(T.a7h2.size() - a7h2_first);
     b.na7h2_units = (int)hu0;
+    double e = 0.0, m = 0.0;
+    for (int i = 0; i < b.na7h2; ++i) {
+      e += (double)T.a7h2[a7h2_first + i].kpad * T.a7h2[a7h2_first + i].npieces;
+      m += (double)T.a7h2[a7h2_first + i].n;
+    }
+    b.a7h2_dense = h2_sparse_dense(e, m);
   }
 
   // ---- h2 segments
@@ -772,7 +782,14 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
   }
   b.nh2 = (int)(T.h2.size() - h2_first);
   b.h2_max_pieces = 0;
-  for (int i = 0; i < b.nh2; ++i) b.h2_max_pieces = std::max(b.h2_max_pieces, (int)T.h2[h2_first + i].npieces);
+  double h2_entries = 0.0, h2_elems = 0.0;
+  for (int i = 0; i < b.nh2; ++i) {
+    const SegH2& x = T.h2[h2_first + i];
+    b.h2_max_pieces = std::max(b.h2_max_pieces, (int)x.npieces);
+    h2_entries += (double)x.kpad * x.npieces;
+    h2_elems += (double)x.n;
+  }
+  b.h2_dense = h2_sparse_dense(h2_entries, h2_elems);
   b.nh2_units = (int)u0;
 
   // per critical rank op counts of the cost table
@@ -1268,7 +1285,7 @@ static void run_mid(Plan& p, Bucket& b, cudaStream_t cs) {
       launch_randomk_h1(b.a7, b.a7_units, b.na7_units, cs);
     } else {
       launch_h2_sparse(b.a7h2, b.a7h2_units, b.na7h2_units, b.a7h2_off_jobs, b.na7h2_off_jobs, pieces,
-                       p.w->nranks, cs);
+                       p.w->nranks, b.a7h2_dense, cs);
       dbg("a7 decode (sparse)", cs);
       launch_dgc_h1(b.a7, b.na7, b.a7_units, b.na7_units, b.a7_groups, b.na7_groups, cs);
     }
@@ -1440,7 +1457,7 @@ static void run_h2(Plan& p, Bucket& b, cudaStream_t st) {
   switch (b.kind) {
     case ESP_DGC: case ESP_TOPK:
       launch_h2_sparse(b.h2, b.h2_units, b.nh2_units, b.h2_off_jobs, b.nh2_off_jobs,
-                       (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, b.h2_max_pieces, st);
+                       (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces, b.h2_max_pieces, b.h2_dense, st);
       break;
     case ESP_RANDOMK:
       launch_h2_randomk(b.h2, b.h2_units, b.nh2_units, (b.fused && (b.epoch & 1)) ? b.h2_pieces_odd : b.h2_pieces,
