@@ -130,6 +130,23 @@ esp_status_t esp_ctx_create(esp_world_t w, const esp_compressor_cfg_t* cfg, int 
       ESP_CUDA(cudaMemset(c->lazy2, 0, sizeof(float) * 2 * nl));
     }
   }
+  if ((cfg->kind == ESP_DGC || cfg->kind == ESP_TOPK) && (cfg->error_feedback || cfg->momentum != 0.0)) {
+    // deferred EF zeroing records: capacity for ~ e + 4 sqrt(e) + 8 selected
+    // per 4096-element tile (e = 4096 ratio); a fuller tile zeroes the rest directly
+    const double e = 4096.0 * std::min(1.0, cfg->ratio), want = e + 4.0 * std::sqrt(e) + 8.0;
+    c->zcap = want <= 31.0 ? 32u : want <= 63.0 ? 64u : 128u;
+    for (int p = 0; p < c->P; ++p) {
+      c->zrec_part.push_back(c->zrec_stride);
+      c->zrec_stride += (size_t)div_up(c->phi[p] - c->plo[p], kDgcTile) * c->zcap;
+    }
+    ESP_CUDA(cudaMalloc(&c->zrec, 2 * std::max<size_t>(1, c->zrec_stride * nl)));
+    ESP_CUDA(cudaMemset(c->zrec, 0, 2 * std::max<size_t>(1, c->zrec_stride * nl)));
+    if (c->r2 && cfg->error_feedback) {
+      c->zrec2_stride = (size_t)div_up(c->r2_len, kDgcTile) * c->zcap;
+      ESP_CUDA(cudaMalloc(&c->zrec2, 2 * std::max<size_t>(1, c->zrec2_stride * nl)));
+      ESP_CUDA(cudaMemset(c->zrec2, 0, 2 * std::max<size_t>(1, c->zrec2_stride * nl)));
+    }
+  }
   w->ctxs.insert(c.get());
   *out = c.release();
   ESP_API_END
@@ -148,6 +165,8 @@ esp_status_t esp_ctx_destroy(esp_ctx_t c) {
   cudaFree(c->r2);
   cudaFree(c->lazy2);
   cudaFree(c->u);
+  cudaFree(c->zrec);
+  cudaFree(c->zrec2);
   if (c->dec.d) cudaFree(c->dec.d);
   if (c->dec.acc) cudaFree(c->dec.acc);
   if (c->dec.h) cudaFreeHost(c->dec.h);
@@ -172,6 +191,25 @@ static uint64_t r2_valid(esp_ctx_t c, int lr) {
   return j == 0 ? c->N : 0;
 }
 
+// The pending deferred EF zeroing of every segment of c applied to r / u / r2
+// in memory (records cleared): the state is then the plain residual.
+static void apply_zrec(esp_ctx_s* c) {
+  const int nl = c->w->nlocal;
+  for (int lr = 0; lr < nl; ++lr) {
+    if (c->zrec)
+      for (int p = 0; p < c->P; ++p) {
+        const size_t off = (size_t)lr * c->N + c->plo[p];
+        launch_dgc_zrec_apply(c->cfg.error_feedback ? c->r + off : nullptr, c->u ? c->u + off : nullptr,
+                              c->zrec + (size_t)lr * c->zrec_stride + c->zrec_part[p], c->zcap, c->phi[p] - c->plo[p], 0);
+      }
+    if (c->zrec2)
+      launch_dgc_zrec_apply(c->r2 + (size_t)lr * c->r2_len, nullptr, c->zrec2 + (size_t)lr * c->zrec2_stride, c->zcap,
+                            (uint32_t)c->r2_len, 0);
+  }
+  ESP_CUDA(cudaGetLastError());
+  ESP_CUDA(cudaDeviceSynchronize());
+}
+
 esp_status_t esp_ctx_get_state(esp_ctx_t c, void* host_buf, size_t* nbytes) {
   ESP_API_BEGIN
   ESP_REQUIRE(c && nbytes, ESP_ERR_INVALID_ARG, "null argument");
@@ -188,6 +226,7 @@ esp_status_t esp_ctx_get_state(esp_ctx_t c, void* host_buf, size_t* nbytes) {
   ESP_REQUIRE(*nbytes >= need, ESP_ERR_INVALID_ARG, "state buffer too small");
   ESP_CUDA(cudaSetDevice(c->w->dev));
   ESP_CUDA(cudaDeviceSynchronize());
+  apply_zrec(c);
   StateHeader h{kStateMagic, c->step, c->N, c->r2_len, (uint64_t)nl};
   std::memcpy(host_buf, &h, sizeof(h));
   float* out = reinterpret_cast<float*>((unsigned char*)host_buf + sizeof(h));
@@ -239,6 +278,7 @@ esp_status_t esp_ctx_set_state(esp_ctx_t c, const void* host_buf, size_t nbytes)
   ESP_REQUIRE(nbytes >= sizeof(h) + (size_t)nl * 4 * (c->N + c->r2_len), ESP_ERR_INVALID_ARG, "blob truncated");
   ESP_CUDA(cudaSetDevice(c->w->dev));
   ESP_CUDA(cudaDeviceSynchronize());
+  apply_zrec(c);   // u's pending zeros stay applied; r / r2 are overwritten below
   const float* in = reinterpret_cast<const float*>((const unsigned char*)host_buf + sizeof(h));
   for (int lr = 0; lr < nl; ++lr) {
     const float* src = in + (size_t)lr * (c->N + c->r2_len);
@@ -259,6 +299,7 @@ esp_status_t esp_ctx_get_momentum(esp_ctx_t c, float* host, size_t count) {
   ESP_REQUIRE(count == c->N * (size_t)c->w->nlocal, ESP_ERR_INVALID_ARG, "count must be nlocal * numel");
   ESP_CUDA(cudaSetDevice(c->w->dev));
   ESP_CUDA(cudaDeviceSynchronize());
+  apply_zrec(c);
   ESP_CUDA(cudaMemcpy(host, c->u, 4 * count, cudaMemcpyDeviceToHost));
   ESP_API_END
 }
@@ -270,6 +311,7 @@ esp_status_t esp_ctx_set_momentum(esp_ctx_t c, const float* host, size_t count) 
   ESP_REQUIRE(count == c->N * (size_t)c->w->nlocal, ESP_ERR_INVALID_ARG, "count must be nlocal * numel");
   ESP_CUDA(cudaSetDevice(c->w->dev));
   ESP_CUDA(cudaDeviceSynchronize());
+  apply_zrec(c);   // r's pending zeros stay applied; u is overwritten below
   ESP_CUDA(cudaMemcpy(c->u, host, 4 * count, cudaMemcpyHostToDevice));
   ESP_API_END
 }

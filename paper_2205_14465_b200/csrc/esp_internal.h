@@ -138,6 +138,13 @@ struct esp_ctx_s {
   float* r2 = nullptr;               // nlocal * r2_len   (second residual, R11)
   float* lazy2 = nullptr;            // nlocal * 2
   float* u = nullptr;                // nlocal * N: DGC momentum buffer (cfg.momentum != 0)
+  // DGC / TOPK deferred EF zeroing records (k_dgc.cu), per local rank: the
+  // 4096-element tiles of every partition of r (zrec) and of r2 (zrec2)
+  uint16_t* zrec = nullptr;
+  uint16_t* zrec2 = nullptr;
+  uint32_t zcap = 0;                 // uint16 per tile record (32, 64 or 128)
+  std::vector<size_t> zrec_part;     // partition p's first record inside a rank's block
+  size_t zrec_stride = 0, zrec2_stride = 0;
   uint64_t r2_len = 0;
   uint64_t step = 0;
   uint64_t hash_base = 0;            // mix(mix(seed) ^ tensor_id)

@@ -23,6 +23,9 @@ void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg
 // DGC / TOPK h1 of a bucket whose segments all have <= 4096 elements: one
 // kernel, one CTA per segment (k_dgc.cu)
 void launch_dgc_small(const SegH1* segs, int nsegs, cudaStream_t st);
+// DGC deferred EF zeroing: apply a segment's pending records to r / u (either
+// may be null) and clear them
+void launch_dgc_zrec_apply(float* r, float* u, uint16_t* zrec, uint32_t zcap, uint32_t n, cudaStream_t st);
 // block the stream until *cnt >= target (arrivals of a fused collective); after
 // timeout_ns of wall time without them, set *err (mapped host memory) and return
 void launch_wait_arrivals(const unsigned long long* cnt, unsigned long long target, unsigned int* err,
@@ -43,7 +46,8 @@ void launch_randomk_h1(const SegH1* segs, const uint32_t* unit_seg, int nunits, 
 void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                         const unsigned char* const* pieces, cudaStream_t st,
                         uint32_t max_len = 0,    // the longest segment (sizes the finalize grid)
-                        cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr);
+                        cudaEvent_t probe0 = nullptr, cudaEvent_t probe1 = nullptr,
+                        int max_pieces = 0);   // a7: pieces per segment (selects the decode variant)
 // out[i] = fl(out[i] + x[i]) (esp_decompress with accumulate)
 void launch_add(float* out, const float* x, uint32_t n, cudaStream_t st);
 // NONE: pack gradients into a contiguous buffer (k_h2.cu)

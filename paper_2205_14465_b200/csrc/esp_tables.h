@@ -88,8 +88,14 @@ struct SegH1 {
   uint16_t strata;
   uint16_t approx;
   uint32_t rpg;          // DGC finalize: runs per group (8..128, power of two; planner's choice)
-  uint32_t pad2_;
+  // DGC deferred EF zeroing: per 4096-element tile a record of zcap uint16,
+  // [0] = count, then the tile offsets of the previous call's selection, whose
+  // r (and u) still hold their acc and are read as +0 by the next streaming
+  // pass (nullptr: the write kernel zeroes r / u directly)
+  uint32_t zcap;
+  uint16_t* zrec;
 };
+constexpr int kZRecMax = 128;   // the largest record (256 B)
 
 // DGC histogram words of a segment: 2048 (stream) + 2048 (fallback) + 1024 x hrep
 // (round 2) + 1024 x hrep (round 3).  A round's matches number about k, all

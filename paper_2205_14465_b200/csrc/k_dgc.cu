@@ -259,9 +259,10 @@ struct StreamSmem {   // followed (128-byte aligned) by `ns` stages of {g[kDgcTi
   GroupSmem grp[kMaxGroups];
 };
 constexpr size_t kStreamHdr = (sizeof(StreamSmem) + 127) / 128 * 128;
-constexpr size_t kStageBytes = 2 * kDgcTile * sizeof(float);
+// a stage: g and r tiles, then the tile's deferred-zeroing record (kZRecMax uint16)
+constexpr size_t kStageBytes = 2 * kDgcTile * sizeof(float) + kZRecMax * 2;
 // momentum correction (R20): a third tile per stage holds u
-constexpr size_t kStageBytesMom = 3 * kDgcTile * sizeof(float);
+constexpr size_t kStageBytesMom = 3 * kDgcTile * sizeof(float) + kZRecMax * 2;
 constexpr int kMaxStagesMom = 4;   // 4 x 48 KB + header
 template <bool MOM = false>
 __device__ __forceinline__ float* stage_g(unsigned char* smem, int s) {
@@ -271,6 +272,10 @@ template <bool MOM = false>
 __device__ __forceinline__ float* stage_r(unsigned char* smem, int s) { return stage_g<MOM>(smem, s) + kDgcTile; }
 template <bool MOM = false>
 __device__ __forceinline__ float* stage_u(unsigned char* smem, int s) { return stage_g<MOM>(smem, s) + 2 * kDgcTile; }
+template <bool MOM = false>
+__device__ __forceinline__ uint16_t* stage_z(unsigned char* smem, int s) {
+  return reinterpret_cast<uint16_t*>(stage_g<MOM>(smem, s) + (MOM ? 3 : 2) * kDgcTile);
+}
 
 // segment bookkeeping by the 256 consumer threads of a CTA that has finished its
 // share (`units` units) of segment S: flush the private histogram, add the
@@ -399,6 +404,8 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
       const float* gseg = nullptr;
       const float* rseg = nullptr;
       const float* useg = nullptr;
+      const uint16_t* zseg = nullptr;
+      uint32_t zcap = 0;
       bool ef = false;
       uint32_t sid_next = u0 < u1 ? unit_seg[u0] : 0u;
       int stage = 0;
@@ -415,6 +422,8 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
           gseg = seg_g(S);
           rseg = S.r;
           useg = S.mom;
+          zseg = S.zrec;
+          zcap = S.zcap;
           ef = S.ef != 0;
         }
         if (wrapped) mbar_wait(&sm.empty[stage], phase ^ 1);
@@ -425,10 +434,12 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
         const float* um = useg + start;
         const uint32_t bytes = (len * 4) & ~15u;
         if (bytes && al16(g) && (!ef || al16(r)) && (!MOM || al16(um))) {
-          mbar_arrive_expect_tx(&sm.full[stage], bytes * ((ef ? 2 : 1) + (MOM ? 1 : 0)));
+          const uint32_t zb = zseg ? zcap * 2 : 0u;   // the tile's deferred-zeroing record
+          mbar_arrive_expect_tx(&sm.full[stage], bytes * ((ef ? 2 : 1) + (MOM ? 1 : 0)) + zb);
           tma_load_1d(stage_g<MOM>(smem_raw, stage), g, bytes, &sm.full[stage], pol);
           if (ef) tma_load_1d(stage_r<MOM>(smem_raw, stage), r, bytes, &sm.full[stage], pol);
           if (MOM) tma_load_1d(stage_u<MOM>(smem_raw, stage), um, bytes, &sm.full[stage], pol);
+          if (zb) tma_load_1d(stage_z<MOM>(smem_raw, stage), zseg + (size_t)(u - unit0) * zcap, zb, &sm.full[stage], pol);
         } else {
           mbar_arrive(&sm.full[stage]);
         }
@@ -478,6 +489,31 @@ __global__ void __launch_bounds__(NCG * kThreads + 32, 1) dgc_stream_kernel(cons
     float4 av[kNJ];
     float4 um[MOM ? kNJ : 1];   // MOM: u' = fl(fl(m u) + g), stored after the stage is released
     mbar_wait(&sm.full[stage], phase);
+    if (S.zrec) {
+      // the previous call's selection in this warp's run reads r = u = +0
+      // (deferred EF zeroing: the write kernel recorded it instead of scattering
+      // zeros into r); in the staged tile, or in memory for an unstaged one
+      const uint32_t len = min((uint32_t)kDgcTile, n - start);
+      const uint32_t sb = (len * 4) & ~15u;
+      const bool staged = sb && al16(g + start) && (!S.ef || al16(S.r + start)) && (!MOM || al16(S.mom + start));
+      const uint16_t* z = staged ? stage_z<MOM>(smem_raw, stage) : S.zrec + (size_t)(u - S.unit0) * S.zcap;
+      const uint32_t cnt = min((uint32_t)z[0], S.zcap - 1);
+      bool wrote = false;
+      for (uint32_t i = 1 + lane; i <= cnt; i += 32) {
+        const uint32_t off = z[i];
+        if (off - lbase >= (uint32_t)kRun || start + off >= n) continue;   // another warp's run
+        if (staged && off < sb / 4) {
+          if (S.ef) stage_r<MOM>(smem_raw, stage)[off] = 0.f;
+          if (MOM) stage_u<MOM>(smem_raw, stage)[off] = 0.f;
+          wrote = true;
+        } else {
+          if (S.ef) S.r[start + off] = 0.f;
+          if (MOM) S.mom[start + off] = 0.f;
+        }
+      }
+      if (wrote) fence_proxy_async_smem();   // generic writes into a TMA stage before its reuse
+      __syncwarp();
+    }
     if (full) {
       const float* sg = stage_g<MOM>(smem_raw, stage) + lbase + lane * 4;
       const float* sr = stage_r<MOM>(smem_raw, stage) + lbase + lane * 4;
@@ -692,6 +728,7 @@ __global__ void __launch_bounds__(kThreads) dgc_fallback_kernel(const SegH1* __r
 // runs l * ppl .. l * ppl + ppl - 1, ppl = rpg / 32 or 1).  128-run groups
 // (0.1% ratios) keep BERT-large's ~5300 groups within one wave of warps.
 static_assert(kRunsPerGroup == 128, "at most four run counts per lane");
+static_assert(kDgcTile == 4096, "deferred-zeroing records address tiles as idx >> 12");
 constexpr int kBatch = 4;   // candidate loads in flight per lane
 // refine: a group with up to this many candidates adds its matches to the
 // global round histogram directly; larger groups (1% ratios, TOPK, fallbacks)
@@ -869,6 +906,11 @@ __global__ void __launch_bounds__(kThreads, 6) dgc_refine_kernel(const SegH1* __
     for (int i = lane; i < 512; i += 32) wh[i] = 0;
     __syncwarp();
   }
+  // round 3 also leaves the write kernel a per-group record (in the run-count
+  // slots 1..3 of the group, free once round 2 made the list dense): the
+  // candidates above the 21-bit bin of T, those inside it, and up to three of
+  // their low 10 bits -- enough to count #above / #ties of T without a pass
+  uint32_t n_hi = 0, n_in = 0, packed = 0;
   for (uint32_t base = 0; base < G.C; base += kBatch * 32) {   // warp-uniform trip count
     uint2 cv[kBatch];
 #pragma unroll
@@ -889,12 +931,27 @@ __global__ void __launch_bounds__(kThreads, 6) dgc_refine_kernel(const SegH1* __
 #pragma unroll
     for (int m = 0; m < kBatch; ++m) {
       const uint32_t key = cv[m].y & 0x7FFFFFFFu;
-      if (base + m * 32 + lane < G.C && (key >> kShiftMatch) == prefix) {
+      const bool valid = base + m * 32 + lane < G.C;
+      const bool match = valid && (key >> kShiftMatch) == prefix;
+      if (match) {
         const uint32_t bin = (key >> kShiftBin) & 1023u;
         if (direct) atomicAdd(&ghist[bin], 1u);
         else atomicAdd(&wh[bin >> 1], 1u << (16 * (bin & 1)));
       }
+      if (ROUND == 3) {
+        n_hi += __popc(__ballot_sync(0xffffffffu, valid && (key >> kShiftMatch) > prefix));
+        const uint32_t mb = __ballot_sync(0xffffffffu, match);
+        const uint32_t pos = n_in + __popc(mb & ((1u << lane) - 1u));
+        packed |= __reduce_or_sync(0xffffffffu, (match && pos < 3) ? (key & 1023u) << (10 * pos) : 0u);
+        n_in += __popc(mb);
+      }
     }
+  }
+  if (ROUND == 3 && lane == 0) {
+    uint32_t* rec = S.runcnt + (size_t)G.g * S.rpg;
+    rec[1] = n_hi;
+    rec[2] = n_in;
+    rec[3] = packed;
   }
   if (ROUND == 2 && lane == 0) S.runcnt[(size_t)G.g * S.rpg] = G.C;   // the dense count
   if (!direct) {
@@ -945,17 +1002,94 @@ __global__ void __launch_bounds__(32) dgc_select_kernel(const SegH1* __restrict_
 }
 
 // ------------------------------------------------------------------ 5. write
+// Whether element i of S is one of dgc_sample_kernel's sample positions (the
+// same strata and hashed offsets, which do not depend on the step): the next
+// call's sampler reads r and u there directly, so a selected sample position is
+// zeroed in memory at once instead of only recorded (a few per segment).
+__device__ __forceinline__ bool dgc_is_sample(const SegH1& S, uint32_t i) {
+  const uint32_t n = S.n, strata = S.strata;
+  if (S.unsampled) return false;
+  if (n <= (uint32_t)kSample) return true;   // the whole segment is sampled
+  auto lo_of = [&](uint32_t G) -> uint32_t {
+    return strata == 512 ? (uint32_t)(((uint64_t)G * n) >> 9) : (uint32_t)(((uint64_t)G * n) / strata);
+  };
+  uint32_t G = (uint32_t)((float)i / (float)n * (float)strata);   // within a few; corrected below
+  if (G >= strata) G = strata - 1;
+  while (G + 1 < strata && lo_of(G + 1) <= i) ++G;
+  while (G > 0 && lo_of(G) > i) --G;
+  const uint32_t a = lo_of(G), b = lo_of(G + 1);
+  const uint32_t p0 = a + (uint32_t)(((uint64_t)(uint32_t)splitmix64(S.hash ^ G) * (b - a - 7)) >> 32);
+  return i >= p0 && i < p0 + 8;
+}
+
 // Look-back status word of a group: flag (2 bits: 1 aggregate, 2 inclusive
-// prefix) | #above (31 bits) | #ties (31 bits).
+// prefix, 3 exclusive prefix from dgc_scan_kernel) | #above (31 bits) | #ties (31 bits).
 __device__ __forceinline__ unsigned long long lb_pack(uint32_t flag, uint32_t above, uint32_t tie) {
   return ((unsigned long long)flag << 62) | ((unsigned long long)above << 31) | tie;
 }
 
-__global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __restrict__ segs,
+// Every group's output offset when round 3's records cover the whole
+// segment (each group has <= 3 candidates inside T's 21-bit bin): one CTA per
+// segment scans the groups' (#above, #ties) -- a thread per contiguous run of
+// groups, one CTA scan -- and stores each group's EXCLUSIVE prefix (flag 3).
+// The write kernel then needs no look-back: the decoupled look-back walks
+// 32 groups per round trip, i.e. ~100 us for the 4096 groups of a 2^28-element
+// tensor whose aggregates all appear at once.  A segment with a group beyond
+// the records (many equal keys) is left to the look-back.
+__global__ void __launch_bounds__(kThreads) dgc_scan_kernel(const SegH1* __restrict__ segs) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
+  __shared__ uint32_t sh[16];
+  __shared__ int sh_bad;
+  const SegH1& S = segs[blockIdx.x];
+  const uint32_t G = S.ngroups;
+  if (G == 0) return;
+  if (threadIdx.x == 0) sh_bad = 0;
+  __syncthreads();
+  const uint32_t T = __ldcg(&S.st->prefix), b3 = T & 1023u;
+  const uint32_t per = (G + kThreads - 1) / kThreads;
+  const uint32_t g0 = min(G, threadIdx.x * per), g1 = min(G, g0 + per);
+  uint32_t ta = 0, tt = 0;
+  bool bad = false;
+  for (uint32_t g = g0; g < g1; ++g) {
+    const uint32_t* rec = S.runcnt + (size_t)g * S.rpg;
+    const uint32_t r_in = __ldcg(rec + 2), pk = __ldcg(rec + 3);
+    ta += __ldcg(rec + 1);
+    bad |= r_in > 3;
+    for (uint32_t i = 0; i < min(r_in, 3u); ++i) {
+      const uint32_t low = (pk >> (10 * i)) & 1023u;
+      ta += low > b3;
+      tt += low == b3;
+    }
+  }
+  if (bad) sh_bad = 1;
+  uint32_t tot;
+  uint32_t ea = block_excl_scan<0>(ta, &tot, sh);
+  uint32_t et = block_excl_scan<0>(tt, &tot, sh);   // (also orders sh_bad)
+  if (sh_bad) return;   // CTA-uniform
+  unsigned long long* lb = reinterpret_cast<unsigned long long*>(S.gcnt);
+  for (uint32_t g = g0; g < g1; ++g) {
+    lb[g] = lb_pack(3, ea, et);
+    const uint32_t* rec = S.runcnt + (size_t)g * S.rpg;
+    const uint32_t r_in = __ldcg(rec + 2), pk = __ldcg(rec + 3);
+    ea += __ldcg(rec + 1);
+    for (uint32_t i = 0; i < r_in; ++i) {
+      const uint32_t low = (pk >> (10 * i)) & 1023u;
+      ea += low > b3;
+      et += low == b3;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 5) dgc_write_kernel(const SegH1* __restrict__ segs,
                                                              const uint32_t* __restrict__ group_seg,
                                                              uint32_t ngroups) {
   pdl_wait();     // predecessors in the stream are complete (PDL)
   pdl_trigger();
+  __shared__ uint32_t sh_zc[kWarpsPerCta][kRunsPerGroup / 8];   // deferred zeroing: per tile of the group
+  // ... and the group's records, assembled here and stored whole (full
+  // sectors: no DRAM read-modify-write of partly written record lines)
+  __shared__ __align__(16) uint16_t sh_zr[kWarpsPerCta][kRunsPerGroup / 8][kZRecMax];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t gi = blockIdx.x * kWarpsPerCta + w;
@@ -966,65 +1100,94 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __r
     const uint2* dense = group_slots(G);
     const uint32_t T = __ldcg(&S.st->prefix);
     const uint32_t need = __ldcg(&S.st->need);
-    // pass 1: the group's aggregate
-    uint32_t above = 0, tie = 0;
-    for (uint32_t q0 = lane; q0 < C; q0 += kBatch * 32) {
-      uint32_t key[kBatch];
-#pragma unroll
-      for (int m = 0; m < kBatch; ++m) {
-        const uint32_t q = q0 + m * 32;
-        key[m] = q < C ? __ldcg(&dense[q].y) & 0x7FFFFFFFu : 0u;
-      }
-#pragma unroll
-      for (int m = 0; m < kBatch; ++m) {
-        const bool in = q0 + m * 32 < C;
-        above += in && key[m] > T;
-        tie += in && key[m] == T;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      above += __shfl_xor_sync(0xffffffffu, above, o);
-      tie += __shfl_xor_sync(0xffffffffu, tie, o);
-    }
-    // decoupled look-back over the segment's groups, 32 predecessors per step
-    // (lane i reads group g-1-i of the window)
     unsigned long long* lb = reinterpret_cast<unsigned long long*>(S.gcnt);
+    const unsigned long long pre = __ldcg(lb + g);
     uint32_t ea = 0, et = 0;
-    if (lane == 0) atomicExch(&lb[g], lb_pack(g == 0 ? 2 : 1, above, tie));
-    if (g > 0) {
-      int top = (int)g - 1;
-      while (true) {
-        const int j = top - lane;
-        unsigned long long v;
-        if (j >= 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(lb + j) : "memory");
-        else v = lb_pack(2, 0, 0);   // before the first group: an inclusive zero
-        const uint32_t flag = (uint32_t)(v >> 62);
-        if (__any_sync(0xffffffffu, flag == 0)) {
-          __nanosleep(20);
-          continue;   // a predecessor in the window has not published yet
+    if ((uint32_t)(pre >> 62) == 3) {   // dgc_scan_kernel's exclusive prefix
+      ea = (uint32_t)((pre >> 31) & 0x7FFFFFFFu);
+      et = (uint32_t)(pre & 0x7FFFFFFFu);
+    } else {
+      // pass 1: the group's aggregate -- from refine<3>'s record when at most
+      // three candidates fell into T's 21-bit bin (almost always), else counted
+      uint32_t above = 0, tie = 0;
+      const uint32_t* rec = S.runcnt + (size_t)g * S.rpg;
+      const uint32_t r_in = __ldcg(rec + 2);
+      if (r_in <= 3) {
+        if (lane == 0) {
+          const uint32_t b3 = T & 1023u, pk = __ldcg(rec + 3);
+          above = __ldcg(rec + 1);
+          for (uint32_t i = 0; i < r_in; ++i) {
+            const uint32_t low = (pk >> (10 * i)) & 1023u;
+            above += low > b3;
+            tie += low == b3;
+          }
         }
-        const uint32_t inc = __ballot_sync(0xffffffffu, flag == 2);
-        const int lim = inc ? __ffs(inc) - 1 : 31;   // nearest inclusive predecessor
-        uint32_t a = lane <= lim ? (uint32_t)((v >> 31) & 0x7FFFFFFFu) : 0u;
-        uint32_t t = lane <= lim ? (uint32_t)(v & 0x7FFFFFFFu) : 0u;
+      } else
+      for (uint32_t q0 = lane; q0 < C; q0 += kBatch * 32) {
+        uint32_t key[kBatch];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(0xffffffffu, a, o);
-          t += __shfl_xor_sync(0xffffffffu, t, o);
+        for (int m = 0; m < kBatch; ++m) {
+          const uint32_t q = q0 + m * 32;
+          key[m] = q < C ? __ldcg(&dense[q].y) & 0x7FFFFFFFu : 0u;
         }
-        ea += a;
-        et += t;
-        if (inc) break;
-        top -= 32;
+#pragma unroll
+        for (int m = 0; m < kBatch; ++m) {
+          const bool in = q0 + m * 32 < C;
+          above += in && key[m] > T;
+          tie += in && key[m] == T;
+        }
       }
-      if (lane == 0) atomicExch(&lb[g], lb_pack(2, ea + above, et + tie));
-    }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        above += __shfl_xor_sync(0xffffffffu, above, o);
+        tie += __shfl_xor_sync(0xffffffffu, tie, o);
+      }
+      // decoupled look-back over the segment's groups, 32 predecessors per step
+      // (lane i reads group g-1-i of the window)
+      if (lane == 0) atomicExch(&lb[g], lb_pack(g == 0 ? 2 : 1, above, tie));
+      if (g > 0) {
+        int top = (int)g - 1;
+        while (true) {
+          const int j = top - lane;
+          unsigned long long v;
+          if (j >= 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(lb + j) : "memory");
+          else v = lb_pack(2, 0, 0);   // before the first group: an inclusive zero
+          const uint32_t flag = (uint32_t)(v >> 62);
+          if (__any_sync(0xffffffffu, flag == 0)) {
+            __nanosleep(20);
+            continue;   // a predecessor in the window has not published yet
+          }
+          const uint32_t inc = __ballot_sync(0xffffffffu, flag == 2);
+          const int lim = inc ? __ffs(inc) - 1 : 31;   // nearest inclusive predecessor
+          uint32_t a = lane <= lim ? (uint32_t)((v >> 31) & 0x7FFFFFFFu) : 0u;
+          uint32_t t = lane <= lim ? (uint32_t)(v & 0x7FFFFFFFu) : 0u;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            t += __shfl_xor_sync(0xffffffffu, t, o);
+          }
+          ea += a;
+          et += t;
+          if (inc) break;
+          top -= 32;
+        }
+        if (lane == 0) atomicExch(&lb[g], lb_pack(2, ea + above, et + tie));
+      }
+    }   // look-back path
     // pass 2: ordered selection; selected before this group = above_before + min(ties_before, need)
     uint32_t tie_run = et;
     uint32_t sel_run = ea + min(et, need);
     uint32_t* out_idx = reinterpret_cast<uint32_t*>(S.chunk);
     float* out_val = reinterpret_cast<float*>(S.chunk + 4 * (size_t)S.kpad);
+    // deferred EF zeroing: the group's tiles (rpg / 8 of them) get records of
+    // their selected offsets (slot = a per-tile shared counter; the order in a
+    // record is immaterial), an overflowing record zeroes r / u directly
+    uint32_t* wz = sh_zc[w];
+    const uint32_t zt0 = g * (S.rpg / 8);
+    if (S.zrec) {
+      if (lane < kRunsPerGroup / 8) wz[lane] = 0u;
+      __syncwarp();
+    }
     // kBatch x 32 candidates in flight per step (large groups at 1% ratios)
     for (uint32_t q0 = 0; q0 < C; q0 += kBatch * 32) {
       uint2 cb[kBatch];
@@ -1048,12 +1211,30 @@ __global__ void __launch_bounds__(kThreads, 8) dgc_write_kernel(const SegH1* __r
         if (sel) {
           out_idx[pos] = c.x;
           out_val[pos] = __uint_as_float(c.y);
-          if (S.ef) S.r[c.x] = 0.0f;
-          if (S.mom) S.mom[c.x] = 0.0f;   // momentum factor masking (R20)
+          const bool rec = S.zrec && !dgc_is_sample(S, c.x);
+          const uint32_t slot = rec ? atomicAdd(&wz[(c.x >> 12) - zt0], 1u) : 0xFFFFFFFFu;
+          if (rec && slot + 1 < S.zcap) {
+            sh_zr[w][(c.x >> 12) - zt0][1 + slot] = (uint16_t)(c.x & (kDgcTile - 1));
+          } else {   // no record, a full one, or a sample position: zeroed now
+            if (S.ef) S.r[c.x] = 0.0f;
+            if (S.mom) S.mom[c.x] = 0.0f;   // momentum factor masking (R20)
+          }
         }
         tie_run += __popc(tb);
         sel_run += __popc(sb);
       }
+    }
+    if (S.zrec) {
+      __syncwarp();
+      const uint32_t ntiles = (S.n + kDgcTile - 1) / kDgcTile;
+      const uint32_t nt = min(S.rpg / 8, ntiles - zt0);
+      if ((uint32_t)lane < nt) sh_zr[w][lane][0] = (uint16_t)min(wz[lane], S.zcap - 1);
+      __syncwarp();
+      // the nt records (zcap uint16 each, contiguous in global memory) as 16-byte stores
+      const uint32_t per = S.zcap / 8;   // uint4 per record
+      uint4* dst = reinterpret_cast<uint4*>(S.zrec + (size_t)zt0 * S.zcap);
+      for (uint32_t q = lane; q < nt * per; q += 32)
+        dst[q] = *reinterpret_cast<const uint4*>(&sh_zr[w][q / per][(q % per) * 8]);
     }
     // approximate-count mode (R22): fewer than k entries may have been sent;
     // the segment's last group pads the rest of [0, k) (the chunk is reused)
@@ -1091,6 +1272,18 @@ __global__ void __launch_bounds__(kThreads) dgc_small_kernel(const SegH1* __rest
   const uint32_t n = S.n, k = S.k;
   const int tid = threadIdx.x;
   const float* g = seg_g(S);
+  if (S.zrec) {   // a pending deferred zeroing (one tile): applied, r is rewritten below
+    const uint32_t cnt = min((uint32_t)S.zrec[0], S.zcap - 1);
+    for (uint32_t i = 1 + tid; i <= cnt; i += kThreads) {
+      const uint32_t off = S.zrec[i];
+      if (off < n) {
+        if (S.ef) S.r[off] = 0.0f;
+        if (S.mom) S.mom[off] = 0.0f;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) S.zrec[0] = 0;
+  }
   for (uint32_t i = tid; i < n; i += kThreads) {
     float x = __ldg(g + i);
     if (S.mom) {   // momentum correction (R20): u = fl(fl(m u) + g)
@@ -1150,6 +1343,32 @@ __global__ void __launch_bounds__(kThreads) dgc_small_kernel(const SegH1* __rest
     ab += is_above;
     tb += is_tie;
   }
+}
+
+// Applies a segment's pending deferred zeroing to r and u in memory and clears
+// the records (state read-out: esp_ctx_get_state / get_momentum).  One warp
+// per tile.
+__global__ void dgc_zrec_apply_kernel(float* r, float* u, uint16_t* zrec, uint32_t zcap, uint32_t n) {
+  const uint32_t t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (t >= (n + kDgcTile - 1) / kDgcTile) return;
+  uint16_t* z = zrec + (size_t)t * zcap;
+  const uint32_t cnt = min((uint32_t)z[0], zcap - 1);
+  for (uint32_t i = 1 + lane; i <= cnt; i += 32) {
+    const uint32_t e = t * kDgcTile + z[i];
+    if (e < n) {
+      if (r) r[e] = 0.0f;
+      if (u) u[e] = 0.0f;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) z[0] = 0;
+}
+
+void launch_dgc_zrec_apply(float* r, float* u, uint16_t* zrec, uint32_t zcap, uint32_t n, cudaStream_t st) {
+  if (!zrec || n == 0) return;
+  const uint32_t ntiles = (n + kDgcTile - 1) / kDgcTile;
+  dgc_zrec_apply_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(r, u, zrec, zcap, n);
+  count_launches(1);
 }
 
 void launch_dgc_small(const SegH1* segs, int nsegs, cudaStream_t st) {
@@ -1282,10 +1501,11 @@ void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg
       launch_pdl(dgc_refine_kernel<3, true>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
     }
     debug_sync("dgc_refine<3>", st);
+    launch_pdl(dgc_scan_kernel, nsegs, kThreads, 0, st, segs);
     launch_pdl(dgc_write_kernel, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_write", st);
   }
-  count_launches(wgrid > 0 ? (sep ? 6 : 4) : 1);
+  count_launches(wgrid > 0 ? (sep ? 7 : 5) : 1);
 }
 
 }  // namespace esp

@@ -55,6 +55,19 @@ __global__ void __launch_bounds__(kThreads) h2_sparse_offsets_kernel(const SegH2
   }
 }
 
+// A warp's zero fill of out[lo, hi) (one 1024-element tile): eight unrolled
+// 16-byte stores per lane for a full aligned tile, else guarded.
+__device__ __forceinline__ void zero_tile(float* out, uint32_t lo, uint32_t hi, uint32_t n) {
+  const int lane = threadIdx.x & 31;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (hi - lo == (uint32_t)kTile && al16(out + lo)) {
+#pragma unroll
+    for (int j = 0; j < kTile / 128; ++j) st4(out + lo + lane * 4 + 128 * j, z);
+  } else {
+    for (uint32_t i = lane * 4; lo + i < hi; i += 128) store4_guard(out, lo + i, n, z);
+  }
+}
+
 // One WARP per output tile, persistent over tiles (stride = all warps of the
 // grid): no CTA barrier anywhere, so 64 independent tiles per SM hide the load
 // latencies of the entry lists (a CTA-wide tile loop was latency-bound).
@@ -222,15 +235,14 @@ __global__ void __launch_bounds__(kTileThreads, MULTI ? 8 : 1) h2_sparse_kernel(
       const float* val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
       uint32_t a, b;
       range(0, &a, &b);
-      for (uint32_t i = lane * 4; lo + i < hi; i += 128)
-        store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
+      zero_tile(out, lo, hi, S.n);
       __syncwarp();   // zero stores before the touched-word stores
       for (uint32_t i = a + lane; i < b; i += 32) {
         const float v = __fadd_rn(0.f, __ldg(val + i));   // +0 + v: the oracle's sum from +0
         out[__ldg(idx + i)] = ones ? v : div(v);
       }
     } else {
-      for (uint32_t i = lane * 4; lo + i < hi; i += 128) store4_guard(out, lo + i, S.n, make_float4(0.f, 0.f, 0.f, 0.f));
+      zero_tile(out, lo, hi, S.n);
       __syncwarp();   // zero stores before the touched-word stores
       {
         // one entry per lane: lanes holding the same index form a group
@@ -272,17 +284,6 @@ __global__ void __launch_bounds__(kTileThreads, MULTI ? 8 : 1) h2_sparse_kernel(
   }
 }
 
-// Several pieces, dense tiles (expected > 32 entries per 1024 elements, e.g.
-// DGC 1% at n >= 4): one CTA per 8192-element tile, persistent over a
-// CONTIGUOUS range of tiles, assembled in a 32 KB shared-memory accumulator:
-// zero fill; warp w streams piece pc + w's entries from a cursor (the
-// entries are sorted by index: those below the tile's end are the tile's, the
-// rest stay for the next tile -- no tile-offset pass; one warp-wide 32-ary
-// lower_bound per piece where a CTA starts inside a segment); the pieces are
-// added in rank order, one CTA phase per piece (indices are distinct within a
-// piece, so a phase has no conflicts); then divided and written once with
-// coalesced stores.
-constexpr int kCtaTile = 8 * kTile;
 // first position in idx[0, len) holding a value >= target (sorted, warp-wide)
 __device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* idx, uint32_t len, uint32_t target) {
   const int lane = threadIdx.x & 31;
@@ -301,6 +302,74 @@ __device__ __forceinline__ uint32_t warp_lower_bound(const uint32_t* idx, uint32
   return lo + __popc(__ballot_sync(0xffffffffu, below));
 }
 
+// One piece per segment (a single rank's payload, an NCCL-reduced bucket's
+// unpack): one WARP per contiguous range of 1024-element tiles, persistent,
+// no tile-offset pass.  The warp keeps a cursor into the piece's sorted
+// entries (a 32-ary lower_bound only where its range starts inside a
+// segment); per tile it issues the next 32 entries' loads, zero-fills the tile
+// from registers (eight 16-byte stores per lane), then stores the tile's
+// entries (those below the tile's end; more batches for dense tiles) as
+// out[e] = (+0 + v) / d and advances the cursor.
+__global__ void __launch_bounds__(kTileThreads) h2_sparse1_kernel(const SegH2* __restrict__ segs,
+                                                                 const uint32_t* __restrict__ tile_seg,
+                                                                 uint32_t ntiles,
+                                                                 const unsigned char* const* __restrict__ pieces) {
+  pdl_wait();     // predecessors in the stream are complete (PDL)
+  pdl_trigger();
+  constexpr int kWarps = kTileThreads / 32;
+  const int lane = threadIdx.x & 31;
+  const uint32_t W = gridDim.x * kWarps, wid = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const uint32_t t0 = (uint32_t)((uint64_t)wid * ntiles / W), t1 = (uint32_t)((uint64_t)(wid + 1) * ntiles / W);
+  uint32_t cur_seg = 0xFFFFFFFFu, cur = 0;
+  SegH2 S{};
+  const uint32_t* idx = nullptr;
+  const float* val = nullptr;
+  for (uint32_t t = t0; t < t1; ++t) {
+    const uint32_t sid = tile_seg[t];
+    if (sid != cur_seg) {
+      cur_seg = sid;
+      S = segs[sid];
+      const unsigned char* pc = pieces[S.piece0];
+      idx = reinterpret_cast<const uint32_t*>(pc);
+      val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
+      cur = t == S.unit0 ? 0u : warp_lower_bound(idx, S.kpad, (t - S.unit0) * kTile);
+    }
+    const uint32_t lo = (t - S.unit0) * kTile, hi = min(lo + (uint32_t)kTile, S.n);
+    uint32_t q = cur + lane;
+    uint32_t e = q < S.kpad ? __ldg(idx + q) : 0xFFFFFFFFu;   // padding entries are 0xFFFFFFFF
+    float v = q < S.kpad ? __ldg(val + q) : 0.f;
+    float* out = seg_out(S);
+    zero_tile(out, lo, hi, S.n);
+    __syncwarp();   // zero stores before the touched-word stores
+    const bool ones = S.divisor == 1.0f;
+    const Divisor div(S.divisor);
+    while (true) {
+      const bool in = e < hi;   // sorted: the tile's entries come first
+      if (in) {
+        const float x = __fadd_rn(0.f, v);   // +0 + v: the oracle's sum from +0
+        out[e] = ones ? x : div(x);
+      }
+      const uint32_t bm = __ballot_sync(0xffffffffu, in);
+      cur += __popc(bm);
+      if (bm != 0xffffffffu) break;
+      q = cur + lane;   // a dense tile: the next 32 entries
+      e = q < S.kpad ? __ldg(idx + q) : 0xFFFFFFFFu;
+      v = q < S.kpad ? __ldg(val + q) : 0.f;
+    }
+  }
+}
+
+// Several pieces, dense tiles (expected > 32 entries per 1024 elements, e.g.
+// DGC 1% at n >= 4): one CTA per 8192-element tile, persistent over a
+// CONTIGUOUS range of tiles, assembled in a 32 KB shared-memory accumulator:
+// zero fill; warp w streams piece pc + w's entries from a cursor (the
+// entries are sorted by index: those below the tile's end are the tile's, the
+// rest stay for the next tile -- no tile-offset pass; one warp-wide 32-ary
+// lower_bound per piece where a CTA starts inside a segment); the pieces are
+// added in rank order, one CTA phase per piece (indices are distinct within a
+// piece, so a phase has no conflicts); then divided and written once with
+// coalesced stores.
+constexpr int kCtaTile = 8 * kTile;
 __global__ void __launch_bounds__(kThreads, 5) h2_sparse_cta_kernel(const SegH2* __restrict__ segs,
                                                                     const uint32_t* __restrict__ tile_seg,
                                                                     uint32_t ntiles,
@@ -665,8 +734,6 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
     count_launches(1);
     return;
   }
-  launch_pdl(h2_sparse_offsets_kernel, njobs, kThreads, 0, st, segs, jobs, pieces);
-  constexpr int kSmem = kTileThreads / 32 * kTile * (int)sizeof(float);
   auto cap = [](const void* fn, int smem) {
     int dev = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev);
@@ -674,19 +741,21 @@ void launch_h2_sparse(const SegH2* segs, const uint32_t* tile_seg, int ntiles, c
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTileThreads, smem);
     return sms * (per_sm > 0 ? per_sm : 8);
   };
-  // one piece: 9 CTAs (36 warps) per SM -- measured faster for the zero-fill
-  // stream than the 12 the registers would allow (BERT-large: 209 vs 250 us)
-  // one piece: as many CTAs as fit (measured on BERT-large's 1.35 GB output:
-  // 4/6/8/12/16 CTAs per SM -> 1.090/1.052/1.029/1.005/1.003 ms per step)
-  static const int cap1 = cap((const void*)h2_sparse_kernel<false>, 0);
+  if (max_pieces <= 1) {
+    // one piece: as many warps as fit, each over a contiguous tile range
+    static const int cap1 = cap((const void*)h2_sparse1_kernel, 0);
+    const int need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);
+    launch_pdl(h2_sparse1_kernel, need < cap1 ? need : cap1, kTileThreads, 0, st, segs, tile_seg, (uint32_t)ntiles,
+               pieces);
+    count_launches(1);
+    return;
+  }
+  launch_pdl(h2_sparse_offsets_kernel, njobs, kThreads, 0, st, segs, jobs, pieces);
+  constexpr int kSmem = kTileThreads / 32 * kTile * (int)sizeof(float);
   static const int capn = cap((const void*)h2_sparse_kernel<true>, kSmem);
   const int need = (ntiles + kTileThreads / 32 - 1) / (kTileThreads / 32);   // one warp per tile
-  if (max_pieces > 1)
-    launch_pdl(h2_sparse_kernel<true>, need < capn ? need : capn, kTileThreads, kSmem, st, segs, tile_seg,
-               (uint32_t)ntiles, pieces);
-  else
-    launch_pdl(h2_sparse_kernel<false>, need < cap1 ? need : cap1, kTileThreads, 0, st, segs, tile_seg,
-               (uint32_t)ntiles, pieces);
+  launch_pdl(h2_sparse_kernel<true>, need < capn ? need : capn, kTileThreads, kSmem, st, segs, tile_seg,
+             (uint32_t)ntiles, pieces);
   count_launches(2);
 }
 

@@ -193,7 +193,13 @@ __global__ void __launch_bounds__(kTileThreads) h2_randomk_kernel(const SegH2* _
     if (lo >= n) continue;   // past the segment's last element (warp-uniform)
     const uint32_t hi = min(lo + (uint32_t)kRkTile, n) - 1;
     float* out = seg_out(S);
-    for (uint32_t i = lo + lane * 4; i <= hi; i += 128) store4_guard(out, i, n, make_float4(0.f, 0.f, 0.f, 0.f));
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (hi + 1 - lo == (uint32_t)kRkTile && al16(out + lo)) {
+#pragma unroll
+      for (int j = 0; j < kRkTile / 128; ++j) st4(out + lo + lane * 4 + 128 * j, z);
+    } else {
+      for (uint32_t i = lo + lane * 4; i <= hi; i += 128) store4_guard(out, i, n, z);
+    }
     __syncwarp();   // zero stores before the picks' stores
     const Divisor div(S.divisor);
     const bool ones = S.divisor == 1.0f;

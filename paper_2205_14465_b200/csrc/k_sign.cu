@@ -43,7 +43,11 @@ __device__ __forceinline__ void piece_scales(const unsigned char* h, float* sp, 
 // No CTA barrier anywhere: every warp run writes its own partial sums (slot =
 // run index, all slots rewritten each call) and sign_finalize_kernel reduces
 // them per segment in run order, so segment boundaries cost nothing here.
-template <int KIND, bool DECODE = false>
+// DECODE: 0 = h1 of a gradient; 1 = a7 with at most 2 pieces (index nibbles);
+// 2 = a7 with 3..8 pieces (byte-group transpose).  Separate instantiations:
+// the byte-group code in the same kernel measured a 1-piece a7 8 us slower
+// on ResNet-50 (57.6 vs 49.1 us).  More than 8 pieces: sequential decode in both.
+template <int KIND, int DECODE = 0>
 struct SignOp {
   // consumer groups of 8 warps (the decoding variant needs ~100 registers)
   static constexpr int kGroups = DECODE ? 2 : 3;
@@ -91,11 +95,16 @@ struct SignOp {
           const float psn = __shfl_sync(0xffffffffu, st.qsn0, r);
           a = __fadd_rn(a, ((t >> r) & 1u) ? psp : psn);
         }
-        // replicated 16 times, [pattern][lane & 15]: the whole 16 KB scratch
+        // 3..8 pieces: replicated 16 times, [pattern][lane & 15] (the whole
+        // 16 KB scratch); 1..2 pieces: one copy (2 or 4 entries, broadcast reads)
         if (t < (1u << S.npieces)) {
           const float v = S.divisor == 1.0f ? a : Divisor(S.divisor)(a);
+          if (S.npieces <= 2) {
+            lut[t] = v;
+          } else {
 #pragma unroll
-          for (int c = 0; c < 16; ++c) lut[t * 16 + c] = v;
+            for (int c = 0; c < 16; ++c) lut[t * 16 + c] = v;
+          }
         }
         csync<BAR>();
       }
@@ -110,9 +119,10 @@ struct SignOp {
     float4 xv[kNJ];
 #pragma unroll
     for (int j = 0; j < kNJ; ++j) xv[j] = gv[j];
-    if (DECODE && sw && S.npieces <= 3) {
-      // staged words, 1..3 pieces: the index nibbles gathered per piece
-      const float* lut = &gh.wscr[0][0] + (lane & 15);
+    if (DECODE == 1 && sw && S.npieces <= 2) {
+      // staged words, 1..2 pieces: the index nibbles gathered per piece
+      // (measured faster than the byte-group transpose below at n = 1)
+      const float* lut = &gh.wscr[0][0];
       const uint32_t lt = (base & (kDgcTile - 1)) + lane * 4;
 #pragma unroll
       for (int j = 0; j < kNJ; ++j) {
@@ -120,10 +130,9 @@ struct SignOp {
         uint32_t idx4 = 0;
         for (uint32_t q = 0; q < S.npieces; ++q)
           idx4 |= spread4((sw[q * (kDgcTile / 32) + (l >> 5)] >> (l & 31)) & 0xFu) << q;
-        xv[j] = make_float4(lut[(idx4 & 0xFFu) * 16], lut[((idx4 >> 8) & 0xFFu) * 16],
-                            lut[((idx4 >> 16) & 0xFFu) * 16], lut[(idx4 >> 24) * 16]);
+        xv[j] = make_float4(lut[idx4 & 0xFFu], lut[(idx4 >> 8) & 0xFFu], lut[(idx4 >> 16) & 0xFFu], lut[idx4 >> 24]);
       }
-    } else if (DECODE && sw && S.npieces <= (uint32_t)kSignLutPieces) {
+    } else if (DECODE == 2 && sw && S.npieces <= (uint32_t)kSignLutPieces) {
       // staged words, few pieces: the decoded mean by table lookup (identical
       // to the sequential rank-order sum + division below)
       // the run's 64 byte groups (8 elements each): lane decodes groups lane
@@ -366,16 +375,19 @@ __global__ void sign_materialize_kernel(const float* __restrict__ p, const float
 
 void launch_sign_h1_tma(int kind, const SegH1* segs, int nsegs, const uint32_t* unit_seg, int nunits,
                         const unsigned char* const* pieces, cudaStream_t st, uint32_t max_len,
-                        cudaEvent_t probe0, cudaEvent_t probe1) {
+                        cudaEvent_t probe0, cudaEvent_t probe1, int max_pieces) {
   if (nunits == 0) return;
   // a7 stages the pieces' sign words by TMA (measured faster than LDG)
   if (probe0) cudaEventRecord(probe0, st);   // the roofline probe brackets the streaming pass only
+  const bool few = max_pieces <= 2;
   if (kind == K_EFSIGN) {
-    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, true>{pieces, true}, st);
-    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, false>{nullptr, false}, st);
+    if (!pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, 0>{nullptr, false}, st);
+    else if (few) launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, 1>{pieces, true}, st);
+    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_EFSIGN, 2>{pieces, true}, st);
   } else {
-    if (pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, true>{pieces, true}, st);
-    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, false>{nullptr, false}, st);
+    if (!pieces) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, 0>{nullptr, false}, st);
+    else if (few) launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, 1>{pieces, true}, st);
+    else launch_tma_op(segs, unit_seg, nunits, SignOp<K_ONEBIT, 2>{pieces, true}, st);
   }
   if (probe1) cudaEventRecord(probe1, st);
   const uint32_t max_runs = (max_len + kRun - 1) / kRun;

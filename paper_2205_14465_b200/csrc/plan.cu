@@ -52,6 +52,7 @@ struct Bucket {
   uint32_t* h2_rankterms = nullptr;
   uint4* h2_off_jobs = nullptr; int nh2_off_jobs = 0;
   bool h2_dense = false;     // sparse h2: the CTA-tile kernel (launch_h2_sparse)
+  uint32_t rpg_cap = kRunsPerGroup;   // DGC finalize group length cap (dgc_rpg_cap)
   bool a7h2_dense = false;
   int h2_max_pieces = 0;
   uint32_t h1_max_len = 0, a7_max_len = 0;   // longest h1 / a7 segment
@@ -216,7 +217,7 @@ static uint16_t dgc_strata(uint64_t n, double rate) {
 // candidates per 512-element run ~ 512 x (sampled rank / sample size) when
 // sampled, ~ 512 k / n for a whole-segment sample, ~ 1024 k / n for TOPK
 // (the k-th key's 11-bit bin and above)
-static uint32_t dgc_rpg(uint64_t len, uint32_t k, const esp_compressor_cfg_t& cfg) {
+static uint32_t dgc_rpg(uint64_t len, uint32_t k, const esp_compressor_cfg_t& cfg, uint32_t cap) {
   double frac;
   if (cfg.kind == ESP_TOPK) {
     frac = 2.0 * k / (double)len;
@@ -229,7 +230,7 @@ static uint32_t dgc_rpg(uint64_t len, uint32_t k, const esp_compressor_cfg_t& cf
     frac = need / s;
   }
   const double c_run = (double)kRun * (frac > 1.0 ? 1.0 : frac);
-  uint32_t rpg = kRunsPerGroup;
+  uint32_t rpg = cap;
   while (rpg > 8 && rpg * c_run > 2048.0) rpg /= 2;
   return rpg;
 }
@@ -459,7 +460,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.unit0 = unit_cursor;
         s.nunits = nunits;
         const uint32_t nruns = div_up(len, kRun);
-        s.rpg = dgc ? dgc_rpg(len, s.k, c->cfg) : kRunsPerGroup;
+        s.rpg = dgc ? dgc_rpg(len, s.k, c->cfg, b.rpg_cap) : kRunsPerGroup;
         s.ngroups = div_up(nruns, s.rpg);
         s.group0 = group_cursor;
         s.ef = c->cfg.error_feedback ? 1 : 0;
@@ -473,6 +474,10 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         s.approx = c->cfg.dgc_approx ? 1 : 0;
         s.mom = c->u ? c->u + (size_t)lr * c->N + lo : nullptr;
         s.mcoef = (float)c->cfg.momentum;
+        if (dgc && c->zrec) {
+          s.zrec = c->zrec + (size_t)lr * c->zrec_stride + c->zrec_part[part];
+          s.zcap = c->zcap;
+        }
         // per-segment state (zeroed every call)
         size_t st_off = zero_off_st + st_cursor * sizeof(SelState);
         ++st_cursor;
@@ -578,6 +583,10 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
         }
         SegH1 s{};
         s.r = c->r2 ? c->r2 + (size_t)lr * c->r2_len : nullptr;
+        if (c->zrec2) {   // DGC / TOPK process 2: r2's deferred zeroing
+          s.zrec = c->zrec2 + (size_t)lr * c->zrec2_stride;
+          s.zcap = c->zcap;
+        }
         s.lazy_in = c->lazy2 ? c->lazy2 + (size_t)lr * 2 : nullptr;
         s.lazy_out = const_cast<float*>(s.lazy_in);
         s.chunk = b.fused ? (b.stage.base ? b.stage.at(lr) + b.coff[ti] : nullptr)
@@ -631,7 +640,7 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
           s.step = p.dyn_dev + nslots + slot_idx;
           s.k = k_of(len, c->cfg.ratio);
           const uint32_t nruns = div_up(len, kRun);
-          s.rpg = dgc ? dgc_rpg(len, s.k, c->cfg) : kRunsPerGroup;
+          s.rpg = dgc ? dgc_rpg(len, s.k, c->cfg, b.rpg_cap) : kRunsPerGroup;
           s.ngroups = div_up(nruns, s.rpg);
           s.group0 = g0;
           s.unsampled = b.kind == ESP_TOPK ? 1 : 0;
@@ -802,8 +811,30 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
   }
 }
 
+// The bucket's cap on the finalize group length: 128 runs unless that leaves
+// fewer than 2048 groups (warps) over the whole bucket -- a small bucket
+// (config 1's 2^20 elements) wants many short groups, whose dependent-load
+// chains run side by side, rather than a few long ones.
+static uint32_t dgc_rpg_cap(const Plan& p, const Bucket& b) {
+  uint32_t cap = kRunsPerGroup;
+  for (; cap > 8; cap /= 2) {
+    uint64_t groups = 0;
+    for (int t : b.tens) {
+      const esp_ctx_s* c = p.ctxs[t];
+      for (int part = 0; part < c->P; ++part) {
+        const uint64_t len = c->phi[part] - c->plo[part];
+        if (len) groups += div_up(div_up(len, kRun), dgc_rpg(len, c->pk[part], c->cfg, cap));
+      }
+    }
+    if (groups * (uint64_t)p.w->nlocal >= 2048) break;
+  }
+  return cap;
+}
+
 static void layout_plan(Plan& p, bool commit, HostTables& T) {
   Layout L{p, commit};
+  for (auto& b : p.buckets)
+    if (b.kind == ESP_DGC || b.kind == ESP_TOPK) b.rpg_cap = dgc_rpg_cap(p, b);
   p.arena.used = 0;
   const int nslots = (int)p.ctxs.size();
   size_t dyn_off = L.reserve(sizeof(uint64_t) * 2 * nslots);
@@ -823,7 +854,7 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
         ++segs;
         // DGC: histograms + look-back status (one u64 per group of runs)
         if (dgc) {
-          const uint32_t ng = (uint32_t)div_up(div_up(len, kRun), dgc_rpg(len, c->pk[part], c->cfg));
+          const uint32_t ng = (uint32_t)div_up(div_up(len, kRun), dgc_rpg(len, c->pk[part], c->cfg, b.rpg_cap));
           nhist += (round_up((size_t)dgc_hist_words(dgc_hrep(c->pk[part], ng)) * 4, 256) +
                     round_up((size_t)ng * 8, 256)) * p.w->nlocal;
         }
@@ -838,7 +869,7 @@ static void layout_plan(Plan& p, bool commit, HostTables& T) {
             const uint64_t len = c->routine == ESP_ALLTOALL_ALLGATHER ? c->phi[j] - c->plo[j] : (j == 0 ? c->N : 0);
             if (!len) continue;
             const uint32_t ng =
-                (uint32_t)div_up(div_up(len, kRun), dgc_rpg(len, k_of(len, c->cfg.ratio), c->cfg));
+                (uint32_t)div_up(div_up(len, kRun), dgc_rpg(len, k_of(len, c->cfg.ratio), c->cfg, b.rpg_cap));
             nhist += round_up((size_t)dgc_hist_words(dgc_hrep(k_of(len, c->cfg.ratio), ng)) * 4, 256) +
                      round_up((size_t)ng * 8, 256);
           }
@@ -1291,7 +1322,8 @@ static void run_mid(Plan& p, Bucket& b, cudaStream_t cs) {
     }
     dbg("a7 recompress", cs);
   } else {
-    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, pieces, cs, b.a7_max_len);
+    launch_sign_h1_tma(k, b.a7, b.na7, b.a7_units, b.na7_units, pieces, cs, b.a7_max_len, nullptr, nullptr,
+                       p.w->nranks);
   }
   ESP_CUDA(cudaGetLastError());
 }

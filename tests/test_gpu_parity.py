@@ -461,3 +461,73 @@ def test_unaligned_gradients(kind, routine):
                 ctx.set_state(st[0].step, np.stack([x.r for x in st]), r2)
     finally:
         w.destroy()
+
+
+# ---------------------------------- DGC deferred EF zeroing across calls
+@pytest.mark.parametrize("kind", ["dgc", "topk"])
+@pytest.mark.parametrize("routine,n,process", [("allgather", 2, 0), ("alltoall_allgather", 4, 1),
+                                               ("alltoall_allgather", 4, 2), ("gather_broadcast", 2, 2)])
+@pytest.mark.parametrize("ratio,momentum", [(0.001, 0.0), (0.01, 0.0), (0.01, 0.9), (0.06, 0.0)])
+def test_dgc_deferred_zeroing_multistep(kind, routine, n, process, ratio, momentum):
+    """The write kernel records each call's selection per 4096-element tile
+    instead of zeroing r (and u) in memory; the next call's streaming pass
+    reads those positions as +0.  Five calls back to back with no state
+    read-out in between (get_state would apply the records): every output bit-
+    exact against the oracle, then r, r2 and u at the end.  6% overflows the
+    64/128-entry records (the rest is zeroed directly); N has a partial tail
+    tile; both processes of the divisible routines (process 2: r2's records)."""
+    E = esp()
+    N = 3 * 4096 * 7 + 1234
+    w = E.World.sim(n, 0)
+    try:
+        ctx = E.Ctx(w, kind, routine, N, tensor_id=12, ratio=ratio, momentum=momentum, process=process)
+        cfg = O.Cfg(kind, ratio, process=process, momentum=momentum)
+        st = O.new_states(n, N, routine, cfg)
+        for s in range(5):
+            grads = [gradient(N, step=s, rank=r, tensor=12, dist="D2") for r in range(n)]
+            ref = O.sync(routine, cfg, grads, st, tensor_id=12)
+            g = upload(grads)
+            E.esp_sync(w, ctx, g)
+            torch.cuda.synchronize()
+            out = g.cpu().numpy().reshape(n, N)
+            for r in range(n):
+                check_out(kind, out[r], ref.outs[r], f"deferred {kind}/{routine} p{process} step {s} rank {r}")
+        _, rg, r2g = ctx.get_state()
+        for r in range(n):
+            assert np.array_equal(bits(rg[r]), bits(st[r].r)), f"residual rank {r}"
+            if st[r].r2 is not None:
+                assert np.array_equal(bits(r2g[r, :st[r].r2.size]), bits(st[r].r2)), f"r2 rank {r}"
+        if momentum:
+            ug = ctx.get_momentum()
+            for r in range(n):
+                assert np.array_equal(bits(ug[r]), bits(st[r].u)), f"u rank {r}"
+    finally:
+        w.destroy()
+
+
+def test_dgc_deferred_zeroing_state_roundtrip():
+    """get_state / set_state between calls: reading the state applies the
+    pending records (so they are not applied twice), writing it drops them."""
+    E = esp()
+    n, N, ratio = 2, 50_000, 0.01
+    w = E.World.sim(n, 0)
+    try:
+        ctx = E.Ctx(w, "dgc", "allgather", N, tensor_id=13, ratio=ratio)
+        cfg = O.Cfg("dgc", ratio)
+        st = O.new_states(n, N, "allgather", cfg)
+        for s in range(4):
+            grads = [gradient(N, step=s, rank=r, tensor=13) for r in range(n)]
+            ref = O.sync("allgather", cfg, grads, st, tensor_id=13)
+            g = upload(grads)
+            E.esp_sync(w, ctx, g)
+            torch.cuda.synchronize()
+            out = g.cpu().numpy().reshape(n, N)
+            for r in range(n):
+                check_out("dgc", out[r], ref.outs[r], f"roundtrip step {s} rank {r}")
+            if s == 1:   # read-out then write-back of the same state
+                step, rg, r2g = ctx.get_state()
+                ctx.set_state(step, rg, r2g)
+            if s == 2:   # read-out only
+                ctx.get_state()
+    finally:
+        w.destroy()
