@@ -324,8 +324,21 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse1_kernel(const SegH2* _
   SegH2 S{};
   const uint32_t* idx = nullptr;
   const float* val = nullptr;
+  // a batch of 32 entries in registers, lane l holding entry bb + l: refilled
+  // only when consumed (a sparse tile uses one or two of them), so most tiles
+  // issue no dependent load at all
+  uint32_t bb = 0, e = 0xFFFFFFFFu;
+  float v = 0.f;
+  auto refill = [&](uint32_t at) {
+    bb = at;
+    const uint32_t q = at + lane;
+    e = q < S.kpad ? __ldg(idx + q) : 0xFFFFFFFFu;   // padding entries are 0xFFFFFFFF
+    v = q < S.kpad ? __ldg(val + q) : 0.f;
+  };
+  uint32_t sid_next = t0 < t1 ? tile_seg[t0] : 0u;
   for (uint32_t t = t0; t < t1; ++t) {
-    const uint32_t sid = tile_seg[t];
+    const uint32_t sid = sid_next;
+    if (t + 1 < t1) sid_next = tile_seg[t + 1];
     if (sid != cur_seg) {
       cur_seg = sid;
       S = segs[sid];
@@ -333,28 +346,23 @@ __global__ void __launch_bounds__(kTileThreads) h2_sparse1_kernel(const SegH2* _
       idx = reinterpret_cast<const uint32_t*>(pc);
       val = reinterpret_cast<const float*>(pc + 4 * (size_t)S.kpad);
       cur = t == S.unit0 ? 0u : warp_lower_bound(idx, S.kpad, (t - S.unit0) * kTile);
+      refill(cur);
     }
     const uint32_t lo = (t - S.unit0) * kTile, hi = min(lo + (uint32_t)kTile, S.n);
-    uint32_t q = cur + lane;
-    uint32_t e = q < S.kpad ? __ldg(idx + q) : 0xFFFFFFFFu;   // padding entries are 0xFFFFFFFF
-    float v = q < S.kpad ? __ldg(val + q) : 0.f;
     float* out = seg_out(S);
     zero_tile(out, lo, hi, S.n);
     __syncwarp();   // zero stores before the touched-word stores
     const bool ones = S.divisor == 1.0f;
     const Divisor div(S.divisor);
     while (true) {
-      const bool in = e < hi;   // sorted: the tile's entries come first
+      const bool in = bb + lane >= cur && e < hi;   // sorted: the tile's entries come first
       if (in) {
         const float x = __fadd_rn(0.f, v);   // +0 + v: the oracle's sum from +0
         out[e] = ones ? x : div(x);
       }
-      const uint32_t bm = __ballot_sync(0xffffffffu, in);
-      cur += __popc(bm);
-      if (bm != 0xffffffffu) break;
-      q = cur + lane;   // a dense tile: the next 32 entries
-      e = q < S.kpad ? __ldg(idx + q) : 0xFFFFFFFFu;
-      v = q < S.kpad ? __ldg(val + q) : 0.f;
+      cur += __popc(__ballot_sync(0xffffffffu, in));
+      if (cur < bb + 32) break;   // entries left in the batch belong to later tiles
+      refill(cur);                // consumed: the next 32 (more of this tile, or later ones)
     }
   }
 }

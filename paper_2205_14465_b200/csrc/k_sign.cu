@@ -43,10 +43,11 @@ __device__ __forceinline__ void piece_scales(const unsigned char* h, float* sp, 
 // No CTA barrier anywhere: every warp run writes its own partial sums (slot =
 // run index, all slots rewritten each call) and sign_finalize_kernel reduces
 // them per segment in run order, so segment boundaries cost nothing here.
-// DECODE: 0 = h1 of a gradient; 1 = a7 with at most 2 pieces (index nibbles);
-// 2 = a7 with 3..8 pieces (byte-group transpose).  Separate instantiations:
-// the byte-group code in the same kernel measured a 1-piece a7 8 us slower
-// on ResNet-50 (57.6 vs 49.1 us).  More than 8 pieces: sequential decode in both.
+// DECODE: 0 = h1 of a gradient; 1 = a7 decoding by index nibbles (launched
+// for <= 2 pieces); 2 = a7 by byte-group transpose (3..8 pieces).  Separate
+// instantiations: any byte-group code in the nibble kernel made the 1-piece
+// a7 of ResNet-50 58 us instead of 50 (same box, A/B).  More than 8 pieces:
+// sequential decode in both.
 template <int KIND, int DECODE = 0>
 struct SignOp {
   // consumer groups of 8 warps (the decoding variant needs ~100 registers)
@@ -95,11 +96,11 @@ struct SignOp {
           const float psn = __shfl_sync(0xffffffffu, st.qsn0, r);
           a = __fadd_rn(a, ((t >> r) & 1u) ? psp : psn);
         }
-        // 3..8 pieces: replicated 16 times, [pattern][lane & 15] (the whole
-        // 16 KB scratch); 1..2 pieces: one copy (2 or 4 entries, broadcast reads)
+        // DECODE 2: replicated 16 times, [pattern][lane & 15] (the whole 16 KB
+        // scratch); DECODE 1: one copy (few pieces: broadcast reads)
         if (t < (1u << S.npieces)) {
           const float v = S.divisor == 1.0f ? a : Divisor(S.divisor)(a);
-          if (S.npieces <= 2) {
+          if (DECODE == 1) {
             lut[t] = v;
           } else {
 #pragma unroll
@@ -119,9 +120,9 @@ struct SignOp {
     float4 xv[kNJ];
 #pragma unroll
     for (int j = 0; j < kNJ; ++j) xv[j] = gv[j];
-    if (DECODE == 1 && sw && S.npieces <= 2) {
-      // staged words, 1..2 pieces: the index nibbles gathered per piece
-      // (measured faster than the byte-group transpose below at n = 1)
+    if (DECODE == 1 && sw && S.npieces <= (uint32_t)kSignLutPieces) {
+      // staged words, few pieces (launched for <= 2): the index nibbles
+      // gathered per piece (measured faster than the byte-group transpose at n = 1)
       const float* lut = &gh.wscr[0][0];
       const uint32_t lt = (base & (kDgcTile - 1)) + lane * 4;
 #pragma unroll
