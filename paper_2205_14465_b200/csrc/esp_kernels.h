@@ -23,6 +23,11 @@ void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg
 // DGC / TOPK h1 of a bucket whose segments all have <= 4096 elements: one
 // kernel, one CTA per segment (k_dgc.cu)
 void launch_dgc_small(const SegH1* segs, int nsegs, cudaStream_t st);
+// DGC / TOPK h1 of a bucket that fits on chip (k_dgc.cu dgc_mid_kernel): one
+// kernel, ceil(tiles / tpc) co-resident CTAs per segment, grid <= #SMs,
+// tpc <= dgc_mid_tpc_max() tiles of 4096 elements per CTA
+uint32_t dgc_mid_tpc_max();
+void launch_dgc_mid(const SegH1* segs, int nsegs, uint32_t tpc, int grid, cudaStream_t st);
 // DGC deferred EF zeroing: apply a segment's pending records to r / u (either
 // may be null) and clear them
 void launch_dgc_zrec_apply(float* r, float* u, uint16_t* zrec, uint32_t zcap, uint32_t n, cudaStream_t st);

@@ -1345,6 +1345,377 @@ __global__ void __launch_bounds__(kThreads) dgc_small_kernel(const SegH1* __rest
   }
 }
 
+// ------------------------------------------------------------------ on-chip h1
+// DGC / TOPK h1 of a bucket that fits the chip's shared memory (every CTA holds
+// <= kMidTpcMax tiles of acc = g + r): the whole h1 in ONE kernel instead of the
+// seven-kernel chain, whose per-kernel latency is the cost at these sizes
+// (BASELINE config 1 is a 2^20-element tensor).  Segment s gets
+// ceil(tiles_s / tpc) CTAs of 1024 threads, all resident at once (grid <= #SMs,
+// one CTA per SM by shared memory), which meet at four spin barriers on the
+// segment's zeroed-every-call counters:
+//   load    acc = g + r (u = m u + g first with momentum, R20) into shared
+//           memory + the slice's 2048-bin histogram of the top 11 key bits
+//   round 1 (barrier) bin of the k-th key from the summed histogram; one pass
+//           lists the offsets of every key above that bin and of its members,
+//           whose next 10 key bits are histogrammed
+//   round 2 (barrier) next bin; round 3 over the members only
+//   count   (barrier) T known: selected / tie bitmaps from the lists, every
+//           CTA's (#above T, #ties) -> the selected in the CTAs before it and
+//           the ties it may take (ascending index); a bitmap prefix gives each
+//           selected entry its place in the index-sorted payload; then
+//           r := acc with 0 where selected (a float4 pass) and u := 0 there.
+// No sampled threshold and no candidate list in HBM: the exact k-th key T and
+// the (key desc, idx asc) selection are the same as the chain's (reading R3).
+constexpr uint32_t kMidTpcMax = 8;
+constexpr uint32_t kMidSmem = kMidTpcMax * kDgcTile * 6;   // acc (4 B) + member list (2 B) per element
+
+__device__ __forceinline__ void seg_barrier(uint32_t* ctr, uint32_t expected) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // release: the CTA's writes before the bar.sync above are ordered before
+    // the arrival (no full fence.sc)
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    uint32_t v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= expected) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
+constexpr int kMidThreads = 1024;   // 32 warps: the passes are latency-bound chains
+constexpr int kMidWarps = kMidThreads / 32;
+
+// exclusive scan of v over the 1024 threads in thread order; sh needs 33 words
+__device__ __forceinline__ uint32_t mid_excl_scan(uint32_t v, uint32_t* total, uint32_t* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = sh[lane];
+    uint32_t s2 = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, s2, o);
+      if (lane >= o) s2 += y;
+    }
+    sh[lane] = s2 - w;
+    if (lane == 31) sh[32] = s2;
+  }
+  __syncthreads();
+  const uint32_t r = x - v + sh[warp];
+  *total = sh[32];
+  __syncthreads();
+  return r;
+}
+
+// CTA-wide radix bin choice by the first 256 threads (select_bin on named
+// barrier 1), broadcast through shared memory
+__device__ __forceinline__ uint2 mid_select(const uint32_t* gh, int nbins, uint32_t need, uint32_t* sh,
+                                            uint32_t* res) {
+  if (threadIdx.x < kThreads) {
+    uint32_t b, a;
+    select_bin<1, true>(gh, nbins, need, &b, &a, sh);
+    if (threadIdx.x == 0) {
+      res[0] = b;
+      res[1] = a;
+    }
+  }
+  __syncthreads();
+  return make_uint2(res[0], res[1]);
+}
+
+__global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __restrict__ segs, int nsegs,
+                                                                 uint32_t tpc) {
+  extern __shared__ float4 mid_smem4[];
+  float* acc = reinterpret_cast<float*>(mid_smem4);
+  uint16_t* list = reinterpret_cast<uint16_t*>(acc + tpc * kDgcTile);
+  __shared__ uint32_t hist1[2048];
+  __shared__ uint32_t hist2[1024];
+  __shared__ uint32_t sh[288];
+  __shared__ uint32_t wcnt[2 * kMidWarps];   // [0]: member count; then per warp: members above T, ties
+  __shared__ uint32_t info[6];   // segment, CTA index in it, CTAs of it, list length, select result (2)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // CTA -> (segment, index) from the static table (before pdl_wait)
+  if (tid < kThreads) {
+    const uint32_t c = tid < nsegs ? ((segs[tid].n + kDgcTile - 1) / kDgcTile + tpc - 1) / tpc : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<1>(c, &tot, sh);
+    if (c && blockIdx.x >= ex && blockIdx.x < ex + c) {
+      info[0] = tid;
+      info[1] = blockIdx.x - ex;
+      info[2] = c;
+    }
+  }
+  for (int b = tid; b < 2048; b += kMidThreads) hist1[b] = 0;
+  for (int b = tid; b < 1024; b += kMidThreads) hist2[b] = 0;
+  if (tid < 2 * kMidWarps) wcnt[tid] = 0;
+  if (tid == 0) info[3] = 0;
+  __syncthreads();
+  const SegH1& S = segs[info[0]];
+  const uint32_t ci = info[1], nc = info[2];
+  const uint32_t n = S.n, k = S.k;
+  const uint32_t lo = ci * tpc * kDgcTile, hi = min(n, lo + tpc * kDgcTile), len = hi - lo;
+  pdl_wait();
+  pdl_trigger();
+  const bool ef = S.ef != 0;
+  float* r = ef ? S.r + lo : nullptr;
+  float* u = S.mom ? S.mom + lo : nullptr;
+  const float m = S.mcoef;
+  const float* g = seg_g(S) + lo;
+  if (S.zrec) {   // pending deferred zeroing of this CTA's tiles (a chained call before): applied first
+    const uint32_t t0 = lo / kDgcTile, t1 = (hi + kDgcTile - 1) / kDgcTile;
+    for (uint32_t t = t0 + warp; t < t1; t += kMidWarps) {
+      uint16_t* z = S.zrec + (size_t)t * S.zcap;
+      const uint32_t cnt = min((uint32_t)z[0], S.zcap - 1);
+      for (uint32_t i = 1 + lane; i <= cnt; i += 32) {
+        const uint32_t e = t * kDgcTile + z[i];
+        if (e < n) {
+          if (ef) S.r[e] = 0.0f;
+          if (S.mom) S.mom[e] = 0.0f;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) z[0] = 0;
+    }
+    __syncthreads();
+  }
+  // ---- load: acc = g + r, histogram of the top 11 key bits (atomicAdd(.., 1)
+  // compiles to ATOMS.POPC.INC: the lanes of a warp that hit one bin are one update)
+  auto elem = [&](float x, float rv, float uv, float& uo) {
+    uo = 0.0f;
+    if (u) {   // momentum correction (R20): u = fl(fl(m u) + g)
+      x = __fadd_rn(__fmul_rn(m, uv), x);
+      uo = x;
+    }
+    return ef ? __fadd_rn(x, rv) : x;
+  };
+  const bool vec = al16(g) && (!ef || al16(r)) && (!u || al16(u));
+  const uint32_t n4 = vec ? len / 4 : 0;
+  // batches of kB float4 per thread, every load of a batch issued before any use
+  // (~64 KB in flight per SM: one CTA per SM has to cover the DRAM latency alone)
+  constexpr int kB = 2;
+  for (uint32_t i0 = 0; i0 < n4; i0 += kB * kMidThreads) {
+    float4 x[kB], rv[kB], uv[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const uint32_t i = i0 + j * kMidThreads + tid;
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      x[j] = i < n4 ? ld_stream4(g + 4 * i) : z;
+      rv[j] = ef && i < n4 ? ld4(r + 4 * i) : z;
+      uv[j] = u && i < n4 ? ld4(u + 4 * i) : z;
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const uint32_t i = i0 + j * kMidThreads + tid;
+      const bool v = i < n4;
+      float4 a, uo;
+      a.x = elem(x[j].x, rv[j].x, uv[j].x, uo.x);
+      a.y = elem(x[j].y, rv[j].y, uv[j].y, uo.y);
+      a.z = elem(x[j].z, rv[j].z, uv[j].z, uo.z);
+      a.w = elem(x[j].w, rv[j].w, uv[j].w, uo.w);
+      if (v) {
+        if (u) st4(u + 4 * i, uo);
+        *reinterpret_cast<float4*>(acc + 4 * i) = a;
+      }
+      if (v) atomicAdd(&hist1[fkey(a.x) >> 20], 1u);
+      if (v) atomicAdd(&hist1[fkey(a.y) >> 20], 1u);
+      if (v) atomicAdd(&hist1[fkey(a.z) >> 20], 1u);
+      if (v) atomicAdd(&hist1[fkey(a.w) >> 20], 1u);
+    }
+  }
+  for (uint32_t i0 = 4 * n4; i0 < len; i0 += kMidThreads) {   // unaligned slices and the tail
+    const uint32_t i = i0 + tid;
+    if (i < len) {
+      float uo;
+      const float a = elem(g[i], ef ? r[i] : 0.0f, u ? u[i] : 0.0f, uo);
+      if (u) u[i] = uo;
+      acc[i] = a;
+      atomicAdd(&hist1[fkey(a) >> 20], 1u);
+    }
+  }
+  __syncthreads();
+  for (int b = tid; b < 2048; b += kMidThreads)
+    if (hist1[b]) atomicAdd(S.hist + b, hist1[b]);
+  seg_barrier(&S.st->done, nc);
+  // hist1 becomes the selection bitmaps (1 bit per element of the slice)
+  uint32_t* selbits = hist1;           // [len / 32]: selected
+  uint32_t* tiebits = hist1 + 1024;    // [len / 32]: key == T
+  uint2 sel = mid_select(S.hist, 2048, k, sh, info + 4);   // (its __syncthreads orders the flush reads)
+  const uint32_t bin1 = sel.x;
+  uint32_t need = k - sel.y;
+  for (int b = tid; b < 2048; b += kMidThreads) hist1[b] = 0;
+  // ---- round 2: one pass over the slice, a float4 per lane.  The list gets
+  // the offsets of every key above bin 1 (from the front) and of bin 1's
+  // members (from the back; their next 10 key bits histogrammed): every key
+  // >= T is in it, and both sets together are at most the slice
+  const uint32_t cap = tpc * kDgcTile;
+  for (uint32_t i = 4 * tid; i < len; i += 4 * kMidThreads) {
+    const float4 a4 = lds4(acc + i);   // (beyond len: stale shared memory, masked below)
+    uint32_t top[4];
+    bool hit = false;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      top[c] = fkey(f4get(a4, c)) >> 20;
+      hit |= i + c < len && top[c] >= bin1;
+    }
+    if (hit) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (i + c >= len) {
+        } else if (top[c] > bin1) {
+          list[atomicAdd(&info[3], 1u)] = (uint16_t)(i + c);
+        } else if (top[c] == bin1) {
+          list[cap - 1 - atomicAdd(&wcnt[0], 1u)] = (uint16_t)(i + c);
+          atomicAdd(&hist2[(fkey(f4get(a4, c)) >> 10) & 1023], 1u);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t nabove = info[3], nmem = wcnt[0];
+  const uint16_t* mlist = list + cap - nmem;   // bin 1's members
+  uint32_t* gh2 = S.hist + 4096;
+  uint32_t* gh3 = S.hist + 4096 + 1024 * S.hrep;
+  for (int b = tid; b < 1024; b += kMidThreads) {
+    if (hist2[b]) atomicAdd(gh2 + b, hist2[b]);
+    hist2[b] = 0;   // reused by round 3 (the barrier below orders it)
+  }
+  seg_barrier(&S.st->done_r2, nc);
+  sel = mid_select(gh2, 1024, need, sh, info + 4);
+  const uint32_t prefix2 = (bin1 << 10) | sel.x;
+  need -= sel.y;
+  // ---- round 3 over the members
+  for (uint32_t j = tid; j < nmem; j += kMidThreads) {
+    const uint32_t key = fkey(acc[mlist[j]]);
+    if ((key >> 10) == prefix2) atomicAdd(&hist2[key & 1023], 1u);
+  }
+  __syncthreads();
+  for (int b = tid; b < 1024; b += kMidThreads)
+    if (hist2[b]) atomicAdd(gh3 + b, hist2[b]);
+  seg_barrier(&S.st->done_r3, nc);
+  sel = mid_select(gh3, 1024, need, sh, info + 4);
+  const uint32_t T = (prefix2 << 10) | sel.x;
+  need -= sel.y;   // the ties at T to take, by ascending index
+  // ---- count: above T = every key above bin 1 + members above T; ties
+  for (uint32_t j = tid; j < nabove; j += kMidThreads) {
+    const uint32_t o = list[j];
+    atomicOr(&selbits[o >> 5], 1u << (o & 31));
+  }
+  uint32_t ma = 0, mt = 0;
+  for (uint32_t j = tid; j < nmem; j += kMidThreads) {
+    const uint32_t o = mlist[j];
+    const uint32_t key = fkey(acc[o]);
+    if (key > T) {
+      atomicOr(&selbits[o >> 5], 1u << (o & 31));
+      ++ma;
+    } else if (key == T) {
+      atomicOr(&tiebits[o >> 5], 1u << (o & 31));
+      ++mt;
+    }
+  }
+  ma = __reduce_add_sync(0xffffffffu, ma);
+  mt = __reduce_add_sync(0xffffffffu, mt);
+  if (lane == 0) {
+    wcnt[warp] = ma;
+    wcnt[kMidWarps + warp] = mt;
+  }
+  __syncthreads();
+  uint2* slots = S.cand;   // per CTA: (#above T, #ties) (the chain's candidate buffer)
+  uint32_t ctie = 0;   // this CTA's ties (every thread)
+#pragma unroll 8
+  for (int w = 0; w < kMidWarps; ++w) ctie += wcnt[kMidWarps + w];
+  if (warp == 0) {
+    const uint32_t ta = nabove + __reduce_add_sync(0xffffffffu, wcnt[lane]);
+    if (lane == 0) __stcg(reinterpret_cast<unsigned long long*>(slots + ci), ((unsigned long long)ctie << 32) | ta);
+  }
+  seg_barrier(&S.st->done_cnt, nc);
+  if (warp == 0) {
+    uint32_t ba = 0, bt = 0;
+    for (uint32_t j = lane; j < ci; j += 32) {
+      const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(slots + j));
+      ba += (uint32_t)v;
+      bt += (uint32_t)(v >> 32);
+    }
+    ba = __reduce_add_sync(0xffffffffu, ba);
+    bt = __reduce_add_sync(0xffffffffu, bt);
+    if (lane == 0) {
+      info[4] = ba + min(bt, need);   // selected in the CTAs before this one
+      info[5] = bt;                   // ties in the CTAs before this one
+    }
+  }
+  __syncthreads();
+  const uint32_t cbase = info[4], tbase = info[5];
+  const uint32_t nwords = (len + 31) / 32;
+  // ties by ascending index: rank = ties before it in this CTA (bitmap prefix)
+  if (tbase < need && ctie != 0) {   // this CTA may take ties
+    const uint32_t w = tid < (int)nwords ? tiebits[tid] : 0u;
+    uint32_t tot;
+    const uint32_t ex = mid_excl_scan(__popc(w), &tot, sh);
+    hist2[tid] = ex;   // (1024 words: one per thread)
+    __syncthreads();
+    {
+      for (uint32_t j = tid; j < nmem; j += kMidThreads) {
+        const uint32_t o = mlist[j];
+        const uint32_t tw = tiebits[o >> 5];
+        if (tw & (1u << (o & 31))) {
+          const uint32_t rank = hist2[o >> 5] + __popc(tw & ((1u << (o & 31)) - 1u));
+          if (tbase + rank < need) atomicOr(&selbits[o >> 5], 1u << (o & 31));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // selected-before prefix per bitmap word
+  {
+    const uint32_t w = tid < (int)nwords ? selbits[tid] : 0u;
+    uint32_t tot;
+    hist2[tid] = mid_excl_scan(__popc(w), &tot, sh);
+    __syncthreads();
+  }
+  // ---- ordered write: idx / val of the selected (from the list), u := 0 there
+  uint32_t* out_idx = reinterpret_cast<uint32_t*>(S.chunk);
+  float* out_val = reinterpret_cast<float*>(S.chunk + 4 * (size_t)S.kpad);
+  auto emit = [&](uint32_t o) {
+    const uint32_t sw = selbits[o >> 5];
+    if (sw & (1u << (o & 31))) {
+      const uint32_t pos = cbase + hist2[o >> 5] + __popc(sw & ((1u << (o & 31)) - 1u));
+      out_idx[pos] = lo + o;
+      out_val[pos] = acc[o];
+      if (u) u[o] = 0.0f;   // momentum factor masking (R20)
+    }
+  };
+  for (uint32_t j = tid; j < nabove; j += kMidThreads) emit(list[j]);
+  for (uint32_t j = tid; j < nmem; j += kMidThreads) emit(mlist[j]);
+  // ---- r := acc, 0 where selected (a float4 per thread and step)
+  if (ef) {
+    const bool rvec = al16(r);
+    for (uint32_t i = 4 * tid; i < len; i += 4 * kMidThreads) {
+      float4 a4 = lds4(acc + i);
+      const uint32_t sb = selbits[i >> 5] >> (i & 31);
+      if (sb & 1u) a4.x = 0.0f;
+      if (sb & 2u) a4.y = 0.0f;
+      if (sb & 4u) a4.z = 0.0f;
+      if (sb & 8u) a4.w = 0.0f;
+      if (rvec && i + 3 < len) {
+        st4(r + i, a4);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (i + c < len) r[i + c] = f4get(a4, c);
+      }
+    }
+  }
+}
+
 // Applies a segment's pending deferred zeroing to r and u in memory and clears
 // the records (state read-out: esp_ctx_get_state / get_momentum).  One warp
 // per tile.
@@ -1368,6 +1739,18 @@ void launch_dgc_zrec_apply(float* r, float* u, uint16_t* zrec, uint32_t zcap, ui
   if (!zrec || n == 0) return;
   const uint32_t ntiles = (n + kDgcTile - 1) / kDgcTile;
   dgc_zrec_apply_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(r, u, zrec, zcap, n);
+  count_launches(1);
+}
+
+uint32_t dgc_mid_tpc_max() { return kMidTpcMax; }
+
+void launch_dgc_mid(const SegH1* segs, int nsegs, uint32_t tpc, int grid, cudaStream_t st) {
+  if (nsegs == 0 || grid == 0) return;
+  static const bool attr_set =
+      cudaFuncSetAttribute(dgc_mid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMidSmem) ==
+      cudaSuccess;
+  (void)attr_set;
+  launch_pdl(dgc_mid_kernel, grid, kMidThreads, (size_t)tpc * kDgcTile * 6, st, segs, nsegs, tpc);
   count_launches(1);
 }
 

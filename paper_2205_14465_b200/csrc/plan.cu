@@ -57,6 +57,9 @@ struct Bucket {
   int h2_max_pieces = 0;
   uint32_t h1_max_len = 0, a7_max_len = 0;   // longest h1 / a7 segment
   bool small = false;          // DGC: every h1 segment has <= kSample elements (one-kernel h1)
+  bool onchip = false;         // DGC: the bucket fits on chip (dgc_mid_kernel, one kernel)
+  uint32_t onchip_tpc = 0;     //   tiles per CTA
+  int onchip_grid = 0;         //   CTAs (<= #SMs, all co-resident)
   cudaEvent_t ev_h1 = nullptr, ev_comm = nullptr, ev_stream = nullptr;
   uint64_t h1_calls = 0, h2_pieces_count = 0;   // per tensor-rank counters
   uint64_t h1_bytes = 0;      // algorithmic HBM bytes of the streaming h1 kernel
@@ -200,6 +203,14 @@ static bool fused_allgather_enabled() {
 static void add_push(std::vector<PushJob>& v, size_t src_off, size_t dst_off, size_t bytes, int d) {
   for (size_t c = 0; c < bytes; c += kPushChunk)
     v.push_back(PushJob{src_off + c, dst_off + c, (uint32_t)std::min<size_t>(kPushChunk, bytes - c), (uint32_t)d});
+}
+
+// ESP_DGC_PATH=chain (test hook, read when a plan is built): DGC / TOPK h1 of
+// buckets that fit on chip takes the sample / stream / finalize chain instead
+// of dgc_mid_kernel, so that both paths stay covered by the parity tests
+static bool dgc_mid_enabled() {
+  const char* e = getenv("ESP_DGC_PATH");
+  return !(e && strcmp(e, "chain") == 0);
 }
 
 // DGC sampler strata of a segment (reading R22): 512 (4096 samples) by
@@ -510,6 +521,28 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
   b.h1_max_len = 0;
   for (int i = 0; i < b.nh1; ++i) b.h1_max_len = std::max(b.h1_max_len, T.h1[h1_first + i].n);
   b.small = dgc && b.h1_max_len <= (uint32_t)kSample;
+  // one-kernel h1 when the bucket fits the chip's shared memory: the smallest
+  // tiles-per-CTA that gives every segment's CTAs a resident slot (grid <= #SMs);
+  // the approximate-count mode keeps the chain (its result depends on the sample)
+  b.onchip = false;
+  if (dgc && !b.small && dgc_mid_enabled()) {
+    bool ok = true;
+    for (int i = 0; i < b.nh1; ++i) ok = ok && !T.h1[h1_first + i].approx;
+    int sms = 0, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 0;
+    for (uint32_t tpc = 1; ok && tpc <= dgc_mid_tpc_max(); ++tpc) {
+      uint64_t ctas = 0;
+      for (int i = 0; i < b.nh1; ++i) ctas += div_up(T.h1[h1_first + i].nunits, tpc);
+      if (ctas <= (uint64_t)sms) {
+        b.onchip = true;
+        b.onchip_tpc = tpc;
+        b.onchip_grid = (int)ctas;
+        break;
+      }
+    }
+  }
   {
     // algorithmic bytes of the streaming h1 pass: read g, read r,
     // write r = 12 B/elem with EF (4 B/elem without); sign adds 1/8 B/elem of
@@ -1264,6 +1297,10 @@ static cudaStream_t run_h1(Plan& p, Bucket& b, cudaStream_t st, cudaStream_t fin
       if (b.small) {   // every segment fits one CTA: the whole h1 in one kernel
         if (e0) ESP_CUDA(cudaEventRecord(e0, st));
         launch_dgc_small(b.h1, b.nh1, st);
+        if (e1) ESP_CUDA(cudaEventRecord(e1, st));
+      } else if (b.onchip) {   // the bucket fits on chip: the whole h1 in one kernel
+        if (e0) ESP_CUDA(cudaEventRecord(e0, st));
+        launch_dgc_mid(b.h1, b.nh1, b.onchip_tpc, b.onchip_grid, st);
         if (e1) ESP_CUDA(cudaEventRecord(e1, st));
       } else if (fin) {
         launch_dgc_stream(b.h1, b.nh1, b.h1_units, b.nh1_units, st, e0, e1, b.momentum != 0.0);

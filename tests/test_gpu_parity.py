@@ -90,23 +90,43 @@ def run_sim(kind, routine, n, N, steps=3, ratio=0.01, dist="D1", mode="mixed", e
         w.destroy()
 
 
+# DGC / TOPK h1 has two paths: buckets that fit the chip's shared memory run the
+# one-kernel on-chip select (dgc_mid_kernel), larger ones the sample / stream /
+# finalize chain; ESP_DGC_PATH=chain (read when a plan is built) forces the
+# chain so that both stay covered at every size
+PATHS = ["onchip", "chain"]
+
+
+def set_path(monkeypatch, path):
+    if path == "chain":
+        monkeypatch.setenv("ESP_DGC_PATH", "chain")
+    else:
+        monkeypatch.delenv("ESP_DGC_PATH", raising=False)
+
+
 # ---------------------------------------------------------------- config 1
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("N", [1 << 20, 10 ** 6])
-def test_config1_dgc_allgather_n2(N):
+def test_config1_dgc_allgather_n2(N, path, monkeypatch):
     """BASELINE config 1: 1M-element fp32 gradient, DGC top-1% with EF, Allgather,
     n = 2 simulated ranks, 5 steps, bit-exact."""
+    set_path(monkeypatch, path)
     run_sim("dgc", "allgather", 2, N, steps=5, ratio=0.01)
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("dist", ["D1", "D2", "D3"])
 @pytest.mark.parametrize("N", [1, 31, 33, 1000, 4097, 8193, (1 << 16) + 3, 100_003])
-def test_dgc_sizes_dists(N, dist):
+def test_dgc_sizes_dists(N, dist, path, monkeypatch):
+    set_path(monkeypatch, path)
     run_sim("dgc", "allgather", 2, N, steps=2, ratio=0.01, dist=dist)
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("mode", ["equal", "zeros", "spike", "pm0", "denormal", "mixed"])
-def test_dgc_adversarial(mode):
+def test_dgc_adversarial(mode, path, monkeypatch):
     # all-equal magnitudes force the fallback and the tie-break; zeros give T = 0
+    set_path(monkeypatch, path)
     run_sim("dgc", "allgather", 2, 50_001, steps=2, ratio=0.01, dist="D4", mode=mode)
 
 
@@ -117,12 +137,15 @@ def test_dgc_forced_fallback(force, N, monkeypatch):
     fallback (1: recompaction at thr_lo; 3: thr_lo misses too -> thr = 0) must
     leave the selection bit-identical (reading R3)."""
     monkeypatch.setenv("ESP_DGC_FORCE_FALLBACK", force)
+    set_path(monkeypatch, "chain")   # the on-chip select has no sampled threshold
     run_sim("dgc", "allgather", 2, N, steps=2, ratio=0.01)
     run_sim("dgc", "alltoall_allgather", 4, N, steps=2, ratio=0.01)
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("ratio", [0.001, 0.05, 0.5, 1.0])
-def test_dgc_ratios(ratio):
+def test_dgc_ratios(ratio, path, monkeypatch):
+    set_path(monkeypatch, path)
     run_sim("dgc", "allgather", 2, 70_000, steps=2, ratio=ratio)
 
 
@@ -386,9 +409,11 @@ def test_processes_unshared_randomk(process):
 @pytest.mark.parametrize("kind", ["dgc", "topk"])
 @pytest.mark.parametrize("routine,n", [("allgather", 2), ("allgather", 4), ("alltoall_allgather", 4),
                                        ("gather_broadcast", 2)])
-def test_momentum_correction(kind, routine, n):
+@pytest.mark.parametrize("path", PATHS)
+def test_momentum_correction(kind, routine, n, path, monkeypatch):
     """u = fl(fl(m u) + g), v = fl(v + u), top-k of v, v[sel] = u[sel] = 0:
     outputs, v (the residual) and u bit-exact against the oracle over 4 steps."""
+    set_path(monkeypatch, path)
     E = esp()
     N, m = 70_001, 0.9
     w = E.World.sim(n, 0)
@@ -468,7 +493,7 @@ def test_unaligned_gradients(kind, routine):
 @pytest.mark.parametrize("routine,n,process", [("allgather", 2, 0), ("alltoall_allgather", 4, 1),
                                                ("alltoall_allgather", 4, 2), ("gather_broadcast", 2, 2)])
 @pytest.mark.parametrize("ratio,momentum", [(0.001, 0.0), (0.01, 0.0), (0.01, 0.9), (0.06, 0.0)])
-def test_dgc_deferred_zeroing_multistep(kind, routine, n, process, ratio, momentum):
+def test_dgc_deferred_zeroing_multistep(kind, routine, n, process, ratio, momentum, monkeypatch):
     """The write kernel records each call's selection per 4096-element tile
     instead of zeroing r (and u) in memory; the next call's streaming pass
     reads those positions as +0.  Five calls back to back with no state
@@ -476,6 +501,7 @@ def test_dgc_deferred_zeroing_multistep(kind, routine, n, process, ratio, moment
     exact against the oracle, then r, r2 and u at the end.  6% overflows the
     64/128-entry records (the rest is zeroed directly); N has a partial tail
     tile; both processes of the divisible routines (process 2: r2's records)."""
+    set_path(monkeypatch, "chain")   # the chain's write kernel keeps the records
     E = esp()
     N = 3 * 4096 * 7 + 1234
     w = E.World.sim(n, 0)
@@ -505,9 +531,10 @@ def test_dgc_deferred_zeroing_multistep(kind, routine, n, process, ratio, moment
         w.destroy()
 
 
-def test_dgc_deferred_zeroing_state_roundtrip():
+def test_dgc_deferred_zeroing_state_roundtrip(monkeypatch):
     """get_state / set_state between calls: reading the state applies the
     pending records (so they are not applied twice), writing it drops them."""
+    set_path(monkeypatch, "chain")
     E = esp()
     n, N, ratio = 2, 50_000, 0.01
     w = E.World.sim(n, 0)
@@ -531,3 +558,113 @@ def test_dgc_deferred_zeroing_state_roundtrip():
                 ctx.get_state()
     finally:
         w.destroy()
+
+
+# ---------------------------------------------- on-chip DGC select (dgc_mid_kernel)
+@pytest.mark.parametrize("kind", ["dgc", "topk"])
+@pytest.mark.parametrize("momentum", [0.0, 0.9])
+def test_onchip_after_chain_records(kind, momentum, monkeypatch):
+    """Chain calls leave deferred-zeroing records; the on-chip kernel applies
+    and clears them before it reads r / u, then zeroes its own selection in
+    memory; and back to the chain.  Outputs, r and u bit-exact each step."""
+    E = esp()
+    n, N, ratio = 2, 5 * 4096 + 77, 0.01
+    w = E.World.sim(n, 0)
+    try:
+        ctx = E.Ctx(w, kind, "allgather", N, tensor_id=21, ratio=ratio, momentum=momentum)
+        cfg = O.Cfg(kind, ratio, momentum=momentum)
+        st = O.new_states(n, N, "allgather", cfg)
+        for s, path in enumerate(["chain", "chain", "onchip", "onchip", "chain", "onchip"]):
+            set_path(monkeypatch, path)
+            w.drop_plans()
+            grads = [gradient(N, step=s, rank=r, tensor=21, dist="D2") for r in range(n)]
+            ref = O.sync("allgather", cfg, grads, st, tensor_id=21)
+            g = upload(grads)
+            E.esp_sync(w, ctx, g)
+            torch.cuda.synchronize()
+            out = g.cpu().numpy().reshape(n, N)
+            for r in range(n):
+                check_out(kind, out[r], ref.outs[r], f"{path} step {s} rank {r}")
+        _, rg, _ = ctx.get_state()
+        for r in range(n):
+            assert np.array_equal(bits(rg[r]), bits(st[r].r)), f"residual rank {r}"
+        if momentum:
+            ug = ctx.get_momentum()
+            for r in range(n):
+                assert np.array_equal(bits(ug[r]), bits(st[r].u)), f"u rank {r}"
+    finally:
+        w.destroy()
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_onchip_many_segments(path, monkeypatch):
+    """One DGC bucket of tensors of very different lengths (one tile, several
+    CTAs, a ragged tail, an odd length that misaligns the next rank's slice,
+    Alltoall partitions): the on-chip kernel maps CTAs to segments from the
+    table; every output bit-exact over 3 steps."""
+    set_path(monkeypatch, path)
+    E = esp()
+    n = 4
+    specs = [("dgc", "allgather", 4097), ("dgc", "allgather", 300_007), ("dgc", "alltoall_allgather", 123_457),
+             ("dgc", "allgather", 64 * 4096), ("topk", "allgather", 50_001), ("dgc", "allgather", 9)]
+    w = E.World.sim(n, 0)
+    try:
+        ctxs = [E.Ctx(w, k, r, N, tensor_id=40 + t, ratio=0.01) for t, (k, r, N) in enumerate(specs)]
+        sts = [O.new_states(n, N, r, O.Cfg(k, 0.01)) for (k, r, N) in specs]
+        for s in range(3):
+            grads = [[gradient(N, step=s, rank=r, tensor=40 + t) for r in range(n)] for t, (_, _, N) in enumerate(specs)]
+            refs = [O.sync(r, O.Cfg(k, 0.01), grads[t], sts[t], tensor_id=40 + t) for t, (k, r, N) in enumerate(specs)]
+            gs = [upload(grads[t]) for t in range(len(specs))]
+            E.esp_sync_many(w, ctxs, gs)
+            torch.cuda.synchronize()
+            for t, (k, r, N) in enumerate(specs):
+                out = gs[t].cpu().numpy().reshape(n, N)
+                for rr in range(n):
+                    check_out(k, out[rr], refs[t].outs[rr], f"{path} t={t} {k}/{r} step {s} rank {rr}")
+    finally:
+        w.destroy()
+
+
+@pytest.mark.parametrize("fits", [True, False])
+def test_onchip_capacity_edge(fits):
+    """The largest bucket the on-chip kernel takes (#SMs CTAs of 8 tiles) and
+    one tile more (the chain): both bit-exact; the first is one h1 launch."""
+    E = esp()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = 2
+    N = (sms // n) * 8 * 4096 - 1000 + (0 if fits else 4096)
+    w = E.World.sim(n, 0)
+    try:
+        ctx = E.Ctx(w, "dgc", "allgather", N, tensor_id=22, ratio=0.01)
+        cfg = O.Cfg("dgc", 0.01)
+        st = O.new_states(n, N, "allgather", cfg)
+        for s in range(2):
+            grads = [gradient(N, step=s, rank=r, tensor=22) for r in range(n)]
+            ref = O.sync("allgather", cfg, grads, st, tensor_id=22)
+            g = upload(grads)
+            l0 = E.esp_launch_count()
+            E.esp_sync(w, ctx, g)
+            torch.cuda.synchronize()
+            if s == 0:   # (later calls replay a CUDA graph, which counts nothing)
+                launches = E.esp_launch_count() - l0
+            out = g.cpu().numpy().reshape(n, N)
+            for r in range(n):
+                check_out("dgc", out[r], ref.outs[r], f"fits={fits} step {s} rank {r}")
+        _, rg, _ = ctx.get_state()
+        for r in range(n):
+            assert np.array_equal(bits(rg[r]), bits(st[r].r)), f"residual rank {r}"
+        if fits:
+            assert launches <= 5, launches
+        else:
+            assert launches >= 8, launches
+    finally:
+        w.destroy()
+
+
+@pytest.mark.parametrize("mode", ["equal", "mixed"])
+@pytest.mark.parametrize("ratio", [0.01, 0.3])
+def test_onchip_many_members(mode, ratio):
+    """Round 1's bin holding more than 16384 keys of a segment (all-equal
+    magnitudes; a 30% ratio on a wide segment) takes the distributed rounds 3
+    and count with two more barriers; few members, the redundant finish."""
+    run_sim("dgc", "allgather", 2, 600_001, steps=2, ratio=ratio, dist="D4", mode=mode)
