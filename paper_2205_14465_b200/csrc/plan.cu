@@ -831,7 +831,9 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
     h2_entries += (double)x.kpad * x.npieces;
     h2_elems += (double)x.n;
   }
-  b.h2_dense = h2_sparse_dense(h2_entries, h2_elems);
+  // small buckets take the CTA-tile kernel at any density: one launch instead of
+  // the offset pass + the warp-per-tile kernel (their latency is the cost there)
+  b.h2_dense = h2_sparse_dense(h2_entries, h2_elems) || h2_elems <= (double)(1u << 22);
   b.nh2_units = (int)u0;
 
   // per critical rank op counts of the cost table
