@@ -642,6 +642,11 @@ def main():
             "gpu_launches": launches,
             "clocks": clk,
             **({"phases_ms_serialised": phases} if phases else {}),
+            # a9: the same step with its phases serialised (events
+            # around each) minus the pipelined step = the time the overlap of
+            # h1(b+1) / finalize chains with the collective of bucket b hides
+            **({"pipelining": {"serialised_ms": phases["total_ms"], "pipelined_ms": t_mean,
+                               "hidden_ms": phases["total_ms"] - t_mean}} if phases else {}),
             **({"link": link} if link else {}),
         }
         if not args.no_latency:
