@@ -1036,47 +1036,101 @@ __device__ __forceinline__ unsigned long long lb_pack(uint32_t flag, uint32_t ab
 // 32 groups per round trip, i.e. ~100 us for the 4096 groups of a 2^28-element
 // tensor whose aggregates all appear at once.  A segment with a group beyond
 // the records (many equal keys) is left to the look-back.
-__global__ void __launch_bounds__(kThreads) dgc_scan_kernel(const SegH1* __restrict__ segs) {
+// exclusive scan of (a, t) over the NT threads of a CTA in thread order; sh
+// needs 2 x 33 words
+template <int NT>
+__device__ __forceinline__ uint2 scan_excl2(uint32_t a, uint32_t t, uint32_t* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t xa = a, xt = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t ya = __shfl_up_sync(0xffffffffu, xa, o), yt = __shfl_up_sync(0xffffffffu, xt, o);
+    if (lane >= o) {
+      xa += ya;
+      xt += yt;
+    }
+  }
+  if (lane == 31) {
+    sh[warp] = xa;
+    sh[33 + warp] = xt;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t wa = lane < NT / 32 ? sh[lane] : 0u, wt = lane < NT / 32 ? sh[33 + lane] : 0u;
+    uint32_t sa = wa, st = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ya = __shfl_up_sync(0xffffffffu, sa, o), yt = __shfl_up_sync(0xffffffffu, st, o);
+      if (lane >= o) {
+        sa += ya;
+        st += yt;
+      }
+    }
+    sh[lane] = sa - wa;
+    sh[33 + lane] = st - wt;
+  }
+  __syncthreads();
+  return make_uint2(xa - a + sh[warp], xt - t + sh[33 + warp]);
+}
+
+// One CTA of NT threads per segment (1024 for segments of thousands of groups,
+// else 256); each thread a contiguous run of groups whose 16-byte records
+// (count, #above, #inside, packed low bits) are loaded kScanB at a time, all in
+// flight together (a 2^28-element tensor at 1%: 4096 groups, one batch per
+// thread).
+template <int NT>
+__global__ void __launch_bounds__(NT) dgc_scan_kernel(const SegH1* __restrict__ segs) {
   pdl_wait();     // predecessors in the stream are complete (PDL)
   pdl_trigger();
-  __shared__ uint32_t sh[16];
-  __shared__ int sh_bad;
+  constexpr int kScanB = 8;
+  __shared__ uint32_t sh[66];
   const SegH1& S = segs[blockIdx.x];
   const uint32_t G = S.ngroups;
   if (G == 0) return;
-  if (threadIdx.x == 0) sh_bad = 0;
-  __syncthreads();
   const uint32_t T = __ldcg(&S.st->prefix), b3 = T & 1023u;
-  const uint32_t per = (G + kThreads - 1) / kThreads;
+  const uint32_t per = (G + NT - 1) / NT;
   const uint32_t g0 = min(G, threadIdx.x * per), g1 = min(G, g0 + per);
+  const uint32_t rpg = S.rpg;
+  auto rec_of = [&](uint32_t g) { return __ldcg(reinterpret_cast<const uint4*>(S.runcnt + (size_t)g * rpg)); };
   uint32_t ta = 0, tt = 0;
   bool bad = false;
-  for (uint32_t g = g0; g < g1; ++g) {
-    const uint32_t* rec = S.runcnt + (size_t)g * S.rpg;
-    const uint32_t r_in = __ldcg(rec + 2), pk = __ldcg(rec + 3);
-    ta += __ldcg(rec + 1);
-    bad |= r_in > 3;
-    for (uint32_t i = 0; i < min(r_in, 3u); ++i) {
-      const uint32_t low = (pk >> (10 * i)) & 1023u;
-      ta += low > b3;
-      tt += low == b3;
+  for (uint32_t gb = g0; gb < g1; gb += kScanB) {
+    uint4 rec[kScanB];
+#pragma unroll
+    for (int j = 0; j < kScanB; ++j) rec[j] = gb + j < g1 ? rec_of(gb + j) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < kScanB; ++j) {
+      ta += rec[j].y;
+      bad |= rec[j].z > 3;
+#pragma unroll
+      for (uint32_t i = 0; i < 3; ++i) {
+        const uint32_t low = (rec[j].w >> (10 * i)) & 1023u;
+        const bool in = i < rec[j].z;
+        ta += in && low > b3;
+        tt += in && low == b3;
+      }
     }
   }
-  if (bad) sh_bad = 1;
-  uint32_t tot;
-  uint32_t ea = block_excl_scan<0>(ta, &tot, sh);
-  uint32_t et = block_excl_scan<0>(tt, &tot, sh);   // (also orders sh_bad)
-  if (sh_bad) return;   // CTA-uniform
+  if (__syncthreads_or(bad)) return;   // CTA-uniform: the write kernel's look-back takes the segment
+  const uint2 ex = scan_excl2<NT>(ta, tt, sh);
+  uint32_t ea = ex.x, et = ex.y;
   unsigned long long* lb = reinterpret_cast<unsigned long long*>(S.gcnt);
-  for (uint32_t g = g0; g < g1; ++g) {
-    lb[g] = lb_pack(3, ea, et);
-    const uint32_t* rec = S.runcnt + (size_t)g * S.rpg;
-    const uint32_t r_in = __ldcg(rec + 2), pk = __ldcg(rec + 3);
-    ea += __ldcg(rec + 1);
-    for (uint32_t i = 0; i < r_in; ++i) {
-      const uint32_t low = (pk >> (10 * i)) & 1023u;
-      ea += low > b3;
-      et += low == b3;
+  for (uint32_t gb = g0; gb < g1; gb += kScanB) {
+    uint4 rec[kScanB];
+#pragma unroll
+    for (int j = 0; j < kScanB; ++j) rec[j] = gb + j < g1 ? rec_of(gb + j) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < kScanB; ++j) {
+      if (gb + j >= g1) break;
+      lb[gb + j] = lb_pack(3, ea, et);
+      ea += rec[j].y;
+#pragma unroll
+      for (uint32_t i = 0; i < 3; ++i) {
+        const uint32_t low = (rec[j].w >> (10 * i)) & 1023u;
+        const bool in = i < rec[j].z;
+        ea += in && low > b3;
+        et += in && low == b3;
+      }
     }
   }
 }
@@ -1884,7 +1938,10 @@ void launch_dgc_finalize(const SegH1* segs, int nsegs, const uint32_t* group_seg
       launch_pdl(dgc_refine_kernel<3, true>, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
     }
     debug_sync("dgc_refine<3>", st);
-    launch_pdl(dgc_scan_kernel, nsegs, kThreads, 0, st, segs);
+    if (ngroups > 2048 * nsegs)
+      launch_pdl(dgc_scan_kernel<1024>, nsegs, 1024, 0, st, segs);
+    else
+      launch_pdl(dgc_scan_kernel<256>, nsegs, 256, 0, st, segs);
     launch_pdl(dgc_write_kernel, wgrid, kThreads, 0, st, segs, group_seg, (uint32_t)ngroups);
     debug_sync("dgc_write", st);
   }
