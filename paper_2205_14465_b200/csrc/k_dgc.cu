@@ -1409,19 +1409,20 @@ __global__ void __launch_bounds__(kThreads) dgc_small_kernel(const SegH1* __rest
 // segment's zeroed-every-call counters:
 //   load    acc = g + r (u = m u + g first with momentum, R20) into shared
 //           memory + the slice's 2048-bin histogram of the top 11 key bits
-//   round 1 (barrier) bin of the k-th key from the summed histogram; one pass
-//           lists the offsets of every key above that bin and of its members,
-//           whose next 10 key bits are histogrammed
-//   round 2 (barrier) next bin; round 3 over the members only
-//   count   (barrier) T known: selected / tie bitmaps from the lists, every
-//           CTA's (#above T, #ties) -> the selected in the CTAs before it and
-//           the ties it may take (ascending index); a bitmap prefix gives each
-//           selected entry its place in the index-sorted payload; then
-//           r := acc with 0 where selected (a float4 pass) and u := 0 there.
-// No sampled threshold and no candidate list in HBM: the exact k-th key T and
-// the (key desc, idx asc) selection are the same as the chain's (reading R3).
-constexpr uint32_t kMidTpcMax = 8;
-constexpr uint32_t kMidSmem = kMidTpcMax * kDgcTile * 6;   // acc (4 B) + member list (2 B) per element
+//   round 1 (barrier) bin of the k-th key from the summed histogram; a pass
+//           histograms the next 10 bits of that bin's keys
+//   round 2 (barrier) next bin; a pass histograms the low 10 bits of its keys
+//   round 3 (barrier) T = the exact k-th key; warp ballots give the bitmaps
+//           key > T and key == T (1 bit per element)
+//   count   (barrier) every CTA's (#above T, #ties) -> the selected in the CTAs
+//           before it and the ties it may take (ascending index); a CTA scan
+//           of the bitmap words places each selected element in the
+//           index-sorted payload; then r := acc with 0 where selected (a
+//           float4 pass) and u := 0 there.
+// No sampled threshold and no candidate list: the exact k-th key T and the
+// (key desc, idx asc) selection are the same as the chain's (reading R3).
+constexpr uint32_t kMidTpcMax = 12;   // 192 KB of acc (the bitmaps of 12 tiles fill the 3072 histogram words)
+constexpr uint32_t kMidSmem = kMidTpcMax * kDgcTile * 4;
 
 __device__ __forceinline__ void seg_barrier(uint32_t* ctr, uint32_t expected) {
   __syncthreads();
@@ -1491,12 +1492,11 @@ __global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __
                                                                  uint32_t tpc) {
   extern __shared__ float4 mid_smem4[];
   float* acc = reinterpret_cast<float*>(mid_smem4);
-  uint16_t* list = reinterpret_cast<uint16_t*>(acc + tpc * kDgcTile);
-  __shared__ uint32_t hist1[2048];
-  __shared__ uint32_t hist2[1024];
+  __shared__ uint32_t hist12[3072];   // round 1 (2048 bins) + rounds 2 / 3 (1024); then the bitmaps
+  uint32_t* hist1 = hist12;
+  uint32_t* hist2 = hist12 + 2048;
   __shared__ uint32_t sh[288];
-  __shared__ uint32_t wcnt[2 * kMidWarps];   // [0]: member count; then per warp: members above T, ties
-  __shared__ uint32_t info[6];   // segment, CTA index in it, CTAs of it, list length, select result (2)
+  __shared__ uint32_t info[6];   // segment, CTA index in it, CTAs of it, (unused), select result (2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // CTA -> (segment, index) from the static table (before pdl_wait)
   if (tid < kThreads) {
@@ -1511,8 +1511,6 @@ __global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __
   }
   for (int b = tid; b < 2048; b += kMidThreads) hist1[b] = 0;
   for (int b = tid; b < 1024; b += kMidThreads) hist2[b] = 0;
-  if (tid < 2 * kMidWarps) wcnt[tid] = 0;
-  if (tid == 0) info[3] = 0;
   __syncthreads();
   const SegH1& S = segs[info[0]];
   const uint32_t ci = info[1], nc = info[2];
@@ -1600,43 +1598,23 @@ __global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __
   for (int b = tid; b < 2048; b += kMidThreads)
     if (hist1[b]) atomicAdd(S.hist + b, hist1[b]);
   seg_barrier(&S.st->done, nc);
-  // hist1 becomes the selection bitmaps (1 bit per element of the slice)
-  uint32_t* selbits = hist1;           // [len / 32]: selected
-  uint32_t* tiebits = hist1 + 1024;    // [len / 32]: key == T
+  // after round 3 the histogram words hold the bitmaps, 1 bit per element of
+  // the slice (<= 12 tiles: 1536 words each)
+  uint32_t* selbits = hist12;          // key > T (then: selected)
+  uint32_t* tiebits = hist12 + 1536;   // key == T
   uint2 sel = mid_select(S.hist, 2048, k, sh, info + 4);   // (its __syncthreads orders the flush reads)
   const uint32_t bin1 = sel.x;
   uint32_t need = k - sel.y;
-  for (int b = tid; b < 2048; b += kMidThreads) hist1[b] = 0;
-  // ---- round 2: one pass over the slice, a float4 per lane.  The list gets
-  // the offsets of every key above bin 1 (from the front) and of bin 1's
-  // members (from the back; their next 10 key bits histogrammed): every key
-  // >= T is in it, and both sets together are at most the slice
-  const uint32_t cap = tpc * kDgcTile;
+  // ---- round 2: the next 10 key bits of round 1's bin (a float4 per thread)
   for (uint32_t i = 4 * tid; i < len; i += 4 * kMidThreads) {
     const float4 a4 = lds4(acc + i);   // (beyond len: stale shared memory, masked below)
-    uint32_t top[4];
-    bool hit = false;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      top[c] = fkey(f4get(a4, c)) >> 20;
-      hit |= i + c < len && top[c] >= bin1;
-    }
-    if (hit) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (i + c >= len) {
-        } else if (top[c] > bin1) {
-          list[atomicAdd(&info[3], 1u)] = (uint16_t)(i + c);
-        } else if (top[c] == bin1) {
-          list[cap - 1 - atomicAdd(&wcnt[0], 1u)] = (uint16_t)(i + c);
-          atomicAdd(&hist2[(fkey(f4get(a4, c)) >> 10) & 1023], 1u);
-        }
-      }
+      const uint32_t key = fkey(f4get(a4, c));
+      if (i + c < len && (key >> 20) == bin1) atomicAdd(&hist2[(key >> 10) & 1023], 1u);
     }
   }
   __syncthreads();
-  const uint32_t nabove = info[3], nmem = wcnt[0];
-  const uint16_t* mlist = list + cap - nmem;   // bin 1's members
   uint32_t* gh2 = S.hist + 4096;
   uint32_t* gh3 = S.hist + 4096 + 1024 * S.hrep;
   for (int b = tid; b < 1024; b += kMidThreads) {
@@ -1647,10 +1625,14 @@ __global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __
   sel = mid_select(gh2, 1024, need, sh, info + 4);
   const uint32_t prefix2 = (bin1 << 10) | sel.x;
   need -= sel.y;
-  // ---- round 3 over the members
-  for (uint32_t j = tid; j < nmem; j += kMidThreads) {
-    const uint32_t key = fkey(acc[mlist[j]]);
-    if ((key >> 10) == prefix2) atomicAdd(&hist2[key & 1023], 1u);
+  // ---- round 3: the low 10 bits of the keys in round 2's bin
+  for (uint32_t i = 4 * tid; i < len; i += 4 * kMidThreads) {
+    const float4 a4 = lds4(acc + i);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint32_t key = fkey(f4get(a4, c));
+      if (i + c < len && (key >> 10) == prefix2) atomicAdd(&hist2[key & 1023], 1u);
+    }
   }
   __syncthreads();
   for (int b = tid; b < 1024; b += kMidThreads)
@@ -1659,38 +1641,31 @@ __global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __
   sel = mid_select(gh3, 1024, need, sh, info + 4);
   const uint32_t T = (prefix2 << 10) | sel.x;
   need -= sel.y;   // the ties at T to take, by ascending index
-  // ---- count: above T = every key above bin 1 + members above T; ties
-  for (uint32_t j = tid; j < nabove; j += kMidThreads) {
-    const uint32_t o = list[j];
-    atomicOr(&selbits[o >> 5], 1u << (o & 31));
-  }
-  uint32_t ma = 0, mt = 0;
-  for (uint32_t j = tid; j < nmem; j += kMidThreads) {
-    const uint32_t o = mlist[j];
-    const uint32_t key = fkey(acc[o]);
-    if (key > T) {
-      atomicOr(&selbits[o >> 5], 1u << (o & 31));
-      ++ma;
-    } else if (key == T) {
-      atomicOr(&tiebits[o >> 5], 1u << (o & 31));
-      ++mt;
+  // ---- bitmaps by warp ballots over 32 consecutive elements: key > T, key == T
+  const uint32_t nwords = (len + 31) / 32;
+  for (uint32_t w = warp; w < nwords; w += kMidWarps) {
+    const uint32_t i = w * 32 + lane;
+    const uint32_t key = i < len ? fkey(acc[i]) : 0u;
+    const unsigned ma = __ballot_sync(0xffffffffu, i < len && key > T);
+    const unsigned mt = __ballot_sync(0xffffffffu, i < len && key == T);
+    if (lane == 0) {
+      selbits[w] = ma;
+      tiebits[w] = mt;
     }
   }
-  ma = __reduce_add_sync(0xffffffffu, ma);
-  mt = __reduce_add_sync(0xffffffffu, mt);
-  if (lane == 0) {
-    wcnt[warp] = ma;
-    wcnt[kMidWarps + warp] = mt;
-  }
   __syncthreads();
-  uint2* slots = S.cand;   // per CTA: (#above T, #ties) (the chain's candidate buffer)
-  uint32_t ctie = 0;   // this CTA's ties (every thread)
-#pragma unroll 8
-  for (int w = 0; w < kMidWarps; ++w) ctie += wcnt[kMidWarps + w];
-  if (warp == 0) {
-    const uint32_t ta = nabove + __reduce_add_sync(0xffffffffu, wcnt[lane]);
-    if (lane == 0) __stcg(reinterpret_cast<unsigned long long*>(slots + ci), ((unsigned long long)ctie << 32) | ta);
+  // thread t owns words 2t and 2t + 1 (elements 64t .. 64t + 63) from here on
+  const uint32_t w0 = 2 * tid;
+  uint32_t s0 = w0 < nwords ? selbits[w0] : 0u, s1 = w0 + 1 < nwords ? selbits[w0 + 1] : 0u;
+  const uint32_t t0 = w0 < nwords ? tiebits[w0] : 0u, t1 = w0 + 1 < nwords ? tiebits[w0 + 1] : 0u;
+  // ---- count: (#above T, #ties) of this CTA, published; the CTAs before it
+  uint32_t ca = __popc(s0) + __popc(s1), ct = __popc(t0) + __popc(t1);
+  const uint2 ex = scan_excl2<kMidThreads>(ca, ct, sh);   // within the CTA, in element order
+  if (tid == kMidThreads - 1) {
+    const uint32_t ta = ex.x + ca, tt = ex.y + ct;
+    __stcg(reinterpret_cast<unsigned long long*>(S.cand + ci), ((unsigned long long)tt << 32) | ta);
   }
+  uint2* slots = S.cand;   // per CTA: (#above T, #ties) (the chain's candidate buffer)
   seg_barrier(&S.st->done_cnt, nc);
   if (warp == 0) {
     uint32_t ba = 0, bt = 0;
@@ -1702,53 +1677,49 @@ __global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __
     ba = __reduce_add_sync(0xffffffffu, ba);
     bt = __reduce_add_sync(0xffffffffu, bt);
     if (lane == 0) {
-      info[4] = ba + min(bt, need);   // selected in the CTAs before this one
-      info[5] = bt;                   // ties in the CTAs before this one
+      info[4] = ba;
+      info[5] = bt;
     }
   }
   __syncthreads();
-  const uint32_t cbase = info[4], tbase = info[5];
-  const uint32_t nwords = (len + 31) / 32;
-  // ties by ascending index: rank = ties before it in this CTA (bitmap prefix)
-  if (tbase < need && ctie != 0) {   // this CTA may take ties
-    const uint32_t w = tid < (int)nwords ? tiebits[tid] : 0u;
-    uint32_t tot;
-    const uint32_t ex = mid_excl_scan(__popc(w), &tot, sh);
-    hist2[tid] = ex;   // (1024 words: one per thread)
-    __syncthreads();
-    {
-      for (uint32_t j = tid; j < nmem; j += kMidThreads) {
-        const uint32_t o = mlist[j];
-        const uint32_t tw = tiebits[o >> 5];
-        if (tw & (1u << (o & 31))) {
-          const uint32_t rank = hist2[o >> 5] + __popc(tw & ((1u << (o & 31)) - 1u));
-          if (tbase + rank < need) atomicOr(&selbits[o >> 5], 1u << (o & 31));
-        }
+  const uint32_t cabove = info[4], ctie = info[5];
+  // ties by ascending index: a tie with tbase ties before it is taken iff tbase < need
+  {
+    uint32_t tb = ctie + ex.y;
+    for (int h = 0; h < 2; ++h) {
+      uint32_t tw = h ? t1 : t0;
+      while (tw) {
+        const uint32_t bit = __ffs(tw) - 1;
+        tw &= tw - 1;
+        if (tb < need) (h ? s1 : s0) |= 1u << bit;
+        ++tb;
       }
     }
-    __syncthreads();
   }
-  // selected-before prefix per bitmap word
-  {
-    const uint32_t w = tid < (int)nwords ? selbits[tid] : 0u;
-    uint32_t tot;
-    hist2[tid] = mid_excl_scan(__popc(w), &tot, sh);
-    __syncthreads();
-  }
-  // ---- ordered write: idx / val of the selected (from the list), u := 0 there
+  // selected before this pair: above in the CTAs before + the ties they took +
+  // this CTA's selected before the pair (scan of the final words)
+  const uint2 ex2 = scan_excl2<kMidThreads>(__popc(s0) + __popc(s1), 0u, sh);
+  const uint32_t cbase = cabove + min(ctie, need) + ex2.x;
+  if (w0 < nwords) selbits[w0] = s0;
+  if (w0 + 1 < nwords) selbits[w0 + 1] = s1;
+  // ---- ordered write: idx / val of the selected, u := 0 there
   uint32_t* out_idx = reinterpret_cast<uint32_t*>(S.chunk);
   float* out_val = reinterpret_cast<float*>(S.chunk + 4 * (size_t)S.kpad);
-  auto emit = [&](uint32_t o) {
-    const uint32_t sw = selbits[o >> 5];
-    if (sw & (1u << (o & 31))) {
-      const uint32_t pos = cbase + hist2[o >> 5] + __popc(sw & ((1u << (o & 31)) - 1u));
-      out_idx[pos] = lo + o;
-      out_val[pos] = acc[o];
-      if (u) u[o] = 0.0f;   // momentum factor masking (R20)
+  {
+    uint32_t pos = cbase;
+    for (int h = 0; h < 2; ++h) {
+      uint32_t sw = h ? s1 : s0;
+      while (sw) {
+        const uint32_t e = (w0 + h) * 32 + __ffs(sw) - 1;
+        sw &= sw - 1;
+        out_idx[pos] = lo + e;
+        out_val[pos] = acc[e];
+        if (u) u[e] = 0.0f;   // momentum factor masking (R20)
+        ++pos;
+      }
     }
-  };
-  for (uint32_t j = tid; j < nabove; j += kMidThreads) emit(list[j]);
-  for (uint32_t j = tid; j < nmem; j += kMidThreads) emit(mlist[j]);
+  }
+  __syncthreads();   // the final selbits
   // ---- r := acc, 0 where selected (a float4 per thread and step)
   if (ef) {
     const bool rvec = al16(r);
@@ -1804,7 +1775,7 @@ void launch_dgc_mid(const SegH1* segs, int nsegs, uint32_t tpc, int grid, cudaSt
       cudaFuncSetAttribute(dgc_mid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMidSmem) ==
       cudaSuccess;
   (void)attr_set;
-  launch_pdl(dgc_mid_kernel, grid, kMidThreads, (size_t)tpc * kDgcTile * 6, st, segs, nsegs, tpc);
+  launch_pdl(dgc_mid_kernel, grid, kMidThreads, (size_t)tpc * kDgcTile * 4, st, segs, nsegs, tpc);
   count_launches(1);
 }
 

@@ -627,12 +627,12 @@ def test_onchip_many_segments(path, monkeypatch):
 
 @pytest.mark.parametrize("fits", [True, False])
 def test_onchip_capacity_edge(fits):
-    """The largest bucket the on-chip kernel takes (#SMs CTAs of 8 tiles) and
+    """The largest bucket the on-chip kernel takes (#SMs CTAs of 12 tiles) and
     one tile more (the chain): both bit-exact; the first is one h1 launch."""
     E = esp()
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     n = 2
-    N = (sms // n) * 8 * 4096 - 1000 + (0 if fits else 4096)
+    N = (sms // n) * 12 * 4096 - 1000 + (0 if fits else 4096)
     w = E.World.sim(n, 0)
     try:
         ctx = E.Ctx(w, "dgc", "allgather", N, tensor_id=22, ratio=0.01)
