@@ -641,12 +641,12 @@ def main():
                     "ms_per_step": e2e_ms, "pipeline": f"{E2E_CHUNKS} tensor groups, H2D / sync / D2H overlapped"},
             "gpu_launches": launches,
             "clocks": clk,
-            **({"phases_ms_serialised": phases} if phases else {}),
+            **({"phases_ms_serialised": phases} if phases and phases.get("total_ms") else {}),
             # a9: the same step with its phases serialised (events
             # around each) minus the pipelined step = the time the overlap of
             # h1(b+1) / finalize chains with the collective of bucket b hides
             **({"pipelining": {"serialised_ms": phases["total_ms"], "pipelined_ms": t_mean,
-                               "hidden_ms": phases["total_ms"] - t_mean}} if phases else {}),
+                               "hidden_ms": phases["total_ms"] - t_mean}} if phases and phases.get("total_ms") else {}),
             **({"link": link} if link else {}),
         }
         if not args.no_latency:
