@@ -1473,12 +1473,14 @@ __device__ __forceinline__ uint32_t mid_excl_scan(uint32_t v, uint32_t* total, u
 }
 
 // CTA-wide radix bin choice by the first 256 threads (select_bin on named
-// barrier 1), broadcast through shared memory
+// barrier 1), broadcast through shared memory; GLOBAL: the segment's summed
+// histogram in global memory, else this CTA's own (a one-CTA segment)
+template <bool GLOBAL = true>
 __device__ __forceinline__ uint2 mid_select(const uint32_t* gh, int nbins, uint32_t need, uint32_t* sh,
                                             uint32_t* res) {
   if (threadIdx.x < kThreads) {
     uint32_t b, a;
-    select_bin<1, true>(gh, nbins, need, &b, &a, sh);
+    select_bin<1, GLOBAL>(gh, nbins, need, &b, &a, sh);
     if (threadIdx.x == 0) {
       res[0] = b;
       res[1] = a;
@@ -1595,14 +1597,19 @@ __global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __
     }
   }
   __syncthreads();
-  for (int b = tid; b < 2048; b += kMidThreads)
-    if (hist1[b]) atomicAdd(S.hist + b, hist1[b]);
-  seg_barrier(&S.st->done, nc);
+  // a one-CTA segment selects from its own shared histograms: no flush, no barrier
+  const bool solo = nc == 1;
+  if (!solo) {
+    for (int b = tid; b < 2048; b += kMidThreads)
+      if (hist1[b]) atomicAdd(S.hist + b, hist1[b]);
+    seg_barrier(&S.st->done, nc);
+  }
   // after round 3 the histogram words hold the bitmaps, 1 bit per element of
   // the slice (<= 12 tiles: 1536 words each)
   uint32_t* selbits = hist12;          // key > T (then: selected)
   uint32_t* tiebits = hist12 + 1536;   // key == T
-  uint2 sel = mid_select(S.hist, 2048, k, sh, info + 4);   // (its __syncthreads orders the flush reads)
+  uint2 sel = solo ? mid_select<false>(hist1, 2048, k, sh, info + 4)
+                   : mid_select(S.hist, 2048, k, sh, info + 4);   // (its __syncthreads orders the flush reads)
   const uint32_t bin1 = sel.x;
   uint32_t need = k - sel.y;
   // ---- round 2: the next 10 key bits of round 1's bin (a float4 per thread)
@@ -1617,12 +1624,18 @@ __global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __
   __syncthreads();
   uint32_t* gh2 = S.hist + 4096;
   uint32_t* gh3 = S.hist + 4096 + 1024 * S.hrep;
-  for (int b = tid; b < 1024; b += kMidThreads) {
-    if (hist2[b]) atomicAdd(gh2 + b, hist2[b]);
-    hist2[b] = 0;   // reused by round 3 (the barrier below orders it)
+  if (solo) {
+    sel = mid_select<false>(hist2, 1024, need, sh, info + 4);
+    for (int b = tid; b < 1024; b += kMidThreads) hist2[b] = 0;   // reused by round 3
+    __syncthreads();
+  } else {
+    for (int b = tid; b < 1024; b += kMidThreads) {
+      if (hist2[b]) atomicAdd(gh2 + b, hist2[b]);
+      hist2[b] = 0;   // reused by round 3 (the barrier below orders it)
+    }
+    seg_barrier(&S.st->done_r2, nc);
+    sel = mid_select(gh2, 1024, need, sh, info + 4);
   }
-  seg_barrier(&S.st->done_r2, nc);
-  sel = mid_select(gh2, 1024, need, sh, info + 4);
   const uint32_t prefix2 = (bin1 << 10) | sel.x;
   need -= sel.y;
   // ---- round 3: the low 10 bits of the keys in round 2's bin
@@ -1635,10 +1648,14 @@ __global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __
     }
   }
   __syncthreads();
-  for (int b = tid; b < 1024; b += kMidThreads)
-    if (hist2[b]) atomicAdd(gh3 + b, hist2[b]);
-  seg_barrier(&S.st->done_r3, nc);
-  sel = mid_select(gh3, 1024, need, sh, info + 4);
+  if (solo) {
+    sel = mid_select<false>(hist2, 1024, need, sh, info + 4);
+  } else {
+    for (int b = tid; b < 1024; b += kMidThreads)
+      if (hist2[b]) atomicAdd(gh3 + b, hist2[b]);
+    seg_barrier(&S.st->done_r3, nc);
+    sel = mid_select(gh3, 1024, need, sh, info + 4);
+  }
   const uint32_t T = (prefix2 << 10) | sel.x;
   need -= sel.y;   // the ties at T to take, by ascending index
   // ---- bitmaps by warp ballots over 32 consecutive elements: key > T, key == T
@@ -1661,12 +1678,14 @@ __global__ void __launch_bounds__(kMidThreads, 1) dgc_mid_kernel(const SegH1* __
   // ---- count: (#above T, #ties) of this CTA, published; the CTAs before it
   uint32_t ca = __popc(s0) + __popc(s1), ct = __popc(t0) + __popc(t1);
   const uint2 ex = scan_excl2<kMidThreads>(ca, ct, sh);   // within the CTA, in element order
-  if (tid == kMidThreads - 1) {
-    const uint32_t ta = ex.x + ca, tt = ex.y + ct;
-    __stcg(reinterpret_cast<unsigned long long*>(S.cand + ci), ((unsigned long long)tt << 32) | ta);
-  }
   uint2* slots = S.cand;   // per CTA: (#above T, #ties) (the chain's candidate buffer)
-  seg_barrier(&S.st->done_cnt, nc);
+  if (!solo) {
+    if (tid == kMidThreads - 1) {
+      const uint32_t ta = ex.x + ca, tt = ex.y + ct;
+      __stcg(reinterpret_cast<unsigned long long*>(slots + ci), ((unsigned long long)tt << 32) | ta);
+    }
+    seg_barrier(&S.st->done_cnt, nc);
+  }
   if (warp == 0) {
     uint32_t ba = 0, bt = 0;
     for (uint32_t j = lane; j < ci; j += 32) {

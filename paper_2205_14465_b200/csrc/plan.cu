@@ -520,22 +520,29 @@ static void build_bucket(Layout& L, Bucket& b, HostTables& T, size_t zero_off_st
   b.nh1 = (int)(T.h1.size() - h1_first);
   b.h1_max_len = 0;
   for (int i = 0; i < b.nh1; ++i) b.h1_max_len = std::max(b.h1_max_len, T.h1[h1_first + i].n);
+  // (segments of <= 1024 elements: dgc_small_kernel, one 256-thread CTA each;
+  // up to 4096 the on-chip kernel's one-CTA path is faster when it fits)
   b.small = dgc && b.h1_max_len <= (uint32_t)kSample;
   // one-kernel h1 when the bucket fits the chip's shared memory: the smallest
   // tiles-per-CTA that gives every segment's CTAs a resident slot (grid <= #SMs);
   // the approximate-count mode keeps the chain (its result depends on the sample)
   b.onchip = false;
-  if (dgc && !b.small && dgc_mid_enabled()) {
+  if (dgc && (!b.small || b.h1_max_len > 1024) && dgc_mid_enabled()) {
     bool ok = true;
     for (int i = 0; i < b.nh1; ++i) ok = ok && !T.h1[h1_first + i].approx;
     int sms = 0, dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
       sms = 0;
-    for (uint32_t tpc = 1; ok && tpc <= dgc_mid_tpc_max(); ++tpc) {
+    // segments of up to 4 tiles stay in one CTA (no global barriers: their
+    // passes are shorter than a barrier round trip), larger ones spread out
+    uint32_t max_tiles = 1;
+    for (int i = 0; i < b.nh1; ++i) max_tiles = std::max(max_tiles, T.h1[h1_first + i].nunits);
+    for (uint32_t tpc = std::min<uint32_t>(max_tiles, 4); ok && tpc <= dgc_mid_tpc_max(); ++tpc) {
       uint64_t ctas = 0;
       for (int i = 0; i < b.nh1; ++i) ctas += div_up(T.h1[h1_first + i].nunits, tpc);
       if (ctas <= (uint64_t)sms) {
+        b.small = false;
         b.onchip = true;
         b.onchip_tpc = tpc;
         b.onchip_grid = (int)ctas;
