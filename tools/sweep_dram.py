@@ -63,7 +63,7 @@ def summary(path):
             launches[key] = {"name": r[ki]}
             order.append(key)
         v = float(r[vi].replace(",", ""))
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(r[ui], 1)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1)
         launches[key][r[mi]] = v * scale
     groups, cur = [], None
     for key in order:
@@ -83,7 +83,7 @@ def summary(path):
             tot_t += t
             tot_b += rd + wr
             print(f"{kind + ' 2^' + str(ex) + ' B':<18}{L['name'][:43]:<44}{t:>9.1f}{rd:>12.2f}{wr:>12.2f}")
-        print(f"{'':<18}{'total':<44}{tot_t:>9.1f}{'':>12}{tot_b:>12.2f}  ({tot_b * 1e6 / max(tot_t, 1e-9) / 1e9:.2f} TB/s DRAM)")
+        print(f"{'':<18}{'total':<44}{tot_t:>9.1f}{'':>12}{tot_b:>12.2f}  ({tot_b / max(tot_t, 1e-9):.2f} TB/s DRAM)")
 
 
 if __name__ == "__main__":
