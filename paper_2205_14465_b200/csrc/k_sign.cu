@@ -125,13 +125,25 @@ struct SignOp {
       // gathered per piece (measured faster than the byte-group transpose at n = 1)
       const float* lut = &gh.wscr[0][0];
       const uint32_t lt = (base & (kDgcTile - 1)) + lane * 4;
+      if (S.npieces == 1) {
+        // one piece (n = 1, and every n = 1 a7): the table's two entries in
+        // registers, a select per element instead of a shared-memory lookup
+        const float L0 = lut[0], L1 = lut[1];
 #pragma unroll
-      for (int j = 0; j < kNJ; ++j) {
-        const uint32_t l = lt + j * 128;
-        uint32_t idx4 = 0;
-        for (uint32_t q = 0; q < S.npieces; ++q)
-          idx4 |= spread4((sw[q * (kDgcTile / 32) + (l >> 5)] >> (l & 31)) & 0xFu) << q;
-        xv[j] = make_float4(lut[idx4 & 0xFFu], lut[(idx4 >> 8) & 0xFFu], lut[(idx4 >> 16) & 0xFFu], lut[idx4 >> 24]);
+        for (int j = 0; j < kNJ; ++j) {
+          const uint32_t l = lt + j * 128;
+          const uint32_t nib = (sw[l >> 5] >> (l & 31)) & 0xFu;
+          xv[j] = make_float4((nib & 1u) ? L1 : L0, (nib & 2u) ? L1 : L0, (nib & 4u) ? L1 : L0, (nib & 8u) ? L1 : L0);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kNJ; ++j) {
+          const uint32_t l = lt + j * 128;
+          uint32_t idx4 = 0;
+          for (uint32_t q = 0; q < S.npieces; ++q)
+            idx4 |= spread4((sw[q * (kDgcTile / 32) + (l >> 5)] >> (l & 31)) & 0xFu) << q;
+          xv[j] = make_float4(lut[idx4 & 0xFFu], lut[(idx4 >> 8) & 0xFFu], lut[(idx4 >> 16) & 0xFFu], lut[idx4 >> 24]);
+        }
       }
     } else if (DECODE == 2 && sw && S.npieces <= (uint32_t)kSignLutPieces) {
       // staged words, few pieces: the decoded mean by table lookup (identical
